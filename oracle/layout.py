@@ -1,0 +1,291 @@
+"""Oracle metadata: tilings, block maps, packed layout, task list, owner partition.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain Python loops, written from the paper:
+
+* IndexSpace / TiledIndexSpace -- PAPER §3.1 P111, P116-127 (Fig. 2): an index range, tiled either
+  with a fixed size (``tN{N,10}``, remainder in the last tile, reading R5) or custom sizes with full
+  coverage (``tM{M,{10,20}}``).  Spin ranges (P138) split the tiling: a tile never straddles a spin
+  boundary (S39, reading R6).
+* Tensor blocks -- "indexed by the Cartesian product of the number of tiles on each dimension"
+  (P111, P140), row-major block grid, row-major elements within a block (reading R9).
+* Non-zero block map -- explicit, or the spin rule sum(spin of upper dims) == sum(spin of lower dims)
+  over a per-tensor (upper, lower) position split (P138, reading R7).
+* Packed storage -- only non-zero blocks are allocated (P210, third scheme); row-major block order,
+  each block start rounded up to a multiple of 2 doubles (16 B) (reading R10).
+* Default owners -- "allocates the tensor blocks in a round-robin fashion while taking block
+  sparsity into account" (P210): owner = (ordinal among non-zero blocks) mod nranks.
+* Task list -- for each non-zero C block (row-major), each contracted-tile tuple (row-major,
+  contracted labels in order of first appearance in A): a task iff the A and B blocks are both
+  non-zero (P111, P138, P210, P543; readings R8, R11).  Brute force over the full grid.
+* LPT owner partition (reading R3-part): C blocks sorted by (cost desc, block id asc), each to the
+  least-loaded rank, ties to the lowest rank.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from itertools import product
+from typing import List, Optional, Sequence, Tuple
+
+
+class OracleError(ValueError):
+    pass
+
+
+@dataclass
+class IndexSpace:
+    """P116-122: ``IndexSpace N{range(100)}``; ``ranges`` = [(begin, end, spin)] covering [0, extent)."""
+    extent: int
+    ranges: List[Tuple[int, int, int]] = field(default_factory=list)
+
+    def __post_init__(self):
+        if self.extent < 0:
+            raise OracleError("negative extent")
+        if self.ranges:
+            pos = 0
+            for b, e, s in self.ranges:
+                if b != pos or e <= b:
+                    raise OracleError("ranges must be ascending, non-empty and cover the space")
+                pos = e
+            if pos != self.extent:
+                raise OracleError("ranges must cover the space")
+
+    def segments(self):
+        if self.ranges:
+            return list(self.ranges)
+        return [(0, self.extent, 0)] if self.extent > 0 else []
+
+
+@dataclass
+class TiledIndexSpace:
+    space: IndexSpace
+    offsets: List[int]        # ntiles + 1 split points
+    tile_spin: List[int]      # spin of each tile (0 = no spin)
+
+    @property
+    def ntiles(self) -> int:
+        return len(self.offsets) - 1
+
+    def size(self, t: int) -> int:
+        return self.offsets[t + 1] - self.offsets[t]
+
+
+def tile_fixed(space: IndexSpace, tile: int) -> TiledIndexSpace:
+    """P125 ``TiledIndexSpace tN{N, 10}``; remainder in the last tile of each spin range (R5, R6)."""
+    if tile < 1:
+        raise OracleError("tile < 1")
+    offs, spins = [0], []
+    for b, e, s in space.segments():
+        p = b
+        while p < e:
+            q = min(p + tile, e)
+            offs.append(q)
+            spins.append(s)
+            p = q
+    return TiledIndexSpace(space, offs, spins)
+
+
+def tile_custom(space: IndexSpace, sizes: Sequence[int]) -> TiledIndexSpace:
+    """P126 ``TiledIndexSpace tM{M, {10,20}}`` -- arbitrary sizes with full coverage (P127)."""
+    if any(int(s) < 1 for s in sizes):
+        raise OracleError("tile size < 1")
+    if sum(sizes) != space.extent:
+        raise OracleError("tile sizes do not cover the index space")
+    offs = [0]
+    for s in sizes:
+        offs.append(offs[-1] + int(s))
+    spins = []
+    segs = space.segments()
+    for t in range(len(sizes)):
+        lo, hi = offs[t], offs[t + 1]
+        owner = [s for (b, e, s) in segs if b <= lo and hi <= e]
+        if not owner:
+            raise OracleError("tile straddles a spin range")
+        spins.append(owner[0])
+    return TiledIndexSpace(space, offs, spins)
+
+
+@dataclass
+class Tensor:
+    dims: List[TiledIndexSpace]
+    nz: List[int]                 # row-major over the block grid, 0/1
+    nranks: int = 1
+
+    @property
+    def order(self) -> int:
+        return len(self.dims)
+
+    @property
+    def grid(self) -> Tuple[int, ...]:
+        return tuple(d.ntiles for d in self.dims)
+
+    @property
+    def shape(self) -> Tuple[int, ...]:
+        return tuple(d.space.extent for d in self.dims)
+
+    def nblocks(self) -> int:
+        n = 1
+        for g in self.grid:
+            n *= g
+        return n
+
+    def block_coords(self, bid: int) -> Tuple[int, ...]:
+        """Row-major block id -> tile indices (P111: Cartesian product of tiles)."""
+        c = []
+        for g in reversed(self.grid):
+            c.append(bid % g)
+            bid //= g
+        return tuple(reversed(c))
+
+    def block_id(self, coords: Sequence[int]) -> int:
+        b = 0
+        for g, t in zip(self.grid, coords):
+            b = b * g + t
+        return b
+
+    def block_extents(self, bid: int) -> Tuple[int, ...]:
+        return tuple(d.size(t) for d, t in zip(self.dims, self.block_coords(bid)))
+
+    def block_origin(self, bid: int) -> Tuple[int, ...]:
+        return tuple(d.offsets[t] for d, t in zip(self.dims, self.block_coords(bid)))
+
+    def block_volume(self, bid: int) -> int:
+        v = 1
+        for e in self.block_extents(bid):
+            v *= e
+        return v
+
+    def blk_off(self) -> List[int]:
+        """P210 (sparsity-aware scheme): packed offsets, -1 for zero blocks, 16-B aligned (R10)."""
+        out, cur = [], 0
+        for b in range(self.nblocks()):
+            if self.nz[b]:
+                cur = (cur + 1) // 2 * 2
+                out.append(cur)
+                cur += self.block_volume(b)
+            else:
+                out.append(-1)
+        return out
+
+    def packed_elems(self) -> int:
+        offs = self.blk_off()
+        end = 0
+        for b, o in enumerate(offs):
+            if o >= 0:
+                end = max(end, o + self.block_volume(b))
+        return (end + 1) // 2 * 2
+
+    def owners(self) -> List[int]:
+        """P210 third scheme: round-robin over non-zero blocks; -1 for zero blocks."""
+        out, k = [], 0
+        for b in range(self.nblocks()):
+            if self.nz[b]:
+                out.append(k % self.nranks)
+                k += 1
+            else:
+                out.append(-1)
+        return out
+
+
+def tensor_dense_map(dims: Sequence[TiledIndexSpace], nranks: int = 1) -> Tensor:
+    n = 1
+    for d in dims:
+        n *= d.ntiles
+    return Tensor(list(dims), [1] * n, nranks)
+
+
+def tensor_explicit(dims: Sequence[TiledIndexSpace], nz: Sequence[int], nranks: int = 1) -> Tensor:
+    t = tensor_dense_map(dims, nranks)
+    if len(nz) != t.nblocks():
+        raise OracleError("nz length != number of blocks")
+    t.nz = [1 if int(v) else 0 for v in nz]
+    return t
+
+
+def tensor_spin(dims: Sequence[TiledIndexSpace], upper: Sequence[int], lower: Sequence[int],
+                nranks: int = 1) -> Tensor:
+    """P138 spin block sparsity, reading R7: block non-zero iff the spin sums of the tiles at the
+    ``upper`` positions and at the ``lower`` positions are equal."""
+    t = tensor_dense_map(dims, nranks)
+    nz = []
+    for b in range(t.nblocks()):
+        c = t.block_coords(b)
+        su = sum(t.dims[p].tile_spin[c[p]] for p in upper)
+        sl = sum(t.dims[p].tile_spin[c[p]] for p in lower)
+        nz.append(1 if su == sl else 0)
+    t.nz = nz
+    return t
+
+
+# ----------------------------------------------------------------------------- labelled contraction
+
+@dataclass
+class ContractionLabels:
+    free_c: List[str]      # C labels in C order
+    con: List[str]         # contracted labels, order of first appearance in A
+    in_a: List[bool]       # per C label: True if it comes from A
+
+
+def analyse_labels(c_lbl: str, a_lbl: str, b_lbl: str) -> ContractionLabels:
+    """P174 ``C(i,a) += alpha * A(i,l) * B(l,a)``: l is contracted (in A and B, not in C)."""
+    for s in (c_lbl, a_lbl, b_lbl):
+        if len(set(s)) != len(s):
+            raise OracleError("repeated label")
+    con = [x for x in a_lbl if x in b_lbl and x not in c_lbl]
+    for x in c_lbl:
+        if (x in a_lbl) == (x in b_lbl):
+            raise OracleError("C label must appear in exactly one of A, B")
+    for x in a_lbl:
+        if x not in c_lbl and x not in b_lbl:
+            raise OracleError("dangling label in A")
+    for x in b_lbl:
+        if x not in c_lbl and x not in a_lbl:
+            raise OracleError("dangling label in B")
+    return ContractionLabels(list(c_lbl), con, [x in a_lbl for x in c_lbl])
+
+
+def task_list(C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str):
+    """Canonical task list by brute force (reading R11).
+
+    Returns (cblocks, ptr, a_blk, b_blk, cost): ``cblocks`` the non-zero C block ids in row-major
+    order, CSR ``ptr`` over them, the A and B block ids of every task, and the FLOP cost
+    2*prod(extents of all labels) summed per C block (S484-492: 2mnk per block GEMM)."""
+    L = analyse_labels(c_lbl, a_lbl, b_lbl)
+    tis = {}
+    for T, lbl in ((C, c_lbl), (A, a_lbl), (B, b_lbl)):
+        for d, x in zip(T.dims, lbl):
+            tis.setdefault(x, d)
+    con_grid = [tis[x].ntiles for x in L.con]
+    cblocks, ptr, ab, bb, cost = [], [0], [], [], []
+    for cb in range(C.nblocks()):
+        ccoord = C.block_coords(cb)
+        tile = dict(zip(c_lbl, ccoord))
+        total = 0
+        if not C.nz[cb]:
+            continue
+        for kt in product(*[range(n) for n in con_grid]):
+            tile.update(zip(L.con, kt))
+            a_id = A.block_id([tile[x] for x in a_lbl])
+            b_id = B.block_id([tile[x] for x in b_lbl])
+            if A.nz[a_id] and B.nz[b_id]:
+                ab.append(a_id)
+                bb.append(b_id)
+                f = 2
+                for x in list(c_lbl) + L.con:
+                    f *= tis[x].size(tile[x])
+                total += f
+        cblocks.append(cb)
+        ptr.append(len(ab))
+        cost.append(total)
+    return cblocks, ptr, ab, bb, cost
+
+
+def lpt_partition(cost: Sequence[int], cblocks: Sequence[int], nranks: int) -> List[int]:
+    """Deterministic LPT: order by (cost desc, block id asc); least-loaded rank, ties lowest rank."""
+    order = sorted(range(len(cost)), key=lambda i: (-cost[i], cblocks[i]))
+    load = [0] * nranks
+    owner = [0] * len(cost)
+    for i in order:
+        r = min(range(nranks), key=lambda q: (load[q], q))
+        owner[i] = r
+        load[r] += cost[i]
+    return owner

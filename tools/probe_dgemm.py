@@ -1,0 +1,12 @@
+# cuBLAS DGEMM ceiling reference (not the product): torch.matmul float64 on cuda:0.
+import json, torch
+torch.backends.cuda.matmul.allow_tf32 = False
+for n in (4096, 8192):
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda"); b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2): c = a @ b
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e30
+    for _ in range(5):
+        e0.record(); c = a @ b; e1.record(); e1.synchronize(); best = min(best, e0.elapsed_time(e1))
+    print(json.dumps({"probe": "cublas_dgemm", "n": n, "ms": best, "tflops": 2 * n**3 / best / 1e9}))
