@@ -1,0 +1,231 @@
+/*
+ * tt.h -- C ABI of the B200-native tiled block-sparse FP64 tensor contraction library (libtt.so).
+ *
+ * The library executes the data-parallel hot path of TAMM (arXiv 2201.01257): labelled tensor
+ * set / addition / contraction over TiledIndexSpaces with block sparsity, on NVIDIA B200 (sm_100a).
+ * Citations: P<n> = PAPER.md line n (/root/reference/PAPER.md, the paper's LaTeX source),
+ * S<n> = SPEC.md line n, R<n> = reading n in DESIGN.md §3.
+ *
+ * Conventions (all entry points)
+ *   - Every call returns tt_status: TT_OK (0) or a negative error code.  tt_last_error() returns a
+ *     thread-local, NUL-terminated message describing the last failure on the calling thread.
+ *   - Handles (tt_ctx, tt_is, tt_tis, tt_tensor) are opaque, created and destroyed by the library.
+ *     They are immutable metadata with shallow-copy semantics (P212: "tensors in terms of handles ...
+ *     any assignment done on tensor objects will be a shallow copy").
+ *   - Tensor DATA is never allocated by the library: the caller binds device memory (e.g. a torch
+ *     tensor) with tt_tensor_bind and keeps ownership; the library never frees it.  Small internal
+ *     metadata (block maps, task lists, plans) is allocated by the library on the context's device
+ *     and freed by tt_ctx_destroy.
+ *   - Execution is SPMD (P212, "single program multiple data"): with nranks > 1 every rank makes
+ *     the same sequence of calls with identical metadata.  Compute calls are asynchronous on the
+ *     context's CUDA stream; argument/validation errors are returned synchronously; CUDA and NCCL
+ *     errors are returned by the call that observes them or by tt_sync.
+ *   - Elements are IEEE FP64 (Tensor<double>, P130-132).
+ *   - Labels are C strings with one character per dimension (e.g. "abij"); a character binds, by
+ *     position, to that dimension's tiled index space (P145-159, Einstein notation).
+ */
+#ifndef TT_H_
+#define TT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t tt_status;
+enum {
+  TT_OK = 0,
+  TT_E_ARG = -1,        /* bad argument (NULL handle, out-of-range value, wrong length)              */
+  TT_E_COVERAGE = -2,   /* tile sizes do not cover the index space exactly (P127; S83-87)            */
+  TT_E_LABEL = -3,      /* label arity / dangling / repeated / batch label (S178, S380, S412)        */
+  TT_E_TILING = -4,     /* matched labels on different tiled spaces (S413), or a tile straddles spin */
+  TT_E_ZERO_BLOCK = -5, /* operation would write into a zero block (S208)                            */
+  TT_E_UNBOUND = -6,    /* tensor has no storage bound, or the bound capacity is too small (S208)    */
+  TT_E_OOM = -7,        /* internal metadata allocation failed                                       */
+  TT_E_CUDA = -8,       /* CUDA runtime error (message in tt_last_error)                             */
+  TT_E_NCCL = -9,       /* NCCL error                                                                */
+  TT_E_STATE = -10,     /* call not valid in this state (e.g. device call on a host-only context)    */
+  TT_E_UNSUPPORTED = -11/* shape outside the supported envelope (e.g. order > TT_MAX_ORDER)          */
+};
+
+enum { TT_MAX_ORDER = 8 };          /* maximum tensor order                                        */
+enum { TT_REPLICATED = -2 };        /* owner value: every rank holds the block                     */
+enum { TT_KIND_UNIFORM = 0, TT_KIND_INTEGER = 1 };   /* synthetic input kinds (tt_fill_synthetic)  */
+
+typedef struct tt_ctx_s* tt_ctx;
+typedef struct tt_is_s* tt_is;
+typedef struct tt_tis_s* tt_tis;
+typedef struct tt_tensor_s* tt_tensor;
+
+/* Per-call statistics of the last set/add/contract/scalar call on a context (host-side counts). */
+typedef struct {
+  int64_t c_blocks;        /* output blocks computed by this rank                                  */
+  int64_t tasks;           /* non-zero (A,B) tile pairs executed by this rank (contraction)        */
+  int64_t work_items;      /* CTA work items launched                                              */
+  double flops;            /* algorithmic FLOPs of this rank: sum over tasks of 2*prod(extents)    */
+  double bytes;            /* compulsory HBM bytes of this rank (8*(A+B+(1+[beta!=0])*C elements)) */
+  int64_t gathered_bytes;  /* bytes received from other ranks by the input-tile gather             */
+  int64_t launches;        /* kernels launched by the call                                         */
+  int32_t plan_cached;     /* 1 if the task list / partition / gather plan came from the cache     */
+  int32_t kernel_variant;  /* contraction kernel tile variant used                  */
+} tt_stats;
+
+/* ------------------------------------------------------------------------------------------------
+ * Execution context (P178-188: ExecutionContext{pg, &distribution, manager}).
+ *   device      CUDA device ordinal, or -1 for a HOST-ONLY context (metadata, validation, host task
+ *               lists and partitions only; every device call then returns TT_E_STATE).
+ *   cuda_stream cudaStream_t the library launches on (NULL = legacy default stream); not owned.
+ *   rank/nranks SPMD rank and size; 0 <= rank < nranks.
+ *   nccl_id     pointer to a 128-byte ncclUniqueId (identical on all ranks) when nranks > 1 and
+ *               device >= 0; otherwise NULL.  The library creates and owns the NCCL communicator.
+ */
+tt_status tt_ctx_create(int32_t device, void* cuda_stream, int32_t rank, int32_t nranks,
+                        const void* nccl_id, tt_ctx* out);
+tt_status tt_ctx_destroy(tt_ctx ctx);
+/* Writes a fresh ncclUniqueId (128 bytes) into out128 (rank 0 calls it and broadcasts the bytes). */
+tt_status tt_nccl_unique_id(void* out128);
+/* Record CUDA events around every kernel the library launches (for roofline timing). */
+tt_status tt_ctx_set_profiling(tt_ctx ctx, int32_t enable);
+/* Synchronises the context stream, then returns the summed event time (ms) and launch count of the
+ * kernels whose name contains `kernel` ("" = all) since the last tt_profile_reset. */
+tt_status tt_profile_read(tt_ctx ctx, const char* kernel, double* total_ms, int64_t* launches);
+tt_status tt_profile_reset(tt_ctx ctx);
+/* Statistics of the last compute call (see tt_stats). */
+tt_status tt_last_stats(tt_ctx ctx, tt_stats* out);
+/* Total kernels launched by the library on this context since creation. */
+tt_status tt_launch_count(tt_ctx ctx, int64_t* out);
+/* Blocks until all work queued on the context stream has finished; surfaces deferred errors. */
+tt_status tt_sync(tt_ctx ctx);
+
+/* ------------------------------------------------------------------------------------------------
+ * IndexSpace (P116-122, Fig. 2: IndexSpace N{range(100)}).
+ *   extent      number of indices (>= 1).
+ *   n_ranges    0, or the number of ranges in begin_end; ranges must be ascending, non-empty and
+ *               cover [0, extent) exactly (TT_E_COVERAGE otherwise).
+ *   begin_end   2*n_ranges int64 [begin, end) pairs.
+ *   spin        n_ranges values (+1 alpha, -1 beta) or NULL (no spin attribute).  P138: "encode spin
+ *               information ... allocate these tensors using a block-sparse representation".
+ * Tilings never straddle a range boundary (S39, reading R6).
+ */
+tt_status tt_is_create(int64_t extent, int32_t n_ranges, const int64_t* begin_end, const int8_t* spin,
+                       tt_is* out);
+tt_status tt_is_destroy(tt_is is);
+
+/* TiledIndexSpace (P125-127): fixed tile size (remainder in the last tile of each range, R5) or
+ * custom sizes with full coverage (TT_E_COVERAGE if they do not sum to the extent, TT_E_TILING if a
+ * tile straddles a range boundary).  The tiled space keeps a reference to its index space. */
+tt_status tt_tis_fixed(tt_is is, int64_t tile, tt_tis* out);
+tt_status tt_tis_custom(tt_is is, int32_t n, const int64_t* sizes, tt_tis* out);
+/* ntiles; offsets = ntiles+1 split points; tile_spin = per-tile spin (0 = none).  Pointers are owned
+ * by the handle and valid until tt_tis_destroy. */
+tt_status tt_tis_info(tt_tis tis, int32_t* ntiles, const int64_t** offsets, const int8_t** tile_spin);
+tt_status tt_tis_destroy(tt_tis tis);
+
+/* ------------------------------------------------------------------------------------------------
+ * Tensor<double> (P129-140): blocks indexed by the Cartesian product of the tiles of its dimensions
+ * (row-major block grid; row-major elements inside a block, R9).  Storage is PACKED: only non-zero
+ * blocks, in row-major block order, each block start rounded up to 2 doubles = 16 B (P210 third
+ * scheme; R10).  Every rank uses the same packed layout; with nranks > 1 a rank holds valid data
+ * only for the blocks it owns (default owners: round robin over non-zero blocks, P210).
+ *   order       1..TT_MAX_ORDER (order 0 scalars are returned by tt_contract_scalar instead)
+ *   dims        order tiled index spaces (referenced, not copied; keep them alive)
+ *   nz          row-major u8 map over the block grid (1 = non-zero) or NULL = dense.
+ * tt_tensor_create_spin derives nz from the spin rule of R7: a block is non-zero iff the sum of tile
+ * spins over the dimensions in upper_mask equals the sum over lower_mask (bit d = dimension d).
+ */
+tt_status tt_tensor_create(tt_ctx ctx, int32_t order, const tt_tis* dims, const uint8_t* nz,
+                           tt_tensor* out);
+tt_status tt_tensor_create_spin(tt_ctx ctx, int32_t order, const tt_tis* dims, uint32_t upper_mask,
+                                uint32_t lower_mask, tt_tensor* out);
+tt_status tt_tensor_info(tt_tensor t, int32_t* order, int64_t* nblocks, int64_t* nnz_blocks);
+/* packed_elems = elements the bound buffer must hold; blk_off[nblocks] (-1 = zero block);
+ * owner[nblocks] (-1 = zero block, TT_REPLICATED, or a rank); nz[nblocks].  Owned by the handle.
+ * These maps are the frozen layout contract compared bit-exactly with the oracle. */
+tt_status tt_tensor_layout(tt_tensor t, int64_t* packed_elems, const int64_t** blk_off,
+                           const int32_t** owner, const uint8_t** nz);
+/* Replace the owner map (nblocks entries; zero blocks ignored; values in [0,nranks) or
+ * TT_REPLICATED).  Must be identical on every rank. */
+tt_status tt_tensor_set_owner(tt_tensor t, const int32_t* owner);
+/* Bind caller-owned DEVICE memory of capacity_elems doubles (>= packed_elems, 16-B aligned). */
+tt_status tt_tensor_bind(tt_tensor t, void* dev_ptr, int64_t capacity_elems);
+/* Host <-> device copies of the whole packed buffer on the context stream (asynchronous when the
+ * host memory is pinned).  host holds packed_elems doubles.  These are the end-to-end entry points
+ * for callers whose data lives in host memory. */
+tt_status tt_tensor_upload(tt_ctx ctx, tt_tensor t, const double* host);
+tt_status tt_tensor_download(tt_ctx ctx, tt_tensor t, double* host);
+tt_status tt_tensor_destroy(tt_tensor t);
+
+/* Seeded synthetic input (not part of the method): every element of every non-zero
+ * block this rank holds is set to the counter-based generator value at its GLOBAL row-major index g:
+ *   h = splitmix64(seed ^ (tag * 0x9E3779B97F4A7C15) ^ g)
+ *   kind UNIFORM: (h >> 11) * 2^-53 * 2 - 1;   kind INTEGER: (h mod 5) - 2.
+ * Identical to synthetic/__init__.py (checked bit-exactly by tests). */
+tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag, int32_t kind);
+
+/* ------------------------------------------------------------------------------------------------
+ * Operations (P170-174, grammar rules 5-7; "=" is beta = 0 and never reads C, "+=" is beta = 1,
+ * general beta per BASELINE north_star; R3, R4).  Only non-zero C blocks owned by this rank (or
+ * replicated) are written; zero input blocks read as zeros (S216); no contribution is computed for
+ * a zero C block (R8).
+ *
+ * tt_set       C = alpha                                      (P172, rule 5)
+ * tt_add       C(c_lbl) = beta*C + alpha*A(a_lbl)             (P173, rule 6: a_lbl is a permutation
+ *                                                              of c_lbl, same tiled spaces)
+ * tt_contract  C(c_lbl) = beta*C + alpha*sum A(a_lbl)*B(b_lbl) (P174, rule 7): contracted labels are
+ *              the labels in both A and B and not in C; every C label appears in exactly one of A, B;
+ *              no label repeats within an operand; a label in all three is rejected (TT_E_LABEL);
+ *              matched labels must use the same tt_tis (TT_E_TILING).
+ *              Each non-zero C block is the sum over the non-zero (A,B) tile pairs of the task list
+ *              (tt_task_list) of a dense FP64 contraction, executed by the DMMA kernel with the
+ *              index permutation folded into the operand staging.  With nranks > 1
+ *              the rank computes the C blocks it owns and first receives, over NCCL, exactly the A/B
+ *              blocks its tasks read but does not own (P212 "access to the remote portions").
+ * tt_contract_scalar  *result = alpha * sum_x A(x)*B(x) over all labels (order-0 result such as the
+ *              CC energy, P534-536), summed over ranks with an NCCL all-reduce; *result is a HOST
+ *              pointer and the call synchronises the stream.  With nranks > 1 each rank sums the A
+ *              blocks it owns (replicated blocks: rank 0).
+ */
+tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha);
+tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha, tt_tensor A,
+                 const char* a_lbl);
+tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha,
+                      tt_tensor A, const char* a_lbl, tt_tensor B, const char* b_lbl);
+tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* a_lbl, tt_tensor B,
+                             const char* b_lbl, double* result);
+
+/* ------------------------------------------------------------------------------------------------
+ * Task list (canonical order, R11): for each non-zero C block in row-major order (all of them, not
+ * only owned ones), each contracted-tile tuple in row-major order with the contracted labels in order
+ * of first appearance in A: a task (A block id, B block id) iff both blocks are non-zero.
+ *   where       0 = host enumerator, 1 = the device builder (count -> scan -> fill) copied back.
+ *   cblk        [n_cblocks] non-zero C block ids;  ptr [n_cblocks+1] CSR offsets into a_blk/b_blk.
+ *   cost        [n_cblocks] FLOPs per C block = sum over its tasks of 2*prod(extents of all labels).
+ * Two-call pattern: pass NULL arrays (cap ignored) to get n_cblocks / n_tasks; then arrays of that
+ * size (cap = capacity of a_blk/b_blk) -- TT_E_ARG if too small.
+ */
+tt_status tt_task_list(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
+                       tt_tensor B, const char* b_lbl, int32_t where, int64_t* cblk, int64_t* ptr,
+                       int64_t* a_blk, int64_t* b_blk, int64_t* cost, int64_t cap,
+                       int64_t* n_cblocks, int64_t* n_tasks);
+
+/* LPT owner partition of C's non-zero blocks over the context's nranks (R3-part): blocks sorted by
+ * (cost desc, block id asc), each to the least-loaded rank, ties to the lowest rank.  Writes
+ * owner[nblocks of C] (-1 for zero blocks).  Does not modify C (use tt_tensor_set_owner). */
+tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
+                           tt_tensor B, const char* b_lbl, int32_t* owner);
+
+/* Input-tile gather plan of this rank for tt_contract (host metadata; for tests and reports).
+ * recv[3*i .. 3*i+2] = (operand 0=A/1=B, block id, source rank) for each block this rank receives;
+ * send[3*i .. 3*i+2] = (operand, block id, destination rank).  Two-call pattern as tt_task_list. */
+tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
+                         tt_tensor B, const char* b_lbl, int64_t* recv, int64_t* n_recv,
+                         int64_t* send, int64_t* n_send, int64_t cap);
+
+const char* tt_last_error(void);
+int32_t tt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_H_ */

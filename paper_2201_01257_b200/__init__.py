@@ -1,0 +1,357 @@
+"""paper_2201_01257_b200 -- thin Python binding of libtt (include/tt.h).
+
+Argument marshalling only: every step of the hot path runs in libtt's sm_100a kernels.  There is no
+CPU fallback: importing this package fails loudly if ``libtt.so`` is missing (build it with
+``python -m paper_2201_01257_b200.build`` or ``__graft_entry__.build()``), and every device call on
+a machine without a B200 returns an error from the library.
+
+Names follow the C ABI (and the paper's vocabulary, P111-174): IndexSpace, TiledIndexSpace, Tensor,
+set_/add/contract/contract_scalar, task_list, partition_lpt, gather_plan.  Device memory is supplied
+by the caller (e.g. a torch tensor); pointers are passed as integers (``t.data_ptr()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtt.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libtt.so not found at {LIB_PATH}: build it with `python -m paper_2201_01257_b200.build` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+
+TT_OK = 0
+ERRORS = {-1: "TT_E_ARG", -2: "TT_E_COVERAGE", -3: "TT_E_LABEL", -4: "TT_E_TILING", -5: "TT_E_ZERO_BLOCK",
+          -6: "TT_E_UNBOUND", -7: "TT_E_OOM", -8: "TT_E_CUDA", -9: "TT_E_NCCL", -10: "TT_E_STATE",
+          -11: "TT_E_UNSUPPORTED"}
+TT_REPLICATED = -2
+KIND_UNIFORM, KIND_INTEGER = 0, 1
+
+_vp, _i32, _i64, _u32, _u64, _dbl = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                     ctypes.c_uint64, ctypes.c_double)
+_P = ctypes.POINTER
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("c_blocks", _i64), ("tasks", _i64), ("work_items", _i64), ("flops", _dbl), ("bytes", _dbl),
+                ("gathered_bytes", _i64), ("launches", _i64), ("plan_cached", _i32), ("kernel_variant", _i32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_SIGS = {
+    "tt_ctx_create": [_i32, _vp, _i32, _i32, _vp, _P(_vp)],
+    "tt_ctx_destroy": [_vp],
+    "tt_nccl_unique_id": [_vp],
+    "tt_ctx_set_profiling": [_vp, _i32],
+    "tt_profile_read": [_vp, ctypes.c_char_p, _P(_dbl), _P(_i64)],
+    "tt_profile_reset": [_vp],
+    "tt_last_stats": [_vp, _P(Stats)],
+    "tt_launch_count": [_vp, _P(_i64)],
+    "tt_sync": [_vp],
+    "tt_is_create": [_i64, _i32, _vp, _vp, _P(_vp)],
+    "tt_is_destroy": [_vp],
+    "tt_tis_fixed": [_vp, _i64, _P(_vp)],
+    "tt_tis_custom": [_vp, _i32, _vp, _P(_vp)],
+    "tt_tis_info": [_vp, _P(_i32), _P(_P(_i64)), _P(_P(ctypes.c_int8))],
+    "tt_tis_destroy": [_vp],
+    "tt_tensor_create": [_vp, _i32, _vp, _vp, _P(_vp)],
+    "tt_tensor_create_spin": [_vp, _i32, _vp, _u32, _u32, _P(_vp)],
+    "tt_tensor_info": [_vp, _P(_i32), _P(_i64), _P(_i64)],
+    "tt_tensor_layout": [_vp, _P(_i64), _P(_P(_i64)), _P(_P(_i32)), _P(_P(ctypes.c_uint8))],
+    "tt_tensor_set_owner": [_vp, _vp],
+    "tt_tensor_bind": [_vp, _vp, _i64],
+    "tt_tensor_upload": [_vp, _vp, _vp],
+    "tt_tensor_download": [_vp, _vp, _vp],
+    "tt_tensor_destroy": [_vp],
+    "tt_fill_synthetic": [_vp, _vp, _u64, _u32, _i32],
+    "tt_set": [_vp, _vp, _dbl],
+    "tt_add": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p],
+    "tt_contract": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p],
+    "tt_contract_scalar": [_vp, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _P(_dbl)],
+    "tt_task_list": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _i32, _vp, _vp, _vp,
+                     _vp, _vp, _i64, _P(_i64), _P(_i64)],
+    "tt_partition_lpt": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp],
+    "tt_gather_plan": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _P(_i64), _vp,
+                       _P(_i64), _i64],
+    "tt_last_error": [],
+    "tt_version": [],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _i32
+_lib.tt_last_error.restype = ctypes.c_char_p
+
+EXPORTED = tuple(_SIGS)
+
+
+class TTError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = ERRORS.get(code, str(code))
+
+
+def _check(status: int):
+    if status != TT_OK:
+        raise TTError(status, _lib.tt_last_error().decode(errors="replace"))
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_vp) if a is not None else None
+
+
+def _b(s: str) -> bytes:
+    return s.encode()
+
+
+def _devptr(x) -> int:
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+def version() -> int:
+    return _lib.tt_version()
+
+
+def last_error() -> str:
+    return _lib.tt_last_error().decode(errors="replace")
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.tt_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """ExecutionContext (P178-188).  device=-1 gives a host-only context (metadata only)."""
+
+    def __init__(self, device: int = 0, stream: int = 0, rank: int = 0, nranks: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        h = _vp()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(_lib.tt_ctx_create(device, _vp(stream or 0), rank, nranks, idbuf, ctypes.byref(h)))
+        self.h, self.device, self.rank, self.nranks = h, device, rank, nranks
+
+    def close(self):
+        if self.h:
+            _check(_lib.tt_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        _check(_lib.tt_sync(self.h))
+
+    def set_profiling(self, on: bool):
+        _check(_lib.tt_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def profile(self, kernel: str = ""):
+        ms, n = _dbl(), _i64()
+        _check(_lib.tt_profile_read(self.h, _b(kernel), ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    def profile_reset(self):
+        _check(_lib.tt_profile_reset(self.h))
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(_lib.tt_last_stats(self.h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def launches(self) -> int:
+        n = _i64()
+        _check(_lib.tt_launch_count(self.h, ctypes.byref(n)))
+        return n.value
+
+
+class IndexSpace:
+    """IndexSpace (P116-122).  ``ranges`` = [(begin, end)], ``spins`` = [+1/-1] per range (P138)."""
+
+    def __init__(self, extent: int, ranges: Optional[Sequence] = None, spins: Optional[Sequence[int]] = None):
+        h = _vp()
+        be = np.asarray([x for r in (ranges or []) for x in r], dtype=np.int64)
+        sp = np.asarray(spins, dtype=np.int8) if spins is not None else None
+        _check(_lib.tt_is_create(extent, len(ranges or []), _ptr(be) if len(be) else None, _ptr(sp),
+                                 ctypes.byref(h)))
+        self.h, self.extent = h, extent
+
+    def __del__(self):  # pragma: no cover
+        try:
+            _lib.tt_is_destroy(self.h)
+        except Exception:
+            pass
+
+
+class TiledIndexSpace:
+    """TiledIndexSpace (P125-127): fixed ``tile`` or custom ``sizes``."""
+
+    def __init__(self, space: IndexSpace, tile: Optional[int] = None, sizes: Optional[Sequence[int]] = None):
+        h = _vp()
+        if sizes is not None:
+            s = np.asarray(sizes, dtype=np.int64)
+            _check(_lib.tt_tis_custom(space.h, len(s), _ptr(s), ctypes.byref(h)))
+        else:
+            _check(_lib.tt_tis_fixed(space.h, int(tile), ctypes.byref(h)))
+        self.h, self.space = h, space
+        n = _i32()
+        off = _P(_i64)()
+        sp = _P(ctypes.c_int8)()
+        _check(_lib.tt_tis_info(h, ctypes.byref(n), ctypes.byref(off), ctypes.byref(sp)))
+        self.ntiles = n.value
+        self.offsets = np.ctypeslib.as_array(off, (n.value + 1,)).copy()
+        self.spin = np.ctypeslib.as_array(sp, (n.value,)).copy() if n.value else np.zeros(0, np.int8)
+
+    def __del__(self):  # pragma: no cover
+        try:
+            _lib.tt_tis_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Tensor:
+    """Tensor<double> (P129-140) with a non-zero block map: explicit ``nz`` (u8 per block, row-major)
+    or the spin rule ``spin=(upper_dims, lower_dims)`` (reading R7)."""
+
+    def __init__(self, ctx: Context, dims: Sequence[TiledIndexSpace], nz=None, spin=None):
+        h = _vp()
+        arr = (_vp * len(dims))(*[d.h.value if isinstance(d.h, _vp) else d.h for d in dims])
+        if spin is not None:
+            up = sum(1 << d for d in spin[0])
+            lo = sum(1 << d for d in spin[1])
+            _check(_lib.tt_tensor_create_spin(ctx.h, len(dims), arr, up, lo, ctypes.byref(h)))
+        else:
+            z = np.ascontiguousarray(nz, dtype=np.uint8) if nz is not None else None
+            _check(_lib.tt_tensor_create(ctx.h, len(dims), arr, _ptr(z), ctypes.byref(h)))
+        self.h, self.ctx, self.dims = h, ctx, list(dims)
+        self._refresh()
+        self.storage = None
+
+    def _refresh(self):
+        order, nb, nnz = _i32(), _i64(), _i64()
+        _check(_lib.tt_tensor_info(self.h, ctypes.byref(order), ctypes.byref(nb), ctypes.byref(nnz)))
+        pe = _i64()
+        bo, ow, z = _P(_i64)(), _P(_i32)(), _P(ctypes.c_uint8)()
+        _check(_lib.tt_tensor_layout(self.h, ctypes.byref(pe), ctypes.byref(bo), ctypes.byref(ow), ctypes.byref(z)))
+        self.order, self.nblocks, self.nnz, self.packed_elems = order.value, nb.value, nnz.value, pe.value
+        self.blk_off = np.ctypeslib.as_array(bo, (nb.value,)).copy()
+        self.owner = np.ctypeslib.as_array(ow, (nb.value,)).copy()
+        self.nz = np.ctypeslib.as_array(z, (nb.value,)).copy()
+
+    @property
+    def shape(self):
+        return tuple(int(d.space.extent) for d in self.dims)
+
+    @property
+    def grid(self):
+        return tuple(int(d.ntiles) for d in self.dims)
+
+    def set_owner(self, owner):
+        o = np.ascontiguousarray(owner, dtype=np.int32)
+        _check(_lib.tt_tensor_set_owner(self.h, _ptr(o)))
+        self._refresh()
+
+    def bind(self, storage, capacity: Optional[int] = None):
+        """Bind caller-owned device memory (a torch tensor, or an int pointer with ``capacity``)."""
+        if capacity is None:
+            capacity = int(storage.numel())
+        _check(_lib.tt_tensor_bind(self.h, _vp(_devptr(storage)), int(capacity)))
+        self.storage = storage
+
+    def upload(self, host: np.ndarray):
+        assert host.dtype == np.float64 and host.size >= self.packed_elems
+        _check(_lib.tt_tensor_upload(self.ctx.h, self.h, _vp(host.ctypes.data)))
+
+    def upload_ptr(self, host_ptr: int):
+        _check(_lib.tt_tensor_upload(self.ctx.h, self.h, _vp(host_ptr)))
+
+    def download(self, host: Optional[np.ndarray] = None) -> np.ndarray:
+        if host is None:
+            host = np.empty(self.packed_elems, dtype=np.float64)
+        _check(_lib.tt_tensor_download(self.ctx.h, self.h, _vp(host.ctypes.data)))
+        return host
+
+    def download_ptr(self, host_ptr: int):
+        _check(_lib.tt_tensor_download(self.ctx.h, self.h, _vp(host_ptr)))
+
+    def __del__(self):  # pragma: no cover
+        try:
+            _lib.tt_tensor_destroy(self.h)
+        except Exception:
+            pass
+
+
+def fill_synthetic(ctx: Context, T: Tensor, seed: int, tag: int, kind: int = KIND_UNIFORM):
+    _check(_lib.tt_fill_synthetic(ctx.h, T.h, seed, tag, kind))
+
+
+def set_(ctx: Context, C: Tensor, alpha: float):
+    """P172 rule 5: C = alpha."""
+    _check(_lib.tt_set(ctx.h, C.h, float(alpha)))
+
+
+def add(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str):
+    """P173 rule 6: C(c_lbl) = beta*C + alpha*A(a_lbl)."""
+    _check(_lib.tt_add(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), A.h, _b(a_lbl)))
+
+
+def contract(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str, B: Tensor,
+             b_lbl: str):
+    """P174 rule 7: C(c_lbl) = beta*C + alpha*A(a_lbl)*B(b_lbl)."""
+    _check(_lib.tt_contract(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), A.h, _b(a_lbl), B.h, _b(b_lbl)))
+
+
+def contract_scalar(ctx: Context, alpha: float, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str) -> float:
+    r = _dbl()
+    _check(_lib.tt_contract_scalar(ctx.h, float(alpha), A.h, _b(a_lbl), B.h, _b(b_lbl), ctypes.byref(r)))
+    return r.value
+
+
+def task_list(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str,
+              device: bool = False):
+    """Canonical task list (R11): returns dict cblk, ptr, a_blk, b_blk, cost (numpy int64)."""
+    nc, nt = _i64(), _i64()
+    args = (ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl), 1 if device else 0)
+    _check(_lib.tt_task_list(*args, None, None, None, None, None, 0, ctypes.byref(nc), ctypes.byref(nt)))
+    cb = np.empty(nc.value, np.int64)
+    ptr = np.empty(nc.value + 1, np.int64)
+    ab = np.empty(max(nt.value, 1), np.int64)
+    bb = np.empty(max(nt.value, 1), np.int64)
+    cost = np.empty(nc.value, np.int64)
+    _check(_lib.tt_task_list(*args, _ptr(cb), _ptr(ptr), _ptr(ab), _ptr(bb), _ptr(cost), len(ab), ctypes.byref(nc),
+                             ctypes.byref(nt)))
+    return {"cblk": cb, "ptr": ptr, "a_blk": ab[:nt.value], "b_blk": bb[:nt.value], "cost": cost}
+
+
+def partition_lpt(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str) -> np.ndarray:
+    own = np.empty(C.nblocks, np.int32)
+    _check(_lib.tt_partition_lpt(ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl), _ptr(own)))
+    return own
+
+
+def gather_plan(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str):
+    """(recv, send) arrays of (operand, block, peer) rows for this rank."""
+    nr, ns = _i64(), _i64()
+    args = (ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl))
+    _check(_lib.tt_gather_plan(*args, None, ctypes.byref(nr), None, ctypes.byref(ns), 0))
+    cap = max(nr.value, ns.value, 1)
+    r = np.empty(3 * cap, np.int64)
+    s = np.empty(3 * cap, np.int64)
+    _check(_lib.tt_gather_plan(*args, _ptr(r), ctypes.byref(nr), _ptr(s), ctypes.byref(ns), cap))
+    return r[:3 * nr.value].reshape(-1, 3), s[:3 * ns.value].reshape(-1, 3)

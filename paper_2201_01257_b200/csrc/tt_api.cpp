@@ -1,0 +1,1465 @@
+// tt_api.cpp -- host side of libtt: handles, validation, layout, task lists, partition, plans and
+// the C ABI entry points declared in include/tt.h.  Citations as in tt.h.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "tt_internal.h"
+#include "tt_launch.h"
+#include "tt_nccl.h"
+
+using namespace tt;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_uid{1};
+
+tt_status fail(tt_status code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define TT_CUDA(x)                                                                    \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) return fail(TT_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TT_TRY(x)                 \
+  do {                            \
+    tt_status s_ = (x);           \
+    if (s_ != TT_OK) return s_;   \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool active = false;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      cudaSetDevice(dev);
+      active = true;
+    }
+  }
+  ~DeviceGuard() {
+    if (active) cudaSetDevice(prev);
+  }
+};
+
+tt_status need_device(tt_ctx ctx) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  if (ctx->device < 0) return fail(TT_E_STATE, "host-only context (device = -1) cannot run device work");
+  return TT_OK;
+}
+
+template <class T>
+tt_status dev_alloc(tt_ctx ctx, T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) return fail(TT_E_OOM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
+  ctx->dev_allocs.push_back(*p);
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// profiling scope: CUDA events around a launch on the ctx stream
+
+struct Launch {
+  tt_ctx ctx;
+  std::string name;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  Launch(tt_ctx c, const char* n) : ctx(c), name(n) {
+    ctx->launches++;
+    ctx->last.launches++;
+    if (ctx->profiling) {
+      e0 = get_event();
+      e1 = get_event();
+      cudaEventRecord(e0, ctx->stream);
+    }
+  }
+  cudaEvent_t get_event() {
+    if (!ctx->event_pool.empty()) {
+      cudaEvent_t e = ctx->event_pool.back();
+      ctx->event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ~Launch() {
+    if (ctx->profiling) {
+      cudaEventRecord(e1, ctx->stream);
+      ctx->prof.push_back({name, e0, e1});
+    }
+  }
+};
+
+tt_status nccl_check(int r, const char* what) {
+  if (r == 0) return TT_OK;
+  const char* err = nullptr;
+  const NcclApi* api = nccl_api(&err);
+  return fail(TT_E_NCCL, "%s failed: %s", what, api && api->GetErrorString ? api->GetErrorString(r) : "?");
+}
+
+// ---------------------------------------------------------------------------------------------
+// label analysis (P145-174; S356-384, S412-413)
+
+struct Analysis {
+  std::string c, a, b;
+  int nc = 0, nk = 0;
+  std::vector<char> uni;                 // universal labels: C labels, then contracted (A order)
+  std::vector<int> a_lab, b_lab;         // universal label of each A / B dim
+  std::vector<int> a_pos, b_pos, c_pos;  // dim of each universal label in A / B / C (-1)
+  std::vector<std::vector<int>> mg, ng, kg;
+  bool a_kc = true, b_nc = true;
+};
+
+bool same_tiling(tt_tis x, tt_tis y) {
+  return x == y || (x->offsets == y->offsets && x->spin == y->spin);
+}
+
+tt_status check_labels(const char* lbl, tt_tensor t, const char* which) {
+  if (!lbl) return fail(TT_E_ARG, "NULL label string for %s", which);
+  if ((int)strlen(lbl) != t->order)
+    return fail(TT_E_LABEL, "%s: %zu labels for an order-%d tensor", which, strlen(lbl), t->order);
+  for (int i = 0; i < t->order; ++i)
+    for (int j = i + 1; j < t->order; ++j)
+      if (lbl[i] == lbl[j]) return fail(TT_E_LABEL, "%s: repeated label '%c' (S412)", which, lbl[i]);
+  return TT_OK;
+}
+
+tt_status tiling_of(const Analysis& an, char x, tt_tensor C, tt_tensor A, tt_tensor B, tt_tis* out) {
+  tt_tis t = nullptr;
+  auto chk = [&](const std::string& s, tt_tensor T) -> tt_status {
+    size_t p = s.find(x);
+    if (p == std::string::npos || !T) return TT_OK;
+    if (!t) t = T->dims[p];
+    else if (!same_tiling(t, T->dims[p]))
+      return fail(TT_E_TILING, "label '%c' bound to different tiled index spaces (S413)", x);
+    return TT_OK;
+  };
+  TT_TRY(chk(an.c, C));
+  TT_TRY(chk(an.a, A));
+  TT_TRY(chk(an.b, B));
+  *out = t;
+  return TT_OK;
+}
+
+tt_status analyse(tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B, const char* bl,
+                  Analysis& an) {
+  if (!C || !A || !B) return fail(TT_E_ARG, "NULL tensor");
+  TT_TRY(check_labels(cl, C, "C"));
+  TT_TRY(check_labels(al, A, "A"));
+  TT_TRY(check_labels(bl, B, "B"));
+  an.c = cl; an.a = al; an.b = bl;
+  for (char x : an.c) {
+    bool ia = an.a.find(x) != std::string::npos, ib = an.b.find(x) != std::string::npos;
+    if (ia && ib) return fail(TT_E_LABEL, "label '%c' appears in C, A and B (batch label, S380)", x);
+    if (!ia && !ib) return fail(TT_E_LABEL, "C label '%c' appears in neither A nor B", x);
+  }
+  for (char x : an.a)
+    if (an.c.find(x) == std::string::npos && an.b.find(x) == std::string::npos)
+      return fail(TT_E_LABEL, "dangling label '%c' in A (S380)", x);
+  for (char x : an.b)
+    if (an.c.find(x) == std::string::npos && an.a.find(x) == std::string::npos)
+      return fail(TT_E_LABEL, "dangling label '%c' in B (S380)", x);
+  an.nc = (int)an.c.size();
+  an.uni.assign(an.c.begin(), an.c.end());
+  for (char x : an.a)
+    if (an.b.find(x) != std::string::npos && an.c.find(x) == std::string::npos) an.uni.push_back(x);
+  an.nk = (int)an.uni.size() - an.nc;
+  if ((int)an.uni.size() > kMaxLab) return fail(TT_E_UNSUPPORTED, "more than %d labels", kMaxLab);
+  for (char x : an.uni) {
+    tt_tis t;
+    TT_TRY(tiling_of(an, x, C, A, B, &t));
+  }
+  auto uidx = [&](char x) { return (int)(std::find(an.uni.begin(), an.uni.end(), x) - an.uni.begin()); };
+  an.a_lab.clear(); an.b_lab.clear();
+  for (char x : an.a) an.a_lab.push_back(uidx(x));
+  for (char x : an.b) an.b_lab.push_back(uidx(x));
+  int nu = (int)an.uni.size();
+  an.a_pos.assign(nu, -1); an.b_pos.assign(nu, -1); an.c_pos.assign(nu, -1);
+  for (int d = 0; d < (int)an.a.size(); ++d) an.a_pos[an.a_lab[d]] = d;
+  for (int d = 0; d < (int)an.b.size(); ++d) an.b_pos[an.b_lab[d]] = d;
+  for (int d = 0; d < an.nc; ++d) an.c_pos[d] = d;
+  // label fusion: adjacent labels in the same order in every operand holding them
+  an.mg.clear(); an.ng.clear(); an.kg.clear();
+  for (int u = 0; u < an.nc; ++u) {
+    bool fromA = an.a_pos[u] >= 0;
+    auto& G = fromA ? an.mg : an.ng;
+    const auto& pos = fromA ? an.a_pos : an.b_pos;
+    if (!G.empty()) {
+      int v = G.back().back();
+      if (an.c_pos[v] + 1 == an.c_pos[u] && pos[v] >= 0 && pos[v] + 1 == pos[u]) {
+        G.back().push_back(u);
+        continue;
+      }
+    }
+    G.push_back({u});
+  }
+  for (int u = an.nc; u < nu; ++u) {
+    if (!an.kg.empty()) {
+      int v = an.kg.back().back();
+      if (an.a_pos[v] + 1 == an.a_pos[u] && an.b_pos[v] + 1 == an.b_pos[u]) {
+        an.kg.back().push_back(u);
+        continue;
+      }
+    }
+    an.kg.push_back({u});
+  }
+  if (an.mg.size() > (size_t)kMaxGroup || an.ng.size() > (size_t)kMaxGroup || an.kg.size() > (size_t)kMaxGroup)
+    return fail(TT_E_UNSUPPORTED, "more than %d label groups on one GEMM side after fusion", kMaxGroup);
+  an.a_kc = an.a_lab.back() >= an.nc;
+  an.b_nc = an.b_lab.back() < an.nc;
+  return TT_OK;
+}
+
+// tiling of universal label u
+tt_tis label_tis(const Analysis& an, int u, tt_tensor C, tt_tensor A) {
+  if (u < an.nc) return C->dims[u];
+  return A->dims[an.a_pos[u]];
+}
+
+// ---------------------------------------------------------------------------------------------
+// host canonical task list (reading R11)
+
+struct HostTasks {
+  std::vector<int64_t> cblk, ptr, a_blk, b_blk, cost;
+  std::vector<int32_t> K;     // contracted extent per task
+};
+
+void enumerate_tasks(const Analysis& an, tt_tensor C, tt_tensor A, tt_tensor B, HostTasks& ht) {
+  std::vector<tt_tis> lt(an.uni.size());
+  for (size_t u = 0; u < an.uni.size(); ++u) lt[u] = label_tis(an, (int)u, C, A);
+  std::vector<int32_t> kg(an.nk);
+  int64_t ntup = 1;
+  for (int l = 0; l < an.nk; ++l) { kg[l] = lt[an.nc + l]->ntiles(); ntup *= kg[l]; }
+  ht.ptr.assign(1, 0);
+  int32_t cc[TT_MAX_ORDER], kc[kMaxLab], tile[kMaxLab];
+  for (int64_t cb = 0; cb < C->nblocks; ++cb) {
+    if (!C->nz[cb]) continue;
+    C->block_coords(cb, cc);
+    int64_t cext = 1;
+    for (int d = 0; d < an.nc; ++d) { tile[d] = cc[d]; cext *= lt[d]->size(cc[d]); }
+    int64_t cost = 0;
+    for (int64_t t = 0; t < ntup; ++t) {
+      int64_t r = t;
+      for (int l = an.nk - 1; l >= 0; --l) { kc[l] = (int32_t)(r % kg[l]); r /= kg[l]; }
+      for (int l = 0; l < an.nk; ++l) tile[an.nc + l] = kc[l];
+      int64_t aid = 0, bid = 0;
+      for (size_t d = 0; d < an.a_lab.size(); ++d) aid = aid * A->grid[d] + tile[an.a_lab[d]];
+      for (size_t d = 0; d < an.b_lab.size(); ++d) bid = bid * B->grid[d] + tile[an.b_lab[d]];
+      if (A->nz[aid] && B->nz[bid]) {
+        int64_t K = 1;
+        for (int l = 0; l < an.nk; ++l) K *= lt[an.nc + l]->size(kc[l]);
+        ht.a_blk.push_back(aid);
+        ht.b_blk.push_back(bid);
+        ht.K.push_back((int32_t)K);
+        cost += 2 * cext * K;
+      }
+    }
+    ht.cblk.push_back(cb);
+    ht.ptr.push_back((int64_t)ht.a_blk.size());
+    ht.cost.push_back(cost);
+  }
+}
+
+std::vector<int32_t> lpt(const std::vector<int64_t>& cost, const std::vector<int64_t>& ids, int nranks) {
+  std::vector<size_t> order(cost.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+    if (cost[x] != cost[y]) return cost[x] > cost[y];
+    return ids[x] < ids[y];
+  });
+  std::vector<int64_t> load(nranks, 0);
+  std::vector<int32_t> own(cost.size(), 0);
+  for (size_t i : order) {
+    int r = 0;
+    for (int q = 1; q < nranks; ++q)
+      if (load[q] < load[r]) r = q;
+    own[i] = r;
+    load[r] += cost[i];
+  }
+  return own;
+}
+
+// ---------------------------------------------------------------------------------------------
+// gather plan: blocks this rank reads but does not hold (P212)
+
+struct Run {
+  int op;        // 0 = A, 1 = B
+  int peer;
+  int64_t off, len;
+};
+
+struct GatherPlan {
+  std::vector<int64_t> recv_list, send_list;   // (op, block, peer) triples
+  std::vector<Run> recv, send;
+  int64_t recv_bytes = 0;
+};
+
+// need[r] = set of (op, block) rank r reads; identical computation on every rank (SPMD)
+void build_gather(tt_ctx ctx, const std::vector<std::vector<std::pair<int, int64_t>>>& need,
+                  const std::vector<tt_tensor>& ops, GatherPlan& gp) {
+  const int me = ctx->rank, P = ctx->nranks;
+  // blocks per (src, dst), sorted by op then block id (= packed order)
+  for (int dst = 0; dst < P; ++dst) {
+    for (const auto& nb : need[dst]) {
+      tt_tensor T = ops[nb.first];
+      int32_t o = T->owner[nb.second];
+      if (o == TT_REPLICATED || o == dst) continue;
+      if (dst == me) {
+        gp.recv_list.insert(gp.recv_list.end(), {nb.first, nb.second, o});
+      }
+      if (o == me) {
+        gp.send_list.insert(gp.send_list.end(), {nb.first, nb.second, dst});
+      }
+    }
+  }
+  auto runs = [&](const std::vector<int64_t>& lst, std::vector<Run>& out) {
+    // sort by (peer, op, block)
+    std::vector<size_t> idx(lst.size() / 3);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::sort(idx.begin(), idx.end(), [&](size_t x, size_t y) {
+      auto kx = std::make_tuple(lst[3 * x + 2], lst[3 * x], lst[3 * x + 1]);
+      auto ky = std::make_tuple(lst[3 * y + 2], lst[3 * y], lst[3 * y + 1]);
+      return kx < ky;
+    });
+    for (size_t i : idx) {
+      int op = (int)lst[3 * i], peer = (int)lst[3 * i + 2];
+      int64_t b = lst[3 * i + 1];
+      tt_tensor T = ops[op];
+      int64_t off = T->blk_off[b], len = T->block_volume(b);
+      if (!out.empty() && out.back().op == op && out.back().peer == peer) {
+        Run& r = out.back();
+        int64_t gap = off - (r.off + r.len);
+        if (gap >= 0 && gap <= 1) {   // adjacent in packed order (<= 1 alignment pad element)
+          r.len = off + len - r.off;
+          continue;
+        }
+      }
+      out.push_back({op, peer, off, len});
+    }
+  };
+  runs(gp.recv_list, gp.recv);
+  runs(gp.send_list, gp.send);
+  for (const Run& r : gp.recv) gp.recv_bytes += r.len * 8;
+}
+
+tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops) {
+  if (ctx->nranks <= 1 || (gp.recv.empty() && gp.send.empty())) return TT_OK;
+  const char* err = nullptr;
+  const NcclApi* api = nccl_api(&err);
+  if (!api) return fail(TT_E_NCCL, "%s", err);
+  TT_TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+  for (const Run& r : gp.send) {
+    TT_TRY(nccl_check(api->Send(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclSend"));
+  }
+  for (const Run& r : gp.recv) {
+    TT_TRY(nccl_check(api->Recv(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclRecv"));
+  }
+  TT_TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// tensor device metadata
+
+tt_status ensure_dev(tt_tensor t) {
+  if (t->dev_ready) return TT_OK;
+  tt_ctx ctx = t->ctx;
+  TT_TRY(need_device(ctx));
+  TT_TRY(dev_alloc(ctx, &t->d_nz, t->nblocks));
+  TT_TRY(dev_alloc(ctx, &t->d_blk_off, t->nblocks));
+  TT_CUDA(cudaMemcpy(t->d_nz, t->nz.data(), t->nblocks, cudaMemcpyHostToDevice));
+  TT_CUDA(cudaMemcpy(t->d_blk_off, t->blk_off.data(), t->nblocks * 8, cudaMemcpyHostToDevice));
+  t->d_toff.assign(t->order, nullptr);
+  for (int d = 0; d < t->order; ++d) {
+    TT_TRY(dev_alloc(ctx, &t->d_toff[d], t->dims[d]->offsets.size()));
+    TT_CUDA(cudaMemcpy(t->d_toff[d], t->dims[d]->offsets.data(), t->dims[d]->offsets.size() * 8, cudaMemcpyHostToDevice));
+  }
+  t->dev_ready = true;
+  return TT_OK;
+}
+
+tt_status check_bound(tt_tensor t, const char* which) {
+  if (!t->data) return fail(TT_E_UNBOUND, "tensor %s has no storage bound (S208)", which);
+  if (t->capacity < t->packed_elems)
+    return fail(TT_E_UNBOUND, "tensor %s: bound capacity %lld < packed size %lld", which, (long long)t->capacity,
+                (long long)t->packed_elems);
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// contraction plan (cached per (tensors, owner versions, labels))
+
+struct ContractPlan {
+  Analysis an;
+  HostTasks ht;
+  std::vector<int> my;             // indices into ht.cblk computed by this rank
+  GatherPlan gp;
+  int variant = 0;
+  int64_t nwork = 0;
+  CGroupDesc* d_groups = nullptr;
+  TaskDesc* d_tasks = nullptr;
+  WorkItem* d_work = nullptr;
+  int64_t* d_ablk = nullptr;
+  int64_t* d_bblk = nullptr;
+  int64_t* d_ptr = nullptr;
+  bool device_built = false;
+  double flops = 0, bytes = 0;
+  int64_t tasks = 0;
+};
+
+std::string plan_key(const char* kind, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
+                     const char* bl, double beta) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s|%llu.%llu|%llu.%llu|%llu.%llu|%s|%s|%s|%d", kind, (unsigned long long)C->uid,
+           (unsigned long long)C->version, (unsigned long long)A->uid, (unsigned long long)A->version,
+           (unsigned long long)(B ? B->uid : 0), (unsigned long long)(B ? B->version : 0), cl, al, bl ? bl : "",
+           beta != 0.0);
+  return buf;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+
+extern "C" {
+
+const char* tt_last_error(void) { return g_err.c_str(); }
+int32_t tt_version(void) { return 1; }
+
+tt_status tt_nccl_unique_id(void* out128) {
+  if (!out128) return fail(TT_E_ARG, "NULL output");
+  const char* err = nullptr;
+  const NcclApi* api = nccl_api(&err);
+  if (!api) return fail(TT_E_NCCL, "%s", err);
+  return nccl_check(api->GetUniqueId(out128), "ncclGetUniqueId");
+}
+
+tt_status tt_ctx_create(int32_t device, void* stream, int32_t rank, int32_t nranks, const void* nccl_id, tt_ctx* out) {
+  if (!out) return fail(TT_E_ARG, "NULL output handle");
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(TT_E_ARG, "bad rank %d / nranks %d", rank, nranks);
+  tt_ctx c = new tt_ctx_s();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  c->rank = rank;
+  c->nranks = nranks;
+  if (device >= 0) {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || device >= ndev) {
+      delete c;
+      return fail(TT_E_CUDA, "device %d not available: %s", device, cudaGetErrorString(e));
+    }
+    DeviceGuard dg(device);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
+    if (prop.major != 10) {
+      delete c;
+      return fail(TT_E_UNSUPPORTED, "libtt is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
+    }
+    for (int v = 0; v < num_contract_variants(); ++v) {
+      cudaError_t e2 = contract_variant_setup(v);
+      if (e2 != cudaSuccess) {
+        delete c;
+        return fail(TT_E_CUDA, "kernel setup: %s", cudaGetErrorString(e2));
+      }
+    }
+    if (nranks > 1) {
+      if (!nccl_id) {
+        delete c;
+        return fail(TT_E_ARG, "nranks > 1 needs an ncclUniqueId");
+      }
+      const char* err = nullptr;
+      const NcclApi* api = nccl_api(&err);
+      if (!api) {
+        delete c;
+        return fail(TT_E_NCCL, "%s", err);
+      }
+      int r = nccl_comm_init(api, &c->comm, nranks, nccl_id, rank);
+      if (r != 0) {
+        delete c;
+        return fail(TT_E_NCCL, "ncclCommInitRank: %s", api->GetErrorString(r));
+      }
+    }
+    tt_status s = dev_alloc(c, &c->d_scalar, 2);
+    if (s != TT_OK) { delete c; return s; }
+  }
+  *out = c;
+  return TT_OK;
+}
+
+tt_status tt_ctx_destroy(tt_ctx ctx) {
+  if (!ctx) return TT_OK;
+  DeviceGuard dg(ctx->device);
+  if (ctx->device >= 0) cudaStreamSynchronize(ctx->stream);
+  ctx->plans.clear();
+  for (void* p : ctx->dev_allocs) cudaFree(p);
+  for (auto& r : ctx->prof) { ctx->event_pool.push_back(r.e0); ctx->event_pool.push_back(r.e1); }
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->comm) {
+    const NcclApi* api = nccl_api(nullptr);
+    if (api) api->CommDestroy(ctx->comm);
+  }
+  delete ctx;
+  return TT_OK;
+}
+
+tt_status tt_ctx_set_profiling(tt_ctx ctx, int32_t enable) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  ctx->profiling = enable != 0;
+  return TT_OK;
+}
+
+tt_status tt_profile_read(tt_ctx ctx, const char* kernel, double* total_ms, int64_t* launches) {
+  if (!ctx || !total_ms || !launches) return fail(TT_E_ARG, "NULL argument");
+  *total_ms = 0;
+  *launches = 0;
+  if (ctx->device < 0) return TT_OK;
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& r : ctx->prof) {
+    if (kernel && kernel[0] && r.name.find(kernel) == std::string::npos) continue;
+    float ms = 0;
+    TT_CUDA(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    *total_ms += ms;
+    *launches += 1;
+  }
+  return TT_OK;
+}
+
+tt_status tt_profile_reset(tt_ctx ctx) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  for (auto& r : ctx->prof) { ctx->event_pool.push_back(r.e0); ctx->event_pool.push_back(r.e1); }
+  ctx->prof.clear();
+  return TT_OK;
+}
+
+tt_status tt_last_stats(tt_ctx ctx, tt_stats* out) {
+  if (!ctx || !out) return fail(TT_E_ARG, "NULL argument");
+  *out = ctx->last;
+  return TT_OK;
+}
+
+tt_status tt_launch_count(tt_ctx ctx, int64_t* out) {
+  if (!ctx || !out) return fail(TT_E_ARG, "NULL argument");
+  *out = ctx->launches;
+  return TT_OK;
+}
+
+tt_status tt_sync(tt_ctx ctx) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  if (ctx->device < 0) return TT_OK;
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(cudaStreamSynchronize(ctx->stream));
+  TT_CUDA(cudaGetLastError());
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// index spaces and tilings
+
+tt_status tt_is_create(int64_t extent, int32_t n_ranges, const int64_t* be, const int8_t* spin, tt_is* out) {
+  if (!out) return fail(TT_E_ARG, "NULL output handle");
+  *out = nullptr;
+  if (extent < 1) return fail(TT_E_ARG, "extent must be >= 1");
+  if (n_ranges < 0 || (n_ranges > 0 && !be)) return fail(TT_E_ARG, "bad ranges");
+  tt_is s = new tt_is_s();
+  s->extent = extent;
+  int64_t pos = 0;
+  for (int i = 0; i < n_ranges; ++i) {
+    int64_t b = be[2 * i], e = be[2 * i + 1];
+    if (b != pos || e <= b) {
+      delete s;
+      return fail(TT_E_COVERAGE, "ranges must be ascending, non-empty and cover [0, extent)");
+    }
+    if (spin && spin[i] != 1 && spin[i] != -1) {
+      delete s;
+      return fail(TT_E_ARG, "spin must be +1 or -1");
+    }
+    s->rb.push_back(b);
+    s->re.push_back(e);
+    s->rspin.push_back(spin ? spin[i] : 0);
+    pos = e;
+  }
+  if (n_ranges > 0 && pos != extent) {
+    delete s;
+    return fail(TT_E_COVERAGE, "ranges must cover [0, extent)");
+  }
+  if (n_ranges == 0) {
+    s->rb.push_back(0);
+    s->re.push_back(extent);
+    s->rspin.push_back(0);
+  }
+  *out = s;
+  return TT_OK;
+}
+
+tt_status tt_is_destroy(tt_is is) {
+  delete is;
+  return TT_OK;
+}
+
+tt_status tt_tis_fixed(tt_is is, int64_t tile, tt_tis* out) {
+  if (!is || !out) return fail(TT_E_ARG, "NULL argument");
+  *out = nullptr;
+  if (tile < 1) return fail(TT_E_ARG, "tile size must be >= 1");
+  tt_tis t = new tt_tis_s();
+  t->is = is;
+  t->uid = g_uid++;
+  t->offsets.push_back(0);
+  for (size_t r = 0; r < is->rb.size(); ++r) {
+    for (int64_t p = is->rb[r]; p < is->re[r]; p += tile) {
+      t->offsets.push_back(std::min(p + tile, is->re[r]));
+      t->spin.push_back(is->rspin[r]);
+    }
+  }
+  *out = t;
+  return TT_OK;
+}
+
+tt_status tt_tis_custom(tt_is is, int32_t n, const int64_t* sizes, tt_tis* out) {
+  if (!is || !out || (n > 0 && !sizes)) return fail(TT_E_ARG, "NULL argument");
+  *out = nullptr;
+  if (n < 1) return fail(TT_E_ARG, "need at least one tile");
+  int64_t sum = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sizes[i] < 1) return fail(TT_E_ARG, "tile size must be >= 1");
+    sum += sizes[i];
+  }
+  if (sum != is->extent) return fail(TT_E_COVERAGE, "tile sizes sum to %lld, extent is %lld (P127)", (long long)sum, (long long)is->extent);
+  tt_tis t = new tt_tis_s();
+  t->is = is;
+  t->uid = g_uid++;
+  t->offsets.push_back(0);
+  for (int i = 0; i < n; ++i) {
+    int64_t lo = t->offsets.back(), hi = lo + sizes[i];
+    int found = -1;
+    for (size_t r = 0; r < is->rb.size(); ++r)
+      if (is->rb[r] <= lo && hi <= is->re[r]) found = (int)r;
+    if (found < 0) {
+      delete t;
+      return fail(TT_E_TILING, "tile [%lld,%lld) straddles a range/spin boundary (S39)", (long long)lo, (long long)hi);
+    }
+    t->offsets.push_back(hi);
+    t->spin.push_back(is->rspin[found]);
+  }
+  *out = t;
+  return TT_OK;
+}
+
+tt_status tt_tis_info(tt_tis tis, int32_t* ntiles, const int64_t** offsets, const int8_t** tile_spin) {
+  if (!tis) return fail(TT_E_ARG, "NULL handle");
+  if (ntiles) *ntiles = tis->ntiles();
+  if (offsets) *offsets = tis->offsets.data();
+  if (tile_spin) *tile_spin = tis->spin.data();
+  return TT_OK;
+}
+
+tt_status tt_tis_destroy(tt_tis tis) {
+  delete tis;
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// tensors
+
+static tt_status tensor_new(tt_ctx ctx, int32_t order, const tt_tis* dims, tt_tensor* out) {
+  if (!ctx || !out || !dims) return fail(TT_E_ARG, "NULL argument");
+  *out = nullptr;
+  if (order < 1 || order > TT_MAX_ORDER) return fail(TT_E_UNSUPPORTED, "order %d outside 1..%d", order, TT_MAX_ORDER);
+  tt_tensor t = new tt_tensor_s();
+  t->ctx = ctx;
+  t->order = order;
+  t->uid = g_uid++;
+  t->nblocks = 1;
+  for (int d = 0; d < order; ++d) {
+    if (!dims[d]) {
+      delete t;
+      return fail(TT_E_ARG, "NULL tiled index space for dim %d", d);
+    }
+    t->dims.push_back(dims[d]);
+    t->grid.push_back(dims[d]->ntiles());
+    t->nblocks *= dims[d]->ntiles();
+  }
+  *out = t;
+  return TT_OK;
+}
+
+static void tensor_finish(tt_tensor t) {
+  // P210 third scheme: packed non-zero blocks, row-major block order, 16-B aligned starts (R10);
+  // default owners round robin over the non-zero blocks.
+  t->blk_off.assign(t->nblocks, -1);
+  t->owner.assign(t->nblocks, -1);
+  int64_t cur = 0, k = 0;
+  t->nnz = 0;
+  for (int64_t b = 0; b < t->nblocks; ++b) {
+    if (!t->nz[b]) continue;
+    cur = (cur + 1) / 2 * 2;
+    t->blk_off[b] = cur;
+    cur += t->block_volume(b);
+    t->owner[b] = (int32_t)(k++ % t->ctx->nranks);
+    t->nnz++;
+  }
+  t->packed_elems = (cur + 1) / 2 * 2;
+}
+
+tt_status tt_tensor_create(tt_ctx ctx, int32_t order, const tt_tis* dims, const uint8_t* nz, tt_tensor* out) {
+  tt_tensor t;
+  TT_TRY(tensor_new(ctx, order, dims, &t));
+  t->nz.resize(t->nblocks);
+  for (int64_t b = 0; b < t->nblocks; ++b) t->nz[b] = nz ? (nz[b] ? 1 : 0) : 1;
+  tensor_finish(t);
+  *out = t;
+  return TT_OK;
+}
+
+tt_status tt_tensor_create_spin(tt_ctx ctx, int32_t order, const tt_tis* dims, uint32_t upper, uint32_t lower,
+                                tt_tensor* out) {
+  tt_tensor t;
+  TT_TRY(tensor_new(ctx, order, dims, &t));
+  if ((upper | lower) >> order) {
+    delete t;
+    return fail(TT_E_ARG, "spin masks reference dims beyond the order");
+  }
+  t->nz.resize(t->nblocks);
+  int32_t c[TT_MAX_ORDER];
+  for (int64_t b = 0; b < t->nblocks; ++b) {
+    t->block_coords(b, c);
+    int su = 0, sl = 0;
+    for (int d = 0; d < order; ++d) {
+      int s = t->dims[d]->spin[c[d]];
+      if (upper >> d & 1) su += s;
+      if (lower >> d & 1) sl += s;
+    }
+    t->nz[b] = (su == sl) ? 1 : 0;   // P138 spin block sparsity, reading R7
+  }
+  tensor_finish(t);
+  *out = t;
+  return TT_OK;
+}
+
+tt_status tt_tensor_info(tt_tensor t, int32_t* order, int64_t* nblocks, int64_t* nnz) {
+  if (!t) return fail(TT_E_ARG, "NULL tensor");
+  if (order) *order = t->order;
+  if (nblocks) *nblocks = t->nblocks;
+  if (nnz) *nnz = t->nnz;
+  return TT_OK;
+}
+
+tt_status tt_tensor_layout(tt_tensor t, int64_t* packed, const int64_t** blk_off, const int32_t** owner,
+                           const uint8_t** nz) {
+  if (!t) return fail(TT_E_ARG, "NULL tensor");
+  if (packed) *packed = t->packed_elems;
+  if (blk_off) *blk_off = t->blk_off.data();
+  if (owner) *owner = t->owner.data();
+  if (nz) *nz = t->nz.data();
+  return TT_OK;
+}
+
+tt_status tt_tensor_set_owner(tt_tensor t, const int32_t* owner) {
+  if (!t || !owner) return fail(TT_E_ARG, "NULL argument");
+  for (int64_t b = 0; b < t->nblocks; ++b) {
+    if (!t->nz[b]) continue;
+    if (owner[b] != TT_REPLICATED && (owner[b] < 0 || owner[b] >= t->ctx->nranks))
+      return fail(TT_E_ARG, "owner[%lld] = %d out of range", (long long)b, owner[b]);
+  }
+  for (int64_t b = 0; b < t->nblocks; ++b) t->owner[b] = t->nz[b] ? owner[b] : -1;
+  t->version++;
+  return TT_OK;
+}
+
+tt_status tt_tensor_bind(tt_tensor t, void* ptr, int64_t cap) {
+  if (!t) return fail(TT_E_ARG, "NULL tensor");
+  if (ptr && ((uintptr_t)ptr % 16) != 0) return fail(TT_E_ARG, "storage must be 16-byte aligned");
+  if (ptr && cap < t->packed_elems)
+    return fail(TT_E_UNBOUND, "capacity %lld < packed size %lld", (long long)cap, (long long)t->packed_elems);
+  t->data = (double*)ptr;
+  t->capacity = cap;
+  return TT_OK;
+}
+
+tt_status tt_tensor_upload(tt_ctx ctx, tt_tensor t, const double* host) {
+  TT_TRY(need_device(ctx));
+  if (!t || !host) return fail(TT_E_ARG, "NULL argument");
+  TT_TRY(check_bound(t, "upload"));
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(cudaMemcpyAsync(t->data, host, t->packed_elems * 8, cudaMemcpyHostToDevice, ctx->stream));
+  return TT_OK;
+}
+
+tt_status tt_tensor_download(tt_ctx ctx, tt_tensor t, double* host) {
+  TT_TRY(need_device(ctx));
+  if (!t || !host) return fail(TT_E_ARG, "NULL argument");
+  TT_TRY(check_bound(t, "download"));
+  DeviceGuard dg(ctx->device);
+  TT_CUDA(cudaMemcpyAsync(host, t->data, t->packed_elems * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  return TT_OK;
+}
+
+tt_status tt_tensor_destroy(tt_tensor t) {
+  // device metadata is owned by the context allocation list (freed by tt_ctx_destroy)
+  delete t;
+  return TT_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// element operations (set / add / fill / scalar): segment lists built on the host
+
+namespace {
+
+constexpr int64_t kSegElems = 1 << 15;
+
+struct ElemPlan {
+  std::vector<ElemDesc> descs;
+  std::vector<Segment> segs;
+  ElemDesc* d_descs = nullptr;
+  Segment* d_segs = nullptr;
+  double* d_partials = nullptr;
+  GatherPlan gp;
+  double bytes = 0;
+  int64_t blocks = 0;
+};
+
+void add_segments(ElemPlan& ep, int32_t desc, int64_t vol) {
+  for (int64_t e = 0; e < vol; e += kSegElems) ep.segs.push_back({desc, 0, e, std::min(vol, e + kSegElems)});
+}
+
+tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
+  TT_TRY(dev_alloc(ctx, &ep.d_descs, ep.descs.size()));
+  TT_TRY(dev_alloc(ctx, &ep.d_segs, ep.segs.size()));
+  if (!ep.descs.empty()) TT_CUDA(cudaMemcpy(ep.d_descs, ep.descs.data(), ep.descs.size() * sizeof(ElemDesc), cudaMemcpyHostToDevice));
+  if (!ep.segs.empty()) TT_CUDA(cudaMemcpy(ep.d_segs, ep.segs.data(), ep.segs.size() * sizeof(Segment), cudaMemcpyHostToDevice));
+  if (partials) TT_TRY(dev_alloc(ctx, &ep.d_partials, ep.segs.size()));
+  return TT_OK;
+}
+
+template <class P>
+std::shared_ptr<P> cached(tt_ctx ctx, const std::string& key) {
+  auto it = ctx->plans.find(key);
+  if (it == ctx->plans.end()) return nullptr;
+  return std::static_pointer_cast<P>(it->second);
+}
+
+void reset_stats(tt_ctx ctx) { ctx->last = tt_stats{}; }
+
+}  // namespace
+
+extern "C" {
+
+tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag, int32_t kind) {
+  TT_TRY(need_device(ctx));
+  if (!t) return fail(TT_E_ARG, "NULL tensor");
+  if (kind != TT_KIND_UNIFORM && kind != TT_KIND_INTEGER) return fail(TT_E_ARG, "bad kind %d", kind);
+  TT_TRY(check_bound(t, "fill"));
+  DeviceGuard dg(ctx->device);
+  char keybuf[128];
+  snprintf(keybuf, sizeof(keybuf), "fill|%llu.%llu", (unsigned long long)t->uid, (unsigned long long)t->version);
+  auto ep = cached<ElemPlan>(ctx, keybuf);
+  if (!ep) {
+    ep = std::make_shared<ElemPlan>();
+    std::vector<int64_t> gstr(t->order);
+    int64_t acc = 1;
+    for (int d = t->order - 1; d >= 0; --d) { gstr[d] = acc; acc *= t->dims[d]->is->extent; }
+    int32_t c[TT_MAX_ORDER];
+    for (int64_t b = 0; b < t->nblocks; ++b) {
+      if (!t->held(b, ctx->rank)) continue;
+      t->block_coords(b, c);
+      ElemDesc d{};
+      d.x_off = t->blk_off[b];
+      d.y_off = -1;
+      d.g_origin = 0;
+      for (int q = 0; q < t->order; ++q) {
+        d.ext[q] = (int32_t)t->dims[q]->size(c[q]);
+        d.g_str[q] = gstr[q];
+        d.g_origin += t->dims[q]->offsets[c[q]] * gstr[q];
+      }
+      ep->descs.push_back(d);
+      add_segments(*ep, (int32_t)ep->descs.size() - 1, t->block_volume(b));
+    }
+    TT_TRY(upload_elem(ctx, *ep, false));
+    ctx->plans[keybuf] = ep;
+  }
+  reset_stats(ctx);
+  ElemParams p{};
+  p.X = t->data;
+  p.descs = ep->d_descs;
+  p.segs = ep->d_segs;
+  p.order = t->order;
+  p.key = seed ^ ((uint64_t)tag * 0x9E3779B97F4A7C15ull);
+  p.kind = kind;
+  {
+    Launch L(ctx, "tt_fill_synthetic");
+    TT_CUDA(launch_fill(p, (int64_t)ep->segs.size(), ctx->stream));
+  }
+  return TT_OK;
+}
+
+tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha) {
+  TT_TRY(need_device(ctx));
+  if (!C) return fail(TT_E_ARG, "NULL tensor");
+  TT_TRY(check_bound(C, "C"));
+  DeviceGuard dg(ctx->device);
+  char keybuf[128];
+  snprintf(keybuf, sizeof(keybuf), "set|%llu.%llu", (unsigned long long)C->uid, (unsigned long long)C->version);
+  auto ep = cached<ElemPlan>(ctx, keybuf);
+  if (!ep) {
+    ep = std::make_shared<ElemPlan>();
+    for (int64_t b = 0; b < C->nblocks; ++b) {
+      if (!C->held(b, ctx->rank)) continue;
+      ElemDesc d{};
+      d.x_off = C->blk_off[b];
+      d.y_off = -1;
+      ep->descs.push_back(d);
+      add_segments(*ep, (int32_t)ep->descs.size() - 1, C->block_volume(b));
+      ep->bytes += 8.0 * C->block_volume(b);
+      ep->blocks++;
+    }
+    TT_TRY(upload_elem(ctx, *ep, false));
+    ctx->plans[keybuf] = ep;
+  }
+  reset_stats(ctx);
+  ElemParams p{};
+  p.X = C->data;
+  p.descs = ep->d_descs;
+  p.segs = ep->d_segs;
+  p.alpha = alpha;
+  {
+    Launch L(ctx, "tt_set");
+    TT_CUDA(launch_set(p, (int64_t)ep->segs.size(), ctx->stream));
+  }
+  ctx->last.c_blocks = ep->blocks;
+  ctx->last.bytes = ep->bytes;
+  return TT_OK;
+}
+
+tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor A, const char* al) {
+  if (!ctx || !C || !A) return fail(TT_E_ARG, "NULL argument");
+  TT_TRY(check_labels(cl, C, "C"));
+  TT_TRY(check_labels(al, A, "A"));
+  if (C == A) return fail(TT_E_ARG, "C and A must be different tensors");
+  std::string c(cl), a(al);
+  if (c.size() != a.size()) return fail(TT_E_LABEL, "add needs the same labels on both sides (P173)");
+  std::vector<int> perm(c.size());   // C dim d holds the label of A dim perm[d]
+  for (size_t d = 0; d < c.size(); ++d) {
+    size_t p = a.find(c[d]);
+    if (p == std::string::npos) return fail(TT_E_LABEL, "label '%c' of C missing in A (P173)", c[d]);
+    if (!same_tiling(C->dims[d], A->dims[p])) return fail(TT_E_TILING, "label '%c' on different tilings (S413)", c[d]);
+    perm[d] = (int)p;
+  }
+  TT_TRY(need_device(ctx));
+  TT_TRY(check_bound(C, "C"));
+  TT_TRY(check_bound(A, "A"));
+  DeviceGuard dg(ctx->device);
+  std::string key = plan_key("add", C, cl, A, al, nullptr, nullptr, beta);
+  auto ep = cached<ElemPlan>(ctx, key);
+  if (!ep) {
+    ep = std::make_shared<ElemPlan>();
+    std::vector<std::vector<std::pair<int, int64_t>>> need(ctx->nranks);
+    int32_t cc[TT_MAX_ORDER], ac[TT_MAX_ORDER];
+    for (int64_t b = 0; b < C->nblocks; ++b) {
+      if (!C->nz[b]) continue;
+      C->block_coords(b, cc);
+      for (int d = 0; d < C->order; ++d) ac[perm[d]] = cc[d];
+      int64_t ab = A->block_id(ac);
+      for (int r = 0; r < ctx->nranks; ++r)
+        if (C->held(b, r) && A->nz[ab]) need[r].push_back({0, ab});
+      if (!C->held(b, ctx->rank)) continue;
+      ElemDesc d{};
+      d.x_off = C->blk_off[b];
+      d.y_off = A->nz[ab] ? A->blk_off[ab] : -1;
+      // strides of the A block, by A dim
+      int64_t sa[TT_MAX_ORDER], acc = 1;
+      for (int q = A->order - 1; q >= 0; --q) { sa[q] = acc; acc *= A->dims[q]->size(ac[q]); }
+      for (int q = 0; q < C->order; ++q) {
+        d.ext[q] = (int32_t)C->dims[q]->size(cc[q]);
+        d.y_str[q] = (int32_t)sa[perm[q]];
+      }
+      ep->descs.push_back(d);
+      add_segments(*ep, (int32_t)ep->descs.size() - 1, C->block_volume(b));
+      ep->bytes += 8.0 * C->block_volume(b) * ((beta != 0.0) + 1 + (A->nz[ab] ? 1 : 0));
+      ep->blocks++;
+    }
+    for (auto& v : need) { std::sort(v.begin(), v.end()); v.erase(std::unique(v.begin(), v.end()), v.end()); }
+    build_gather(ctx, need, {A}, ep->gp);
+    TT_TRY(upload_elem(ctx, *ep, false));
+    ctx->plans[key] = ep;
+  }
+  reset_stats(ctx);
+  TT_TRY(run_gather(ctx, ep->gp, {A}));
+  ElemParams p{};
+  p.X = C->data;
+  p.Y = A->data;
+  p.descs = ep->d_descs;
+  p.segs = ep->d_segs;
+  p.order = C->order;
+  p.alpha = alpha;
+  p.beta = beta;
+  {
+    Launch L(ctx, "tt_add");
+    TT_CUDA(launch_add(p, (int64_t)ep->segs.size(), ctx->stream));
+  }
+  ctx->last.c_blocks = ep->blocks;
+  ctx->last.bytes = ep->bytes;
+  ctx->last.gathered_bytes = ep->gp.recv_bytes;
+  return TT_OK;
+}
+
+tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* al, tt_tensor B, const char* bl,
+                             double* result) {
+  if (!ctx || !A || !B || !result) return fail(TT_E_ARG, "NULL argument");
+  TT_TRY(check_labels(al, A, "A"));
+  TT_TRY(check_labels(bl, B, "B"));
+  std::string a(al), b(bl);
+  if (a.size() != b.size()) return fail(TT_E_LABEL, "scalar contraction needs the same label set in A and B");
+  std::vector<int> perm(a.size());   // A dim d holds the label of B dim perm[d]
+  for (size_t d = 0; d < a.size(); ++d) {
+    size_t p = b.find(a[d]);
+    if (p == std::string::npos) return fail(TT_E_LABEL, "label '%c' of A missing in B", a[d]);
+    if (!same_tiling(A->dims[d], B->dims[p])) return fail(TT_E_TILING, "label '%c' on different tilings (S413)", a[d]);
+    perm[d] = (int)p;
+  }
+  TT_TRY(need_device(ctx));
+  TT_TRY(check_bound(A, "A"));
+  TT_TRY(check_bound(B, "B"));
+  DeviceGuard dg(ctx->device);
+  std::string key = plan_key("scalar", A, al, B, bl, nullptr, nullptr, 0.0);
+  auto ep = cached<ElemPlan>(ctx, key);
+  if (!ep) {
+    ep = std::make_shared<ElemPlan>();
+    std::vector<std::vector<std::pair<int, int64_t>>> need(ctx->nranks);
+    int32_t ac[TT_MAX_ORDER], bc[TT_MAX_ORDER];
+    for (int64_t blk = 0; blk < A->nblocks; ++blk) {
+      if (!A->nz[blk]) continue;
+      A->block_coords(blk, ac);
+      for (int d = 0; d < A->order; ++d) bc[perm[d]] = ac[d];
+      int64_t bb = B->block_id(bc);
+      if (!B->nz[bb]) continue;
+      // the rank that sums this pair: A's owner (replicated A blocks: rank 0)
+      int32_t r = A->owner[blk] == TT_REPLICATED ? 0 : A->owner[blk];
+      need[r].push_back({1, bb});
+      if (r != ctx->rank) continue;
+      ElemDesc d{};
+      d.x_off = A->blk_off[blk];
+      d.y_off = B->blk_off[bb];
+      int64_t sb[TT_MAX_ORDER], acc = 1;
+      for (int q = B->order - 1; q >= 0; --q) { sb[q] = acc; acc *= B->dims[q]->size(bc[q]); }
+      for (int q = 0; q < A->order; ++q) {
+        d.ext[q] = (int32_t)A->dims[q]->size(ac[q]);
+        d.y_str[q] = (int32_t)sb[perm[q]];
+      }
+      ep->descs.push_back(d);
+      add_segments(*ep, (int32_t)ep->descs.size() - 1, A->block_volume(blk));
+      ep->bytes += 16.0 * A->block_volume(blk);
+      ep->blocks++;
+    }
+    for (auto& v : need) { std::sort(v.begin(), v.end()); v.erase(std::unique(v.begin(), v.end()), v.end()); }
+    build_gather(ctx, need, {A, B}, ep->gp);
+    TT_TRY(upload_elem(ctx, *ep, true));
+    ctx->plans[key] = ep;
+  }
+  reset_stats(ctx);
+  TT_TRY(run_gather(ctx, ep->gp, {A, B}));
+  ElemParams p{};
+  p.X = A->data;
+  p.Y = B->data;
+  p.descs = ep->d_descs;
+  p.segs = ep->d_segs;
+  p.order = A->order;
+  p.partials = ep->d_partials;
+  {
+    Launch L(ctx, "tt_scalar_partials");
+    TT_CUDA(launch_scalar_partials(p, (int64_t)ep->segs.size(), ctx->stream));
+  }
+  {
+    Launch L(ctx, "tt_scalar_final");
+    TT_CUDA(launch_scalar_final(ep->d_partials, (int64_t)ep->segs.size(), alpha, ctx->d_scalar, ctx->stream));
+  }
+  if (ctx->nranks > 1) {
+    const char* err = nullptr;
+    const NcclApi* api = nccl_api(&err);
+    if (!api) return fail(TT_E_NCCL, "%s", err);
+    TT_TRY(nccl_check(api->AllReduce(ctx->d_scalar, ctx->d_scalar, 1, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream),
+                      "ncclAllReduce"));
+  }
+  TT_CUDA(cudaMemcpyAsync(result, ctx->d_scalar, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->last.c_blocks = ep->blocks;
+  ctx->last.bytes = ep->bytes;
+  ctx->last.flops = ep->bytes / 8.0;   // one multiply-add per element pair
+  ctx->last.gathered_bytes = ep->gp.recv_bytes;
+  return TT_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// contraction
+
+namespace {
+
+tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B, double beta, ContractPlan& pl) {
+  const Analysis& an = pl.an;
+  enumerate_tasks(an, C, A, B, pl.ht);
+  const HostTasks& ht = pl.ht;
+  std::vector<tt_tis> lt(an.uni.size());
+  for (size_t u = 0; u < an.uni.size(); ++u) lt[u] = label_tis(an, (int)u, C, A);
+  // blocks computed per rank; inputs read per rank
+  std::vector<std::vector<std::pair<int, int64_t>>> need(ctx->nranks);
+  for (size_t g = 0; g < ht.cblk.size(); ++g) {
+    for (int r = 0; r < ctx->nranks; ++r) {
+      if (!C->held(ht.cblk[g], r)) continue;
+      for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
+        need[r].push_back({0, ht.a_blk[t]});
+        need[r].push_back({1, ht.b_blk[t]});
+      }
+    }
+    if (C->held(ht.cblk[g], ctx->rank)) pl.my.push_back((int)g);
+  }
+  for (auto& v : need) { std::sort(v.begin(), v.end()); v.erase(std::unique(v.begin(), v.end()), v.end()); }
+  // A and B may be the same tensor: then both operands index the same storage
+  build_gather(ctx, need, {A, B}, pl.gp);
+  if (A == B) {
+    // drop duplicate B entries that refer to the same block as an A entry
+    GatherPlan gp2;
+    std::vector<std::vector<std::pair<int, int64_t>>> need2(ctx->nranks);
+    for (int r = 0; r < ctx->nranks; ++r) {
+      for (auto& x : need[r]) need2[r].push_back({0, x.second});
+      std::sort(need2[r].begin(), need2[r].end());
+      need2[r].erase(std::unique(need2[r].begin(), need2[r].end()), need2[r].end());
+    }
+    build_gather(ctx, need2, {A}, gp2);
+    pl.gp = gp2;
+  }
+  // stats for this rank
+  {
+    std::vector<char> ua(A->nblocks, 0), ub(B->nblocks, 0);
+    for (int g : pl.my) {
+      pl.flops += (double)ht.cost[g];
+      pl.tasks += ht.ptr[g + 1] - ht.ptr[g];
+      pl.bytes += 8.0 * C->block_volume(ht.cblk[g]) * (1 + (beta != 0.0));
+      for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
+        if (!ua[ht.a_blk[t]]) { ua[ht.a_blk[t]] = 1; pl.bytes += 8.0 * A->block_volume(ht.a_blk[t]); }
+        if (!ub[ht.b_blk[t]]) { ub[ht.b_blk[t]] = 1; pl.bytes += 8.0 * B->block_volume(ht.b_blk[t]); }
+      }
+    }
+  }
+  if (ctx->device < 0) return TT_OK;
+
+  // ---- device task-list builder (count -> scan -> fill)
+  TT_TRY(ensure_dev(C));
+  TT_TRY(ensure_dev(A));
+  TT_TRY(ensure_dev(B));
+  const int64_t ncb = (int64_t)ht.cblk.size(), ntasks = (int64_t)ht.a_blk.size();
+  int64_t *d_cblocks, *d_counts;
+  TT_TRY(dev_alloc(ctx, &d_cblocks, ncb));
+  TT_TRY(dev_alloc(ctx, &d_counts, ncb));
+  TT_TRY(dev_alloc(ctx, &pl.d_ptr, ncb + 1));
+  TT_TRY(dev_alloc(ctx, &pl.d_ablk, ntasks));
+  TT_TRY(dev_alloc(ctx, &pl.d_bblk, ntasks));
+  TT_TRY(dev_alloc(ctx, &pl.d_tasks, ntasks));
+  TT_CUDA(cudaMemcpy(d_cblocks, ht.cblk.data(), ncb * 8, cudaMemcpyHostToDevice));
+  BuildParams bp{};
+  bp.nc = an.nc;
+  bp.nk = an.nk;
+  for (int d = 0; d < an.nc; ++d) bp.c_grid[d] = C->grid[d];
+  bp.ntuples = 1;
+  for (int l = 0; l < an.nk; ++l) { bp.k_grid[l] = lt[an.nc + l]->ntiles(); bp.ntuples *= bp.k_grid[l]; }
+  bp.a_order = A->order;
+  bp.b_order = B->order;
+  for (int d = 0; d < A->order; ++d) { bp.a_lab[d] = an.a_lab[d]; bp.a_grid[d] = A->grid[d]; }
+  for (int d = 0; d < B->order; ++d) { bp.b_lab[d] = an.b_lab[d]; bp.b_grid[d] = B->grid[d]; }
+  for (size_t u = 0; u < an.uni.size(); ++u) {
+    bp.a_pos[u] = an.a_pos[u];
+    bp.b_pos[u] = an.b_pos[u];
+    bp.lab_toff[u] = (int)u < an.nc ? C->d_toff[u] : A->d_toff[an.a_pos[u]];
+  }
+  bp.a_nz = A->d_nz;
+  bp.b_nz = B->d_nz;
+  bp.a_boff = A->d_blk_off;
+  bp.b_boff = B->d_blk_off;
+  int nl = 0;
+  auto put = [&](const std::vector<std::vector<int>>& G, int32_t* first, int32_t* cnt) {
+    for (size_t g = 0; g < G.size(); ++g) {
+      first[g] = nl;
+      cnt[g] = (int32_t)G[g].size();
+      for (int u : G[g]) bp.glab[nl++] = u;
+    }
+    return (int32_t)G.size();
+  };
+  bp.nM = put(an.mg, bp.m_first, bp.m_cnt);
+  bp.nN = put(an.ng, bp.n_first, bp.n_cnt);
+  bp.nK = put(an.kg, bp.k_first, bp.k_cnt);
+  bp.cblocks = d_cblocks;
+  bp.ncb = (int32_t)ncb;
+  bp.counts = d_counts;
+  bp.ptr = pl.d_ptr;
+  bp.a_blk = pl.d_ablk;
+  bp.b_blk = pl.d_bblk;
+  bp.tasks = pl.d_tasks;
+  {
+    Launch L(ctx, "tt_build_count");
+    TT_CUDA(launch_build_count(bp, ctx->stream));
+  }
+  {
+    Launch L(ctx, "tt_build_scan");
+    TT_CUDA(launch_build_scan(bp, ctx->stream));
+  }
+  {
+    Launch L(ctx, "tt_build_fill");
+    TT_CUDA(launch_build_fill(bp, ctx->stream));
+  }
+  int64_t dev_total = -1;
+  TT_CUDA(cudaMemcpyAsync(&dev_total, pl.d_ptr + ncb, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (dev_total != ntasks)
+    return fail(TT_E_STATE, "device task builder produced %lld tasks, host enumerator %lld", (long long)dev_total,
+                (long long)ntasks);
+  pl.device_built = true;
+
+  // ---- tile variant: greedy list-scheduling estimate of the makespan
+  std::vector<int64_t> Ms(ht.cblk.size()), Ns(ht.cblk.size());
+  int32_t cc[TT_MAX_ORDER];
+  for (int g : pl.my) {
+    C->block_coords(ht.cblk[g], cc);
+    int64_t M = 1, N = 1;
+    for (int u = 0; u < an.nc; ++u) (an.a_pos[u] >= 0 ? M : N) *= lt[u]->size(cc[u]);
+    Ms[g] = M;
+    Ns[g] = N;
+  }
+  double best = -1;
+  for (int v = 0; v < num_contract_variants(); ++v) {
+    VariantInfo vi = contract_variant_info(v);
+    std::vector<double> items;
+    for (int g : pl.my) {
+      double kst = 0;
+      for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) kst += (double)((ht.K[t] + vi.bk - 1) / vi.bk);
+      const int64_t nit = ((Ms[g] + vi.bm - 1) / vi.bm) * ((Ns[g] + vi.bn - 1) / vi.bn);
+      const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm;
+      for (int64_t i = 0; i < nit; ++i) items.push_back(c);
+    }
+    std::sort(items.begin(), items.end(), std::greater<double>());
+    std::priority_queue<double, std::vector<double>, std::greater<double>> slots;
+    for (int s = 0; s < ctx->sm_count * vi.ctas_per_sm; ++s) slots.push(0.0);
+    double mk = 0;
+    for (double c : items) {
+      double t0 = slots.top();
+      slots.pop();
+      slots.push(t0 + c);
+      mk = std::max(mk, t0 + c);
+    }
+    if (best < 0 || mk < best * 0.97) {  // prefer earlier (larger) tiles unless >3% better
+      best = mk;
+      pl.variant = v;
+    }
+  }
+  if (const char* fv = getenv("TT_FORCE_VARIANT")) pl.variant = atoi(fv) % num_contract_variants();
+  VariantInfo vi = contract_variant_info(pl.variant);
+
+  // ---- groups + work items (groups by cost desc, block id asc)
+  std::vector<int> order(pl.my);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    if (ht.cost[x] != ht.cost[y]) return ht.cost[x] > ht.cost[y];
+    return ht.cblk[x] < ht.cblk[y];
+  });
+  std::vector<CGroupDesc> groups;
+  std::vector<WorkItem> work;
+  for (int g : order) {
+    CGroupDesc gd{};
+    int64_t cb = ht.cblk[g];
+    C->block_coords(cb, cc);
+    gd.c_off = C->blk_off[cb];
+    gd.M = (int32_t)Ms[g];
+    gd.N = (int32_t)Ns[g];
+    gd.task_begin = (int32_t)ht.ptr[g];
+    gd.task_end = (int32_t)ht.ptr[g + 1];
+    int64_t st = 0;
+    for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) st += (ht.K[t] + vi.bk - 1) / vi.bk;
+    gd.nstages = (int32_t)st;
+    int64_t sc[TT_MAX_ORDER], acc = 1;
+    for (int d = an.nc - 1; d >= 0; --d) { sc[d] = acc; acc *= lt[d]->size(cc[d]); }
+    for (int i = 0; i < kMaxGroup; ++i) { gd.mext[i] = gd.next[i] = 1; gd.cm_str[i] = gd.cn_str[i] = 0; }
+    for (size_t i = 0; i < an.mg.size(); ++i) {
+      int32_t e = 1;
+      for (int u : an.mg[i]) e *= (int32_t)lt[u]->size(cc[u]);
+      gd.mext[i] = e;
+      gd.cm_str[i] = (int32_t)sc[an.mg[i].back()];
+    }
+    for (size_t i = 0; i < an.ng.size(); ++i) {
+      int32_t e = 1;
+      for (int u : an.ng[i]) e *= (int32_t)lt[u]->size(cc[u]);
+      gd.next[i] = e;
+      gd.cn_str[i] = (int32_t)sc[an.ng[i].back()];
+    }
+    const int32_t gi = (int32_t)groups.size();
+    groups.push_back(gd);
+    const int32_t mtn = (gd.M + vi.bm - 1) / vi.bm, ntn = (gd.N + vi.bn - 1) / vi.bn;
+    for (int32_t mt = 0; mt < mtn; ++mt)
+      for (int32_t nt = 0; nt < ntn; ++nt) work.push_back({gi, mt, nt});
+  }
+  pl.nwork = (int64_t)work.size();
+  TT_TRY(dev_alloc(ctx, &pl.d_groups, groups.size()));
+  TT_TRY(dev_alloc(ctx, &pl.d_work, work.size()));
+  if (!groups.empty()) TT_CUDA(cudaMemcpy(pl.d_groups, groups.data(), groups.size() * sizeof(CGroupDesc), cudaMemcpyHostToDevice));
+  if (!work.empty()) TT_CUDA(cudaMemcpy(pl.d_work, work.data(), work.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
+  return TT_OK;
+}
+
+tt_status get_contract_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
+                            const char* bl, double beta, std::shared_ptr<ContractPlan>& out, bool* cached_flag) {
+  Analysis an;
+  TT_TRY(analyse(C, cl, A, al, B, bl, an));
+  if (C == A || C == B) return fail(TT_E_ARG, "C must not alias A or B");
+  std::string key = plan_key("contract", C, cl, A, al, B, bl, beta);
+  out = cached<ContractPlan>(ctx, key);
+  if (cached_flag) *cached_flag = out != nullptr;
+  if (out) return TT_OK;
+  auto pl = std::make_shared<ContractPlan>();
+  pl->an = an;
+  DeviceGuard dg(ctx->device);
+  TT_TRY(build_contract_plan(ctx, C, A, B, beta, *pl));
+  ctx->plans[key] = pl;
+  out = pl;
+  return TT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor A,
+                      const char* al, tt_tensor B, const char* bl) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  std::shared_ptr<ContractPlan> pl;
+  bool was_cached = false;
+  TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, pl, &was_cached));
+  TT_TRY(need_device(ctx));
+  TT_TRY(check_bound(C, "C"));
+  TT_TRY(check_bound(A, "A"));
+  TT_TRY(check_bound(B, "B"));
+  DeviceGuard dg(ctx->device);
+  reset_stats(ctx);
+  TT_TRY(run_gather(ctx, pl->gp, A == B ? std::vector<tt_tensor>{A} : std::vector<tt_tensor>{A, B}));
+  ContractParams p{};
+  p.A = A->data;
+  p.B = B->data;
+  p.C = C->data;
+  p.groups = pl->d_groups;
+  p.tasks = pl->d_tasks;
+  p.work = pl->d_work;
+  p.nM = (int32_t)pl->an.mg.size();
+  p.nN = (int32_t)pl->an.ng.size();
+  p.nK = (int32_t)pl->an.kg.size();
+  p.alpha = alpha;
+  p.beta = beta;
+  {
+    Launch L(ctx, "tt_contract_dmma");
+    TT_CUDA(launch_contract(pl->variant, pl->an.a_kc, pl->an.b_nc, p, pl->nwork, ctx->stream));
+  }
+  ctx->last.c_blocks = (int64_t)pl->my.size();
+  ctx->last.tasks = pl->tasks;
+  ctx->last.work_items = pl->nwork;
+  ctx->last.flops = pl->flops;
+  ctx->last.bytes = pl->bytes;
+  ctx->last.gathered_bytes = pl->gp.recv_bytes;
+  ctx->last.plan_cached = was_cached ? 1 : 0;
+  ctx->last.kernel_variant = pl->variant;
+  return TT_OK;
+}
+
+tt_status tt_task_list(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
+                       const char* bl, int32_t where, int64_t* cblk, int64_t* ptr, int64_t* a_blk, int64_t* b_blk,
+                       int64_t* cost, int64_t cap, int64_t* n_cblocks, int64_t* n_tasks) {
+  if (!ctx || !n_cblocks || !n_tasks) return fail(TT_E_ARG, "NULL argument");
+  Analysis an;
+  TT_TRY(analyse(C, cl, A, al, B, bl, an));
+  if (where == 0) {
+    HostTasks ht;
+    enumerate_tasks(an, C, A, B, ht);
+    *n_cblocks = (int64_t)ht.cblk.size();
+    *n_tasks = (int64_t)ht.a_blk.size();
+    if (!a_blk) return TT_OK;
+    if (cap < *n_tasks) return fail(TT_E_ARG, "capacity %lld < %lld tasks", (long long)cap, (long long)*n_tasks);
+    std::copy(ht.cblk.begin(), ht.cblk.end(), cblk);
+    std::copy(ht.ptr.begin(), ht.ptr.end(), ptr);
+    std::copy(ht.a_blk.begin(), ht.a_blk.end(), a_blk);
+    std::copy(ht.b_blk.begin(), ht.b_blk.end(), b_blk);
+    if (cost) std::copy(ht.cost.begin(), ht.cost.end(), cost);
+    return TT_OK;
+  }
+  TT_TRY(need_device(ctx));
+  std::shared_ptr<ContractPlan> pl;
+  TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, 1.0, pl, nullptr));
+  const HostTasks& ht = pl->ht;
+  *n_cblocks = (int64_t)ht.cblk.size();
+  *n_tasks = (int64_t)ht.a_blk.size();
+  if (!a_blk) return TT_OK;
+  if (cap < *n_tasks) return fail(TT_E_ARG, "capacity %lld < %lld tasks", (long long)cap, (long long)*n_tasks);
+  DeviceGuard dg(ctx->device);
+  // device-built arrays (ptr, a_blk, b_blk) copied back; cblk / cost are host plan metadata
+  std::copy(ht.cblk.begin(), ht.cblk.end(), cblk);
+  TT_CUDA(cudaMemcpy(ptr, pl->d_ptr, (*n_cblocks + 1) * 8, cudaMemcpyDeviceToHost));
+  if (*n_tasks) {
+    TT_CUDA(cudaMemcpy(a_blk, pl->d_ablk, *n_tasks * 8, cudaMemcpyDeviceToHost));
+    TT_CUDA(cudaMemcpy(b_blk, pl->d_bblk, *n_tasks * 8, cudaMemcpyDeviceToHost));
+  }
+  if (cost) std::copy(ht.cost.begin(), ht.cost.end(), cost);
+  return TT_OK;
+}
+
+tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
+                           const char* bl, int32_t* owner) {
+  if (!ctx || !owner) return fail(TT_E_ARG, "NULL argument");
+  Analysis an;
+  TT_TRY(analyse(C, cl, A, al, B, bl, an));
+  HostTasks ht;
+  enumerate_tasks(an, C, A, B, ht);
+  std::vector<int32_t> own = lpt(ht.cost, ht.cblk, ctx->nranks);
+  for (int64_t b = 0; b < C->nblocks; ++b) owner[b] = -1;
+  for (size_t g = 0; g < ht.cblk.size(); ++g) owner[ht.cblk[g]] = own[g];
+  return TT_OK;
+}
+
+tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
+                         const char* bl, int64_t* recv, int64_t* n_recv, int64_t* send, int64_t* n_send, int64_t cap) {
+  if (!ctx || !n_recv || !n_send) return fail(TT_E_ARG, "NULL argument");
+  Analysis an;
+  TT_TRY(analyse(C, cl, A, al, B, bl, an));
+  if (C == A || C == B) return fail(TT_E_ARG, "C must not alias A or B");
+  ContractPlan pl;
+  pl.an = an;
+  tt_ctx_s host;             // host-only planning context (no device work)
+  host.device = -1;
+  host.rank = ctx->rank;
+  host.nranks = ctx->nranks;
+  host.sm_count = ctx->sm_count;
+  TT_TRY(build_contract_plan(&host, C, A, B, 1.0, pl));
+  *n_recv = (int64_t)pl.gp.recv_list.size() / 3;
+  *n_send = (int64_t)pl.gp.send_list.size() / 3;
+  if (!recv && !send) return TT_OK;
+  if (cap < std::max(*n_recv, *n_send)) return fail(TT_E_ARG, "capacity too small");
+  if (recv) std::copy(pl.gp.recv_list.begin(), pl.gp.recv_list.end(), recv);
+  if (send) std::copy(pl.gp.send_list.begin(), pl.gp.send_list.end(), send);
+  return TT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// tt_internal.h -- internal types of libtt (host metadata + device descriptors).
+// Not part of the ABI (include/tt.h is).  Citations as in tt.h.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tt.h"
+
+namespace tt {
+
+constexpr int kMaxGroup = 4;  // fused label groups per GEMM side (M, N, K)
+
+// ------------------------------------------------------------------------------------------------
+// Device descriptors (built on device by the task builder, read by the contraction kernel).
+
+// One per non-zero C block this rank computes.  GEMM view of the block:
+// m = mixed radix over the fused M groups (labels of C that come from A, C order), n over the
+// fused N groups (labels from B), innermost last.
+struct CGroupDesc {
+  int64_t c_off;                 // packed offset of the C block
+  int32_t M, N;                  // GEMM extents of the block
+  int32_t task_begin, task_end;  // CSR range in the task array
+  int32_t nstages;               // sum over tasks of ceil(K_t / BK) for the chosen kernel BK
+  int32_t pad;
+  int32_t mext[kMaxGroup], next[kMaxGroup];     // fused group extents
+  int32_t cm_str[kMaxGroup], cn_str[kMaxGroup]; // their strides inside the C block
+};
+
+// One per non-zero (A block, B block) pair.
+struct TaskDesc {
+  int64_t a_off, b_off;          // packed offsets of the A and B blocks
+  int32_t K;                     // contracted extent of this pair
+  int32_t pad;
+  int32_t kext[kMaxGroup];                      // fused K group extents (order of first appearance in A)
+  int32_t ak_str[kMaxGroup], bk_str[kMaxGroup]; // K group strides in the A / B block
+  int32_t am_str[kMaxGroup], bn_str[kMaxGroup]; // M group strides in A, N group strides in B
+};
+
+struct WorkItem {
+  int32_t group;   // index into CGroupDesc array
+  int32_t mt, nt;  // tile coordinates inside the block
+};
+
+// Label analysis of a contraction after fusing adjacent labels (DESIGN.md §5 "label fusion").
+struct LabelGroup {
+  std::vector<int> labels;  // original label chars (as ints), in group order
+};
+
+struct ContractionShape {
+  std::string c_lbl, a_lbl, b_lbl;
+  std::vector<char> con;                   // contracted labels, order of first appearance in A
+  std::vector<LabelGroup> mg, ng, kg;      // fused groups
+  bool a_kcontig = true;                   // A's innermost label is a K label
+  bool b_ncontig = true;                   // B's innermost label is an N label
+};
+
+}  // namespace tt
+
+// ------------------------------------------------------------------------------------------------
+// Host handle types.
+
+struct tt_is_s {
+  int64_t extent = 0;
+  std::vector<int64_t> rb, re;   // ranges [rb, re)
+  std::vector<int8_t> rspin;
+};
+
+struct tt_tis_s {
+  tt_is is = nullptr;
+  std::vector<int64_t> offsets;  // ntiles + 1
+  std::vector<int8_t> spin;      // per tile
+  uint64_t uid = 0;
+  int32_t ntiles() const { return (int32_t)offsets.size() - 1; }
+  int64_t size(int t) const { return offsets[t + 1] - offsets[t]; }
+};
+
+struct tt_tensor_s {
+  tt_ctx ctx = nullptr;
+  int32_t order = 0;
+  std::vector<tt_tis> dims;
+  std::vector<int32_t> grid;       // ntiles per dim
+  int64_t nblocks = 0, nnz = 0;
+  std::vector<uint8_t> nz;
+  std::vector<int64_t> blk_off;
+  std::vector<int32_t> owner;
+  int64_t packed_elems = 0;
+  double* data = nullptr;
+  int64_t capacity = 0;
+  uint64_t uid = 0;
+  uint64_t version = 0;            // bumped when the owner map changes (plan cache key)
+  // device metadata (lazily uploaded)
+  uint8_t* d_nz = nullptr;
+  int64_t* d_blk_off = nullptr;
+  std::vector<int64_t*> d_toff;   // per dim tile offsets on the device
+  bool dev_ready = false;
+  bool held(int64_t b, int32_t rank) const { return nz[b] && (owner[b] == rank || owner[b] == TT_REPLICATED); }
+
+  void block_coords(int64_t b, int32_t* c) const {
+    for (int d = order - 1; d >= 0; --d) { c[d] = (int32_t)(b % grid[d]); b /= grid[d]; }
+  }
+  int64_t block_id(const int32_t* c) const {
+    int64_t b = 0;
+    for (int d = 0; d < order; ++d) b = b * grid[d] + c[d];
+    return b;
+  }
+  int64_t block_volume(int64_t b) const {
+    int32_t c[TT_MAX_ORDER];
+    block_coords(b, c);
+    int64_t v = 1;
+    for (int d = 0; d < order; ++d) v *= dims[d]->size(c[d]);
+    return v;
+  }
+};
+
+struct ProfileRec {
+  std::string name;
+  cudaEvent_t e0, e1;
+};
+
+struct tt_ctx_s {
+  int32_t device = -1;
+  cudaStream_t stream = nullptr;
+  int32_t rank = 0, nranks = 1;
+  void* comm = nullptr;            // ncclComm_t
+  bool profiling = false;
+  std::vector<ProfileRec> prof;
+  std::vector<cudaEvent_t> event_pool;
+  int64_t launches = 0;
+  tt_stats last{};
+  std::map<std::string, std::shared_ptr<void>> plans;   // plan cache (type-erased)
+  std::vector<void*> dev_allocs;                         // metadata allocations freed at destroy
+  double* d_scalar = nullptr;                            // scratch for scalar results
+  double* d_partials = nullptr;
+  int32_t sm_count = 148;
+};

@@ -1,0 +1,279 @@
+"""GPU parity: libtt (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE north_star, reading R13): normwise max|gpu - oracle| / max|oracle| <= 1e-11 per output
+tensor for uniform inputs; bit-exact for integer-valued inputs, tile maps, task lists and the
+synthetic fill.  Sizes span several CTA tiles with ragged tails; edge cases: ragged tiles, permuted
+labels, beta = 0 with NaN in C, C blocks without tasks, every kernel tile variant, determinism."""
+import os
+
+import numpy as np
+import pytest
+
+import synthetic as S
+from oracle import layout as L
+from oracle import ops as O
+from tests.cases import Problem, SpaceSpec, TensorSpec, ccsd_problem, oracle_objects, product_objects
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_2201_01257_b200 as tt
+    torch.cuda.init()
+    return tt, torch
+
+
+def new_ctx(tt, torch, variant=None):
+    if variant is None:
+        os.environ.pop("TT_FORCE_VARIANT", None)
+    else:
+        os.environ["TT_FORCE_VARIANT"] = str(variant)
+    return tt.Context(device=0, stream=torch.cuda.current_stream().cuda_stream)
+
+
+def bind_host(torch, T, packed):
+    dev = torch.from_numpy(np.ascontiguousarray(packed)).cuda()
+    T.bind(dev)
+    return dev
+
+
+def normwise(x, ref):
+    return float(np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-300)) if ref.size else 0.0
+
+
+def run_contract(tt, torch, ctx, pb, op, alpha=1.0, beta=1.0, kind=S.KIND_UNIFORM, seed=1, nan_c=False):
+    C, cl, a, al, b, bl = op
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    dense = {}
+    bufs = []
+    for name, tag in ((C, 3), (a, 1), (b, 2)):
+        D = O.dense_masked(orc[name], S.dense(orc[name].shape, seed, tag, kind))
+        if name == C and nan_c:
+            D = np.where(O.nz_mask(orc[name]).astype(bool), np.nan, 0.0)
+        dense[name] = D
+        bufs.append(bind_host(torch, P[name], O.pack(orc[name], D)))
+    tt.contract(ctx, P[C], cl, beta, alpha, P[a], al, P[b], bl)
+    got = P[C].download()
+    ctx.sync()
+    ref = O.contract(dense[C], cl, dense[a], al, dense[b], bl, alpha, beta, cmask=O.nz_mask(orc[C]))
+    return got, O.pack(orc[C], ref), P, orc
+
+
+PROBLEMS = {
+    "cfg1_ring_dense": (ccsd_problem(4, 8, 4, 4, False, terms=("ring",)), 0),
+    "spin_small_ladder": (ccsd_problem(8, 12, 2, 3, True), 0),
+    "spin_small_ring": (ccsd_problem(8, 12, 2, 3, True), 1),
+    "spin_small_hh": (ccsd_problem(8, 12, 2, 3, True), 2),
+    "ragged_dense_ring": (ccsd_problem(7, 13, 3, 5, False), 1),
+    "ragged_dense_ladder": (ccsd_problem(7, 13, 3, 5, False), 0),
+    "multi_tile_spin_ladder": (ccsd_problem(24, 80, 12, 20, True, terms=("ladder",)), 0),
+    "multi_tile_spin_ring": (ccsd_problem(24, 80, 12, 20, True, terms=("ring",)), 0),
+}
+
+
+@pytest.mark.parametrize("name", list(PROBLEMS))
+def test_contract_parity(env, name):
+    tt, torch = env
+    pb, k = PROBLEMS[name]
+    ctx = new_ctx(tt, torch)
+    got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[k], alpha=0.75, beta=1.0)
+    assert normwise(got, ref) <= TOL, normwise(got, ref)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_every_tile_variant(env, variant):
+    tt, torch = env
+    pb = ccsd_problem(24, 80, 12, 20, True, terms=("ladder", "ring"))
+    ctx = new_ctx(tt, torch, variant)
+    for op in pb.ops:
+        got, ref, _, _ = run_contract(tt, torch, ctx, pb, op, alpha=1.5, beta=-0.5)
+        assert normwise(got, ref) <= TOL
+        assert ctx.stats()["kernel_variant"] == variant
+    os.environ.pop("TT_FORCE_VARIANT", None)
+
+
+def test_integer_inputs_bit_exact(env):
+    tt, torch = env
+    pb = ccsd_problem(12, 30, 6, 10, True)
+    ctx = new_ctx(tt, torch)
+    for op in pb.ops:
+        got, ref, _, _ = run_contract(tt, torch, ctx, pb, op, alpha=2.0, beta=1.0, kind=S.KIND_INTEGER)
+        assert np.array_equal(got, ref)
+
+
+def test_beta_zero_never_reads_c(env):
+    tt, torch = env
+    pb = ccsd_problem(8, 12, 2, 3, True)
+    ctx = new_ctx(tt, torch)
+    for op in pb.ops:
+        got, ref, _, _ = run_contract(tt, torch, ctx, pb, op, alpha=0.5, beta=0.0, nan_c=True)
+        assert np.isfinite(got).all()
+        assert normwise(got, np.nan_to_num(ref)) <= TOL
+
+
+def test_permuted_labels(env):
+    """Operands whose innermost labels are free/contracted in every combination (all four kernel
+    orientations), output permuted relative to both."""
+    tt, torch = env
+    spaces = {"X": SpaceSpec(11, tile=4), "Y": SpaceSpec(9, tile=5), "Z": SpaceSpec(10, tile=3)}
+    ls = {"a": "X", "b": "Y", "c": "Z", "i": "Y", "j": "X", "k": "Z"}
+    ctx = new_ctx(tt, torch)
+    for cl, al, bl in [("jbia", "kcai", "bjck"), ("abij", "iack", "kcjb"), ("ijab", "akci", "jbkc"),
+                       ("bjai", "ciak", "cbkj")]:
+        tens = {"C": TensorSpec(cl), "A": TensorSpec(al), "B": TensorSpec(bl)}
+        pb = Problem(spaces, ls, tens, [("C", cl, "A", al, "B", bl)])
+        got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[0], alpha=1.0, beta=0.5)
+        assert normwise(got, ref) <= TOL, (cl, al, bl)
+
+
+def test_c_blocks_without_tasks(env):
+    """Non-zero C blocks with no non-zero (A,B) pair get C = beta*C (A8 / S509)."""
+    tt, torch = env
+    spaces = {"X": SpaceSpec(12, tile=4)}
+    ls = {x: "X" for x in "ikl"}
+    nzA = [1, 0, 0, 0, 1, 0, 1, 0, 0]     # A blocks (i,k): row 2 has A(2,0) only
+    nzB = [0, 1, 1, 0, 1, 0, 0, 0, 1]     # B(0,*) zero except cols 1,2 ...
+    pb = Problem(spaces, ls, {"C": TensorSpec("il"), "A": TensorSpec("ik", ("nz", nzA)), "B": TensorSpec("kl", ("nz", nzB))},
+                 [("C", "il", "A", "ik", "B", "kl")])
+    ctx = new_ctx(tt, torch)
+    got, ref, P, _ = run_contract(tt, torch, ctx, pb, pb.ops[0], alpha=1.0, beta=-2.0)
+    assert normwise(got, ref) <= TOL
+
+
+def test_determinism(env):
+    tt, torch = env
+    pb = ccsd_problem(24, 80, 12, 20, True, terms=("ring",))
+    ctx = new_ctx(tt, torch)
+    g1, _, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[0], seed=5)
+    g2, _, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[0], seed=5)
+    assert np.array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("pi", [0, 1])
+def test_device_task_list_bit_exact(env, pi):
+    tt, torch = env
+    pb = [ccsd_problem(8, 12, 2, 3, True), ccsd_problem(60, 400, 30, 40, True)][pi]
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    for (c, cl, a, al, b, bl) in pb.ops:
+        ocb, optr, oab, obb, ocost = L.task_list(orc[c], cl, orc[a], al, orc[b], bl)
+        tl = tt.task_list(ctx, P[c], cl, P[a], al, P[b], bl, device=True)
+        assert list(tl["cblk"]) == ocb and list(tl["ptr"]) == optr
+        assert list(tl["a_blk"]) == oab and list(tl["b_blk"]) == obb
+
+
+@pytest.mark.parametrize("kind", [S.KIND_UNIFORM, S.KIND_INTEGER])
+def test_fill_synthetic_bit_exact(env, kind):
+    tt, torch = env
+    pb = ccsd_problem(10, 14, 3, 4, True, terms=("ring",))
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    for name in ("Ta", "Wr", "R"):
+        buf = torch.zeros(P[name].packed_elems, dtype=torch.float64, device="cuda")
+        P[name].bind(buf)
+        tt.fill_synthetic(ctx, P[name], 7, 4, kind)
+        got = P[name].download()
+        ctx.sync()
+        ref = O.pack(orc[name], S.dense(orc[name].shape, 7, 4, kind))
+        assert np.array_equal(got, ref)
+
+
+def test_set_add_scalar(env):
+    tt, torch = env
+    pb = ccsd_problem(8, 12, 2, 3, True)
+    pb.tensors["Rt"] = TensorSpec("ijab", ("spin", [0, 1], [2, 3]))
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    bufs = {}
+    dense = {}
+    for name, tag in (("R", 3), ("Rt", 1), ("Ta", 2)):
+        dense[name] = O.dense_masked(orc[name], S.dense(orc[name].shape, 3, tag))
+        bufs[name] = bind_host(torch, P[name], O.pack(orc[name], dense[name]))
+    # add with permutation: R(abij) = -0.5*R + 2*Rt(ijab)
+    tt.add(ctx, P["R"], "abij", -0.5, 2.0, P["Rt"], "ijab")
+    got = P["R"].download()
+    ctx.sync()
+    ref = O.add(dense["R"], "abij", dense["Rt"], "ijab", 2.0, -0.5, cmask=O.nz_mask(orc["R"]))
+    assert normwise(got, O.pack(orc["R"], ref)) <= 1e-15
+    # scalar: s = 0.25 * sum Ta(acik) R(acik)  (relabelled R)
+    R2 = ref
+    s = tt.contract_scalar(ctx, 0.25, P["Ta"], "acik", P["R"], "acik")
+    so = O.scalar(dense["Ta"], "acik", R2, "acik", 0.25)
+    assert abs(s - so) <= 1e-13 * max(abs(so), 1.0)
+    # set
+    tt.set_(ctx, P["R"], 3.25)
+    got = P["R"].download()
+    ctx.sync()
+    assert np.array_equal(got, O.pack(orc["R"], O.set_(np.zeros(orc["R"].shape), 3.25, O.nz_mask(orc["R"]))))
+
+
+def test_fig5_program(env):
+    """P194-198 (Fig. 5) through the ABI, reading R2: A = 1; B = -1; C = 0.5 A.B -> -10.0."""
+    tt, torch = env
+    ctx = new_ctx(tt, torch)
+    N, M, K = tt.IndexSpace(100), tt.IndexSpace(30), tt.IndexSpace(20)
+    tN, tM, tK = tt.TiledIndexSpace(N, 10), tt.TiledIndexSpace(M, sizes=[10, 20]), tt.TiledIndexSpace(K, 5)
+    A, B, C = tt.Tensor(ctx, [tM, tK]), tt.Tensor(ctx, [tK, tN]), tt.Tensor(ctx, [tM, tN])
+    bufs = [torch.full((T.packed_elems,), float("nan"), dtype=torch.float64, device="cuda") for T in (A, B, C)]
+    for T, b in zip((A, B, C), bufs):
+        T.bind(b)
+    tt.set_(ctx, A, 1.0)
+    tt.set_(ctx, B, 0.0)
+    J = tt.Tensor(ctx, [tK, tN])
+    jb = torch.ones(J.packed_elems, dtype=torch.float64, device="cuda")
+    J.bind(jb)
+    tt.add(ctx, B, "la", 1.0, -1.0, J, "la")
+    tt.contract(ctx, C, "ia", 0.0, 0.5, A, "il", B, "la")
+    got = C.download()
+    ctx.sync()
+    assert np.all(got[:3000] == -10.0)
+
+
+def test_config2_full_size_sampled(env):
+    """BASELINE configs[1] (the bench workload: ladder O=40 V=200 tile 40) at full size, in the
+    bench launch configuration: 192 sampled outputs (every C block) vs the oracle element by element
+    (K = 40000 each), plus the inputs' fill checked on the same samples."""
+    tt, torch = env
+    pb = ccsd_problem(40, 200, 40, 40, False, terms=("ladder",))
+    ctx = new_ctx(tt, torch)
+    P = product_objects(tt, ctx, pb)
+    bufs = {}
+    for name, tag in (("R", 3), ("Vv", 4), ("T", 5)):
+        bufs[name] = torch.empty(P[name].packed_elems, dtype=torch.float64, device="cuda")
+        P[name].bind(bufs[name])
+        tt.fill_synthetic(ctx, P[name], 11, tag)
+    tt.contract(ctx, P["R"], "abij", 1.0, 1.0, P["Vv"], "abcd", P["T"], "cdij")
+    got = P["R"].download()
+    ctx.sync()
+    orc = oracle_objects(pb)
+    R = orc["R"]
+    rng = np.random.default_rng(0)
+    idx = []
+    for b in range(R.nblocks):          # 8 per block: 4 corners + 4 random
+        o, e = R.block_origin(b), R.block_extents(b)
+        corners = [[o[d] + (e[d] - 1 if (q >> d) & 1 else 0) for d in range(4)] for q in (0, 3, 12, 15)]
+        idx += corners + [[o[d] + rng.integers(e[d]) for d in range(4)] for _ in range(4)]
+    idx = np.array(idx[:192] if len(idx) > 192 else idx)
+    ext = dict(a=200, b=200, c=200, d=200, i=40, j=40)
+    sums = O.sampled_elements(idx, "abij", "abcd", "cdij", ext,
+                              lambda ix: S.values(11, 4, S.linear_index((200,) * 4, ix)),
+                              lambda ix: S.values(11, 5, S.linear_index((200, 200, 40, 40), ix)))
+    c0 = S.values(11, 3, S.linear_index((200, 200, 40, 40), idx))
+    ref = c0 + sums
+    # packed position of each sampled element
+    offs = R.blk_off()
+    pos = []
+    for x in idx:
+        b = R.block_id([x[d] // 40 for d in range(4)])
+        loc = [x[d] % 40 for d in range(4)]
+        pos.append(offs[b] + ((loc[0] * 40 + loc[1]) * 40 + loc[2]) * 40 + loc[3])
+    g = got[np.array(pos)]
+    assert np.abs(g - ref).max() / np.abs(ref).max() <= TOL

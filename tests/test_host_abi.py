@@ -1,0 +1,198 @@
+"""CPU tests of libtt's host side through the C ABI (host-only context, no GPU needed):
+symbol exports, tilings and tile maps (bit-exact vs the oracle), validation errors, the host task
+list and LPT partition (bit-exact vs the oracle enumerator), gather plans."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2201_01257_b200 as tt
+from oracle import layout as L
+from tests.cases import Problem, SpaceSpec, TensorSpec, ccsd_problem, oracle_objects, product_objects
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hctx():
+    c = tt.Context(device=-1)
+    yield c
+    c.close()
+
+
+def test_exports_every_declared_symbol():
+    """Every function declared in include/tt.h is exported by libtt.so and bound by the wrapper."""
+    hdr = open(os.path.join(ROOT, "include", "tt.h")).read()
+    declared = set(re.findall(r"^(?:tt_status|const char\*|int32_t)\s+(tt_\w+)\(", hdr, re.M))
+    assert len(declared) >= 30
+    for name in declared:
+        assert hasattr(tt._lib, name), name
+    assert declared == set(tt.EXPORTED)
+
+
+def test_fig2_layout(hctx):
+    """P140: A{tM,tK} 30x20 with eight blocks; packed offsets = oracle (bit-exact)."""
+    N, M, K = tt.IndexSpace(100), tt.IndexSpace(30), tt.IndexSpace(20)
+    tN, tM, tK = tt.TiledIndexSpace(N, 10), tt.TiledIndexSpace(M, sizes=[10, 20]), tt.TiledIndexSpace(K, 5)
+    assert tN.ntiles == 10 and tK.ntiles == 4 and list(tM.offsets) == [0, 10, 30]
+    A = tt.Tensor(hctx, [tM, tK])
+    assert A.nblocks == 8 and A.shape == (30, 20)
+    oA = L.tensor_dense_map([L.tile_custom(L.IndexSpace(30), [10, 20]), L.tile_fixed(L.IndexSpace(20), 5)])
+    assert list(A.blk_off) == oA.blk_off() and A.packed_elems == oA.packed_elems()
+
+
+def test_tiling_errors():
+    K = tt.IndexSpace(20)
+    with pytest.raises(tt.TTError) as e:
+        tt.TiledIndexSpace(K, sizes=[10, 5])
+    assert e.value.name == "TT_E_COVERAGE"
+    sp = tt.IndexSpace(150, [(0, 75), (75, 150)], [1, -1])
+    t = tt.TiledIndexSpace(sp, 64)
+    assert list(np.diff(t.offsets)) == [64, 11, 64, 11] and list(t.spin) == [1, 1, -1, -1]
+    with pytest.raises(tt.TTError) as e:
+        tt.TiledIndexSpace(sp, sizes=[70, 80])
+    assert e.value.name == "TT_E_TILING"
+    with pytest.raises(tt.TTError) as e:
+        tt.IndexSpace(10, [(0, 4), (5, 10)], [1, -1])
+    assert e.value.name == "TT_E_COVERAGE"
+    with pytest.raises(tt.TTError):
+        tt.TiledIndexSpace(K, 0)
+
+
+LAYOUT_PROBLEMS = [
+    ccsd_problem(8, 12, 2, 3, True),
+    ccsd_problem(7, 11, 3, 4, False),
+    ccsd_problem(60, 400, 30, 40, True, terms=("ladder",)),
+    Problem({"X": SpaceSpec(13, sizes=[5, 1, 7]), "Y": SpaceSpec(9, tile=4, spin_split=True)},
+            {"p": "X", "q": "Y", "r": "X", "s": "Y"},
+            {"A": TensorSpec("pqs", ("spin", [1], [2])), "B": TensorSpec("sr", ("nz", [1, 0, 1, 1, 0, 1, 0, 1, 1])),
+             "C": TensorSpec("pqr", None)}),
+]
+
+
+@pytest.mark.parametrize("pi", range(len(LAYOUT_PROBLEMS)))
+def test_tile_maps_bit_exact(hctx, pi):
+    """nz maps, packed offsets (16-B aligned, R10), default RR owners (P210) == oracle."""
+    pb = LAYOUT_PROBLEMS[pi]
+    orc = oracle_objects(pb)
+    prod = product_objects(tt, hctx, pb)
+    for name in pb.tensors:
+        o, p = orc[name], prod[name]
+        assert list(p.nz) == o.nz, name
+        assert list(p.blk_off) == o.blk_off(), name
+        assert p.packed_elems == o.packed_elems(), name
+        assert list(p.owner) == o.owners(), name
+
+
+def test_owner_rr_multi_rank():
+    c = tt.Context(device=-1, rank=1, nranks=3)
+    pb = ccsd_problem(8, 12, 2, 3, True, terms=("ladder",))
+    orc = oracle_objects(pb, nranks=3)
+    prod = product_objects(tt, c, pb)
+    assert list(prod["Vv"].owner) == orc["Vv"].owners()
+
+
+def test_validation_errors(hctx):
+    pb = ccsd_problem(4, 8, 4, 4, False, terms=("ring",))
+    P = product_objects(tt, hctx, pb)
+    R, A, B = P["R"], P["Ta"], P["Wr"]
+    cases = [
+        (("abij", "acik", "cbkk"), "TT_E_LABEL"),     # repeated label (S412)
+        (("abij", "acik", "cbkx"), "TT_E_LABEL"),     # dangling
+        (("abi", "acik", "cbkj"), "TT_E_LABEL"),      # arity
+        (("abij", "abik", "cbkj"), "TT_E_LABEL"),     # b in C, A and B (batch, S380)
+        (("abij", "acik", "kbcj"), "TT_E_TILING"),    # k bound to V on B, O on A (S413)
+    ]
+    for (cl, al, bl), err in cases:
+        with pytest.raises(tt.TTError) as e:
+            tt.task_list(hctx, R, cl, A, al, B, bl)
+        assert e.value.name == err, (cl, al, bl)
+    with pytest.raises(tt.TTError) as e:
+        tt.contract(hctx, R, "abij", 1.0, 1.0, A, "acik", B, "cbkj")
+    assert e.value.name == "TT_E_STATE"
+
+
+TL_PROBLEMS = [ccsd_problem(4, 8, 4, 4, False), ccsd_problem(8, 12, 2, 3, True), ccsd_problem(10, 14, 3, 4, True),
+               ccsd_problem(9, 13, 4, 5, False)]
+
+
+@pytest.mark.parametrize("pi", range(len(TL_PROBLEMS)))
+def test_host_task_list_bit_exact(hctx, pi):
+    """Host enumerator == oracle brute force: C blocks, CSR, (A,B) block ids, FLOP cost (R11)."""
+    pb = TL_PROBLEMS[pi]
+    orc = oracle_objects(pb)
+    prod = product_objects(tt, hctx, pb)
+    for (c, cl, a, al, b, bl) in pb.ops:
+        ocb, optr, oab, obb, ocost = L.task_list(orc[c], cl, orc[a], al, orc[b], bl)
+        tl = tt.task_list(hctx, prod[c], cl, prod[a], al, prod[b], bl)
+        assert list(tl["cblk"]) == ocb and list(tl["ptr"]) == optr
+        assert list(tl["a_blk"]) == oab and list(tl["b_blk"]) == obb
+        assert list(tl["cost"]) == ocost
+
+
+def test_task_counts_closed_forms(hctx):
+    """cfg2 ladder 625 tasks; cfg3 ladder/ring/hh 6250/1250/250; cfg4 ladder 40960."""
+    pb = ccsd_problem(40, 200, 40, 40, False, terms=("ladder",))
+    P = product_objects(tt, hctx, pb)
+    assert len(tt.task_list(hctx, P["R"], "abij", P["Vv"], "abcd", P["T"], "cdij")["a_blk"]) == 625
+    pb = ccsd_problem(60, 400, 30, 40, True)
+    P = product_objects(tt, hctx, pb)
+    got = [len(tt.task_list(hctx, P[c], cl, P[a], al, P[b], bl)["a_blk"]) for (c, cl, a, al, b, bl) in pb.ops]
+    assert got == [6250, 1250, 250]
+    pb = ccsd_problem(100, 800, 50, 50, True, terms=("ladder",))
+    P = product_objects(tt, hctx, pb)
+    tl = tt.task_list(hctx, P["R"], "abij", P["Vv"], "abcd", P["T"], "cdij")
+    assert len(tl["a_blk"]) == 40960 and int(tl["cost"].sum()) == 1280000000000000
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_lpt_partition_matches_oracle(nranks):
+    c = tt.Context(device=-1, nranks=nranks)
+    pb = ccsd_problem(10, 14, 3, 4, True)
+    orc = oracle_objects(pb, nranks)
+    prod = product_objects(tt, c, pb)
+    for (C, cl, a, al, b, bl) in pb.ops:
+        ocb, _, _, _, ocost = L.task_list(orc[C], cl, orc[a], al, orc[b], bl)
+        oown = L.lpt_partition(ocost, ocb, nranks)
+        own = tt.partition_lpt(c, prod[C], cl, prod[a], al, prod[b], bl)
+        assert [own[x] for x in ocb] == oown
+        assert all(own[x] == -1 for x in range(prod[C].nblocks) if not prod[C].nz[x])
+
+
+def _expected_gather(orc, pb_op, owners, me, nranks):
+    C, cl, a, al, b, bl = pb_op
+    ocb, optr, oab, obb, _ = L.task_list(orc[C], cl, orc[a], al, orc[b], bl)
+    need = {r: set() for r in range(nranks)}
+    for g, cb in enumerate(ocb):
+        r = owners[C][cb]
+        for t in range(optr[g], optr[g + 1]):
+            need[r].add((0, oab[t]))
+            need[r].add((1, obb[t]))
+    recv = sorted((op, blk, owners[[a, b][op]][blk]) for (op, blk) in need[me] if owners[[a, b][op]][blk] != me)
+    send = sorted((op, blk, r) for r in range(nranks) for (op, blk) in need[r]
+                  if r != me and owners[[a, b][op]][blk] == me)
+    return recv, send
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_gather_plan_exactly_needed_blocks(nranks):
+    """Each rank receives exactly the A/B blocks its owned C blocks' tasks read but it does not own,
+    and the sends of every rank mirror the receives of its peers (P212)."""
+    pb = ccsd_problem(8, 12, 2, 3, True)
+    sends, recvs = {}, {}
+    for me in range(nranks):
+        c = tt.Context(device=-1, rank=me, nranks=nranks)
+        orc = oracle_objects(pb, nranks)
+        prod = product_objects(tt, c, pb)
+        C, cl, a, al, b, bl = pb.ops[1]        # ring term
+        own = tt.partition_lpt(c, prod[C], cl, prod[a], al, prod[b], bl)
+        prod[C].set_owner(own)
+        owners = {n: list(prod[n].owner) for n in pb.tensors}
+        r, s = tt.gather_plan(c, prod[C], cl, prod[a], al, prod[b], bl)
+        er, es = _expected_gather(orc, pb.ops[1], owners, me, nranks)
+        assert sorted(map(tuple, r.tolist())) == er
+        assert sorted(map(tuple, s.tolist())) == es
+        sends[me] = {(op, blk, me, peer) for op, blk, peer in s.tolist()}
+        recvs[me] = {(op, blk, peer, me) for op, blk, peer in r.tolist()}
+    assert set().union(*sends.values()) == set().union(*recvs.values())
