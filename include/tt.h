@@ -209,7 +209,7 @@ tt_status tt_task_list(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, 
                        int64_t* a_blk, int64_t* b_blk, int64_t* cost, int64_t cap,
                        int64_t* n_cblocks, int64_t* n_tasks);
 
-/* LPT owner partition of C's non-zero blocks over the context's nranks (R3-part): blocks sorted by
+/* LPT owner partition of C's non-zero blocks over the context's nranks (R24): blocks sorted by
  * (cost desc, block id asc), each to the least-loaded rank, ties to the lowest rank.  Writes
  * owner[nblocks of C] (-1 for zero blocks).  Does not modify C (use tt_tensor_set_owner). */
 tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,

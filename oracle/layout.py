@@ -17,7 +17,7 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain Python loops, written 
 * Task list -- for each non-zero C block (row-major), each contracted-tile tuple (row-major,
   contracted labels in order of first appearance in A): a task iff the A and B blocks are both
   non-zero (P111, P138, P210, P543; readings R8, R11).  Brute force over the full grid.
-* LPT owner partition (reading R3-part): C blocks sorted by (cost desc, block id asc), each to the
+* LPT owner partition (reading R24): C blocks sorted by (cost desc, block id asc), each to the
   least-loaded rank, ties to the lowest rank.
 """
 from __future__ import annotations
