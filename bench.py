@@ -167,7 +167,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--variant", type=int, default=None, help="force a contraction kernel variant (TT_FORCE_VARIANT)")
     args = ap.parse_args()
+    if args.variant is not None:
+        os.environ["TT_FORCE_VARIANT"] = str(args.variant)
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)

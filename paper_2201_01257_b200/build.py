@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtt.so")
-SOURCES = ["tt_kernels.cu", "tt_api.cpp", "tt_nccl.cpp"]
+SOURCES = ["tt_kernels.cu", "tt_contract_ws.cu", "tt_api.cpp", "tt_nccl.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
@@ -22,19 +22,21 @@ def _newest_source() -> float:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= _newest_source():
         return SO
-    objs = []
+    objs, procs = [], []
     for src in SOURCES:
         obj = os.path.join(CSRC, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, *CFLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+        objs.append(obj)
+    for src, pr in procs:   # compile in parallel
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(obj)
+            sys.stderr.write(err)
     tmp = SO + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-lpthread", "-lrt"]
     r = subprocess.run(cmd, capture_output=True, text=True)

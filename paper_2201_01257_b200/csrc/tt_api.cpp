@@ -227,6 +227,17 @@ tt_status analyse(tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_t
   return TT_OK;
 }
 
+// kernel variants: 0..2 classic cp.async + __syncthreads family, 3.. warp-specialised family
+int n_variants() { return num_contract_variants() + num_ws_variants(); }
+VariantInfo variant_info(int v) {
+  return v < num_contract_variants() ? contract_variant_info(v) : ws_variant_info(v - num_contract_variants());
+}
+// DMMA-pipe efficiency of each variant on unpadded work (calibrated on cfg2, profiles/r01_variants.txt)
+double variant_efficiency(int v) {
+  static const double eff[] = {0.70, 0.81, 0.75, 0.93, 0.63};
+  return v < (int)(sizeof(eff) / sizeof(eff[0])) ? eff[v] : 0.5;
+}
+
 // tiling of universal label u
 tt_tis label_tis(const Analysis& an, int u, tt_tensor C, tt_tensor A) {
   if (u < an.nc) return C->dims[u];
@@ -412,6 +423,7 @@ struct ContractPlan {
   std::vector<int> my;             // indices into ht.cblk computed by this rank
   GatherPlan gp;
   int variant = 0;
+  bool a_vec = false, b_vec = false;   // 16-byte copies along the operand's contiguous direction
   int64_t nwork = 0;
   CGroupDesc* d_groups = nullptr;
   TaskDesc* d_tasks = nullptr;
@@ -475,8 +487,9 @@ tt_status tt_ctx_create(int32_t device, void* stream, int32_t rank, int32_t nran
       delete c;
       return fail(TT_E_UNSUPPORTED, "libtt is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
     }
-    for (int v = 0; v < num_contract_variants(); ++v) {
-      cudaError_t e2 = contract_variant_setup(v);
+    for (int v = 0; v < n_variants(); ++v) {
+      cudaError_t e2 = v < num_contract_variants() ? contract_variant_setup(v)
+                                                   : ws_variant_setup(v - num_contract_variants());
       if (e2 != cudaSuccess) {
         delete c;
         return fail(TT_E_CUDA, "kernel setup: %s", cudaGetErrorString(e2));
@@ -1246,15 +1259,29 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     Ms[g] = M;
     Ns[g] = N;
   }
+  // 16-B copies: the operand's innermost dim is the innermost label of its contiguous group, with
+  // even extent in every tile
+  {
+    auto even = [&](int u) {
+      for (int t = 0; t < lt[u]->ntiles(); ++t)
+        if (lt[u]->size(t) % 2) return false;
+      return true;
+    };
+    const int a_last = an.a_lab.back(), b_last = an.b_lab.back();
+    const int a_grp_last = an.a_kc ? an.kg.back().back() : an.mg.back().back();
+    const int b_grp_last = an.b_nc ? an.ng.back().back() : an.kg.back().back();
+    pl.a_vec = a_last == a_grp_last && even(a_last);
+    pl.b_vec = b_last == b_grp_last && even(b_last);
+  }
   double best = -1;
-  for (int v = 0; v < num_contract_variants(); ++v) {
-    VariantInfo vi = contract_variant_info(v);
+  for (int v = 0; v < n_variants(); ++v) {
+    VariantInfo vi = variant_info(v);
     std::vector<double> items;
     for (int g : pl.my) {
       double kst = 0;
       for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) kst += (double)((ht.K[t] + vi.bk - 1) / vi.bk);
       const int64_t nit = ((Ms[g] + vi.bm - 1) / vi.bm) * ((Ns[g] + vi.bn - 1) / vi.bn);
-      const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm;
+      const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm / variant_efficiency(v);
       for (int64_t i = 0; i < nit; ++i) items.push_back(c);
     }
     std::sort(items.begin(), items.end(), std::greater<double>());
@@ -1272,8 +1299,8 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       pl.variant = v;
     }
   }
-  if (const char* fv = getenv("TT_FORCE_VARIANT")) pl.variant = atoi(fv) % num_contract_variants();
-  VariantInfo vi = contract_variant_info(pl.variant);
+  if (const char* fv = getenv("TT_FORCE_VARIANT")) pl.variant = atoi(fv) % n_variants();
+  VariantInfo vi = variant_info(pl.variant);
 
   // ---- groups + work items (groups by cost desc, block id asc)
   std::vector<int> order(pl.my);
@@ -1373,7 +1400,11 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   p.beta = beta;
   {
     Launch L(ctx, "tt_contract_dmma");
-    TT_CUDA(launch_contract(pl->variant, pl->an.a_kc, pl->an.b_nc, p, pl->nwork, ctx->stream));
+    if (pl->variant < num_contract_variants())
+      TT_CUDA(launch_contract(pl->variant, pl->an.a_kc, pl->an.b_nc, p, pl->nwork, ctx->stream));
+    else
+      TT_CUDA(launch_contract_ws(pl->variant - num_contract_variants(), pl->an.a_kc, pl->an.b_nc, pl->a_vec,
+                                 pl->b_vec, p, pl->nwork, ctx->stream));
   }
   ctx->last.c_blocks = (int64_t)pl->my.size();
   ctx->last.tasks = pl->tasks;

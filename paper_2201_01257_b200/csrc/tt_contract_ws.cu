@@ -1,0 +1,369 @@
+// tt_contract_ws.cu -- warp-specialised block-sparse FP64 contraction kernel for sm_100a.
+//
+// Same work decomposition and descriptors as tt_contract_kernel (tt_kernels.cu), reorganised for
+// Blackwell's asynchronous pipeline style:
+//   * PRODUCER warps (one per operand) stream the A and B tiles of every (task, BK slice) straight
+//     from their native block layout into a STAGES-deep shared-memory ring with cp.async (16-byte
+//     copies along the operand's contiguous direction when its innermost extent is even), and
+//     signal a per-stage "full" mbarrier with cp.async.mbarrier.arrive.noinc.  The index
+//     permutation of each operand (TAMM's HPTT/LibreTT pass, P107/P220) is folded into these source
+//     addresses via the label-group strides of the task descriptor.
+//   * MMA warps wait on "full", load fragments and issue FP64 tensor-core MMAs (mma.sync m8n8k4 ->
+//     DMMA.8x8x4), then release the slot on an "empty" mbarrier.  No CTA-wide barrier in the loop.
+//   * Shared-memory layouts are chosen so that both the cp.async writes and the fragment loads are
+//     bank-conflict free: the contiguous direction of the operand stays contiguous in smem;
+//     k-contiguous tiles use rows of BK+8 doubles (row stride = 64 mod 128 B, fragment loads are
+//     128-bit and cover two DMMA k-steps), row-contiguous tiles use rows of R+2 doubles (row stride
+//     = 16 mod 64 B, the two k-steps of an 8-wide k octet use k = 2*(lane%4) + t).
+//   * Accumulation over all pairs of an output tile stays in registers in canonical task order
+//     (deterministic, reading R12); epilogue C = beta*C + alpha*acc through the C strides.
+#include <cstdint>
+
+#include "tt_launch.h"
+
+namespace tt {
+
+namespace ws {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(s));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(s) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(s),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int32_t dot_decode(int32_t idx, int n, const int32_t* ext, const int32_t* str) {
+  int32_t off = 0;
+#pragma unroll
+  for (int g = kMaxGroup - 1; g > 0; --g) {
+    if (g < n) {
+      int32_t q = idx / ext[g];
+      off += (idx - q * ext[g]) * str[g];
+      idx = q;
+    }
+  }
+  return off + idx * str[0];
+}
+
+// Shared-memory geometry of one operand tile (R rows = BM or BN, BK k's).
+template <int R, int BK, bool KC>
+struct Tile {
+  static constexpr int LD = KC ? (BK + 8) : (R + 2);     // doubles per smem row
+  static constexpr int ELEMS = KC ? R * LD : BK * LD;     // doubles per stage
+};
+
+// Copy geometry of one operand for one producer warp.
+//   KC (k contiguous in global and smem):  lane -> (row = lane / 8, k unit = lane % 8); a k unit is
+//       a 16-B pair (VEC) or, without VEC, two single doubles k and k+8.  NR = R/4 rows per lane.
+//   !KC (rows contiguous): lane -> (row unit = lane % QL, k = lane / QL + (32/QL)*j); a row unit is
+//       a 16-B pair (VEC) or a single double.  NR row units per lane, NK k values per lane.
+template <int R, int BK, bool KC, bool VEC>
+struct Copy {
+  static constexpr int RU = VEC ? 2 : 1;                            // rows per unit (row-contig)
+  static constexpr int QL = KC ? 8 : ((R / RU) % 32 == 0 ? 32 : ((R / RU) % 16 == 0 ? 16 : 8));
+  static constexpr int NR = KC ? R / 4 : (R / RU) / QL;
+  static constexpr int NK = KC ? (VEC ? 1 : 2) : BK / (32 / QL);
+  static_assert(KC ? (R % 4 == 0) : ((R / RU) % QL == 0), "copy geometry");
+  static_assert(KC || (BK % (32 / QL) == 0), "copy geometry k");
+};
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct WCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int NMMA = WM * WN, NPROD = 2, NW = NMMA + NPROD, NTHREADS = NW * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN, MT = WTM / 8, NT = WTN / 8;
+  static_assert(BK % 8 == 0, "BK multiple of 8 (k octets)");
+};
+
+template <class K, bool AKC, bool BNC>
+struct Smem {
+  static constexpr bool BKC = !BNC;
+  using TA = Tile<K::BM, K::BK, AKC>;
+  using TB = Tile<K::BN, K::BK, BKC>;
+  static constexpr int A_ELEMS = TA::ELEMS, B_ELEMS = TB::ELEMS;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr int BYTES = K::STAGES * STAGE * 8 + 2 * K::STAGES * 8 + 256;
+};
+
+// Producer: stream one operand.  ROWS = BM (A) or BN (B); KC = k contiguous.
+template <class K, int ROWS, bool KC, bool VEC>
+__device__ __forceinline__ void produce(const ContractParams& p, const CGroupDesc& g, int row0, bool isA,
+                                        double* sbase, int stage_elems, int ld, uint64_t* full, uint64_t* empty) {
+  using C = Copy<ROWS, K::BK, KC, VEC>;
+  const int lane = threadIdx.x & 31;
+  const int nG = isA ? p.nM : p.nN;                 // row groups
+  const int nK = p.nK;
+  const int32_t* rext = isA ? g.mext : g.next;
+  const int ROWMAX = isA ? g.M : g.N;
+  // lane geometry
+  const int r_l = KC ? (lane >> 3) : (lane % C::QL) * C::RU;   // first row of the lane
+  const int k_l = KC ? (lane & 7) * (VEC ? 2 : 1) : (lane / C::QL);
+  const int r_step = KC ? 4 : C::QL * C::RU;
+  const int k_step = KC ? 8 : 32 / C::QL;          // (!VEC KC: second k at +8)
+  int32_t roff[C::NR];
+  int32_t kext[kMaxGroup], kst[kMaxGroup];
+  const double* base = nullptr;
+  int32_t Kt = 0;
+  int t = g.task_begin, k0 = 0, st = 0;
+  unsigned phase = 1;   // empty barriers: first wait passes
+  auto setup = [&](int tt_) {
+    const TaskDesc* td = p.tasks + tt_;
+    base = isA ? p.A + td->a_off : p.B + td->b_off;
+    Kt = td->K;
+    int32_t rst[kMaxGroup];
+#pragma unroll
+    for (int i = 0; i < kMaxGroup; ++i) {
+      kext[i] = td->kext[i];
+      kst[i] = isA ? td->ak_str[i] : td->bk_str[i];
+      rst[i] = isA ? td->am_str[i] : td->bn_str[i];
+    }
+#pragma unroll
+    for (int i = 0; i < C::NR; ++i) {
+      const int r = row0 + r_l + r_step * i;
+      roff[i] = (r < ROWMAX) ? dot_decode(r, nG, rext, rst) : -1;
+    }
+  };
+  if (t < g.task_end) setup(t);
+  const int nst = g.nstages;
+  for (int s = 0; s < nst; ++s) {
+    mbar_wait(&empty[st], phase);
+    double* dst = sbase + st * stage_elems;
+#pragma unroll
+    for (int j = 0; j < C::NK; ++j) {
+      const int kl = k_l + k_step * j;
+      const int k = k0 + kl;
+      const bool kv = k < Kt;
+      const int32_t ko = kv ? dot_decode(k, nK, kext, kst) : 0;
+#pragma unroll
+      for (int i = 0; i < C::NR; ++i) {
+        const int rl = r_l + r_step * i;
+        const bool v = kv && roff[i] >= 0;
+        const double* src = v ? base + roff[i] + ko : p.A;
+        double* d = KC ? dst + rl * ld + kl : dst + kl * ld + rl;
+        if (VEC) cp_async16(d, src, v);
+        else cp_async8(d, src, v);
+      }
+    }
+    mbar_arrive_cp_async(&full[st]);
+    k0 += K::BK;
+    if (k0 >= Kt) {
+      k0 = 0;
+      ++t;
+      if (t < g.task_end) setup(t);
+    }
+    if (++st == K::STAGES) { st = 0; phase ^= 1; }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+template <class K, bool AKC, bool BNC, bool AVEC, bool BVEC>
+__global__ void __launch_bounds__(K::NTHREADS, 1) tt_contract_ws_kernel(const ContractParams p) {
+  using SM = Smem<K, AKC, BNC>;
+  constexpr bool BKC = !BNC;
+  extern __shared__ __align__(128) double smem[];
+  double* sA = smem;
+  double* sB = smem + K::STAGES * SM::A_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + K::STAGES * SM::STAGE);
+  uint64_t* empty = full + K::STAGES;
+  __shared__ CGroupDesc g;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const WorkItem w = p.work[blockIdx.x];
+  if (tid == 0) {
+    g = p.groups[w.group];
+    for (int s = 0; s < K::STAGES; ++s) {
+      mbar_init(&full[s], 2 * 32);        // every producer thread arrives once per stage
+      mbar_init(&empty[s], K::NMMA);      // one arrival per MMA warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int m0 = w.mt * K::BM, n0 = w.nt * K::BN;
+
+  if (warp >= K::NMMA) {
+    // ------------------------------------------------------------- producers
+    if (warp == K::NMMA)
+      produce<K, K::BM, AKC, AVEC>(p, g, m0, true, sA, SM::A_ELEMS, SM::TA::LD, full, empty);
+    else
+      produce<K, K::BN, BKC, BVEC>(p, g, n0, false, sB, SM::B_ELEMS, SM::TB::LD, full, empty);
+    return;
+  }
+
+  // --------------------------------------------------------------- MMA warps
+  const int wm = warp / K::WN, wn = warp % K::WN;
+  double acc[K::MT][K::NT][2];
+#pragma unroll
+  for (int i = 0; i < K::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < K::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int q = lane & 3, r8 = lane >> 2;
+  const int nst = g.nstages;
+  int st = 0;
+  unsigned phase = 0;
+  for (int s = 0; s < nst; ++s) {
+    mbar_wait(&full[st], phase);
+    const double* a = sA + st * SM::A_ELEMS;
+    const double* b = sB + st * SM::B_ELEMS;
+#pragma unroll
+    for (int o = 0; o < K::BK / 8; ++o) {
+      double af[K::MT][2], bf[K::NT][2];
+#pragma unroll
+      for (int i = 0; i < K::MT; ++i) {
+        const int m = wm * K::WTM + i * 8 + r8;
+        if (AKC) {
+          const double2 v = *reinterpret_cast<const double2*>(a + m * SM::TA::LD + 8 * o + 2 * q);
+          af[i][0] = v.x;
+          af[i][1] = v.y;
+        } else {
+          af[i][0] = a[(8 * o + 2 * q) * SM::TA::LD + m];
+          af[i][1] = a[(8 * o + 2 * q + 1) * SM::TA::LD + m];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < K::NT; ++j) {
+        const int n = wn * K::WTN + j * 8 + r8;
+        if (BKC) {
+          const double2 v = *reinterpret_cast<const double2*>(b + n * SM::TB::LD + 8 * o + 2 * q);
+          bf[j][0] = v.x;
+          bf[j][1] = v.y;
+        } else {
+          bf[j][0] = b[(8 * o + 2 * q) * SM::TB::LD + n];
+          bf[j][1] = b[(8 * o + 2 * q + 1) * SM::TB::LD + n];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int i = 0; i < K::MT; ++i)
+#pragma unroll
+          for (int j = 0; j < K::NT; ++j) dmma884(acc[i][j], af[i][t], bf[j][t]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (++st == K::STAGES) { st = 0; phase ^= 1; }
+  }
+
+  // epilogue
+  double* Cb = p.C + g.c_off;
+  const double alpha = p.alpha, beta = p.beta;
+  const int M = g.M, N = g.N;
+#pragma unroll
+  for (int i = 0; i < K::MT; ++i) {
+    const int m = m0 + wm * K::WTM + i * 8 + r8;
+    if (m >= M) continue;
+    const int32_t om = dot_decode(m, p.nM, g.mext, g.cm_str);
+#pragma unroll
+    for (int j = 0; j < K::NT; ++j) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int n = n0 + wn * K::WTN + j * 8 + 2 * q + r;
+        if (n >= N) continue;
+        double* c = Cb + om + dot_decode(n, p.nN, g.next, g.cn_str);
+        const double v = alpha * acc[i][j][r];
+        *c = (beta == 0.0) ? v : beta * *c + v;
+      }
+    }
+  }
+}
+
+using W0 = WCfg<160, 80, 16, 4, 2, 4>;    // 8 MMA warps (warp tile 40x40) + 2 producer warps
+using W1 = WCfg<128, 128, 16, 2, 4, 4>;   // 8 MMA warps (warp tile 64x32) + 2 producer warps
+
+template <class K, bool AKC, bool BNC, bool AV, bool BV>
+static cudaError_t setup_one() {
+  return cudaFuncSetAttribute(tt_contract_ws_kernel<K, AKC, BNC, AV, BV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Smem<K, AKC, BNC>::BYTES);
+}
+template <class K, bool AKC, bool BNC>
+static cudaError_t setup_orient() {
+  cudaError_t e;
+  if ((e = setup_one<K, AKC, BNC, true, true>()) != cudaSuccess) return e;
+  if ((e = setup_one<K, AKC, BNC, true, false>()) != cudaSuccess) return e;
+  if ((e = setup_one<K, AKC, BNC, false, true>()) != cudaSuccess) return e;
+  return setup_one<K, AKC, BNC, false, false>();
+}
+template <class K>
+static cudaError_t setup_cfg() {
+  cudaError_t e;
+  if ((e = setup_orient<K, true, true>()) != cudaSuccess) return e;
+  if ((e = setup_orient<K, true, false>()) != cudaSuccess) return e;
+  if ((e = setup_orient<K, false, true>()) != cudaSuccess) return e;
+  return setup_orient<K, false, false>();
+}
+
+template <class K, bool AKC, bool BNC, bool AV, bool BV>
+static cudaError_t launch_one(const ContractParams& p, int64_t nwork, cudaStream_t s) {
+  tt_contract_ws_kernel<K, AKC, BNC, AV, BV><<<(unsigned)nwork, K::NTHREADS, Smem<K, AKC, BNC>::BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+template <class K, bool AKC, bool BNC>
+static cudaError_t launch_orient(bool av, bool bv, const ContractParams& p, int64_t nwork, cudaStream_t s) {
+  if (av && bv) return launch_one<K, AKC, BNC, true, true>(p, nwork, s);
+  if (av) return launch_one<K, AKC, BNC, true, false>(p, nwork, s);
+  if (bv) return launch_one<K, AKC, BNC, false, true>(p, nwork, s);
+  return launch_one<K, AKC, BNC, false, false>(p, nwork, s);
+}
+template <class K>
+static cudaError_t launch_cfg(bool akc, bool bnc, bool av, bool bv, const ContractParams& p, int64_t nwork,
+                              cudaStream_t s) {
+  if (akc && bnc) return launch_orient<K, true, true>(av, bv, p, nwork, s);
+  if (akc) return launch_orient<K, true, false>(av, bv, p, nwork, s);
+  if (bnc) return launch_orient<K, false, true>(av, bv, p, nwork, s);
+  return launch_orient<K, false, false>(av, bv, p, nwork, s);
+}
+
+}  // namespace ws
+
+int num_ws_variants() { return 2; }
+
+VariantInfo ws_variant_info(int v) {
+  using namespace ws;
+  // smem is the worst case over orientations (both operands k-contiguous)
+  if (v == 0) return {W0::BM, W0::BN, W0::BK, W0::NTHREADS, Smem<W0, true, false>::BYTES, 1, "ws160x80x16"};
+  return {W1::BM, W1::BN, W1::BK, W1::NTHREADS, Smem<W1, true, false>::BYTES, 1, "ws128x128x16"};
+}
+
+cudaError_t ws_variant_setup(int v) {
+  return v == 0 ? ws::setup_cfg<ws::W0>() : ws::setup_cfg<ws::W1>();
+}
+
+cudaError_t launch_contract_ws(int v, bool akc, bool bnc, bool avec, bool bvec, const ContractParams& p,
+                               int64_t nwork, cudaStream_t s) {
+  if (nwork <= 0) return cudaSuccess;
+  return v == 0 ? ws::launch_cfg<ws::W0>(akc, bnc, avec, bvec, p, nwork, s)
+                : ws::launch_cfg<ws::W1>(akc, bnc, avec, bvec, p, nwork, s);
+}
+
+}  // namespace tt

@@ -65,6 +65,13 @@ cudaError_t launch_contract(int variant, bool a_kcontig, bool b_ncontig, const C
                             int64_t nwork, cudaStream_t s);
 cudaError_t contract_variant_setup(int variant);   // opt-in shared memory sizes
 
+// Warp-specialised family (tt_contract_ws.cu): producer warps + mbarrier ring.
+int num_ws_variants();
+VariantInfo ws_variant_info(int v);
+cudaError_t ws_variant_setup(int v);
+cudaError_t launch_contract_ws(int v, bool a_kcontig, bool b_ncontig, bool a_vec, bool b_vec,
+                               const ContractParams& p, int64_t nwork, cudaStream_t s);
+
 // Segment-based element kernels (set / add / scalar / synthetic fill).
 struct Segment {
   int32_t desc;       // block descriptor index

@@ -85,7 +85,7 @@ def test_contract_parity(env, name):
     assert normwise(got, ref) <= TOL, normwise(got, ref)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_every_tile_variant(env, variant):
     tt, torch = env
     pb = ccsd_problem(24, 80, 12, 20, True, terms=("ladder", "ring"))
@@ -116,19 +116,25 @@ def test_beta_zero_never_reads_c(env):
         assert normwise(got, np.nan_to_num(ref)) <= TOL
 
 
-def test_permuted_labels(env):
+@pytest.mark.parametrize("variant", [None, 1, 3, 4])
+@pytest.mark.parametrize("even", [False, True])
+def test_permuted_labels(env, variant, even):
     """Operands whose innermost labels are free/contracted in every combination (all four kernel
-    orientations), output permuted relative to both."""
+    orientations; with even tiles also the 16-byte copy paths), output permuted relative to both."""
     tt, torch = env
-    spaces = {"X": SpaceSpec(11, tile=4), "Y": SpaceSpec(9, tile=5), "Z": SpaceSpec(10, tile=3)}
+    if even:
+        spaces = {"X": SpaceSpec(12, tile=4), "Y": SpaceSpec(10, tile=6), "Z": SpaceSpec(14, tile=8)}
+    else:
+        spaces = {"X": SpaceSpec(11, tile=4), "Y": SpaceSpec(9, tile=5), "Z": SpaceSpec(10, tile=3)}
     ls = {"a": "X", "b": "Y", "c": "Z", "i": "Y", "j": "X", "k": "Z"}
-    ctx = new_ctx(tt, torch)
+    ctx = new_ctx(tt, torch, variant)
     for cl, al, bl in [("jbia", "kcai", "bjck"), ("abij", "iack", "kcjb"), ("ijab", "akci", "jbkc"),
                        ("bjai", "ciak", "cbkj")]:
         tens = {"C": TensorSpec(cl), "A": TensorSpec(al), "B": TensorSpec(bl)}
         pb = Problem(spaces, ls, tens, [("C", cl, "A", al, "B", bl)])
         got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[0], alpha=1.0, beta=0.5)
         assert normwise(got, ref) <= TOL, (cl, al, bl)
+    os.environ.pop("TT_FORCE_VARIANT", None)
 
 
 def test_c_blocks_without_tasks(env):
