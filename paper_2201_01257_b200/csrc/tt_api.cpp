@@ -234,7 +234,7 @@ VariantInfo variant_info(int v) {
 }
 // DMMA-pipe efficiency of each variant on unpadded work (calibrated on cfg2, profiles/r01_variants.txt)
 double variant_efficiency(int v) {
-  static const double eff[] = {0.70, 0.81, 0.75, 0.93, 0.63};
+  static const double eff[] = {0.70, 0.81, 0.75, 0.925, 0.915, 0.95};
   return v < (int)(sizeof(eff) / sizeof(eff[0])) ? eff[v] : 0.5;
 }
 

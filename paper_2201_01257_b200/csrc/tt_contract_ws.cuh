@@ -1,4 +1,4 @@
-// tt_contract_ws.cu -- warp-specialised block-sparse FP64 contraction kernel for sm_100a.
+// tt_contract_ws.cuh -- warp-specialised block-sparse FP64 contraction kernel for sm_100a.
 //
 // Same work decomposition and descriptors as tt_contract_kernel (tt_kernels.cu), reorganised for
 // Blackwell's asynchronous pipeline style:
@@ -17,6 +17,7 @@
 //     = 16 mod 64 B, the two k-steps of an 8-wide k octet use k = 2*(lane%4) + t).
 //   * Accumulation over all pairs of an output tile stays in registers in canonical task order
 //     (deterministic, reading R12); epilogue C = beta*C + alpha*acc through the C strides.
+#pragma once
 #include <cstdint>
 
 #include "tt_launch.h"
@@ -56,6 +57,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       " @!p bra WAIT_%=;\n}\n" ::"r"(s),
       "r"(parity)
       : "memory");
+}
+// producer-side wait: back off so that idle producers do not take issue slots from the MMA warps
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(s), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
 }
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -98,9 +113,9 @@ struct Copy {
   static_assert(KC || (BK % (32 / QL) == 0), "copy geometry k");
 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int MAXSTAGES_, int MINB_>
 struct WCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, MAXSTAGES = MAXSTAGES_, MINB = MINB_;
   static constexpr int NMMA = WM * WN, NPROD = 2, NW = NMMA + NPROD, NTHREADS = NW * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN, MT = WTM / 8, NT = WTN / 8;
   static_assert(BK % 8 == 0, "BK multiple of 8 (k octets)");
@@ -113,11 +128,16 @@ struct Smem {
   using TB = Tile<K::BN, K::BK, BKC>;
   static constexpr int A_ELEMS = TA::ELEMS, B_ELEMS = TB::ELEMS;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr int BYTES = K::STAGES * STAGE * 8 + 2 * K::STAGES * 8 + 256;
+  // as many stages as fit the shared-memory budget of MINB CTAs per SM (227 KB per SM usable)
+  static constexpr int BUDGET = (227 * 1024) / K::MINB - 1024;
+  static constexpr int FIT = BUDGET / (STAGE * 8 + 16);
+  static constexpr int STAGES = FIT < K::MAXSTAGES ? FIT : K::MAXSTAGES;
+  static constexpr int BYTES = STAGES * STAGE * 8 + 2 * STAGES * 8 + 256;
+  static_assert(STAGES >= 3, "pipeline too shallow");
 };
 
 // Producer: stream one operand.  ROWS = BM (A) or BN (B); KC = k contiguous.
-template <class K, int ROWS, bool KC, bool VEC>
+template <class K, int STAGES, int ROWS, bool KC, bool VEC>
 __device__ __forceinline__ void produce(const ContractParams& p, const CGroupDesc& g, int row0, bool isA,
                                         double* sbase, int stage_elems, int ld, uint64_t* full, uint64_t* empty) {
   using C = Copy<ROWS, K::BK, KC, VEC>;
@@ -157,7 +177,7 @@ __device__ __forceinline__ void produce(const ContractParams& p, const CGroupDes
   if (t < g.task_end) setup(t);
   const int nst = g.nstages;
   for (int s = 0; s < nst; ++s) {
-    mbar_wait(&empty[st], phase);
+    mbar_wait_sleep(&empty[st], phase);
     double* dst = sbase + st * stage_elems;
 #pragma unroll
     for (int j = 0; j < C::NK; ++j) {
@@ -182,27 +202,28 @@ __device__ __forceinline__ void produce(const ContractParams& p, const CGroupDes
       ++t;
       if (t < g.task_end) setup(t);
     }
-    if (++st == K::STAGES) { st = 0; phase ^= 1; }
+    if (++st == STAGES) { st = 0; phase ^= 1; }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 template <class K, bool AKC, bool BNC, bool AVEC, bool BVEC>
-__global__ void __launch_bounds__(K::NTHREADS, 1) tt_contract_ws_kernel(const ContractParams p) {
+__global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(const ContractParams p) {
   using SM = Smem<K, AKC, BNC>;
   constexpr bool BKC = !BNC;
   extern __shared__ __align__(128) double smem[];
   double* sA = smem;
-  double* sB = smem + K::STAGES * SM::A_ELEMS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + K::STAGES * SM::STAGE);
-  uint64_t* empty = full + K::STAGES;
+  constexpr int STAGES = SM::STAGES;
+  double* sB = smem + STAGES * SM::A_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::STAGE);
+  uint64_t* empty = full + STAGES;
   __shared__ CGroupDesc g;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const WorkItem w = p.work[blockIdx.x];
   if (tid == 0) {
     g = p.groups[w.group];
-    for (int s = 0; s < K::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 2 * 32);        // every producer thread arrives once per stage
       mbar_init(&empty[s], K::NMMA);      // one arrival per MMA warp
     }
@@ -214,9 +235,9 @@ __global__ void __launch_bounds__(K::NTHREADS, 1) tt_contract_ws_kernel(const Co
   if (warp >= K::NMMA) {
     // ------------------------------------------------------------- producers
     if (warp == K::NMMA)
-      produce<K, K::BM, AKC, AVEC>(p, g, m0, true, sA, SM::A_ELEMS, SM::TA::LD, full, empty);
+      produce<K, STAGES, K::BM, AKC, AVEC>(p, g, m0, true, sA, SM::A_ELEMS, SM::TA::LD, full, empty);
     else
-      produce<K, K::BN, BKC, BVEC>(p, g, n0, false, sB, SM::B_ELEMS, SM::TB::LD, full, empty);
+      produce<K, STAGES, K::BN, BKC, BVEC>(p, g, n0, false, sB, SM::B_ELEMS, SM::TB::LD, full, empty);
     return;
   }
 
@@ -272,7 +293,7 @@ __global__ void __launch_bounds__(K::NTHREADS, 1) tt_contract_ws_kernel(const Co
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    if (++st == K::STAGES) { st = 0; phase ^= 1; }
+    if (++st == STAGES) { st = 0; phase ^= 1; }
   }
 
   // epilogue
@@ -297,9 +318,6 @@ __global__ void __launch_bounds__(K::NTHREADS, 1) tt_contract_ws_kernel(const Co
     }
   }
 }
-
-using W0 = WCfg<160, 80, 16, 4, 2, 4>;    // 8 MMA warps (warp tile 40x40) + 2 producer warps
-using W1 = WCfg<128, 128, 16, 2, 4, 4>;   // 8 MMA warps (warp tile 64x32) + 2 producer warps
 
 template <class K, bool AKC, bool BNC, bool AV, bool BV>
 static cudaError_t setup_one() {
@@ -343,27 +361,27 @@ static cudaError_t launch_cfg(bool akc, bool bnc, bool av, bool bv, const Contra
   if (bnc) return launch_orient<K, false, true>(av, bv, p, nwork, s);
   return launch_orient<K, false, false>(av, bv, p, nwork, s);
 }
+template <class K>
+static VariantInfo info_cfg(const char* name) {
+  // shared memory: worst case over orientations
+  int smem = Smem<K, true, false>::BYTES;
+  if (Smem<K, true, true>::BYTES > smem) smem = Smem<K, true, true>::BYTES;
+  if (Smem<K, false, true>::BYTES > smem) smem = Smem<K, false, true>::BYTES;
+  if (Smem<K, false, false>::BYTES > smem) smem = Smem<K, false, false>::BYTES;
+  return {K::BM, K::BN, K::BK, K::NTHREADS, smem, K::MINB, name};
+}
+
+// One translation unit per tile configuration (parallel compilation):
+#define TT_WS_DEFINE(NAME, CFG, LABEL)                                                              \
+  namespace tt {                                                                                   \
+  VariantInfo ws_info_##NAME() { return ws::info_cfg<CFG>(LABEL); }                                \
+  cudaError_t ws_setup_##NAME() { return ws::setup_cfg<CFG>(); }                                  \
+  cudaError_t ws_launch_##NAME(bool akc, bool bnc, bool av, bool bv, const ContractParams& p,      \
+                               int64_t nwork, cudaStream_t s) {                                    \
+    return ws::launch_cfg<CFG>(akc, bnc, av, bv, p, nwork, s);                                     \
+  }                                                                                                \
+  }
 
 }  // namespace ws
-
-int num_ws_variants() { return 2; }
-
-VariantInfo ws_variant_info(int v) {
-  using namespace ws;
-  // smem is the worst case over orientations (both operands k-contiguous)
-  if (v == 0) return {W0::BM, W0::BN, W0::BK, W0::NTHREADS, Smem<W0, true, false>::BYTES, 1, "ws160x80x16"};
-  return {W1::BM, W1::BN, W1::BK, W1::NTHREADS, Smem<W1, true, false>::BYTES, 1, "ws128x128x16"};
-}
-
-cudaError_t ws_variant_setup(int v) {
-  return v == 0 ? ws::setup_cfg<ws::W0>() : ws::setup_cfg<ws::W1>();
-}
-
-cudaError_t launch_contract_ws(int v, bool akc, bool bnc, bool avec, bool bvec, const ContractParams& p,
-                               int64_t nwork, cudaStream_t s) {
-  if (nwork <= 0) return cudaSuccess;
-  return v == 0 ? ws::launch_cfg<ws::W0>(akc, bnc, avec, bvec, p, nwork, s)
-                : ws::launch_cfg<ws::W1>(akc, bnc, avec, bvec, p, nwork, s);
-}
 
 }  // namespace tt

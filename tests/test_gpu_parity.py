@@ -85,7 +85,7 @@ def test_contract_parity(env, name):
     assert normwise(got, ref) <= TOL, normwise(got, ref)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_every_tile_variant(env, variant):
     tt, torch = env
     pb = ccsd_problem(24, 80, 12, 20, True, terms=("ladder", "ring"))
@@ -116,7 +116,7 @@ def test_beta_zero_never_reads_c(env):
         assert normwise(got, np.nan_to_num(ref)) <= TOL
 
 
-@pytest.mark.parametrize("variant", [None, 1, 3, 4])
+@pytest.mark.parametrize("variant", [None, 1, 3, 4, 5])
 @pytest.mark.parametrize("even", [False, True])
 def test_permuted_labels(env, variant, even):
     """Operands whose innermost labels are free/contracted in every combination (all four kernel
