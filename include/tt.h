@@ -209,11 +209,15 @@ tt_status tt_task_list(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, 
                        int64_t* a_blk, int64_t* b_blk, int64_t* cost, int64_t cap,
                        int64_t* n_cblocks, int64_t* n_tasks);
 
-/* LPT owner partition of C's non-zero blocks over the context's nranks (R24): blocks sorted by
- * (cost desc, block id asc), each to the least-loaded rank, ties to the lowest rank.  Writes
- * owner[nblocks of C] (-1 for zero blocks).  Does not modify C (use tt_tensor_set_owner). */
+/* LPT owner partition of C's non-zero blocks over the context's nranks (R24): units sorted by
+ * (cost desc, smallest block id asc), each to the least-loaded rank, ties to the lowest rank.
+ *   group_mask  0: every non-zero C block is a unit.  Otherwise bit d set = C dimension d is a
+ *               grouping dimension: blocks with equal tile coordinates on all grouping dimensions
+ *               form one unit (e.g. the (a,b) rows of R(a,b,i,j) with mask 0b0011, so that the
+ *               V(a,b,c,d) rows each rank reads are its own).  Unit cost = sum of block costs.
+ * Writes owner[nblocks of C] (-1 for zero blocks).  Does not modify C (use tt_tensor_set_owner). */
 tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
-                           tt_tensor B, const char* b_lbl, int32_t* owner);
+                           tt_tensor B, const char* b_lbl, uint32_t group_mask, int32_t* owner);
 
 /* Input-tile gather plan of this rank for tt_contract (host metadata; for tests and reports).
  * recv[3*i .. 3*i+2] = (operand 0=A/1=B, block id, source rank) for each block this rank receives;

@@ -289,3 +289,20 @@ def lpt_partition(cost: Sequence[int], cblocks: Sequence[int], nranks: int) -> L
         owner[i] = r
         load[r] += cost[i]
     return owner
+
+
+def lpt_partition_grouped(C: Tensor, cost: Sequence[int], cblocks: Sequence[int], group_dims: Sequence[int],
+                          nranks: int) -> List[int]:
+    """LPT over units of C blocks sharing the tile coordinates of ``group_dims`` (R24); unit cost =
+    sum of its blocks' costs, unit id = its smallest block id.  Returns the owner of each C block."""
+    units, ucost, uid, unit_of = {}, [], [], []
+    for c, b in zip(cost, cblocks):
+        key = tuple(C.block_coords(b)[d] for d in group_dims) if group_dims else (b,)
+        if key not in units:
+            units[key] = len(ucost)
+            ucost.append(0)
+            uid.append(b)
+        ucost[units[key]] += c
+        unit_of.append(units[key])
+    uown = lpt_partition(ucost, uid, nranks)
+    return [uown[u] for u in unit_of]

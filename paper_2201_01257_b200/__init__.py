@@ -78,7 +78,7 @@ _SIGS = {
     "tt_contract_scalar": [_vp, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _P(_dbl)],
     "tt_task_list": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _i32, _vp, _vp, _vp,
                      _vp, _vp, _i64, _P(_i64), _P(_i64)],
-    "tt_partition_lpt": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp],
+    "tt_partition_lpt": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32, _vp],
     "tt_gather_plan": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _P(_i64), _vp,
                        _P(_i64), _i64],
     "tt_last_error": [],
@@ -339,9 +339,12 @@ def task_list(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Ten
     return {"cblk": cb, "ptr": ptr, "a_blk": ab[:nt.value], "b_blk": bb[:nt.value], "cost": cost}
 
 
-def partition_lpt(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str) -> np.ndarray:
+def partition_lpt(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str,
+                  group_dims: Sequence[int] = ()) -> np.ndarray:
+    """LPT owner partition (R24); ``group_dims`` = C dims whose tile coordinates define a unit."""
     own = np.empty(C.nblocks, np.int32)
-    _check(_lib.tt_partition_lpt(ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl), _ptr(own)))
+    mask = sum(1 << d for d in group_dims)
+    _check(_lib.tt_partition_lpt(ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl), mask, _ptr(own)))
     return own
 
 

@@ -1458,15 +1458,39 @@ tt_status tt_task_list(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, con
 }
 
 tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
-                           const char* bl, int32_t* owner) {
+                           const char* bl, uint32_t group_mask, int32_t* owner) {
   if (!ctx || !owner) return fail(TT_E_ARG, "NULL argument");
   Analysis an;
   TT_TRY(analyse(C, cl, A, al, B, bl, an));
+  if (group_mask >> C->order) return fail(TT_E_ARG, "group_mask references dims beyond the order of C");
   HostTasks ht;
   enumerate_tasks(an, C, A, B, ht);
-  std::vector<int32_t> own = lpt(ht.cost, ht.cblk, ctx->nranks);
+  // units: blocks sharing the tile coordinates of the grouping dims (group_mask = 0: single blocks)
+  std::map<std::vector<int32_t>, size_t> unit_of;
+  std::vector<int64_t> ucost, uid;
+  std::vector<size_t> unit(ht.cblk.size());
+  int32_t cc[TT_MAX_ORDER];
+  for (size_t g = 0; g < ht.cblk.size(); ++g) {
+    std::vector<int32_t> key;
+    if (group_mask) {
+      C->block_coords(ht.cblk[g], cc);
+      for (int d = 0; d < C->order; ++d)
+        if (group_mask >> d & 1) key.push_back(cc[d]);
+    } else {
+      key.push_back((int32_t)g);
+    }
+    auto it = unit_of.find(key);
+    if (it == unit_of.end()) {
+      it = unit_of.emplace(key, ucost.size()).first;
+      ucost.push_back(0);
+      uid.push_back(ht.cblk[g]);      // smallest block id of the unit (blocks visited in order)
+    }
+    unit[g] = it->second;
+    ucost[it->second] += ht.cost[g];
+  }
+  std::vector<int32_t> own = lpt(ucost, uid, ctx->nranks);
   for (int64_t b = 0; b < C->nblocks; ++b) owner[b] = -1;
-  for (size_t g = 0; g < ht.cblk.size(); ++g) owner[ht.cblk[g]] = own[g];
+  for (size_t g = 0; g < ht.cblk.size(); ++g) owner[ht.cblk[g]] = own[unit[g]];
   return TT_OK;
 }
 

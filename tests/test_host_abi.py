@@ -196,3 +196,22 @@ def test_gather_plan_exactly_needed_blocks(nranks):
         sends[me] = {(op, blk, me, peer) for op, blk, peer in s.tolist()}
         recvs[me] = {(op, blk, peer, me) for op, blk, peer in r.tolist()}
     assert set().union(*sends.values()) == set().union(*recvs.values())
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_lpt_grouped_matches_oracle(nranks):
+    """LPT over (a,b) rows of R (group dims 0,1), so each rank owns whole rows (R24)."""
+    c = tt.Context(device=-1, nranks=nranks)
+    pb = ccsd_problem(12, 20, 3, 4, True)
+    orc = oracle_objects(pb, nranks)
+    prod = product_objects(tt, c, pb)
+    C, cl, a, al, b, bl = pb.ops[0]
+    ocb, _, _, _, ocost = L.task_list(orc[C], cl, orc[a], al, orc[b], bl)
+    oown = L.lpt_partition_grouped(orc[C], ocost, ocb, [0, 1], nranks)
+    own = tt.partition_lpt(c, prod[C], cl, prod[a], al, prod[b], bl, group_dims=(0, 1))
+    assert [own[x] for x in ocb] == oown
+    rows = {}
+    for x in ocb:
+        key = orc[C].block_coords(x)[:2]
+        rows.setdefault(key, set()).add(own[x])
+    assert all(len(v) == 1 for v in rows.values())
