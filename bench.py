@@ -1,19 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark of the hot path: BASELINE.json configs[1], the CCSD particle-particle ladder
-R(a,b,i,j) += V(a,b,c,d) * T(c,d,i,j), O=40 V=200 tile=40, FP64, on B200.
+"""Benchmark of the hot path on B200.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config cfg2|cfg3]
 
-One step = one tt_contract call (task list and partition cached; input-tile gather over NCCL when
-N > 1; the DMMA contraction kernel) over the whole tensor.  value = algorithmic FLOPs of all ranks
-/ max over ranks of the device time (CUDA events on the context stream).  Inputs (V 12.8 GB) are
-larger than L2 (126 MB), so no explicit L2 flush is needed between steps.
+Default workload (the bench line the driver records): BASELINE.json configs[1], the CCSD
+particle-particle ladder R(a,b,i,j) += V(a,b,c,d) * T(c,d,i,j), O=40 V=200 tile=40, FP64.
+--config cfg3: configs[2], spin-block-sparse doubles terms ladder + ring + hole-hole, O=60 V=400,
+tO=30 tV=40 with the alpha/beta block maps of DESIGN.md R7 (one step = all three contractions).
 
-N > 1 (torchrun): strong scaling of the same problem.  Owner-computes: R blocks are LPT-partitioned
-over the ranks, V blocks live with the R rows that read them, T blocks are distributed round robin
-and each step gathers the T blocks a rank needs with grouped NCCL send/recv inside tt_contract.
+One step = the tt_contract call(s) of the workload over the whole tensors (task lists, partition and
+gather plans cached; the input-tile gather over NCCL when N > 1; the DMMA contraction kernel).
+value = algorithmic FLOPs of all ranks (non-zero tile pairs only) / max over ranks of the device
+time of the K timed steps (CUDA events on the context stream).  The operands (V = 12.8 GB for cfg2,
+76.8 GB for cfg3) are larger than L2 (126 MB), so no explicit L2 flush is needed between steps.
 
---impl reference: the CPU oracle (oracle/) timed on the host cores on a bounded sample of the same
+N > 1 (torchrun): strong scaling of the same problem.  Owner-computes: the R blocks are LPT-
+partitioned by (a,b) rows (tt_partition_lpt with group dims a,b), the V blocks live with the R rows
+that read them, every other input is distributed round robin (P210 scheme 3) and gathered inside
+tt_contract with grouped NCCL send/recv every step.
+
+--impl reference: the CPU oracle (oracle/) on the host cores, on a bounded sample of the same
 workload (rank 0 only), same metric and unit.
 """
 from __future__ import annotations
@@ -30,12 +36,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FP64 GFLOP/s and % of FP64 TC peak, CCSD contractions at 1/2/4/8 B200"
-O_, V_, TILE = 40, 200, 40
-WORKLOAD = "cfg2 CCSD ladder R(a,b,i,j) += V(a,b,c,d)*T(c,d,i,j), O=40 V=200 tile=40, dense, FP64"
 # FP64 tensor-core peak: register-only mma.sync m8n8k4 (DMMA.8x8x4) probe on this pool's B200,
 # 148 SMs at 1964 MHz (profiles/r01_probe_fp64.jsonl).  MEASURED_PEAKS.json has no FP64 entry.
 FP64_PEAK_TFLOPS = 37.1
 FP64_PEAK_SOURCE = "measured DMMA probe profiles/r01_probe_fp64.jsonl (37.1 TF/s @1964 MHz; cuBLAS DGEMM 35.5)"
+
+CONFIGS = {
+    "cfg2": dict(O=40, V=200, tO=40, tV=40, spin=False, terms=("ladder",),
+                 workload="cfg2 CCSD ladder R(a,b,i,j) += V(a,b,c,d)*T(c,d,i,j), O=40 V=200 tile=40, dense, FP64"),
+    "cfg3": dict(O=60, V=400, tO=30, tV=40, spin=True, terms=("ladder", "ring", "hh"),
+                 workload="cfg3 spin-sparse CCSD doubles: ladder R+=V(abcd)T(cdij), ring R+=T(acik)W(cbkj), "
+                          "hole-hole R+=T(abkl)W(klij); O=60 V=400 tO=30 tV=40, alpha/beta maps (R7), FP64"),
+}
 
 
 def load_peaks():
@@ -43,6 +55,15 @@ def load_peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def load_traffic(cfg: str, variant: int):
+    """dram bytes per launch of the contraction kernel from the committed ncu --set full capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(f"{cfg}/v{variant}")
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -97,36 +118,79 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def build_problem(tt, ctx):
-    so, sv = tt.IndexSpace(O_), tt.IndexSpace(V_)
-    to, tv = tt.TiledIndexSpace(so, TILE), tt.TiledIndexSpace(sv, TILE)
-    R = tt.Tensor(ctx, [tv, tv, to, to])
-    V = tt.Tensor(ctx, [tv, tv, tv, tv])
-    T = tt.Tensor(ctx, [tv, tv, to, to])
-    return (so, sv, to, tv), R, V, T
+# --------------------------------------------------------------------------------------------- problem
+
+def build_problem(tt, ctx, c):
+    """Tensors and contraction terms of a CCSD-shaped config (maps per DESIGN.md R6/R7)."""
+    O_, V_ = c["O"], c["V"]
+    if c["spin"]:
+        so = tt.IndexSpace(O_, [(0, O_ // 2), (O_ // 2, O_)], [1, -1])
+        sv = tt.IndexSpace(V_, [(0, V_ // 2), (V_ // 2, V_)], [1, -1])
+    else:
+        so, sv = tt.IndexSpace(O_), tt.IndexSpace(V_)
+    to, tv = tt.TiledIndexSpace(so, c["tO"]), tt.TiledIndexSpace(sv, c["tV"])
+    sp = (lambda up, lo: (up, lo)) if c["spin"] else (lambda up, lo: None)
+    T = {"R": tt.Tensor(ctx, [tv, tv, to, to], spin=sp([0, 1], [2, 3]))}
+    ops = []
+    if "ladder" in c["terms"]:
+        T["V"] = tt.Tensor(ctx, [tv, tv, tv, tv], spin=sp([0, 1], [2, 3]))
+        T["T"] = tt.Tensor(ctx, [tv, tv, to, to], spin=sp([0, 1], [2, 3]))
+        ops.append(("R", "abij", "V", "abcd", "T", "cdij"))
+    if "ring" in c["terms"]:
+        T["Ta"] = tt.Tensor(ctx, [tv, tv, to, to], spin=sp([0, 1], [2, 3]))
+        T["Wr"] = tt.Tensor(ctx, [tv, tv, to, to], spin=sp([2, 1], [0, 3]))
+        ops.append(("R", "abij", "Ta", "acik", "Wr", "cbkj"))
+    if "hh" in c["terms"]:
+        T["Tb"] = tt.Tensor(ctx, [tv, tv, to, to], spin=sp([0, 1], [2, 3]))
+        T["Wh"] = tt.Tensor(ctx, [to, to, to, to], spin=sp([0, 1], [2, 3]))
+        ops.append(("R", "abij", "Tb", "abkl", "Wh", "klij"))
+    return (so, sv, to, tv), T, ops
 
 
-_T_CACHE = None
+def distribute(tt, ctx, T, ops, np):
+    """Owner-computes placement for N > 1: R by (a,b) rows (grouped LPT on the first term's costs),
+    V with the R rows that read it; other inputs keep the default round-robin owners (P210)."""
+    R = T["R"]
+    c, cl, a, al, b, bl = ops[0]
+    own = tt.partition_lpt(ctx, R, cl, T[a], al, T[b], bl, group_dims=(0, 1))
+    R.set_owner(own)
+    if "V" in T:
+        V = T["V"]
+        row = {}
+        for blk in range(R.nblocks):
+            if R.nz[blk]:
+                ta, tb = np.unravel_index(blk, R.grid)[:2]
+                row[(int(ta), int(tb))] = int(own[blk])
+        vo = np.full(V.nblocks, -1, np.int32)
+        for blk in range(V.nblocks):
+            if V.nz[blk]:
+                ta, tb = np.unravel_index(blk, V.grid)[:2]
+                vo[blk] = row.get((int(ta), int(tb)), 0)
+        V.set_owner(vo)
 
 
-def cpu_oracle_sample(rows_a: int = 1, a0: int = 0):
-    """Oracle (as it stands) on a bounded sample: the R rows a in [a0, a0+rows_a) of the same ladder,
-    all b, i, j, full K = 40000.  Returns (flops, seconds, threads)."""
+_T_CACHE = {}
+
+
+def cpu_oracle_sample(c, a0: int = 0):
+    """The oracle (as it stands) on a bounded sample of the workload: the ladder output rows
+    R[a0, :, :, :] (all b, i, j; K = V^2 contracted pairs), dense loops over the masked operands.
+    Returns (flops the oracle executes, seconds, threads)."""
     import numpy as np
     import synthetic as S
     from oracle import ops as O
-    global _T_CACHE
-    ga = np.arange(a0, a0 + rows_a)
-    gV = S.values(11, 4, (ga[:, None] * V_ ** 3 + np.arange(V_ ** 3)[None, :]).reshape(-1)).reshape(rows_a, V_, V_, V_)
-    if _T_CACHE is None:
-        _T_CACHE = S.dense((V_, V_, O_, O_), 11, 5)
-    T = _T_CACHE
-    C0 = S.values(11, 3, (ga[:, None] * (V_ * O_ * O_) + np.arange(V_ * O_ * O_)[None, :]).reshape(-1))
-    C0 = C0.reshape(rows_a, V_, O_, O_)
+    O_, V_ = c["O"], c["V"]
+    key = (O_, V_)
+    if key not in _T_CACHE:
+        _T_CACHE[key] = S.dense((V_, V_, O_, O_), 11, 5)
+    Tt = _T_CACHE[key]
+    g = a0 * V_ ** 3 + np.arange(V_ ** 3)
+    Vs = S.values(11, 4, g).reshape(1, V_, V_, V_)
+    C0 = S.values(11, 3, a0 * V_ * O_ * O_ + np.arange(V_ * O_ * O_)).reshape(1, V_, O_, O_)
     t0 = time.perf_counter()
-    O.contract(C0, "abij", gV, "abcd", T, "cdij", 1.0, 1.0)
+    O.contract(C0, "abij", Vs, "abcd", Tt, "cdij", 1.0, 1.0)
     dt = time.perf_counter() - t0
-    flops = 2.0 * rows_a * V_ * O_ * O_ * V_ * V_
+    flops = 2.0 * V_ * O_ * O_ * V_ * V_
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return flops, dt, threads
 
@@ -135,23 +199,23 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np  # noqa: F401
     from oracle import _lib
     _lib.build()
+    c = CONFIGS[args.config]
     for _ in range(args.warmup):
-        cpu_oracle_sample(1, 0)
-    tot_f, tot_t = 0.0, 0.0
-    threads = 1
+        cpu_oracle_sample(c, 0)
+    tot_f, tot_t, threads = 0.0, 0.0, 1
     for s in range(args.steps):
-        f, dt, threads = cpu_oracle_sample(1, (s * 7) % V_)
+        f, dt, threads = cpu_oracle_sample(c, (s * 7) % c["V"])
         tot_f += f
         tot_t += dt
     value = tot_f / tot_t / 1e9
-    sample = f"R rows a=one value per step (200 of 40000 (a,b) rows, K=40000), {args.steps} steps"
+    sample = (f"one ladder output slice R[a,:,:,:] per step ({c['V']} of {c['V'] ** 2} (a,b) rows, "
+              f"K={c['V'] ** 2}), {args.steps} steps, dense oracle loops")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
+            "data": "synthetic", "config": {"workload": c["workload"], "sample": sample},
             "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -164,6 +228,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -181,6 +246,7 @@ def main():
 
     import paper_2201_01257_b200 as tt
 
+    cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -194,32 +260,32 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     ctx = tt.Context(device=local, stream=stream.cuda_stream, rank=rank, nranks=world, nccl_id=nid)
-    keep, R, V, T = build_problem(tt, ctx)
+    keep, T, ops = build_problem(tt, ctx, cfg)
     if world > 1:
-        own = tt.partition_lpt(ctx, R, "abij", V, "abcd", T, "cdij")
-        R.set_owner(own)
-        # V block (a,b,c,d) lives with the R block (a,b,0,0) that reads it (owner-computes)
-        vo = np.empty(V.nblocks, np.int32)
-        g = V_ // TILE
-        for b in range(V.nblocks):
-            ab = b // (g * g)
-            vo[b] = own[ab]      # R grid is (g, g, 1, 1)
-        V.set_owner(vo)
+        distribute(tt, ctx, T, ops, np)
     bufs = {}
-    for name, Tn, tag in (("R", R, 3), ("V", V, 4), ("T", T, 5)):
+    tags = {"R": 3, "V": 4, "T": 5, "Ta": 1, "Wr": 2, "Tb": 6, "Wh": 7}
+    for name, Tn in T.items():
         bufs[name] = torch.empty(Tn.packed_elems, dtype=torch.float64, device="cuda")
         Tn.bind(bufs[name])
-        tt.fill_synthetic(ctx, Tn, 11, tag)
+        tt.fill_synthetic(ctx, Tn, 11, tags[name])
     torch.cuda.synchronize()
 
     def step():
-        tt.contract(ctx, R, "abij", 1.0, 1.0, V, "abcd", T, "cdij")
+        for (c, cl, a, al, b, bl) in ops:
+            tt.contract(ctx, T[c], cl, 1.0, 1.0, T[a], al, T[b], bl)
 
-    for _ in range(args.warmup):
-        step()
+    stats = []
+    for w in range(args.warmup):
+        if w == args.warmup - 1:
+            stats = []
+            for (c, cl, a, al, b, bl) in ops:
+                tt.contract(ctx, T[c], cl, 1.0, 1.0, T[a], al, T[b], bl)
+                stats.append(ctx.stats())
+        else:
+            step()
     torch.cuda.synchronize()
-    st = ctx.stats()
-    flops_rank = st["flops"]
+    flops_rank = sum(s["flops"] for s in stats)
     if world > 1:
         dist.barrier()
     ctx.set_profiling(True)
@@ -241,7 +307,7 @@ def main():
     ms = e0.elapsed_time(e1)
     kern_ms, kern_n = ctx.profile("tt_contract_dmma")
     ctx.set_profiling(False)
-    tot = torch.tensor([ms, flops_rank, kern_ms / max(kern_n, 1)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([ms, flops_rank], dtype=torch.float64, device="cuda")
     if world > 1:
         mx = tot.clone()
         dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
@@ -253,30 +319,33 @@ def main():
     ms_per_step = ms_max / args.steps
     value = flops_all / (ms_per_step * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (this rank)
+    # roofline of the dominant kernel (this rank): FLOPs per launch / average launch time
+    launches_per_step = max(kern_n // args.steps, 1)
     avg_kernel_ms = kern_ms / max(kern_n, 1)
-    achieved = flops_rank / (avg_kernel_ms * 1e-3) / 1e12
+    achieved = (flops_rank / launches_per_step) / (avg_kernel_ms * 1e-3) / 1e12
+    variant = stats[0]["kernel_variant"]
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "kernel": "tt_contract_dmma",
-            "avg_kernel_ms": avg_kernel_ms, "kernel_share_of_step": avg_kernel_ms / ms_per_step,
-            "peak_source": FP64_PEAK_SOURCE}
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": load_traffic(args.config, variant),
+            "kernel": "tt_contract_dmma", "avg_kernel_ms": avg_kernel_ms,
+            "kernel_share_of_step": kern_ms / args.steps / ms_per_step, "peak_source": FP64_PEAK_SOURCE,
+            "algorithmic_bytes_per_step": sum(s["bytes"] for s in stats)}
 
     # end to end through the C ABI with host buffers (pinned), N GPUs
     e2e = None
     if not args.no_e2e:
         hosts = {}
-        for name, Tn in (("R", R), ("V", V), ("T", T)):
+        for name, Tn in T.items():
             hosts[name] = torch.empty(Tn.packed_elems, dtype=torch.float64, pin_memory=True)
             Tn.download_ptr(hosts[name].data_ptr())
         torch.cuda.synchronize()
-        h2d = 8 * (R.packed_elems + V.packed_elems + T.packed_elems)
-        d2h = 8 * R.packed_elems
+        h2d = 8 * sum(Tn.packed_elems for Tn in T.values())
+        d2h = 8 * T["R"].packed_elems
 
         def e2e_step():
-            for name, Tn in (("V", V), ("T", T), ("R", R)):
+            for name, Tn in T.items():
                 Tn.upload_ptr(hosts[name].data_ptr())
             step()
-            R.download_ptr(hosts["R"].data_ptr())
+            T["R"].download_ptr(hosts["R"].data_ptr())
 
         e2e_step()
         torch.cuda.synchronize()
@@ -297,17 +366,16 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        f, dt, threads = cpu_oracle_sample(1, 0)
+        f, dt, threads = cpu_oracle_sample(cfg, 0)
+        reps = 1
         if dt < 5.0:   # aim for ~10-30 s of CPU work
             reps = max(1, min(8, int(15.0 / max(dt, 1e-3))))
-            f, dt = 0.0, 0.0
-            for r in range(reps):
-                ff, dd, threads = cpu_oracle_sample(1, r)
+            for r in range(1, reps):
+                ff, dd, threads = cpu_oracle_sample(cfg, r)
                 f += ff
                 dt += dd
-            sample = f"{reps} R slices a=0..{reps - 1} (each 200 (a,b) rows x 1600 (i,j), K=40000)"
-        else:
-            sample = "1 R slice a=0 (200 (a,b) rows x 1600 (i,j), K=40000)"
+        sample = (f"{reps} ladder output slice(s) R[a,:,:,:], a=0..{reps - 1} (each {cfg['V']} (a,b) rows x "
+                  f"{cfg['O'] ** 2} (i,j), K={cfg['V'] ** 2}), dense oracle loops")
         cpu = {"value": f / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": sample,
                "seconds": dt}
 
@@ -318,10 +386,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded splitmix64 counter generator over global indices, uniform [-1,1)",
-            "config": {"workload": WORKLOAD, "flops_per_step": flops_all, "tasks": st["tasks"] * world,
-                       "kernel_variant": st["kernel_variant"],
-                       "l2": "inputs larger than L2 (V = 12.8 GB >> 126 MB); no flush",
-                       "parallelism": f"owner-computes over {world} GPU(s), LPT partition of R blocks"},
+            "config": {"workload": cfg["workload"], "flops_per_step": flops_all,
+                       "tasks_per_step": sum(s["tasks"] for s in stats), "kernel_variant": variant,
+                       "l2": "operands larger than L2 (126 MB); no flush",
+                       "parallelism": f"owner-computes over {world} GPU(s), LPT partition of R by (a,b) rows"},
             "pct_fp64_peak": value / world / (FP64_PEAK_TFLOPS * 1e3) * 100.0,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"),
