@@ -1294,7 +1294,7 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       slots.push(t0 + c);
       mk = std::max(mk, t0 + c);
     }
-    if (best < 0 || mk < best * 0.97) {  // prefer earlier (larger) tiles unless >3% better
+    if (best < 0 || mk < best * 0.99) {  // prefer earlier variants unless >1% better
       best = mk;
       pl.variant = v;
     }
