@@ -306,6 +306,13 @@ def main():
     launches = ctx.launches() - l0
     ms = e0.elapsed_time(e1)
     kern_ms, kern_n = ctx.profile("tt_contract_dmma")
+    terms = []
+    for (c, cl, a, al, b, bl), st in zip(ops, stats):
+        t_ms, t_n = ctx.profile(f"tt_contract_dmma[{cl}={al}*{bl}]")
+        t_avg = t_ms / max(t_n, 1)
+        terms.append({"term": f"{c}({cl}) += {a}({al}) * {b}({bl})", "flops": st["flops"], "tasks": st["tasks"],
+                      "kernel_ms": t_avg, "tflops": st["flops"] / (t_avg * 1e-3) / 1e12 if t_avg > 0 else None,
+                      "variant": st["kernel_variant"]})
     ctx.set_profiling(False)
     tot = torch.tensor([ms, flops_rank], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -391,7 +398,7 @@ def main():
                        "l2": "operands larger than L2 (126 MB); no flush",
                        "parallelism": f"owner-computes over {world} GPU(s), LPT partition of R by (a,b) rows"},
             "pct_fp64_peak": value / world / (FP64_PEAK_TFLOPS * 1e3) * 100.0,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "terms": terms, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"),
         }
         print(json.dumps(line), flush=True)

@@ -1399,7 +1399,8 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   p.alpha = alpha;
   p.beta = beta;
   {
-    Launch L(ctx, "tt_contract_dmma");
+    const std::string nm = std::string("tt_contract_dmma[") + cl + "=" + al + "*" + bl + "]";
+    Launch L(ctx, nm.c_str());
     if (pl->variant < num_contract_variants())
       TT_CUDA(launch_contract(pl->variant, pl->an.a_kc, pl->an.b_nc, p, pl->nwork, ctx->stream));
     else
