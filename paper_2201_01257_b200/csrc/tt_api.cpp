@@ -845,13 +845,58 @@ constexpr int64_t kSegElems = 1 << 15;
 struct ElemPlan {
   std::vector<ElemDesc> descs;
   std::vector<Segment> segs;
+  std::vector<TileItem> tiles;
   ElemDesc* d_descs = nullptr;
   Segment* d_segs = nullptr;
+  TileItem* d_tiles = nullptr;
   double* d_partials = nullptr;
   GatherPlan gp;
+  int mode = kElemGeneric;
   double bytes = 0;
   int64_t blocks = 0;
+  int64_t nwork() const { return mode == kElemTranspose ? (int64_t)tiles.size() : (int64_t)segs.size(); }
 };
+
+// Fuse adjacent x dims that are adjacent (same order) in y; fill the group extents / y strides of
+// one block descriptor.  ext[d] = x block extents, ypos[d] = y dim of x dim d, ystr[e] = y block
+// strides by y dim.  Returns the element-op mode of this descriptor.
+int fuse_elem(ElemDesc& d, int order, const int32_t* ext, const int* ypos, const int64_t* ystr) {
+  int n = 0;
+  int64_t gext[TT_MAX_ORDER];
+  int last_y[TT_MAX_ORDER];
+  for (int q = 0; q < order; ++q) {
+    if (n > 0 && ypos[q] == last_y[n - 1] + 1) {
+      gext[n - 1] *= ext[q];
+      last_y[n - 1] = ypos[q];
+    } else {
+      gext[n] = ext[q];
+      last_y[n] = ypos[q];
+      ++n;
+    }
+  }
+  d.n = n;
+  d.gy = -1;
+  for (int g = 0; g < n; ++g) {
+    d.div[g] = make_fastdiv((uint32_t)gext[g]);
+    d.y_str[g] = (int32_t)ystr[last_y[g]];
+    if (d.y_str[g] == 1) d.gy = g;
+  }
+  if (n == 1 && d.y_str[0] == 1) return kElemContig;
+  if (d.y_str[n - 1] == 1 || d.gy < 0) return kElemGeneric;
+  return kElemTranspose;
+}
+
+void add_tiles(ElemPlan& ep, int32_t desc) {
+  const ElemDesc& d = ep.descs[desc];
+  const int gx = d.n - 1, gy = d.gy;
+  int64_t batch = 1;
+  for (int g = 0; g < d.n; ++g)
+    if (g != gx && g != gy) batch *= d.div[g].d;
+  const int ntx = (int)((d.div[gx].d + 31) / 32), nty = (int)((d.div[gy].d + 31) / 32);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int ty = 0; ty < nty; ++ty)
+      for (int tx = 0; tx < ntx; ++tx) ep.tiles.push_back({desc, tx, ty, (int32_t)b});
+}
 
 void add_segments(ElemPlan& ep, int32_t desc, int64_t vol) {
   for (int64_t e = 0; e < vol; e += kSegElems) ep.segs.push_back({desc, 0, e, std::min(vol, e + kSegElems)});
@@ -862,6 +907,10 @@ tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
   TT_TRY(dev_alloc(ctx, &ep.d_segs, ep.segs.size()));
   if (!ep.descs.empty()) TT_CUDA(cudaMemcpy(ep.d_descs, ep.descs.data(), ep.descs.size() * sizeof(ElemDesc), cudaMemcpyHostToDevice));
   if (!ep.segs.empty()) TT_CUDA(cudaMemcpy(ep.d_segs, ep.segs.data(), ep.segs.size() * sizeof(Segment), cudaMemcpyHostToDevice));
+  if (!ep.tiles.empty()) {
+    TT_TRY(dev_alloc(ctx, &ep.d_tiles, ep.tiles.size()));
+    TT_CUDA(cudaMemcpy(ep.d_tiles, ep.tiles.data(), ep.tiles.size() * sizeof(TileItem), cudaMemcpyHostToDevice));
+  }
   if (partials) TT_TRY(dev_alloc(ctx, &ep.d_partials, ep.segs.size()));
   return TT_OK;
 }
@@ -901,8 +950,9 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
       d.x_off = t->blk_off[b];
       d.y_off = -1;
       d.g_origin = 0;
+      d.n = t->order;
       for (int q = 0; q < t->order; ++q) {
-        d.ext[q] = (int32_t)t->dims[q]->size(c[q]);
+        d.div[q] = make_fastdiv((uint32_t)t->dims[q]->size(c[q]));
         d.g_str[q] = gstr[q];
         d.g_origin += t->dims[q]->offsets[c[q]] * gstr[q];
       }
@@ -1003,12 +1053,13 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
       // strides of the A block, by A dim
       int64_t sa[TT_MAX_ORDER], acc = 1;
       for (int q = A->order - 1; q >= 0; --q) { sa[q] = acc; acc *= A->dims[q]->size(ac[q]); }
-      for (int q = 0; q < C->order; ++q) {
-        d.ext[q] = (int32_t)C->dims[q]->size(cc[q]);
-        d.y_str[q] = (int32_t)sa[perm[q]];
-      }
+      int32_t ext[TT_MAX_ORDER];
+      for (int q = 0; q < C->order; ++q) ext[q] = (int32_t)C->dims[q]->size(cc[q]);
+      ep->mode = fuse_elem(d, C->order, ext, perm.data(), sa);
       ep->descs.push_back(d);
-      add_segments(*ep, (int32_t)ep->descs.size() - 1, C->block_volume(b));
+      const int32_t di = (int32_t)ep->descs.size() - 1;
+      if (ep->mode == kElemTranspose) add_tiles(*ep, di);
+      else add_segments(*ep, di, C->block_volume(b));
       ep->bytes += 8.0 * C->block_volume(b) * ((beta != 0.0) + 1 + (A->nz[ab] ? 1 : 0));
       ep->blocks++;
     }
@@ -1024,12 +1075,14 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
   p.Y = A->data;
   p.descs = ep->d_descs;
   p.segs = ep->d_segs;
+  p.tiles = ep->d_tiles;
+  p.mode = ep->mode;
   p.order = C->order;
   p.alpha = alpha;
   p.beta = beta;
   {
     Launch L(ctx, "tt_add");
-    TT_CUDA(launch_add(p, (int64_t)ep->segs.size(), ctx->stream));
+    TT_CUDA(launch_add(p, ep->nwork(), ctx->stream));
   }
   ctx->last.c_blocks = ep->blocks;
   ctx->last.bytes = ep->bytes;
@@ -1076,10 +1129,10 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
       d.y_off = B->blk_off[bb];
       int64_t sb[TT_MAX_ORDER], acc = 1;
       for (int q = B->order - 1; q >= 0; --q) { sb[q] = acc; acc *= B->dims[q]->size(bc[q]); }
-      for (int q = 0; q < A->order; ++q) {
-        d.ext[q] = (int32_t)A->dims[q]->size(ac[q]);
-        d.y_str[q] = (int32_t)sb[perm[q]];
-      }
+      int32_t ext[TT_MAX_ORDER];
+      for (int q = 0; q < A->order; ++q) ext[q] = (int32_t)A->dims[q]->size(ac[q]);
+      const int mode = fuse_elem(d, A->order, ext, perm.data(), sb);
+      ep->mode = mode == kElemContig ? kElemContig : kElemGeneric;
       ep->descs.push_back(d);
       add_segments(*ep, (int32_t)ep->descs.size() - 1, A->block_volume(blk));
       ep->bytes += 16.0 * A->block_volume(blk);
@@ -1098,6 +1151,7 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
   p.descs = ep->d_descs;
   p.segs = ep->d_segs;
   p.order = A->order;
+  p.mode = ep->mode;
   p.partials = ep->d_partials;
   {
     Launch L(ctx, "tt_scalar_partials");

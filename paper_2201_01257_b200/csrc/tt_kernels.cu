@@ -428,35 +428,126 @@ cudaError_t launch_build_fill(const BuildParams& p, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// Element kernels.  One CTA per segment (a contiguous element range of one block).
+// Element kernels.  One CTA per segment (a contiguous element range of one block), or per 32x32
+// tile in transpose mode.  HBM-bound: vectorised contiguous paths, multiply-high index decode.
 
 constexpr int kElemThreads = 256;
 
-// x-order element index -> offset in the other operand (decode over the block extents)
-__device__ __forceinline__ int64_t y_offset(int64_t e, int order, const ElemDesc& d) {
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  const uint32_t t = __umulhi(n, f.m);
+  return (t + n) >> f.l;
+}
+
+// x-order element index (row-major over the groups) -> offset in the other operand
+__device__ __forceinline__ int64_t y_offset(uint32_t e, const ElemDesc& d) {
   int64_t off = 0;
-  for (int q = order - 1; q >= 0; --q) {
-    const int64_t c = e % d.ext[q];
-    e /= d.ext[q];
-    off += c * d.y_str[q];
+  for (int g = d.n - 1; g > 0; --g) {
+    const uint32_t q = fdiv(e, d.div[g]);
+    off += (int64_t)(e - q * d.div[g].d) * d.y_str[g];
+    e = q;
   }
-  return off;
+  return off + (int64_t)e * d.y_str[0];
 }
 
 __global__ void set_kernel(const ElemParams p) {
   const Segment sg = p.segs[blockIdx.x];
   double* x = p.X + p.descs[sg.desc].x_off;
-  for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) x[e] = p.alpha;
+  // segments start at even offsets inside 16-B aligned blocks: double2 stores, scalar tail
+  const int64_t n2 = (sg.e1 - sg.e0) / 2;
+  double2* x2 = reinterpret_cast<double2*>(x + sg.e0);
+  const double2 v = make_double2(p.alpha, p.alpha);
+  for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) x2[i] = v;
+  if (threadIdx.x == 0 && (sg.e1 - sg.e0) % 2) x[sg.e1 - 1] = p.alpha;
 }
 
+template <int MODE>
 __global__ void add_kernel(const ElemParams p) {
+  __shared__ ElemDesc d;
   const Segment sg = p.segs[blockIdx.x];
-  const ElemDesc d = p.descs[sg.desc];
+  if (threadIdx.x == 0) d = p.descs[sg.desc];
+  __syncthreads();
   double* x = p.X + d.x_off;
   const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
-  for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) {
-    const double v = y ? p.alpha * y[y_offset(e, p.order, d)] : 0.0;
-    x[e] = (p.beta == 0.0) ? v : p.beta * x[e] + v;
+  const double alpha = p.alpha, beta = p.beta;
+  if (MODE == kElemContig) {
+    const int64_t n2 = (sg.e1 - sg.e0) / 2;
+    double2* x2 = reinterpret_cast<double2*>(x + sg.e0);
+    const double2* y2 = y ? reinterpret_cast<const double2*>(y + sg.e0) : nullptr;
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
+      double2 v = y2 ? y2[i] : make_double2(0.0, 0.0);
+      v.x *= alpha;
+      v.y *= alpha;
+      if (beta != 0.0) {
+        const double2 o = x2[i];
+        v.x += beta * o.x;
+        v.y += beta * o.y;
+      }
+      x2[i] = v;
+    }
+    if (threadIdx.x == 0 && (sg.e1 - sg.e0) % 2) {
+      const int64_t e = sg.e1 - 1;
+      const double v = y ? alpha * y[e] : 0.0;
+      x[e] = (beta == 0.0) ? v : beta * x[e] + v;
+    }
+  } else {
+    for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) {
+      const double v = y ? alpha * y[y_offset((uint32_t)e, d)] : 0.0;
+      x[e] = (beta == 0.0) ? v : beta * x[e] + v;
+    }
+  }
+}
+
+// Transpose mode: x innermost group gx = n-1 is strided in y, group gy has y stride 1.  Each CTA
+// moves one 32x32 tile: coalesced reads along gy, shared-memory transpose, coalesced x writes.
+__device__ __forceinline__ void tile_offsets(const ElemDesc& d, const TileItem& t, int64_t& xb, int64_t& yb,
+                                             int64_t& xs_gy) {
+  // x strides of the groups (row-major over group extents)
+  int64_t xs[TT_MAX_ORDER];
+  int64_t acc = 1;
+  for (int g = d.n - 1; g >= 0; --g) { xs[g] = acc; acc *= d.div[g].d; }
+  uint32_t b = (uint32_t)t.batch;
+  xb = 0;
+  yb = 0;
+  for (int g = d.n - 1; g >= 0; --g) {
+    if (g == d.n - 1 || g == d.gy) continue;
+    const uint32_t q = fdiv(b, d.div[g]);
+    const int64_t c = b - q * d.div[g].d;
+    b = q;
+    xb += c * xs[g];
+    yb += c * d.y_str[g];
+  }
+  xs_gy = xs[d.gy];
+}
+
+__global__ void add_transpose_kernel(const ElemParams p) {
+  __shared__ ElemDesc d;
+  __shared__ double tile[32][33];
+  const TileItem t = p.tiles[blockIdx.x];
+  if (threadIdx.x == 0 && threadIdx.y == 0) d = p.descs[t.desc];
+  __syncthreads();
+  int64_t xb, yb, xs_gy;
+  tile_offsets(d, t, xb, yb, xs_gy);
+  const int gx = d.n - 1, gy = d.gy;
+  const int ex = d.div[gx].d, ey = d.div[gy].d;
+  const int x0 = t.tx * 32, y0 = t.ty * 32;
+  const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
+  // read: lanes along gy (y contiguous), rows along gx
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int ix = x0 + r, iy = y0 + threadIdx.x;
+    double v = 0.0;
+    if (y && ix < ex && iy < ey) v = y[yb + (int64_t)ix * d.y_str[gx] + iy];
+    tile[r][threadIdx.x] = v;
+  }
+  __syncthreads();
+  double* x = p.X + d.x_off;
+  // write: lanes along gx (x contiguous)
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int ix = x0 + threadIdx.x, iy = y0 + r;
+    if (ix < ex && iy < ey) {
+      double* o = x + xb + (int64_t)iy * xs_gy + ix;
+      const double v = p.alpha * tile[threadIdx.x][r];
+      *o = (p.beta == 0.0) ? v : p.beta * *o + v;
+    }
   }
 }
 
@@ -472,12 +563,14 @@ __global__ void fill_kernel(const ElemParams p) {
   const ElemDesc d = p.descs[sg.desc];
   double* x = p.X + d.x_off;
   for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) {
-    int64_t r = e, g = d.g_origin;
-    for (int q = p.order - 1; q >= 0; --q) {
-      const int64_t c = r % d.ext[q];
-      r /= d.ext[q];
-      g += c * d.g_str[q];
+    uint32_t r = (uint32_t)e;
+    int64_t g = d.g_origin;
+    for (int q = p.order - 1; q > 0; --q) {
+      const uint32_t qq = fdiv(r, d.div[q]);
+      g += (int64_t)(r - qq * d.div[q].d) * d.g_str[q];
+      r = qq;
     }
+    g += (int64_t)r * d.g_str[0];
     const uint64_t h = splitmix64(p.key ^ (uint64_t)g);
     x[e] = (p.kind == TT_KIND_INTEGER) ? (double)(int64_t)(h % 5ull) - 2.0
                                        : (double)(h >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
@@ -485,14 +578,29 @@ __global__ void fill_kernel(const ElemParams p) {
 }
 
 // Deterministic: each CTA sums its segment in a fixed order (strided per thread, then a fixed tree).
+template <int MODE>
 __global__ void scalar_partials_kernel(const ElemParams p) {
   __shared__ double red[kElemThreads];
+  __shared__ ElemDesc d;
   const Segment sg = p.segs[blockIdx.x];
-  const ElemDesc d = p.descs[sg.desc];
+  if (threadIdx.x == 0) d = p.descs[sg.desc];
+  __syncthreads();
   const double* x = p.X + d.x_off;
   const double* y = p.Y + d.y_off;
   double s = 0.0;
-  for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) s += x[e] * y[y_offset(e, p.order, d)];
+  if (MODE == kElemContig) {
+    const int64_t n2 = (sg.e1 - sg.e0) / 2;
+    const double2* x2 = reinterpret_cast<const double2*>(x + sg.e0);
+    const double2* y2 = reinterpret_cast<const double2*>(y + sg.e0);
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
+      const double2 a = x2[i], b = y2[i];
+      s += a.x * b.x;
+      s += a.y * b.y;
+    }
+    if (threadIdx.x == 0 && (sg.e1 - sg.e0) % 2) s += x[sg.e1 - 1] * y[sg.e1 - 1];
+  } else {
+    for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) s += x[e] * y[y_offset((uint32_t)e, d)];
+  }
   red[threadIdx.x] = s;
   __syncthreads();
   for (int o = kElemThreads / 2; o > 0; o >>= 1) {
@@ -522,7 +630,9 @@ cudaError_t launch_set(const ElemParams& p, int64_t nseg, cudaStream_t s) {
 }
 cudaError_t launch_add(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   if (nseg <= 0) return cudaSuccess;
-  add_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  if (p.mode == kElemContig) add_kernel<kElemContig><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  else if (p.mode == kElemGeneric) add_kernel<kElemGeneric><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  else add_transpose_kernel<<<(unsigned)nseg, dim3(32, 8), 0, s>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
@@ -532,7 +642,8 @@ cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
 }
 cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   if (nseg <= 0) return cudaSuccess;
-  scalar_partials_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  if (p.mode == kElemContig) scalar_partials_kernel<kElemContig><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  else scalar_partials_kernel<kElemGeneric><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, cudaStream_t s) {

@@ -79,14 +79,39 @@ struct Segment {
   int64_t e0, e1;     // element range inside the block
 };
 
-// Per-block descriptor for add / scalar / fill: dims in the DESTINATION / first operand order.
+// n / d for 0 <= n < 2^31 by multiply-high (Granlund-Montgomery round-up method): no integer
+// division instructions in the element kernels.
+struct FastDiv {
+  uint32_t d, m, l;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+  return {d, (uint32_t)m, l};
+}
+
+// Per-block descriptor for add / scalar / fill: label groups in the DESTINATION / first operand
+// order (adjacent dims fused when they are adjacent and in the same order in the other operand).
 struct ElemDesc {
   int64_t x_off;                        // packed offset of the block being written / walked
   int64_t y_off;                        // packed offset of the other operand's block (-1 = zero)
   int64_t g_origin;                     // global linear index of the block origin (fill)
-  int32_t ext[TT_MAX_ORDER];            // block extents (x order)
-  int32_t y_str[TT_MAX_ORDER];          // strides of the other operand for each x dim
-  int64_t g_str[TT_MAX_ORDER];          // global strides (fill)
+  int32_t n;                            // number of groups
+  int32_t gy;                           // transpose mode: the group with y stride 1
+  FastDiv div[TT_MAX_ORDER];            // group extents
+  int32_t y_str[TT_MAX_ORDER];          // strides of the other operand for each group
+  int64_t g_str[TT_MAX_ORDER];          // global strides (fill; groups = dims)
+};
+
+// Element-op modes: contiguous (one group, y stride 1: vectorised), generic (multiply-high decode),
+// transpose (innermost x group strided in y: 32x32 shared-memory tiles, coalesced both ways).
+enum { kElemContig = 0, kElemGeneric = 1, kElemTranspose = 2 };
+
+struct TileItem {        // transpose mode: one 32x32 tile of one block
+  int32_t desc;
+  int32_t tx, ty;        // tile index along the innermost x group / the y-contiguous group
+  int32_t batch;         // linear index over the remaining groups
 };
 
 struct ElemParams {
@@ -94,11 +119,13 @@ struct ElemParams {
   const double* Y;
   const ElemDesc* descs;
   const Segment* segs;
+  const TileItem* tiles;
   int32_t order;
+  int32_t mode;
   double alpha, beta;
   uint64_t key;           // fill: seed ^ tag*golden
   int32_t kind;           // fill kind
-  double* partials;       // scalar: one per segment
+  double* partials;       // scalar: one per segment / tile
 };
 
 cudaError_t launch_set(const ElemParams& p, int64_t nseg, cudaStream_t s);

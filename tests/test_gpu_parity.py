@@ -283,3 +283,53 @@ def test_config2_full_size_sampled(env):
         pos.append(offs[b] + ((loc[0] * 40 + loc[1]) * 40 + loc[2]) * 40 + loc[3])
     g = got[np.array(pos)]
     assert np.abs(g - ref).max() / np.abs(ref).max() <= TOL
+
+
+@pytest.mark.parametrize("a_lbl", ["abij", "ijab", "aibj", "jiba", "bajI".replace("I", "i")])
+def test_add_modes(env, a_lbl):
+    """tt_add in its three element modes (contiguous / multiply-high decode / 32x32 smem transpose)
+    on ragged spin-sparse blocks, with zero A blocks read as zeros (S216); scalar on the same pair."""
+    tt, torch = env
+    spaces = {"O": SpaceSpec(14, tile=5, spin_split=True), "V": SpaceSpec(46, tile=9, spin_split=True)}
+    ls = {"a": "V", "b": "V", "i": "O", "j": "O"}
+    perm = [a_lbl.index(x) for x in "abij"]        # A dim of each C dim
+    c_rule = ("spin", [0, 1], [2, 3])
+    a_rule = ("spin", [perm[0], perm[1]], [perm[2], perm[3]])
+    pb = Problem(spaces, ls, {"C": TensorSpec("abij", c_rule), "A": TensorSpec(a_lbl, a_rule)})
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    dense = {n: O.dense_masked(orc[n], S.dense(orc[n].shape, 9, t)) for n, t in (("C", 3), ("A", 1))}
+    # knock out some A blocks (explicitly zero) to exercise the y_off = -1 path
+    bufs = {n: bind_host(torch, P[n], O.pack(orc[n], dense[n])) for n in ("C", "A")}
+    for beta in (1.0, 0.0, -0.5):
+        tt.add(ctx, P["C"], "abij", beta, 0.75, P["A"], a_lbl)
+        got = P["C"].download()
+        ctx.sync()
+        ref = O.add(dense["C"], "abij", dense["A"], a_lbl, 0.75, beta, cmask=O.nz_mask(orc["C"]))
+        assert normwise(got, O.pack(orc["C"], ref)) <= 1e-15
+        dense["C"] = ref
+    s = tt.contract_scalar(ctx, -0.5, P["A"], a_lbl, P["C"], "abij")
+    so = O.scalar(dense["A"], a_lbl, dense["C"], "abij", -0.5)
+    assert abs(s - so) <= 1e-13 * max(abs(so), 1.0)
+
+
+def test_add_zero_input_blocks(env):
+    """Explicit nz maps: C blocks whose A block is zero get C = beta*C."""
+    tt, torch = env
+    spaces = {"X": SpaceSpec(10, tile=4)}
+    ls = {"p": "X", "q": "X"}
+    nzC = [1, 1, 1, 1, 1, 1, 0, 1, 1]
+    nzA = [1, 0, 1, 0, 0, 1, 1, 1, 0]
+    pb = Problem(spaces, ls, {"C": TensorSpec("pq", ("nz", nzC)), "A": TensorSpec("pq", ("nz", nzA))})
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    dense = {n: O.dense_masked(orc[n], S.dense(orc[n].shape, 2, t)) for n, t in (("C", 3), ("A", 1))}
+    bufs = {n: bind_host(torch, P[n], O.pack(orc[n], dense[n])) for n in ("C", "A")}
+    for al in ("pq", "qp"):
+        tt.add(ctx, P["C"], "pq", 2.0, 1.0, P["A"], al)
+        got = P["C"].download()
+        ctx.sync()
+        dense["C"] = O.add(dense["C"], "pq", dense["A"], al, 1.0, 2.0, cmask=O.nz_mask(orc["C"]))
+        assert normwise(got, O.pack(orc["C"], dense["C"])) <= 1e-15
