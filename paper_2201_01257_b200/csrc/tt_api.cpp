@@ -911,7 +911,7 @@ tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
     TT_TRY(dev_alloc(ctx, &ep.d_tiles, ep.tiles.size()));
     TT_CUDA(cudaMemcpy(ep.d_tiles, ep.tiles.data(), ep.tiles.size() * sizeof(TileItem), cudaMemcpyHostToDevice));
   }
-  if (partials) TT_TRY(dev_alloc(ctx, &ep.d_partials, ep.segs.size()));
+  if (partials) TT_TRY(dev_alloc(ctx, &ep.d_partials, std::max<size_t>(ep.segs.size(), ep.tiles.size())));
   return TT_OK;
 }
 
@@ -1131,10 +1131,10 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
       for (int q = B->order - 1; q >= 0; --q) { sb[q] = acc; acc *= B->dims[q]->size(bc[q]); }
       int32_t ext[TT_MAX_ORDER];
       for (int q = 0; q < A->order; ++q) ext[q] = (int32_t)A->dims[q]->size(ac[q]);
-      const int mode = fuse_elem(d, A->order, ext, perm.data(), sb);
-      ep->mode = mode == kElemContig ? kElemContig : kElemGeneric;
+      ep->mode = fuse_elem(d, A->order, ext, perm.data(), sb);
       ep->descs.push_back(d);
-      add_segments(*ep, (int32_t)ep->descs.size() - 1, A->block_volume(blk));
+      if (ep->mode == kElemTranspose) add_tiles(*ep, (int32_t)ep->descs.size() - 1);
+      else add_segments(*ep, (int32_t)ep->descs.size() - 1, A->block_volume(blk));
       ep->bytes += 16.0 * A->block_volume(blk);
       ep->blocks++;
     }
@@ -1152,14 +1152,16 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
   p.segs = ep->d_segs;
   p.order = A->order;
   p.mode = ep->mode;
+  p.tiles = ep->d_tiles;
   p.partials = ep->d_partials;
   {
     Launch L(ctx, "tt_scalar_partials");
-    TT_CUDA(launch_scalar_partials(p, (int64_t)ep->segs.size(), ctx->stream));
+    TT_CUDA(launch_scalar_partials(p, ep->nwork(), ctx->stream));
   }
   {
     Launch L(ctx, "tt_scalar_final");
-    TT_CUDA(launch_scalar_final(ep->d_partials, (int64_t)ep->segs.size(), alpha, ctx->d_scalar, ctx->stream));
+    TT_CUDA(launch_scalar_final(ep->d_partials, scalar_num_partials(ep->mode, ep->nwork()), alpha, ctx->d_scalar,
+                                ctx->stream));
   }
   if (ctx->nranks > 1) {
     const char* err = nullptr;

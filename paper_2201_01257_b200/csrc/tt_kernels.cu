@@ -433,6 +433,17 @@ cudaError_t launch_build_fill(const BuildParams& p, cudaStream_t s) {
 
 constexpr int kElemThreads = 256;
 
+// all threads of the CTA copy a descriptor into shared memory (word-parallel), then barrier
+template <class T>
+__device__ __forceinline__ void load_desc(T& dst, const T* src) {
+  static_assert(sizeof(T) % 4 == 0, "descriptor size");
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&dst);
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x, nt = blockDim.x * blockDim.y;
+  for (int i = tid; i < (int)(sizeof(T) / 4); i += nt) d[i] = s[i];
+  __syncthreads();
+}
+
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   const uint32_t t = __umulhi(n, f.m);
   return (t + n) >> f.l;
@@ -464,8 +475,7 @@ template <int MODE>
 __global__ void add_kernel(const ElemParams p) {
   __shared__ ElemDesc d;
   const Segment sg = p.segs[blockIdx.x];
-  if (threadIdx.x == 0) d = p.descs[sg.desc];
-  __syncthreads();
+  load_desc(d, p.descs + sg.desc);
   double* x = p.X + d.x_off;
   const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
   const double alpha = p.alpha, beta = p.beta;
@@ -519,36 +529,96 @@ __device__ __forceinline__ void tile_offsets(const ElemDesc& d, const TileItem& 
   xs_gy = xs[d.gy];
 }
 
-__global__ void add_transpose_kernel(const ElemParams p) {
+constexpr int kTilesPerCta = 8;
+
+__global__ void add_transpose_kernel(const ElemParams p, int64_t ntiles) {
   __shared__ ElemDesc d;
   __shared__ double tile[32][33];
-  const TileItem t = p.tiles[blockIdx.x];
-  if (threadIdx.x == 0 && threadIdx.y == 0) d = p.descs[t.desc];
-  __syncthreads();
-  int64_t xb, yb, xs_gy;
-  tile_offsets(d, t, xb, yb, xs_gy);
-  const int gx = d.n - 1, gy = d.gy;
-  const int ex = d.div[gx].d, ey = d.div[gy].d;
-  const int x0 = t.tx * 32, y0 = t.ty * 32;
-  const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
-  // read: lanes along gy (y contiguous), rows along gx
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int ix = x0 + r, iy = y0 + threadIdx.x;
-    double v = 0.0;
-    if (y && ix < ex && iy < ey) v = y[yb + (int64_t)ix * d.y_str[gx] + iy];
-    tile[r][threadIdx.x] = v;
-  }
-  __syncthreads();
-  double* x = p.X + d.x_off;
-  // write: lanes along gx (x contiguous)
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int ix = x0 + threadIdx.x, iy = y0 + r;
-    if (ix < ex && iy < ey) {
-      double* o = x + xb + (int64_t)iy * xs_gy + ix;
-      const double v = p.alpha * tile[threadIdx.x][r];
-      *o = (p.beta == 0.0) ? v : p.beta * *o + v;
+  int cur = -1;
+  for (int it = 0; it < kTilesPerCta; ++it) {
+    const int64_t ti = (int64_t)blockIdx.x * kTilesPerCta + it;
+    if (ti >= ntiles) break;
+    const TileItem t = p.tiles[ti];
+    if (t.desc != cur) {          // uniform across the CTA
+      __syncthreads();
+      load_desc(d, p.descs + t.desc);
+      cur = t.desc;
     }
+    int64_t xb, yb, xs_gy;
+    tile_offsets(d, t, xb, yb, xs_gy);
+    const int gx = d.n - 1, gy = d.gy;
+    const int ex = d.div[gx].d, ey = d.div[gy].d;
+    const int x0 = t.tx * 32, y0 = t.ty * 32;
+    const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
+    // read: lanes along gy (y contiguous), rows along gx
+#pragma unroll
+    for (int r = threadIdx.y; r < 32; r += 8) {
+      const int ix = x0 + r, iy = y0 + threadIdx.x;
+      double v = 0.0;
+      if (y && ix < ex && iy < ey) v = y[yb + (int64_t)ix * d.y_str[gx] + iy];
+      tile[r][threadIdx.x] = v;
+    }
+    __syncthreads();
+    double* x = p.X + d.x_off;
+    // write: lanes along gx (x contiguous)
+#pragma unroll
+    for (int r = threadIdx.y; r < 32; r += 8) {
+      const int ix = x0 + threadIdx.x, iy = y0 + r;
+      if (ix < ex && iy < ey) {
+        double* o = x + xb + (int64_t)iy * xs_gy + ix;
+        const double v = p.alpha * tile[threadIdx.x][r];
+        *o = (p.beta == 0.0) ? v : p.beta * *o + v;
+      }
+    }
+    __syncthreads();
   }
+}
+
+// Scalar in transpose mode: partial sum of one run of tiles (fixed order: tile by tile, then a
+// fixed tree over the CTA), transposing y through shared memory so both operands are read coalesced.
+__global__ void scalar_transpose_kernel(const ElemParams p, int64_t ntiles) {
+  __shared__ ElemDesc d;
+  __shared__ double tile[32][33];
+  __shared__ double red[256];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  double s = 0.0;
+  int cur = -1;
+  for (int it = 0; it < kTilesPerCta; ++it) {
+    const int64_t ti = (int64_t)blockIdx.x * kTilesPerCta + it;
+    if (ti >= ntiles) break;
+    const TileItem t = p.tiles[ti];
+    if (t.desc != cur) {
+      __syncthreads();
+      load_desc(d, p.descs + t.desc);
+      cur = t.desc;
+    }
+    int64_t xb, yb, xs_gy;
+    tile_offsets(d, t, xb, yb, xs_gy);
+    const int gx = d.n - 1, gy = d.gy;
+    const int ex = d.div[gx].d, ey = d.div[gy].d;
+    const int x0 = t.tx * 32, y0 = t.ty * 32;
+    const double* y = p.Y + d.y_off;
+#pragma unroll
+    for (int r = threadIdx.y; r < 32; r += 8) {
+      const int ix = x0 + r, iy = y0 + threadIdx.x;
+      tile[r][threadIdx.x] = (ix < ex && iy < ey) ? y[yb + (int64_t)ix * d.y_str[gx] + iy] : 0.0;
+    }
+    __syncthreads();
+    const double* x = p.X + d.x_off;
+#pragma unroll
+    for (int r = threadIdx.y; r < 32; r += 8) {
+      const int ix = x0 + threadIdx.x, iy = y0 + r;
+      if (ix < ex && iy < ey) s += x[xb + (int64_t)iy * xs_gy + ix] * tile[threadIdx.x][r];
+    }
+    __syncthreads();
+  }
+  red[tid] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) p.partials[blockIdx.x] = red[0];
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -583,8 +653,7 @@ __global__ void scalar_partials_kernel(const ElemParams p) {
   __shared__ double red[kElemThreads];
   __shared__ ElemDesc d;
   const Segment sg = p.segs[blockIdx.x];
-  if (threadIdx.x == 0) d = p.descs[sg.desc];
-  __syncthreads();
+  load_desc(d, p.descs + sg.desc);
   const double* x = p.X + d.x_off;
   const double* y = p.Y + d.y_off;
   double s = 0.0;
@@ -632,7 +701,7 @@ cudaError_t launch_add(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   if (nseg <= 0) return cudaSuccess;
   if (p.mode == kElemContig) add_kernel<kElemContig><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   else if (p.mode == kElemGeneric) add_kernel<kElemGeneric><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
-  else add_transpose_kernel<<<(unsigned)nseg, dim3(32, 8), 0, s>>>(p);
+  else add_transpose_kernel<<<(unsigned)((nseg + kTilesPerCta - 1) / kTilesPerCta), dim3(32, 8), 0, s>>>(p, nseg);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
@@ -643,9 +712,14 @@ cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
 cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   if (nseg <= 0) return cudaSuccess;
   if (p.mode == kElemContig) scalar_partials_kernel<kElemContig><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
-  else scalar_partials_kernel<kElemGeneric><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  else if (p.mode == kElemGeneric) scalar_partials_kernel<kElemGeneric><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  else scalar_transpose_kernel<<<(unsigned)((nseg + kTilesPerCta - 1) / kTilesPerCta), dim3(32, 8), 0, s>>>(p, nseg);
   return cudaGetLastError();
 }
+int64_t scalar_num_partials(int mode, int64_t nseg) {
+  return mode == kElemTranspose ? (nseg + kTilesPerCta - 1) / kTilesPerCta : nseg;
+}
+
 cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, cudaStream_t s) {
   scalar_final_kernel<<<1, 1024, 0, s>>>(partials, n, alpha, out);
   return cudaGetLastError();

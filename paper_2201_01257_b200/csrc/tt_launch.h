@@ -131,7 +131,9 @@ struct ElemParams {
 cudaError_t launch_set(const ElemParams& p, int64_t nseg, cudaStream_t s);
 cudaError_t launch_add(const ElemParams& p, int64_t nseg, cudaStream_t s);
 cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s);
+// nseg = segments (contig / generic) or tiles (transpose); returns the number of partials written
 cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, cudaStream_t s);
+int64_t scalar_num_partials(int mode, int64_t nseg);
 cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out,
                                 cudaStream_t s);
 
