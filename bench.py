@@ -14,10 +14,11 @@ value = algorithmic FLOPs of all ranks (non-zero tile pairs only) / max over ran
 time of the K timed steps (CUDA events on the context stream).  The operands (V = 12.8 GB for cfg2,
 76.8 GB for cfg3) are larger than L2 (126 MB), so no explicit L2 flush is needed between steps.
 
-N > 1 (torchrun): strong scaling of the same problem.  Owner-computes: the R blocks are LPT-
-partitioned by (a,b) rows (tt_partition_lpt with group dims a,b), the V blocks live with the R rows
-that read them, every other input is distributed round robin (P210 scheme 3) and gathered inside
-tt_contract with grouped NCCL send/recv every step.
+N > 1 (torchrun): strong scaling of the same problem.  Owner-computes: the R (a,b) rows are laid
+along a cost axis and cut into equal shares (tt_partition_split: a row straddling a rank boundary is
+split along a), the V blocks live with the R rows (or row parts) that read them, every other input is
+distributed round robin (P210 scheme 3) and gathered inside tt_contract with grouped NCCL send/recv
+every step.
 
 --impl reference: the CPU oracle (oracle/) on the host cores, on a bounded sample of the same
 workload (rank 0 only), same metric and unit.
@@ -148,25 +149,37 @@ def build_problem(tt, ctx, c):
 
 
 def distribute(tt, ctx, T, ops, np):
-    """Owner-computes placement for N > 1: R by (a,b) rows (grouped LPT on the first term's costs),
-    V with the R rows that read it; other inputs keep the default round-robin owners (P210)."""
+    """Owner-computes placement for N > 1: R by (a,b) rows with the balanced row-splitting partition
+    (tt_partition_split, group dims a,b: a row straddling a rank boundary is cut along a), V with the
+    R rows (or row parts) that read it; other inputs keep the default round-robin owners (P210)."""
     R = T["R"]
     c, cl, a, al, b, bl = ops[0]
-    own = tt.partition_lpt(ctx, R, cl, T[a], al, T[b], bl, group_dims=(0, 1))
-    R.set_owner(own)
+    tt.partition_split(ctx, R, cl, T[a], al, T[b], bl, group_dims=(0, 1))
     if "V" in T:
         V = T["V"]
-        row = {}
+        whole, split = {}, {}
         for blk in range(R.nblocks):
             if R.nz[blk]:
-                ta, tb = np.unravel_index(blk, R.grid)[:2]
-                row[(int(ta), int(tb))] = int(own[blk])
+                ta, tb = (int(x) for x in np.unravel_index(blk, R.grid)[:2])
+                if R.owner[blk] >= 0:
+                    whole[(ta, tb)] = int(R.owner[blk])
+        for (blk, lo, hi, ow) in R.parts:
+            ta, tb = (int(x) for x in np.unravel_index(blk, R.grid)[:2])
+            split.setdefault((ta, tb), set()).add((lo, hi, ow))
         vo = np.full(V.nblocks, -1, np.int32)
+        vparts = []
         for blk in range(V.nblocks):
-            if V.nz[blk]:
-                ta, tb = np.unravel_index(blk, V.grid)[:2]
-                vo[blk] = row.get((int(ta), int(tb)), 0)
+            if not V.nz[blk]:
+                continue
+            ta, tb = (int(x) for x in np.unravel_index(blk, V.grid)[:2])
+            if (ta, tb) in split:
+                vparts += [(blk, lo, hi, ow) for (lo, hi, ow) in sorted(split[(ta, tb)])]
+                vo[blk] = 0
+            else:
+                vo[blk] = whole.get((ta, tb), 0)
         V.set_owner(vo)
+        if vparts:
+            V.set_parts(vparts)
 
 
 _T_CACHE = {}
@@ -396,7 +409,7 @@ def main():
             "config": {"workload": cfg["workload"], "flops_per_step": flops_all,
                        "tasks_per_step": sum(s["tasks"] for s in stats), "kernel_variant": variant,
                        "l2": "operands larger than L2 (126 MB); no flush",
-                       "parallelism": f"owner-computes over {world} GPU(s), LPT partition of R by (a,b) rows"},
+                       "parallelism": f"owner-computes over {world} GPU(s), balanced row-split partition of R by (a,b) rows"},
             "pct_fp64_peak": value / world / (FP64_PEAK_TFLOPS * 1e3) * 100.0,
             "roofline": roof, "terms": terms, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"),

@@ -51,6 +51,7 @@ enum {
 
 enum { TT_MAX_ORDER = 8 };          /* maximum tensor order                                        */
 enum { TT_REPLICATED = -2 };        /* owner value: every rank holds the block                     */
+enum { TT_SPLIT = -3 };             /* owner value: the block is owned by row-range parts          */
 enum { TT_KIND_UNIFORM = 0, TT_KIND_INTEGER = 1 };   /* synthetic input kinds (tt_fill_synthetic)  */
 
 typedef struct tt_ctx_s* tt_ctx;
@@ -147,6 +148,17 @@ tt_status tt_tensor_layout(tt_tensor t, int64_t* packed_elems, const int64_t** b
 /* Replace the owner map (nblocks entries; zero blocks ignored; values in [0,nranks) or
  * TT_REPLICATED).  Must be identical on every rank. */
 tt_status tt_tensor_set_owner(tt_tensor t, const int32_t* owner);
+/* Row-range ownership (SURVEY §8(e) "block splitting", owner-computes at a finer grain than a block):
+ * part i is rows [lo[i], hi[i]) of the dimension-0 tile of block blk[i], owned by rank owner[i].  The
+ * parts of a block must tile its dimension-0 range in order; listed blocks get owner TT_SPLIT (one
+ * part covering the whole tile = an ordinary owner); unlisted blocks keep their owner.  Because
+ * dimension 0 is outermost, a part is a contiguous element range of the packed block.  Must be
+ * identical on every rank. */
+tt_status tt_tensor_set_parts(tt_tensor t, int64_t n, const int64_t* blk, const int32_t* lo,
+                              const int32_t* hi, const int32_t* owner);
+/* The parts of all split blocks (arrays owned by the handle, valid until the next ownership change). */
+tt_status tt_tensor_parts(tt_tensor t, int64_t* n, const int64_t** blk, const int32_t** lo,
+                          const int32_t** hi, const int32_t** owner);
 /* Bind caller-owned DEVICE memory of capacity_elems doubles (>= packed_elems, 16-B aligned). */
 tt_status tt_tensor_bind(tt_tensor t, void* dev_ptr, int64_t capacity_elems);
 /* Host <-> device copies of the whole packed buffer on the context stream (asynchronous when the
@@ -219,9 +231,20 @@ tt_status tt_task_list(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, 
 tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
                            tt_tensor B, const char* b_lbl, uint32_t group_mask, int32_t* owner);
 
+/* Balanced owner-computes partition with row splitting (reading R24): units (blocks,
+ * or groups of blocks per group_mask, which must then include dimension 0) are ordered by (cost desc,
+ * smallest block id asc) and laid along a cost axis; rank r gets [floor(r*W/P), floor((r+1)*W/P)) of
+ * it, and a unit that straddles a boundary is cut at the nearest row of its dimension-0 tile (round
+ * half up).  Balance is exact to one row; at most P-1 units are split.  Writes C's owners / parts
+ * (as tt_tensor_set_owner + tt_tensor_set_parts). */
+tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
+                             tt_tensor B, const char* b_lbl, uint32_t group_mask);
+
 /* Input-tile gather plan of this rank for tt_contract (host metadata; for tests and reports).
- * recv[3*i .. 3*i+2] = (operand 0=A/1=B, block id, source rank) for each block this rank receives;
- * send[3*i .. 3*i+2] = (operand, block id, destination rank).  Two-call pattern as tt_task_list. */
+ * recv[5*i .. 5*i+4] = (operand 0=A/1=B, block id, source rank, e0, e1): element range [e0, e1) of
+ * the block this rank receives (whole blocks, or rows of row-split parts);
+ * send[5*i .. 5*i+4] = (operand, block id, destination rank, e0, e1).  Two-call pattern as
+ * tt_task_list. */
 tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
                          tt_tensor B, const char* b_lbl, int64_t* recv, int64_t* n_recv,
                          int64_t* send, int64_t* n_send, int64_t cap);

@@ -306,3 +306,48 @@ def lpt_partition_grouped(C: Tensor, cost: Sequence[int], cblocks: Sequence[int]
         unit_of.append(units[key])
     uown = lpt_partition(ucost, uid, nranks)
     return [uown[u] for u in unit_of]
+
+
+def partition_split(C: Tensor, cost: Sequence[int], cblocks: Sequence[int], group_dims: Sequence[int],
+                    nranks: int):
+    """Balanced partition with row splitting (reading R24b, SURVEY 8(e) "block splitting").
+
+    Units (single blocks, or blocks sharing the tile coordinates of ``group_dims``, which then
+    include dim 0) are ordered by (cost desc, smallest block id asc) and laid end to end on a cost
+    axis of length W; rank r owns [floor(r*W/P), floor((r+1)*W/P)).  A unit that straddles a
+    boundary is cut at the nearest row of its dim-0 tile: row = round_half_up((B_r - c0)*rows/cost).
+    Returns {block: [(lo, hi, owner), ...]} for every non-zero C block in ``cblocks``."""
+    units, order_keys = {}, []
+    for c, b in zip(cost, cblocks):
+        coords = C.block_coords(b)
+        key = tuple(coords[d] for d in group_dims) if group_dims else (b,)
+        if key not in units:
+            units[key] = {"cost": 0, "id": b, "rows": C.dims[0].size(coords[0]), "blocks": []}
+            order_keys.append(key)
+        units[key]["cost"] += c
+        units[key]["blocks"].append(b)
+    order = sorted(order_keys, key=lambda k: (-units[k]["cost"], units[k]["id"]))
+    W = sum(units[k]["cost"] for k in order)
+    Bd = [r * W // nranks for r in range(nranks + 1)]
+    out, cum = {}, 0
+    for k in order:
+        u = units[k]
+        c0, c1, rows = cum, cum + u["cost"], u["rows"]
+        cum = c1
+        r0 = max([r for r in range(nranks) if Bd[r] <= c0] or [0])
+        parts, cur, start = [], r0, 0
+        if u["cost"] > 0:
+            for r in range(r0 + 1, nranks):
+                if Bd[r] >= c1:
+                    break
+                row = ((Bd[r] - c0) * rows * 2 + u["cost"]) // (2 * u["cost"])
+                row = min(max(row, 0), rows)
+                if row > start:
+                    parts.append((start, row, cur))
+                    start = row
+                cur = r
+        if rows > start:
+            parts.append((start, rows, cur))
+        for b in u["blocks"]:
+            out[b] = parts
+    return out

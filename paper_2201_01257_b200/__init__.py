@@ -31,6 +31,7 @@ ERRORS = {-1: "TT_E_ARG", -2: "TT_E_COVERAGE", -3: "TT_E_LABEL", -4: "TT_E_TILIN
           -6: "TT_E_UNBOUND", -7: "TT_E_OOM", -8: "TT_E_CUDA", -9: "TT_E_NCCL", -10: "TT_E_STATE",
           -11: "TT_E_UNSUPPORTED"}
 TT_REPLICATED = -2
+TT_SPLIT = -3
 KIND_UNIFORM, KIND_INTEGER = 0, 1
 
 _vp, _i32, _i64, _u32, _u64, _dbl = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
@@ -67,6 +68,8 @@ _SIGS = {
     "tt_tensor_info": [_vp, _P(_i32), _P(_i64), _P(_i64)],
     "tt_tensor_layout": [_vp, _P(_i64), _P(_P(_i64)), _P(_P(_i32)), _P(_P(ctypes.c_uint8))],
     "tt_tensor_set_owner": [_vp, _vp],
+    "tt_tensor_set_parts": [_vp, _i64, _vp, _vp, _vp, _vp],
+    "tt_tensor_parts": [_vp, _P(_i64), _P(_P(_i64)), _P(_P(_i32)), _P(_P(_i32)), _P(_P(_i32))],
     "tt_tensor_bind": [_vp, _vp, _i64],
     "tt_tensor_upload": [_vp, _vp, _vp],
     "tt_tensor_download": [_vp, _vp, _vp],
@@ -79,6 +82,7 @@ _SIGS = {
     "tt_task_list": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _i32, _vp, _vp, _vp,
                      _vp, _vp, _i64, _P(_i64), _P(_i64)],
     "tt_partition_lpt": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32, _vp],
+    "tt_partition_split": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32],
     "tt_gather_plan": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _P(_i64), _vp,
                        _P(_i64), _i64],
     "tt_last_error": [],
@@ -253,6 +257,14 @@ class Tensor:
         self.blk_off = np.ctypeslib.as_array(bo, (nb.value,)).copy()
         self.owner = np.ctypeslib.as_array(ow, (nb.value,)).copy()
         self.nz = np.ctypeslib.as_array(z, (nb.value,)).copy()
+        n = _i64()
+        pb, plo, phi, pow_ = _P(_i64)(), _P(_i32)(), _P(_i32)(), _P(_i32)()
+        _check(_lib.tt_tensor_parts(self.h, ctypes.byref(n), ctypes.byref(pb), ctypes.byref(plo), ctypes.byref(phi),
+                                    ctypes.byref(pow_)))
+        k = n.value
+        self.parts = [tuple(int(x) for x in row) for row in zip(
+            np.ctypeslib.as_array(pb, (k,)) if k else [], np.ctypeslib.as_array(plo, (k,)) if k else [],
+            np.ctypeslib.as_array(phi, (k,)) if k else [], np.ctypeslib.as_array(pow_, (k,)) if k else [])]
 
     @property
     def shape(self):
@@ -265,6 +277,14 @@ class Tensor:
     def set_owner(self, owner):
         o = np.ascontiguousarray(owner, dtype=np.int32)
         _check(_lib.tt_tensor_set_owner(self.h, _ptr(o)))
+        self._refresh()
+
+    def set_parts(self, parts):
+        """Row-range ownership: ``parts`` = [(block, lo, hi, owner)] (see tt_tensor_set_parts)."""
+        a = np.asarray(parts, dtype=np.int64).reshape(-1, 4)
+        blk = np.ascontiguousarray(a[:, 0])
+        lo, hi, ow = (np.ascontiguousarray(a[:, i], dtype=np.int32) for i in (1, 2, 3))
+        _check(_lib.tt_tensor_set_parts(self.h, len(a), _ptr(blk), _ptr(lo), _ptr(hi), _ptr(ow)))
         self._refresh()
 
     def bind(self, storage, capacity: Optional[int] = None):
@@ -348,13 +368,21 @@ def partition_lpt(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B:
     return own
 
 
+def partition_split(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str,
+                    group_dims: Sequence[int] = ()):
+    """Balanced partition with row splitting (tt_partition_split); updates C's ownership in place."""
+    mask = sum(1 << d for d in group_dims)
+    _check(_lib.tt_partition_split(ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl), mask))
+    C._refresh()
+
+
 def gather_plan(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str):
-    """(recv, send) arrays of (operand, block, peer) rows for this rank."""
+    """(recv, send) arrays of (operand, block, peer, e0, e1) rows for this rank."""
     nr, ns = _i64(), _i64()
     args = (ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl))
     _check(_lib.tt_gather_plan(*args, None, ctypes.byref(nr), None, ctypes.byref(ns), 0))
     cap = max(nr.value, ns.value, 1)
-    r = np.empty(3 * cap, np.int64)
-    s = np.empty(3 * cap, np.int64)
+    r = np.empty(5 * cap, np.int64)
+    s = np.empty(5 * cap, np.int64)
     _check(_lib.tt_gather_plan(*args, _ptr(r), ctypes.byref(nr), _ptr(s), ctypes.byref(ns), cap))
-    return r[:3 * nr.value].reshape(-1, 3), s[:3 * ns.value].reshape(-1, 3)
+    return r[:5 * nr.value].reshape(-1, 5), s[:5 * ns.value].reshape(-1, 5)

@@ -308,55 +308,84 @@ std::vector<int32_t> lpt(const std::vector<int64_t>& cost, const std::vector<int
 }
 
 // ---------------------------------------------------------------------------------------------
-// gather plan: blocks this rank reads but does not hold (P212)
+// gather plan: element ranges of input blocks this rank reads but does not hold (P212; SURVEY
+// §8(a) A4).  A need is a range [e0, e1) of a block (the whole block, or the rows of a row-split
+// part); the sources are the block's owner or the owners of the overlapping parts.
 
 struct Run {
-  int op;        // 0 = A, 1 = B
+  int op;        // operand index into the ops list
   int peer;
   int64_t off, len;
 };
 
 struct GatherPlan {
-  std::vector<int64_t> recv_list, send_list;   // (op, block, peer) triples
+  std::vector<int64_t> recv_list, send_list;   // (op, block, peer, e0, e1) rows
   std::vector<Run> recv, send;
   int64_t recv_bytes = 0;
 };
 
-// need[r] = set of (op, block) rank r reads; identical computation on every rank (SPMD)
-void build_gather(tt_ctx ctx, const std::vector<std::vector<std::pair<int, int64_t>>>& need,
-                  const std::vector<tt_tensor>& ops, GatherPlan& gp) {
+struct Need {
+  int op;
+  int64_t blk, e0, e1;
+};
+using Needs = std::vector<std::vector<Need>>;   // per rank
+
+// sort and merge overlapping ranges of the same (op, block)
+void normalize(std::vector<Need>& v) {
+  std::sort(v.begin(), v.end(), [](const Need& x, const Need& y) {
+    return std::make_tuple(x.op, x.blk, x.e0, x.e1) < std::make_tuple(y.op, y.blk, y.e0, y.e1);
+  });
+  std::vector<Need> out;
+  for (const Need& n : v) {
+    if (!out.empty() && out.back().op == n.op && out.back().blk == n.blk && n.e0 <= out.back().e1) {
+      out.back().e1 = std::max(out.back().e1, n.e1);
+      continue;
+    }
+    out.push_back(n);
+  }
+  v.swap(out);
+}
+
+// owners of the pieces of [e0, e1) of block b of T
+template <class F>
+void pieces(tt_tensor T, int64_t b, int64_t e0, int64_t e1, F&& emit) {
+  if (T->parts[b].empty()) {
+    emit(T->owner[b], e0, e1);
+    return;
+  }
+  const int64_t inner = T->block_volume(b) / T->ext0(b);
+  for (const auto& p : T->parts[b]) {
+    const int64_t a = std::max(e0, p.lo * inner), z = std::min(e1, p.hi * inner);
+    if (a < z) emit(p.owner, a, z);
+  }
+}
+
+void build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops, GatherPlan& gp) {
   const int me = ctx->rank, P = ctx->nranks;
-  // blocks per (src, dst), sorted by op then block id (= packed order)
   for (int dst = 0; dst < P; ++dst) {
-    for (const auto& nb : need[dst]) {
-      tt_tensor T = ops[nb.first];
-      int32_t o = T->owner[nb.second];
-      if (o == TT_REPLICATED || o == dst) continue;
-      if (dst == me) {
-        gp.recv_list.insert(gp.recv_list.end(), {nb.first, nb.second, o});
-      }
-      if (o == me) {
-        gp.send_list.insert(gp.send_list.end(), {nb.first, nb.second, dst});
-      }
+    normalize(need[dst]);
+    for (const Need& n : need[dst]) {
+      tt_tensor T = ops[n.op];
+      pieces(T, n.blk, n.e0, n.e1, [&](int32_t src, int64_t a, int64_t z) {
+        if (src == TT_REPLICATED || src == dst) return;
+        if (dst == me) gp.recv_list.insert(gp.recv_list.end(), {n.op, n.blk, src, a, z});
+        if (src == me) gp.send_list.insert(gp.send_list.end(), {n.op, n.blk, dst, a, z});
+      });
     }
   }
   auto runs = [&](const std::vector<int64_t>& lst, std::vector<Run>& out) {
-    // sort by (peer, op, block)
-    std::vector<size_t> idx(lst.size() / 3);
+    std::vector<size_t> idx(lst.size() / 5);
     std::iota(idx.begin(), idx.end(), 0);
+    auto goff = [&](size_t i) { return ops[lst[5 * i]]->blk_off[lst[5 * i + 1]] + lst[5 * i + 3]; };
     std::sort(idx.begin(), idx.end(), [&](size_t x, size_t y) {
-      auto kx = std::make_tuple(lst[3 * x + 2], lst[3 * x], lst[3 * x + 1]);
-      auto ky = std::make_tuple(lst[3 * y + 2], lst[3 * y], lst[3 * y + 1]);
-      return kx < ky;
+      return std::make_tuple(lst[5 * x + 2], lst[5 * x], goff(x)) < std::make_tuple(lst[5 * y + 2], lst[5 * y], goff(y));
     });
     for (size_t i : idx) {
-      int op = (int)lst[3 * i], peer = (int)lst[3 * i + 2];
-      int64_t b = lst[3 * i + 1];
-      tt_tensor T = ops[op];
-      int64_t off = T->blk_off[b], len = T->block_volume(b);
+      const int op = (int)lst[5 * i], peer = (int)lst[5 * i + 2];
+      const int64_t off = goff(i), len = lst[5 * i + 4] - lst[5 * i + 3];
       if (!out.empty() && out.back().op == op && out.back().peer == peer) {
         Run& r = out.back();
-        int64_t gap = off - (r.off + r.len);
+        const int64_t gap = off - (r.off + r.len);
         if (gap >= 0 && gap <= 1) {   // adjacent in packed order (<= 1 alignment pad element)
           r.len = off + len - r.off;
           continue;
@@ -420,7 +449,11 @@ tt_status check_bound(tt_tensor t, const char* which) {
 struct ContractPlan {
   Analysis an;
   HostTasks ht;
-  std::vector<int> my;             // indices into ht.cblk computed by this rank
+  struct MyPart {
+    int g;                         // index into ht.cblk
+    int64_t lo, hi;                // rows of the block's dim-0 tile computed by this rank
+  };
+  std::vector<MyPart> my;
   GatherPlan gp;
   int variant = 0;
   bool a_vec = false, b_vec = false;   // 16-byte copies along the operand's contiguous direction
@@ -732,6 +765,19 @@ static void tensor_finish(tt_tensor t) {
     t->nnz++;
   }
   t->packed_elems = (cur + 1) / 2 * 2;
+  t->parts.assign(t->nblocks, {});
+  t->any_split = false;
+}
+
+static void refresh_parts_view(tt_tensor t) {
+  t->pv_blk.clear(); t->pv_lo.clear(); t->pv_hi.clear(); t->pv_owner.clear();
+  t->any_split = false;
+  for (int64_t b = 0; b < t->nblocks; ++b) {
+    for (const auto& p : t->parts[b]) {
+      t->pv_blk.push_back(b); t->pv_lo.push_back(p.lo); t->pv_hi.push_back(p.hi); t->pv_owner.push_back(p.owner);
+      t->any_split = true;
+    }
+  }
 }
 
 tt_status tt_tensor_create(tt_ctx ctx, int32_t order, const tt_tis* dims, const uint8_t* nz, tt_tensor* out) {
@@ -795,7 +841,52 @@ tt_status tt_tensor_set_owner(tt_tensor t, const int32_t* owner) {
       return fail(TT_E_ARG, "owner[%lld] = %d out of range", (long long)b, owner[b]);
   }
   for (int64_t b = 0; b < t->nblocks; ++b) t->owner[b] = t->nz[b] ? owner[b] : -1;
+  t->parts.assign(t->nblocks, {});
+  refresh_parts_view(t);
   t->version++;
+  return TT_OK;
+}
+
+tt_status tt_tensor_set_parts(tt_tensor t, int64_t n, const int64_t* blk, const int32_t* lo, const int32_t* hi,
+                              const int32_t* owner) {
+  if (!t || (n > 0 && (!blk || !lo || !hi || !owner))) return fail(TT_E_ARG, "NULL argument");
+  std::map<int64_t, std::vector<tt_tensor_s::Part>> np;
+  for (int64_t i = 0; i < n; ++i) {
+    if (blk[i] < 0 || blk[i] >= t->nblocks || !t->nz[blk[i]])
+      return fail(TT_E_ARG, "part %lld: block %lld is not a non-zero block", (long long)i, (long long)blk[i]);
+    if (owner[i] < 0 || owner[i] >= t->ctx->nranks) return fail(TT_E_ARG, "part %lld: owner %d out of range", (long long)i, owner[i]);
+    np[blk[i]].push_back({lo[i], hi[i], owner[i]});
+  }
+  for (auto& kv : np) {   // validate: parts tile [0, ext0) in order, non-empty
+    int32_t pos = 0;
+    for (const auto& p : kv.second) {
+      if (p.lo != pos || p.hi <= p.lo) return fail(TT_E_ARG, "parts of block %lld must tile its dim-0 range in order", (long long)kv.first);
+      pos = p.hi;
+    }
+    if (pos != t->ext0(kv.first)) return fail(TT_E_ARG, "parts of block %lld do not cover its dim-0 tile", (long long)kv.first);
+  }
+  for (auto& kv : np) {
+    if (kv.second.size() == 1) {
+      t->owner[kv.first] = kv.second[0].owner;
+      t->parts[kv.first].clear();
+    } else {
+      t->owner[kv.first] = TT_SPLIT;
+      t->parts[kv.first] = kv.second;
+    }
+  }
+  refresh_parts_view(t);
+  t->version++;
+  return TT_OK;
+}
+
+tt_status tt_tensor_parts(tt_tensor t, int64_t* n, const int64_t** blk, const int32_t** lo, const int32_t** hi,
+                          const int32_t** owner) {
+  if (!t || !n) return fail(TT_E_ARG, "NULL argument");
+  *n = (int64_t)t->pv_blk.size();
+  if (blk) *blk = t->pv_blk.data();
+  if (lo) *lo = t->pv_lo.data();
+  if (hi) *hi = t->pv_hi.data();
+  if (owner) *owner = t->pv_owner.data();
   return TT_OK;
 }
 
@@ -898,8 +989,24 @@ void add_tiles(ElemPlan& ep, int32_t desc) {
       for (int tx = 0; tx < ntx; ++tx) ep.tiles.push_back({desc, tx, ty, (int32_t)b});
 }
 
-void add_segments(ElemPlan& ep, int32_t desc, int64_t vol) {
-  for (int64_t e = 0; e < vol; e += kSegElems) ep.segs.push_back({desc, 0, e, std::min(vol, e + kSegElems)});
+void add_segments(ElemPlan& ep, int32_t desc, int64_t e_begin, int64_t e_end) {
+  for (int64_t e = e_begin; e < e_end; e += kSegElems) ep.segs.push_back({desc, 0, e, std::min(e_end, e + kSegElems)});
+}
+
+// whether the dim-0 label of X is also the dim-0 label of Y: then a row range of an X part maps to
+// a contiguous row range of the matching Y block
+int64_t sub_range_inner(tt_tensor Y, int64_t yb, bool same_dim0, int64_t lo_row, int64_t hi_row, int64_t* e0,
+                        int64_t* e1) {
+  const int64_t vol = Y->block_volume(yb);
+  if (!same_dim0) {
+    *e0 = 0;
+    *e1 = vol;
+    return vol;
+  }
+  const int64_t inner = vol / Y->ext0(yb);
+  *e0 = lo_row * inner;
+  *e1 = hi_row * inner;
+  return inner;
 }
 
 tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
@@ -943,8 +1050,10 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
     int64_t acc = 1;
     for (int d = t->order - 1; d >= 0; --d) { gstr[d] = acc; acc *= t->dims[d]->is->extent; }
     int32_t c[TT_MAX_ORDER];
+    std::vector<std::pair<int64_t, int64_t>> hr;
     for (int64_t b = 0; b < t->nblocks; ++b) {
-      if (!t->held(b, ctx->rank)) continue;
+      t->held_ranges(b, ctx->rank, hr);
+      if (hr.empty()) continue;
       t->block_coords(b, c);
       ElemDesc d{};
       d.x_off = t->blk_off[b];
@@ -957,7 +1066,7 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
         d.g_origin += t->dims[q]->offsets[c[q]] * gstr[q];
       }
       ep->descs.push_back(d);
-      add_segments(*ep, (int32_t)ep->descs.size() - 1, t->block_volume(b));
+      for (auto& r : hr) add_segments(*ep, (int32_t)ep->descs.size() - 1, r.first, r.second);
     }
     TT_TRY(upload_elem(ctx, *ep, false));
     ctx->plans[keybuf] = ep;
@@ -987,14 +1096,18 @@ tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha) {
   auto ep = cached<ElemPlan>(ctx, keybuf);
   if (!ep) {
     ep = std::make_shared<ElemPlan>();
+    std::vector<std::pair<int64_t, int64_t>> hr;
     for (int64_t b = 0; b < C->nblocks; ++b) {
-      if (!C->held(b, ctx->rank)) continue;
+      C->held_ranges(b, ctx->rank, hr);
+      if (hr.empty()) continue;
       ElemDesc d{};
       d.x_off = C->blk_off[b];
       d.y_off = -1;
       ep->descs.push_back(d);
-      add_segments(*ep, (int32_t)ep->descs.size() - 1, C->block_volume(b));
-      ep->bytes += 8.0 * C->block_volume(b);
+      for (auto& r : hr) {
+        add_segments(*ep, (int32_t)ep->descs.size() - 1, r.first, r.second);
+        ep->bytes += 8.0 * (r.second - r.first);
+      }
       ep->blocks++;
     }
     TT_TRY(upload_elem(ctx, *ep, false));
@@ -1037,16 +1150,27 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
   auto ep = cached<ElemPlan>(ctx, key);
   if (!ep) {
     ep = std::make_shared<ElemPlan>();
-    std::vector<std::vector<std::pair<int, int64_t>>> need(ctx->nranks);
+    Needs need(ctx->nranks);
     int32_t cc[TT_MAX_ORDER], ac[TT_MAX_ORDER];
+    const bool same0 = perm[0] == 0;
+    std::vector<std::pair<int64_t, int64_t>> hr, mine;
     for (int64_t b = 0; b < C->nblocks; ++b) {
       if (!C->nz[b]) continue;
       C->block_coords(b, cc);
       for (int d = 0; d < C->order; ++d) ac[perm[d]] = cc[d];
       int64_t ab = A->block_id(ac);
-      for (int r = 0; r < ctx->nranks; ++r)
-        if (C->held(b, r) && A->nz[ab]) need[r].push_back({0, ab});
-      if (!C->held(b, ctx->rank)) continue;
+      const int64_t cin = C->block_volume(b) / C->ext0(b);
+      for (int r = 0; r < ctx->nranks; ++r) {
+        C->held_ranges(b, r, hr);
+        if (r == ctx->rank) mine = hr;
+        if (!A->nz[ab]) continue;
+        for (auto& h : hr) {
+          int64_t e0, e1;
+          sub_range_inner(A, ab, same0, h.first / cin, h.second / cin, &e0, &e1);
+          need[r].push_back({0, ab, e0, e1});
+        }
+      }
+      if (mine.empty()) continue;
       ElemDesc d{};
       d.x_off = C->blk_off[b];
       d.y_off = A->nz[ab] ? A->blk_off[ab] : -1;
@@ -1056,14 +1180,17 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
       int32_t ext[TT_MAX_ORDER];
       for (int q = 0; q < C->order; ++q) ext[q] = (int32_t)C->dims[q]->size(cc[q]);
       ep->mode = fuse_elem(d, C->order, ext, perm.data(), sa);
+      if (ep->mode == kElemTranspose && C->any_split) ep->mode = kElemGeneric;   // tiles need whole blocks
       ep->descs.push_back(d);
       const int32_t di = (int32_t)ep->descs.size() - 1;
-      if (ep->mode == kElemTranspose) add_tiles(*ep, di);
-      else add_segments(*ep, di, C->block_volume(b));
-      ep->bytes += 8.0 * C->block_volume(b) * ((beta != 0.0) + 1 + (A->nz[ab] ? 1 : 0));
+      for (auto& h : mine) {
+        if (ep->mode == kElemTranspose) add_tiles(*ep, di);
+        else add_segments(*ep, di, h.first, h.second);
+        ep->bytes += 8.0 * (h.second - h.first) * ((beta != 0.0) + 1 + (A->nz[ab] ? 1 : 0));
+      }
       ep->blocks++;
     }
-    for (auto& v : need) { std::sort(v.begin(), v.end()); v.erase(std::unique(v.begin(), v.end()), v.end()); }
+    if (ep->mode != kElemTranspose) ep->tiles.clear();
     build_gather(ctx, need, {A}, ep->gp);
     TT_TRY(upload_elem(ctx, *ep, false));
     ctx->plans[key] = ep;
@@ -1112,18 +1239,32 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
   auto ep = cached<ElemPlan>(ctx, key);
   if (!ep) {
     ep = std::make_shared<ElemPlan>();
-    std::vector<std::vector<std::pair<int, int64_t>>> need(ctx->nranks);
+    Needs need(ctx->nranks);
     int32_t ac[TT_MAX_ORDER], bc[TT_MAX_ORDER];
+    const bool same0 = perm[0] == 0;
     for (int64_t blk = 0; blk < A->nblocks; ++blk) {
       if (!A->nz[blk]) continue;
       A->block_coords(blk, ac);
       for (int d = 0; d < A->order; ++d) bc[perm[d]] = ac[d];
       int64_t bb = B->block_id(bc);
       if (!B->nz[bb]) continue;
-      // the rank that sums this pair: A's owner (replicated A blocks: rank 0)
-      int32_t r = A->owner[blk] == TT_REPLICATED ? 0 : A->owner[blk];
-      need[r].push_back({1, bb});
-      if (r != ctx->rank) continue;
+      // the rank that sums a piece of this pair: A's owner of the piece (replicated A blocks: rank 0)
+      std::vector<std::pair<int32_t, std::pair<int64_t, int64_t>>> who;
+      if (A->parts[blk].empty()) {
+        who.push_back({A->owner[blk] == TT_REPLICATED ? 0 : A->owner[blk], {0, A->block_volume(blk)}});
+      } else {
+        const int64_t inner = A->block_volume(blk) / A->ext0(blk);
+        for (const auto& pt : A->parts[blk]) who.push_back({pt.owner, {pt.lo * inner, pt.hi * inner}});
+      }
+      const int64_t ain = A->block_volume(blk) / A->ext0(blk);
+      std::vector<std::pair<int64_t, int64_t>> mine;
+      for (auto& w : who) {
+        int64_t e0, e1;
+        sub_range_inner(B, bb, same0, w.second.first / ain, w.second.second / ain, &e0, &e1);
+        need[w.first].push_back({1, bb, e0, e1});
+        if (w.first == ctx->rank) mine.push_back(w.second);
+      }
+      if (mine.empty()) continue;
       ElemDesc d{};
       d.x_off = A->blk_off[blk];
       d.y_off = B->blk_off[bb];
@@ -1132,13 +1273,16 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
       int32_t ext[TT_MAX_ORDER];
       for (int q = 0; q < A->order; ++q) ext[q] = (int32_t)A->dims[q]->size(ac[q]);
       ep->mode = fuse_elem(d, A->order, ext, perm.data(), sb);
+      if (ep->mode == kElemTranspose && A->any_split) ep->mode = kElemGeneric;
       ep->descs.push_back(d);
-      if (ep->mode == kElemTranspose) add_tiles(*ep, (int32_t)ep->descs.size() - 1);
-      else add_segments(*ep, (int32_t)ep->descs.size() - 1, A->block_volume(blk));
-      ep->bytes += 16.0 * A->block_volume(blk);
+      for (auto& h : mine) {
+        if (ep->mode == kElemTranspose) add_tiles(*ep, (int32_t)ep->descs.size() - 1);
+        else add_segments(*ep, (int32_t)ep->descs.size() - 1, h.first, h.second);
+        ep->bytes += 16.0 * (h.second - h.first);
+      }
       ep->blocks++;
     }
-    for (auto& v : need) { std::sort(v.begin(), v.end()); v.erase(std::unique(v.begin(), v.end()), v.end()); }
+    if (ep->mode != kElemTranspose) ep->tiles.clear();
     build_gather(ctx, need, {A, B}, ep->gp);
     TT_TRY(upload_elem(ctx, *ep, true));
     ctx->plans[key] = ep;
@@ -1192,43 +1336,44 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
   const HostTasks& ht = pl.ht;
   std::vector<tt_tis> lt(an.uni.size());
   for (size_t u = 0; u < an.uni.size(); ++u) lt[u] = label_tis(an, (int)u, C, A);
-  // blocks computed per rank; inputs read per rank
-  std::vector<std::vector<std::pair<int, int64_t>>> need(ctx->nranks);
+  // C parts computed per rank (owner-computes); input ranges read per rank.  When C is row-split
+  // and C's dim-0 label is also the dim-0 label of A (B), only the matching rows of A (B) are read.
+  Needs need(ctx->nranks);
+  const bool a_same0 = an.a_lab[0] == 0, b_same0 = an.b_lab[0] == 0;
+  const int bop = (A == B) ? 0 : 1;   // A and B may be the same tensor (same storage)
+  std::vector<std::pair<int64_t, int64_t>> hr;
   for (size_t g = 0; g < ht.cblk.size(); ++g) {
+    const int64_t cb = ht.cblk[g];
+    const int64_t cin = C->block_volume(cb) / C->ext0(cb);
     for (int r = 0; r < ctx->nranks; ++r) {
-      if (!C->held(ht.cblk[g], r)) continue;
-      for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
-        need[r].push_back({0, ht.a_blk[t]});
-        need[r].push_back({1, ht.b_blk[t]});
+      C->held_ranges(cb, r, hr);
+      for (auto& h : hr) {
+        const int64_t lo = h.first / cin, hi = h.second / cin;
+        if (r == ctx->rank) pl.my.push_back({(int)g, lo, hi});
+        for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
+          int64_t e0, e1;
+          sub_range_inner(A, ht.a_blk[t], a_same0, lo, hi, &e0, &e1);
+          need[r].push_back({0, ht.a_blk[t], e0, e1});
+          sub_range_inner(B, ht.b_blk[t], b_same0, lo, hi, &e0, &e1);
+          need[r].push_back({bop, ht.b_blk[t], e0, e1});
+        }
       }
     }
-    if (C->held(ht.cblk[g], ctx->rank)) pl.my.push_back((int)g);
   }
-  for (auto& v : need) { std::sort(v.begin(), v.end()); v.erase(std::unique(v.begin(), v.end()), v.end()); }
-  // A and B may be the same tensor: then both operands index the same storage
-  build_gather(ctx, need, {A, B}, pl.gp);
-  if (A == B) {
-    // drop duplicate B entries that refer to the same block as an A entry
-    GatherPlan gp2;
-    std::vector<std::vector<std::pair<int, int64_t>>> need2(ctx->nranks);
-    for (int r = 0; r < ctx->nranks; ++r) {
-      for (auto& x : need[r]) need2[r].push_back({0, x.second});
-      std::sort(need2[r].begin(), need2[r].end());
-      need2[r].erase(std::unique(need2[r].begin(), need2[r].end()), need2[r].end());
-    }
-    build_gather(ctx, need2, {A}, gp2);
-    pl.gp = gp2;
-  }
+  if (A == B) build_gather(ctx, need, {A}, pl.gp);
+  else build_gather(ctx, need, {A, B}, pl.gp);
   // stats for this rank
   {
     std::vector<char> ua(A->nblocks, 0), ub(B->nblocks, 0);
-    for (int g : pl.my) {
-      pl.flops += (double)ht.cost[g];
+    for (const auto& mp : pl.my) {
+      const int g = mp.g;
+      const double frac = (double)(mp.hi - mp.lo) / (double)C->ext0(ht.cblk[g]);
+      pl.flops += (double)ht.cost[g] * frac;
       pl.tasks += ht.ptr[g + 1] - ht.ptr[g];
-      pl.bytes += 8.0 * C->block_volume(ht.cblk[g]) * (1 + (beta != 0.0));
+      pl.bytes += 8.0 * C->block_volume(ht.cblk[g]) * frac * (1 + (beta != 0.0));
       for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
-        if (!ua[ht.a_blk[t]]) { ua[ht.a_blk[t]] = 1; pl.bytes += 8.0 * A->block_volume(ht.a_blk[t]); }
-        if (!ub[ht.b_blk[t]]) { ub[ht.b_blk[t]] = 1; pl.bytes += 8.0 * B->block_volume(ht.b_blk[t]); }
+        if (!ua[ht.a_blk[t]]) { ua[ht.a_blk[t]] = 1; pl.bytes += 8.0 * A->block_volume(ht.a_blk[t]) * (a_same0 ? frac : 1.0); }
+        if (!ub[ht.b_blk[t]]) { ub[ht.b_blk[t]] = 1; pl.bytes += 8.0 * B->block_volume(ht.b_blk[t]) * (b_same0 ? frac : 1.0); }
       }
     }
   }
@@ -1306,14 +1451,20 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
   pl.device_built = true;
 
   // ---- tile variant: greedy list-scheduling estimate of the makespan
-  std::vector<int64_t> Ms(ht.cblk.size()), Ns(ht.cblk.size());
+  // GEMM row / column ranges of every part (the split dim 0 of C is the outermost label of the first
+  // M group when it comes from A, else of the first N group)
+  const bool split_in_m = an.a_pos[0] >= 0;
+  std::vector<int64_t> Mb(pl.my.size()), Me(pl.my.size()), Nb(pl.my.size()), Ne(pl.my.size());
   int32_t cc[TT_MAX_ORDER];
-  for (int g : pl.my) {
-    C->block_coords(ht.cblk[g], cc);
+  for (size_t i = 0; i < pl.my.size(); ++i) {
+    const auto& mp = pl.my[i];
+    C->block_coords(ht.cblk[mp.g], cc);
     int64_t M = 1, N = 1;
     for (int u = 0; u < an.nc; ++u) (an.a_pos[u] >= 0 ? M : N) *= lt[u]->size(cc[u]);
-    Ms[g] = M;
-    Ns[g] = N;
+    const int64_t e0 = lt[0]->size(cc[0]);
+    Mb[i] = 0; Me[i] = M; Nb[i] = 0; Ne[i] = N;
+    if (split_in_m) { Mb[i] = mp.lo * (M / e0); Me[i] = mp.hi * (M / e0); }
+    else { Nb[i] = mp.lo * (N / e0); Ne[i] = mp.hi * (N / e0); }
   }
   // 16-B copies: the operand's innermost dim is the innermost label of its contiguous group, with
   // even extent in every tile
@@ -1333,10 +1484,11 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
   for (int v = 0; v < n_variants(); ++v) {
     VariantInfo vi = variant_info(v);
     std::vector<double> items;
-    for (int g : pl.my) {
+    for (size_t i = 0; i < pl.my.size(); ++i) {
+      const int g = pl.my[i].g;
       double kst = 0;
       for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) kst += (double)((ht.K[t] + vi.bk - 1) / vi.bk);
-      const int64_t nit = ((Ms[g] + vi.bm - 1) / vi.bm) * ((Ns[g] + vi.bn - 1) / vi.bn);
+      const int64_t nit = ((Me[i] - Mb[i] + vi.bm - 1) / vi.bm) * ((Ne[i] - Nb[i] + vi.bn - 1) / vi.bn);
       const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm / variant_efficiency(v);
       for (int64_t i = 0; i < nit; ++i) items.push_back(c);
     }
@@ -1359,20 +1511,28 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
   VariantInfo vi = variant_info(pl.variant);
 
   // ---- groups + work items (groups by cost desc, block id asc)
-  std::vector<int> order(pl.my);
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-    if (ht.cost[x] != ht.cost[y]) return ht.cost[x] > ht.cost[y];
-    return ht.cblk[x] < ht.cblk[y];
+  std::vector<size_t> order(pl.my.size());
+  std::iota(order.begin(), order.end(), 0);
+  auto pcost = [&](size_t i) {
+    const auto& mp = pl.my[i];
+    return (double)ht.cost[mp.g] * (double)(mp.hi - mp.lo) / (double)C->ext0(ht.cblk[mp.g]);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+    if (pcost(x) != pcost(y)) return pcost(x) > pcost(y);
+    return ht.cblk[pl.my[x].g] < ht.cblk[pl.my[y].g];
   });
   std::vector<CGroupDesc> groups;
   std::vector<WorkItem> work;
-  for (int g : order) {
+  for (size_t oi : order) {
+    const int g = pl.my[oi].g;
     CGroupDesc gd{};
     int64_t cb = ht.cblk[g];
     C->block_coords(cb, cc);
     gd.c_off = C->blk_off[cb];
-    gd.M = (int32_t)Ms[g];
-    gd.N = (int32_t)Ns[g];
+    gd.M = (int32_t)Me[oi];
+    gd.N = (int32_t)Ne[oi];
+    gd.m_begin = (int32_t)Mb[oi];
+    gd.n_begin = (int32_t)Nb[oi];
     gd.task_begin = (int32_t)ht.ptr[g];
     gd.task_end = (int32_t)ht.ptr[g + 1];
     int64_t st = 0;
@@ -1395,7 +1555,7 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     }
     const int32_t gi = (int32_t)groups.size();
     groups.push_back(gd);
-    const int32_t mtn = (gd.M + vi.bm - 1) / vi.bm, ntn = (gd.N + vi.bn - 1) / vi.bn;
+    const int32_t mtn = (gd.M - gd.m_begin + vi.bm - 1) / vi.bm, ntn = (gd.N - gd.n_begin + vi.bn - 1) / vi.bn;
     for (int32_t mt = 0; mt < mtn; ++mt)
       for (int32_t nt = 0; nt < ntn; ++nt) work.push_back({gi, mt, nt});
   }
@@ -1551,6 +1711,88 @@ tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A,
   return TT_OK;
 }
 
+tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
+                             const char* bl, uint32_t group_mask) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  Analysis an;
+  TT_TRY(analyse(C, cl, A, al, B, bl, an));
+  if (group_mask >> C->order) return fail(TT_E_ARG, "group_mask references dims beyond the order of C");
+  if (group_mask && !(group_mask & 1u)) return fail(TT_E_ARG, "row splitting needs dim 0 among the grouping dims");
+  HostTasks ht;
+  enumerate_tasks(an, C, A, B, ht);
+  // units (as tt_partition_lpt)
+  std::map<std::vector<int32_t>, size_t> unit_of;
+  std::vector<int64_t> ucost, uid, urows;
+  std::vector<std::vector<int64_t>> ublocks;
+  int32_t cc[TT_MAX_ORDER];
+  for (size_t g = 0; g < ht.cblk.size(); ++g) {
+    std::vector<int32_t> key;
+    C->block_coords(ht.cblk[g], cc);
+    if (group_mask) {
+      for (int d = 0; d < C->order; ++d)
+        if (group_mask >> d & 1) key.push_back(cc[d]);
+    } else {
+      key.push_back((int32_t)g);
+    }
+    auto it = unit_of.find(key);
+    if (it == unit_of.end()) {
+      it = unit_of.emplace(key, ucost.size()).first;
+      ucost.push_back(0);
+      uid.push_back(ht.cblk[g]);
+      urows.push_back(C->dims[0]->size(cc[0]));
+      ublocks.push_back({});
+    }
+    ucost[it->second] += ht.cost[g];
+    ublocks[it->second].push_back(ht.cblk[g]);
+  }
+  std::vector<size_t> order(ucost.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+    if (ucost[x] != ucost[y]) return ucost[x] > ucost[y];
+    return uid[x] < uid[y];
+  });
+  // water-filling along the ordered cost axis: rank r owns [B_r, B_{r+1}), B_r = floor(r*W/P);
+  // a unit straddling a boundary is cut at the nearest row (round half up)
+  const int P = ctx->nranks;
+  __int128 W = 0;
+  for (int64_t c : ucost) W += c;
+  std::vector<int64_t> Bd(P + 1);
+  for (int r = 0; r <= P; ++r) Bd[r] = (int64_t)((__int128)r * W / P);
+  std::vector<int32_t> own(C->nblocks, -1);
+  std::vector<std::vector<tt_tensor_s::Part>> parts(C->nblocks);
+  int64_t cum = 0;
+  for (size_t u : order) {
+    const int64_t c0 = cum, c1 = cum + ucost[u], rows = urows[u];
+    cum = c1;
+    int r0 = 0;
+    for (int r = 1; r < P; ++r)
+      if (Bd[r] <= c0) r0 = r;
+    std::vector<tt_tensor_s::Part> pp;
+    int cur = r0;
+    int64_t start = 0;
+    for (int r = r0 + 1; r < P && ucost[u] > 0; ++r) {
+      if (Bd[r] >= c1) break;
+      int64_t row = (int64_t)(((__int128)(Bd[r] - c0) * rows * 2 + ucost[u]) / ((__int128)2 * ucost[u]));
+      row = std::min(std::max(row, (int64_t)0), rows);
+      if (row > start) {
+        pp.push_back({(int32_t)start, (int32_t)row, cur});
+        start = row;
+      }
+      cur = r;
+    }
+    if (rows > start) pp.push_back({(int32_t)start, (int32_t)rows, cur});
+    for (int64_t b : ublocks[u]) {
+      if (pp.size() == 1) own[b] = pp[0].owner;
+      else { own[b] = TT_SPLIT; parts[b] = pp; }
+    }
+  }
+  for (int64_t b = 0; b < C->nblocks; ++b) C->owner[b] = C->nz[b] ? own[b] : -1;
+  C->parts = parts;
+  refresh_parts_view(C);
+  C->version++;
+  return TT_OK;
+}
+
 tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
                          const char* bl, int64_t* recv, int64_t* n_recv, int64_t* send, int64_t* n_send, int64_t cap) {
   if (!ctx || !n_recv || !n_send) return fail(TT_E_ARG, "NULL argument");
@@ -1565,8 +1807,8 @@ tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, c
   host.nranks = ctx->nranks;
   host.sm_count = ctx->sm_count;
   TT_TRY(build_contract_plan(&host, C, A, B, 1.0, pl));
-  *n_recv = (int64_t)pl.gp.recv_list.size() / 3;
-  *n_send = (int64_t)pl.gp.send_list.size() / 3;
+  *n_recv = (int64_t)pl.gp.recv_list.size() / 5;
+  *n_send = (int64_t)pl.gp.send_list.size() / 5;
   if (!recv && !send) return TT_OK;
   if (cap < std::max(*n_recv, *n_send)) return fail(TT_E_ARG, "capacity too small");
   if (recv) std::copy(pl.gp.recv_list.begin(), pl.gp.recv_list.end(), recv);

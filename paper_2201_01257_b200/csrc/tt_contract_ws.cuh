@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(co
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int m0 = w.mt * K::BM, n0 = w.nt * K::BN;
+  const int m0 = g.m_begin + w.mt * K::BM, n0 = g.n_begin + w.nt * K::BN;
 
   if (warp >= K::NMMA) {
     // ------------------------------------------------------------- producers

@@ -24,7 +24,8 @@ constexpr int kMaxGroup = 4;  // fused label groups per GEMM side (M, N, K)
 // fused N groups (labels from B), innermost last.
 struct CGroupDesc {
   int64_t c_off;                 // packed offset of the C block
-  int32_t M, N;                  // GEMM extents of the block
+  int32_t M, N;                  // GEMM row / column END of this group (exclusive)
+  int32_t m_begin, n_begin;      // first row / column (a part of a row-split block; else 0)
   int32_t task_begin, task_end;  // CSR range in the task array
   int32_t nstages;               // sum over tasks of ceil(K_t / BK) for the chosen kernel BK
   int32_t pad;
@@ -99,6 +100,33 @@ struct tt_tensor_s {
   int64_t* d_blk_off = nullptr;
   std::vector<int64_t*> d_toff;   // per dim tile offsets on the device
   bool dev_ready = false;
+  // row-range ownership (SURVEY §8(e) block splitting): a split block is owned by parts, each a
+  // range [lo, hi) of the block's dimension-0 tile; owner[b] is then TT_SPLIT
+  struct Part {
+    int32_t lo, hi, owner;
+  };
+  std::vector<std::vector<Part>> parts;     // per block; empty = whole block owned by owner[b]
+  std::vector<int64_t> pv_blk;              // flattened view for tt_tensor_parts
+  std::vector<int32_t> pv_lo, pv_hi, pv_owner;
+  bool any_split = false;
+
+  int64_t ext0(int64_t b) const {
+    int32_t c[TT_MAX_ORDER];
+    block_coords(b, c);
+    return dims[0]->size(c[0]);
+  }
+  // element ranges [e0, e1) of block b held by `rank` (whole block, replicated, or its parts)
+  void held_ranges(int64_t b, int32_t rank, std::vector<std::pair<int64_t, int64_t>>& out) const {
+    out.clear();
+    if (!nz[b]) return;
+    if (parts[b].empty()) {
+      if (owner[b] == rank || owner[b] == TT_REPLICATED) out.push_back({0, block_volume(b)});
+      return;
+    }
+    const int64_t inner = block_volume(b) / ext0(b);
+    for (const Part& p : parts[b])
+      if (p.owner == rank) out.push_back({p.lo * inner, p.hi * inner});
+  }
   bool held(int64_t b, int32_t rank) const { return nz[b] && (owner[b] == rank || owner[b] == TT_REPLICATED); }
 
   void block_coords(int64_t b, int32_t* c) const {

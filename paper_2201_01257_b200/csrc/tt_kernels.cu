@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_kernel(const
   if (tid == 0) g = p.groups[w.group];
   __syncthreads();
 
-  const int m0 = w.mt * K::BM, n0 = w.nt * K::BN;
+  const int m0 = g.m_begin + w.mt * K::BM, n0 = g.n_begin + w.nt * K::BN;
   const int M = g.M, N = g.N;
   const int nM = p.nM, nN = p.nN, nK = p.nK;
 
@@ -463,12 +463,14 @@ __device__ __forceinline__ int64_t y_offset(uint32_t e, const ElemDesc& d) {
 __global__ void set_kernel(const ElemParams p) {
   const Segment sg = p.segs[blockIdx.x];
   double* x = p.X + p.descs[sg.desc].x_off;
-  // segments start at even offsets inside 16-B aligned blocks: double2 stores, scalar tail
-  const int64_t n2 = (sg.e1 - sg.e0) / 2;
-  double2* x2 = reinterpret_cast<double2*>(x + sg.e0);
+  // blocks are 16-B aligned: peel an odd first element, double2 stores, scalar tail
+  const int64_t es = sg.e0 + (sg.e0 & 1);
+  const int64_t n2 = (sg.e1 - es) / 2;
+  double2* x2 = reinterpret_cast<double2*>(x + es);
   const double2 v = make_double2(p.alpha, p.alpha);
   for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) x2[i] = v;
-  if (threadIdx.x == 0 && (sg.e1 - sg.e0) % 2) x[sg.e1 - 1] = p.alpha;
+  if (threadIdx.x == 0 && es != sg.e0 && sg.e0 < sg.e1) x[sg.e0] = p.alpha;
+  if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) x[sg.e1 - 1] = p.alpha;
 }
 
 template <int MODE>
@@ -480,9 +482,10 @@ __global__ void add_kernel(const ElemParams p) {
   const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
   const double alpha = p.alpha, beta = p.beta;
   if (MODE == kElemContig) {
-    const int64_t n2 = (sg.e1 - sg.e0) / 2;
-    double2* x2 = reinterpret_cast<double2*>(x + sg.e0);
-    const double2* y2 = y ? reinterpret_cast<const double2*>(y + sg.e0) : nullptr;
+    const int64_t es = sg.e0 + (sg.e0 & 1);
+    const int64_t n2 = (sg.e1 - es) / 2;
+    double2* x2 = reinterpret_cast<double2*>(x + es);
+    const double2* y2 = y ? reinterpret_cast<const double2*>(y + es) : nullptr;
     for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
       double2 v = y2 ? y2[i] : make_double2(0.0, 0.0);
       v.x *= alpha;
@@ -494,10 +497,13 @@ __global__ void add_kernel(const ElemParams p) {
       }
       x2[i] = v;
     }
-    if (threadIdx.x == 0 && (sg.e1 - sg.e0) % 2) {
-      const int64_t e = sg.e1 - 1;
-      const double v = y ? alpha * y[e] : 0.0;
-      x[e] = (beta == 0.0) ? v : beta * x[e] + v;
+    if (threadIdx.x == 0) {
+      int64_t peel[2] = {es != sg.e0 ? sg.e0 : -1, es + 2 * n2 < sg.e1 ? sg.e1 - 1 : -1};
+      for (int64_t e : peel) {
+        if (e < 0) continue;
+        const double v = y ? alpha * y[e] : 0.0;
+        x[e] = (beta == 0.0) ? v : beta * x[e] + v;
+      }
     }
   } else {
     for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) {
@@ -658,15 +664,17 @@ __global__ void scalar_partials_kernel(const ElemParams p) {
   const double* y = p.Y + d.y_off;
   double s = 0.0;
   if (MODE == kElemContig) {
-    const int64_t n2 = (sg.e1 - sg.e0) / 2;
-    const double2* x2 = reinterpret_cast<const double2*>(x + sg.e0);
-    const double2* y2 = reinterpret_cast<const double2*>(y + sg.e0);
+    const int64_t es = sg.e0 + (sg.e0 & 1);
+    const int64_t n2 = (sg.e1 - es) / 2;
+    const double2* x2 = reinterpret_cast<const double2*>(x + es);
+    const double2* y2 = reinterpret_cast<const double2*>(y + es);
     for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
       const double2 a = x2[i], b = y2[i];
       s += a.x * b.x;
       s += a.y * b.y;
     }
-    if (threadIdx.x == 0 && (sg.e1 - sg.e0) % 2) s += x[sg.e1 - 1] * y[sg.e1 - 1];
+    if (threadIdx.x == 0 && es != sg.e0 && sg.e0 < sg.e1) s += x[sg.e0] * y[sg.e0];
+    if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) s += x[sg.e1 - 1] * y[sg.e1 - 1];
   } else {
     for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) s += x[e] * y[y_offset((uint32_t)e, d)];
   }

@@ -333,3 +333,104 @@ def test_add_zero_input_blocks(env):
         ctx.sync()
         dense["C"] = O.add(dense["C"], "pq", dense["A"], al, 1.0, 2.0, cmask=O.nz_mask(orc["C"]))
         assert normwise(got, O.pack(orc["C"], dense["C"])) <= 1e-15
+
+
+def _split_all(T, nparts):
+    """row parts of every non-zero block of T (all owned by rank 0): exercises the part paths of the
+    kernels (row / column offsets of C groups, element ranges of the element ops) on one GPU."""
+    parts = []
+    for blk in range(T.nblocks):
+        if not T.nz[blk]:
+            continue
+        e0 = int(T.dims[0].offsets[np.unravel_index(blk, T.grid)[0] + 1] - T.dims[0].offsets[np.unravel_index(blk, T.grid)[0]])
+        cuts = sorted(set([0, e0] + [e0 * k // nparts for k in range(1, nparts)]))
+        parts += [(blk, lo, hi, 0) for lo, hi in zip(cuts[:-1], cuts[1:])]
+    T.set_parts(parts)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_row_split_parts_single_rank(env, k):
+    """C owned by row parts (all on rank 0) gives bitwise the same contraction as whole blocks;
+    set / add / scalar / fill on split tensors match the oracle."""
+    tt, torch = env
+    pb = ccsd_problem(24, 80, 12, 20, True)
+    op = pb.ops[k]
+    ctx = new_ctx(tt, torch)
+    g1, ref, _, _ = run_contract(tt, torch, ctx, pb, op, alpha=0.5, beta=1.0, seed=4)
+    ctx2 = new_ctx(tt, torch)
+    C, cl, a, al, b, bl = op
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx2, pb)
+    _split_all(P[C], 3)
+    assert P[C].parts and all(o == tt.TT_SPLIT for x, o in enumerate(P[C].owner) if P[C].nz[x])
+    dense = {}
+    bufs = []
+    for name, tag in ((C, 3), (a, 1), (b, 2)):
+        dense[name] = O.dense_masked(orc[name], S.dense(orc[name].shape, 4, tag))
+        bufs.append(bind_host(torch, P[name], O.pack(orc[name], dense[name])))
+    tt.contract(ctx2, P[C], cl, 1.0, 0.5, P[a], al, P[b], bl)
+    g2 = P[C].download()
+    ctx2.sync()
+    assert np.array_equal(g1, g2)
+    assert normwise(g2, ref) <= TOL
+    # element ops on the split tensor
+    tt.set_(ctx2, P[C], 0.25)
+    got = P[C].download()
+    ctx2.sync()
+    assert np.array_equal(got, O.pack(orc[C], O.set_(np.zeros(orc[C].shape), 0.25, O.nz_mask(orc[C]))))
+    tt.fill_synthetic(ctx2, P[C], 8, 3)
+    got = P[C].download()
+    ctx2.sync()
+    assert np.array_equal(got, O.pack(orc[C], S.dense(orc[C].shape, 8, 3)))
+
+
+def test_row_split_add_scalar_single_rank(env):
+    tt, torch = env
+    pb = ccsd_problem(8, 12, 2, 3, True)
+    pb.tensors["Rt"] = TensorSpec("ijab", ("spin", [0, 1], [2, 3]))
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    _split_all(P["R"], 2)
+    _split_all(P["Ta"], 3)
+    dense = {}
+    bufs = []
+    for name, tag in (("R", 3), ("Rt", 1), ("Ta", 2)):
+        dense[name] = O.dense_masked(orc[name], S.dense(orc[name].shape, 3, tag))
+        bufs.append(bind_host(torch, P[name], O.pack(orc[name], dense[name])))
+    for al in ("ijab", ):
+        tt.add(ctx, P["R"], "abij", -0.5, 2.0, P["Rt"], al)
+        got = P["R"].download()
+        ctx.sync()
+        dense["R"] = O.add(dense["R"], "abij", dense["Rt"], al, 2.0, -0.5, cmask=O.nz_mask(orc["R"]))
+        assert normwise(got, O.pack(orc["R"], dense["R"])) <= 1e-15
+    tt.add(ctx, P["R"], "abij", 1.0, 1.0, P["Ta"], "abij")
+    got = P["R"].download()
+    ctx.sync()
+    dense["R"] = O.add(dense["R"], "abij", dense["Ta"], "abij", 1.0, 1.0, cmask=O.nz_mask(orc["R"]))
+    assert normwise(got, O.pack(orc["R"], dense["R"])) <= 1e-15
+    for bl in ("acik", "abij"):
+        s = tt.contract_scalar(ctx, 0.25, P["Ta"], "acik", P["R"], bl.replace("abij", "acik"))
+        so = O.scalar(dense["Ta"], "acik", dense["R"], "acik", 0.25)
+        assert abs(s - so) <= 1e-13 * max(abs(so), 1.0)
+
+
+@pytest.mark.parametrize("labels", [("jbia", "kcai", "bjck"), ("abij", "iack", "kcjb")])
+def test_row_split_column_side(env, labels):
+    """Row parts of C whose dim-0 label comes from B (the split becomes an n range) or from A."""
+    tt, torch = env
+    cl, al, bl = labels
+    spaces = {"X": SpaceSpec(12, tile=4), "Y": SpaceSpec(10, tile=6), "Z": SpaceSpec(14, tile=8)}
+    ls = {"a": "X", "b": "Y", "c": "Z", "i": "Y", "j": "X", "k": "Z"}
+    pb = Problem(spaces, ls, {"C": TensorSpec(cl), "A": TensorSpec(al), "B": TensorSpec(bl)}, [("C", cl, "A", al, "B", bl)])
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    _split_all(P["C"], 3)
+    dense = {n: O.dense_masked(orc[n], S.dense(orc[n].shape, 6, t)) for n, t in (("C", 3), ("A", 1), ("B", 2))}
+    bufs = [bind_host(torch, P[n], O.pack(orc[n], dense[n])) for n in ("C", "A", "B")]
+    tt.contract(ctx, P["C"], cl, 0.5, 1.0, P["A"], al, P["B"], bl)
+    got = P["C"].download()
+    ctx.sync()
+    ref = O.contract(dense["C"], cl, dense["A"], al, dense["B"], bl, 1.0, 0.5)
+    assert normwise(got, O.pack(orc["C"], ref)) <= TOL

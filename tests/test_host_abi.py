@@ -160,42 +160,130 @@ def test_lpt_partition_matches_oracle(nranks):
         assert all(own[x] == -1 for x in range(prod[C].nblocks) if not prod[C].nz[x])
 
 
-def _expected_gather(orc, pb_op, owners, me, nranks):
+def _ranges_of(T, blk, rank):
+    """element ranges of block blk of product tensor T held by rank (whole / replicated / parts)."""
+    vol = int(np.prod([d.offsets[t + 1] - d.offsets[t] for d, t in zip(T.dims, np.unravel_index(blk, T.grid))]))
+    parts = [p for p in T.parts if p[0] == blk]
+    if not parts:
+        return [(0, vol)] if T.owner[blk] in (rank, tt.TT_REPLICATED) else []
+    inner = vol // (parts[-1][2])
+    return [(lo * inner, hi * inner) for (_, lo, hi, o) in parts if o == rank]
+
+
+def _pieces(T, blk, e0, e1):
+    vol = int(np.prod([d.offsets[t + 1] - d.offsets[t] for d, t in zip(T.dims, np.unravel_index(blk, T.grid))]))
+    parts = [p for p in T.parts if p[0] == blk]
+    if not parts:
+        return [(int(T.owner[blk]), e0, e1)]
+    inner = vol // parts[-1][2]
+    out = []
+    for (_, lo, hi, o) in parts:
+        a, z = max(e0, lo * inner), min(e1, hi * inner)
+        if a < z:
+            out.append((o, a, z))
+    return out
+
+
+def _expected_gather(orc, prod, pb_op, me, nranks):
+    """Needed input ranges per rank from the oracle task list and the product's ownership; the
+    receives / sends of rank `me` (whole blocks, or matching rows when C is row-split along a label
+    that is also the operand's dim 0)."""
     C, cl, a, al, b, bl = pb_op
     ocb, optr, oab, obb, _ = L.task_list(orc[C], cl, orc[a], al, orc[b], bl)
-    need = {r: set() for r in range(nranks)}
+    need = {r: {} for r in range(nranks)}
     for g, cb in enumerate(ocb):
-        r = owners[C][cb]
-        for t in range(optr[g], optr[g + 1]):
-            need[r].add((0, oab[t]))
-            need[r].add((1, obb[t]))
-    recv = sorted((op, blk, owners[[a, b][op]][blk]) for (op, blk) in need[me] if owners[[a, b][op]][blk] != me)
-    send = sorted((op, blk, r) for r in range(nranks) for (op, blk) in need[r]
-                  if r != me and owners[[a, b][op]][blk] == me)
-    return recv, send
+        cvol = orc[C].block_volume(cb)
+        cin = cvol // orc[C].block_extents(cb)[0]
+        for r in range(nranks):
+            for (h0, h1) in _ranges_of(prod[C], cb, r):
+                lo, hi = h0 // cin, h1 // cin
+                for t in range(optr[g], optr[g + 1]):
+                    for op, (name, lbl, blk) in enumerate(((a, al, oab[t]), (b, bl, obb[t]))):
+                        vol = orc[name].block_volume(blk)
+                        if lbl[0] == cl[0]:
+                            inner = vol // orc[name].block_extents(blk)[0]
+                            rng = (lo * inner, hi * inner)
+                        else:
+                            rng = (0, vol)
+                        need[r].setdefault((op, blk), []).append(rng)
+    recv, send = [], []
+    for r in range(nranks):
+        for (op, blk), rngs in need[r].items():
+            rngs.sort()
+            merged = []
+            for x in rngs:
+                if merged and x[0] <= merged[-1][1]:
+                    merged[-1] = (merged[-1][0], max(merged[-1][1], x[1]))
+                else:
+                    merged.append(x)
+            T = prod[[a, b][op]]
+            for (e0, e1) in merged:
+                for (src, x0, x1) in _pieces(T, blk, e0, e1):
+                    if src in (tt.TT_REPLICATED, r):
+                        continue
+                    if r == me:
+                        recv.append((op, blk, src, x0, x1))
+                    if src == me:
+                        send.append((op, blk, r, x0, x1))
+    return sorted(recv), sorted(send)
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
-def test_gather_plan_exactly_needed_blocks(nranks):
-    """Each rank receives exactly the A/B blocks its owned C blocks' tasks read but it does not own,
-    and the sends of every rank mirror the receives of its peers (P212)."""
+@pytest.mark.parametrize("split", [False, True])
+def test_gather_plan_exactly_needed_blocks(nranks, split):
+    """Each rank receives exactly the A/B ranges its owned C blocks (or C row parts) read but it does
+    not hold, and the sends of every rank mirror the receives of its peers (P212)."""
     pb = ccsd_problem(8, 12, 2, 3, True)
     sends, recvs = {}, {}
-    for me in range(nranks):
-        c = tt.Context(device=-1, rank=me, nranks=nranks)
+    for k in (0, 1):              # ladder (C dim 0 shared with A) and ring
+        for me in range(nranks):
+            c = tt.Context(device=-1, rank=me, nranks=nranks)
+            orc = oracle_objects(pb, nranks)
+            prod = product_objects(tt, c, pb)
+            C, cl, a, al, b, bl = pb.ops[k]
+            if split:
+                tt.partition_split(c, prod[C], cl, prod[a], al, prod[b], bl)
+            else:
+                prod[C].set_owner(tt.partition_lpt(c, prod[C], cl, prod[a], al, prod[b], bl))
+            r, s = tt.gather_plan(c, prod[C], cl, prod[a], al, prod[b], bl)
+            er, es = _expected_gather(orc, prod, pb.ops[k], me, nranks)
+            assert sorted(map(tuple, r.tolist())) == er
+            assert sorted(map(tuple, s.tolist())) == es
+            sends[me] = {(op, blk, me, peer, e0, e1) for op, blk, peer, e0, e1 in s.tolist()}
+            recvs[me] = {(op, blk, peer, me, e0, e1) for op, blk, peer, e0, e1 in r.tolist()}
+        assert set().union(*sends.values()) == set().union(*recvs.values())
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+@pytest.mark.parametrize("grouped", [False, True])
+def test_partition_split_matches_oracle(nranks, grouped):
+    """Row-splitting water-filling partition == oracle (R24b); loads balanced to within one row."""
+    c = tt.Context(device=-1, nranks=nranks)
+    for pb in (ccsd_problem(40, 200, 40, 40, False, terms=("ladder",)), ccsd_problem(10, 14, 3, 4, True)):
         orc = oracle_objects(pb, nranks)
         prod = product_objects(tt, c, pb)
-        C, cl, a, al, b, bl = pb.ops[1]        # ring term
-        own = tt.partition_lpt(c, prod[C], cl, prod[a], al, prod[b], bl)
-        prod[C].set_owner(own)
-        owners = {n: list(prod[n].owner) for n in pb.tensors}
-        r, s = tt.gather_plan(c, prod[C], cl, prod[a], al, prod[b], bl)
-        er, es = _expected_gather(orc, pb.ops[1], owners, me, nranks)
-        assert sorted(map(tuple, r.tolist())) == er
-        assert sorted(map(tuple, s.tolist())) == es
-        sends[me] = {(op, blk, me, peer) for op, blk, peer in s.tolist()}
-        recvs[me] = {(op, blk, peer, me) for op, blk, peer in r.tolist()}
-    assert set().union(*sends.values()) == set().union(*recvs.values())
+        C, cl, a, al, b, bl = pb.ops[0]
+        ocb, _, _, _, ocost = L.task_list(orc[C], cl, orc[a], al, orc[b], bl)
+        gd = (0, 1) if grouped else ()
+        exp = L.partition_split(orc[C], ocost, ocb, list(gd), nranks)
+        tt.partition_split(c, prod[C], cl, prod[a], al, prod[b], bl, group_dims=gd)
+        got = {}
+        for x in ocb:
+            if prod[C].owner[x] == tt.TT_SPLIT:
+                got[x] = [(lo, hi, o) for (bb, lo, hi, o) in prod[C].parts if bb == x]
+            else:
+                got[x] = [(0, orc[C].block_extents(x)[0], int(prod[C].owner[x]))]
+        assert got == exp
+        load = [0.0] * nranks
+        maxrow = 0.0
+        for x, cst in zip(ocb, ocost):
+            rows = orc[C].block_extents(x)[0]
+            maxrow = max(maxrow, cst / rows)
+            for lo, hi, o in exp[x]:
+                load[o] += cst * (hi - lo) / rows
+        W = sum(ocost)
+        tol = maxrow * (len(pb.spaces) + 4 if grouped else 1)
+        assert max(load) - W / nranks <= tol + 1e-6
 
 
 @pytest.mark.parametrize("nranks", [2, 4])

@@ -38,8 +38,20 @@ def main():
     single = tt.Context(device=local, stream=stream) if rank == 0 else None
     P1 = product_objects(tt, single, pb) if rank == 0 else None
     c0, cl0, a0, al0, b0, bl0 = pb.ops[0]
-    own = tt.partition_lpt(ctx, P[c0], cl0, P[a0], al0, P[b0], bl0)
-    P["R"].set_owner(own)
+    if os.environ.get("MGPU_SPLIT", "1") == "1":
+        tt.partition_split(ctx, P[c0], cl0, P[a0], al0, P[b0], bl0, group_dims=(0, 1))
+        # scatter some V rows across ranks too (parts of the inputs are gathered by row ranges)
+        vparts = []
+        for blk in range(P["Ta"].nblocks):
+            if P["Ta"].nz[blk] and blk % 3 == 0:
+                e0 = int(np.diff(P["Ta"].dims[0].offsets)[np.unravel_index(blk, P["Ta"].grid)[0]])
+                vparts += [(blk, 0, e0 // 2, blk % world), (blk, e0 // 2, e0, (blk + 1) % world)]
+        P["Ta"].set_parts(vparts)
+    else:
+        own = tt.partition_lpt(ctx, P[c0], cl0, P[a0], al0, P[b0], bl0)
+        P["R"].set_owner(own)
+    print(f"rank {rank}: R parts {len(P['R'].parts)}, split blocks {sum(1 for o in P['R'].owner if o == tt.TT_SPLIT)}",
+          flush=True)
     bufs = {}
     for name, tag in (("R", 3), ("Vv", 4), ("T", 5), ("Ta", 1), ("Wr", 2), ("Tb", 6), ("Wh", 7), ("Rt", 8)):
         bufs[name] = torch.full((P[name].packed_elems,), float("nan"), dtype=torch.float64, device="cuda")
@@ -71,11 +83,15 @@ def main():
         if not P["R"].nz[blk]:
             continue
         o = P["R"].blk_off[blk]
-        n = int(np.prod([d.offsets[t + 1] - d.offsets[t] for d, t in
-                         zip(P["R"].dims, np.unravel_index(blk, P["R"].grid))]))
+        ext = [d.offsets[t + 1] - d.offsets[t] for d, t in zip(P["R"].dims, np.unravel_index(blk, P["R"].grid))]
+        n = int(np.prod(ext))
         live[o:o + n] = True
         if P["R"].owner[blk] == rank:
             mine[o:o + n] = got[o:o + n]
+        inner = n // int(ext[0])
+        for (bb, lo, hi, ow) in P["R"].parts:
+            if bb == blk and ow == rank:
+                mine[o + lo * inner:o + hi * inner] = got[o + lo * inner:o + hi * inner]
     tot = torch.from_numpy(mine).cuda()
     dist.all_reduce(tot)   # each element owned by exactly one rank: the sum assembles the tensor
     assembled = tot.cpu().numpy()
