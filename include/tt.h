@@ -70,6 +70,7 @@ typedef struct {
   int64_t launches;        /* kernels launched by the call                                         */
   int32_t plan_cached;     /* 1 if the task list / partition / gather plan came from the cache     */
   int32_t kernel_variant;  /* contraction kernel tile variant used                  */
+  double aux_flops;        /* FLOPs spent building implicit operands (tt_contract_cholesky)         */
 } tt_stats;
 
 /* ------------------------------------------------------------------------------------------------
@@ -205,6 +206,21 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, d
                       tt_tensor A, const char* a_lbl, tt_tensor B, const char* b_lbl);
 tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* a_lbl, tt_tensor B,
                              const char* b_lbl, double* result);
+
+/* Contraction with an IMPLICIT Cholesky-factored operand (PAPER Eq. cc12,
+ * P312-318, the paper's CD-CCSD P325/P463):
+ *   C(c_lbl) = beta*C + alpha * sum V(v_lbl) * B(b_lbl),
+ *   V(p,q,r,s) = sum_L X(p,r,L) X(q,s,L) - X(p,s,L) X(q,r,L)     (v_lbl = "pqrs"; formula as printed, R19)
+ * V is never stored whole: the rank's C parts are processed in batches of (p,q) tile rows; the V blocks
+ * of a batch are built by the DMMA contraction kernel into `workspace` (caller-owned device memory of
+ * ws_elems doubles, at least one (p,q) row of V) and consumed by the contraction restricted to the
+ * batch.  Ladder form only: p, q free labels of C, r, s contracted with B; X(p,r,L) is order 3 with
+ * dims 0 and 1 on the tiled space of p, q, r, s.  B's missing blocks are gathered once per call; with
+ * nranks > 1 every X block must be TT_REPLICATED.  The V block map: non-zero iff the Coulomb or the
+ * exchange term conserves spin pairwise.  tt_stats.flops = consuming FLOPs, aux_flops = building. */
+tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha,
+                               tt_tensor X, const char* v_lbl, tt_tensor B, const char* b_lbl,
+                               void* workspace, int64_t ws_elems);
 
 /* ------------------------------------------------------------------------------------------------
  * Task list (canonical order, R11): for each non-zero C block in row-major order (all of them, not

@@ -216,3 +216,12 @@ def sampled_elements(c_idx: np.ndarray, c_lbl: str, a_lbl: str, b_lbl: str, ext:
             bv = np.where(b_nz_elem(ib) != 0, bv, 0.0)
         out[r] = dots(av[None, :], bv[None, :])[0]
     return out
+
+
+def cholesky_v(X: np.ndarray) -> np.ndarray:
+    """PAPER Eq. cc12 (P312-318) as printed (reading R19):
+        v(p,q,r,s) = sum_L X(p,r,L) X(q,s,L) - X(p,s,L) X(q,r,L)
+    Two oracle contractions over L (sequential sums)."""
+    n = X.shape[0]
+    V = contract(np.zeros((n, n, n, n)), "pqrs", X, "prL", X, "qsL", 1.0, 0.0)
+    return contract(V, "pqrs", X, "psL", X, "qrL", -1.0, 1.0)

@@ -41,7 +41,8 @@ _P = ctypes.POINTER
 
 class Stats(ctypes.Structure):
     _fields_ = [("c_blocks", _i64), ("tasks", _i64), ("work_items", _i64), ("flops", _dbl), ("bytes", _dbl),
-                ("gathered_bytes", _i64), ("launches", _i64), ("plan_cached", _i32), ("kernel_variant", _i32)]
+                ("gathered_bytes", _i64), ("launches", _i64), ("plan_cached", _i32), ("kernel_variant", _i32),
+                ("aux_flops", _dbl)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -78,6 +79,8 @@ _SIGS = {
     "tt_set": [_vp, _vp, _dbl],
     "tt_add": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p],
     "tt_contract": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p],
+    "tt_contract_cholesky": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
+                             _i64],
     "tt_contract_scalar": [_vp, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _P(_dbl)],
     "tt_task_list": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _i32, _vp, _vp, _vp,
                      _vp, _vp, _i64, _P(_i64), _P(_i64)],
@@ -335,6 +338,16 @@ def contract(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: 
              b_lbl: str):
     """P174 rule 7: C(c_lbl) = beta*C + alpha*A(a_lbl)*B(b_lbl)."""
     _check(_lib.tt_contract(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), A.h, _b(a_lbl), B.h, _b(b_lbl)))
+
+
+def contract_cholesky(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, X: Tensor, v_lbl: str,
+                      B: Tensor, b_lbl: str, workspace, ws_elems: Optional[int] = None):
+    """C = beta*C + alpha * V(v_lbl) * B(b_lbl), V(p,q,r,s) = sum_L X(p,r,L)X(q,s,L) - X(p,s,L)X(q,r,L)
+    built batch by batch in ``workspace`` (Eq. cc12; tt_contract_cholesky)."""
+    if ws_elems is None:
+        ws_elems = int(workspace.numel())
+    _check(_lib.tt_contract_cholesky(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), X.h, _b(v_lbl), B.h,
+                                     _b(b_lbl), _vp(_devptr(workspace)), int(ws_elems)))
 
 
 def contract_scalar(ctx: Context, alpha: float, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str) -> float:

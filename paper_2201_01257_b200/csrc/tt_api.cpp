@@ -446,6 +446,19 @@ tt_status check_bound(tt_tensor t, const char* which) {
 // ---------------------------------------------------------------------------------------------
 // contraction plan (cached per (tensors, owner versions, labels))
 
+// Internal contraction options (used by the implicit-operand driver): `local` plans compute exactly
+// the listed C parts of this rank and never gather (the operands are local / replicated);
+// `no_a_needs` plans gather only B (A is a metadata-only implicit operand).
+struct PartSel {
+  int64_t blk, lo, hi;
+};
+struct ContractOpts {
+  bool local = false;
+  bool no_a_needs = false;
+  std::vector<PartSel> sel;
+  std::string tag;
+};
+
 struct ContractPlan {
   Analysis an;
   HostTasks ht;
@@ -1330,7 +1343,8 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
 
 namespace {
 
-tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B, double beta, ContractPlan& pl) {
+tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B, double beta, ContractPlan& pl,
+                              const ContractOpts& opts = ContractOpts()) {
   const Analysis& an = pl.an;
   enumerate_tasks(an, C, A, B, pl.ht);
   const HostTasks& ht = pl.ht;
@@ -1342,26 +1356,38 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
   const bool a_same0 = an.a_lab[0] == 0, b_same0 = an.b_lab[0] == 0;
   const int bop = (A == B) ? 0 : 1;   // A and B may be the same tensor (same storage)
   std::vector<std::pair<int64_t, int64_t>> hr;
-  for (size_t g = 0; g < ht.cblk.size(); ++g) {
-    const int64_t cb = ht.cblk[g];
-    const int64_t cin = C->block_volume(cb) / C->ext0(cb);
-    for (int r = 0; r < ctx->nranks; ++r) {
-      C->held_ranges(cb, r, hr);
-      for (auto& h : hr) {
-        const int64_t lo = h.first / cin, hi = h.second / cin;
-        if (r == ctx->rank) pl.my.push_back({(int)g, lo, hi});
-        for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
-          int64_t e0, e1;
-          sub_range_inner(A, ht.a_blk[t], a_same0, lo, hi, &e0, &e1);
-          need[r].push_back({0, ht.a_blk[t], e0, e1});
-          sub_range_inner(B, ht.b_blk[t], b_same0, lo, hi, &e0, &e1);
-          need[r].push_back({bop, ht.b_blk[t], e0, e1});
+  if (opts.local) {
+    std::map<int64_t, int> g_of;
+    for (size_t g = 0; g < ht.cblk.size(); ++g) g_of[ht.cblk[g]] = (int)g;
+    for (const PartSel& ps : opts.sel) {
+      auto it = g_of.find(ps.blk);
+      if (it == g_of.end()) return fail(TT_E_ARG, "selected C block %lld is not a non-zero block", (long long)ps.blk);
+      pl.my.push_back({it->second, ps.lo, ps.hi});
+    }
+  } else {
+    for (size_t g = 0; g < ht.cblk.size(); ++g) {
+      const int64_t cb = ht.cblk[g];
+      const int64_t cin = C->block_volume(cb) / C->ext0(cb);
+      for (int r = 0; r < ctx->nranks; ++r) {
+        C->held_ranges(cb, r, hr);
+        for (auto& h : hr) {
+          const int64_t lo = h.first / cin, hi = h.second / cin;
+          if (r == ctx->rank) pl.my.push_back({(int)g, lo, hi});
+          for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
+            int64_t e0, e1;
+            if (!opts.no_a_needs) {
+              sub_range_inner(A, ht.a_blk[t], a_same0, lo, hi, &e0, &e1);
+              need[r].push_back({0, ht.a_blk[t], e0, e1});
+            }
+            sub_range_inner(B, ht.b_blk[t], b_same0, lo, hi, &e0, &e1);
+            need[r].push_back({bop, ht.b_blk[t], e0, e1});
+          }
         }
       }
     }
+    if (A == B) build_gather(ctx, need, {A}, pl.gp);
+    else build_gather(ctx, need, {A, B}, pl.gp);
   }
-  if (A == B) build_gather(ctx, need, {A}, pl.gp);
-  else build_gather(ctx, need, {A, B}, pl.gp);
   // stats for this rank
   {
     std::vector<char> ua(A->nblocks, 0), ub(B->nblocks, 0);
@@ -1568,20 +1594,46 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
 }
 
 tt_status get_contract_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
-                            const char* bl, double beta, std::shared_ptr<ContractPlan>& out, bool* cached_flag) {
+                            const char* bl, double beta, std::shared_ptr<ContractPlan>& out, bool* cached_flag,
+                            const ContractOpts& opts = ContractOpts()) {
   Analysis an;
   TT_TRY(analyse(C, cl, A, al, B, bl, an));
   if (C == A || C == B) return fail(TT_E_ARG, "C must not alias A or B");
-  std::string key = plan_key("contract", C, cl, A, al, B, bl, beta);
+  std::string key = plan_key("contract", C, cl, A, al, B, bl, beta) + opts.tag;
   out = cached<ContractPlan>(ctx, key);
   if (cached_flag) *cached_flag = out != nullptr;
   if (out) return TT_OK;
   auto pl = std::make_shared<ContractPlan>();
   pl->an = an;
   DeviceGuard dg(ctx->device);
-  TT_TRY(build_contract_plan(ctx, C, A, B, beta, *pl));
+  TT_TRY(build_contract_plan(ctx, C, A, B, beta, *pl, opts));
   ctx->plans[key] = pl;
   out = pl;
+  return TT_OK;
+}
+
+// the DMMA contraction kernel of a plan (no gather)
+tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const char* cl, double beta, double alpha,
+                      tt_tensor A, const char* al, tt_tensor B, const char* bl) {
+  ContractParams p{};
+  p.A = A->data;
+  p.B = B->data;
+  p.C = C->data;
+  p.groups = pl.d_groups;
+  p.tasks = pl.d_tasks;
+  p.work = pl.d_work;
+  p.nM = (int32_t)pl.an.mg.size();
+  p.nN = (int32_t)pl.an.ng.size();
+  p.nK = (int32_t)pl.an.kg.size();
+  p.alpha = alpha;
+  p.beta = beta;
+  const std::string nm = std::string("tt_contract_dmma[") + cl + "=" + al + "*" + bl + "]";
+  Launch L(ctx, nm.c_str());
+  if (pl.variant < num_contract_variants())
+    TT_CUDA(launch_contract(pl.variant, pl.an.a_kc, pl.an.b_nc, p, pl.nwork, ctx->stream));
+  else
+    TT_CUDA(launch_contract_ws(pl.variant - num_contract_variants(), pl.an.a_kc, pl.an.b_nc, pl.a_vec, pl.b_vec, p,
+                               pl.nwork, ctx->stream));
   return TT_OK;
 }
 
@@ -1602,27 +1654,7 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   DeviceGuard dg(ctx->device);
   reset_stats(ctx);
   TT_TRY(run_gather(ctx, pl->gp, A == B ? std::vector<tt_tensor>{A} : std::vector<tt_tensor>{A, B}));
-  ContractParams p{};
-  p.A = A->data;
-  p.B = B->data;
-  p.C = C->data;
-  p.groups = pl->d_groups;
-  p.tasks = pl->d_tasks;
-  p.work = pl->d_work;
-  p.nM = (int32_t)pl->an.mg.size();
-  p.nN = (int32_t)pl->an.ng.size();
-  p.nK = (int32_t)pl->an.kg.size();
-  p.alpha = alpha;
-  p.beta = beta;
-  {
-    const std::string nm = std::string("tt_contract_dmma[") + cl + "=" + al + "*" + bl + "]";
-    Launch L(ctx, nm.c_str());
-    if (pl->variant < num_contract_variants())
-      TT_CUDA(launch_contract(pl->variant, pl->an.a_kc, pl->an.b_nc, p, pl->nwork, ctx->stream));
-    else
-      TT_CUDA(launch_contract_ws(pl->variant - num_contract_variants(), pl->an.a_kc, pl->an.b_nc, pl->a_vec,
-                                 pl->b_vec, p, pl->nwork, ctx->stream));
-  }
+  TT_TRY(launch_plan(ctx, *pl, C, cl, beta, alpha, A, al, B, bl));
   ctx->last.c_blocks = (int64_t)pl->my.size();
   ctx->last.tasks = pl->tasks;
   ctx->last.work_items = pl->nwork;
@@ -1813,6 +1845,229 @@ tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, c
   if (cap < std::max(*n_recv, *n_send)) return fail(TT_E_ARG, "capacity too small");
   if (recv) std::copy(pl.gp.recv_list.begin(), pl.gp.recv_list.end(), recv);
   if (send) std::copy(pl.gp.send_list.begin(), pl.gp.send_list.end(), send);
+  return TT_OK;
+}
+
+}  // extern "C"
+
+// =============================================================================================
+// Implicit Cholesky-factored operand (PAPER Eq. cc12, P312-318)
+//
+//   C(c) = beta*C + alpha * sum_{r,s} V(p,q,r,s) * B(..r..s..)   with V never stored:
+//   V(p,q,r,s) = sum_L X(p,r,L) X(q,s,L) - X(p,s,L) X(q,r,L)         (Eq. cc12 as printed, R19)
+//
+// The rank's C parts are processed in batches of (p,q) tile rows.  For each batch the V blocks of
+// those rows are BUILT by the same DMMA contraction kernel (two contractions over L with output
+// permutation, into a caller-provided workspace) and immediately CONSUMED by the ladder contraction
+// restricted to the batch's C parts.  B is gathered once per call (SPMD); X must be replicated.
+
+namespace {
+
+struct CholBatch {
+  tt_tensor Vb = nullptr;            // scratch V blocks of the batch (bound to the workspace)
+  ContractOpts vopt, copt;           // local build / consume selections
+};
+
+struct CholPlan {
+  tt_tensor Vmeta = nullptr;         // metadata-only implicit operand (block map of V)
+  std::shared_ptr<ContractPlan> gplan;
+  std::vector<CholBatch> batches;
+  std::string lc;                    // the auxiliary label used for L
+  ~CholPlan() {
+    delete Vmeta;
+    for (auto& b : batches) delete b.Vb;
+  }
+};
+
+tt_status new_meta_tensor(tt_ctx ctx, const std::vector<tt_tis>& dims, const std::vector<uint8_t>& nz, tt_tensor* out) {
+  tt_tensor t;
+  TT_TRY(tensor_new(ctx, (int32_t)dims.size(), dims.data(), &t));
+  t->nz = nz;
+  tensor_finish(t);
+  *out = t;
+  return TT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor X,
+                               const char* vl, tt_tensor B, const char* bl, void* workspace, int64_t ws_elems) {
+  if (!ctx || !C || !X || !B || !vl) return fail(TT_E_ARG, "NULL argument");
+  TT_TRY(check_labels(cl, C, "C"));
+  TT_TRY(check_labels(bl, B, "B"));
+  const std::string c(cl), v(vl), b(bl);
+  if (v.size() != 4) return fail(TT_E_LABEL, "the implicit operand V(p,q,r,s) needs 4 labels");
+  for (int i = 0; i < 4; ++i)
+    for (int j = i + 1; j < 4; ++j)
+      if (v[i] == v[j]) return fail(TT_E_LABEL, "repeated label in V");
+  if (X->order != 3) return fail(TT_E_ARG, "X must be order 3: X(p, r, L)");
+  const char p = v[0], q = v[1], r = v[2], s = v[3];
+  if (c.find(p) == std::string::npos || c.find(q) == std::string::npos)
+    return fail(TT_E_UNSUPPORTED, "V's first two labels must be free labels of C (ladder form)");
+  if (b.find(r) == std::string::npos || b.find(s) == std::string::npos || c.find(r) != std::string::npos ||
+      c.find(s) != std::string::npos)
+    return fail(TT_E_UNSUPPORTED, "V's last two labels must be contracted with B (ladder form)");
+  tt_tis tp = C->dims[c.find(p)], tq = C->dims[c.find(q)], tr = B->dims[b.find(r)], ts = B->dims[b.find(s)];
+  for (tt_tis t : {tp, tq, tr, ts})
+    if (!same_tiling(t, X->dims[0]) || !same_tiling(t, X->dims[1]))
+      return fail(TT_E_TILING, "V's labels and X's first two dims must share one tiled space (Eq. cc12)");
+  if (ctx->nranks > 1)
+    for (int64_t x = 0; x < X->nblocks; ++x)
+      if (X->nz[x] && X->owner[x] != TT_REPLICATED)
+        return fail(TT_E_UNSUPPORTED, "with nranks > 1 the Cholesky vectors X must be replicated");
+  std::string lc;
+  for (char ch : std::string("LMNOPQRSTUVWXYZ0123456789"))
+    if (c.find(ch) == std::string::npos && v.find(ch) == std::string::npos && b.find(ch) == std::string::npos) {
+      lc = std::string(1, ch);
+      break;
+    }
+  TT_TRY(need_device(ctx));
+  TT_TRY(check_bound(C, "C"));
+  TT_TRY(check_bound(X, "X"));
+  TT_TRY(check_bound(B, "B"));
+  if (!workspace || ws_elems <= 0) return fail(TT_E_UNBOUND, "a device workspace is required");
+  DeviceGuard dg(ctx->device);
+
+  char keybuf[256];
+  snprintf(keybuf, sizeof(keybuf), "chol|%llu.%llu|%llu.%llu|%llu.%llu|%s|%s|%s|%d|%p|%lld",
+           (unsigned long long)C->uid, (unsigned long long)C->version, (unsigned long long)X->uid,
+           (unsigned long long)X->version, (unsigned long long)B->uid, (unsigned long long)B->version, cl, vl, bl,
+           beta != 0.0, workspace, (long long)ws_elems);
+  auto cp = cached<CholPlan>(ctx, keybuf);
+  if (!cp) {
+    cp = std::make_shared<CholPlan>();
+    cp->lc = lc;
+    // block map of V: reachable by the Coulomb or the exchange term (spin conserved pairwise)
+    std::vector<tt_tis> vd = {tp, tq, tr, ts};
+    int64_t nvb = 1;
+    for (auto t : vd) nvb *= t->ntiles();
+    std::vector<uint8_t> vnz(nvb);
+    for (int64_t x = 0; x < nvb; ++x) {
+      int64_t y = x;
+      int32_t co[4];
+      for (int d = 3; d >= 0; --d) { co[d] = (int32_t)(y % vd[d]->ntiles()); y /= vd[d]->ntiles(); }
+      const int sp = tp->spin[co[0]], sq = tq->spin[co[1]], sr = tr->spin[co[2]], ss = ts->spin[co[3]];
+      vnz[x] = ((sp == sr && sq == ss) || (sp == ss && sq == sr)) ? 1 : 0;
+    }
+    TT_TRY(new_meta_tensor(ctx, vd, vnz, &cp->Vmeta));
+    ContractOpts g;
+    g.no_a_needs = true;
+    g.tag = "|cholmeta";
+    bool dummy;
+    TT_TRY(get_contract_plan(ctx, C, cl, cp->Vmeta, vl, B, bl, beta, cp->gplan, &dummy, g));
+    const ContractPlan& gp = *cp->gplan;
+    // units: my C parts grouped by the (p,q) tile coordinates; V rows restricted when C's dim 0 is p
+    const bool rows_on_p = c[0] == p;
+    const int cp_pos = (int)c.find(p), cq_pos = (int)c.find(q);
+    struct Unit {
+      int32_t tp, tq;
+      std::vector<std::pair<int64_t, int64_t>> vrows;
+      std::vector<PartSel> cparts;
+    };
+    std::map<std::pair<int32_t, int32_t>, Unit> units;
+    int32_t cc[TT_MAX_ORDER];
+    for (const auto& mp : gp.my) {
+      const int64_t cb = gp.ht.cblk[mp.g];
+      C->block_coords(cb, cc);
+      Unit& u = units[{cc[cp_pos], cc[cq_pos]}];
+      u.tp = cc[cp_pos];
+      u.tq = cc[cq_pos];
+      u.cparts.push_back({cb, mp.lo, mp.hi});
+      if (rows_on_p) u.vrows.push_back({mp.lo, mp.hi});
+      else u.vrows.push_back({0, tp->size(u.tp)});
+    }
+    // batches: consecutive units while the V blocks of the batch fit the workspace
+    auto flush = [&](std::vector<const Unit*>& cur) -> tt_status {
+      if (cur.empty()) return TT_OK;
+      CholBatch bt;
+      std::vector<uint8_t> bnz(nvb, 0);
+      std::vector<std::pair<int64_t, std::pair<int64_t, int64_t>>> vparts;
+      for (const Unit* u : cur) {
+        // merged row ranges of this unit
+        auto rows = u->vrows;
+        std::sort(rows.begin(), rows.end());
+        std::vector<std::pair<int64_t, int64_t>> mr;
+        for (auto& x : rows) {
+          if (!mr.empty() && x.first <= mr.back().second) mr.back().second = std::max(mr.back().second, x.second);
+          else mr.push_back(x);
+        }
+        for (int32_t a2 = 0; a2 < tr->ntiles(); ++a2)
+          for (int32_t b2 = 0; b2 < ts->ntiles(); ++b2) {
+            const int64_t vb = (((int64_t)u->tp * tq->ntiles() + u->tq) * tr->ntiles() + a2) * ts->ntiles() + b2;
+            if (!vnz[vb]) continue;
+            bnz[vb] = 1;
+            for (auto& x : mr) vparts.push_back({vb, x});
+          }
+        for (const PartSel& ps : u->cparts) bt.copt.sel.push_back(ps);
+      }
+      TT_TRY(new_meta_tensor(ctx, vd, bnz, &bt.Vb));
+      if (bt.Vb->packed_elems > ws_elems) {
+        delete bt.Vb;
+        return fail(TT_E_OOM, "workspace of %lld doubles cannot hold one (p,q) row of V (%lld doubles)",
+                    (long long)ws_elems, (long long)bt.Vb->packed_elems);
+      }
+      bt.Vb->data = (double*)workspace;
+      bt.Vb->capacity = ws_elems;
+      for (auto& vp : vparts) bt.vopt.sel.push_back({vp.first, vp.second.first, vp.second.second});
+      bt.vopt.local = bt.copt.local = true;
+      const size_t bi = cp->batches.size();
+      bt.vopt.tag = "|cholV" + std::to_string(bi);
+      bt.copt.tag = "|cholC" + std::to_string(bi);
+      cp->batches.push_back(bt);
+      cur.clear();
+      return TT_OK;
+    };
+    std::vector<const Unit*> cur;
+    int64_t cur_elems = 0;
+    for (auto& kv : units) {
+      const Unit& u = kv.second;
+      int64_t uel = 0;
+      for (int32_t a2 = 0; a2 < tr->ntiles(); ++a2)
+        for (int32_t b2 = 0; b2 < ts->ntiles(); ++b2) {
+          const int64_t vb = (((int64_t)u.tp * tq->ntiles() + u.tq) * tr->ntiles() + a2) * ts->ntiles() + b2;
+          if (vnz[vb]) uel += (cp->Vmeta->block_volume(vb) + 1) / 2 * 2;
+        }
+      if (!cur.empty() && cur_elems + uel > ws_elems) {
+        TT_TRY(flush(cur));
+        cur_elems = 0;
+      }
+      cur.push_back(&u);
+      cur_elems += uel;
+    }
+    TT_TRY(flush(cur));
+    ctx->plans[keybuf] = cp;
+  }
+  reset_stats(ctx);
+  const ContractPlan& gp = *cp->gplan;
+  TT_TRY(run_gather(ctx, gp.gp, {cp->Vmeta, B}));
+  const std::string L = cp->lc;
+  const std::string xc1 = std::string(1, p) + r + L, xc2 = std::string(1, q) + s + L;   // Coulomb
+  const std::string xe1 = std::string(1, p) + s + L, xe2 = std::string(1, q) + r + L;   // exchange
+  double flops = 0, aux = 0;
+  int64_t tasks = 0;
+  for (auto& bt : cp->batches) {
+    std::shared_ptr<ContractPlan> pc, pe, pu;
+    bool dummy;
+    TT_TRY(get_contract_plan(ctx, bt.Vb, vl, X, xc1.c_str(), X, xc2.c_str(), 0.0, pc, &dummy, bt.vopt));
+    ContractOpts eo = bt.vopt;
+    eo.tag += "x";
+    TT_TRY(get_contract_plan(ctx, bt.Vb, vl, X, xe1.c_str(), X, xe2.c_str(), 1.0, pe, &dummy, eo));
+    TT_TRY(get_contract_plan(ctx, C, cl, bt.Vb, vl, B, bl, beta, pu, &dummy, bt.copt));
+    TT_TRY(launch_plan(ctx, *pc, bt.Vb, vl, 0.0, 1.0, X, xc1.c_str(), X, xc2.c_str()));
+    TT_TRY(launch_plan(ctx, *pe, bt.Vb, vl, 1.0, -1.0, X, xe1.c_str(), X, xe2.c_str()));
+    TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Vb, vl, B, bl));
+    aux += pc->flops + pe->flops;
+    flops += pu->flops;
+    tasks += pu->tasks;
+  }
+  ctx->last.c_blocks = (int64_t)gp.my.size();
+  ctx->last.tasks = tasks;
+  ctx->last.flops = flops;
+  ctx->last.aux_flops = aux;
+  ctx->last.gathered_bytes = gp.gp.recv_bytes;
+  ctx->last.work_items = (int64_t)cp->batches.size();
   return TT_OK;
 }
 

@@ -434,3 +434,39 @@ def test_row_split_column_side(env, labels):
     ctx.sync()
     ref = O.contract(dense["C"], cl, dense["A"], al, dense["B"], bl, 1.0, 0.5)
     assert normwise(got, O.pack(orc["C"], ref)) <= TOL
+
+
+def _cholesky_problem(O_, V_, tO, tV, NL, tL, spin):
+    pb = ccsd_problem(O_, V_, tO, tV, spin, terms=("ladder",))
+    pb.spaces["L"] = SpaceSpec(NL, tile=tL)
+    pb.label_space["L"] = "L"
+    pb.tensors["X"] = TensorSpec("acL", ("spin", [0], [1]) if spin else None)
+    del pb.tensors["Vv"]
+    return pb
+
+
+@pytest.mark.parametrize("spin,ws_rows", [(True, 1), (True, 100), (False, 2)])
+def test_contract_cholesky(env, spin, ws_rows):
+    """Implicit Eq. cc12 operand (NEXT-1): R(abij) = beta*R + alpha*sum V(abcd) T(cdij) with V built
+    batch by batch from X in a small workspace == oracle with V formed explicitly."""
+    tt, torch = env
+    pb = _cholesky_problem(8, 12, 2, 3, 10, 5, spin) if spin else _cholesky_problem(5, 9, 3, 4, 7, 4, False)
+    ctx = new_ctx(tt, torch)
+    orc = oracle_objects(pb)
+    P = product_objects(tt, ctx, pb)
+    dense, bufs = {}, []
+    for name, tag in (("R", 3), ("T", 5), ("X", 7)):
+        dense[name] = O.dense_masked(orc[name], S.dense(orc[name].shape, 2, tag))
+        bufs.append(bind_host(torch, P[name], O.pack(orc[name], dense[name])))
+    tv = max(np.diff(P["X"].dims[0].offsets))
+    ws = torch.empty(int(ws_rows * tv ** 4 * P["X"].dims[0].ntiles ** 2 + 64), dtype=torch.float64, device="cuda")
+    for beta in (1.0, 0.0):
+        tt.contract_cholesky(ctx, P["R"], "abij", beta, 0.5, P["X"], "abcd", P["T"], "cdij", ws)
+        got = P["R"].download()
+        ctx.sync()
+        st = ctx.stats()
+        assert st["aux_flops"] > 0 and st["flops"] > 0
+        Vx = O.cholesky_v(dense["X"])
+        ref = O.contract(dense["R"], "abij", Vx, "abcd", dense["T"], "cdij", 0.5, beta, cmask=O.nz_mask(orc["R"]))
+        assert normwise(got, O.pack(orc["R"], ref)) <= TOL
+        dense["R"] = ref

@@ -403,3 +403,23 @@ def test_sampled_elements_match_full():
                              lambda ix: S.values(4, 1, S.linear_index(sh(a), ix)),
                              lambda ix: S.values(4, 2, S.linear_index(sh(b), ix)))
     assert np.array_equal(got, full[tuple(idx.T)])
+
+
+def test_cholesky_v_pins():
+    """Eq. cc12 oracle: brute force on a tiny case, antisymmetry (p<->q, r<->s), closed forms:
+    separable rank-1 X gives V = 0; X(p,r,L) = delta_pr delta_L0 gives V = d_pr d_qs - d_ps d_qr."""
+    n, nl = 4, 3
+    X = rnd((n, n, nl), 5, 7)
+    V = O.cholesky_v(X)
+    for p, q, r, s in [(0, 1, 2, 3), (3, 3, 1, 0), (2, 0, 2, 1)]:
+        bf = sum(X[p, r, l] * X[q, s, l] - X[p, s, l] * X[q, r, l] for l in range(nl))
+        assert abs(V[p, q, r, s] - bf) < 1e-15
+    assert np.abs(V + V.transpose(1, 0, 2, 3)).max() < 1e-15
+    assert np.abs(V + V.transpose(0, 1, 3, 2)).max() < 1e-15
+    x, y, z = rnd((n,), 1, 7), rnd((n,), 2, 7), rnd((nl,), 3, 7)
+    X1 = np.einsum("p,r,l->prl", x, y, z)
+    assert np.abs(O.cholesky_v(X1)).max() < 1e-15
+    Xd = np.zeros((n, n, nl))
+    Xd[np.arange(n), np.arange(n), 0] = 1.0
+    I = np.eye(n)
+    assert np.array_equal(O.cholesky_v(Xd), np.einsum("pr,qs->pqrs", I, I) - np.einsum("ps,qr->pqrs", I, I))
