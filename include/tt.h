@@ -211,13 +211,16 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
  * P312-318, the paper's CD-CCSD P325/P463):
  *   C(c_lbl) = beta*C + alpha * sum V(v_lbl) * B(b_lbl),
  *   V(p,q,r,s) = sum_L X(p,r,L) X(q,s,L) - X(p,s,L) X(q,r,L)     (v_lbl = "pqrs"; formula as printed, R19)
- * V is never stored whole: the rank's C parts are processed in batches of (p,q) tile rows; the V blocks
- * of a batch are built by the DMMA contraction kernel into `workspace` (caller-owned device memory of
- * ws_elems doubles, at least one (p,q) row of V) and consumed by the contraction restricted to the
- * batch.  Ladder form only: p, q free labels of C, r, s contracted with B; X(p,r,L) is order 3 with
- * dims 0 and 1 on the tiled space of p, q, r, s.  B's missing blocks are gathered once per call; with
- * nranks > 1 every X block must be TT_REPLICATED.  The V block map: non-zero iff the Coulomb or the
- * exchange term conserves spin pairwise.  tt_stats.flops = consuming FLOPs, aux_flops = building. */
+ * V is never stored.  Since the exchange term is the Coulomb term W(p,q,r,s) = sum_L X(p,r,L)X(q,s,L)
+ * with r,s swapped, the call evaluates the identical sum W * (B - B(r<->s)): Bm = B - B(r<->s) is formed
+ * once in the workspace, then the rank's C parts are processed in batches of (p,q) tile rows whose W
+ * blocks are built by the DMMA contraction kernel (over L) into the rest of the workspace and consumed
+ * by the contraction restricted to the batch.  workspace: caller-owned device memory of ws_elems
+ * doubles >= B's packed size (rounded up to 32) + one (p,q) row of W.  Ladder form only: p, q free
+ * labels of C, r, s contracted with B; X(p,r,L) order 3 with dims 0 and 1 on the tiled space of p,q,r,s.
+ * B is all-gathered once per call; with nranks > 1 every X block must be TT_REPLICATED.
+ * tt_stats.flops = algorithmic FLOPs of the defined contraction over V's block map (non-zero iff the
+ * Coulomb or the exchange term conserves spin pairwise); aux_flops = FLOPs executed (W build + consume). */
 tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha,
                                tt_tensor X, const char* v_lbl, tt_tensor B, const char* b_lbl,
                                void* workspace, int64_t ws_elems);

@@ -1854,28 +1854,36 @@ tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, c
 // Implicit Cholesky-factored operand (PAPER Eq. cc12, P312-318)
 //
 //   C(c) = beta*C + alpha * sum_{r,s} V(p,q,r,s) * B(..r..s..)   with V never stored:
-//   V(p,q,r,s) = sum_L X(p,r,L) X(q,s,L) - X(p,s,L) X(q,r,L)         (Eq. cc12 as printed, R19)
+//   V(p,q,r,s) = W(p,q,r,s) - W(p,q,s,r),   W(p,q,r,s) = sum_L X(p,r,L) X(q,s,L)   (Eq. cc12, R19)
 //
-// The rank's C parts are processed in batches of (p,q) tile rows.  For each batch the V blocks of
-// those rows are BUILT by the same DMMA contraction kernel (two contractions over L with output
-// permutation, into a caller-provided workspace) and immediately CONSUMED by the ladder contraction
-// restricted to the batch's C parts.  B is gathered once per call (SPMD); X must be replicated.
+// Because the exchange term of Eq. cc12 is the Coulomb term W with r and s swapped, re-indexing the
+// second sum gives exactly
+//   sum_{r,s} V(p,q,r,s) B(..r..s..) = sum_{r,s} W(p,q,r,s) Bm(..r..s..),  Bm = B - B(r<->s)
+// so only the Coulomb blocks W are built (one DMMA contraction over L per block) and consumed
+// against Bm (one HBM-bound pass per call).  The rank's C parts are processed in batches of (p,q)
+// tile rows: W of the batch is built into the workspace and immediately consumed by the ladder
+// contraction restricted to the batch.  B is all-gathered once per call (SPMD); X must be replicated.
 
 namespace {
 
 struct CholBatch {
-  tt_tensor Vb = nullptr;            // scratch V blocks of the batch (bound to the workspace)
-  ContractOpts vopt, copt;           // local build / consume selections
+  tt_tensor Wb = nullptr;            // scratch W blocks of the batch (bound to the workspace)
+  ContractOpts wopt, copt;           // local build / consume selections
 };
 
 struct CholPlan {
-  tt_tensor Vmeta = nullptr;         // metadata-only implicit operand (block map of V)
-  std::shared_ptr<ContractPlan> gplan;
+  tt_tensor Vmeta = nullptr, Wmeta = nullptr;   // block maps of V (algorithmic count) and W
+  tt_tensor Bm = nullptr;                       // B - B(r<->s), in the workspace
+  std::shared_ptr<ContractPlan> vplan, wplan;   // SPMD plans: this rank's C parts, FLOP counts
+  std::shared_ptr<ElemPlan> copy_plan, swap_plan;
+  GatherPlan bgather;                           // all-gather of B
   std::vector<CholBatch> batches;
-  std::string lc;                    // the auxiliary label used for L
+  std::string lc;                               // the auxiliary label used for L
   ~CholPlan() {
     delete Vmeta;
-    for (auto& b : batches) delete b.Vb;
+    delete Wmeta;
+    delete Bm;
+    for (auto& b : batches) delete b.Wb;
   }
 };
 
@@ -1885,6 +1893,52 @@ tt_status new_meta_tensor(tt_ctx ctx, const std::vector<tt_tis>& dims, const std
   t->nz = nz;
   tensor_finish(t);
   *out = t;
+  return TT_OK;
+}
+
+// local element add X(all blocks) = beta*X + alpha*Y(perm) with no gather (Y fully present)
+tt_status local_add_plan(tt_ctx ctx, tt_tensor Xt, tt_tensor Yt, const std::vector<int>& perm, double beta,
+                         std::shared_ptr<ElemPlan>& out) {
+  auto ep = std::make_shared<ElemPlan>();
+  int32_t cc[TT_MAX_ORDER], ac[TT_MAX_ORDER];
+  for (int64_t b = 0; b < Xt->nblocks; ++b) {
+    if (!Xt->nz[b]) continue;
+    Xt->block_coords(b, cc);
+    for (int d = 0; d < Xt->order; ++d) ac[perm[d]] = cc[d];
+    const int64_t ab = Yt->block_id(ac);
+    ElemDesc d{};
+    d.x_off = Xt->blk_off[b];
+    d.y_off = Yt->nz[ab] ? Yt->blk_off[ab] : -1;
+    int64_t sa[TT_MAX_ORDER], acc = 1;
+    for (int q = Yt->order - 1; q >= 0; --q) { sa[q] = acc; acc *= Yt->dims[q]->size(ac[q]); }
+    int32_t ext[TT_MAX_ORDER];
+    for (int q = 0; q < Xt->order; ++q) ext[q] = (int32_t)Xt->dims[q]->size(cc[q]);
+    ep->mode = fuse_elem(d, Xt->order, ext, perm.data(), sa);
+    ep->descs.push_back(d);
+    if (ep->mode == kElemTranspose) add_tiles(*ep, (int32_t)ep->descs.size() - 1);
+    else add_segments(*ep, (int32_t)ep->descs.size() - 1, 0, Xt->block_volume(b));
+    ep->bytes += 8.0 * Xt->block_volume(b) * ((beta != 0.0) + 2);
+    ep->blocks++;
+  }
+  if (ep->mode != kElemTranspose) ep->tiles.clear();
+  TT_TRY(upload_elem(ctx, *ep, false));
+  out = ep;
+  return TT_OK;
+}
+
+tt_status run_local_add(tt_ctx ctx, const ElemPlan& ep, tt_tensor Xt, tt_tensor Yt, double beta, double alpha) {
+  ElemParams p{};
+  p.X = Xt->data;
+  p.Y = Yt->data;
+  p.descs = ep.d_descs;
+  p.segs = ep.d_segs;
+  p.tiles = ep.d_tiles;
+  p.mode = ep.mode;
+  p.order = Xt->order;
+  p.alpha = alpha;
+  p.beta = beta;
+  Launch L(ctx, "tt_add[cholesky Bm]");
+  TT_CUDA(launch_add(p, ep.nwork(), ctx->stream));
   return TT_OK;
 }
 
@@ -1927,7 +1981,10 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   TT_TRY(check_bound(C, "C"));
   TT_TRY(check_bound(X, "X"));
   TT_TRY(check_bound(B, "B"));
-  if (!workspace || ws_elems <= 0) return fail(TT_E_UNBOUND, "a device workspace is required");
+  const int64_t bm_elems = (B->packed_elems + 31) / 32 * 32;
+  if (!workspace || ws_elems <= bm_elems)
+    return fail(TT_E_UNBOUND, "workspace must hold B's packed size (%lld doubles) plus one (p,q) row of W",
+                (long long)B->packed_elems);
   DeviceGuard dg(ctx->device);
 
   char keybuf[256];
@@ -1939,31 +1996,57 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   if (!cp) {
     cp = std::make_shared<CholPlan>();
     cp->lc = lc;
-    // block map of V: reachable by the Coulomb or the exchange term (spin conserved pairwise)
     std::vector<tt_tis> vd = {tp, tq, tr, ts};
     int64_t nvb = 1;
     for (auto t : vd) nvb *= t->ntiles();
-    std::vector<uint8_t> vnz(nvb);
+    std::vector<uint8_t> vnz(nvb), wnz(nvb);
     for (int64_t x = 0; x < nvb; ++x) {
       int64_t y = x;
       int32_t co[4];
       for (int d = 3; d >= 0; --d) { co[d] = (int32_t)(y % vd[d]->ntiles()); y /= vd[d]->ntiles(); }
       const int sp = tp->spin[co[0]], sq = tq->spin[co[1]], sr = tr->spin[co[2]], ss = ts->spin[co[3]];
-      vnz[x] = ((sp == sr && sq == ss) || (sp == ss && sq == sr)) ? 1 : 0;
+      wnz[x] = (sp == sr && sq == ss) ? 1 : 0;             // Coulomb term reachable
+      vnz[x] = (wnz[x] || (sp == ss && sq == sr)) ? 1 : 0;  // Coulomb or exchange
     }
     TT_TRY(new_meta_tensor(ctx, vd, vnz, &cp->Vmeta));
+    TT_TRY(new_meta_tensor(ctx, vd, wnz, &cp->Wmeta));
+    // Bm: B's layout, replicated scratch at the start of the workspace
+    TT_TRY(new_meta_tensor(ctx, B->dims, B->nz, &cp->Bm));
+    for (int64_t x = 0; x < cp->Bm->nblocks; ++x)
+      if (cp->Bm->nz[x]) cp->Bm->owner[x] = TT_REPLICATED;
+    cp->Bm->data = (double*)workspace;
+    cp->Bm->capacity = bm_elems;
+    // all-gather of B (every rank needs every B block for Bm)
+    {
+      Needs need(ctx->nranks);
+      for (int rr = 0; rr < ctx->nranks; ++rr)
+        for (int64_t x = 0; x < B->nblocks; ++x)
+          if (B->nz[x]) need[rr].push_back({0, x, 0, B->block_volume(x)});
+      build_gather(ctx, need, {B}, cp->bgather);
+    }
+    // Bm = B - B(r<->s)
+    std::vector<int> id(B->order), sw(B->order);
+    const size_t rp = b.find(r), sp_ = b.find(s);
+    for (int d = 0; d < B->order; ++d) id[d] = sw[d] = d;
+    sw[rp] = (int)sp_;
+    sw[sp_] = (int)rp;
+    TT_TRY(local_add_plan(ctx, cp->Bm, B, id, 0.0, cp->copy_plan));
+    TT_TRY(local_add_plan(ctx, cp->Bm, B, sw, 1.0, cp->swap_plan));
+    // SPMD plans for this rank's C parts: V map (algorithmic FLOPs) and W map (executed pairs)
     ContractOpts g;
     g.no_a_needs = true;
-    g.tag = "|cholmeta";
+    g.tag = "|cholV";
     bool dummy;
-    TT_TRY(get_contract_plan(ctx, C, cl, cp->Vmeta, vl, B, bl, beta, cp->gplan, &dummy, g));
-    const ContractPlan& gp = *cp->gplan;
-    // units: my C parts grouped by the (p,q) tile coordinates; V rows restricted when C's dim 0 is p
+    TT_TRY(get_contract_plan(ctx, C, cl, cp->Vmeta, vl, B, bl, beta, cp->vplan, &dummy, g));
+    g.tag = "|cholW";
+    TT_TRY(get_contract_plan(ctx, C, cl, cp->Wmeta, vl, cp->Bm, bl, beta, cp->wplan, &dummy, g));
+    const ContractPlan& gp = *cp->wplan;
+    // units: my C parts grouped by the (p,q) tile coordinates; W rows restricted when C's dim 0 is p
     const bool rows_on_p = c[0] == p;
     const int cp_pos = (int)c.find(p), cq_pos = (int)c.find(q);
     struct Unit {
       int32_t tp, tq;
-      std::vector<std::pair<int64_t, int64_t>> vrows;
+      std::vector<std::pair<int64_t, int64_t>> wrows;
       std::vector<PartSel> cparts;
     };
     std::map<std::pair<int32_t, int32_t>, Unit> units;
@@ -1975,61 +2058,65 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       u.tp = cc[cp_pos];
       u.tq = cc[cq_pos];
       u.cparts.push_back({cb, mp.lo, mp.hi});
-      if (rows_on_p) u.vrows.push_back({mp.lo, mp.hi});
-      else u.vrows.push_back({0, tp->size(u.tp)});
+      if (rows_on_p) u.wrows.push_back({mp.lo, mp.hi});
+      else u.wrows.push_back({0, tp->size(u.tp)});
     }
-    // batches: consecutive units while the V blocks of the batch fit the workspace
+    double* wbase = (double*)workspace + bm_elems;
+    const int64_t w_elems = ws_elems - bm_elems;
+    auto row_blocks = [&](const Unit& u, std::vector<int64_t>& out) {
+      out.clear();
+      for (int32_t a2 = 0; a2 < tr->ntiles(); ++a2)
+        for (int32_t b2 = 0; b2 < ts->ntiles(); ++b2) {
+          const int64_t vb = (((int64_t)u.tp * tq->ntiles() + u.tq) * tr->ntiles() + a2) * ts->ntiles() + b2;
+          if (wnz[vb]) out.push_back(vb);
+        }
+    };
     auto flush = [&](std::vector<const Unit*>& cur) -> tt_status {
       if (cur.empty()) return TT_OK;
       CholBatch bt;
       std::vector<uint8_t> bnz(nvb, 0);
-      std::vector<std::pair<int64_t, std::pair<int64_t, int64_t>>> vparts;
+      std::vector<int64_t> rb;
       for (const Unit* u : cur) {
-        // merged row ranges of this unit
-        auto rows = u->vrows;
+        auto rows = u->wrows;
         std::sort(rows.begin(), rows.end());
         std::vector<std::pair<int64_t, int64_t>> mr;
         for (auto& x : rows) {
           if (!mr.empty() && x.first <= mr.back().second) mr.back().second = std::max(mr.back().second, x.second);
           else mr.push_back(x);
         }
-        for (int32_t a2 = 0; a2 < tr->ntiles(); ++a2)
-          for (int32_t b2 = 0; b2 < ts->ntiles(); ++b2) {
-            const int64_t vb = (((int64_t)u->tp * tq->ntiles() + u->tq) * tr->ntiles() + a2) * ts->ntiles() + b2;
-            if (!vnz[vb]) continue;
-            bnz[vb] = 1;
-            for (auto& x : mr) vparts.push_back({vb, x});
-          }
+        row_blocks(*u, rb);
+        for (int64_t vb : rb) {
+          bnz[vb] = 1;
+          for (auto& x : mr) bt.wopt.sel.push_back({vb, x.first, x.second});
+        }
         for (const PartSel& ps : u->cparts) bt.copt.sel.push_back(ps);
       }
-      TT_TRY(new_meta_tensor(ctx, vd, bnz, &bt.Vb));
-      if (bt.Vb->packed_elems > ws_elems) {
-        delete bt.Vb;
-        return fail(TT_E_OOM, "workspace of %lld doubles cannot hold one (p,q) row of V (%lld doubles)",
-                    (long long)ws_elems, (long long)bt.Vb->packed_elems);
+      TT_TRY(new_meta_tensor(ctx, vd, bnz, &bt.Wb));
+      if (bt.Wb->packed_elems > w_elems) {
+        const long long need = (long long)bt.Wb->packed_elems;
+        delete bt.Wb;
+        return fail(TT_E_OOM, "workspace after Bm holds %lld doubles; one (p,q) row of W needs %lld",
+                    (long long)w_elems, need);
       }
-      bt.Vb->data = (double*)workspace;
-      bt.Vb->capacity = ws_elems;
-      for (auto& vp : vparts) bt.vopt.sel.push_back({vp.first, vp.second.first, vp.second.second});
-      bt.vopt.local = bt.copt.local = true;
+      bt.Wb->data = wbase;
+      bt.Wb->capacity = w_elems;
+      bt.wopt.local = bt.copt.local = true;
       const size_t bi = cp->batches.size();
-      bt.vopt.tag = "|cholV" + std::to_string(bi);
-      bt.copt.tag = "|cholC" + std::to_string(bi);
+      bt.wopt.tag = "|cholWb" + std::to_string(bi);
+      bt.copt.tag = "|cholCb" + std::to_string(bi);
       cp->batches.push_back(bt);
       cur.clear();
       return TT_OK;
     };
     std::vector<const Unit*> cur;
     int64_t cur_elems = 0;
+    std::vector<int64_t> rb;
     for (auto& kv : units) {
       const Unit& u = kv.second;
+      row_blocks(u, rb);
       int64_t uel = 0;
-      for (int32_t a2 = 0; a2 < tr->ntiles(); ++a2)
-        for (int32_t b2 = 0; b2 < ts->ntiles(); ++b2) {
-          const int64_t vb = (((int64_t)u.tp * tq->ntiles() + u.tq) * tr->ntiles() + a2) * ts->ntiles() + b2;
-          if (vnz[vb]) uel += (cp->Vmeta->block_volume(vb) + 1) / 2 * 2;
-        }
-      if (!cur.empty() && cur_elems + uel > ws_elems) {
+      for (int64_t vb : rb) uel += (cp->Wmeta->block_volume(vb) + 1) / 2 * 2;
+      if (!cur.empty() && cur_elems + uel > w_elems) {
         TT_TRY(flush(cur));
         cur_elems = 0;
       }
@@ -2040,33 +2127,29 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     ctx->plans[keybuf] = cp;
   }
   reset_stats(ctx);
-  const ContractPlan& gp = *cp->gplan;
-  TT_TRY(run_gather(ctx, gp.gp, {cp->Vmeta, B}));
+  TT_TRY(run_gather(ctx, cp->bgather, {B}));
+  TT_TRY(run_local_add(ctx, *cp->copy_plan, cp->Bm, B, 0.0, 1.0));
+  TT_TRY(run_local_add(ctx, *cp->swap_plan, cp->Bm, B, 1.0, -1.0));
   const std::string L = cp->lc;
-  const std::string xc1 = std::string(1, p) + r + L, xc2 = std::string(1, q) + s + L;   // Coulomb
-  const std::string xe1 = std::string(1, p) + s + L, xe2 = std::string(1, q) + r + L;   // exchange
-  double flops = 0, aux = 0;
+  const std::string x1 = std::string(1, p) + r + L, x2 = std::string(1, q) + s + L;   // W = X(prL) X(qsL)
+  double exec = 0, build = 0;
   int64_t tasks = 0;
   for (auto& bt : cp->batches) {
-    std::shared_ptr<ContractPlan> pc, pe, pu;
+    std::shared_ptr<ContractPlan> pw, pu;
     bool dummy;
-    TT_TRY(get_contract_plan(ctx, bt.Vb, vl, X, xc1.c_str(), X, xc2.c_str(), 0.0, pc, &dummy, bt.vopt));
-    ContractOpts eo = bt.vopt;
-    eo.tag += "x";
-    TT_TRY(get_contract_plan(ctx, bt.Vb, vl, X, xe1.c_str(), X, xe2.c_str(), 1.0, pe, &dummy, eo));
-    TT_TRY(get_contract_plan(ctx, C, cl, bt.Vb, vl, B, bl, beta, pu, &dummy, bt.copt));
-    TT_TRY(launch_plan(ctx, *pc, bt.Vb, vl, 0.0, 1.0, X, xc1.c_str(), X, xc2.c_str()));
-    TT_TRY(launch_plan(ctx, *pe, bt.Vb, vl, 1.0, -1.0, X, xe1.c_str(), X, xe2.c_str()));
-    TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Vb, vl, B, bl));
-    aux += pc->flops + pe->flops;
-    flops += pu->flops;
+    TT_TRY(get_contract_plan(ctx, bt.Wb, vl, X, x1.c_str(), X, x2.c_str(), 0.0, pw, &dummy, bt.wopt));
+    TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
+    TT_TRY(launch_plan(ctx, *pw, bt.Wb, vl, 0.0, 1.0, X, x1.c_str(), X, x2.c_str()));
+    TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Wb, vl, cp->Bm, bl));
+    build += pw->flops;
+    exec += pu->flops;
     tasks += pu->tasks;
   }
-  ctx->last.c_blocks = (int64_t)gp.my.size();
+  ctx->last.c_blocks = (int64_t)cp->wplan->my.size();
   ctx->last.tasks = tasks;
-  ctx->last.flops = flops;
-  ctx->last.aux_flops = aux;
-  ctx->last.gathered_bytes = gp.gp.recv_bytes;
+  ctx->last.flops = cp->vplan->flops;       // algorithmic: the defined contraction over V's block map
+  ctx->last.aux_flops = build + exec;       // executed: W build + consume against Bm
+  ctx->last.gathered_bytes = cp->bgather.recv_bytes;
   ctx->last.work_items = (int64_t)cp->batches.size();
   return TT_OK;
 }

@@ -459,7 +459,8 @@ def test_contract_cholesky(env, spin, ws_rows):
         dense[name] = O.dense_masked(orc[name], S.dense(orc[name].shape, 2, tag))
         bufs.append(bind_host(torch, P[name], O.pack(orc[name], dense[name])))
     tv = max(np.diff(P["X"].dims[0].offsets))
-    ws = torch.empty(int(ws_rows * tv ** 4 * P["X"].dims[0].ntiles ** 2 + 64), dtype=torch.float64, device="cuda")
+    ws = torch.empty(int(P["T"].packed_elems + 32 + ws_rows * tv ** 4 * P["X"].dims[0].ntiles ** 2 + 64),
+                     dtype=torch.float64, device="cuda")
     for beta in (1.0, 0.0):
         tt.contract_cholesky(ctx, P["R"], "abij", beta, 0.5, P["X"], "abcd", P["T"], "cdij", ws)
         got = P["R"].download()
