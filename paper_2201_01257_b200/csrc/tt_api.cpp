@@ -470,6 +470,7 @@ struct ContractPlan {
   GatherPlan gp;
   int variant = 0;
   bool a_vec = false, b_vec = false;   // 16-byte copies along the operand's contiguous direction
+  bool persistent = false;             // short work items: persistent CTAs hide pipeline fill / epilogue
   int64_t nwork = 0;
   CGroupDesc* d_groups = nullptr;
   TaskDesc* d_tasks = nullptr;
@@ -1586,6 +1587,14 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       for (int32_t nt = 0; nt < ntn; ++nt) work.push_back({gi, mt, nt});
   }
   pl.nwork = (int64_t)work.size();
+  {
+    // persistent CTAs pay off when items are short (pipeline fill and epilogue are a visible share);
+    // long items keep the hardware's dynamic block scheduling (better for uneven item costs)
+    double st_sum = 0;
+    for (const WorkItem& w : work) st_sum += groups[w.group].nstages;
+    pl.persistent = !work.empty() && st_sum / (double)work.size() < 512.0;
+    if (const char* fp = getenv("TT_PERSISTENT")) pl.persistent = atoi(fp) != 0;
+  }
   TT_TRY(dev_alloc(ctx, &pl.d_groups, groups.size()));
   TT_TRY(dev_alloc(ctx, &pl.d_work, work.size()));
   if (!groups.empty()) TT_CUDA(cudaMemcpy(pl.d_groups, groups.data(), groups.size() * sizeof(CGroupDesc), cudaMemcpyHostToDevice));
@@ -1627,6 +1636,9 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
   p.nK = (int32_t)pl.an.kg.size();
   p.alpha = alpha;
   p.beta = beta;
+  p.nwork = pl.nwork;
+  p.sm_count = ctx->sm_count;
+  p.persistent = pl.persistent ? 1 : 0;
   const std::string nm = std::string("tt_contract_dmma[") + cl + "=" + al + "*" + bl + "]";
   Launch L(ctx, nm.c_str());
   if (pl.variant < num_contract_variants())

@@ -136,77 +136,88 @@ struct Smem {
   static_assert(STAGES >= 3, "pipeline too shallow");
 };
 
-// Producer: stream one operand.  ROWS = BM (A) or BN (B); KC = k contiguous.
+// Producer: stream one operand for every work item of this (persistent) CTA.  ROWS = BM (A) or BN
+// (B); KC = k contiguous.  The stage ring and its phases continue across work items, so the next
+// item's first stages are in flight while the MMA warps finish the current item and its epilogue.
 template <class K, int STAGES, int ROWS, bool KC, bool VEC>
-__device__ __forceinline__ void produce(const ContractParams& p, const CGroupDesc& g, int row0, bool isA,
-                                        double* sbase, int stage_elems, int ld, uint64_t* full, uint64_t* empty) {
+__device__ __forceinline__ void produce(const ContractParams& p, bool isA, double* sbase, int stage_elems, int ld,
+                                        uint64_t* full, uint64_t* empty) {
   using C = Copy<ROWS, K::BK, KC, VEC>;
   const int lane = threadIdx.x & 31;
   const int nG = isA ? p.nM : p.nN;                 // row groups
   const int nK = p.nK;
-  const int32_t* rext = isA ? g.mext : g.next;
-  const int ROWMAX = isA ? g.M : g.N;
   // lane geometry
   const int r_l = KC ? (lane >> 3) : (lane % C::QL) * C::RU;   // first row of the lane
   const int k_l = KC ? (lane & 7) * (VEC ? 2 : 1) : (lane / C::QL);
   const int r_step = KC ? 4 : C::QL * C::RU;
   const int k_step = KC ? 8 : 32 / C::QL;          // (!VEC KC: second k at +8)
   int32_t roff[C::NR];
-  int32_t kext[kMaxGroup], kst[kMaxGroup];
+  int32_t kext[kMaxGroup], kst[kMaxGroup], rext[kMaxGroup];
   const double* base = nullptr;
   int32_t Kt = 0;
-  int t = g.task_begin, k0 = 0, st = 0;
+  int st = 0;
   unsigned phase = 1;   // empty barriers: first wait passes
-  auto setup = [&](int tt_) {
-    const TaskDesc* td = p.tasks + tt_;
-    base = isA ? p.A + td->a_off : p.B + td->b_off;
-    Kt = td->K;
-    int32_t rst[kMaxGroup];
+  for (int64_t wi = blockIdx.x; wi < p.nwork; wi += gridDim.x) {
+    const WorkItem w = p.work[wi];
+    const CGroupDesc* g = p.groups + w.group;
+    const int row0 = isA ? g->m_begin + w.mt * K::BM : g->n_begin + w.nt * K::BN;
+    const int ROWMAX = isA ? g->M : g->N;
+    const int t_end = g->task_end, nst = g->nstages;
 #pragma unroll
-    for (int i = 0; i < kMaxGroup; ++i) {
-      kext[i] = td->kext[i];
-      kst[i] = isA ? td->ak_str[i] : td->bk_str[i];
-      rst[i] = isA ? td->am_str[i] : td->bn_str[i];
-    }
+    for (int i = 0; i < kMaxGroup; ++i) rext[i] = isA ? g->mext[i] : g->next[i];
+    int t = g->task_begin, k0 = 0;
+    auto setup = [&](int tt_) {
+      const TaskDesc* td = p.tasks + tt_;
+      base = isA ? p.A + td->a_off : p.B + td->b_off;
+      Kt = td->K;
+      int32_t rst[kMaxGroup];
 #pragma unroll
-    for (int i = 0; i < C::NR; ++i) {
-      const int r = row0 + r_l + r_step * i;
-      roff[i] = (r < ROWMAX) ? dot_decode(r, nG, rext, rst) : -1;
-    }
-  };
-  if (t < g.task_end) setup(t);
-  const int nst = g.nstages;
-  for (int s = 0; s < nst; ++s) {
-    mbar_wait_sleep(&empty[st], phase);
-    double* dst = sbase + st * stage_elems;
-#pragma unroll
-    for (int j = 0; j < C::NK; ++j) {
-      const int kl = k_l + k_step * j;
-      const int k = k0 + kl;
-      const bool kv = k < Kt;
-      const int32_t ko = kv ? dot_decode(k, nK, kext, kst) : 0;
+      for (int i = 0; i < kMaxGroup; ++i) {
+        kext[i] = td->kext[i];
+        kst[i] = isA ? td->ak_str[i] : td->bk_str[i];
+        rst[i] = isA ? td->am_str[i] : td->bn_str[i];
+      }
 #pragma unroll
       for (int i = 0; i < C::NR; ++i) {
-        const int rl = r_l + r_step * i;
-        const bool v = kv && roff[i] >= 0;
-        const double* src = v ? base + roff[i] + ko : p.A;
-        double* d = KC ? dst + rl * ld + kl : dst + kl * ld + rl;
-        if (VEC) cp_async16(d, src, v);
-        else cp_async8(d, src, v);
+        const int r = row0 + r_l + r_step * i;
+        roff[i] = (r < ROWMAX) ? dot_decode(r, nG, rext, rst) : -1;
       }
+    };
+    if (t < t_end) setup(t);
+    for (int s = 0; s < nst; ++s) {
+      mbar_wait_sleep(&empty[st], phase);
+      double* dst = sbase + st * stage_elems;
+#pragma unroll
+      for (int j = 0; j < C::NK; ++j) {
+        const int kl = k_l + k_step * j;
+        const int k = k0 + kl;
+        const bool kv = k < Kt;
+        const int32_t ko = kv ? dot_decode(k, nK, kext, kst) : 0;
+#pragma unroll
+        for (int i = 0; i < C::NR; ++i) {
+          const int rl = r_l + r_step * i;
+          const bool v = kv && roff[i] >= 0;
+          const double* src = v ? base + roff[i] + ko : p.A;
+          double* d = KC ? dst + rl * ld + kl : dst + kl * ld + rl;
+          if (VEC) cp_async16(d, src, v);
+          else cp_async8(d, src, v);
+        }
+      }
+      mbar_arrive_cp_async(&full[st]);
+      k0 += K::BK;
+      if (k0 >= Kt) {
+        k0 = 0;
+        ++t;
+        if (t < t_end) setup(t);
+      }
+      if (++st == STAGES) { st = 0; phase ^= 1; }
     }
-    mbar_arrive_cp_async(&full[st]);
-    k0 += K::BK;
-    if (k0 >= Kt) {
-      k0 = 0;
-      ++t;
-      if (t < g.task_end) setup(t);
-    }
-    if (++st == STAGES) { st = 0; phase ^= 1; }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// Persistent CTAs (grid = min(work items, resident CTAs)): CTA b processes items b, b+G, b+2G, ...
+// (items are sorted by cost, so striding balances like LPT).
 template <class K, bool AKC, bool BNC, bool AVEC, bool BVEC>
 __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(const ContractParams p) {
   using SM = Smem<K, AKC, BNC>;
@@ -217,12 +228,9 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(co
   double* sB = smem + STAGES * SM::A_ELEMS;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::STAGE);
   uint64_t* empty = full + STAGES;
-  __shared__ CGroupDesc g;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const WorkItem w = p.work[blockIdx.x];
   if (tid == 0) {
-    g = p.groups[w.group];
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 2 * 32);        // every producer thread arrives once per stage
       mbar_init(&empty[s], K::NMMA);      // one arrival per MMA warp
@@ -230,90 +238,102 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(co
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  const int m0 = g.m_begin + w.mt * K::BM, n0 = g.n_begin + w.nt * K::BN;
 
   if (warp >= K::NMMA) {
     // ------------------------------------------------------------- producers
     if (warp == K::NMMA)
-      produce<K, STAGES, K::BM, AKC, AVEC>(p, g, m0, true, sA, SM::A_ELEMS, SM::TA::LD, full, empty);
+      produce<K, STAGES, K::BM, AKC, AVEC>(p, true, sA, SM::A_ELEMS, SM::TA::LD, full, empty);
     else
-      produce<K, STAGES, K::BN, BKC, BVEC>(p, g, n0, false, sB, SM::B_ELEMS, SM::TB::LD, full, empty);
+      produce<K, STAGES, K::BN, BKC, BVEC>(p, false, sB, SM::B_ELEMS, SM::TB::LD, full, empty);
     return;
   }
 
   // --------------------------------------------------------------- MMA warps
   const int wm = warp / K::WN, wn = warp % K::WN;
-  double acc[K::MT][K::NT][2];
-#pragma unroll
-  for (int i = 0; i < K::MT; ++i)
-#pragma unroll
-    for (int j = 0; j < K::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
   const int q = lane & 3, r8 = lane >> 2;
-  const int nst = g.nstages;
+  const double alpha = p.alpha, beta = p.beta;
   int st = 0;
   unsigned phase = 0;
-  for (int s = 0; s < nst; ++s) {
-    mbar_wait(&full[st], phase);
-    const double* a = sA + st * SM::A_ELEMS;
-    const double* b = sB + st * SM::B_ELEMS;
+  for (int64_t wi = blockIdx.x; wi < p.nwork; wi += gridDim.x) {
+    const WorkItem w = p.work[wi];
+    const CGroupDesc* g = p.groups + w.group;
+    const int m0 = g->m_begin + w.mt * K::BM, n0 = g->n_begin + w.nt * K::BN;
+    const int nst = g->nstages;
+    double acc[K::MT][K::NT][2];
 #pragma unroll
-    for (int o = 0; o < K::BK / 8; ++o) {
-      double af[K::MT][2], bf[K::NT][2];
+    for (int i = 0; i < K::MT; ++i)
 #pragma unroll
-      for (int i = 0; i < K::MT; ++i) {
-        const int m = wm * K::WTM + i * 8 + r8;
-        if (AKC) {
-          const double2 v = *reinterpret_cast<const double2*>(a + m * SM::TA::LD + 8 * o + 2 * q);
-          af[i][0] = v.x;
-          af[i][1] = v.y;
-        } else {
-          af[i][0] = a[(8 * o + 2 * q) * SM::TA::LD + m];
-          af[i][1] = a[(8 * o + 2 * q + 1) * SM::TA::LD + m];
+      for (int j = 0; j < K::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int s = 0; s < nst; ++s) {
+      mbar_wait(&full[st], phase);
+      const double* a = sA + st * SM::A_ELEMS;
+      const double* b = sB + st * SM::B_ELEMS;
+#pragma unroll
+      for (int o = 0; o < K::BK / 8; ++o) {
+        double af[K::MT][2], bf[K::NT][2];
+#pragma unroll
+        for (int i = 0; i < K::MT; ++i) {
+          const int m = wm * K::WTM + i * 8 + r8;
+          if (AKC) {
+            const double2 v = *reinterpret_cast<const double2*>(a + m * SM::TA::LD + 8 * o + 2 * q);
+            af[i][0] = v.x;
+            af[i][1] = v.y;
+          } else {
+            af[i][0] = a[(8 * o + 2 * q) * SM::TA::LD + m];
+            af[i][1] = a[(8 * o + 2 * q + 1) * SM::TA::LD + m];
+          }
         }
+#pragma unroll
+        for (int j = 0; j < K::NT; ++j) {
+          const int n = wn * K::WTN + j * 8 + r8;
+          if (BKC) {
+            const double2 v = *reinterpret_cast<const double2*>(b + n * SM::TB::LD + 8 * o + 2 * q);
+            bf[j][0] = v.x;
+            bf[j][1] = v.y;
+          } else {
+            bf[j][0] = b[(8 * o + 2 * q) * SM::TB::LD + n];
+            bf[j][1] = b[(8 * o + 2 * q + 1) * SM::TB::LD + n];
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int i = 0; i < K::MT; ++i)
+#pragma unroll
+            for (int j = 0; j < K::NT; ++j) dmma884(acc[i][j], af[i][t], bf[j][t]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == STAGES) { st = 0; phase ^= 1; }
+    }
+
+    // epilogue (the producers are already streaming the next item)
+    double* Cb = p.C + g->c_off;
+    const int M = g->M, N = g->N;
+    int32_t mext[kMaxGroup], next[kMaxGroup], cms[kMaxGroup], cns[kMaxGroup];
+#pragma unroll
+    for (int i = 0; i < kMaxGroup; ++i) {
+      mext[i] = g->mext[i];
+      next[i] = g->next[i];
+      cms[i] = g->cm_str[i];
+      cns[i] = g->cn_str[i];
+    }
+#pragma unroll
+    for (int i = 0; i < K::MT; ++i) {
+      const int m = m0 + wm * K::WTM + i * 8 + r8;
+      if (m >= M) continue;
+      const int32_t om = dot_decode(m, p.nM, mext, cms);
 #pragma unroll
       for (int j = 0; j < K::NT; ++j) {
-        const int n = wn * K::WTN + j * 8 + r8;
-        if (BKC) {
-          const double2 v = *reinterpret_cast<const double2*>(b + n * SM::TB::LD + 8 * o + 2 * q);
-          bf[j][0] = v.x;
-          bf[j][1] = v.y;
-        } else {
-          bf[j][0] = b[(8 * o + 2 * q) * SM::TB::LD + n];
-          bf[j][1] = b[(8 * o + 2 * q + 1) * SM::TB::LD + n];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int n = n0 + wn * K::WTN + j * 8 + 2 * q + r;
+          if (n >= N) continue;
+          double* c = Cb + om + dot_decode(n, p.nN, next, cns);
+          const double v = alpha * acc[i][j][r];
+          *c = (beta == 0.0) ? v : beta * *c + v;
         }
-      }
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int i = 0; i < K::MT; ++i)
-#pragma unroll
-          for (int j = 0; j < K::NT; ++j) dmma884(acc[i][j], af[i][t], bf[j][t]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-    if (++st == STAGES) { st = 0; phase ^= 1; }
-  }
-
-  // epilogue
-  double* Cb = p.C + g.c_off;
-  const double alpha = p.alpha, beta = p.beta;
-  const int M = g.M, N = g.N;
-#pragma unroll
-  for (int i = 0; i < K::MT; ++i) {
-    const int m = m0 + wm * K::WTM + i * 8 + r8;
-    if (m >= M) continue;
-    const int32_t om = dot_decode(m, p.nM, g.mext, g.cm_str);
-#pragma unroll
-    for (int j = 0; j < K::NT; ++j) {
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int n = n0 + wn * K::WTN + j * 8 + 2 * q + r;
-        if (n >= N) continue;
-        double* c = Cb + om + dot_decode(n, p.nN, g.next, g.cn_str);
-        const double v = alpha * acc[i][j][r];
-        *c = (beta == 0.0) ? v : beta * *c + v;
       }
     }
   }
@@ -343,7 +363,12 @@ static cudaError_t setup_cfg() {
 
 template <class K, bool AKC, bool BNC, bool AV, bool BV>
 static cudaError_t launch_one(const ContractParams& p, int64_t nwork, cudaStream_t s) {
-  tt_contract_ws_kernel<K, AKC, BNC, AV, BV><<<(unsigned)nwork, K::NTHREADS, Smem<K, AKC, BNC>::BYTES, s>>>(p);
+  // persistent grid: at most the resident CTAs (SM count x CTAs per SM)
+  const int64_t slots = (int64_t)p.sm_count * K::MINB;
+  const unsigned grid = (unsigned)((p.persistent && nwork > slots) ? slots : nwork);
+  ContractParams q = p;
+  q.nwork = nwork;
+  tt_contract_ws_kernel<K, AKC, BNC, AV, BV><<<grid, K::NTHREADS, Smem<K, AKC, BNC>::BYTES, s>>>(q);
   return cudaGetLastError();
 }
 template <class K, bool AKC, bool BNC>

@@ -53,6 +53,9 @@ struct ContractParams {
   const WorkItem* work;
   int32_t nM, nN, nK;
   double alpha, beta;
+  int64_t nwork;          // work items (persistent kernels loop over them)
+  int32_t sm_count;       // SMs of the device (persistent grid size)
+  int32_t persistent;     // 1: grid = resident CTAs looping over items; 0: one CTA per item
 };
 
 struct VariantInfo {
