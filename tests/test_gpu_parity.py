@@ -471,3 +471,67 @@ def test_contract_cholesky(env, spin, ws_rows):
         ref = O.contract(dense["R"], "abij", Vx, "abcd", dense["T"], "cdij", 0.5, beta, cmask=O.nz_mask(orc["R"]))
         assert normwise(got, O.pack(orc["R"], ref)) <= TOL
         dense["R"] = ref
+
+
+def test_config3_full_size_sampled(env):
+    """BASELINE configs[2] at full size (O=60 V=400 tO=30 tV=40, alpha/beta maps; V is 76.8 GB):
+    the three doubles terms accumulated into R as bench.py --config cfg3 runs them; 8 sampled outputs
+    per non-zero R block (4 corners + 4 random) vs the oracle element by element, zero blocks masked."""
+    tt, torch = env
+    pb = ccsd_problem(60, 400, 30, 40, True)
+    ctx = new_ctx(tt, torch)
+    P = product_objects(tt, ctx, pb)
+    orc = oracle_objects(pb)
+    tags = {"R": 3, "Vv": 4, "T": 5, "Ta": 1, "Wr": 2, "Tb": 6, "Wh": 7}
+    bufs = {}
+    for name in pb.tensors:
+        bufs[name] = torch.empty(P[name].packed_elems, dtype=torch.float64, device="cuda")
+        P[name].bind(bufs[name])
+        tt.fill_synthetic(ctx, P[name], 13, tags[name])
+    for (c, cl, a, al, b, bl) in pb.ops:
+        tt.contract(ctx, P[c], cl, 1.0, 1.0, P[a], al, P[b], bl)
+    got = P["R"].download()
+    ctx.sync()
+    del bufs
+    torch.cuda.empty_cache()
+    R = orc["R"]
+    rng = np.random.default_rng(1)
+    idx = []
+    for blk in range(R.nblocks()):
+        if not R.nz[blk]:
+            continue
+        o, e = R.block_origin(blk), R.block_extents(blk)
+        idx += [[o[d] + (e[d] - 1 if (qq >> d) & 1 else 0) for d in range(4)] for qq in (0, 5, 10, 15)]
+        idx += [[o[d] + rng.integers(e[d]) for d in range(4)] for _ in range(4)]
+    idx = np.array(idx)
+    ext = dict(a=400, b=400, c=400, d=400, i=60, j=60, k=60, l=60)
+
+    def gen(name):
+        T = orc[name]
+        return (lambda ix: S.values(13, tags[name], S.linear_index(T.shape, ix)),
+                lambda ix: _nz_elem(T, ix))
+
+    ref = S.values(13, 3, S.linear_index(R.shape, idx))
+    for (c, cl, a, al, b, bl) in pb.ops:
+        av, anz = gen(a)
+        bv, bnz = gen(b)
+        ref = ref + O.sampled_elements(idx, cl, al, bl, ext, av, bv, anz, bnz)
+    offs = R.blk_off()
+    pos = []
+    for x in idx:
+        blk = R.block_id([int(np.searchsorted(R.dims[d].offsets, x[d], side="right") - 1) for d in range(4)])
+        org, e = R.block_origin(blk), R.block_extents(blk)
+        loc = [x[d] - org[d] for d in range(4)]
+        pos.append(offs[blk] + ((loc[0] * e[1] + loc[1]) * e[2] + loc[2]) * e[3] + loc[3])
+    g = got[np.array(pos)]
+    assert np.abs(g - ref).max() / np.abs(ref).max() <= TOL
+
+
+def _nz_elem(T, ix):
+    """1 where the global index tuples ix lie in a non-zero block of oracle tensor T."""
+    ix = np.asarray(ix)
+    tiles = [np.searchsorted(np.asarray(T.dims[d].offsets), ix[..., d], side="right") - 1 for d in range(T.order)]
+    bid = np.zeros(ix.shape[:-1], dtype=np.int64)
+    for d, g in enumerate(T.grid):
+        bid = bid * g + tiles[d]
+    return np.asarray(T.nz, dtype=np.uint8)[bid]
