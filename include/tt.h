@@ -58,6 +58,7 @@ typedef struct tt_ctx_s* tt_ctx;
 typedef struct tt_is_s* tt_is;
 typedef struct tt_tis_s* tt_tis;
 typedef struct tt_tensor_s* tt_tensor;
+typedef struct tt_sched_s* tt_sched;
 
 /* Per-call statistics of the last set/add/contract/scalar call on a context (host-side counts). */
 typedef struct {
@@ -267,6 +268,33 @@ tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tens
 tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
                          tt_tensor B, const char* b_lbl, int64_t* recv, int64_t* n_recv,
                          int64_t* send, int64_t* n_send, int64_t cap);
+
+/* ------------------------------------------------------------------------------------------------
+ * Scheduler (P178, P191-199, P215: "Scheduler sch{&ec}; sch(op)(op)...execute()").  Operations are
+ * queued (arguments as the immediate calls; tensors and host result pointers must stay valid until
+ * tt_sched_execute returns) and executed in LEVELS (reading R25): two ops conflict when they share a
+ * tensor and one of them writes it (a "+=" / beta != 0 update reads and writes its output); the level
+ * of an op is 1 + the largest level of the earlier ops it conflicts with (0 if none).  Each level's
+ * ops run concurrently on the scheduler's `nstreams` CUDA streams, forked from and joined back into
+ * the context stream (one synchronisation point per level); with nranks > 1 they run in queue order
+ * on the context stream (every rank then issues its NCCL calls in the same order).  execute clears
+ * the queue.  A host-only context can queue and levelize but not execute (TT_E_STATE). */
+tt_status tt_sched_create(tt_ctx ctx, int32_t nstreams, tt_sched* out);
+tt_status tt_sched_destroy(tt_sched s);
+tt_status tt_sched_set(tt_sched s, tt_tensor C, double alpha);
+tt_status tt_sched_add(tt_sched s, tt_tensor C, const char* c_lbl, double beta, double alpha, tt_tensor A,
+                       const char* a_lbl);
+tt_status tt_sched_contract(tt_sched s, tt_tensor C, const char* c_lbl, double beta, double alpha,
+                            tt_tensor A, const char* a_lbl, tt_tensor B, const char* b_lbl);
+tt_status tt_sched_contract_cholesky(tt_sched s, tt_tensor C, const char* c_lbl, double beta, double alpha,
+                                     tt_tensor X, const char* v_lbl, tt_tensor B, const char* b_lbl,
+                                     void* workspace, int64_t ws_elems);
+tt_status tt_sched_scalar(tt_sched s, double alpha, tt_tensor A, const char* a_lbl, tt_tensor B,
+                          const char* b_lbl, double* result);
+/* level[nops] of every queued op (NULL to query only), nops, number of levels. */
+tt_status tt_sched_levels(tt_sched s, int32_t* level, int64_t* nops, int32_t* nlevels);
+tt_status tt_sched_execute(tt_sched s);
+tt_status tt_sched_stats(tt_sched s, int64_t* queued, int64_t* levels_executed);
 
 const char* tt_last_error(void);
 int32_t tt_version(void);

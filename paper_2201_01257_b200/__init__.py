@@ -88,6 +88,17 @@ _SIGS = {
     "tt_partition_split": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32],
     "tt_gather_plan": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _P(_i64), _vp,
                        _P(_i64), _i64],
+    "tt_sched_create": [_vp, _i32, _P(_vp)],
+    "tt_sched_destroy": [_vp],
+    "tt_sched_set": [_vp, _vp, _dbl],
+    "tt_sched_add": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p],
+    "tt_sched_contract": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p],
+    "tt_sched_contract_cholesky": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp,
+                                   ctypes.c_char_p, _vp, _i64],
+    "tt_sched_scalar": [_vp, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _P(_dbl)],
+    "tt_sched_levels": [_vp, _vp, _P(_i64), _P(_i32)],
+    "tt_sched_execute": [_vp],
+    "tt_sched_stats": [_vp, _P(_i64), _P(_i64)],
     "tt_last_error": [],
     "tt_version": [],
 }
@@ -399,3 +410,75 @@ def gather_plan(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: T
     s = np.empty(5 * cap, np.int64)
     _check(_lib.tt_gather_plan(*args, _ptr(r), ctypes.byref(nr), _ptr(s), ctypes.byref(ns), cap))
     return r[:5 * nr.value].reshape(-1, 5), s[:5 * ns.value].reshape(-1, 5)
+
+
+class Scheduler:
+    """Scheduler (P178, P191-199, P215): queue operations, levelize by conflicts, execute level by
+    level (concurrent streams inside a level).  Mirrors ``sch(op)(op)...execute()``."""
+
+    def __init__(self, ctx: Context, nstreams: int = 4):
+        h = _vp()
+        _check(_lib.tt_sched_create(ctx.h, nstreams, ctypes.byref(h)))
+        self.h, self.ctx = h, ctx
+        self._results = []
+        self._keep = []
+
+    def close(self):
+        if self.h:
+            _check(_lib.tt_sched_destroy(self.h))
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_(self, C: Tensor, alpha: float):
+        _check(_lib.tt_sched_set(self.h, C.h, float(alpha)))
+        return self
+
+    def add(self, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str):
+        _check(_lib.tt_sched_add(self.h, C.h, _b(c_lbl), float(beta), float(alpha), A.h, _b(a_lbl)))
+        return self
+
+    def contract(self, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str, B: Tensor,
+                 b_lbl: str):
+        _check(_lib.tt_sched_contract(self.h, C.h, _b(c_lbl), float(beta), float(alpha), A.h, _b(a_lbl), B.h,
+                                      _b(b_lbl)))
+        return self
+
+    def contract_cholesky(self, C: Tensor, c_lbl: str, beta: float, alpha: float, X: Tensor, v_lbl: str,
+                          B: Tensor, b_lbl: str, workspace, ws_elems: Optional[int] = None):
+        if ws_elems is None:
+            ws_elems = int(workspace.numel())
+        self._keep.append(workspace)
+        _check(_lib.tt_sched_contract_cholesky(self.h, C.h, _b(c_lbl), float(beta), float(alpha), X.h, _b(v_lbl),
+                                               B.h, _b(b_lbl), _vp(_devptr(workspace)), int(ws_elems)))
+        return self
+
+    def scalar(self, alpha: float, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str):
+        """Queues an order-0 contraction; its value is in ``results[i]`` after execute()."""
+        r = _dbl()
+        self._results.append(r)
+        _check(_lib.tt_sched_scalar(self.h, float(alpha), A.h, _b(a_lbl), B.h, _b(b_lbl), ctypes.byref(r)))
+        return self
+
+    def levels(self):
+        n, L = _i64(), _i32()
+        _check(_lib.tt_sched_levels(self.h, None, ctypes.byref(n), ctypes.byref(L)))
+        lv = np.empty(max(n.value, 1), np.int32)
+        _check(_lib.tt_sched_levels(self.h, _ptr(lv), ctypes.byref(n), ctypes.byref(L)))
+        return lv[:n.value].tolist(), L.value
+
+    def execute(self):
+        _check(_lib.tt_sched_execute(self.h))
+        out = [r.value for r in self._results]
+        self._results = []
+        self._keep = []
+        return out
+
+    def stats(self):
+        q, lv = _i64(), _i64()
+        _check(_lib.tt_sched_stats(self.h, ctypes.byref(q), ctypes.byref(lv)))
+        return {"queued": q.value, "levels_executed": lv.value}

@@ -31,6 +31,12 @@ tt_status fail(tt_status code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+
+tt_status tt::set_error(tt_status code, const char* msg) { return fail(code, "%s", msg); }
+
+namespace {
+
 #define TT_CUDA(x)                                                                    \
   do {                                                                                \
     cudaError_t e_ = (x);                                                             \

@@ -43,6 +43,9 @@ struct TaskDesc {
   int32_t am_str[kMaxGroup], bn_str[kMaxGroup]; // M group strides in A, N group strides in B
 };
 
+// sets the thread-local error message of tt_last_error and returns `code`
+tt_status set_error(tt_status code, const char* msg);
+
 struct WorkItem {
   int32_t group;   // index into CGroupDesc array
   int32_t mt, nt;  // tile coordinates inside the block
