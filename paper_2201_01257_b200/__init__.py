@@ -42,7 +42,7 @@ _P = ctypes.POINTER
 class Stats(ctypes.Structure):
     _fields_ = [("c_blocks", _i64), ("tasks", _i64), ("work_items", _i64), ("flops", _dbl), ("bytes", _dbl),
                 ("gathered_bytes", _i64), ("launches", _i64), ("plan_cached", _i32), ("kernel_variant", _i32),
-                ("aux_flops", _dbl)]
+                ("producer", _i32), ("aux_flops", _dbl)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "tt_internal.h"
 #include "tt_launch.h"
 #include "tt_nccl.h"
@@ -477,6 +479,10 @@ struct ContractPlan {
   int variant = 0;
   bool a_vec = false, b_vec = false;   // 16-byte copies along the operand's contiguous direction
   bool persistent = false;             // short work items: persistent CTAs hide pipeline fill / epilogue
+  bool tma = false;                    // TMA producer (uniform fused GEMM-shaped operands)
+  int64_t tma_k = 0, tma_n = 0;        // row lengths of the A [rows][K] and B [rows][N] views
+  CUtensorMap maps[2];                 // A, B tensor maps (encoded for map_ptr)
+  const void* map_ptr[2] = {nullptr, nullptr};
   int64_t nwork = 0;
   CGroupDesc* d_groups = nullptr;
   TaskDesc* d_tasks = nullptr;
@@ -1350,6 +1356,52 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
 
 namespace {
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return fn;
+}
+
+// 2-D tensor map of a packed buffer viewed as [rows][cols] doubles
+tt_status encode_2d(CUtensorMap* m, const double* base, int64_t cols, int64_t rows, uint32_t box_cols, uint32_t box_rows,
+                    bool swizzle128) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(TT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 8};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TT_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TT_OK;
+}
+
+// uniform extent of a fused label group over every non-zero block of T (-1 if it varies)
+int64_t uniform_group_extent(tt_tensor T, const std::vector<int>& tdims) {
+  int64_t e = -1;
+  int32_t c[TT_MAX_ORDER];
+  for (int64_t b = 0; b < T->nblocks; ++b) {
+    if (!T->nz[b]) continue;
+    T->block_coords(b, c);
+    int64_t x = 1;
+    for (int d : tdims) x *= T->dims[d]->size(c[d]);
+    if (e < 0) e = x;
+    else if (e != x) return -1;
+  }
+  return e;
+}
+
 tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B, double beta, ContractPlan& pl,
                               const ContractOpts& opts = ContractOpts()) {
   const Analysis& an = pl.an;
@@ -1601,6 +1653,26 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     pl.persistent = !work.empty() && st_sum / (double)work.size() < 512.0;
     if (const char* fp = getenv("TT_PERSISTENT")) pl.persistent = atoi(fp) != 0;
   }
+  // TMA producer: warp-specialised variant, single fused groups, A = [M][K] and B = [K][N] with the
+  // same K extent in every A block, the same N extent in every B block, K a multiple of 16 (no K tail)
+  {
+    const char* ft = getenv("TT_TMA");
+    const bool allow = !ft || atoi(ft) != 0;
+    if (allow && pl.variant >= num_contract_variants() && an.mg.size() == 1 && an.ng.size() == 1 &&
+        an.kg.size() == 1 && an.a_kc && an.b_nc && !ht.K.empty()) {
+      std::vector<int> ak, bn;
+      for (int u : an.kg[0]) ak.push_back(an.a_pos[u]);
+      for (int u : an.ng[0]) bn.push_back(an.b_pos[u]);
+      const int64_t K = uniform_group_extent(A, ak), N = uniform_group_extent(B, bn);
+      bool ok = K > 0 && N > 0 && K % 16 == 0 && N % 2 == 0;
+      for (int32_t k : ht.K) ok = ok && k == K;
+      if (ok) {
+        pl.tma = true;
+        pl.tma_k = K;
+        pl.tma_n = N;
+      }
+    }
+  }
   TT_TRY(dev_alloc(ctx, &pl.d_groups, groups.size()));
   TT_TRY(dev_alloc(ctx, &pl.d_work, work.size()));
   if (!groups.empty()) TT_CUDA(cudaMemcpy(pl.d_groups, groups.data(), groups.size() * sizeof(CGroupDesc), cudaMemcpyHostToDevice));
@@ -1645,9 +1717,21 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
   p.nwork = pl.nwork;
   p.sm_count = ctx->sm_count;
   p.persistent = pl.persistent ? 1 : 0;
+  p.tma_n = (int32_t)pl.tma_n;
   const std::string nm = std::string("tt_contract_dmma[") + cl + "=" + al + "*" + bl + "]";
   Launch L(ctx, nm.c_str());
-  if (pl.variant < num_contract_variants())
+  if (pl.tma) {
+    // (re-)encode the tensor maps when the bound storage changed
+    ContractPlan& mp = const_cast<ContractPlan&>(pl);
+    if (mp.map_ptr[0] != A->data || mp.map_ptr[1] != B->data) {
+      const VariantInfo vi = variant_info(pl.variant);
+      TT_TRY(encode_2d(&mp.maps[0], A->data, pl.tma_k, A->packed_elems / pl.tma_k, 16, (uint32_t)vi.bm, true));
+      TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->packed_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
+      mp.map_ptr[0] = A->data;
+      mp.map_ptr[1] = B->data;
+    }
+    TT_CUDA(launch_contract_tma(pl.variant - num_contract_variants(), p, pl.maps, pl.nwork, ctx->stream));
+  } else if (pl.variant < num_contract_variants())
     TT_CUDA(launch_contract(pl.variant, pl.an.a_kc, pl.an.b_nc, p, pl.nwork, ctx->stream));
   else
     TT_CUDA(launch_contract_ws(pl.variant - num_contract_variants(), pl.an.a_kc, pl.an.b_nc, pl.a_vec, pl.b_vec, p,
@@ -1681,6 +1765,7 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   ctx->last.gathered_bytes = pl->gp.recv_bytes;
   ctx->last.plan_cached = was_cached ? 1 : 0;
   ctx->last.kernel_variant = pl->variant;
+  ctx->last.producer = pl->tma ? 1 : 0;
   return TT_OK;
 }
 

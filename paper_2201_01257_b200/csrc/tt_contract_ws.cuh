@@ -20,6 +20,8 @@
 #pragma once
 #include <cstdint>
 
+#include <cuda.h>
+
 #include "tt_launch.h"
 
 namespace tt {
@@ -339,6 +341,188 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(co
   }
 }
 
+
+// =================================================================================================
+// TMA variant (fused GEMM-shaped operands with uniform blocks: the ladder / hole-hole layouts).
+// One producer THREAD issues two 2-D cp.async.bulk.tensor loads per stage (A box {16 k, BM rows}
+// with 128-byte swizzle, B box {BN+2 n, 16 k} unswizzled) that complete_tx on the stage's mbarrier;
+// the tensor maps view the whole packed A / B buffer as [rows][K] / [rows][N] matrices (blocks of
+// one shape are contiguous in packed order).  A rows beyond a block's M read the next block (their
+// outputs are discarded), columns beyond K / N read zeros (TMA out-of-bounds fill).  A fragments read
+// swizzled 16-byte chunks; the 8 rows of a fragment are permuted (r -> (r>>1) | ((r&1)<<2)) so that
+// the two rows of every quarter-warp hit opposite 64-byte halves: conflict-free LDS.128.
+
+__device__ __forceinline__ int perm8(int r) { return (r >> 1) | ((r & 1) << 2); }
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(s),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(d),
+      "l"(map), "r"(x), "r"(y), "r"(b)
+      : "memory");
+}
+
+template <class K>
+struct TmaSmem {
+  static constexpr int A_BYTES = K::BM * 128;                 // BK = 16 doubles = 128 B rows, swizzled
+  static constexpr int B_LD = K::BN + 2;                      // doubles per B row (box width)
+  static constexpr int B_BYTES = K::BK * B_LD * 8;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BUDGET = (227 * 1024) / K::MINB - 2048;
+  static constexpr int FIT = BUDGET / (STAGE + 16);
+  static constexpr int STAGES = FIT < K::MAXSTAGES ? FIT : K::MAXSTAGES;
+  static constexpr int BYTES = 1024 + STAGES * STAGE + 2 * STAGES * 8 + 64;
+  static constexpr unsigned TX = (unsigned)(A_BYTES + B_BYTES);
+  static_assert(K::BK == 16, "TMA variant assumes 128-byte A rows");
+  static_assert(A_BYTES % 1024 == 0, "swizzled A stages must stay 1024-byte aligned");
+  static_assert(STAGES >= 3, "pipeline too shallow");
+};
+
+template <class K>
+__global__ void __launch_bounds__(K::NTHREADS, K::MINB)
+    tt_contract_tma_kernel(const ContractParams p, const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB) {
+  using SM = TmaSmem<K>;
+  constexpr int STAGES = SM::STAGES;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = base;                                   // STAGES * A_BYTES
+  unsigned char* sB = base + STAGES * SM::A_BYTES;            // STAGES * B_BYTES
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * SM::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);             // the producer thread's arrive.expect_tx
+      mbar_init(&empty[s], K::NMMA);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp >= K::NMMA) {
+    if (warp != K::NMMA || lane != 0) return;
+    // ------------------------------------------------------------- TMA producer (one thread)
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+    int st = 0;
+    unsigned phase = 1;
+    for (int64_t wi = blockIdx.x; wi < p.nwork; wi += gridDim.x) {
+      const WorkItem w = p.work[wi];
+      const CGroupDesc* g = p.groups + w.group;
+      const int m0 = g->m_begin + w.mt * K::BM, n0 = g->n_begin + w.nt * K::BN;
+      for (int t = g->task_begin; t < g->task_end; ++t) {
+        const TaskDesc* td = p.tasks + t;
+        const int Kt = td->K;
+        const int arow = (int)(td->a_off / Kt) + m0;
+        const int brow0 = (int)(td->b_off / p.tma_n);
+        for (int k0 = 0; k0 < Kt; k0 += K::BK) {
+          mbar_wait_sleep(&empty[st], phase);
+          mbar_expect_tx(&full[st], SM::TX);
+          tma_load_2d(sA + st * SM::A_BYTES, &tmA, k0, arow, &full[st]);
+          tma_load_2d(sB + st * SM::B_BYTES, &tmB, n0, brow0 + k0, &full[st]);
+          if (++st == STAGES) { st = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------- MMA warps
+  const int wm = warp / K::WN, wn = warp % K::WN;
+  const int q = lane & 3, r8 = lane >> 2, pr = perm8(r8);
+  const double alpha = p.alpha, beta = p.beta;
+  int st = 0;
+  unsigned phase = 0;
+  for (int64_t wi = blockIdx.x; wi < p.nwork; wi += gridDim.x) {
+    const WorkItem w = p.work[wi];
+    const CGroupDesc* g = p.groups + w.group;
+    const int m0 = g->m_begin + w.mt * K::BM, n0 = g->n_begin + w.nt * K::BN;
+    const int nst = g->nstages;
+    double acc[K::MT][K::NT][2];
+#pragma unroll
+    for (int i = 0; i < K::MT; ++i)
+#pragma unroll
+      for (int j = 0; j < K::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int s = 0; s < nst; ++s) {
+      mbar_wait(&full[st], phase);
+      const unsigned char* a = sA + st * SM::A_BYTES;
+      const double* b = reinterpret_cast<const double*>(sB + st * SM::B_BYTES);
+#pragma unroll
+      for (int o = 0; o < K::BK / 8; ++o) {
+        double af[K::MT][2], bf[K::NT][2];
+#pragma unroll
+        for (int i = 0; i < K::MT; ++i) {
+          const int m = wm * K::WTM + i * 8 + pr;
+          const double2 v =
+              *reinterpret_cast<const double2*>(a + m * 128 + ((((4 * o + q) ^ (m & 7))) << 4));
+          af[i][0] = v.x;
+          af[i][1] = v.y;
+        }
+#pragma unroll
+        for (int j = 0; j < K::NT; ++j) {
+          const int n = wn * K::WTN + j * 8 + r8;
+          bf[j][0] = b[(8 * o + 2 * q) * SM::B_LD + n];
+          bf[j][1] = b[(8 * o + 2 * q + 1) * SM::B_LD + n];
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int i = 0; i < K::MT; ++i)
+#pragma unroll
+            for (int j = 0; j < K::NT; ++j) dmma884(acc[i][j], af[i][t], bf[j][t]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == STAGES) { st = 0; phase ^= 1; }
+    }
+    // epilogue (single M and N groups: C row m has stride cm_str[0], column n stride cn_str[0])
+    double* Cb = p.C + g->c_off;
+    const int M = g->M, N = g->N;
+    const int32_t cms = g->cm_str[0], cns = g->cn_str[0];
+#pragma unroll
+    for (int i = 0; i < K::MT; ++i) {
+      const int m = m0 + wm * K::WTM + i * 8 + pr;
+      if (m >= M) continue;
+#pragma unroll
+      for (int j = 0; j < K::NT; ++j) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int n = n0 + wn * K::WTN + j * 8 + 2 * q + r;
+          if (n >= N) continue;
+          double* c = Cb + (int64_t)m * cms + (int64_t)n * cns;
+          const double v = alpha * acc[i][j][r];
+          *c = (beta == 0.0) ? v : beta * *c + v;
+        }
+      }
+    }
+  }
+}
+
+template <class K>
+static cudaError_t setup_tma() {
+  return cudaFuncSetAttribute(tt_contract_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              TmaSmem<K>::BYTES);
+}
+template <class K>
+static cudaError_t launch_tma(const ContractParams& p, const CUtensorMap& a, const CUtensorMap& b, int64_t nwork,
+                              cudaStream_t s) {
+  const int64_t slots = (int64_t)p.sm_count * K::MINB;
+  const unsigned grid = (unsigned)((p.persistent && nwork > slots) ? slots : nwork);
+  ContractParams q = p;
+  q.nwork = nwork;
+  tt_contract_tma_kernel<K><<<grid, K::NTHREADS, TmaSmem<K>::BYTES, s>>>(q, a, b);
+  return cudaGetLastError();
+}
+
 template <class K, bool AKC, bool BNC, bool AV, bool BV>
 static cudaError_t setup_one() {
   return cudaFuncSetAttribute(tt_contract_ws_kernel<K, AKC, BNC, AV, BV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -400,7 +584,14 @@ static VariantInfo info_cfg(const char* name) {
 #define TT_WS_DEFINE(NAME, CFG, LABEL)                                                              \
   namespace tt {                                                                                   \
   VariantInfo ws_info_##NAME() { return ws::info_cfg<CFG>(LABEL); }                                \
-  cudaError_t ws_setup_##NAME() { return ws::setup_cfg<CFG>(); }                                  \
+  cudaError_t ws_setup_##NAME() {                                                                 \
+    cudaError_t e = ws::setup_cfg<CFG>();                                                          \
+    return e != cudaSuccess ? e : ws::setup_tma<CFG>();                                            \
+  }                                                                                                \
+  cudaError_t ws_launch_tma_##NAME(const ContractParams& p, const CUtensorMap& a, const CUtensorMap& b, \
+                                   int64_t nwork, cudaStream_t s) {                                \
+    return ws::launch_tma<CFG>(p, a, b, nwork, s);                                                 \
+  }                                                                                                \
   cudaError_t ws_launch_##NAME(bool akc, bool bnc, bool av, bool bv, const ContractParams& p,      \
                                int64_t nwork, cudaStream_t s) {                                    \
     return ws::launch_cfg<CFG>(akc, bnc, av, bv, p, nwork, s);                                     \

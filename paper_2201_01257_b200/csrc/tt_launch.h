@@ -56,6 +56,7 @@ struct ContractParams {
   int64_t nwork;          // work items (persistent kernels loop over them)
   int32_t sm_count;       // SMs of the device (persistent grid size)
   int32_t persistent;     // 1: grid = resident CTAs looping over items; 0: one CTA per item
+  int32_t tma_n;          // TMA variant: row length N of the B matrix view
 };
 
 struct VariantInfo {
@@ -74,6 +75,9 @@ VariantInfo ws_variant_info(int v);
 cudaError_t ws_variant_setup(int v);
 cudaError_t launch_contract_ws(int v, bool a_kcontig, bool b_ncontig, bool a_vec, bool b_vec,
                                const ContractParams& p, int64_t nwork, cudaStream_t s);
+// TMA producer variant of the warp-specialised family (uniform fused GEMM-shaped operands);
+// `maps` points to two CUtensorMap (A, B).
+cudaError_t launch_contract_tma(int v, const ContractParams& p, const void* maps, int64_t nwork, cudaStream_t s);
 
 // Segment-based element kernels (set / add / scalar / synthetic fill).
 struct Segment {

@@ -535,3 +535,23 @@ def _nz_elem(T, ix):
     for d, g in enumerate(T.grid):
         bid = bid * g + tiles[d]
     return np.asarray(T.nz, dtype=np.uint8)[bid]
+
+
+@pytest.mark.parametrize("variant", [3, 4, 5])
+@pytest.mark.parametrize("tv", [20, 24])
+def test_tma_producer(env, variant, tv):
+    """TMA producer (uniform fused ladder operands; tV=24 gives a ragged last M tile whose extra rows
+    read the next block): bitwise equal to the cp.async producer, and the oracle within 1e-11."""
+    tt, torch = env
+    pb = ccsd_problem(24, 4 * tv, 12, tv, True, terms=("ladder",))
+    outs = []
+    for tma in ("1", "0"):
+        os.environ["TT_TMA"] = tma
+        ctx = new_ctx(tt, torch, variant)
+        got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[0], alpha=0.5, beta=1.0, seed=8)
+        assert ctx.stats()["producer"] == (1 if tma == "1" else 0)
+        assert normwise(got, ref) <= TOL
+        outs.append(got)
+    os.environ.pop("TT_TMA", None)
+    os.environ.pop("TT_FORCE_VARIANT", None)
+    assert np.array_equal(outs[0], outs[1])
