@@ -240,10 +240,13 @@ int n_variants() { return num_contract_variants() + num_ws_variants(); }
 VariantInfo variant_info(int v) {
   return v < num_contract_variants() ? contract_variant_info(v) : ws_variant_info(v - num_contract_variants());
 }
-// DMMA-pipe efficiency of each variant on unpadded work (calibrated on cfg2, profiles/r01_variants.txt)
-double variant_efficiency(int v) {
-  static const double eff[] = {0.70, 0.81, 0.75, 0.925, 0.915, 0.95};
-  return v < (int)(sizeof(eff) / sizeof(eff[0])) ? eff[v] : 0.5;
+// DMMA-pipe efficiency of each variant on unpadded work (calibrated on cfg2, profiles/r01_variants.txt;
+// warp-specialised variants with the TMA producer where it applies)
+double variant_efficiency(int v, bool tma) {
+  static const double eff[] = {0.70, 0.81, 0.75, 0.925, 0.925, 0.947};
+  static const double eff_tma[] = {0.70, 0.81, 0.75, 0.958, 0.95, 0.952};
+  const int n = (int)(sizeof(eff) / sizeof(eff[0]));
+  return v < n ? (tma ? eff_tma[v] : eff[v]) : 0.5;
 }
 
 // tiling of universal label u
@@ -1565,6 +1568,26 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     pl.a_vec = a_last == a_grp_last && even(a_last);
     pl.b_vec = b_last == b_grp_last && even(b_last);
   }
+  // TMA producer: warp-specialised variant, single fused groups, A = [M][K] and B = [K][N] with the
+  // same K extent in every A block, the same N extent in every B block, K a multiple of 16 (no K tail)
+  {
+    const char* ft = getenv("TT_TMA");
+    const bool allow = !ft || atoi(ft) != 0;
+    if (allow && an.mg.size() == 1 && an.ng.size() == 1 &&
+        an.kg.size() == 1 && an.a_kc && an.b_nc && !ht.K.empty()) {
+      std::vector<int> ak, bn;
+      for (int u : an.kg[0]) ak.push_back(an.a_pos[u]);
+      for (int u : an.ng[0]) bn.push_back(an.b_pos[u]);
+      const int64_t K = uniform_group_extent(A, ak), N = uniform_group_extent(B, bn);
+      bool ok = K > 0 && N > 0 && K % 16 == 0 && N % 2 == 0;
+      for (int32_t k : ht.K) ok = ok && k == K;
+      if (ok) {
+        pl.tma = true;
+        pl.tma_k = K;
+        pl.tma_n = N;
+      }
+    }
+  }
   double best = -1;
   for (int v = 0; v < n_variants(); ++v) {
     VariantInfo vi = variant_info(v);
@@ -1574,7 +1597,8 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       double kst = 0;
       for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) kst += (double)((ht.K[t] + vi.bk - 1) / vi.bk);
       const int64_t nit = ((Me[i] - Mb[i] + vi.bm - 1) / vi.bm) * ((Ne[i] - Nb[i] + vi.bn - 1) / vi.bn);
-      const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm / variant_efficiency(v);
+      const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm /
+                       variant_efficiency(v, pl.tma && v >= num_contract_variants());
       for (int64_t i = 0; i < nit; ++i) items.push_back(c);
     }
     std::sort(items.begin(), items.end(), std::greater<double>());
@@ -1593,6 +1617,7 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     }
   }
   if (const char* fv = getenv("TT_FORCE_VARIANT")) pl.variant = atoi(fv) % n_variants();
+  if (pl.variant < num_contract_variants()) pl.tma = false;   // the classic family has no TMA path
   VariantInfo vi = variant_info(pl.variant);
 
   // ---- groups + work items (groups by cost desc, block id asc)
@@ -1652,26 +1677,6 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     for (const WorkItem& w : work) st_sum += groups[w.group].nstages;
     pl.persistent = !work.empty() && st_sum / (double)work.size() < 512.0;
     if (const char* fp = getenv("TT_PERSISTENT")) pl.persistent = atoi(fp) != 0;
-  }
-  // TMA producer: warp-specialised variant, single fused groups, A = [M][K] and B = [K][N] with the
-  // same K extent in every A block, the same N extent in every B block, K a multiple of 16 (no K tail)
-  {
-    const char* ft = getenv("TT_TMA");
-    const bool allow = !ft || atoi(ft) != 0;
-    if (allow && pl.variant >= num_contract_variants() && an.mg.size() == 1 && an.ng.size() == 1 &&
-        an.kg.size() == 1 && an.a_kc && an.b_nc && !ht.K.empty()) {
-      std::vector<int> ak, bn;
-      for (int u : an.kg[0]) ak.push_back(an.a_pos[u]);
-      for (int u : an.ng[0]) bn.push_back(an.b_pos[u]);
-      const int64_t K = uniform_group_extent(A, ak), N = uniform_group_extent(B, bn);
-      bool ok = K > 0 && N > 0 && K % 16 == 0 && N % 2 == 0;
-      for (int32_t k : ht.K) ok = ok && k == K;
-      if (ok) {
-        pl.tma = true;
-        pl.tma_k = K;
-        pl.tma_n = N;
-      }
-    }
   }
   TT_TRY(dev_alloc(ctx, &pl.d_groups, groups.size()));
   TT_TRY(dev_alloc(ctx, &pl.d_work, work.size()));
