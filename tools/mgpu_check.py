@@ -74,6 +74,40 @@ def main():
     if rank == 0:
         tt.add(single, P1["R"], "abij", 1.0, -0.25, P1["Rt"], "ijab")
     s_multi = tt.contract_scalar(ctx, 0.25, P["Ta"], "acik", P["R"], "acik")
+    # implicit Cholesky ladder (NEXT-1) across ranks: X replicated, R2 row-split, T gathered
+    so, sv = P["_keep"][1]["O"], P["_keep"][1]["V"]
+    sL = tt.IndexSpace(10)
+    tL = tt.TiledIndexSpace(sL, 5)
+    X = tt.Tensor(ctx, [sv, sv, tL], spin=([0], [1]))
+    X.set_owner(np.where(X.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
+    R2 = tt.Tensor(ctx, [sv, sv, so, so], spin=([0, 1], [2, 3]))
+    tt.partition_split(ctx, R2, "abij", P["Vv"], "abcd", P["T"], "cdij", group_dims=(0, 1))
+    xb = torch.empty(X.packed_elems, dtype=torch.float64, device="cuda")
+    r2b = torch.full((R2.packed_elems,), float("nan"), dtype=torch.float64, device="cuda")
+    X.bind(xb)
+    R2.bind(r2b)
+    tt.fill_synthetic(ctx, X, 3, 9)
+    tt.fill_synthetic(ctx, R2, 3, 10)
+    ws = torch.empty(P["T"].packed_elems + 32 + 40 ** 4 * 16, dtype=torch.float64, device="cuda")
+    tt.contract_cholesky(ctx, R2, "abij", 1.0, 0.5, X, "abcd", P["T"], "cdij", ws)
+    g2 = R2.download()
+    ctx.sync()
+    mine2 = np.zeros_like(g2)
+    for blk in range(R2.nblocks):
+        if not R2.nz[blk]:
+            continue
+        o = R2.blk_off[blk]
+        ext = [d.offsets[t + 1] - d.offsets[t] for d, t in zip(R2.dims, np.unravel_index(blk, R2.grid))]
+        n = int(np.prod(ext))
+        if R2.owner[blk] == rank:
+            mine2[o:o + n] = g2[o:o + n]
+        inner = n // int(ext[0])
+        for (bb, lo, hi, ow) in R2.parts:
+            if bb == blk and ow == rank:
+                mine2[o + lo * inner:o + hi * inner] = g2[o + lo * inner:o + hi * inner]
+    t2 = torch.from_numpy(mine2).cuda()
+    dist.all_reduce(t2)
+    assembled2 = t2.cpu().numpy()
     torch.cuda.synchronize()
     got = P["R"].download()
     ctx.sync()
@@ -117,6 +151,16 @@ def main():
         print(f"world {world}: normwise error vs oracle {err:.3e}; scalar multi {s_multi:.15e} single {s_single:.15e} "
               f"oracle {so:.15e}", flush=True)
         ok &= err <= 1e-11 and abs(s_multi - so) <= 1e-12 * abs(so) and abs(s_single - so) <= 1e-12 * abs(so)
+        # Cholesky term vs oracle (V formed explicitly from X, Eq. cc12)
+        from oracle import layout as Lo
+        oX = Lo.tensor_spin([orc["Vv"].dims[0], orc["Vv"].dims[0], Lo.tile_fixed(Lo.IndexSpace(10), 5)], [0], [1])
+        Xd = O.dense_masked(oX, S.dense(oX.shape, 3, 9))
+        R2d = O.dense_masked(orc["R"], S.dense(orc["R"].shape, 3, 10))
+        ref2 = O.pack(orc["R"], O.contract(R2d, "abij", O.cholesky_v(Xd), "abcd", dense["T"], "cdij", 0.5, 1.0,
+                                           cmask=m))
+        err2 = np.abs(assembled2[live] - ref2[live]).max() / np.abs(ref2[live]).max()
+        print(f"world {world}: Cholesky ladder normwise error vs oracle {err2:.3e}", flush=True)
+        ok &= err2 <= 1e-11
         print("MGPU_CHECK", "PASS" if ok else "FAIL", flush=True)
     dist.barrier()
     ctx.close()
