@@ -295,6 +295,14 @@ tt_status tt_sched_scalar(tt_sched s, double alpha, tt_tensor A, const char* a_l
 /* level[nops] of every queued op (NULL to query only), nops, number of levels. */
 tt_status tt_sched_levels(tt_sched s, int32_t* level, int64_t* nops, int32_t* nlevels);
 tt_status tt_sched_execute(tt_sched s);
+/* CUDA graph of the queue (iterative methods replay the same operations; launch-bound small problems
+ * pay one graph launch instead of per-op host work and launches): capture builds every plan first
+ * (outside the capture), then records the levels -- streams, fork/join events, NCCL calls -- into a
+ * graph; the queue is kept.  replay launches the graph on the context stream; if the queue has scalar
+ * ops their results are copied to the host pointers given at queue time (the call then synchronises).
+ * A later tt_sched_execute clears the queue and the graph. */
+tt_status tt_sched_capture(tt_sched s);
+tt_status tt_sched_replay(tt_sched s);
 tt_status tt_sched_stats(tt_sched s, int64_t* queued, int64_t* levels_executed);
 
 const char* tt_last_error(void);

@@ -98,6 +98,8 @@ _SIGS = {
     "tt_sched_scalar": [_vp, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _P(_dbl)],
     "tt_sched_levels": [_vp, _vp, _P(_i64), _P(_i32)],
     "tt_sched_execute": [_vp],
+    "tt_sched_capture": [_vp],
+    "tt_sched_replay": [_vp],
     "tt_sched_stats": [_vp, _P(_i64), _P(_i64)],
     "tt_last_error": [],
     "tt_version": [],
@@ -477,6 +479,16 @@ class Scheduler:
         self._results = []
         self._keep = []
         return out
+
+    def capture(self):
+        """Record the queue into a CUDA graph (plans are built first); the queue is kept."""
+        _check(_lib.tt_sched_capture(self.h))
+        return self
+
+    def replay(self):
+        """Launch the captured graph; returns the scalar results (in queue order)."""
+        _check(_lib.tt_sched_replay(self.h))
+        return [r.value for r in self._results]
 
     def stats(self):
         q, lv = _i64(), _i64()

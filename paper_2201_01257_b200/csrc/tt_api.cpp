@@ -1100,6 +1100,7 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
     TT_TRY(upload_elem(ctx, *ep, false));
     ctx->plans[keybuf] = ep;
   }
+  if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
   ElemParams p{};
   p.X = t->data;
@@ -1142,6 +1143,7 @@ tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha) {
     TT_TRY(upload_elem(ctx, *ep, false));
     ctx->plans[keybuf] = ep;
   }
+  if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
   ElemParams p{};
   p.X = C->data;
@@ -1224,6 +1226,7 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
     TT_TRY(upload_elem(ctx, *ep, false));
     ctx->plans[key] = ep;
   }
+  if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
   TT_TRY(run_gather(ctx, ep->gp, {A}));
   ElemParams p{};
@@ -1316,6 +1319,7 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
     TT_TRY(upload_elem(ctx, *ep, true));
     ctx->plans[key] = ep;
   }
+  if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
   TT_TRY(run_gather(ctx, ep->gp, {A, B}));
   ElemParams p{};
@@ -1327,24 +1331,25 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
   p.mode = ep->mode;
   p.tiles = ep->d_tiles;
   p.partials = ep->d_partials;
+  double* dst = ctx->scalar_dev_out ? ctx->scalar_dev_out : ctx->d_scalar;
   {
     Launch L(ctx, "tt_scalar_partials");
     TT_CUDA(launch_scalar_partials(p, ep->nwork(), ctx->stream));
   }
   {
     Launch L(ctx, "tt_scalar_final");
-    TT_CUDA(launch_scalar_final(ep->d_partials, scalar_num_partials(ep->mode, ep->nwork()), alpha, ctx->d_scalar,
-                                ctx->stream));
+    TT_CUDA(launch_scalar_final(ep->d_partials, scalar_num_partials(ep->mode, ep->nwork()), alpha, dst, ctx->stream));
   }
   if (ctx->nranks > 1) {
     const char* err = nullptr;
     const NcclApi* api = nccl_api(&err);
     if (!api) return fail(TT_E_NCCL, "%s", err);
-    TT_TRY(nccl_check(api->AllReduce(ctx->d_scalar, ctx->d_scalar, 1, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream),
-                      "ncclAllReduce"));
+    TT_TRY(nccl_check(api->AllReduce(dst, dst, 1, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream), "ncclAllReduce"));
   }
-  TT_CUDA(cudaMemcpyAsync(result, ctx->d_scalar, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  TT_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (!ctx->scalar_dev_out) {   // inside a captured graph the scheduler copies the device slot later
+    TT_CUDA(cudaMemcpyAsync(result, dst, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    TT_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   ctx->last.c_blocks = ep->blocks;
   ctx->last.bytes = ep->bytes;
   ctx->last.flops = ep->bytes / 8.0;   // one multiply-add per element pair
@@ -1755,6 +1760,7 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   bool was_cached = false;
   TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, pl, &was_cached));
   TT_TRY(need_device(ctx));
+  if (ctx->prepare_only) return TT_OK;
   TT_TRY(check_bound(C, "C"));
   TT_TRY(check_bound(A, "A"));
   TT_TRY(check_bound(B, "B"));
@@ -2234,12 +2240,21 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     TT_TRY(flush(cur));
     ctx->plans[keybuf] = cp;
   }
+  const std::string L = cp->lc;
+  const std::string x1 = std::string(1, p) + r + L, x2 = std::string(1, q) + s + L;   // W = X(prL) X(qsL)
+  if (ctx->prepare_only) {   // build every batch plan now (they are cached), launch nothing
+    for (auto& bt : cp->batches) {
+      std::shared_ptr<ContractPlan> pw, pu;
+      bool dummy;
+      TT_TRY(get_contract_plan(ctx, bt.Wb, vl, X, x1.c_str(), X, x2.c_str(), 0.0, pw, &dummy, bt.wopt));
+      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
+    }
+    return TT_OK;
+  }
   reset_stats(ctx);
   TT_TRY(run_gather(ctx, cp->bgather, {B}));
   TT_TRY(run_local_add(ctx, *cp->copy_plan, cp->Bm, B, 0.0, 1.0));
   TT_TRY(run_local_add(ctx, *cp->swap_plan, cp->Bm, B, 1.0, -1.0));
-  const std::string L = cp->lc;
-  const std::string x1 = std::string(1, p) + r + L, x2 = std::string(1, q) + s + L;   // W = X(prL) X(qsL)
   double exec = 0, build = 0;
   int64_t tasks = 0;
   for (auto& bt : cp->batches) {

@@ -169,4 +169,8 @@ struct tt_ctx_s {
   double* d_scalar = nullptr;                            // scratch for scalar results
   double* d_partials = nullptr;
   int32_t sm_count = 148;
+  // scheduler support: build plans without launching (graph capture preparation), and write scalar
+  // results to a device slot instead of the host (inside a captured graph)
+  bool prepare_only = false;
+  double* scalar_dev_out = nullptr;
 };

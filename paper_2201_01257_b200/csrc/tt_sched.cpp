@@ -56,6 +56,13 @@ struct tt_sched_s {
   std::vector<cudaEvent_t> done;   // one per stream
   cudaEvent_t fork = nullptr;
   int64_t levels_executed = 0;
+  // captured CUDA graph of the queue (tt_sched_capture / tt_sched_replay)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int32_t graph_levels = 0;
+  double* d_results = nullptr;       // device slots of the scalar ops of the graph
+  std::vector<double*> h_targets;    // their host destinations
+  std::vector<double> h_results;
 };
 
 using tt::set_error;
@@ -111,6 +118,9 @@ tt_status tt_sched_destroy(tt_sched s) {
     }
     for (cudaEvent_t e : s->done) cudaEventDestroy(e);
     if (s->fork) cudaEventDestroy(s->fork);
+    if (s->exec) cudaGraphExecDestroy(s->exec);
+    if (s->graph) cudaGraphDestroy(s->graph);
+    if (s->d_results) cudaFree(s->d_results);
     if (prev >= 0) cudaSetDevice(prev);
   }
   delete s;
@@ -230,6 +240,58 @@ static tt_status run_op(tt_ctx ctx, const SchedOp& op) {
   return set_error(TT_E_ARG, "unknown op");
 }
 
+// runs the queued ops level by level on the context stream (+ the scheduler's streams); in graph mode
+// scalar results go to device slots
+static tt_status run_levels(tt_sched s, const std::vector<int32_t>& lv, int32_t L, bool graph_mode) {
+  tt_ctx ctx = s->ctx;
+  const cudaStream_t main = ctx->stream;
+  const bool concurrent = ctx->nranks == 1 && s->streams.size() > 1;
+  tt_status st = TT_OK;
+  std::vector<int> slot(s->ops.size(), -1);
+  int ns = 0;
+  for (size_t i = 0; i < s->ops.size(); ++i)
+    if (s->ops[i].kind == kScalar) slot[i] = ns++;
+  auto one = [&](size_t i) {
+    ctx->scalar_dev_out = (graph_mode && slot[i] >= 0) ? s->d_results + slot[i] : nullptr;
+    tt_status r = run_op(ctx, s->ops[i]);
+    ctx->scalar_dev_out = nullptr;
+    return r;
+  };
+  for (int32_t l = 0; l < L && st == TT_OK; ++l) {
+    std::vector<size_t> ids;
+    for (size_t i = 0; i < s->ops.size(); ++i)
+      if (lv[i] == l) ids.push_back(i);
+    if (!concurrent || ids.size() == 1) {
+      for (size_t i : ids)
+        if ((st = one(i)) != TT_OK) break;
+    } else {
+      // fork: every stream used by the level waits for the work queued so far on the main stream
+      cudaEventRecord(s->fork, main);
+      const size_t used = std::min(ids.size(), s->streams.size());
+      for (size_t k = 0; k < used; ++k) cudaStreamWaitEvent(s->streams[k], s->fork, 0);
+      for (size_t k = 0; k < ids.size() && st == TT_OK; ++k) {
+        ctx->stream = s->streams[k % used];
+        st = one(ids[k]);
+      }
+      ctx->stream = main;
+      // join: the main stream waits for every stream of the level
+      for (size_t k = 0; k < used; ++k) {
+        cudaEventRecord(s->done[k], s->streams[k]);
+        cudaStreamWaitEvent(main, s->done[k], 0);
+      }
+    }
+  }
+  ctx->stream = main;
+  return st;
+}
+
+static void drop_graph(tt_sched s) {
+  if (s->exec) cudaGraphExecDestroy(s->exec);
+  if (s->graph) cudaGraphDestroy(s->graph);
+  s->exec = nullptr;
+  s->graph = nullptr;
+}
+
 tt_status tt_sched_execute(tt_sched s) {
   if (!s) return set_error(TT_E_ARG, "NULL scheduler");
   tt_ctx ctx = s->ctx;
@@ -239,39 +301,88 @@ tt_status tt_sched_execute(tt_sched s) {
   std::vector<int32_t> lv(s->ops.size());
   tt_status st = tt_sched_levels(s, lv.data(), &n, &L);
   if (st != TT_OK) return st;
-  const cudaStream_t main = ctx->stream;
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(ctx->device);
-  const bool concurrent = ctx->nranks == 1 && s->streams.size() > 1;
-  for (int32_t l = 0; l < L && st == TT_OK; ++l) {
-    std::vector<size_t> ids;
-    for (size_t i = 0; i < s->ops.size(); ++i)
-      if (lv[i] == l) ids.push_back(i);
-    if (!concurrent || ids.size() == 1) {
-      for (size_t i : ids)
-        if ((st = run_op(ctx, s->ops[i])) != TT_OK) break;
-    } else {
-      // fork: every stream used by the level waits for the work queued so far on the main stream
-      cudaEventRecord(s->fork, main);
-      const size_t used = std::min(ids.size(), s->streams.size());
-      for (size_t k = 0; k < used; ++k) cudaStreamWaitEvent(s->streams[k], s->fork, 0);
-      for (size_t k = 0; k < ids.size() && st == TT_OK; ++k) {
-        ctx->stream = s->streams[k % used];
-        st = run_op(ctx, s->ops[ids[k]]);
-      }
-      ctx->stream = main;
-      // join: the main stream waits for every stream of the level
-      for (size_t k = 0; k < used; ++k) {
-        cudaEventRecord(s->done[k], s->streams[k]);
-        cudaStreamWaitEvent(main, s->done[k], 0);
-      }
-    }
-    s->levels_executed++;
-  }
-  ctx->stream = main;
+  st = run_levels(s, lv, L, false);
+  if (st == TT_OK) s->levels_executed += L;
   if (prev >= 0) cudaSetDevice(prev);
   s->ops.clear();
+  drop_graph(s);
+  return st;
+}
+
+tt_status tt_sched_capture(tt_sched s) {
+  if (!s) return set_error(TT_E_ARG, "NULL scheduler");
+  tt_ctx ctx = s->ctx;
+  if (ctx->device < 0) return set_error(TT_E_STATE, "host-only context cannot capture");
+  int64_t n;
+  int32_t L;
+  std::vector<int32_t> lv(s->ops.size());
+  tt_status st = tt_sched_levels(s, lv.data(), &n, &L);
+  if (st != TT_OK) return st;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ctx->device);
+  drop_graph(s);
+  // 1. build every plan (host work, uploads, device task builders) outside the capture
+  ctx->prepare_only = true;
+  for (const SchedOp& op : s->ops)
+    if ((st = run_op(ctx, op)) != TT_OK) break;
+  ctx->prepare_only = false;
+  // 2. device slots for the scalar results
+  s->h_targets.clear();
+  for (const SchedOp& op : s->ops)
+    if (op.kind == kScalar) s->h_targets.push_back(op.result);
+  s->h_results.assign(s->h_targets.size(), 0.0);
+  if (st == TT_OK && s->d_results) { cudaFree(s->d_results); s->d_results = nullptr; }
+  if (st == TT_OK && !s->h_targets.empty() &&
+      cudaMalloc(&s->d_results, s->h_targets.size() * sizeof(double)) != cudaSuccess)
+    st = set_error(TT_E_OOM, "cannot allocate scalar result slots");
+  // 3. record the levels into a CUDA graph (profiling events off while capturing)
+  if (st == TT_OK) {
+    const bool prof = ctx->profiling;
+    ctx->profiling = false;
+    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+    tt_status rs = TT_OK;
+    if (st == TT_OK) rs = run_levels(s, lv, L, true);
+    if (st == TT_OK) {
+      e = cudaStreamEndCapture(ctx->stream, &s->graph);
+      if (rs != TT_OK) st = rs;
+      else if (e != cudaSuccess) st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+      else if ((e = cudaGraphInstantiate(&s->exec, s->graph, 0)) != cudaSuccess)
+        st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+    }
+    ctx->profiling = prof;
+    s->graph_levels = L;
+  }
+  if (st != TT_OK) drop_graph(s);
+  if (prev >= 0) cudaSetDevice(prev);
+  return st;
+}
+
+tt_status tt_sched_replay(tt_sched s) {
+  if (!s) return set_error(TT_E_ARG, "NULL scheduler");
+  if (!s->exec) return set_error(TT_E_STATE, "no captured graph (call tt_sched_capture)");
+  tt_ctx ctx = s->ctx;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ctx->device);
+  tt_status st = TT_OK;
+  cudaError_t e = cudaGraphLaunch(s->exec, ctx->stream);
+  ctx->launches += 1;
+  if (e != cudaSuccess) st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+  if (st == TT_OK && !s->h_targets.empty()) {
+    e = cudaMemcpyAsync(s->h_results.data(), s->d_results, s->h_results.size() * sizeof(double),
+                        cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+    else
+      for (size_t i = 0; i < s->h_targets.size(); ++i) *s->h_targets[i] = s->h_results[i];
+  }
+  if (st == TT_OK) s->levels_executed += s->graph_levels;
+  if (prev >= 0) cudaSetDevice(prev);
   return st;
 }
 

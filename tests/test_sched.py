@@ -161,3 +161,43 @@ def test_sched_matches_sequential_bitwise():
     ref = O.pack(orc["R"], R)
     assert np.abs(a[0] - ref).max() / np.abs(ref).max() <= 1e-11
     assert abs(ra[0] - E) <= 1e-12 * abs(E)
+
+
+@pytest.mark.gpu
+def test_sched_graph_replay_bitwise():
+    """CUDA-graph capture of a queue (plans built first, levels with forked streams recorded) and two
+    replays == running the same program twice with immediate calls, bitwise; scalar results too."""
+    import torch
+    pb = ccsd_problem(8, 12, 2, 3, True)
+    pb.tensors["R2"] = TensorSpec("abij", ("spin", [0, 1], [2, 3]))
+    stream = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for mode in ("graph", "seq"):
+        ctx = tt.Context(device=0, stream=stream)
+        orc = oracle_objects(pb)
+        P = product_objects(tt, ctx, pb)
+        bufs = []
+        for i, name in enumerate(sorted(pb.tensors)):
+            b = torch.from_numpy(O.pack(orc[name], O.dense_masked(orc[name], S.dense(orc[name].shape, 6, i + 1)))).cuda()
+            P[name].bind(b)
+            bufs.append(b)
+        res = []
+        if mode == "graph":
+            s = tt.Scheduler(ctx, nstreams=2)
+            s.contract(P["R"], "abij", 1.0, 0.5, P["Vv"], "abcd", P["T"], "cdij")
+            s.contract(P["R2"], "abij", 0.0, 1.0, P["Ta"], "acik", P["Wr"], "cbkj")
+            s.add(P["R"], "abij", 1.0, -1.0, P["R2"], "baji")
+            s.scalar(0.25, P["R"], "abij", P["T"], "abij".replace("ab", "ab"))
+            s.capture()
+            for _ in range(2):
+                res += s.replay()
+        else:
+            for _ in range(2):
+                tt.contract(ctx, P["R"], "abij", 1.0, 0.5, P["Vv"], "abcd", P["T"], "cdij")
+                tt.contract(ctx, P["R2"], "abij", 0.0, 1.0, P["Ta"], "acik", P["Wr"], "cbkj")
+                tt.add(ctx, P["R"], "abij", 1.0, -1.0, P["R2"], "baji")
+                res.append(tt.contract_scalar(ctx, 0.25, P["R"], "abij", P["T"], "abij"))
+        outs.append((P["R"].download(), P["R2"].download(), res))
+        ctx.sync()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
