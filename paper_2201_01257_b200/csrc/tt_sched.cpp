@@ -57,6 +57,7 @@ struct tt_sched_s {
   cudaEvent_t fork = nullptr;
   int64_t levels_executed = 0;
   // captured CUDA graph of the queue (tt_sched_capture / tt_sched_replay)
+  cudaStream_t cap = nullptr;        // capture stream (the context stream may be the legacy stream)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int32_t graph_levels = 0;
@@ -85,7 +86,8 @@ tt_status tt_sched_create(tt_ctx ctx, int32_t nstreams, tt_sched* out) {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
-    bool ok = cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) == cudaSuccess;
+    bool ok = cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking) == cudaSuccess;
     for (int i = 0; ok && i < nstreams; ++i) {
       cudaStream_t st;
       cudaEvent_t ev;
@@ -118,6 +120,7 @@ tt_status tt_sched_destroy(tt_sched s) {
     }
     for (cudaEvent_t e : s->done) cudaEventDestroy(e);
     if (s->fork) cudaEventDestroy(s->fork);
+    if (s->cap) cudaStreamDestroy(s->cap);
     if (s->exec) cudaGraphExecDestroy(s->exec);
     if (s->graph) cudaGraphDestroy(s->graph);
     if (s->d_results) cudaFree(s->d_results);
@@ -343,17 +346,21 @@ tt_status tt_sched_capture(tt_sched s) {
   if (st == TT_OK) {
     const bool prof = ctx->profiling;
     ctx->profiling = false;
-    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
-    if (e != cudaSuccess) st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+    const cudaStream_t user = ctx->stream;
+    ctx->stream = s->cap;          // record on the scheduler's capture stream; replay on the context stream
+    cudaError_t e = cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) st = set_error(TT_E_CUDA, (std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e)).c_str());
     tt_status rs = TT_OK;
     if (st == TT_OK) rs = run_levels(s, lv, L, true);
     if (st == TT_OK) {
-      e = cudaStreamEndCapture(ctx->stream, &s->graph);
+      e = cudaStreamEndCapture(s->cap, &s->graph);
       if (rs != TT_OK) st = rs;
-      else if (e != cudaSuccess) st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+      else if (e != cudaSuccess)
+        st = set_error(TT_E_CUDA, (std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e)).c_str());
       else if ((e = cudaGraphInstantiate(&s->exec, s->graph, 0)) != cudaSuccess)
-        st = set_error(TT_E_CUDA, cudaGetErrorString(e));
+        st = set_error(TT_E_CUDA, (std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e)).c_str());
     }
+    ctx->stream = user;
     ctx->profiling = prof;
     s->graph_levels = L;
   }
