@@ -1,0 +1,141 @@
+"""Synthetic CCSD-shaped iteration driver (BASELINE configs[3]).
+
+The paper does not list the CCSD equations (P283-293; reading R18), so this is a frozen, CCSD-shaped
+term list in the style of spin-orbital CCSD with tau-based ladder and Stanton-Gauss-like
+intermediates (Fvv, Foo, Fov, Woooo, Wovvo): every term is a labelled set / add / contraction of the
+library, the n_o^2 n_u^4 ladder uses the implicit Cholesky-factored V (Eq. cc12), and the energy is an
+order-0 contraction summed over ranks.  Inputs are seeded synthetic tensors (no molecule, no
+convergence): one call = one residual evaluation + energy.  All operations are queued in a
+Scheduler (P178/P191-199/P215) and executed level by level.
+
+Index classes: 'o' (occupied, spin halves), 'v' (virtual, spin halves), 'L' (Cholesky auxiliary).
+"""
+from __future__ import annotations
+
+from typing import Dict, Optional
+
+import numpy as np
+
+# name -> (index classes per dim, spin split (upper dims, lower dims), synthetic input tag or None)
+TENSORS = {
+    "foo": ("oo", ([0], [1]), 11),
+    "fvv": ("vv", ([0], [1]), 12),
+    "T1": ("vo", ([0], [1]), 13),
+    "T2": ("vvoo", ([0, 1], [2, 3]), 14),
+    "Voovv": ("vvoo", ([0, 1], [2, 3]), 15),
+    "Voooo": ("oooo", ([0, 1], [2, 3]), 16),
+    "Wr": ("ovvo", ([0, 1], [2, 3]), 17),
+    "X": ("vvL", ([0], [1]), 18),
+    "tau": ("vvoo", ([0, 1], [2, 3]), None),
+    "Wo": ("oooo", ([0, 1], [2, 3]), None),
+    "Fv": ("vv", ([0], [1]), None),
+    "Fo": ("oo", ([0], [1]), None),
+    "Fov": ("ov", ([0], [1]), None),
+    "Z": ("vvoo", ([0, 1], [2, 3]), None),
+    "R2": ("vvoo", ([0, 1], [2, 3]), None),
+    "R1": ("vo", ([0], [1]), None),
+}
+
+# (kind, out, out labels, beta, alpha, in1, labels1, in2, labels2)
+TERMS = [
+    ("add", "tau", "abij", 0.0, 1.0, "T2", "abij"),
+    ("contract", "tau", "abij", 1.0, 1.0, "T1", "ai", "T1", "bj"),
+    ("contract", "tau", "abij", 1.0, -1.0, "T1", "bi", "T1", "aj"),
+    ("add", "Wo", "klij", 0.0, 1.0, "Voooo", "klij"),
+    ("contract", "Wo", "klij", 1.0, 0.25, "Voovv", "cdkl", "tau", "cdij"),
+    ("contract", "Wr", "kbcj", 1.0, -0.5, "T2", "dblj", "Voovv", "cdkl"),
+    ("add", "Fv", "ae", 0.0, 1.0, "fvv", "ae"),
+    ("contract", "Fv", "ae", 1.0, -0.5, "T2", "afmn", "Voovv", "efmn"),
+    ("add", "Fo", "mi", 0.0, 1.0, "foo", "mi"),
+    ("contract", "Fo", "mi", 1.0, 0.5, "Voovv", "efmn", "T2", "efin"),
+    ("contract", "Fov", "me", 0.0, 1.0, "Voovv", "efmn", "T1", "fn"),
+    ("add", "R2", "abij", 0.0, 1.0, "Voovv", "abij"),
+    ("cholesky", "R2", "abij", 1.0, 0.5, "X", "abcd", "tau", "cdij"),
+    ("contract", "R2", "abij", 1.0, 0.5, "tau", "abkl", "Wo", "klij"),
+    ("contract", "Z", "abij", 0.0, 1.0, "T2", "acik", "Wr", "kbcj"),
+    ("add", "R2", "abij", 1.0, 1.0, "Z", "abij"),
+    ("add", "R2", "abij", 1.0, -1.0, "Z", "baij"),
+    ("add", "R2", "abij", 1.0, -1.0, "Z", "abji"),
+    ("add", "R2", "abij", 1.0, 1.0, "Z", "baji"),
+    ("contract", "Z", "abij", 0.0, 1.0, "T2", "aeij", "Fv", "be"),
+    ("add", "R2", "abij", 1.0, 1.0, "Z", "abij"),
+    ("add", "R2", "abij", 1.0, -1.0, "Z", "baij"),
+    ("contract", "Z", "abij", 0.0, 1.0, "T2", "abim", "Fo", "mj"),
+    ("add", "R2", "abij", 1.0, -1.0, "Z", "abij"),
+    ("add", "R2", "abij", 1.0, 1.0, "Z", "abji"),
+    ("contract", "R1", "ai", 0.0, 1.0, "Fv", "ae", "T1", "ei"),
+    ("contract", "R1", "ai", 1.0, -1.0, "T1", "am", "Fo", "mi"),
+    ("contract", "R1", "ai", 1.0, 1.0, "T2", "aeim", "Fov", "me"),
+    ("scalar", "E", "", 0.0, 0.25, "Voovv", "abij", "tau", "abij"),
+]
+
+
+class CCSDIteration:
+    """Builds the tensors of the iteration on a libtt context and runs it through a Scheduler.
+
+    O, V: occupied / virtual spin-orbital counts (even; alpha then beta halves, R6); tO, tV, tL:
+    tile sizes; NL: Cholesky auxiliary extent.  Device buffers are torch tensors (plumbing)."""
+
+    def __init__(self, tt, ctx, O: int, V: int, tO: int, tV: int, NL: int, tL: int, seed: int = 1,
+                 ws_gb: float = 4.0, nstreams: int = 4, distribute: bool = True):
+        import torch
+        self.tt, self.ctx, self.seed = tt, ctx, seed
+        so = tt.IndexSpace(O, [(0, O // 2), (O // 2, O)], [1, -1])
+        sv = tt.IndexSpace(V, [(0, V // 2), (V // 2, V)], [1, -1])
+        sl = tt.IndexSpace(NL)
+        self.spaces = (so, sv, sl)
+        self.tis = {"o": tt.TiledIndexSpace(so, tO), "v": tt.TiledIndexSpace(sv, tV), "L": tt.TiledIndexSpace(sl, tL)}
+        self.T: Dict[str, object] = {}
+        for name, (cls, (up, lo), tag) in TENSORS.items():
+            self.T[name] = tt.Tensor(ctx, [self.tis[c] for c in cls], spin=(up, lo))
+        if ctx.nranks > 1 and distribute:
+            self._distribute()
+        self.bufs = {}
+        for name, T in self.T.items():
+            self.bufs[name] = torch.zeros(T.packed_elems, dtype=torch.float64, device="cuda")
+            T.bind(self.bufs[name])
+        ws = self.T["T2"].packed_elems + 64 + int(ws_gb * 1e9 / 8)
+        self.ws = torch.empty(ws, dtype=torch.float64, device="cuda")
+        self.nstreams = nstreams
+        self.reset_inputs()
+
+    def _distribute(self):
+        """Owner-computes placement: the doubles residual R2 by (a,b) rows with the balanced row-
+        splitting partition; small tensors and the Cholesky vectors replicated; the rest round robin."""
+        tt, T = self.tt, self.T
+        tt.partition_split(self.ctx, T["R2"], "abij", T["tau"], "abkl", T["Wo"], "klij", group_dims=(0, 1))
+        for name in ("foo", "fvv", "T1", "Fv", "Fo", "Fov", "R1", "X", "Wo", "Voooo"):
+            t = T[name]
+            t.set_owner(np.where(t.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
+
+    def reset_inputs(self):
+        for name, (cls, spin, tag) in TENSORS.items():
+            if tag is not None:
+                self.tt.fill_synthetic(self.ctx, self.T[name], self.seed, tag)
+
+    def queue(self, sched):
+        T = self.T
+        for term in TERMS:
+            kind = term[0]
+            if kind == "add":
+                _, out, ol, beta, alpha, a, al = term
+                sched.add(T[out], ol, beta, alpha, T[a], al)
+            elif kind == "contract":
+                _, out, ol, beta, alpha, a, al, b, bl = term
+                sched.contract(T[out], ol, beta, alpha, T[a], al, T[b], bl)
+            elif kind == "cholesky":
+                _, out, ol, beta, alpha, x, vl, b, bl = term
+                sched.contract_cholesky(T[out], ol, beta, alpha, T[x], vl, T[b], bl, self.ws)
+            else:
+                _, out, ol, beta, alpha, a, al, b, bl = term
+                sched.scalar(alpha, T[a], al, T[b], bl)
+        return sched
+
+    def run(self):
+        """One residual evaluation; returns (levels, energy)."""
+        s = self.tt.Scheduler(self.ctx, nstreams=self.nstreams)
+        self.queue(s)
+        _, nlev = s.levels()
+        res = s.execute()
+        s.close()
+        return nlev, res[0]
