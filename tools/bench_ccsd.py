@@ -1,0 +1,114 @@
+"""Synthetic CCSD-shaped iteration at BASELINE configs[3] scale (O=100 V=800 tile 50, alpha/beta maps,
+N_L = 2(O+V) = 1800, implicit Cholesky V) on 1..N GPUs (torchrun for N > 1).
+
+    python tools/bench_ccsd.py [--O 100 --V 800 --tile 50 --nl 1800 --ltile 450 --ws-gb 12]
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/bench_ccsd.py
+
+One step = one residual evaluation (29 queued operations, levelized by the scheduler) + the energy
+all-reduce.  Reports the step time (max over ranks), the algorithmic FLOPs of all terms (task-list
+costs over the tensors' block maps; the ladder over the block map of the implicit V) and the rate."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2201_01257_b200 as tt  # noqa: E402
+from paper_2201_01257_b200.ccsd import TERMS, CCSDIteration  # noqa: E402
+
+
+def algorithmic_flops(it):
+    T = it.T
+    total, parts = 0.0, {}
+    ctx0 = tt.Context(device=-1)       # host-only planning context for the FLOP counts
+    for term in TERMS:
+        if term[0] == "contract":
+            _, out, ol, beta, alpha, a, al, b, bl = term
+            f = float(tt.task_list(ctx0, T[out], ol, T[a], al, T[b], bl)["cost"].sum())
+        elif term[0] == "cholesky":
+            _, out, ol, beta, alpha, x, vl, b, bl = term
+            tv = it.tis["v"]
+            # block map of the implicit V: Coulomb or exchange term conserves spin pairwise (R19b)
+            sp = tv.spin
+            n = tv.ntiles
+            nz = np.zeros((n, n, n, n), np.uint8)
+            for p in range(n):
+                for q in range(n):
+                    for r in range(n):
+                        for s in range(n):
+                            nz[p, q, r, s] = (sp[p] == sp[r] and sp[q] == sp[s]) or (sp[p] == sp[s] and sp[q] == sp[r])
+            V = tt.Tensor(ctx0, [tv, tv, tv, tv], nz=nz.reshape(-1))
+            f = float(tt.task_list(ctx0, T[out], ol, V, vl, T[b], bl)["cost"].sum())
+        else:
+            continue
+        parts[f"{term[1]}({term[2]})+={term[5]}*{term[7]}"] = f
+        total += f
+    return total, parts
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--O", type=int, default=100)
+    ap.add_argument("--V", type=int, default=800)
+    ap.add_argument("--tile", type=int, default=50)
+    ap.add_argument("--nl", type=int, default=1800)
+    ap.add_argument("--ltile", type=int, default=450)
+    ap.add_argument("--ws-gb", type=float, default=12.0)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=1)
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    nid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [tt.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    stream = torch.cuda.current_stream()
+    ctx = tt.Context(device=local, stream=stream.cuda_stream, rank=rank, nranks=world, nccl_id=nid)
+    t0 = time.time()
+    it = CCSDIteration(tt, ctx, a.O, a.V, a.tile, a.tile, a.nl, a.ltile, seed=1, ws_gb=a.ws_gb, nstreams=4)
+    setup_s = time.time() - t0
+    for _ in range(a.warmup):
+        it.run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    levels, E = 0, 0.0
+    for _ in range(a.steps):
+        levels, E = it.run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    if rank == 0:
+        flops, parts = algorithmic_flops(it)
+        mem = {n: T.packed_elems * 8e-9 for n, T in it.T.items()}
+        print(json.dumps({"workload": f"synthetic CCSD-shaped iteration O={a.O} V={a.V} tile={a.tile} N_L={a.nl}, "
+                                      f"alpha/beta maps, implicit Cholesky V", "n_gpus": world,
+                          "ms_per_iteration": ms, "levels": levels, "energy": E, "algorithmic_flops": flops,
+                          "gflops": flops / (ms * 1e-3) / 1e9, "pct_fp64_peak": flops / (ms * 1e-3) / 1e12 / 37.1 / world * 100,
+                          "flops_by_term": parts, "setup_s": setup_s,
+                          "tensor_gb": round(sum(mem.values()), 1), "workspace_gb": a.ws_gb}), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
