@@ -103,7 +103,20 @@ class CCSDIteration:
         """Owner-computes placement: the doubles residual R2 by (a,b) rows with the balanced row-
         splitting partition; small tensors and the Cholesky vectors replicated; the rest round robin."""
         tt, T = self.tt, self.T
-        tt.partition_split(self.ctx, T["R2"], "abij", T["tau"], "abkl", T["Wo"], "klij", group_dims=(0, 1))
+        # R2 rows balanced on the dominant term, the ladder over the block map of the implicit V
+        tv = self.tis["v"]
+        sp, n = tv.spin, tv.ntiles
+        nz = np.zeros((n, n, n, n), np.uint8)
+        for p in range(n):
+            for q in range(n):
+                for r in range(n):
+                    for s in range(n):
+                        nz[p, q, r, s] = (sp[p] == sp[r] and sp[q] == sp[s]) or (sp[p] == sp[s] and sp[q] == sp[r])
+        self.Vmeta = tt.Tensor(self.ctx, [tv, tv, tv, tv], nz=nz.reshape(-1))
+        tt.partition_split(self.ctx, T["R2"], "abij", self.Vmeta, "abcd", T["tau"], "cdij", group_dims=(0, 1))
+        # the ring intermediates balanced on their own costs
+        tt.partition_split(self.ctx, T["Z"], "abij", T["T2"], "acik", T["Wr"], "kbcj")
+        tt.partition_split(self.ctx, T["Wr"], "kbcj", T["T2"], "dblj", T["Voovv"], "cdkl")
         for name in ("foo", "fvv", "T1", "Fv", "Fo", "Fov", "R1", "X", "Wo", "Voooo"):
             t = T[name]
             t.set_owner(np.where(t.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))

@@ -85,6 +85,8 @@ def main():
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.set_profiling(True)
+    ctx.profile_reset()
     e0.record(stream)
     levels, E = 0, 0.0
     for _ in range(a.steps):
@@ -96,6 +98,16 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
+    kernels = {}
+    for name in ["tt_contract_dmma[abij=abcd*cdij]", "tt_contract_dmma[abcd=", "tt_contract_dmma[kbcj=",
+                 "tt_contract_dmma[abij=acik", "tt_contract_dmma[abij=abkl", "tt_contract_dmma[klij=",
+                 "tt_contract_dmma", "tt_add", "tt_scalar", "tt_set"]:
+        kms, kn = ctx.profile(name)
+        kernels[name] = round(kms / a.steps, 2)
+    ctx.set_profiling(False)
+    kt = torch.tensor([kernels["tt_contract_dmma"]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
     if rank == 0:
         flops, parts = algorithmic_flops(it)
         mem = {n: T.packed_elems * 8e-9 for n, T in it.T.items()}
@@ -103,7 +115,8 @@ def main():
                                       f"alpha/beta maps, implicit Cholesky V", "n_gpus": world,
                           "ms_per_iteration": ms, "levels": levels, "energy": E, "algorithmic_flops": flops,
                           "gflops": flops / (ms * 1e-3) / 1e9, "pct_fp64_peak": flops / (ms * 1e-3) / 1e12 / 37.1 / world * 100,
-                          "flops_by_term": parts, "setup_s": setup_s,
+                          "flops_by_term": parts, "setup_s": setup_s, "kernel_ms_rank0": kernels,
+                          "max_rank_contract_kernel_ms": float(kt[0]),
                           "tensor_gb": round(sum(mem.values()), 1), "workspace_gb": a.ws_gb}), flush=True)
     ctx.close()
     if world > 1:
