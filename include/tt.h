@@ -261,6 +261,13 @@ tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor
 tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor A, const char* a_lbl,
                              tt_tensor B, const char* b_lbl, uint32_t group_mask);
 
+/* As tt_partition_split with caller-supplied costs instead of a contraction's task list, for
+ * operations whose work is not one contraction's (e.g. the implicit Cholesky evaluation, whose
+ * work per row is its W formation plus the GEMMs over W's block map, reading R19b).
+ *   cost  [number of non-zero C blocks] non-negative cost of each non-zero C block, in block-id
+ *         order (host pointer, read only).  TT_E_ARG on NULL or a negative cost. */
+tt_status tt_partition_split_cost(tt_ctx ctx, tt_tensor C, const int64_t* cost, uint32_t group_mask);
+
 /* Input-tile gather plan of this rank for tt_contract (host metadata; for tests and reports).
  * recv[5*i .. 5*i+4] = (operand 0=A/1=B, block id, source rank, e0, e1): element range [e0, e1) of
  * the block this rank receives (whole blocks, or rows of row-split parts);

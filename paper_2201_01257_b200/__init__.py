@@ -86,6 +86,7 @@ _SIGS = {
                      _vp, _vp, _i64, _P(_i64), _P(_i64)],
     "tt_partition_lpt": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32, _vp],
     "tt_partition_split": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32],
+    "tt_partition_split_cost": [_vp, _vp, _vp, _u32],
     "tt_gather_plan": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _P(_i64), _vp,
                        _P(_i64), _i64],
     "tt_sched_create": [_vp, _i32, _P(_vp)],
@@ -399,6 +400,16 @@ def partition_split(ctx: Context, C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, 
     """Balanced partition with row splitting (tt_partition_split); updates C's ownership in place."""
     mask = sum(1 << d for d in group_dims)
     _check(_lib.tt_partition_split(ctx.h, C.h, _b(c_lbl), A.h, _b(a_lbl), B.h, _b(b_lbl), mask))
+    C._refresh()
+
+
+def partition_split_cost(ctx: Context, C: Tensor, cost, group_dims: Sequence[int] = ()):
+    """tt_partition_split with caller-supplied costs (one per non-zero C block, block-id order)."""
+    c = np.ascontiguousarray(cost, dtype=np.int64)
+    if c.shape != (int((C.nz > 0).sum()),):
+        raise ValueError("cost needs one entry per non-zero block of C")
+    mask = sum(1 << d for d in group_dims)
+    _check(_lib.tt_partition_split_cost(ctx.h, C.h, _ptr(c), mask))
     C._refresh()
 
 

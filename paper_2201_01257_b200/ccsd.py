@@ -100,26 +100,48 @@ class CCSDIteration:
         self.reset_inputs()
 
     def _distribute(self):
-        """Owner-computes placement: the doubles residual R2 by (a,b) rows with the balanced row-
-        splitting partition; small tensors and the Cholesky vectors replicated; the rest round robin."""
+        """Owner-computes placement (P178-180, reading R24b).  T2, Voovv and tau are read whole by
+        most terms, so they are replicated (inputs filled on every rank; tau recomputed redundantly:
+        O(o^2 v^2) work) -- with 180 GB per GPU this trades memory for gathers of these tensors in every
+        contraction.  The expensive outputs are split with the row-splitting water-filling partition:
+        R2 by (a,b) rows on the cost of the implicit Cholesky ladder as executed (W formation + the
+        GEMMs over W's Coulomb block map, R19b), Wr / Z / Wo / Fv on their own task-list costs; the
+        small ones (foo, fvv, T1, Fo, Fov, R1, X, Voooo) are replicated."""
         tt, T = self.tt, self.T
-        # R2 rows balanced on the dominant term, the ladder over the block map of the implicit V
-        tv = self.tis["v"]
-        sp, n = tv.spin, tv.ntiles
-        nz = np.zeros((n, n, n, n), np.uint8)
-        for p in range(n):
-            for q in range(n):
-                for r in range(n):
-                    for s in range(n):
-                        nz[p, q, r, s] = (sp[p] == sp[r] and sp[q] == sp[s]) or (sp[p] == sp[s] and sp[q] == sp[r])
-        self.Vmeta = tt.Tensor(self.ctx, [tv, tv, tv, tv], nz=nz.reshape(-1))
-        tt.partition_split(self.ctx, T["R2"], "abij", self.Vmeta, "abcd", T["tau"], "cdij", group_dims=(0, 1))
-        # the ring intermediates balanced on their own costs
-        tt.partition_split(self.ctx, T["Z"], "abij", T["T2"], "acik", T["Wr"], "kbcj")
-        tt.partition_split(self.ctx, T["Wr"], "kbcj", T["T2"], "dblj", T["Voovv"], "cdkl")
-        for name in ("foo", "fvv", "T1", "Fv", "Fo", "Fov", "R1", "X", "Wo", "Voooo"):
+        for name in ("foo", "fvv", "T1", "T2", "Voovv", "tau", "Fo", "Fov", "R1", "X", "Voooo"):
             t = T[name]
             t.set_owner(np.where(t.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
+        tt.partition_split_cost(self.ctx, T["R2"], self.ladder_costs(), group_dims=(0, 1))
+        tt.partition_split(self.ctx, T["Wr"], "kbcj", T["T2"], "dblj", T["Voovv"], "cdkl")
+        tt.partition_split(self.ctx, T["Z"], "abij", T["T2"], "acik", T["Wr"], "kbcj")
+        tt.partition_split(self.ctx, T["Wo"], "klij", T["Voovv"], "cdkl", T["tau"], "cdij")
+        tt.partition_split(self.ctx, T["Fv"], "ae", T["T2"], "afmn", T["Voovv"], "efmn")
+
+    def ladder_costs(self) -> np.ndarray:
+        """Executed cost of R2(abij) += V(abcd) tau(cdij) per non-zero R2 block with the implicit V
+        (tt_contract_cholesky): the GEMMs over W's block map (W(pqrs) = sum_L X(prL) X(qsL) is non-zero
+        when spin p = spin r and spin q = spin s) against tau, plus the W formation of the (a,b) row
+        (2 N_L |a||b| sum_{c,d in W's map} |c||d|), shared evenly by the row's blocks."""
+        tt, T = self.tt, self.T
+        tv, NL = self.tis["v"], self.spaces[2].extent
+        sp, n = tv.spin, tv.ntiles
+        sz = np.diff(tv.offsets)
+        wnz = (sp[:, None, None, None] == sp[None, None, :, None]) & (sp[None, :, None, None] == sp[None, None, None, :])
+        ctx0 = tt.Context(device=-1)
+        W = tt.Tensor(ctx0, [tv, tv, tv, tv], nz=wnz.astype(np.uint8).reshape(-1))
+        tl = tt.task_list(ctx0, T["R2"], "abij", W, "abcd", T["tau"], "cdij")
+        cost = tl["cost"].astype(np.int64)
+        R2 = T["R2"]
+        g = R2.grid
+        coords = np.stack(np.unravel_index(tl["cblk"], g), axis=1)
+        # W formation per (a,b) row: 2 N_L |a| |b| sum_{(c,d) in W's map} |c| |d|
+        wsum = np.einsum("abcd,c,d->ab", wnz.astype(np.int64), sz, sz)
+        build = 2 * NL * sz[:, None] * sz[None, :] * wsum
+        ab = coords[:, 0] * n + coords[:, 1]
+        cnt = np.bincount(ab, minlength=n * n)
+        share = build.reshape(-1) // np.maximum(cnt, 1)
+        cost += share[ab]
+        return cost
 
     def reset_inputs(self):
         for name, (cls, spin, tag) in TENSORS.items():

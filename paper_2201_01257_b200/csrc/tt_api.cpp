@@ -1857,23 +1857,20 @@ tt_status tt_partition_lpt(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A,
   return TT_OK;
 }
 
-tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
-                             const char* bl, uint32_t group_mask) {
-  if (!ctx) return fail(TT_E_ARG, "NULL context");
-  Analysis an;
-  TT_TRY(analyse(C, cl, A, al, B, bl, an));
+namespace {
+// water-filling partition with row splitting over (non-zero C block, cost) pairs in block order
+tt_status split_partition(tt_ctx ctx, tt_tensor C, const std::vector<int64_t>& cblk,
+                          const std::vector<int64_t>& cost, uint32_t group_mask) {
   if (group_mask >> C->order) return fail(TT_E_ARG, "group_mask references dims beyond the order of C");
   if (group_mask && !(group_mask & 1u)) return fail(TT_E_ARG, "row splitting needs dim 0 among the grouping dims");
-  HostTasks ht;
-  enumerate_tasks(an, C, A, B, ht);
   // units (as tt_partition_lpt)
   std::map<std::vector<int32_t>, size_t> unit_of;
   std::vector<int64_t> ucost, uid, urows;
   std::vector<std::vector<int64_t>> ublocks;
   int32_t cc[TT_MAX_ORDER];
-  for (size_t g = 0; g < ht.cblk.size(); ++g) {
+  for (size_t g = 0; g < cblk.size(); ++g) {
     std::vector<int32_t> key;
-    C->block_coords(ht.cblk[g], cc);
+    C->block_coords(cblk[g], cc);
     if (group_mask) {
       for (int d = 0; d < C->order; ++d)
         if (group_mask >> d & 1) key.push_back(cc[d]);
@@ -1884,12 +1881,12 @@ tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor 
     if (it == unit_of.end()) {
       it = unit_of.emplace(key, ucost.size()).first;
       ucost.push_back(0);
-      uid.push_back(ht.cblk[g]);
+      uid.push_back(cblk[g]);
       urows.push_back(C->dims[0]->size(cc[0]));
       ublocks.push_back({});
     }
-    ucost[it->second] += ht.cost[g];
-    ublocks[it->second].push_back(ht.cblk[g]);
+    ucost[it->second] += cost[g];
+    ublocks[it->second].push_back(cblk[g]);
   }
   std::vector<size_t> order(ucost.size());
   std::iota(order.begin(), order.end(), 0);
@@ -1937,6 +1934,30 @@ tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor 
   refresh_parts_view(C);
   C->version++;
   return TT_OK;
+}
+}  // namespace
+
+tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
+                             const char* bl, uint32_t group_mask) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  Analysis an;
+  TT_TRY(analyse(C, cl, A, al, B, bl, an));
+  HostTasks ht;
+  enumerate_tasks(an, C, A, B, ht);
+  return split_partition(ctx, C, ht.cblk, ht.cost, group_mask);
+}
+
+tt_status tt_partition_split_cost(tt_ctx ctx, tt_tensor C, const int64_t* cost, uint32_t group_mask) {
+  if (!ctx || !C || !cost) return fail(TT_E_ARG, "NULL context, tensor or cost array");
+  std::vector<int64_t> cblk, cst;
+  for (int64_t b = 0; b < C->nblocks; ++b) {
+    if (!C->nz[b]) continue;
+    const int64_t c = cost[cblk.size()];
+    if (c < 0) return fail(TT_E_ARG, "negative block cost");
+    cblk.push_back(b);
+    cst.push_back(c);
+  }
+  return split_partition(ctx, C, cblk, cst, group_mask);
 }
 
 tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,

@@ -286,6 +286,37 @@ def test_partition_split_matches_oracle(nranks, grouped):
         assert max(load) - W / nranks <= tol + 1e-6
 
 
+@pytest.mark.parametrize("nranks", [2, 5])
+@pytest.mark.parametrize("grouped", [False, True])
+def test_partition_split_cost_matches_oracle(nranks, grouped):
+    """Caller-supplied block costs (seeded, with zeros) -> the same water-filling partition as the
+    oracle's partition_split on those costs; wrong-length or negative costs are rejected."""
+    c = tt.Context(device=-1, nranks=nranks)
+    pb = ccsd_problem(10, 14, 3, 4, True)
+    orc = oracle_objects(pb, nranks)
+    prod = product_objects(tt, c, pb)
+    C = pb.ops[0][0]
+    cb = [int(x) for x in np.flatnonzero(orc[C].nz)]
+    rng = np.random.default_rng(7)
+    cost = rng.integers(0, 1000, len(cb)) * (rng.random(len(cb)) > 0.2)
+    gd = (0, 1) if grouped else ()
+    exp = L.partition_split(orc[C], [int(x) for x in cost], cb, list(gd), nranks)
+    tt.partition_split_cost(c, prod[C], cost, group_dims=gd)
+    got = {}
+    for x in cb:
+        if prod[C].owner[x] == tt.TT_SPLIT:
+            got[x] = [(lo, hi, o) for (bb, lo, hi, o) in prod[C].parts if bb == x]
+        else:
+            got[x] = [(0, orc[C].block_extents(x)[0], int(prod[C].owner[x]))]
+    assert got == exp
+    with pytest.raises(ValueError):
+        tt.partition_split_cost(c, prod[C], cost[:-1])
+    bad = cost.copy()
+    bad[0] = -1
+    with pytest.raises(tt.TTError):
+        tt.partition_split_cost(c, prod[C], bad)
+
+
 @pytest.mark.parametrize("nranks", [2, 4])
 def test_lpt_grouped_matches_oracle(nranks):
     """LPT over (a,b) rows of R (group dims 0,1), so each rank owns whole rows (R24)."""
