@@ -1,6 +1,7 @@
 // tt_api.cpp -- host side of libtt: handles, validation, layout, task lists, partition, plans and
 // the C ABI entry points declared in include/tt.h.  Citations as in tt.h.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -490,6 +491,10 @@ struct ContractPlan {
   CGroupDesc* d_groups = nullptr;
   TaskDesc* d_tasks = nullptr;
   WorkItem* d_work = nullptr;
+  std::vector<SplitDesc> splits;       // split-K parts (reduced after the GEMM kernel)
+  SplitDesc* d_splits = nullptr;
+  double* d_partials = nullptr;        // their partial sums, one slot per chunk
+  int64_t partial_elems = 0;
   int64_t* d_ablk = nullptr;
   int64_t* d_bblk = nullptr;
   int64_t* d_ptr = nullptr;
@@ -1593,18 +1598,56 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       }
     }
   }
+  // ---- split-K: when the whole contraction (all ranks) has too few output elements to give every
+  // SM two tiles, each C block's task list is cut into up to S contiguous chunks of balanced K that
+  // run as separate work items writing partial sums, reduced in chunk order afterwards.  The cut
+  // depends only on the block's own task list and the global output size -- not on the rank count,
+  // the row split or the kernel variant -- so results stay independent of them (R12).
+  std::vector<std::vector<int64_t>> chunks(ht.cblk.size());   // task boundaries per C block
+  {
+    double e_total = 0;
+    for (size_t g = 0; g < ht.cblk.size(); ++g)
+      if (ht.ptr[g + 1] > ht.ptr[g]) e_total += (double)C->block_volume(ht.cblk[g]);
+    const double target = (double)ctx->sm_count * 2.0 * 80.0 * 80.0;
+    int64_t s_target = 1;
+    if (e_total > 0 && e_total < target) s_target = std::min<int64_t>(64, (int64_t)std::ceil(target / e_total));
+    const char* fs = getenv("TT_SPLITK");   // testing / tuning override of the chunk count
+    const bool forced = fs != nullptr;
+    if (forced) s_target = std::max(1, atoi(fs));
+    for (const auto& mp : pl.my) {
+      const int g = mp.g;
+      auto& cb = chunks[g];
+      if (!cb.empty()) continue;
+      int64_t ktot = 0;
+      for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) ktot += ht.K[t];
+      const int64_t ntk = ht.ptr[g + 1] - ht.ptr[g];
+      const int64_t S = std::max<int64_t>(1, std::min<int64_t>({s_target, ntk, forced ? ntk : ktot / 512}));
+      cb.push_back(ht.ptr[g]);
+      int64_t cum = 0, j = 1;
+      for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1] && j < S; ++t) {
+        cum += ht.K[t];
+        if (cum * S >= j * ktot && t + 1 < ht.ptr[g + 1]) {   // boundary after task t
+          cb.push_back(t + 1);
+          while (j < S && cum * S >= j * ktot) ++j;
+        }
+      }
+      cb.push_back(ht.ptr[g + 1]);
+    }
+  }
   double best = -1;
   for (int v = 0; v < n_variants(); ++v) {
     VariantInfo vi = variant_info(v);
     std::vector<double> items;
     for (size_t i = 0; i < pl.my.size(); ++i) {
-      const int g = pl.my[i].g;
-      double kst = 0;
-      for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) kst += (double)((ht.K[t] + vi.bk - 1) / vi.bk);
+      const auto& cb = chunks[pl.my[i].g];
       const int64_t nit = ((Me[i] - Mb[i] + vi.bm - 1) / vi.bm) * ((Ne[i] - Nb[i] + vi.bn - 1) / vi.bn);
-      const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm /
-                       variant_efficiency(v, pl.tma && v >= num_contract_variants());
-      for (int64_t i = 0; i < nit; ++i) items.push_back(c);
+      for (size_t h = 0; h + 1 < cb.size(); ++h) {
+        double kst = 0;
+        for (int64_t t = cb[h]; t < cb[h + 1]; ++t) kst += (double)((ht.K[t] + vi.bk - 1) / vi.bk);
+        const double c = (double)vi.bm * vi.bn * vi.bk * std::max(kst, 1.0) * vi.ctas_per_sm /
+                         variant_efficiency(v, pl.tma && v >= num_contract_variants());
+        for (int64_t i = 0; i < nit; ++i) items.push_back(c);
+      }
     }
     std::sort(items.begin(), items.end(), std::greater<double>());
     std::priority_queue<double, std::vector<double>, std::greater<double>> slots;
@@ -1650,9 +1693,6 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     gd.n_begin = (int32_t)Nb[oi];
     gd.task_begin = (int32_t)ht.ptr[g];
     gd.task_end = (int32_t)ht.ptr[g + 1];
-    int64_t st = 0;
-    for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) st += (ht.K[t] + vi.bk - 1) / vi.bk;
-    gd.nstages = (int32_t)st;
     int64_t sc[TT_MAX_ORDER], acc = 1;
     for (int d = an.nc - 1; d >= 0; --d) { sc[d] = acc; acc *= lt[d]->size(cc[d]); }
     for (int i = 0; i < kMaxGroup; ++i) { gd.mext[i] = gd.next[i] = 1; gd.cm_str[i] = gd.cn_str[i] = 0; }
@@ -1668,11 +1708,30 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       gd.next[i] = e;
       gd.cn_str[i] = (int32_t)sc[an.ng[i].back()];
     }
-    const int32_t gi = (int32_t)groups.size();
-    groups.push_back(gd);
+    const auto& ch = chunks[g];
+    const int64_t nch = (int64_t)ch.size() - 1;
     const int32_t mtn = (gd.M - gd.m_begin + vi.bm - 1) / vi.bm, ntn = (gd.N - gd.n_begin + vi.bn - 1) / vi.bn;
-    for (int32_t mt = 0; mt < mtn; ++mt)
-      for (int32_t nt = 0; nt < ntn; ++nt) work.push_back({gi, mt, nt});
+    if (nch > 1) {
+      const int64_t bvol = (C->block_volume(ht.cblk[g]) + 1) / 2 * 2;
+      pl.splits.push_back({gd.c_off, pl.partial_elems, bvol, (int32_t)groups.size(), (int32_t)nch});
+    }
+    for (int64_t h = 0; h < nch; ++h) {
+      CGroupDesc gc = gd;
+      gc.task_begin = (int32_t)ch[h];
+      gc.task_end = (int32_t)ch[h + 1];
+      int64_t st = 0;
+      for (int64_t t = ch[h]; t < ch[h + 1]; ++t) st += (ht.K[t] + vi.bk - 1) / vi.bk;
+      gc.nstages = (int32_t)st;
+      if (nch > 1) {
+        gc.flags = kGroupPartial;
+        gc.c_off = pl.partial_elems + h * pl.splits.back().vol;
+      }
+      const int32_t gi = (int32_t)groups.size();
+      groups.push_back(gc);
+      for (int32_t mt = 0; mt < mtn; ++mt)
+        for (int32_t nt = 0; nt < ntn; ++nt) work.push_back({gi, mt, nt});
+    }
+    if (nch > 1) pl.partial_elems += nch * pl.splits.back().vol;
   }
   pl.nwork = (int64_t)work.size();
   {
@@ -1687,6 +1746,11 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
   TT_TRY(dev_alloc(ctx, &pl.d_work, work.size()));
   if (!groups.empty()) TT_CUDA(cudaMemcpy(pl.d_groups, groups.data(), groups.size() * sizeof(CGroupDesc), cudaMemcpyHostToDevice));
   if (!work.empty()) TT_CUDA(cudaMemcpy(pl.d_work, work.data(), work.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
+  if (!pl.splits.empty()) {
+    TT_TRY(dev_alloc(ctx, &pl.d_splits, pl.splits.size()));
+    TT_TRY(dev_alloc(ctx, &pl.d_partials, (size_t)pl.partial_elems));
+    TT_CUDA(cudaMemcpy(pl.d_splits, pl.splits.data(), pl.splits.size() * sizeof(SplitDesc), cudaMemcpyHostToDevice));
+  }
   return TT_OK;
 }
 
@@ -1716,6 +1780,7 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
   p.A = A->data;
   p.B = B->data;
   p.C = C->data;
+  p.P = pl.d_partials;
   p.groups = pl.d_groups;
   p.tasks = pl.d_tasks;
   p.work = pl.d_work;
@@ -1729,23 +1794,31 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
   p.persistent = pl.persistent ? 1 : 0;
   p.tma_n = (int32_t)pl.tma_n;
   const std::string nm = std::string("tt_contract_dmma[") + cl + "=" + al + "*" + bl + "]";
-  Launch L(ctx, nm.c_str());
-  if (pl.tma) {
-    // (re-)encode the tensor maps when the bound storage changed
-    ContractPlan& mp = const_cast<ContractPlan&>(pl);
-    if (mp.map_ptr[0] != A->data || mp.map_ptr[1] != B->data) {
-      const VariantInfo vi = variant_info(pl.variant);
-      TT_TRY(encode_2d(&mp.maps[0], A->data, pl.tma_k, A->packed_elems / pl.tma_k, 16, (uint32_t)vi.bm, true));
-      TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->packed_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
-      mp.map_ptr[0] = A->data;
-      mp.map_ptr[1] = B->data;
-    }
-    TT_CUDA(launch_contract_tma(pl.variant - num_contract_variants(), p, pl.maps, pl.nwork, ctx->stream));
-  } else if (pl.variant < num_contract_variants())
-    TT_CUDA(launch_contract(pl.variant, pl.an.a_kc, pl.an.b_nc, p, pl.nwork, ctx->stream));
-  else
-    TT_CUDA(launch_contract_ws(pl.variant - num_contract_variants(), pl.an.a_kc, pl.an.b_nc, pl.a_vec, pl.b_vec, p,
-                               pl.nwork, ctx->stream));
+  {
+    Launch L(ctx, nm.c_str());
+    if (pl.tma) {
+      // (re-)encode the tensor maps when the bound storage changed
+      ContractPlan& mp = const_cast<ContractPlan&>(pl);
+      if (mp.map_ptr[0] != A->data || mp.map_ptr[1] != B->data) {
+        const VariantInfo vi = variant_info(pl.variant);
+        TT_TRY(encode_2d(&mp.maps[0], A->data, pl.tma_k, A->packed_elems / pl.tma_k, 16, (uint32_t)vi.bm, true));
+        TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->packed_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
+        mp.map_ptr[0] = A->data;
+        mp.map_ptr[1] = B->data;
+      }
+      TT_CUDA(launch_contract_tma(pl.variant - num_contract_variants(), p, pl.maps, pl.nwork, ctx->stream));
+    } else if (pl.variant < num_contract_variants())
+      TT_CUDA(launch_contract(pl.variant, pl.an.a_kc, pl.an.b_nc, p, pl.nwork, ctx->stream));
+    else
+      TT_CUDA(launch_contract_ws(pl.variant - num_contract_variants(), pl.an.a_kc, pl.an.b_nc, pl.a_vec, pl.b_vec, p,
+                                 pl.nwork, ctx->stream));
+  }
+  if (!pl.splits.empty()) {
+    const std::string rn = std::string("tt_contract_reduce[") + cl + "=" + al + "*" + bl + "]";
+    Launch R(ctx, rn.c_str());
+    TT_CUDA(launch_split_reduce(pl.d_partials, C->data, pl.d_groups, pl.d_splits, (int32_t)pl.splits.size(),
+                                p.nM, p.nN, alpha, beta, ctx->stream));
+  }
   return TT_OK;
 }
 

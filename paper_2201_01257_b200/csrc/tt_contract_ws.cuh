@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(co
   // --------------------------------------------------------------- MMA warps
   const int wm = warp / K::WN, wn = warp % K::WN;
   const int q = lane & 3, r8 = lane >> 2;
-  const double alpha = p.alpha, beta = p.beta;
+  const double alpha_ = p.alpha, beta_ = p.beta;
   int st = 0;
   unsigned phase = 0;
   for (int64_t wi = blockIdx.x; wi < p.nwork; wi += gridDim.x) {
@@ -311,7 +311,9 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(co
     }
 
     // epilogue (the producers are already streaming the next item)
-    double* Cb = p.C + g->c_off;
+    const bool part = g->flags & kGroupPartial;
+    double* Cb = (part ? p.P : p.C) + g->c_off;
+    const double alpha = part ? 1.0 : alpha_, beta = part ? 0.0 : beta_;
     const int M = g->M, N = g->N;
     int32_t mext[kMaxGroup], next[kMaxGroup], cms[kMaxGroup], cns[kMaxGroup];
 #pragma unroll
@@ -439,7 +441,7 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
   // --------------------------------------------------------------- MMA warps
   const int wm = warp / K::WN, wn = warp % K::WN;
   const int q = lane & 3, r8 = lane >> 2, pr = perm8(r8);
-  const double alpha = p.alpha, beta = p.beta;
+  const double alpha_ = p.alpha, beta_ = p.beta;
   int st = 0;
   unsigned phase = 0;
   for (int64_t wi = blockIdx.x; wi < p.nwork; wi += gridDim.x) {
@@ -485,7 +487,9 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
       if (++st == STAGES) { st = 0; phase ^= 1; }
     }
     // epilogue (single M and N groups: C row m has stride cm_str[0], column n stride cn_str[0])
-    double* Cb = p.C + g->c_off;
+    const bool part = g->flags & kGroupPartial;
+    double* Cb = (part ? p.P : p.C) + g->c_off;
+    const double alpha = part ? 1.0 : alpha_, beta = part ? 0.0 : beta_;
     const int M = g->M, N = g->N;
     const int32_t cms = g->cm_str[0], cns = g->cn_str[0];
 #pragma unroll

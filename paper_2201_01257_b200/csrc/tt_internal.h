@@ -22,13 +22,16 @@ constexpr int kMaxGroup = 4;  // fused label groups per GEMM side (M, N, K)
 // One per non-zero C block this rank computes.  GEMM view of the block:
 // m = mixed radix over the fused M groups (labels of C that come from A, C order), n over the
 // fused N groups (labels from B), innermost last.
+constexpr int32_t kGroupPartial = 1;
+
 struct CGroupDesc {
   int64_t c_off;                 // packed offset of the C block
   int32_t M, N;                  // GEMM row / column END of this group (exclusive)
   int32_t m_begin, n_begin;      // first row / column (a part of a row-split block; else 0)
   int32_t task_begin, task_end;  // CSR range in the task array
   int32_t nstages;               // sum over tasks of ceil(K_t / BK) for the chosen kernel BK
-  int32_t pad;
+  int32_t flags;                 // kGroupPartial: a split-K chunk writing raw sums into the partial
+                                 // buffer (c_off is then an offset into ContractParams::P)
   int32_t mext[kMaxGroup], next[kMaxGroup];     // fused group extents
   int32_t cm_str[kMaxGroup], cn_str[kMaxGroup]; // their strides inside the C block
 };

@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_kernel(const
   cp_async_wait<0>();
 
   // ---- epilogue: C = beta*C + alpha*acc (beta == 0: C not read), output permutation via strides
-  double* Cb = p.C + g.c_off;
-  const double alpha = p.alpha, beta = p.beta;
+  const bool part = g.flags & kGroupPartial;
+  double* Cb = (part ? p.P : p.C) + g.c_off;
+  const double alpha = part ? 1.0 : p.alpha, beta = part ? 0.0 : p.beta;
 #pragma unroll
   for (int i = 0; i < K::MT; ++i) {
     const int m = m0 + wm * K::WTM + i * 8 + fr_r;
@@ -730,6 +731,36 @@ int64_t scalar_num_partials(int mode, int64_t nseg) {
 
 cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, cudaStream_t s) {
   scalar_final_kernel<<<1, 1024, 0, s>>>(partials, n, alpha, out);
+  return cudaGetLastError();
+}
+
+
+// ------------------------------------------------------------------------------------------------
+// Split-K reduction (contractions with too few output tiles to fill the GPU): the chunks of a C part
+// wrote raw sums into slots of P laid out like the C block; C = beta*C + alpha * (slot 0 + slot 1 + ...)
+// in slot order -- deterministic (R12).  blockIdx.y = split descriptor; threads stride its elements.
+__global__ void split_reduce_kernel(const double* __restrict__ P, double* __restrict__ C,
+                                    const CGroupDesc* __restrict__ groups, const SplitDesc* __restrict__ splits,
+                                    int32_t nM, int32_t nN, double alpha, double beta) {
+  const SplitDesc sd = splits[blockIdx.y];
+  const CGroupDesc& g = groups[sd.group];
+  const int32_t rows = g.M - g.m_begin, cols = g.N - g.n_begin;
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t m = g.m_begin + (int32_t)(e / cols), c = g.n_begin + (int32_t)(e % cols);
+    const int64_t off = dot_decode(m, nM, g.mext, g.cm_str) + dot_decode(c, nN, g.next, g.cn_str);
+    const double* ps = P + sd.p_off + off;
+    double acc = 0.0;
+    for (int32_t s = 0; s < sd.nslots; ++s) acc += ps[(int64_t)s * sd.vol];
+    double* o = C + sd.c_off + off;
+    *o = (beta == 0.0) ? alpha * acc : beta * *o + alpha * acc;
+  }
+}
+
+cudaError_t launch_split_reduce(const double* P, double* C, const CGroupDesc* groups, const SplitDesc* splits,
+                                int32_t nsplit, int32_t nM, int32_t nN, double alpha, double beta, cudaStream_t s) {
+  if (nsplit <= 0) return cudaSuccess;
+  split_reduce_kernel<<<dim3(16, (unsigned)nsplit), 256, 0, s>>>(P, C, groups, splits, nM, nN, alpha, beta);
   return cudaGetLastError();
 }
 

@@ -48,6 +48,7 @@ struct ContractParams {
   const double* A;
   const double* B;
   double* C;
+  double* P;              // split-K partial buffer (groups flagged kGroupPartial write here)
   const CGroupDesc* groups;
   const TaskDesc* tasks;
   const WorkItem* work;
@@ -58,6 +59,15 @@ struct ContractParams {
   int32_t persistent;     // 1: grid = resident CTAs looping over items; 0: one CTA per item
   int32_t tma_n;          // TMA variant: row length N of the B matrix view
 };
+
+// Split-K reduction: C part = beta*C + alpha * sum_{s < nslots} P[p_off + s*vol + .] in slot order
+// (deterministic, reading R12); `group` = the first chunk group (extents, strides, row range).
+struct SplitDesc {
+  int64_t c_off, p_off, vol;
+  int32_t group, nslots;
+};
+cudaError_t launch_split_reduce(const double* P, double* C, const CGroupDesc* groups, const SplitDesc* splits,
+                                int32_t nsplit, int32_t nM, int32_t nN, double alpha, double beta, cudaStream_t s);
 
 struct VariantInfo {
   int bm, bn, bk, threads, smem, ctas_per_sm;

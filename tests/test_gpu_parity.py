@@ -160,6 +160,61 @@ def test_determinism(env):
     assert np.array_equal(g1, g2)
 
 
+@pytest.mark.parametrize("splitk", [2, 3, 7])
+@pytest.mark.parametrize("variant", [None, 1, 3, 5])
+def test_split_k_forced(env, splitk, variant):
+    """Task lists cut into up to `splitk` chunks (partial sums reduced in chunk order): parity on
+    ladder / ring / hole-hole terms, beta = 0 with NaN in C, permuted labels; deterministic."""
+    tt, torch = env
+    os.environ["TT_SPLITK"] = str(splitk)
+    try:
+        pb = ccsd_problem(12, 30, 3, 5, True)
+        ctx = new_ctx(tt, torch, variant)
+        for op in pb.ops:
+            got, ref, _, _ = run_contract(tt, torch, ctx, pb, op, alpha=1.25, beta=-0.5)
+            assert normwise(got, ref) <= TOL
+            got2, ref2, _, _ = run_contract(tt, torch, ctx, pb, op, alpha=0.5, beta=0.0, nan_c=True)
+            assert np.isfinite(got2).all() and normwise(got2, np.nan_to_num(ref2)) <= TOL
+            got3, _, _, _ = run_contract(tt, torch, ctx, pb, op, alpha=1.25, beta=-0.5)
+            assert np.array_equal(got, got3)
+        spaces = {"X": SpaceSpec(11, tile=4), "Y": SpaceSpec(9, tile=5), "Z": SpaceSpec(10, tile=3)}
+        ls = {"a": "X", "b": "Y", "c": "Z", "i": "Y", "j": "X", "k": "Z"}
+        for cl, al, bl in [("jbia", "kcai", "bjck"), ("ijab", "akci", "jbkc")]:
+            tens = {"C": TensorSpec(cl), "A": TensorSpec(al), "B": TensorSpec(bl)}
+            q = Problem(spaces, ls, tens, [("C", cl, "A", al, "B", bl)])
+            got, ref, _, _ = run_contract(tt, torch, ctx, q, q.ops[0], alpha=1.0, beta=0.5)
+            assert normwise(got, ref) <= TOL, (cl, al, bl)
+    finally:
+        os.environ.pop("TT_SPLITK", None)
+        os.environ.pop("TT_FORCE_VARIANT", None)
+
+
+def test_split_k_small_output_large_k(env):
+    """Hole-hole-shaped C(m,i) += A(e,f,m,n) B(e,f,i,n): few output tiles, long task lists -- the
+    planner splits K on its own (one launch of the reduce kernel), parity and bitwise equality with
+    the row-split (parts) version of the same C (chunking independent of the part rows)."""
+    tt, torch = env
+    spaces = {"O": SpaceSpec(12, tile=6), "V": SpaceSpec(120, tile=10)}
+    ls = {"m": "O", "i": "O", "n": "O", "e": "V", "f": "V"}
+    tens = {"C": TensorSpec("mi"), "A": TensorSpec("efmn"), "B": TensorSpec("efin")}
+    pb = Problem(spaces, ls, tens, [("C", "mi", "A", "efmn", "B", "efin")])
+    ctx = new_ctx(tt, torch)
+    got, ref, P, orc = run_contract(tt, torch, ctx, pb, pb.ops[0], alpha=0.5, beta=1.0, seed=6)
+    assert normwise(got, ref) <= TOL
+    assert ctx.stats()["work_items"] > 4          # 4 C blocks, chunked
+    ctx2 = new_ctx(tt, torch)
+    orc2 = oracle_objects(pb)
+    P2 = product_objects(tt, ctx2, pb)
+    _split_all(P2["C"], 2)
+    bufs = []
+    for name, tag in (("C", 3), ("A", 1), ("B", 2)):
+        bufs.append(bind_host(torch, P2[name], O.pack(orc2[name], O.dense_masked(orc2[name], S.dense(orc2[name].shape, 6, tag)))))
+    tt.contract(ctx2, P2["C"], "mi", 1.0, 0.5, P2["A"], "efmn", P2["B"], "efin")
+    g2 = P2["C"].download()
+    ctx2.sync()
+    assert np.array_equal(got, g2)
+
+
 @pytest.mark.parametrize("pi", [0, 1])
 def test_device_task_list_bit_exact(env, pi):
     tt, torch = env

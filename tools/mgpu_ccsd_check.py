@@ -53,7 +53,7 @@ def main():
     ctx = tt.Context(device=local, stream=stream, rank=rank, nranks=world, nccl_id=obj[0])
     ok = True
     for shape in ((12, 20, 3, 5, 14, 7), (16, 40, 4, 6, 24, 10)):
-        it = CCSDIteration(tt, ctx, *shape, seed=3, ws_gb=2e-5, nstreams=3)
+        it = CCSDIteration(tt, ctx, *shape, seed=3, ws_gb=2e-3, nstreams=3)
         for rep in range(2):      # the second run replays the cached plans
             nlev, E = it.run()
             res = {}
