@@ -162,10 +162,24 @@ tt_status tt_tensor_set_parts(tt_tensor t, int64_t n, const int64_t* blk, const 
 /* The parts of all split blocks (arrays owned by the handle, valid until the next ownership change). */
 tt_status tt_tensor_parts(tt_tensor t, int64_t* n, const int64_t** blk, const int32_t** lo,
                           const int32_t** hi, const int32_t** owner);
-/* Bind caller-owned DEVICE memory of capacity_elems doubles (>= packed_elems, 16-B aligned). */
+/* Compact storage (memory for 180 GB per GPU at configs[4] scale): with on != 0 the bound buffer
+ * holds only the element ranges THIS rank holds (its owned blocks and row parts, and replicated
+ * blocks): per non-zero block the span from its first to its last held element, packed in block
+ * order, each block base 16-B aligned.  Storage offsets are recomputed on every ownership change
+ * (set_owner / set_parts / partitions).  A compact tensor may be the output of any operation and an
+ * input whose reads are all local; an operation that would gather remote pieces INTO it fails with
+ * TT_E_UNSUPPORTED (on every rank alike).  upload/download move the storage buffer.  Must be
+ * identical on every rank.  Default off (storage = the global packed layout). */
+tt_status tt_tensor_set_compact(tt_tensor t, int32_t on);
+/* Storage size in doubles (what tt_tensor_bind needs) and the per-block storage offsets (nblocks
+ * entries; -1 = not stored on this rank; block base, i.e. element e of block b is at off[b] + e).
+ * Without compact storage these equal packed_elems / blk_off of tt_tensor_layout. */
+tt_status tt_tensor_storage(tt_tensor t, int64_t* storage_elems, const int64_t** storage_off);
+/* Bind caller-owned DEVICE memory of capacity_elems doubles (>= the storage size: packed_elems, or
+ * tt_tensor_storage's size when compact; 16-B aligned). */
 tt_status tt_tensor_bind(tt_tensor t, void* dev_ptr, int64_t capacity_elems);
-/* Host <-> device copies of the whole packed buffer on the context stream (asynchronous when the
- * host memory is pinned).  host holds packed_elems doubles.  These are the end-to-end entry points
+/* Host <-> device copies of the whole storage buffer on the context stream (asynchronous when the
+ * host memory is pinned).  host holds the storage size in doubles (packed_elems unless compact).  These are the end-to-end entry points
  * for callers whose data lives in host memory. */
 tt_status tt_tensor_upload(tt_ctx ctx, tt_tensor t, const double* host);
 tt_status tt_tensor_download(tt_ctx ctx, tt_tensor t, double* host);

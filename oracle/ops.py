@@ -225,3 +225,17 @@ def cholesky_v(X: np.ndarray) -> np.ndarray:
     n = X.shape[0]
     V = contract(np.zeros((n, n, n, n)), "pqrs", X, "prL", X, "qsL", 1.0, 0.0)
     return contract(V, "pqrs", X, "psL", X, "qrL", -1.0, 1.0)
+
+
+def cholesky_v_row(Xa: np.ndarray, Xb: np.ndarray) -> np.ndarray:
+    """PAPER Eq. cc12 at one fixed (p,q) = (a,b) (reading R19), for sampled checks at sizes where V
+    cannot be formed:  v(a,b,r,s) = sum_L X(a,r,L) X(b,s,L) - X(a,s,L) X(b,r,L)
+    with Xa = X(a,:,:), Xb = X(b,:,:) dense [n, N_L].  Two matrix products over L."""
+    return Xa @ Xb.T - Xb @ Xa.T
+
+
+def ladder_sample(vrow: np.ndarray, Tij: np.ndarray, alpha: float) -> float:
+    """One output element of the ladder R(a,b,i,j) = alpha * sum_{r,s} v(a,b,r,s) T(r,s,i,j) (beta = 0),
+    vrow = v(a,b,:,:), Tij = T(:,:,i,j); sequential-order sum over r then s."""
+    return alpha * float(np.sum(vrow * Tij))
+

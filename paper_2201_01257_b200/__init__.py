@@ -87,6 +87,8 @@ _SIGS = {
     "tt_partition_lpt": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32, _vp],
     "tt_partition_split": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32],
     "tt_partition_split_cost": [_vp, _vp, _vp, _u32],
+    "tt_tensor_set_compact": [_vp, _i32],
+    "tt_tensor_storage": [_vp, _P(_i64), _P(_P(_i64))],
     "tt_gather_plan": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _P(_i64), _vp,
                        _P(_i64), _i64],
     "tt_sched_create": [_vp, _i32, _P(_vp)],
@@ -278,6 +280,10 @@ class Tensor:
         pb, plo, phi, pow_ = _P(_i64)(), _P(_i32)(), _P(_i32)(), _P(_i32)()
         _check(_lib.tt_tensor_parts(self.h, ctypes.byref(n), ctypes.byref(pb), ctypes.byref(plo), ctypes.byref(phi),
                                     ctypes.byref(pow_)))
+        se, so = _i64(), _P(_i64)()
+        _check(_lib.tt_tensor_storage(self.h, ctypes.byref(se), ctypes.byref(so)))
+        self.storage_elems = se.value
+        self.storage_off = np.ctypeslib.as_array(so, (nb.value,)).copy()
         k = n.value
         self.parts = [tuple(int(x) for x in row) for row in zip(
             np.ctypeslib.as_array(pb, (k,)) if k else [], np.ctypeslib.as_array(plo, (k,)) if k else [],
@@ -304,6 +310,11 @@ class Tensor:
         _check(_lib.tt_tensor_set_parts(self.h, len(a), _ptr(blk), _ptr(lo), _ptr(hi), _ptr(ow)))
         self._refresh()
 
+    def set_compact(self, on: bool = True):
+        """Compact storage: the buffer holds only this rank's parts (tt_tensor_set_compact)."""
+        _check(_lib.tt_tensor_set_compact(self.h, 1 if on else 0))
+        self._refresh()
+
     def bind(self, storage, capacity: Optional[int] = None):
         """Bind caller-owned device memory (a torch tensor, or an int pointer with ``capacity``)."""
         if capacity is None:
@@ -312,7 +323,7 @@ class Tensor:
         self.storage = storage
 
     def upload(self, host: np.ndarray):
-        assert host.dtype == np.float64 and host.size >= self.packed_elems
+        assert host.dtype == np.float64 and host.size >= self.storage_elems
         _check(_lib.tt_tensor_upload(self.ctx.h, self.h, _vp(host.ctypes.data)))
 
     def upload_ptr(self, host_ptr: int):
@@ -320,7 +331,7 @@ class Tensor:
 
     def download(self, host: Optional[np.ndarray] = None) -> np.ndarray:
         if host is None:
-            host = np.empty(self.packed_elems, dtype=np.float64)
+            host = np.empty(self.storage_elems, dtype=np.float64)
         _check(_lib.tt_tensor_download(self.ctx.h, self.h, _vp(host.ctypes.data)))
         return host
 

@@ -372,43 +372,58 @@ void pieces(tt_tensor T, int64_t b, int64_t e0, int64_t e1, F&& emit) {
   }
 }
 
-void build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops, GatherPlan& gp) {
+tt_status build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops, GatherPlan& gp) {
   const int me = ctx->rank, P = ctx->nranks;
+  bool into_compact = false;
   for (int dst = 0; dst < P; ++dst) {
     normalize(need[dst]);
     for (const Need& n : need[dst]) {
       tt_tensor T = ops[n.op];
       pieces(T, n.blk, n.e0, n.e1, [&](int32_t src, int64_t a, int64_t z) {
         if (src == TT_REPLICATED || src == dst) return;
+        if (T->compact) into_compact = true;
         if (dst == me) gp.recv_list.insert(gp.recv_list.end(), {n.op, n.blk, src, a, z});
         if (src == me) gp.send_list.insert(gp.send_list.end(), {n.op, n.blk, dst, a, z});
       });
     }
   }
+  // a compact tensor (storage = the rank's own parts only) has no room for received pieces; every
+  // rank sees the same needs, so every rank fails alike
+  if (into_compact)
+    return fail(TT_E_UNSUPPORTED, "an operand with compact storage would have to receive remote pieces");
+  // runs: pieces of one (operand, peer) merged when adjacent in the GLOBAL packed order (the same
+  // decision on sender and receiver); compact tensors never merge across blocks
   auto runs = [&](const std::vector<int64_t>& lst, std::vector<Run>& out) {
     std::vector<size_t> idx(lst.size() / 5);
     std::iota(idx.begin(), idx.end(), 0);
-    auto goff = [&](size_t i) { return ops[lst[5 * i]]->blk_off[lst[5 * i + 1]] + lst[5 * i + 3]; };
+    auto goff = [&](size_t i) { return ops[lst[5 * i]]->gblk_off[lst[5 * i + 1]] + lst[5 * i + 3]; };
+    auto soff = [&](size_t i) { return ops[lst[5 * i]]->blk_off[lst[5 * i + 1]] + lst[5 * i + 3]; };
     std::sort(idx.begin(), idx.end(), [&](size_t x, size_t y) {
       return std::make_tuple(lst[5 * x + 2], lst[5 * x], goff(x)) < std::make_tuple(lst[5 * y + 2], lst[5 * y], goff(y));
     });
+    int64_t gend = 0, lastblk = -1;
     for (size_t i : idx) {
       const int op = (int)lst[5 * i], peer = (int)lst[5 * i + 2];
-      const int64_t off = goff(i), len = lst[5 * i + 4] - lst[5 * i + 3];
+      const int64_t off = goff(i), len = lst[5 * i + 4] - lst[5 * i + 3], blk = lst[5 * i + 1];
       if (!out.empty() && out.back().op == op && out.back().peer == peer) {
         Run& r = out.back();
-        const int64_t gap = off - (r.off + r.len);
-        if (gap >= 0 && gap <= 1) {   // adjacent in packed order (<= 1 alignment pad element)
-          r.len = off + len - r.off;
+        const int64_t gap = off - gend;
+        if (gap >= 0 && gap <= 1 && (!ops[op]->compact || blk == lastblk)) {   // <= 1 alignment pad element
+          r.len += gap + len;
+          gend = off + len;
+          lastblk = blk;
           continue;
         }
       }
-      out.push_back({op, peer, off, len});
+      out.push_back({op, peer, soff(i), len});
+      gend = off + len;
+      lastblk = blk;
     }
   };
   runs(gp.recv_list, gp.recv);
   runs(gp.send_list, gp.send);
   for (const Run& r : gp.recv) gp.recv_bytes += r.len * 8;
+  return TT_OK;
 }
 
 tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops) {
@@ -431,27 +446,30 @@ tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tens
 // tensor device metadata
 
 tt_status ensure_dev(tt_tensor t) {
-  if (t->dev_ready) return TT_OK;
+  if (t->dev_ready && !t->dev_off_stale) return TT_OK;
   tt_ctx ctx = t->ctx;
   TT_TRY(need_device(ctx));
-  TT_TRY(dev_alloc(ctx, &t->d_nz, t->nblocks));
-  TT_TRY(dev_alloc(ctx, &t->d_blk_off, t->nblocks));
-  TT_CUDA(cudaMemcpy(t->d_nz, t->nz.data(), t->nblocks, cudaMemcpyHostToDevice));
-  TT_CUDA(cudaMemcpy(t->d_blk_off, t->blk_off.data(), t->nblocks * 8, cudaMemcpyHostToDevice));
-  t->d_toff.assign(t->order, nullptr);
-  for (int d = 0; d < t->order; ++d) {
-    TT_TRY(dev_alloc(ctx, &t->d_toff[d], t->dims[d]->offsets.size()));
-    TT_CUDA(cudaMemcpy(t->d_toff[d], t->dims[d]->offsets.data(), t->dims[d]->offsets.size() * 8, cudaMemcpyHostToDevice));
+  if (!t->dev_ready) {
+    TT_TRY(dev_alloc(ctx, &t->d_nz, t->nblocks));
+    TT_TRY(dev_alloc(ctx, &t->d_blk_off, t->nblocks));
+    TT_CUDA(cudaMemcpy(t->d_nz, t->nz.data(), t->nblocks, cudaMemcpyHostToDevice));
+    t->d_toff.assign(t->order, nullptr);
+    for (int d = 0; d < t->order; ++d) {
+      TT_TRY(dev_alloc(ctx, &t->d_toff[d], t->dims[d]->offsets.size()));
+      TT_CUDA(cudaMemcpy(t->d_toff[d], t->dims[d]->offsets.data(), t->dims[d]->offsets.size() * 8, cudaMemcpyHostToDevice));
+    }
   }
+  TT_CUDA(cudaMemcpy(t->d_blk_off, t->blk_off.data(), t->nblocks * 8, cudaMemcpyHostToDevice));
   t->dev_ready = true;
+  t->dev_off_stale = false;
   return TT_OK;
 }
 
 tt_status check_bound(tt_tensor t, const char* which) {
   if (!t->data) return fail(TT_E_UNBOUND, "tensor %s has no storage bound (S208)", which);
-  if (t->capacity < t->packed_elems)
-    return fail(TT_E_UNBOUND, "tensor %s: bound capacity %lld < packed size %lld", which, (long long)t->capacity,
-                (long long)t->packed_elems);
+  if (t->capacity < t->storage_elems)
+    return fail(TT_E_UNBOUND, "tensor %s: bound capacity %lld < storage size %lld", which, (long long)t->capacity,
+                (long long)t->storage_elems);
   return TT_OK;
 }
 
@@ -799,8 +817,35 @@ static void tensor_finish(tt_tensor t) {
     t->nnz++;
   }
   t->packed_elems = (cur + 1) / 2 * 2;
+  t->gblk_off = t->blk_off;
+  t->storage_elems = t->packed_elems;
   t->parts.assign(t->nblocks, {});
   t->any_split = false;
+}
+
+// storage offsets: the global packed layout, or (compact) only the ranges this rank holds -- per
+// block the span [first held element, last held element) packed in block order, each block base
+// even (16-B aligned) so the vectorised paths keep their alignment
+static void apply_storage(tt_tensor t) {
+  if (!t->compact) {
+    t->blk_off = t->gblk_off;
+    t->storage_elems = t->packed_elems;
+  } else {
+    std::vector<std::pair<int64_t, int64_t>> hr;
+    int64_t cur = 0;
+    for (int64_t b = 0; b < t->nblocks; ++b) {
+      t->blk_off[b] = -1;
+      t->held_ranges(b, t->ctx->rank, hr);
+      if (hr.empty()) continue;
+      int64_t e0 = hr[0].first, e1 = hr[0].second;
+      for (auto& h : hr) { e0 = std::min(e0, h.first); e1 = std::max(e1, h.second); }
+      if ((cur - e0) & 1) ++cur;
+      t->blk_off[b] = cur - e0;
+      cur += e1 - e0;
+    }
+    t->storage_elems = std::max<int64_t>(2, (cur + 1) / 2 * 2);
+  }
+  t->dev_off_stale = true;
 }
 
 static void refresh_parts_view(tt_tensor t) {
@@ -861,9 +906,26 @@ tt_status tt_tensor_layout(tt_tensor t, int64_t* packed, const int64_t** blk_off
                            const uint8_t** nz) {
   if (!t) return fail(TT_E_ARG, "NULL tensor");
   if (packed) *packed = t->packed_elems;
-  if (blk_off) *blk_off = t->blk_off.data();
+  if (blk_off) *blk_off = t->gblk_off.data();
   if (owner) *owner = t->owner.data();
   if (nz) *nz = t->nz.data();
+  return TT_OK;
+}
+
+tt_status tt_tensor_set_compact(tt_tensor t, int32_t on) {
+  if (!t) return fail(TT_E_ARG, "NULL tensor");
+  if ((on != 0) != t->compact) {
+    t->compact = on != 0;
+    apply_storage(t);
+    t->version++;
+  }
+  return TT_OK;
+}
+
+tt_status tt_tensor_storage(tt_tensor t, int64_t* storage_elems, const int64_t** storage_off) {
+  if (!t) return fail(TT_E_ARG, "NULL tensor");
+  if (storage_elems) *storage_elems = t->storage_elems;
+  if (storage_off) *storage_off = t->blk_off.data();
   return TT_OK;
 }
 
@@ -877,6 +939,7 @@ tt_status tt_tensor_set_owner(tt_tensor t, const int32_t* owner) {
   for (int64_t b = 0; b < t->nblocks; ++b) t->owner[b] = t->nz[b] ? owner[b] : -1;
   t->parts.assign(t->nblocks, {});
   refresh_parts_view(t);
+  apply_storage(t);
   t->version++;
   return TT_OK;
 }
@@ -909,6 +972,7 @@ tt_status tt_tensor_set_parts(tt_tensor t, int64_t n, const int64_t* blk, const 
     }
   }
   refresh_parts_view(t);
+  apply_storage(t);
   t->version++;
   return TT_OK;
 }
@@ -927,8 +991,8 @@ tt_status tt_tensor_parts(tt_tensor t, int64_t* n, const int64_t** blk, const in
 tt_status tt_tensor_bind(tt_tensor t, void* ptr, int64_t cap) {
   if (!t) return fail(TT_E_ARG, "NULL tensor");
   if (ptr && ((uintptr_t)ptr % 16) != 0) return fail(TT_E_ARG, "storage must be 16-byte aligned");
-  if (ptr && cap < t->packed_elems)
-    return fail(TT_E_UNBOUND, "capacity %lld < packed size %lld", (long long)cap, (long long)t->packed_elems);
+  if (ptr && cap < t->storage_elems)
+    return fail(TT_E_UNBOUND, "capacity %lld < storage size %lld", (long long)cap, (long long)t->storage_elems);
   t->data = (double*)ptr;
   t->capacity = cap;
   return TT_OK;
@@ -939,7 +1003,7 @@ tt_status tt_tensor_upload(tt_ctx ctx, tt_tensor t, const double* host) {
   if (!t || !host) return fail(TT_E_ARG, "NULL argument");
   TT_TRY(check_bound(t, "upload"));
   DeviceGuard dg(ctx->device);
-  TT_CUDA(cudaMemcpyAsync(t->data, host, t->packed_elems * 8, cudaMemcpyHostToDevice, ctx->stream));
+  TT_CUDA(cudaMemcpyAsync(t->data, host, t->storage_elems * 8, cudaMemcpyHostToDevice, ctx->stream));
   return TT_OK;
 }
 
@@ -948,7 +1012,7 @@ tt_status tt_tensor_download(tt_ctx ctx, tt_tensor t, double* host) {
   if (!t || !host) return fail(TT_E_ARG, "NULL argument");
   TT_TRY(check_bound(t, "download"));
   DeviceGuard dg(ctx->device);
-  TT_CUDA(cudaMemcpyAsync(host, t->data, t->packed_elems * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  TT_CUDA(cudaMemcpyAsync(host, t->data, t->storage_elems * 8, cudaMemcpyDeviceToHost, ctx->stream));
   return TT_OK;
 }
 
@@ -1227,7 +1291,7 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
       ep->blocks++;
     }
     if (ep->mode != kElemTranspose) ep->tiles.clear();
-    build_gather(ctx, need, {A}, ep->gp);
+    TT_TRY(build_gather(ctx, need, {A}, ep->gp));
     TT_TRY(upload_elem(ctx, *ep, false));
     ctx->plans[key] = ep;
   }
@@ -1320,7 +1384,7 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
       ep->blocks++;
     }
     if (ep->mode != kElemTranspose) ep->tiles.clear();
-    build_gather(ctx, need, {A, B}, ep->gp);
+    TT_TRY(build_gather(ctx, need, {A, B}, ep->gp));
     TT_TRY(upload_elem(ctx, *ep, true));
     ctx->plans[key] = ep;
   }
@@ -1457,8 +1521,8 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
         }
       }
     }
-    if (A == B) build_gather(ctx, need, {A}, pl.gp);
-    else build_gather(ctx, need, {A, B}, pl.gp);
+    if (A == B) TT_TRY(build_gather(ctx, need, {A}, pl.gp));
+    else TT_TRY(build_gather(ctx, need, {A, B}, pl.gp));
   }
   // stats for this rank
   {
@@ -1801,8 +1865,8 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
       ContractPlan& mp = const_cast<ContractPlan&>(pl);
       if (mp.map_ptr[0] != A->data || mp.map_ptr[1] != B->data) {
         const VariantInfo vi = variant_info(pl.variant);
-        TT_TRY(encode_2d(&mp.maps[0], A->data, pl.tma_k, A->packed_elems / pl.tma_k, 16, (uint32_t)vi.bm, true));
-        TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->packed_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
+        TT_TRY(encode_2d(&mp.maps[0], A->data, pl.tma_k, A->storage_elems / pl.tma_k, 16, (uint32_t)vi.bm, true));
+        TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->storage_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
         mp.map_ptr[0] = A->data;
         mp.map_ptr[1] = B->data;
       }
@@ -2005,6 +2069,7 @@ tt_status split_partition(tt_ctx ctx, tt_tensor C, const std::vector<int64_t>& c
   for (int64_t b = 0; b < C->nblocks; ++b) C->owner[b] = C->nz[b] ? own[b] : -1;
   C->parts = parts;
   refresh_parts_view(C);
+  apply_storage(C);
   C->version++;
   return TT_OK;
 }
@@ -2071,6 +2136,9 @@ tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, c
 // against Bm (one HBM-bound pass per call).  The rank's C parts are processed in batches of (p,q)
 // tile rows: W of the batch is built into the workspace and immediately consumed by the ladder
 // contraction restricted to the batch.  B is all-gathered once per call (SPMD); X must be replicated.
+// When the workspace cannot hold Bm (configs[4]: B is 97 GB) the consume runs in two passes instead,
+// C += alpha W.B and C -= alpha W.B(r<->s) (the second contraction reads B with r, s relabelled):
+// no Bm, twice the consume FLOPs.
 
 namespace {
 
@@ -2087,6 +2155,7 @@ struct CholPlan {
   GatherPlan bgather;                           // all-gather of B
   std::vector<CholBatch> batches;
   std::string lc;                               // the auxiliary label used for L
+  bool two_pass = false;                        // no room for Bm: consume W.B and W.B(r<->s)
   ~CholPlan() {
     delete Vmeta;
     delete Wmeta;
@@ -2190,9 +2259,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   TT_TRY(check_bound(X, "X"));
   TT_TRY(check_bound(B, "B"));
   const int64_t bm_elems = (B->packed_elems + 31) / 32 * 32;
-  if (!workspace || ws_elems <= bm_elems)
-    return fail(TT_E_UNBOUND, "workspace must hold B's packed size (%lld doubles) plus one (p,q) row of W",
-                (long long)B->packed_elems);
+  if (!workspace || ws_elems <= 0) return fail(TT_E_UNBOUND, "no workspace bound");
   DeviceGuard dg(ctx->device);
 
   char keybuf[256];
@@ -2218,19 +2285,17 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     }
     TT_TRY(new_meta_tensor(ctx, vd, vnz, &cp->Vmeta));
     TT_TRY(new_meta_tensor(ctx, vd, wnz, &cp->Wmeta));
-    // Bm: B's layout, replicated scratch at the start of the workspace
+    // Bm: B's layout, replicated scratch at the start of the workspace (if it fits, below)
     TT_TRY(new_meta_tensor(ctx, B->dims, B->nz, &cp->Bm));
     for (int64_t x = 0; x < cp->Bm->nblocks; ++x)
       if (cp->Bm->nz[x]) cp->Bm->owner[x] = TT_REPLICATED;
-    cp->Bm->data = (double*)workspace;
-    cp->Bm->capacity = bm_elems;
     // all-gather of B (every rank needs every B block for Bm)
     {
       Needs need(ctx->nranks);
       for (int rr = 0; rr < ctx->nranks; ++rr)
         for (int64_t x = 0; x < B->nblocks; ++x)
           if (B->nz[x]) need[rr].push_back({0, x, 0, B->block_volume(x)});
-      build_gather(ctx, need, {B}, cp->bgather);
+      TT_TRY(build_gather(ctx, need, {B}, cp->bgather));
     }
     // Bm = B - B(r<->s)
     std::vector<int> id(B->order), sw(B->order);
@@ -2247,7 +2312,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     bool dummy;
     TT_TRY(get_contract_plan(ctx, C, cl, cp->Vmeta, vl, B, bl, beta, cp->vplan, &dummy, g));
     g.tag = "|cholW";
-    TT_TRY(get_contract_plan(ctx, C, cl, cp->Wmeta, vl, cp->Bm, bl, beta, cp->wplan, &dummy, g));
+    TT_TRY(get_contract_plan(ctx, C, cl, cp->Wmeta, vl, B, bl, beta, cp->wplan, &dummy, g));
     const ContractPlan& gp = *cp->wplan;
     // units: my C parts grouped by the (p,q) tile coordinates; W rows restricted when C's dim 0 is p
     const bool rows_on_p = c[0] == p;
@@ -2269,8 +2334,6 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       if (rows_on_p) u.wrows.push_back({mp.lo, mp.hi});
       else u.wrows.push_back({0, tp->size(u.tp)});
     }
-    double* wbase = (double*)workspace + bm_elems;
-    const int64_t w_elems = ws_elems - bm_elems;
     auto row_blocks = [&](const Unit& u, std::vector<int64_t>& out) {
       out.clear();
       for (int32_t a2 = 0; a2 < tr->ntiles(); ++a2)
@@ -2279,6 +2342,27 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
           if (wnz[vb]) out.push_back(vb);
         }
     };
+    // workspace: Bm then the W batches; without room for Bm plus the largest W row, two passes
+    std::vector<int64_t> rb;
+    int64_t max_uel = 0;
+    for (auto& kv : units) {
+      row_blocks(kv.second, rb);
+      int64_t uel = 0;
+      for (int64_t vb : rb) uel += (cp->Wmeta->block_volume(vb) + 1) / 2 * 2;
+      max_uel = std::max(max_uel, uel);
+    }
+    if (const char* f2 = getenv("TT_CHOL_TWO_PASS")) cp->two_pass = atoi(f2) != 0;
+    if (ws_elems < bm_elems + max_uel) cp->two_pass = true;
+    if (ws_elems < max_uel)
+      return fail(TT_E_OOM, "workspace holds %lld doubles; one (p,q) row of W needs %lld", (long long)ws_elems,
+                  (long long)max_uel);
+    const int64_t w_off = cp->two_pass ? 0 : bm_elems;
+    double* wbase = (double*)workspace + w_off;
+    const int64_t w_elems = ws_elems - w_off;
+    if (!cp->two_pass) {
+      cp->Bm->data = (double*)workspace;
+      cp->Bm->capacity = bm_elems;
+    }
     auto flush = [&](std::vector<const Unit*>& cur) -> tt_status {
       if (cur.empty()) return TT_OK;
       CholBatch bt;
@@ -2318,7 +2402,6 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     };
     std::vector<const Unit*> cur;
     int64_t cur_elems = 0;
-    std::vector<int64_t> rb;
     for (auto& kv : units) {
       const Unit& u = kv.second;
       row_blocks(u, rb);
@@ -2336,31 +2419,49 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   }
   const std::string L = cp->lc;
   const std::string x1 = std::string(1, p) + r + L, x2 = std::string(1, q) + s + L;   // W = X(prL) X(qsL)
+  std::string bsw(bl);                                                              // B with r <-> s
+  std::swap(bsw[b.find(r)], bsw[b.find(s)]);
   if (ctx->prepare_only) {   // build every batch plan now (they are cached), launch nothing
     for (auto& bt : cp->batches) {
-      std::shared_ptr<ContractPlan> pw, pu;
+      std::shared_ptr<ContractPlan> pw, pu, px;
       bool dummy;
       TT_TRY(get_contract_plan(ctx, bt.Wb, vl, X, x1.c_str(), X, x2.c_str(), 0.0, pw, &dummy, bt.wopt));
-      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
+      if (cp->two_pass) {
+        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, B, bl, beta, pu, &dummy, bt.copt));
+        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, B, bsw.c_str(), 1.0, px, &dummy, bt.copt));
+      } else {
+        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
+      }
     }
     return TT_OK;
   }
   reset_stats(ctx);
   TT_TRY(run_gather(ctx, cp->bgather, {B}));
-  TT_TRY(run_local_add(ctx, *cp->copy_plan, cp->Bm, B, 0.0, 1.0));
-  TT_TRY(run_local_add(ctx, *cp->swap_plan, cp->Bm, B, 1.0, -1.0));
+  if (!cp->two_pass) {
+    TT_TRY(run_local_add(ctx, *cp->copy_plan, cp->Bm, B, 0.0, 1.0));
+    TT_TRY(run_local_add(ctx, *cp->swap_plan, cp->Bm, B, 1.0, -1.0));
+  }
   double exec = 0, build = 0;
   int64_t tasks = 0;
   for (auto& bt : cp->batches) {
-    std::shared_ptr<ContractPlan> pw, pu;
+    std::shared_ptr<ContractPlan> pw, pu, px;
     bool dummy;
     TT_TRY(get_contract_plan(ctx, bt.Wb, vl, X, x1.c_str(), X, x2.c_str(), 0.0, pw, &dummy, bt.wopt));
-    TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
     TT_TRY(launch_plan(ctx, *pw, bt.Wb, vl, 0.0, 1.0, X, x1.c_str(), X, x2.c_str()));
-    TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Wb, vl, cp->Bm, bl));
     build += pw->flops;
-    exec += pu->flops;
-    tasks += pu->tasks;
+    if (cp->two_pass) {
+      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, B, bl, beta, pu, &dummy, bt.copt));
+      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, B, bsw.c_str(), 1.0, px, &dummy, bt.copt));
+      TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Wb, vl, B, bl));
+      TT_TRY(launch_plan(ctx, *px, C, cl, 1.0, -alpha, bt.Wb, vl, B, bsw.c_str()));
+      exec += pu->flops + px->flops;
+      tasks += pu->tasks + px->tasks;
+    } else {
+      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
+      TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Wb, vl, cp->Bm, bl));
+      exec += pu->flops;
+      tasks += pu->tasks;
+    }
   }
   ctx->last.c_blocks = (int64_t)cp->wplan->my.size();
   ctx->last.tasks = tasks;

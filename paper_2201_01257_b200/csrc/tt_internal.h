@@ -94,9 +94,12 @@ struct tt_tensor_s {
   std::vector<int32_t> grid;       // ntiles per dim
   int64_t nblocks = 0, nnz = 0;
   std::vector<uint8_t> nz;
-  std::vector<int64_t> blk_off;
+  std::vector<int64_t> blk_off;    // STORAGE offsets (= gblk_off unless compact; -1 = not stored)
+  std::vector<int64_t> gblk_off;   // global packed offsets (R10)
   std::vector<int32_t> owner;
   int64_t packed_elems = 0;
+  bool compact = false;            // storage holds only this rank's held ranges (tt_tensor_set_compact)
+  int64_t storage_elems = 0;       // doubles the bound buffer must hold
   double* data = nullptr;
   int64_t capacity = 0;
   uint64_t uid = 0;
@@ -106,6 +109,7 @@ struct tt_tensor_s {
   int64_t* d_blk_off = nullptr;
   std::vector<int64_t*> d_toff;   // per dim tile offsets on the device
   bool dev_ready = false;
+  bool dev_off_stale = false;      // storage offsets changed since the last upload
   // row-range ownership (SURVEY §8(e) block splitting): a split block is owned by parts, each a
   // range [lo, hi) of the block's dimension-0 tile; owner[b] is then TT_SPLIT
   struct Part {

@@ -1,6 +1,6 @@
 """Multi-GPU parity check of the synthetic CCSD-shaped iteration (run under torchrun, NCCL).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29513 tools/mgpu_ccsd_check.py
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29513 tests/mgpu_ccsd_check.py
 
 CCSDIteration distributes its tensors (replicated inputs, row-split R2 / Wr / Z / Wo / Fv); every
 rank runs the scheduler; the owned parts of R2 and Wr are assembled on rank 0 (sum of the owned
@@ -24,20 +24,21 @@ from tests.test_ccsd_iteration import _oracle_tensors  # noqa: E402
 
 
 def owned(T, got, rank):
-    """Copy of ``got`` (packed) with only the elements this rank owns (replicated: rank 0)."""
-    mine = np.zeros_like(got)
+    """Packed-layout copy of the storage buffer ``got`` with only the elements this rank owns
+    (replicated blocks: rank 0); works for compact storage (storage_off) and the full layout."""
+    mine = np.zeros(T.packed_elems)
     for blk in range(T.nblocks):
         if not T.nz[blk]:
             continue
-        o = T.blk_off[blk]
+        o, so = T.blk_off[blk], T.storage_off[blk]
         ext = [d.offsets[t + 1] - d.offsets[t] for d, t in zip(T.dims, np.unravel_index(blk, T.grid))]
         n = int(np.prod(ext))
         if T.owner[blk] == rank or (T.owner[blk] == tt.TT_REPLICATED and rank == 0):
-            mine[o:o + n] = got[o:o + n]
+            mine[o:o + n] = got[so:so + n]
         inner = n // int(ext[0])
         for (bb, lo, hi, ow) in T.parts:
             if bb == blk and ow == rank:
-                mine[o + lo * inner:o + hi * inner] = got[o + lo * inner:o + hi * inner]
+                mine[o + lo * inner:o + hi * inner] = got[so + lo * inner:so + hi * inner]
     return mine
 
 

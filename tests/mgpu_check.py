@@ -1,6 +1,6 @@
 """Multi-GPU parity check (run under torchrun, one process per GPU, NCCL).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 tools/mgpu_check.py
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 tests/mgpu_check.py
 
 For spin-sparse ladder / ring / hole-hole terms: output blocks LPT-partitioned over the ranks, inputs
 distributed round robin (P210 scheme 3); tt_contract gathers the needed input blocks over NCCL. The

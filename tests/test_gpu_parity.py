@@ -500,12 +500,17 @@ def _cholesky_problem(O_, V_, tO, tV, NL, tL, spin):
     return pb
 
 
-@pytest.mark.parametrize("spin,ws_rows", [(True, 1), (True, 100), (False, 2)])
-def test_contract_cholesky(env, spin, ws_rows):
+@pytest.mark.parametrize("spin,ws_rows,mode", [(True, 1, "bm"), (True, 100, "bm"), (False, 2, "bm"),
+                                                (True, 1, "env"), (False, 2, "env"), (True, 3, "auto")])
+def test_contract_cholesky(env, spin, ws_rows, mode):
     """Implicit Eq. cc12 operand (NEXT-1): R(abij) = beta*R + alpha*sum V(abcd) T(cdij) with V built
-    batch by batch from X in a small workspace == oracle with V formed explicitly."""
+    batch by batch from X in a small workspace == oracle with V formed explicitly.  mode "bm": the
+    workspace holds Bm = T - T(c<->d); "env"/"auto": the two-pass consume (forced, or because the
+    workspace holds only W rows)."""
     tt, torch = env
     pb = _cholesky_problem(8, 12, 2, 3, 10, 5, spin) if spin else _cholesky_problem(5, 9, 3, 4, 7, 4, False)
+    if mode == "env":
+        os.environ["TT_CHOL_TWO_PASS"] = "1"
     ctx = new_ctx(tt, torch)
     orc = oracle_objects(pb)
     P = product_objects(tt, ctx, pb)
@@ -514,10 +519,12 @@ def test_contract_cholesky(env, spin, ws_rows):
         dense[name] = O.dense_masked(orc[name], S.dense(orc[name].shape, 2, tag))
         bufs.append(bind_host(torch, P[name], O.pack(orc[name], dense[name])))
     tv = max(np.diff(P["X"].dims[0].offsets))
-    ws = torch.empty(int(P["T"].packed_elems + 32 + ws_rows * tv ** 4 * P["X"].dims[0].ntiles ** 2 + 64),
-                     dtype=torch.float64, device="cuda")
+    row = tv ** 4 * P["X"].dims[0].ntiles ** 2 + 64
+    bm = 0 if mode == "auto" else P["T"].packed_elems + 32
+    ws = torch.empty(int(bm + ws_rows * row), dtype=torch.float64, device="cuda")
     for beta in (1.0, 0.0):
         tt.contract_cholesky(ctx, P["R"], "abij", beta, 0.5, P["X"], "abcd", P["T"], "cdij", ws)
+        os.environ.pop("TT_CHOL_TWO_PASS", None)
         got = P["R"].download()
         ctx.sync()
         st = ctx.stats()

@@ -317,6 +317,69 @@ def test_partition_split_cost_matches_oracle(nranks, grouped):
         tt.partition_split_cost(c, prod[C], bad)
 
 
+@pytest.mark.parametrize("rank", [0, 1, 2])
+def test_compact_storage_layout(rank):
+    """Compact storage: per non-zero block the span of this rank's held ranges (owned blocks, owned
+    row parts, replicated blocks) packed in block order with even (16-B aligned) bases; -1 for blocks
+    not stored; recomputed on ownership changes; the global layout (tt_tensor_layout) unchanged."""
+    nranks = 3
+    c = tt.Context(device=-1, rank=rank, nranks=nranks)
+    pb = ccsd_problem(10, 14, 3, 4, True)
+    P = product_objects(tt, c, pb)
+    R = P[pb.ops[0][0]]
+    glob = R.blk_off.copy()
+    _, cl, a, al, b, bl = pb.ops[0]
+    tt.partition_split(c, R, cl, P[a], al, P[b], bl, group_dims=(0, 1))
+    own = R.owner.copy()
+    own[own == tt.TT_SPLIT] = 0                    # re-split by set_parts below
+    rep = np.flatnonzero(R.nz)[::7]
+    own[rep] = tt.TT_REPLICATED                    # some replicated blocks too (parts kept elsewhere)
+    parts = [p for p in R.parts if p[0] not in set(rep.tolist())]
+    R.set_owner(own)
+    R.set_parts(parts)
+    R.set_compact(True)
+    assert np.array_equal(R.blk_off, glob)
+    cur, exp = 0, np.full(R.nblocks, -1, np.int64)
+    for b in range(R.nblocks):
+        if not R.nz[b]:
+            continue
+        vol = int(np.prod([d.offsets[t + 1] - d.offsets[t] for d, t in zip(R.dims, np.unravel_index(b, R.grid))]))
+        inner = vol // int(np.diff(R.dims[0].offsets)[np.unravel_index(b, R.grid)[0]])
+        if R.owner[b] == rank or R.owner[b] == tt.TT_REPLICATED:
+            rng = [(0, vol)]
+        else:
+            rng = [(lo * inner, hi * inner) for (bb, lo, hi, o) in R.parts if bb == b and o == rank]
+        if not rng:
+            continue
+        e0, e1 = min(r[0] for r in rng), max(r[1] for r in rng)
+        if (cur - e0) % 2:
+            cur += 1
+        exp[b] = cur - e0
+        cur += e1 - e0
+    assert np.array_equal(R.storage_off, exp)
+    assert R.storage_elems == max(2, (cur + 1) // 2 * 2)
+    assert all(x % 2 == 0 for x in R.storage_off[R.storage_off >= 0])
+    R.set_compact(False)
+    assert np.array_equal(R.storage_off, glob) and R.storage_elems == R.packed_elems
+
+
+def test_compact_operand_cannot_receive():
+    """An operand with compact storage that would have to receive remote pieces is rejected."""
+    c = tt.Context(device=-1, rank=0, nranks=2)
+    pb = ccsd_problem(10, 14, 3, 4, True)
+    P = product_objects(tt, c, pb)
+    C, cl, a, al, b, bl = pb.ops[0]
+    r, _ = tt.gather_plan(c, P[C], cl, P[a], al, P[b], bl)   # A round robin: pieces received
+    assert any(row[0] == 0 for row in r.tolist())
+    P[a].set_compact(True)
+    with pytest.raises(tt.TTError) as e:
+        tt.gather_plan(c, P[C], cl, P[a], al, P[b], bl)
+    assert e.value.name == "TT_E_UNSUPPORTED"
+    P[a].set_owner(np.where(P[a].nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))   # all local: fine
+    r, s_ = tt.gather_plan(c, P[C], cl, P[a], al, P[b], bl)
+    assert not any(row[0] == 0 for row in r.tolist())
+
+
 @pytest.mark.parametrize("nranks", [2, 4])
 def test_lpt_grouped_matches_oracle(nranks):
     """LPT over (a,b) rows of R (group dims 0,1), so each rank owns whole rows (R24)."""

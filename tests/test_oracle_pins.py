@@ -423,3 +423,32 @@ def test_cholesky_v_pins():
     Xd[np.arange(n), np.arange(n), 0] = 1.0
     I = np.eye(n)
     assert np.array_equal(O.cholesky_v(Xd), np.einsum("pr,qs->pqrs", I, I) - np.einsum("ps,qr->pqrs", I, I))
+
+
+def test_cholesky_v_row_and_ladder_sample_pins():
+    """Row form of Eq. cc12 (sampled checks at configs[4] scale): brute force per element, closed
+    forms (separable X: 0; X(p,r,L) = delta_pr delta_L0: d_ar d_bs - d_as d_br), antisymmetry in
+    (r,s); the ladder sample is the brute-force double sum."""
+    n, nl = 5, 4
+    X = rnd((n, n, nl), 6, 7)
+    for a, b in [(0, 1), (3, 3), (4, 2)]:
+        v = O.cholesky_v_row(X[a], X[b])
+        for r in range(n):
+            for s in range(n):
+                bf = sum(X[a, r, l] * X[b, s, l] - X[a, s, l] * X[b, r, l] for l in range(nl))
+                assert abs(v[r, s] - bf) < 1e-15
+        assert np.abs(v + v.T).max() < 1e-15
+    x, y, z = rnd((n,), 1, 8), rnd((n,), 2, 8), rnd((nl,), 3, 8)
+    X1 = np.einsum("p,r,l->prl", x, y, z)
+    assert np.abs(O.cholesky_v_row(X1[1], X1[3])).max() < 1e-15
+    Xd = np.zeros((n, n, nl))
+    Xd[np.arange(n), np.arange(n), 0] = 1.0
+    I = np.eye(n)
+    assert np.array_equal(O.cholesky_v_row(Xd[1], Xd[3]), np.outer(I[1], I[3]) - np.outer(I[3], I[1]))
+    T = rnd((n, n), 4, 8)
+    v = O.cholesky_v_row(X[2], X[0])
+    bf = 0.0
+    for r in range(n):
+        for s in range(n):
+            bf += v[r, s] * T[r, s]
+    assert abs(O.ladder_sample(v, T, 0.5) - 0.5 * bf) < 1e-14

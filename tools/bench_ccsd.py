@@ -110,7 +110,7 @@ def main():
         dist.all_reduce(kt, op=dist.ReduceOp.MAX)
     if rank == 0:
         flops, parts = algorithmic_flops(it)
-        mem = {n: T.packed_elems * 8e-9 for n, T in it.T.items()}
+        mem = {n: T.storage_elems * 8e-9 for n, T in it.T.items()}
         print(json.dumps({"workload": f"synthetic CCSD-shaped iteration O={a.O} V={a.V} tile={a.tile} N_L={a.nl}, "
                                       f"alpha/beta maps, implicit Cholesky V", "n_gpus": world,
                           "ms_per_iteration": ms, "levels": levels, "energy": E, "algorithmic_flops": flops,
