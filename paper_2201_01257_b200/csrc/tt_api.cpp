@@ -2132,13 +2132,17 @@ tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, c
 // Because the exchange term of Eq. cc12 is the Coulomb term W with r and s swapped, re-indexing the
 // second sum gives exactly
 //   sum_{r,s} V(p,q,r,s) B(..r..s..) = sum_{r,s} W(p,q,r,s) Bm(..r..s..),  Bm = B - B(r<->s)
-// so only the Coulomb blocks W are built (one DMMA contraction over L per block) and consumed
-// against Bm (one HBM-bound pass per call).  The rank's C parts are processed in batches of (p,q)
-// tile rows: W of the batch is built into the workspace and immediately consumed by the ladder
-// contraction restricted to the batch.  B is all-gathered once per call (SPMD); X must be replicated.
-// When the workspace cannot hold Bm (configs[4]: B is 97 GB) the consume runs in two passes instead,
-// C += alpha W.B and C -= alpha W.B(r<->s) (the second contraction reads B with r, s relabelled):
-// no Bm, twice the consume FLOPs.
+// so only the Coulomb blocks W are built (one DMMA contraction over L per block).  Bm is
+// antisymmetric in (r,s), so only its tile pairs r_t <= s_t are formed ("Bh", about half of B):
+//   sum_{r,s} W Bm = sum_{r_t <= s_t} W(p,q,r,s) Bh(r,s) - sum_{r_t < s_t} W(p,q,s,r) Bh(r,s)
+// (pass 1 over Bh's blocks, pass 2 over its strictly-upper blocks with W read as (p,q,s,r)): the
+// same consume FLOPs as a full Bm, half its memory.  When B's blocks (r,s) and (s,r) sit on the same
+// rank, each rank forms its own Bh blocks from its own B blocks and Bh is all-gathered (half of B's
+// bytes; B itself may then use compact storage); otherwise B is all-gathered and every rank forms
+// all of Bh.  The rank's C parts are processed in batches of (p,q) tile rows: W of the batch is
+// built into the workspace and immediately consumed restricted to the batch.  X must be replicated.
+// When the workspace cannot hold Bh plus one W row (or TT_CHOL_TWO_PASS=1) the consume reads B
+// directly in two passes, C += alpha W.B and C -= alpha W.B(r<->s): no Bh, twice the consume FLOPs.
 
 namespace {
 
@@ -2149,17 +2153,21 @@ struct CholBatch {
 
 struct CholPlan {
   tt_tensor Vmeta = nullptr, Wmeta = nullptr;   // block maps of V (algorithmic count) and W
-  tt_tensor Bm = nullptr;                       // B - B(r<->s), in the workspace
+  tt_tensor Bh = nullptr;                       // (B - B(r<->s)) on tile pairs r_t <= s_t, in the workspace
+  tt_tensor Bs = nullptr;                       // view of Bh's strictly-upper blocks (r_t < s_t)
   std::shared_ptr<ContractPlan> vplan, wplan;   // SPMD plans: this rank's C parts, FLOP counts
-  std::shared_ptr<ElemPlan> copy_plan, swap_plan;
-  GatherPlan bgather;                           // all-gather of B
+  std::shared_ptr<ElemPlan> copy_plan, swap_plan;   // Bh formation (this rank's Bh blocks)
+  GatherPlan bgather;                           // all-gather of B (not co-located) ...
+  GatherPlan hgather;                           // ... or of Bh (co-located B pairs)
   std::vector<CholBatch> batches;
   std::string lc;                               // the auxiliary label used for L
-  bool two_pass = false;                        // no room for Bm: consume W.B and W.B(r<->s)
+  bool two_pass = false;                        // no room for Bh: consume W.B and W.B(r<->s)
+  bool colocated = false;
   ~CholPlan() {
     delete Vmeta;
     delete Wmeta;
-    delete Bm;
+    delete Bh;
+    delete Bs;
     for (auto& b : batches) delete b.Wb;
   }
 };
@@ -2175,11 +2183,11 @@ tt_status new_meta_tensor(tt_ctx ctx, const std::vector<tt_tis>& dims, const std
 
 // local element add X(all blocks) = beta*X + alpha*Y(perm) with no gather (Y fully present)
 tt_status local_add_plan(tt_ctx ctx, tt_tensor Xt, tt_tensor Yt, const std::vector<int>& perm, double beta,
-                         std::shared_ptr<ElemPlan>& out) {
+                         std::shared_ptr<ElemPlan>& out, const std::vector<uint8_t>* only = nullptr) {
   auto ep = std::make_shared<ElemPlan>();
   int32_t cc[TT_MAX_ORDER], ac[TT_MAX_ORDER];
   for (int64_t b = 0; b < Xt->nblocks; ++b) {
-    if (!Xt->nz[b]) continue;
+    if (!Xt->nz[b] || (only && !(*only)[b])) continue;
     Xt->block_coords(b, cc);
     for (int d = 0; d < Xt->order; ++d) ac[perm[d]] = cc[d];
     const int64_t ab = Yt->block_id(ac);
@@ -2214,7 +2222,7 @@ tt_status run_local_add(tt_ctx ctx, const ElemPlan& ep, tt_tensor Xt, tt_tensor 
   p.order = Xt->order;
   p.alpha = alpha;
   p.beta = beta;
-  Launch L(ctx, "tt_add[cholesky Bm]");
+  Launch L(ctx, "tt_add[cholesky Bh]");
   TT_CUDA(launch_add(p, ep.nwork(), ctx->stream));
   return TT_OK;
 }
@@ -2258,7 +2266,6 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   TT_TRY(check_bound(C, "C"));
   TT_TRY(check_bound(X, "X"));
   TT_TRY(check_bound(B, "B"));
-  const int64_t bm_elems = (B->packed_elems + 31) / 32 * 32;
   if (!workspace || ws_elems <= 0) return fail(TT_E_UNBOUND, "no workspace bound");
   DeviceGuard dg(ctx->device);
 
@@ -2285,26 +2292,66 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     }
     TT_TRY(new_meta_tensor(ctx, vd, vnz, &cp->Vmeta));
     TT_TRY(new_meta_tensor(ctx, vd, wnz, &cp->Wmeta));
-    // Bm: B's layout, replicated scratch at the start of the workspace (if it fits, below)
-    TT_TRY(new_meta_tensor(ctx, B->dims, B->nz, &cp->Bm));
-    for (int64_t x = 0; x < cp->Bm->nblocks; ++x)
-      if (cp->Bm->nz[x]) cp->Bm->owner[x] = TT_REPLICATED;
-    // all-gather of B (every rank needs every B block for Bm)
-    {
-      Needs need(ctx->nranks);
+    // Bh: B's blocks with r_t <= s_t (the antisymmetric Bm's independent half), and its strict view
+    const size_t rp = b.find(r), sp_ = b.find(s);
+    std::vector<uint8_t> hnz(B->nblocks, 0), snz(B->nblocks, 0);
+    std::vector<int> id(B->order), sw(B->order);
+    for (int d = 0; d < B->order; ++d) id[d] = sw[d] = d;
+    sw[rp] = (int)sp_;
+    sw[sp_] = (int)rp;
+    int32_t bc[TT_MAX_ORDER], bsc[TT_MAX_ORDER];
+    std::vector<int64_t> swap_of(B->nblocks, -1);
+    for (int64_t x = 0; x < B->nblocks; ++x) {
+      B->block_coords(x, bc);
+      for (int d = 0; d < B->order; ++d) bsc[sw[d]] = bc[d];
+      swap_of[x] = B->block_id(bsc);
+      const bool nzm = B->nz[x] || B->nz[swap_of[x]];       // Bm(x) = B(x) - B(swap x)^T
+      hnz[x] = (nzm && bc[rp] <= bc[sp_]) ? 1 : 0;
+      snz[x] = (hnz[x] && bc[rp] < bc[sp_]) ? 1 : 0;
+    }
+    TT_TRY(new_meta_tensor(ctx, B->dims, hnz, &cp->Bh));
+    TT_TRY(new_meta_tensor(ctx, B->dims, snz, &cp->Bs));
+    for (int64_t x = 0; x < B->nblocks; ++x) {     // Bs shares Bh's storage
+      cp->Bs->blk_off[x] = cp->Bs->gblk_off[x] = snz[x] ? cp->Bh->blk_off[x] : -1;
+      if (snz[x]) cp->Bs->owner[x] = TT_REPLICATED;
+    }
+    cp->Bs->packed_elems = cp->Bs->storage_elems = cp->Bh->packed_elems;
+    // formation owner of each Bh block: the rank holding both B(x) and B(swap x) whole (replicated
+    // blocks are held everywhere); B pairs split across ranks -> all-gather B instead
+    cp->colocated = true;
+    std::vector<uint8_t> mine(B->nblocks, 0);
+    for (int64_t x = 0; x < B->nblocks; ++x) {
+      if (!hnz[x]) continue;
+      const int64_t y = swap_of[x];
+      int32_t ox = B->nz[x] ? B->owner[x] : TT_REPLICATED, oy = B->nz[y] ? B->owner[y] : TT_REPLICATED;
+      if ((B->nz[x] && !B->parts[x].empty()) || (B->nz[y] && !B->parts[y].empty()) || ox == TT_SPLIT || oy == TT_SPLIT) {
+        cp->colocated = false;
+        break;
+      }
+      const int32_t f = (ox == TT_REPLICATED) ? oy : ox;
+      if (oy != TT_REPLICATED && oy != f) { cp->colocated = false; break; }
+      cp->Bh->owner[x] = f;
+      mine[x] = (f == TT_REPLICATED || f == ctx->rank) ? 1 : 0;
+    }
+    Needs need(ctx->nranks);
+    if (cp->colocated) {
+      for (int rr = 0; rr < ctx->nranks; ++rr)
+        for (int64_t x = 0; x < B->nblocks; ++x)
+          if (hnz[x]) need[rr].push_back({0, x, 0, cp->Bh->block_volume(x)});
+      TT_TRY(build_gather(ctx, need, {cp->Bh}, cp->hgather));
+    } else {
+      for (int64_t x = 0; x < B->nblocks; ++x) {
+        if (hnz[x]) cp->Bh->owner[x] = TT_REPLICATED;
+        mine[x] = hnz[x];
+      }
       for (int rr = 0; rr < ctx->nranks; ++rr)
         for (int64_t x = 0; x < B->nblocks; ++x)
           if (B->nz[x]) need[rr].push_back({0, x, 0, B->block_volume(x)});
       TT_TRY(build_gather(ctx, need, {B}, cp->bgather));
     }
-    // Bm = B - B(r<->s)
-    std::vector<int> id(B->order), sw(B->order);
-    const size_t rp = b.find(r), sp_ = b.find(s);
-    for (int d = 0; d < B->order; ++d) id[d] = sw[d] = d;
-    sw[rp] = (int)sp_;
-    sw[sp_] = (int)rp;
-    TT_TRY(local_add_plan(ctx, cp->Bm, B, id, 0.0, cp->copy_plan));
-    TT_TRY(local_add_plan(ctx, cp->Bm, B, sw, 1.0, cp->swap_plan));
+    // Bh = B - B(r<->s) on this rank's Bh blocks
+    TT_TRY(local_add_plan(ctx, cp->Bh, B, id, 0.0, cp->copy_plan, &mine));
+    TT_TRY(local_add_plan(ctx, cp->Bh, B, sw, 1.0, cp->swap_plan, &mine));
     // SPMD plans for this rank's C parts: V map (algorithmic FLOPs) and W map (executed pairs)
     ContractOpts g;
     g.no_a_needs = true;
@@ -2342,7 +2389,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
           if (wnz[vb]) out.push_back(vb);
         }
     };
-    // workspace: Bm then the W batches; without room for Bm plus the largest W row, two passes
+    // workspace: Bh then the W batches; without room for Bh plus the largest W row, two passes
     std::vector<int64_t> rb;
     int64_t max_uel = 0;
     for (auto& kv : units) {
@@ -2352,16 +2399,27 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       max_uel = std::max(max_uel, uel);
     }
     if (const char* f2 = getenv("TT_CHOL_TWO_PASS")) cp->two_pass = atoi(f2) != 0;
-    if (ws_elems < bm_elems + max_uel) cp->two_pass = true;
+    const int64_t bh_elems = (cp->Bh->packed_elems + 31) / 32 * 32;
+    if (ws_elems < bh_elems + max_uel) cp->two_pass = true;
+    if (cp->two_pass) {    // B is read directly: all-gather it (not Bh)
+      cp->hgather = GatherPlan();
+      if (cp->colocated) {
+        Needs nb(ctx->nranks);
+        for (int rr = 0; rr < ctx->nranks; ++rr)
+          for (int64_t x = 0; x < B->nblocks; ++x)
+            if (B->nz[x]) nb[rr].push_back({0, x, 0, B->block_volume(x)});
+        TT_TRY(build_gather(ctx, nb, {B}, cp->bgather));
+      }
+    }
     if (ws_elems < max_uel)
       return fail(TT_E_OOM, "workspace holds %lld doubles; one (p,q) row of W needs %lld", (long long)ws_elems,
                   (long long)max_uel);
-    const int64_t w_off = cp->two_pass ? 0 : bm_elems;
+    const int64_t w_off = cp->two_pass ? 0 : bh_elems;
     double* wbase = (double*)workspace + w_off;
     const int64_t w_elems = ws_elems - w_off;
     if (!cp->two_pass) {
-      cp->Bm->data = (double*)workspace;
-      cp->Bm->capacity = bm_elems;
+      cp->Bh->data = cp->Bs->data = (double*)workspace;
+      cp->Bh->capacity = cp->Bs->capacity = bh_elems;
     }
     auto flush = [&](std::vector<const Unit*>& cur) -> tt_status {
       if (cur.empty()) return TT_OK;
@@ -2387,7 +2445,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       if (bt.Wb->packed_elems > w_elems) {
         const long long need = (long long)bt.Wb->packed_elems;
         delete bt.Wb;
-        return fail(TT_E_OOM, "workspace after Bm holds %lld doubles; one (p,q) row of W needs %lld",
+        return fail(TT_E_OOM, "workspace after Bh holds %lld doubles; one (p,q) row of W needs %lld",
                     (long long)w_elems, need);
       }
       bt.Wb->data = wbase;
@@ -2421,6 +2479,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   const std::string x1 = std::string(1, p) + r + L, x2 = std::string(1, q) + s + L;   // W = X(prL) X(qsL)
   std::string bsw(bl);                                                              // B with r <-> s
   std::swap(bsw[b.find(r)], bsw[b.find(s)]);
+  const std::string vsw = std::string(1, p) + q + s + r;                              // W read as (p,q,s,r)
   if (ctx->prepare_only) {   // build every batch plan now (they are cached), launch nothing
     for (auto& bt : cp->batches) {
       std::shared_ptr<ContractPlan> pw, pu, px;
@@ -2430,7 +2489,8 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
         TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, B, bl, beta, pu, &dummy, bt.copt));
         TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, B, bsw.c_str(), 1.0, px, &dummy, bt.copt));
       } else {
-        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
+        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bh, bl, beta, pu, &dummy, bt.copt));
+        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vsw.c_str(), cp->Bs, bl, 1.0, px, &dummy, bt.copt));
       }
     }
     return TT_OK;
@@ -2438,8 +2498,9 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   reset_stats(ctx);
   TT_TRY(run_gather(ctx, cp->bgather, {B}));
   if (!cp->two_pass) {
-    TT_TRY(run_local_add(ctx, *cp->copy_plan, cp->Bm, B, 0.0, 1.0));
-    TT_TRY(run_local_add(ctx, *cp->swap_plan, cp->Bm, B, 1.0, -1.0));
+    TT_TRY(run_local_add(ctx, *cp->copy_plan, cp->Bh, B, 0.0, 1.0));
+    TT_TRY(run_local_add(ctx, *cp->swap_plan, cp->Bh, B, 1.0, -1.0));
+    TT_TRY(run_gather(ctx, cp->hgather, {cp->Bh}));
   }
   double exec = 0, build = 0;
   int64_t tasks = 0;
@@ -2457,17 +2518,19 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       exec += pu->flops + px->flops;
       tasks += pu->tasks + px->tasks;
     } else {
-      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bm, bl, beta, pu, &dummy, bt.copt));
-      TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Wb, vl, cp->Bm, bl));
-      exec += pu->flops;
-      tasks += pu->tasks;
+      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bh, bl, beta, pu, &dummy, bt.copt));
+      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vsw.c_str(), cp->Bs, bl, 1.0, px, &dummy, bt.copt));
+      TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Wb, vl, cp->Bh, bl));
+      TT_TRY(launch_plan(ctx, *px, C, cl, 1.0, -alpha, bt.Wb, vsw.c_str(), cp->Bs, bl));
+      exec += pu->flops + px->flops;
+      tasks += pu->tasks + px->tasks;
     }
   }
   ctx->last.c_blocks = (int64_t)cp->wplan->my.size();
   ctx->last.tasks = tasks;
   ctx->last.flops = cp->vplan->flops;       // algorithmic: the defined contraction over V's block map
-  ctx->last.aux_flops = build + exec;       // executed: W build + consume against Bm
-  ctx->last.gathered_bytes = cp->bgather.recv_bytes;
+  ctx->last.aux_flops = build + exec;       // executed: W build + consume (passes 1 and 2, or two-pass)
+  ctx->last.gathered_bytes = cp->bgather.recv_bytes + (cp->two_pass ? 0 : cp->hgather.recv_bytes);
   ctx->last.work_items = (int64_t)cp->batches.size();
   return TT_OK;
 }

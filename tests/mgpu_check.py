@@ -108,6 +108,48 @@ def main():
     t2 = torch.from_numpy(mine2).cuda()
     dist.all_reduce(t2)
     assembled2 = t2.cpu().numpy()
+    # again with T's (c,d) / (d,c) blocks co-located and T, R compact: each rank forms its own half of
+    # Bm = T - T(c<->d) and the half is all-gathered (T itself is never gathered)
+    T3 = tt.Tensor(ctx, [sv, sv, so, so], spin=([0, 1], [2, 3]))
+    own3 = np.full(T3.nblocks, -1, np.int32)
+    for blk in range(T3.nblocks):
+        if T3.nz[blk]:
+            cc = list(np.unravel_index(blk, T3.grid))
+            cc[0], cc[1] = min(cc[0], cc[1]), max(cc[0], cc[1])
+            own3[blk] = int(np.ravel_multi_index(cc, T3.grid)) % world
+    T3.set_owner(own3)
+    T3.set_compact(True)
+    R3 = tt.Tensor(ctx, [sv, sv, so, so], spin=([0, 1], [2, 3]))
+    tt.partition_split(ctx, R3, "abij", P["Vv"], "abcd", P["T"], "cdij", group_dims=(0, 1))
+    R3.set_compact(True)
+    t3b = torch.empty(T3.storage_elems, dtype=torch.float64, device="cuda")
+    r3b = torch.full((R3.storage_elems,), float("nan"), dtype=torch.float64, device="cuda")
+    T3.bind(t3b)
+    R3.bind(r3b)
+    tt.fill_synthetic(ctx, T3, 3, 5)
+    ws3 = torch.empty(T3.packed_elems + 32 + 40 ** 4 * 16, dtype=torch.float64, device="cuda")
+    tt.contract_cholesky(ctx, R3, "abij", 0.0, 0.5, X, "abcd", T3, "cdij", ws3)
+    st3 = ctx.stats()
+    g3 = R3.download()
+    ctx.sync()
+    mine3 = np.zeros(R3.packed_elems)
+    for blk in range(R3.nblocks):
+        if not R3.nz[blk]:
+            continue
+        o, so3 = R3.blk_off[blk], R3.storage_off[blk]
+        ext = [d.offsets[t + 1] - d.offsets[t] for d, t in zip(R3.dims, np.unravel_index(blk, R3.grid))]
+        n = int(np.prod(ext))
+        if R3.owner[blk] == rank:
+            mine3[o:o + n] = g3[so3:so3 + n]
+        inner = n // int(ext[0])
+        for (bb, lo, hi, ow) in R3.parts:
+            if bb == blk and ow == rank:
+                mine3[o + lo * inner:o + hi * inner] = g3[so3 + lo * inner:so3 + hi * inner]
+    t3 = torch.from_numpy(mine3).cuda()
+    dist.all_reduce(t3)
+    assembled3 = t3.cpu().numpy()
+    print(f"rank {rank}: co-located Cholesky ladder, T storage {T3.storage_elems} of {T3.packed_elems}, "
+          f"gathered {st3['gathered_bytes']} B", flush=True)
     torch.cuda.synchronize()
     got = P["R"].download()
     ctx.sync()
@@ -161,6 +203,11 @@ def main():
         err2 = np.abs(assembled2[live] - ref2[live]).max() / np.abs(ref2[live]).max()
         print(f"world {world}: Cholesky ladder normwise error vs oracle {err2:.3e}", flush=True)
         ok &= err2 <= 1e-11
+        ref3 = O.pack(orc["R"], O.contract(np.zeros_like(R2d), "abij", O.cholesky_v(Xd), "abcd", dense["T"], "cdij",
+                                           0.5, 0.0, cmask=m))
+        err3 = np.abs(assembled3[live] - ref3[live]).max() / np.abs(ref3[live]).max()
+        print(f"world {world}: co-located compact Cholesky ladder normwise error vs oracle {err3:.3e}", flush=True)
+        ok &= err3 <= 1e-11
         print("MGPU_CHECK", "PASS" if ok else "FAIL", flush=True)
     dist.barrier()
     ctx.close()

@@ -500,13 +500,13 @@ def _cholesky_problem(O_, V_, tO, tV, NL, tL, spin):
     return pb
 
 
-@pytest.mark.parametrize("spin,ws_rows,mode", [(True, 1, "bm"), (True, 100, "bm"), (False, 2, "bm"),
+@pytest.mark.parametrize("spin,ws_rows,mode", [(True, 1, "bh"), (True, 100, "bh"), (False, 2, "bh"),
                                                 (True, 1, "env"), (False, 2, "env"), (True, 3, "auto")])
 def test_contract_cholesky(env, spin, ws_rows, mode):
     """Implicit Eq. cc12 operand (NEXT-1): R(abij) = beta*R + alpha*sum V(abcd) T(cdij) with V built
-    batch by batch from X in a small workspace == oracle with V formed explicitly.  mode "bm": the
-    workspace holds Bm = T - T(c<->d); "env"/"auto": the two-pass consume (forced, or because the
-    workspace holds only W rows)."""
+    batch by batch from X in a small workspace == oracle with V formed explicitly.  mode "bh": the
+    workspace holds the r_t <= s_t half of Bm = T - T(c<->d); "env"/"auto": the two-pass consume
+    (forced, or because the workspace holds only W rows)."""
     tt, torch = env
     pb = _cholesky_problem(8, 12, 2, 3, 10, 5, spin) if spin else _cholesky_problem(5, 9, 3, 4, 7, 4, False)
     if mode == "env":

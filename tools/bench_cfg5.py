@@ -5,10 +5,12 @@ N_L = 2(O+V), owner-computes over the GPUs of one box (torchrun, NCCL).
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/bench_cfg5.py            # strong
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/bench_cfg5.py --weak     # weak
 
-Placement: X replicated; T distributed round robin and all-gathered inside every call (the input-tile
+Placement: X replicated; T distributed over (c,d)-symmetric block pairs (T(c,d,i,j) and T(d,c,i,j) on
+one rank, round robin over the pairs) with compact storage: each rank forms its half of
+Bm = T - T(c<->d) from its own blocks and the half is all-gathered inside every call (the input-tile
 gather of §8(e)); R split by (a,b) rows with tt_partition_split_cost on the executed cost of the
-implicit ladder and stored compactly (each rank allocates only its rows).  The workspace holds W
-rows (and Bm = T - T(c<->d) when it fits; otherwise the two-pass consume).  Weak scaling keeps the
+implicit ladder, compact.  The workspace holds that half of Bm plus W rows (--ws-gb 0: sized
+automatically; too small a workspace selects the two-pass consume).  Weak scaling keeps the
 per-GPU FLOPs constant: V = 714 / 848 / 1010 / 1200 for 1 / 2 / 4 / 8 GPUs.
 
 Timing: W warm-up calls, then K calls bracketed by a barrier + CUDA events, max over ranks.
@@ -60,7 +62,7 @@ def main():
     ap.add_argument("--tile", type=int, default=64)
     ap.add_argument("--nl", type=int, default=0, help="0: 2(O+V)")
     ap.add_argument("--ltile", type=int, default=450)
-    ap.add_argument("--ws-gb", type=float, default=14.0)
+    ap.add_argument("--ws-gb", type=float, default=0.0, help="0: half of Bm + one W row + 1 GB")
     ap.add_argument("--weak", action="store_true")
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=1)
@@ -92,6 +94,23 @@ def main():
     if world > 1:
         tt.partition_split_cost(ctx, R, cholesky_ladder_costs(tt, R, T, tv, NL), group_dims=(0, 1))
         R.set_compact(True)
+        own = np.full(T.nblocks, -1, np.int32)
+        pair_id = {}
+        for blk in np.flatnonzero(T.nz):
+            c = list(np.unravel_index(blk, T.grid))
+            c[0], c[1] = min(c[0], c[1]), max(c[0], c[1])
+            own[blk] = pair_id.setdefault(tuple(c), len(pair_id)) % world
+        T.set_owner(own)
+        T.set_compact(True)
+    sz = np.diff(tv.offsets)
+    if a.ws_gb <= 0:      # half of Bm (tile pairs c_t <= d_t of T's map) + the largest W row + 1 GB
+        half = 0
+        for blk in np.flatnonzero(T.nz):
+            c = np.unravel_index(blk, T.grid)
+            if c[0] <= c[1]:
+                half += int(sz[c[0]] * sz[c[1]] * np.diff(to.offsets)[c[2]] * np.diff(to.offsets)[c[3]])
+        wrow = int(sz.max() ** 2 * (V // 2) ** 2)
+        a.ws_gb = (half + wrow) * 8e-9 + 1.0
     bufs = {}
     for name, Tn, tag in (("R", R, 3), ("T", T, 5), ("X", X, 7)):
         bufs[name] = torch.empty(Tn.storage_elems, dtype=torch.float64, device="cuda")
