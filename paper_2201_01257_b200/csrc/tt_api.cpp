@@ -478,13 +478,14 @@ tt_status check_bound(tt_tensor t, const char* which) {
 
 // Internal contraction options (used by the implicit-operand driver): `local` plans compute exactly
 // the listed C parts of this rank and never gather (the operands are local / replicated);
-// `no_a_needs` plans gather only B (A is a metadata-only implicit operand).
+// `no_gather` plans list this rank's C parts (ownership) but build no gather (accounting plans of
+// the implicit-operand driver, which moves its operands itself).
 struct PartSel {
   int64_t blk, lo, hi;
 };
 struct ContractOpts {
   bool local = false;
-  bool no_a_needs = false;
+  bool no_gather = false;
   std::vector<PartSel> sel;
   std::string tag;
 };
@@ -1509,20 +1510,21 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
         for (auto& h : hr) {
           const int64_t lo = h.first / cin, hi = h.second / cin;
           if (r == ctx->rank) pl.my.push_back({(int)g, lo, hi});
+          if (opts.no_gather) continue;
           for (int64_t t = ht.ptr[g]; t < ht.ptr[g + 1]; ++t) {
             int64_t e0, e1;
-            if (!opts.no_a_needs) {
-              sub_range_inner(A, ht.a_blk[t], a_same0, lo, hi, &e0, &e1);
-              need[r].push_back({0, ht.a_blk[t], e0, e1});
-            }
+            sub_range_inner(A, ht.a_blk[t], a_same0, lo, hi, &e0, &e1);
+            need[r].push_back({0, ht.a_blk[t], e0, e1});
             sub_range_inner(B, ht.b_blk[t], b_same0, lo, hi, &e0, &e1);
             need[r].push_back({bop, ht.b_blk[t], e0, e1});
           }
         }
       }
     }
-    if (A == B) TT_TRY(build_gather(ctx, need, {A}, pl.gp));
-    else TT_TRY(build_gather(ctx, need, {A, B}, pl.gp));
+    if (!opts.no_gather) {
+      if (A == B) TT_TRY(build_gather(ctx, need, {A}, pl.gp));
+      else TT_TRY(build_gather(ctx, need, {A, B}, pl.gp));
+    }
   }
   // stats for this rank
   {
@@ -2354,7 +2356,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     TT_TRY(local_add_plan(ctx, cp->Bh, B, sw, 1.0, cp->swap_plan, &mine));
     // SPMD plans for this rank's C parts: V map (algorithmic FLOPs) and W map (executed pairs)
     ContractOpts g;
-    g.no_a_needs = true;
+    g.no_gather = true;
     g.tag = "|cholV";
     bool dummy;
     TT_TRY(get_contract_plan(ctx, C, cl, cp->Vmeta, vl, B, bl, beta, cp->vplan, &dummy, g));
