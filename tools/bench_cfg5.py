@@ -20,6 +20,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -70,6 +71,14 @@ def main():
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    t_start = time.time()
+
+    def log(msg):
+        if rank == 0:
+            free, tot = torch.cuda.mem_get_info()
+            print(f"[{time.time() - t_start:8.1f} s] {msg} (free {free / 1e9:.1f} of {tot / 1e9:.1f} GB)",
+                  file=sys.stderr, flush=True)
+
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     nid = None
@@ -118,8 +127,11 @@ def main():
         tt.fill_synthetic(ctx, Tn, SEED, tag)
     ws = torch.empty(int(a.ws_gb * 1e9 / 8), dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
+    log(f"inputs filled, workspace {a.ws_gb:.1f} GB")
     for _ in range(a.warmup):
         tt.contract_cholesky(ctx, R, "abij", 0.0, ALPHA, X, "abcd", T, "cdij", ws)
+        torch.cuda.synchronize()
+        log("warm-up call done")
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
