@@ -63,7 +63,8 @@ def main():
     ap.add_argument("--tile", type=int, default=64)
     ap.add_argument("--nl", type=int, default=0, help="0: 2(O+V)")
     ap.add_argument("--ltile", type=int, default=450)
-    ap.add_argument("--ws-gb", type=float, default=0.0, help="0: half of Bm + one W row + 1 GB")
+    ap.add_argument("--ws-gb", type=float, default=0.0,
+                    help="0: half of Bm + one W row + 1 GB, capped by the free memory (else two-pass)")
     ap.add_argument("--weak", action="store_true")
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=1)
@@ -103,28 +104,42 @@ def main():
     if world > 1:
         tt.partition_split_cost(ctx, R, cholesky_ladder_costs(tt, R, T, tv, NL), group_dims=(0, 1))
         R.set_compact(True)
-        own = np.full(T.nblocks, -1, np.int32)
-        pair_id = {}
+        # T's (c,d) / (d,c) block pairs placed together, balanced by bytes (LPT over pair volumes)
+        offs = [np.diff(d.offsets) for d in T.dims]
+        pairs = {}
         for blk in np.flatnonzero(T.nz):
             c = list(np.unravel_index(blk, T.grid))
-            c[0], c[1] = min(c[0], c[1]), max(c[0], c[1])
-            own[blk] = pair_id.setdefault(tuple(c), len(pair_id)) % world
+            key = (min(c[0], c[1]), max(c[0], c[1]), c[2], c[3])
+            pairs.setdefault(key, []).append(int(blk))
+        vol = {k: sum(int(np.prod([offs[d][x] for d, x in enumerate(np.unravel_index(b, T.grid))])) for b in v)
+               for k, v in pairs.items()}
+        load = np.zeros(world)
+        own = np.full(T.nblocks, -1, np.int32)
+        for k in sorted(pairs, key=lambda k: (-vol[k], k)):
+            r = int(np.argmin(load))
+            load[r] += vol[k]
+            own[pairs[k]] = r
         T.set_owner(own)
         T.set_compact(True)
     sz = np.diff(tv.offsets)
-    if a.ws_gb <= 0:      # half of Bm (tile pairs c_t <= d_t of T's map) + the largest W row + 1 GB
-        half = 0
-        for blk in np.flatnonzero(T.nz):
-            c = np.unravel_index(blk, T.grid)
-            if c[0] <= c[1]:
-                half += int(sz[c[0]] * sz[c[1]] * np.diff(to.offsets)[c[2]] * np.diff(to.offsets)[c[3]])
-        wrow = int(sz.max() ** 2 * (V // 2) ** 2)
-        a.ws_gb = (half + wrow) * 8e-9 + 1.0
+    half = 0
+    for blk in np.flatnonzero(T.nz):
+        c = np.unravel_index(blk, T.grid)
+        if c[0] <= c[1]:
+            half += int(sz[c[0]] * sz[c[1]] * np.diff(to.offsets)[c[2]] * np.diff(to.offsets)[c[3]])
+    wrow = int(sz.max() ** 2 * (V // 2) ** 2)
     bufs = {}
     for name, Tn, tag in (("R", R, 3), ("T", T, 5), ("X", X, 7)):
         bufs[name] = torch.empty(Tn.storage_elems, dtype=torch.float64, device="cuda")
         Tn.bind(bufs[name])
         tt.fill_synthetic(ctx, Tn, SEED, tag)
+    if a.ws_gb <= 0:      # half of Bm (tile pairs c_t <= d_t of T's map) + the largest W row + 1 GB
+        free = torch.tensor([torch.cuda.mem_get_info()[0] / 1e9 - 4.0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(free, op=dist.ReduceOp.MIN)
+        a.ws_gb = min((half + wrow) * 8e-9 + 1.0, float(free[0]))
+        if a.ws_gb < (half + wrow) * 8e-9:
+            a.ws_gb = min(a.ws_gb, wrow * 8e-9 + 1.0)    # two-pass consume: W rows only
     ws = torch.empty(int(a.ws_gb * 1e9 / 8), dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     log(f"inputs filled, workspace {a.ws_gb:.1f} GB")
@@ -193,4 +208,10 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    except Exception:     # do not leave the other ranks waiting in NCCL
+        import traceback
+        traceback.print_exc()
+        sys.stderr.flush()
+        os._exit(1)
