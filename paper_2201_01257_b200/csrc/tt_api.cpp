@@ -1,6 +1,7 @@
 // tt_api.cpp -- host side of libtt: handles, validation, layout, task lists, partition, plans and
 // the C ABI entry points declared in include/tt.h.  Citations as in tt.h.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <atomic>
 #include <cstdarg>
@@ -2148,6 +2149,22 @@ tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, c
 
 namespace {
 
+// TT_DEBUG=1: phase trace of the implicit-operand driver on stderr (synchronises the stream)
+struct PhaseTrace {
+  tt_ctx ctx;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseTrace(tt_ctx c) : ctx(c), on(getenv("TT_DEBUG") && atoi(getenv("TT_DEBUG")) != 0),
+                                  t0(std::chrono::steady_clock::now()) {}
+  void operator()(const char* what, long long a = -1) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[tt rank %d] %10.1f ms  %s %lld\n", ctx->rank, ms, what, a);
+    fflush(stderr);
+  }
+};
+
 struct CholBatch {
   tt_tensor Wb = nullptr;            // scratch W blocks of the batch (bound to the workspace)
   ContractOpts wopt, copt;           // local build / consume selections
@@ -2270,6 +2287,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   TT_TRY(check_bound(B, "B"));
   if (!workspace || ws_elems <= 0) return fail(TT_E_UNBOUND, "no workspace bound");
   DeviceGuard dg(ctx->device);
+  PhaseTrace trace(ctx);
 
   char keybuf[256];
   snprintf(keybuf, sizeof(keybuf), "chol|%llu.%llu|%llu.%llu|%llu.%llu|%s|%s|%s|%d|%p|%lld",
@@ -2498,11 +2516,15 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     return TT_OK;
   }
   reset_stats(ctx);
+  trace("cholesky: plans ready, batches", (long long)cp->batches.size());
   TT_TRY(run_gather(ctx, cp->bgather, {B}));
+  trace("B gathered, runs", (long long)(cp->bgather.recv.size() + cp->bgather.send.size()));
   if (!cp->two_pass) {
     TT_TRY(run_local_add(ctx, *cp->copy_plan, cp->Bh, B, 0.0, 1.0));
     TT_TRY(run_local_add(ctx, *cp->swap_plan, cp->Bh, B, 1.0, -1.0));
+    trace("Bh formed");
     TT_TRY(run_gather(ctx, cp->hgather, {cp->Bh}));
+    trace("Bh gathered, runs", (long long)(cp->hgather.recv.size() + cp->hgather.send.size()));
   }
   double exec = 0, build = 0;
   int64_t tasks = 0;
@@ -2527,7 +2549,9 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       exec += pu->flops + px->flops;
       tasks += pu->tasks + px->tasks;
     }
+    if (trace.on && (&bt - &cp->batches[0]) % 16 == 0) trace("batch done", (long long)(&bt - &cp->batches[0]));
   }
+  trace("cholesky done");
   ctx->last.c_blocks = (int64_t)cp->wplan->my.size();
   ctx->last.tasks = tasks;
   ctx->last.flops = cp->vplan->flops;       // algorithmic: the defined contraction over V's block map
