@@ -427,19 +427,44 @@ tt_status build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops
   return TT_OK;
 }
 
+// Exchange schedule: P-1 rounds; in round k every rank sends to rank+k and receives from rank-k,
+// and each round is cut into NCCL groups of at most kGatherGroupOps runs per direction (the i-th
+// group of a round holds the i-th slices of both lists, which the partner slices identically).
+// One group with thousands of point-to-point calls to several peers stalled NCCL at 4 ranks.
+constexpr size_t kGatherGroupOps = 128;
+
 tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops) {
   if (ctx->nranks <= 1 || (gp.recv.empty() && gp.send.empty())) return TT_OK;
   const char* err = nullptr;
   const NcclApi* api = nccl_api(&err);
   if (!api) return fail(TT_E_NCCL, "%s", err);
-  TT_TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
-  for (const Run& r : gp.send) {
-    TT_TRY(nccl_check(api->Send(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclSend"));
+  const int P = ctx->nranks, me = ctx->rank;
+  auto peer_range = [](const std::vector<Run>& v, int peer, size_t& b, size_t& e) {   // runs sorted by peer
+    b = 0;
+    while (b < v.size() && v[b].peer < peer) ++b;
+    e = b;
+    while (e < v.size() && v[e].peer == peer) ++e;
+  };
+  for (int k = 1; k < P; ++k) {
+    const int to = (me + k) % P, from = (me - k + P) % P;
+    size_t sb, se, rb, re;
+    peer_range(gp.send, to, sb, se);
+    peer_range(gp.recv, from, rb, re);
+    const size_t ns = se - sb, nr = re - rb;
+    const size_t ng = std::max((ns + kGatherGroupOps - 1) / kGatherGroupOps, (nr + kGatherGroupOps - 1) / kGatherGroupOps);
+    for (size_t g = 0; g < ng; ++g) {
+      TT_TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+      for (size_t i = sb + g * kGatherGroupOps; i < std::min(se, sb + (g + 1) * kGatherGroupOps); ++i) {
+        const Run& r = gp.send[i];
+        TT_TRY(nccl_check(api->Send(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclSend"));
+      }
+      for (size_t i = rb + g * kGatherGroupOps; i < std::min(re, rb + (g + 1) * kGatherGroupOps); ++i) {
+        const Run& r = gp.recv[i];
+        TT_TRY(nccl_check(api->Recv(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclRecv"));
+      }
+      TT_TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+    }
   }
-  for (const Run& r : gp.recv) {
-    TT_TRY(nccl_check(api->Recv(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclRecv"));
-  }
-  TT_TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
   return TT_OK;
 }
 
