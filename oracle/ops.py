@@ -239,3 +239,22 @@ def ladder_sample(vrow: np.ndarray, Tij: np.ndarray, alpha: float) -> float:
     vrow = v(a,b,:,:), Tij = T(:,:,i,j); sequential-order sum over r then s."""
     return alpha * float(np.sum(vrow * Tij))
 
+
+
+# ----------------------------------------------------------------------------- Freivalds check
+
+def freivalds(c_blk: np.ndarray, c_lbl: str, a_sub: np.ndarray, a_lbl: str, b_sub: np.ndarray, b_lbl: str,
+              x: np.ndarray, alpha: float, beta: float, c0_blk: np.ndarray):
+    """SURVEY §8(c) step 5 (Freivalds): for one output block C_blk = beta*C0 + alpha*sum A.B, with
+    x random over the C labels that come from B, returns (C_blk . x, beta*C0 . x + alpha*A.(B.x)).
+    a_sub / b_sub are the operands restricted to the block's free index ranges (all contracted
+    indices, zero blocks zero).  O(|A| + |B|) instead of O(|C| K); a wrong element of C changes the
+    left side for almost every x.  Products by numpy.einsum (a library primitive)."""
+    nb = "".join(l for l in c_lbl if l in b_lbl)
+    na = "".join(l for l in c_lbl if l in a_lbl)
+    con = "".join(l for l in a_lbl if l in b_lbl)
+    y = np.einsum(f"{b_lbl},{nb}->{con}", b_sub, x)
+    z = np.einsum(f"{a_lbl},{con}->{na}", a_sub, y)
+    lhs = np.einsum(f"{c_lbl},{nb}->{na}", c_blk, x)
+    rhs = beta * np.einsum(f"{c_lbl},{nb}->{na}", c0_blk, x) + alpha * z
+    return lhs, rhs

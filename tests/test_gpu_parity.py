@@ -301,7 +301,8 @@ def test_fig5_program(env):
 def test_config2_full_size_sampled(env):
     """BASELINE configs[1] (the bench workload: ladder O=40 V=200 tile 40) at full size, in the
     bench launch configuration: 200 sampled outputs (every C block) vs the oracle element by element
-    (K = 40000 each), plus the inputs' fill checked on the same samples."""
+    (K = 40000 each), then a Freivalds check of every output block (inputs regenerated on the host
+    by the seeded generator)."""
     tt, torch = env
     pb = ccsd_problem(40, 200, 40, 40, False, terms=("ladder",))
     ctx = new_ctx(tt, torch)
@@ -338,6 +339,23 @@ def test_config2_full_size_sampled(env):
         pos.append(offs[b] + ((loc[0] * 40 + loc[1]) * 40 + loc[2]) * 40 + loc[3])
     g = got[np.array(pos)]
     assert np.abs(g - ref).max() / np.abs(ref).max() <= TOL
+    # Freivalds over every output block: all 1.6e6 x 25 outputs, not samples
+    n = np.arange(200, dtype=np.int64)
+    t_sub = S.values(11, 5, ((n[:, None, None, None] * 200 + n[None, :, None, None]) * 40
+                             + np.arange(40)[None, None, :, None]) * 40 + np.arange(40)[None, None, None, :])
+    worst = 0.0
+    for b in range(R.nblocks()):
+        o = R.block_origin(b)
+        ra, rb = np.arange(o[0], o[0] + 40), np.arange(o[1], o[1] + 40)
+        v_sub = S.values(11, 4, ((ra[:, None, None, None] * 200 + rb[None, :, None, None]) * 200
+                                 + n[None, None, :, None]) * 200 + n[None, None, None, :])
+        c0 = S.values(11, 3, ((ra[:, None, None, None] * 200 + rb[None, :, None, None]) * 40
+                              + np.arange(40)[None, None, :, None]) * 40 + np.arange(40)[None, None, None, :])
+        c_blk = got[offs[b]:offs[b] + 40 ** 4].reshape(40, 40, 40, 40)
+        x = rng.uniform(-1.0, 1.0, (40, 40))
+        lhs, rhs = O.freivalds(c_blk, "abij", v_sub, "abcd", t_sub, "cdij", x, 1.0, 1.0, c0)
+        worst = max(worst, float(np.abs(lhs - rhs).max() / np.abs(rhs).max()))
+    assert worst <= TOL, worst
 
 
 @pytest.mark.parametrize("a_lbl", ["abij", "ijab", "aibj", "jiba", "bajI".replace("I", "i")])

@@ -452,3 +452,35 @@ def test_cholesky_v_row_and_ladder_sample_pins():
         for s in range(n):
             bf += v[r, s] * T[r, s]
     assert abs(O.ladder_sample(v, T, 0.5) - 0.5 * bf) < 1e-14
+
+
+def test_freivalds_pins():
+    """Freivalds check: exact results give a residual at rounding level for a permuted-label ring
+    term; one perturbed element of C (1e-9 relative) is detected for random x; the right side is the
+    brute-force vector sum."""
+    rng = np.random.default_rng(3)
+    ext = dict(a=5, b=4, c=3, i=2, j=3, k=4)
+    A = rnd((ext["a"], ext["c"], ext["i"], ext["k"]), 7, 9)         # A(a,c,i,k)
+    B = rnd((ext["c"], ext["b"], ext["k"], ext["j"]), 8, 9)         # B(c,b,k,j)
+    C0 = rnd((ext["a"], ext["b"], ext["i"], ext["j"]), 9, 9)
+    C = O.contract(C0.copy(), "abij", A, "acik", B, "cbkj", 0.7, 1.3)
+    x = rng.uniform(-1, 1, (ext["b"], ext["j"]))
+    lhs, rhs = O.freivalds(C, "abij", A, "acik", B, "cbkj", x, 0.7, 1.3, C0)
+    assert np.abs(lhs - rhs).max() <= 1e-13 * np.abs(lhs).max()
+    bf = np.zeros((ext["a"], ext["i"]))
+    for a in range(ext["a"]):
+        for i in range(ext["i"]):
+            s = 0.0
+            for b in range(ext["b"]):
+                for j in range(ext["j"]):
+                    t = 1.3 * C0[a, b, i, j]
+                    for c in range(ext["c"]):
+                        for k in range(ext["k"]):
+                            t += 0.7 * A[a, c, i, k] * B[c, b, k, j]
+                    s += t * x[b, j]
+            bf[a, i] = s
+    assert np.abs(rhs - bf).max() <= 1e-13 * np.abs(bf).max()
+    Cbad = C.copy()
+    Cbad[2, 1, 0, 2] *= 1 + 1e-9
+    lhs2, _ = O.freivalds(Cbad, "abij", A, "acik", B, "cbkj", x, 0.7, 1.3, C0)
+    assert np.abs(lhs2 - rhs).max() > 1e-11 * np.abs(C).max()
