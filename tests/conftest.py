@@ -9,6 +9,11 @@ if ROOT not in sys.path:
 
 
 def pytest_configure(config):
+    # a fresh checkout has no built artefacts: compile libtt.so / the C oracle once (no-op when up to date)
+    if not os.path.exists(os.path.join(ROOT, "paper_2201_01257_b200", "libtt.so")) or \
+            not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
+        import __graft_entry__
+        __graft_entry__.build()
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a); run on the GPU box")
     config.addinivalue_line("markers", "slow: longer CPU test")
 
