@@ -125,6 +125,16 @@ tt_status tt_tis_custom(tt_is is, int32_t n, const int64_t* sizes, tt_tis* out);
  * by the handle and valid until tt_tis_destroy. */
 tt_status tt_tis_info(tt_tis tis, int32_t* ntiles, const int64_t** offsets, const int8_t** tile_spin);
 tt_status tt_tis_destroy(tt_tis tis);
+/* Sub-spaces (P116-122 named ranges "first"/"second"; P152 `tK("first").labels<3>()`; P159 "string-based
+ * sub-spaces ... operations on different slices of the underlying allocated tensor").
+ *   tt_tis_sub    the tiles of `parent` covering [begin, end); both ends must be tile boundaries of the
+ *                 parent (TT_E_TILING otherwise).  Offsets are relative to begin, so a sub-space matches
+ *                 (S413) any tiled space with the same tile sizes and spins.
+ *   tt_tis_range  the sub-space of range `range` of the parent's index space (the paper's named
+ *                 sub-range; names live in the caller, the index is the range's position).
+ * The sub-space references its parent (keep it alive). */
+tt_status tt_tis_sub(tt_tis parent, int64_t begin, int64_t end, tt_tis* out);
+tt_status tt_tis_range(tt_tis parent, int32_t range, tt_tis* out);
 
 /* ------------------------------------------------------------------------------------------------
  * Tensor<double> (P129-140): blocks indexed by the Cartesian product of the tiles of its dimensions
@@ -171,6 +181,16 @@ tt_status tt_tensor_parts(tt_tensor t, int64_t* n, const int64_t** blk, const in
  * TT_E_UNSUPPORTED (on every rank alike).  upload/download move the storage buffer.  Must be
  * identical on every rank.  Default off (storage = the global packed layout). */
 tt_status tt_tensor_set_compact(tt_tensor t, int32_t on);
+/* Sliced view (P152, P159): a tensor whose dimension d is dims[d] = the tensor's own tiled space or a
+ * sub-space of it (tt_tis_sub / tt_tis_range of exactly T's dims[d]; TT_E_TILING otherwise).  The view's
+ * blocks ARE the parent's blocks at the shifted tile coordinates: same storage (the parent's current
+ * binding is used at every call), same packed offsets and owners, no copy.  A view can be an operand or
+ * the output of every operation; reads and writes go to the parent's memory.  Its block map, offsets
+ * and owners are captured at creation (re-create the view after changing the parent's ownership);
+ * views of compact or row-split tensors, views of views, and ownership / compact changes on a view are
+ * TT_E_UNSUPPORTED.  tt_fill_synthetic on a view uses the view's own global indices.  Destroy the view
+ * before its parent. */
+tt_status tt_tensor_view(tt_tensor T, const tt_tis* dims, tt_tensor* out);
 /* Storage size in doubles (what tt_tensor_bind needs) and the per-block storage offsets (nblocks
  * entries; -1 = not stored on this rank; block base, i.e. element e of block b is at off[b] + e).
  * Without compact storage these equal packed_elems / blk_off of tt_tensor_layout. */
@@ -222,6 +242,36 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, d
                       tt_tensor A, const char* a_lbl, tt_tensor B, const char* b_lbl);
 tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* a_lbl, tt_tensor B,
                              const char* b_lbl, double* result);
+
+/* Three-operand contraction through an intermediate (PAPER Eqs. cc9-cc11, P293-311):
+ *   C(c_lbl) = beta*C + alpha * sum A(a_lbl) * B(b_lbl) * D(d_lbl)
+ * e.g. cc9 "1/4 v^{ef}_{mn} t^{ij}_{ef} t^{mn}_{ab}": C = R "abij", A = v "efmn", B = t "efij", D = t "abmn",
+ * alpha = 1/4.  Every label must appear in exactly two of C, A, B, D (TT_E_LABEL).  The three pairings
+ * (A*B)*D, (A*D)*B, (B*D)*A are costed on the block maps: the intermediate I of a pair (X, Y) carries the
+ * labels of X then Y that survive (appear in the third operand or C), on their tiled spaces, and its
+ * block map is the set of blocks that receive at least one non-zero pair; the cost is the FLOPs
+ * (2*m*n*k per task, as tt_task_list) of I = X*Y plus C += I*Z.  The cheapest pairing (ties: the first in
+ * the order above; reading R26) runs as two tt_contract calls (I = 1*X*Y with beta 0, then
+ * C = beta*C + alpha*I*Z), I stored in the caller's workspace.
+ *   workspace  device memory of ws_elems doubles >= info->ws_elems (I's packed size), or NULL to
+ *              return only the plan (info) without computing.
+ *   info       (may be NULL) pair = 0/1/2 in the order above; i_lbl = the intermediate's labels;
+ *              flops[p] = factorized FLOPs of pairing p (-1: intermediate order > TT_MAX_ORDER);
+ *              naive_macs = multiply-adds of the unfactorized loop (one product per combination of
+ *              all label values whose C, A, B, D blocks are non-zero; n_o^4 n_u^4 for dense cc9;
+ *              -1 if the label tile grid exceeds 5e7 tuples); ws_elems = intermediate size in doubles.
+ * With nranks > 1 I is owned round robin (P210) and the second contraction gathers what it reads.
+ * tt_stats after the call = the sum over both contractions. */
+typedef struct {
+  int32_t pair;
+  char i_lbl[TT_MAX_ORDER + 1];
+  double flops[3];
+  double naive_macs;
+  int64_t ws_elems;
+} tt_contract3_info;
+tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha,
+                       tt_tensor A, const char* a_lbl, tt_tensor B, const char* b_lbl, tt_tensor D,
+                       const char* d_lbl, void* workspace, int64_t ws_elems, tt_contract3_info* info);
 
 /* Contraction with an IMPLICIT Cholesky-factored operand (PAPER Eq. cc12,
  * P312-318, the paper's CD-CCSD P325/P463):

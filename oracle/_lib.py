@@ -42,6 +42,10 @@ def lib():
         L.orc_dots.restype = None
         L.orc_matvec.argtypes = [ctypes.c_int64, ctypes.c_int64, f64p, f64p, f64p]
         L.orc_matvec.restype = None
+        L.orc_contract3_naive.argtypes = [ctypes.c_int, i64p, i64p, i64p, i64p, i64p, ctypes.c_int, i64p, i64p,
+                                          i64p, i64p, f64p, f64p, f64p, f64p, u8p, ctypes.c_double,
+                                          ctypes.c_double]
+        L.orc_contract3_naive.restype = None
         _lib = L
     return _lib
 

@@ -104,6 +104,22 @@ def tile_custom(space: IndexSpace, sizes: Sequence[int]) -> TiledIndexSpace:
     return TiledIndexSpace(space, offs, spins)
 
 
+def tile_sub(tis: TiledIndexSpace, begin: int, end: int) -> TiledIndexSpace:
+    """P152/P159 sub-space ``tK("first")``: the tiles of ``tis`` covering [begin, end), which must start
+    and end on tile boundaries; offsets relative to ``begin``."""
+    if begin >= end or begin not in tis.offsets or end not in tis.offsets:
+        raise OracleError("sub-space does not start and end on tile boundaries")
+    t0, t1 = tis.offsets.index(begin), tis.offsets.index(end)
+    sub = IndexSpace(end - begin)
+    return TiledIndexSpace(sub, [o - begin for o in tis.offsets[t0:t1 + 1]], list(tis.tile_spin[t0:t1]))
+
+
+def tile_range(tis: TiledIndexSpace, r: int) -> TiledIndexSpace:
+    """P120-121 named range ("first" = range 0, "second" = range 1) of the tiled space's index space."""
+    b, e, _ = tis.space.segments()[r]
+    return tile_sub(tis, b, e)
+
+
 @dataclass
 class Tensor:
     dims: List[TiledIndexSpace]
@@ -351,3 +367,56 @@ def partition_split(C: Tensor, cost: Sequence[int], cblocks: Sequence[int], grou
         for b in u["blocks"]:
             out[b] = parts
     return out
+
+
+# ----------------------------------------------------------------------------- NEXT-3 factorization
+
+def contract3_plan(C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str, D: Tensor, d_lbl: str):
+    """PAPER Eqs. cc9-cc11 (P293-311), reading R26: the three pairings (A*B)*D, (A*D)*B, (B*D)*A of the
+    three-operand term, each as two binary contractions through an intermediate I whose labels are those
+    of the pair (first operand's order, then the second's) that appear in the third operand or in C, and
+    whose non-zero blocks are those receiving at least one task.  Cost = the FLOPs of both task lists;
+    the cheapest pairing wins (ties: the first).  ``naive_macs`` = one product per combination of all
+    label values with C, A, B, D blocks all non-zero (the unfactorized cc9 loop, brute force)."""
+    ops = [(A, a_lbl), (B, b_lbl), (D, d_lbl)]
+    flops, cand = [], []
+    for x, y, z in ((0, 1, 2), (0, 2, 1), (1, 2, 0)):
+        (X, xl), (Y, yl), (Z, zl) = ops[x], ops[y], ops[z]
+        il, idims = "", []
+        for T, l in ((X, xl), (Y, yl)):
+            for d, ch in zip(T.dims, l):
+                if (ch in zl or ch in c_lbl) and ch not in il:
+                    il += ch
+                    idims.append(d)
+        if not il or len(il) > 8:
+            flops.append(-1.0)
+            cand.append(None)
+            continue
+        I = tensor_dense_map(idims)
+        cbl, ptr, _, _, cost1 = task_list(I, il, X, xl, Y, yl)
+        inz = [0] * I.nblocks()
+        for g, cb in enumerate(cbl):
+            if ptr[g + 1] > ptr[g]:
+                inz[cb] = 1
+        I.nz = inz
+        _, _, _, _, cost2 = task_list(C, c_lbl, I, il, Z, zl)
+        flops.append(float(sum(cost1) + sum(cost2)))
+        cand.append(il)
+    best = min((p for p in range(3) if flops[p] >= 0), key=lambda p: (flops[p], p))
+    # naive loop count
+    tis, order = {}, []
+    for T, l in ((C, c_lbl), (A, a_lbl), (B, b_lbl), (D, d_lbl)):
+        for d, ch in zip(T.dims, l):
+            if ch not in tis:
+                tis[ch] = d
+                order.append(ch)
+    macs = 0
+    for tup in product(*[range(tis[ch].ntiles) for ch in order]):
+        tile = dict(zip(order, tup))
+        if all(T.nz[T.block_id([tile[ch] for ch in l])] for T, l in ((C, c_lbl), (A, a_lbl), (B, b_lbl),
+                                                                      (D, d_lbl))):
+            v = 1
+            for ch in order:
+                v *= tis[ch].size(tile[ch])
+            macs += v
+    return {"pair": best, "i_lbl": cand[best], "flops": flops, "naive_macs": float(macs)}

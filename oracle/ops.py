@@ -141,6 +141,53 @@ def contract(C: np.ndarray, c_lbl: str, A: np.ndarray, a_lbl: str, B: np.ndarray
     return np.ascontiguousarray(np.where(cmask.astype(bool), new, out))
 
 
+def contract3_naive(C: np.ndarray, c_lbl: str, A: np.ndarray, a_lbl: str, B: np.ndarray, b_lbl: str,
+                    D: np.ndarray, d_lbl: str, alpha: float, beta: float,
+                    cmask: Optional[np.ndarray] = None) -> np.ndarray:
+    """PAPER Eq. cc9 evaluated as written (P293-300): C <- beta*C + alpha*sum A*B*D over every label not
+    in C, one product per combination of label values -- the unfactorized loop (oracle.c
+    orc_contract3_naive).  Each label must appear in exactly two of C, A, B, D.  Returns a new C."""
+    lbls = (c_lbl, a_lbl, b_lbl, d_lbl)
+    for l in lbls:
+        for x in l:
+            if sum(x in q for q in lbls) != 2:
+                raise ValueError(f"label {x} must appear in exactly two operands")
+    ext = {}
+    for arr, lbl in ((C, c_lbl), (A, a_lbl), (B, b_lbl), (D, d_lbl)):
+        for n, x in zip(arr.shape, lbl):
+            if ext.setdefault(x, n) != n:
+                raise ValueError(f"extent mismatch on label {x}")
+    summed = []
+    for l in (a_lbl, b_lbl, d_lbl):
+        for x in l:
+            if x not in c_lbl and x not in summed:
+                summed.append(x)
+    st = [_strides(X.shape) for X in (C, A, B, D)]
+
+    def strides_of(labels, k):
+        return _lib.i64([st[k][lbls[k].index(x)] if x in lbls[k] else 0 for x in labels] or [0])
+
+    ext_f = _lib.i64([ext[x] for x in c_lbl])
+    ext_k = _lib.i64([ext[x] for x in summed] or [1])
+    sf = [strides_of(c_lbl, k) for k in range(4)]
+    sk = [strides_of(summed, k) for k in range(1, 4)]
+    Co = _lib.f64(C).copy()
+    Ao, Bo, Do = _lib.f64(A), _lib.f64(B), _lib.f64(D)
+    m = None if cmask is None else np.ascontiguousarray(cmask, dtype=np.uint8)
+    P64, PD = ctypes.c_int64, ctypes.c_double
+    _lib.lib().orc_contract3_naive(len(c_lbl), _lib.ptr(ext_f, P64), *[_lib.ptr(x, P64) for x in sf], len(summed),
+                                   _lib.ptr(ext_k, P64), *[_lib.ptr(x, P64) for x in sk], _lib.ptr(Co, PD),
+                                   _lib.ptr(Ao, PD), _lib.ptr(Bo, PD), _lib.ptr(Do, PD),
+                                   None if m is None else _lib.ptr(m, ctypes.c_uint8), float(alpha), float(beta))
+    return Co
+
+
+def slice_of(D: np.ndarray, ranges) -> np.ndarray:
+    """P159 "operations on different slices of the underlying allocated tensor": the sub-array over the
+    index ranges [(begin, end)] of each dimension (a numpy view: writes go to D)."""
+    return D[tuple(slice(b, e) for b, e in ranges)]
+
+
 def add(C: np.ndarray, c_lbl: str, A: np.ndarray, a_lbl: str, alpha: float, beta: float,
         cmask: Optional[np.ndarray] = None) -> np.ndarray:
     """P173 ``A(i,l) += alpha * D(l,i)``: C[x] <- beta*C[x] + alpha*A[pi(x)] (beta=0: C not read)."""

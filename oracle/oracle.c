@@ -100,3 +100,45 @@ void orc_matvec(int64_t rows, int64_t cols, const double* M, const double* x, do
     y[r] = s;
   }
 }
+
+/* Naive three-operand contraction (PAPER Eq. cc9, P293-300: the unfactorized n_o^4 n_u^4 loop):
+ *   C[x] <- beta*C[x] + alpha * sum_{y} (A[.] * B[.]) * D[.]
+ * free labels (C order) ext_f[nf] with strides in C/A/B/D (0 = absent); summed labels (every label
+ * not in C, order of first appearance in A, then B, then D) ext_k[nk] with strides in A/B/D.
+ * Sequential sum per output element, row-major over the summed tuple.  cmask as orc_contract_naive. */
+void orc_contract3_naive(int nf, const int64_t* ext_f, const int64_t* sfc, const int64_t* sfa,
+                         const int64_t* sfb, const int64_t* sfd, int nk, const int64_t* ext_k,
+                         const int64_t* ska, const int64_t* skb, const int64_t* skd, double* C,
+                         const double* A, const double* B, const double* D, const uint8_t* cmask,
+                         double alpha, double beta) {
+  int64_t fi[MAXL], ki[MAXL];
+  for (int d = 0; d < nf; ++d) { fi[d] = 0; if (ext_f[d] == 0) return; }
+  for (;;) {
+    int64_t oc = 0, oa = 0, ob = 0, od = 0;
+    for (int d = 0; d < nf; ++d) {
+      oc += fi[d] * sfc[d]; oa += fi[d] * sfa[d]; ob += fi[d] * sfb[d]; od += fi[d] * sfd[d];
+    }
+    if (cmask == NULL || cmask[oc]) {
+      double s = 0.0;
+      int empty = 0;
+      for (int d = 0; d < nk; ++d) { ki[d] = 0; if (ext_k[d] == 0) empty = 1; }
+      if (!empty) {
+        for (;;) {
+          int64_t ia = oa, ib = ob, id = od;
+          for (int d = 0; d < nk; ++d) { ia += ki[d] * ska[d]; ib += ki[d] * skb[d]; id += ki[d] * skd[d]; }
+          double ab = A[ia] * B[ib];
+          double p = ab * D[id];
+          s = s + p;
+          int d = nk - 1;
+          while (d >= 0) { if (++ki[d] < ext_k[d]) break; ki[d] = 0; --d; }
+          if (d < 0) break;
+        }
+      }
+      double as = alpha * s;
+      C[oc] = (beta == 0.0) ? as : beta * C[oc] + as;
+    }
+    int d = nf - 1;
+    while (d >= 0) { if (++fi[d] < ext_f[d]) break; fi[d] = 0; --d; }
+    if (d < 0) break;
+  }
+}

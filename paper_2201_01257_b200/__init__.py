@@ -48,6 +48,15 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class Contract3Info(ctypes.Structure):
+    _fields_ = [("pair", _i32), ("i_lbl", ctypes.c_char * 9), ("flops", _dbl * 3), ("naive_macs", _dbl),
+                ("ws_elems", _i64)]
+
+    def as_dict(self):
+        return {"pair": self.pair, "i_lbl": self.i_lbl.decode(), "flops": list(self.flops),
+                "naive_macs": self.naive_macs, "ws_elems": self.ws_elems}
+
+
 _SIGS = {
     "tt_ctx_create": [_i32, _vp, _i32, _i32, _vp, _P(_vp)],
     "tt_ctx_destroy": [_vp],
@@ -64,6 +73,9 @@ _SIGS = {
     "tt_tis_custom": [_vp, _i32, _vp, _P(_vp)],
     "tt_tis_info": [_vp, _P(_i32), _P(_P(_i64)), _P(_P(ctypes.c_int8))],
     "tt_tis_destroy": [_vp],
+    "tt_tis_sub": [_vp, _i64, _i64, _P(_vp)],
+    "tt_tis_range": [_vp, _i32, _P(_vp)],
+    "tt_tensor_view": [_vp, _vp, _P(_vp)],
     "tt_tensor_create": [_vp, _i32, _vp, _vp, _P(_vp)],
     "tt_tensor_create_spin": [_vp, _i32, _vp, _u32, _u32, _P(_vp)],
     "tt_tensor_info": [_vp, _P(_i32), _P(_i64), _P(_i64)],
@@ -81,6 +93,8 @@ _SIGS = {
     "tt_contract": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p],
     "tt_contract_cholesky": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
                              _i64],
+    "tt_contract3": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
+                     ctypes.c_char_p, _vp, _i64, _vp],
     "tt_contract_scalar": [_vp, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _P(_dbl)],
     "tt_task_list": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _i32, _vp, _vp, _vp,
                      _vp, _vp, _i64, _P(_i64), _P(_i64)],
@@ -205,9 +219,12 @@ class Context:
 
 
 class IndexSpace:
-    """IndexSpace (P116-122).  ``ranges`` = [(begin, end)], ``spins`` = [+1/-1] per range (P138)."""
+    """IndexSpace (P116-122).  ``ranges`` = [(begin, end)], ``spins`` = [+1/-1] per range (P138),
+    ``names`` = optional names of the ranges (P120-121 "first"/"second"; used by TiledIndexSpace(name))."""
 
-    def __init__(self, extent: int, ranges: Optional[Sequence] = None, spins: Optional[Sequence[int]] = None):
+    def __init__(self, extent: int, ranges: Optional[Sequence] = None, spins: Optional[Sequence[int]] = None,
+                 names: Optional[Sequence[str]] = None):
+        self.names = list(names or [])
         h = _vp()
         be = np.asarray([x for r in (ranges or []) for x in r], dtype=np.int64)
         sp = np.asarray(spins, dtype=np.int8) if spins is not None else None
@@ -223,11 +240,16 @@ class IndexSpace:
 
 
 class TiledIndexSpace:
-    """TiledIndexSpace (P125-127): fixed ``tile`` or custom ``sizes``."""
+    """TiledIndexSpace (P125-127): fixed ``tile`` or custom ``sizes``.  ``tis("first")`` / ``tis.sub(b, e)``
+    give the sub-space of a named range / of [b, e) (P152, P159; tt_tis_range / tt_tis_sub)."""
 
-    def __init__(self, space: IndexSpace, tile: Optional[int] = None, sizes: Optional[Sequence[int]] = None):
+    def __init__(self, space: IndexSpace, tile: Optional[int] = None, sizes: Optional[Sequence[int]] = None,
+                 _handle=None, _parent=None):
         h = _vp()
-        if sizes is not None:
+        self.parent = _parent
+        if _handle is not None:
+            h = _handle
+        elif sizes is not None:
             s = np.asarray(sizes, dtype=np.int64)
             _check(_lib.tt_tis_custom(space.h, len(s), _ptr(s), ctypes.byref(h)))
         else:
@@ -240,6 +262,18 @@ class TiledIndexSpace:
         self.ntiles = n.value
         self.offsets = np.ctypeslib.as_array(off, (n.value + 1,)).copy()
         self.spin = np.ctypeslib.as_array(sp, (n.value,)).copy() if n.value else np.zeros(0, np.int8)
+        self.extent = int(self.offsets[-1])
+
+    def sub(self, begin: int, end: int) -> "TiledIndexSpace":
+        h = _vp()
+        _check(_lib.tt_tis_sub(self.h, int(begin), int(end), ctypes.byref(h)))
+        return TiledIndexSpace(self.space, _handle=h, _parent=self)
+
+    def __call__(self, name) -> "TiledIndexSpace":
+        r = self.space.names.index(name) if isinstance(name, str) else int(name)
+        h = _vp()
+        _check(_lib.tt_tis_range(self.h, r, ctypes.byref(h)))
+        return TiledIndexSpace(self.space, _handle=h, _parent=self)
 
     def __del__(self):  # pragma: no cover
         try:
@@ -252,10 +286,13 @@ class Tensor:
     """Tensor<double> (P129-140) with a non-zero block map: explicit ``nz`` (u8 per block, row-major)
     or the spin rule ``spin=(upper_dims, lower_dims)`` (reading R7)."""
 
-    def __init__(self, ctx: Context, dims: Sequence[TiledIndexSpace], nz=None, spin=None):
+    def __init__(self, ctx: Context, dims: Sequence[TiledIndexSpace], nz=None, spin=None, _view_of=None):
         h = _vp()
         arr = (_vp * len(dims))(*[d.h.value if isinstance(d.h, _vp) else d.h for d in dims])
-        if spin is not None:
+        self.parent = _view_of
+        if _view_of is not None:
+            _check(_lib.tt_tensor_view(_view_of.h, arr, ctypes.byref(h)))
+        elif spin is not None:
             up = sum(1 << d for d in spin[0])
             lo = sum(1 << d for d in spin[1])
             _check(_lib.tt_tensor_create_spin(ctx.h, len(dims), arr, up, lo, ctypes.byref(h)))
@@ -289,9 +326,16 @@ class Tensor:
             np.ctypeslib.as_array(pb, (k,)) if k else [], np.ctypeslib.as_array(plo, (k,)) if k else [],
             np.ctypeslib.as_array(phi, (k,)) if k else [], np.ctypeslib.as_array(pow_, (k,)) if k else [])]
 
+    def view(self, dims: Sequence[TiledIndexSpace]) -> "Tensor":
+        """Sliced view over sub-spaces of this tensor's dims (P152, P159; tt_tensor_view): no copy, the
+        view reads and writes this tensor's storage."""
+        v = Tensor(self.ctx, dims, _view_of=self)
+        v.storage = self.storage
+        return v
+
     @property
     def shape(self):
-        return tuple(int(d.space.extent) for d in self.dims)
+        return tuple(int(d.extent) for d in self.dims)
 
     @property
     def grid(self):
@@ -373,6 +417,18 @@ def contract_cholesky(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: f
         ws_elems = int(workspace.numel())
     _check(_lib.tt_contract_cholesky(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), X.h, _b(v_lbl), B.h,
                                      _b(b_lbl), _vp(_devptr(workspace)), int(ws_elems)))
+
+
+def contract3(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str, B: Tensor,
+              b_lbl: str, D: Tensor, d_lbl: str, workspace=None, ws_elems: Optional[int] = None) -> dict:
+    """Three-operand contraction through the cheapest intermediate (PAPER Eqs. cc9-cc11; tt_contract3).
+    ``workspace=None`` only plans: returns the pairing, its costs and the workspace size."""
+    info = Contract3Info()
+    ws = _vp(_devptr(workspace)) if workspace is not None else None
+    n = int(ws_elems if ws_elems is not None else (workspace.numel() if workspace is not None else 0))
+    _check(_lib.tt_contract3(ctx.h, C.h, _b(c_lbl), beta, alpha, A.h, _b(a_lbl), B.h, _b(b_lbl), D.h, _b(d_lbl),
+                             ws, n, ctypes.byref(info)))
+    return info.as_dict()
 
 
 def contract_scalar(ctx: Context, alpha: float, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str) -> float:

@@ -83,6 +83,8 @@ struct tt_tis_s {
   std::vector<int64_t> offsets;  // ntiles + 1
   std::vector<int8_t> spin;      // per tile
   uint64_t uid = 0;
+  tt_tis parent = nullptr;       // sub-space (tt_tis_sub / tt_tis_range): the tiled space it slices
+  int32_t tile0 = 0;             // ... and the parent tile index of its tile 0
   int32_t ntiles() const { return (int32_t)offsets.size() - 1; }
   int64_t size(int t) const { return offsets[t + 1] - offsets[t]; }
 };
@@ -119,6 +121,7 @@ struct tt_tensor_s {
   std::vector<int64_t> pv_blk;              // flattened view for tt_tensor_parts
   std::vector<int32_t> pv_lo, pv_hi, pv_owner;
   bool any_split = false;
+  tt_tensor view_of = nullptr;     // sliced view (tt_tensor_view): blocks live in this tensor's storage
 
   int64_t ext0(int64_t b) const {
     int32_t c[TT_MAX_ORDER];
