@@ -1,0 +1,143 @@
+"""perturbative triples (T), PAPER Eqs. cc13, cc14, tensort, abt, tensort2 (P343-413).
+
+CPU: the oracle (oracle/triples.py) pinned against the DEFINITION <Phi_ijk^abc|V_N X|Phi> evaluated by
+second quantization on a tiny Fock space (independent of the printed 18-term expansion; it also fixes
+reading R27, the sign of the sixth term), sign / scaling / zero laws of Eq. cc14, and the by-triple
+matmul form against the element loops.  GPU: tt_triples_energy against the oracle (normwise on E).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import triples as TR
+
+
+# ------------------------------------------------------------------------ second quantization (tests only)
+
+def _op(kind, p, det):
+    """a_p^+ (kind 'c') or a_p ('a') on a determinant bit string; sign (-1)^(occupied below p)."""
+    occ = (det >> p) & 1
+    if (kind == "c" and occ) or (kind == "a" and not occ):
+        return None, 0
+    sign = -1 if bin(det & ((1 << p) - 1)).count("1") % 2 else 1
+    return det ^ (1 << p), sign
+
+
+def _apply(ops, state, coef=1.0, out=None):
+    """sum coef * (op_1 op_2 ... op_n) |state>, the rightmost operator acting first."""
+    out = {} if out is None else out
+    for det, c in state.items():
+        d, s = det, c * coef
+        for kind, p in reversed(ops):
+            d, sg = _op(kind, p, d)
+            if d is None:
+                break
+            s *= sg
+        if d is not None:
+            out[d] = out.get(d, 0.0) + s
+    return out
+
+
+def _antisym_inputs(nO, nV, seed):
+    rng = np.random.default_rng(seed)
+    n = nO + nV
+    g = rng.uniform(-1, 1, (n, n, n, n))
+    g = g + g.transpose(2, 3, 0, 1)                      # real integrals: v^{pq}_{rs} = v^{rs}_{pq}
+    v = g - g.transpose(1, 0, 2, 3)
+    v = v - v.transpose(0, 1, 3, 2)                      # antisymmetrized <pq||rs>
+    t = rng.uniform(-1, 1, (nV, nV, nO, nO))
+    t = t - t.transpose(1, 0, 2, 3)
+    t = t - t.transpose(0, 1, 3, 2)                      # t^{ij}_{ab} = T2[a,b,i,j], antisymmetric
+    t1 = rng.uniform(-1, 1, (nV, nO))
+    return v, t, t1
+
+
+def _slices(v, nO):
+    o, w = slice(0, nO), slice(nO, None)
+    return v[o, o, o, w], v[w, o, w, w], v[o, o, w, w]   # Vooov(i,j,m,a), Vvovv(e,i,a,b), Voovv(i,j,a,b)
+
+
+def test_w_and_v1_equal_the_second_quantized_definition():
+    """<Phi_ijk^abc| V_N T2 |Phi> and <Phi_ijk^abc| V_N T1 |Phi> with V = 1/4 sum v^{pq}_{rs} a+_p a+_q a_s a_r,
+    V_N = V - sum_pq (sum_i v^{pi}_{qi}) a+_p a_q - const (normal order w.r.t. Phi), T2 = 1/4 sum
+    t^{ij}_{ab} a+_a a+_b a_j a_i, T1 = sum t^i_a a+_a a_i, |Phi_ijk^abc> = a+_a a+_b a+_c a_k a_j a_i |Phi>
+    (P365-369).  Matches Eq. tensort with reading R27 and Eq. tensort2 as printed; the printed sixth
+    term ("+") does not."""
+    nO, nV = 3, 4
+    n = nO + nV
+    v, t, t1 = _antisym_inputs(nO, nV, 5)
+    phi = {sum(1 << i for i in range(nO)): 1.0}
+    vir = range(nO, n)
+    T2phi, T1phi = {}, {}
+    for i, j in itertools.product(range(nO), repeat=2):
+        for a, b in itertools.product(vir, repeat=2):
+            _apply([("c", a), ("c", b), ("a", j), ("a", i)], phi, 0.25 * t[a - nO, b - nO, i, j], T2phi)
+    for i in range(nO):
+        for a in vir:
+            _apply([("c", a), ("a", i)], phi, t1[a - nO, i], T1phi)
+    gm = np.einsum("piqi->pq", v[:, :nO, :, :nO])
+    res2, res1 = {}, {}
+    for p, q, r, s in itertools.product(range(n), repeat=4):
+        if v[p, q, r, s] != 0.0:
+            _apply([("c", p), ("c", q), ("a", s), ("a", r)], T2phi, 0.25 * v[p, q, r, s], res2)
+            _apply([("c", p), ("c", q), ("a", s), ("a", r)], T1phi, 0.25 * v[p, q, r, s], res1)
+    for p, q in itertools.product(range(n), repeat=2):
+        _apply([("c", p), ("a", q)], T2phi, -gm[p, q], res2)
+        _apply([("c", p), ("a", q)], T1phi, -gm[p, q], res1)
+    Vooov, Vvovv, Voovv = _slices(v, nO)
+    checked = 0
+    for i, j, k in itertools.combinations(range(nO), 3):
+        for a, b, c in itertools.combinations(range(nV), 3):
+            ket = _apply([("c", a + nO), ("c", b + nO), ("c", c + nO), ("a", k), ("a", j), ("a", i)], phi)
+            w_def = sum(res2.get(d, 0.0) * x for d, x in ket.items())
+            v1_def = sum(res1.get(d, 0.0) * x for d, x in ket.items())
+            A, B = TR.w_terms(Vooov, Vvovv, t, i, j, k, a, b, c)
+            assert abs(A + B - w_def) <= 1e-13 * max(1.0, abs(w_def))
+            assert abs(TR.v1_term(Voovv, t1, i, j, k, a, b, c) - v1_def) <= 1e-13 * max(1.0, abs(v1_def))
+            # the sixth term as printed ("+") would add 2 * v^{ik}_{mc} t^{mj}_{ab}
+            printed = A + B + 2 * float(Vooov[i, k, :, c] @ t[a, b, :, j])
+            assert abs(printed - w_def) > 1e-6
+            checked += 1
+    assert checked == 4
+
+
+def _random_inputs(nO, nV, seed, antisym=False):
+    rng = np.random.default_rng(seed)
+    if antisym:
+        v, T2, T1 = _antisym_inputs(nO, nV, seed)
+        Vooov, Vvovv, Voovv = _slices(v, nO)
+    else:
+        T1 = rng.uniform(-1, 1, (nV, nO))
+        T2 = rng.uniform(-1, 1, (nV, nV, nO, nO))
+        Vooov = rng.uniform(-1, 1, (nO, nO, nO, nV))
+        Vvovv = rng.uniform(-1, 1, (nV, nO, nV, nV))
+        Voovv = rng.uniform(-1, 1, (nO, nO, nV, nV))
+    eo = rng.uniform(-2, -1, nO)      # S641 orbital-energy ranges: D < 0
+    ev = rng.uniform(1, 2, nV)
+    return T1, np.ascontiguousarray(T2), np.ascontiguousarray(Vooov), np.ascontiguousarray(Vvovv), \
+        np.ascontiguousarray(Voovv), eo, ev
+
+
+@pytest.mark.parametrize("nO,nV", [(4, 6), (5, 7), (3, 9)])
+def test_energy_by_triple_equals_element_loops(nO, nV):
+    args = _random_inputs(nO, nV, nO * 10 + nV)
+    E1, n1 = TR.energy(*args)
+    E2, n2 = TR.energy_by_triple(*args)
+    assert n1 == n2 == (nO * (nO - 1) * (nO - 2) // 6) * (nV * (nV - 1) * (nV - 2) // 6)
+    assert abs(E1 - E2) <= 1e-13 * abs(E1)
+
+
+def test_energy_laws():
+    """Eq. cc14: no T2 => W = 0 => E = 0; no T1 => E = sum W^2 / D < 0 (D < 0) and E(lambda T2) = lambda^2 E;
+    E is affine in T1 (the second term is linear in T1)."""
+    T1, T2, Vooov, Vvovv, Voovv, eo, ev = _random_inputs(4, 6, 1, antisym=True)
+    E0, _ = TR.energy(T1, 0 * T2, Vooov, Vvovv, Voovv, eo, ev)
+    assert E0 == 0.0
+    z = 0 * T1
+    E1, _ = TR.energy(z, T2, Vooov, Vvovv, Voovv, eo, ev)
+    E3, _ = TR.energy(z, 3 * T2, Vooov, Vvovv, Voovv, eo, ev)
+    assert E1 < 0 and abs(E3 - 9 * E1) <= 1e-13 * abs(E3)
+    Ea, _ = TR.energy(T1, T2, Vooov, Vvovv, Voovv, eo, ev)
+    Eb, _ = TR.energy(2 * T1, T2, Vooov, Vvovv, Voovv, eo, ev)
+    assert abs((Eb - E1) - 2 * (Ea - E1)) <= 1e-12 * abs(Eb)
