@@ -273,6 +273,40 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, 
                        tt_tensor A, const char* a_lbl, tt_tensor B, const char* b_lbl, tt_tensor D,
                        const char* d_lbl, void* workspace, int64_t ws_elems, tt_contract3_info* info);
 
+/* Perturbative triples correction (T) (PAPER Eqs. cc13, cc14, tensort, abt, tensort2,
+ * P343-413):
+ *   E(T) = sum_{i<j<k, a<b<c} (W + V1) * W / (e_i + e_j + e_k - e_a - e_b - e_c)          (Eq. cc14, R28)
+ *   W  = Eq. tensort: 9 terms v^{xy}_{mp} t^{mz}_{qr} summed over occupied m (A of Eq. abt) and 9 terms
+ *        v^{ex}_{pq} t^{yz}_{er} summed over virtual e (B); the sixth term with "-" (reading R27),
+ *   V1 = Eq. tensort2: the nine v^{xy}_{pq} t^z_r products.
+ * Inputs (real amplitudes and integrals; storage conventions of oracle/triples.py):
+ *   T1     t^i_a    as T1(a,i)          dims (V, O)      -- V = T1's dim 0 tiling, O = its dim 1 tiling
+ *   T2     t^{ij}_{ab} as T2(a,b,i,j)   dims (V, V, O, O)
+ *   Vooov  v^{ij}_{ma} as Vooov(i,j,m,a)  dims (O, O, O, V)
+ *   Vvovv  v^{ei}_{ab} as Vvovv(e,i,a,b)  dims (V, O, V, V)
+ *   Voovv  v^{ij}_{ab} as Voovv(i,j,a,b)  dims (O, O, V, V)
+ *   every dim must be T1's tiled-space object itself (TT_E_TILING); block maps are free (zero blocks read as
+ *   0); eps_o[n_o], eps_v[n_v]: DEVICE arrays of orbital energies (global index order).
+ * Execution: the summed labels m and e are first re-tiled into the workspace (one tile per spin range of
+ * O and V), then for batches of restricted tile triples (a_t<=b_t<=c_t, i_t<=j_t<=k_t, spin sums equal)
+ * the 18 terms run as DMMA contractions into a W batch in the workspace, and the energy kernel sums the
+ * elements with a<b<c, i<j<k (deterministic partials, fixed-order final sum).  With nranks > 1 the W
+ * blocks are partitioned by LPT on their volume, every input block must be TT_REPLICATED, and the energy
+ * is all-reduced (NCCL).  energy: HOST pointer; the call synchronises the stream.
+ *   workspace  device memory of ws_elems doubles >= info->ws_elems (coarse inputs + one W block; more
+ *              gives larger batches), or NULL to return only info.
+ *   info       (may be NULL) w_blocks_total / w_blocks (this rank) / batches; flops_alg = FLOPs of the
+ *              defined sums over the restricted elements (2 per multiply-add of the 18 terms); flops_exec
+ *              = FLOPs the contractions execute (whole tile triples); ws_elems = minimum workspace. */
+typedef struct {
+  int64_t w_blocks_total, w_blocks, batches;
+  double flops_alg, flops_exec;
+  int64_t ws_elems;
+} tt_triples_info;
+tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vooov, tt_tensor Vvovv,
+                            tt_tensor Voovv, const double* eps_o, const double* eps_v, void* workspace,
+                            int64_t ws_elems, double* energy, tt_triples_info* info);
+
 /* Contraction with an IMPLICIT Cholesky-factored operand (PAPER Eq. cc12,
  * P312-318, the paper's CD-CCSD P325/P463):
  *   C(c_lbl) = beta*C + alpha * sum V(v_lbl) * B(b_lbl),

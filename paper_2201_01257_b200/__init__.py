@@ -57,6 +57,14 @@ class Contract3Info(ctypes.Structure):
                 "naive_macs": self.naive_macs, "ws_elems": self.ws_elems}
 
 
+class TriplesInfo(ctypes.Structure):
+    _fields_ = [("w_blocks_total", _i64), ("w_blocks", _i64), ("batches", _i64), ("flops_alg", _dbl),
+                ("flops_exec", _dbl), ("ws_elems", _i64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _SIGS = {
     "tt_ctx_create": [_i32, _vp, _i32, _i32, _vp, _P(_vp)],
     "tt_ctx_destroy": [_vp],
@@ -95,6 +103,7 @@ _SIGS = {
                              _i64],
     "tt_contract3": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
                      ctypes.c_char_p, _vp, _i64, _vp],
+    "tt_triples_energy": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _P(_dbl), _vp],
     "tt_contract_scalar": [_vp, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _P(_dbl)],
     "tt_task_list": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _i32, _vp, _vp, _vp,
                      _vp, _vp, _i64, _P(_i64), _P(_i64)],
@@ -429,6 +438,21 @@ def contract3(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A:
     _check(_lib.tt_contract3(ctx.h, C.h, _b(c_lbl), beta, alpha, A.h, _b(a_lbl), B.h, _b(b_lbl), D.h, _b(d_lbl),
                              ws, n, ctypes.byref(info)))
     return info.as_dict()
+
+
+def triples_energy(ctx: Context, T1: Tensor, T2: Tensor, Vooov: Tensor, Vvovv: Tensor, Voovv: Tensor,
+                   eps_o=None, eps_v=None, workspace=None, ws_elems: Optional[int] = None):
+    """(T) energy, PAPER Eq. cc14 (tt_triples_energy).  ``eps_o``/``eps_v`` device arrays (torch); with
+    ``workspace=None`` only plans and returns (None, info)."""
+    info = TriplesInfo()
+    e = _dbl(0.0)
+    ws = _vp(_devptr(workspace)) if workspace is not None else None
+    n = int(ws_elems if ws_elems is not None else (workspace.numel() if workspace is not None else 0))
+    _check(_lib.tt_triples_energy(ctx.h, T1.h, T2.h, Vooov.h, Vvovv.h, Voovv.h,
+                                  _vp(_devptr(eps_o)) if eps_o is not None else None,
+                                  _vp(_devptr(eps_v)) if eps_v is not None else None, ws, n, ctypes.byref(e),
+                                  ctypes.byref(info)))
+    return (e.value if workspace is not None else None), info.as_dict()
 
 
 def contract_scalar(ctx: Context, alpha: float, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str) -> float:

@@ -154,4 +154,43 @@ int64_t scalar_num_partials(int mode, int64_t nseg);
 cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out,
                                 cudaStream_t s);
 
+// ---- perturbative triples (NEXT-4, tt_triples.cu)
+// re-tiling copy: dst block (origin, extents) elements <- the same global elements of src (another tiling)
+struct RetileBlk {
+  int64_t dst_off;
+  int32_t org[TT_MAX_ORDER];
+  int32_t ext[TT_MAX_ORDER];
+};
+struct RetileParams {
+  int32_t order;
+  const double* src;
+  double* dst;
+  const RetileBlk* blks;
+  const Segment* segs;                 // desc = RetileBlk index, [e0, e1) inside the dst block
+  const int32_t* g2t[TT_MAX_ORDER];     // src tile of each global index, per dim
+  const int64_t* toff[TT_MAX_ORDER];    // src tile offsets, per dim
+  int32_t sgrid[TT_MAX_ORDER];
+  const int64_t* sblk_off;             // src storage offsets (-1 = zero block)
+};
+cudaError_t launch_retile(const RetileParams& p, int64_t nseg, cudaStream_t s);
+
+// one W block (a_t,b_t,c_t,i_t,j_t,k_t) of Eq. tensort, row-major (a,b,c,i,j,k)
+struct TriplesBlk {
+  int64_t w_off;
+  int32_t org[6], ext[6];
+  int64_t v_off[9];   // Voovv blocks (x_t,y_t,p_t,q_t), index pair*3 + pq (-1: zero block)
+  int64_t t_off[9];   // T1 blocks (r_t, z_t)
+};
+struct TriplesParams {
+  const double* W;
+  const double* Voovv;
+  const double* T1;
+  const double* eps_o;
+  const double* eps_v;
+  const TriplesBlk* blks;
+  const Segment* segs;
+  double* partials;   // one per segment
+};
+cudaError_t launch_triples_energy(const TriplesParams& p, int64_t nseg, cudaStream_t s);
+
 }  // namespace tt

@@ -141,3 +141,119 @@ def test_energy_laws():
     Ea, _ = TR.energy(T1, T2, Vooov, Vvovv, Voovv, eo, ev)
     Eb, _ = TR.energy(2 * T1, T2, Vooov, Vvovv, Voovv, eo, ev)
     assert abs((Eb - E1) - 2 * (Ea - E1)) <= 1e-12 * abs(Eb)
+
+
+# ------------------------------------------------------------------------------------------ product side
+
+def _spaces(tt, nO, nV, tO, tV, spin):
+    if spin:
+        O = tt.IndexSpace(nO, [(0, nO // 2), (nO // 2, nO)], [1, -1])
+        V = tt.IndexSpace(nV, [(0, nV // 2), (nV // 2, nV)], [1, -1])
+    else:
+        O, V = tt.IndexSpace(nO), tt.IndexSpace(nV)
+    return O, V, tt.TiledIndexSpace(O, tO), tt.TiledIndexSpace(V, tV)
+
+
+def _oracle_dims(nO, nV, tO, tV, spin):
+    from oracle import layout as L
+    if spin:
+        O = L.IndexSpace(nO, [(0, nO // 2, 1), (nO // 2, nO, -1)])
+        V = L.IndexSpace(nV, [(0, nV // 2, 1), (nV // 2, nV, -1)])
+    else:
+        O, V = L.IndexSpace(nO), L.IndexSpace(nV)
+    return L.tile_fixed(O, tO), L.tile_fixed(V, tV)
+
+
+# (name, dims as 'o'/'v', spin (upper dims, lower dims), generator tag)
+TRIPLES_INPUTS = [("T1", "vo", ([0], [1]), 11), ("T2", "vvoo", ([0, 1], [2, 3]), 12),
+                  ("Vooov", "ooov", ([0, 1], [2, 3]), 13), ("Vvovv", "vovv", ([0, 1], [2, 3]), 14),
+                  ("Voovv", "oovv", ([0, 1], [2, 3]), 15)]
+
+
+def _restricted_tile_triples(tO, tV, spin):
+    from math import comb
+    def cnt(t, x, y, z):
+        n = [t.size(q) for q in (x, y, z)]
+        if x == y == z:
+            return comb(n[0], 3)
+        if x == y:
+            return comb(n[0], 2) * n[2]
+        if y == z:
+            return n[0] * comb(n[1], 2)
+        return n[0] * n[1] * n[2]
+    out = 0
+    for a, b, c in itertools.combinations_with_replacement(range(tV.ntiles), 3):
+        for i, j, k in itertools.combinations_with_replacement(range(tO.ntiles), 3):
+            if cnt(tV, a, b, c) and cnt(tO, i, j, k):
+                if not spin or sum(tV.tile_spin[x] for x in (a, b, c)) == sum(tO.tile_spin[x] for x in (i, j, k)):
+                    out += 1
+    return out
+
+
+@pytest.mark.parametrize("nO,nV,tO,tV,spin", [(7, 10, 3, 4, False), (8, 12, 2, 3, True), (6, 9, 1, 2, False)])
+def test_triples_plan_host(nO, nV, tO, tV, spin):
+    import paper_2201_01257_b200 as tt
+    ctx = tt.Context(device=-1)
+    O, V, to, tv = _spaces(tt, nO, nV, tO, tV, spin)
+    dims = {"o": to, "v": tv}
+    T = {n: tt.Tensor(ctx, [dims[c] for c in d], spin=sp if spin else None) for n, d, sp, _ in TRIPLES_INPUTS}
+    _, info = tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
+    oO, oV = _oracle_dims(nO, nV, tO, tV, spin)
+    assert info["w_blocks_total"] == info["w_blocks"] == _restricted_tile_triples(oO, oV, spin)
+    # a dimension on another tiling object is refused
+    other = tt.TiledIndexSpace(V, tV)
+    bad = tt.Tensor(ctx, [to, to, tv, other])
+    with pytest.raises(tt.TTError) as e:
+        tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], bad)
+    assert e.value.name == "TT_E_TILING"
+
+
+def _gpu_case(nO, nV, tO, tV, spin, seed, ws_factor):
+    import torch
+    import paper_2201_01257_b200 as tt
+    import synthetic as S
+    from oracle import layout as L
+    from oracle import ops as O_
+    ctx = tt.Context(device=0, stream=torch.cuda.current_stream().cuda_stream)
+    _, _, to, tv = _spaces(tt, nO, nV, tO, tV, spin)
+    oO, oV = _oracle_dims(nO, nV, tO, tV, spin)
+    dims, odims = {"o": to, "v": tv}, {"o": oO, "v": oV}
+    T, dense, keep = {}, {}, []
+    for n, d, sp, tag in TRIPLES_INPUTS:
+        T[n] = tt.Tensor(ctx, [dims[c] for c in d], spin=sp if spin else None)
+        ot = L.tensor_spin([odims[c] for c in d], *sp) if spin else L.tensor_dense_map([odims[c] for c in d])
+        dense[n] = O_.dense_masked(ot, S.dense(ot.shape, seed, tag))
+        buf = torch.from_numpy(O_.pack(ot, dense[n])).cuda()
+        T[n].bind(buf)
+        keep.append(buf)
+    rng = np.random.default_rng(seed)
+    eo, ev = rng.uniform(-2, -1, nO), rng.uniform(1, 2, nV)
+    deo, dev = torch.from_numpy(eo).cuda(), torch.from_numpy(ev).cuda()
+    args = (T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
+    _, info = tt.triples_energy(ctx, *args)
+    ws = torch.empty(int(info["ws_elems"] * ws_factor), dtype=torch.float64, device="cuda")
+    E, info = tt.triples_energy(ctx, *args, deo, dev, ws)
+    orc = (dense["T1"], dense["T2"], dense["Vooov"], dense["Vvovv"], dense["Voovv"], eo, ev)
+    return E, info, orc, ctx
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nO,nV,tO,tV,spin", [(7, 10, 3, 4, False), (8, 12, 2, 3, True), (6, 11, 4, 5, False)])
+def test_triples_energy_gpu_parity(nO, nV, tO, tV, spin):
+    E, info, orc, _ = _gpu_case(nO, nV, tO, tV, spin, 3, 50.0)
+    Eo, n = TR.energy(*orc)
+    scale = sum(abs(c[0]) for c in TR.energy_elements(*orc, [(i, j, k, a, b, c)
+                for i, j, k in itertools.combinations(range(nO), 3) for a, b, c in itertools.combinations(range(nV), 3)]))
+    assert abs(E - Eo) <= 1e-11 * scale, (E, Eo, scale)
+    assert info["flops_alg"] <= info["flops_exec"]
+    if not spin:
+        assert info["flops_alg"] == pytest.approx(18.0 * (nO + nV) * n, rel=1e-12)
+
+
+@pytest.mark.gpu
+def test_triples_batching_is_bitwise_invariant():
+    """One W block per batch vs everything in one batch: same partial order, same bits (R12)."""
+    E1, i1, _, _ = _gpu_case(7, 10, 2, 3, False, 4, 1.0)
+    E2, i2, _, _ = _gpu_case(7, 10, 2, 3, False, 4, 1000.0)
+    assert i1["batches"] > 1 and i2["batches"] == 1
+    assert E1 == E2
