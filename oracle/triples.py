@@ -102,10 +102,10 @@ def energy_by_triple(T1, T2, Vooov, Vvovv, Voovv, eps_o, eps_v):
     T2o = np.ascontiguousarray(np.transpose(T2, (2, 0, 1, 3)))     # [m][b][c][k]
 
     def A_term(x, y, z):   # X[a,b,c] = sum_m v^{xy}_{m a} t^{m z}_{b c}
-        return np.einsum("ma,mbc->abc", Vooov[x, y], T2o[:, :, :, z], optimize=False)
+        return np.tensordot(Vooov[x, y], T2o[:, :, :, z], axes=([0], [0]))
 
     def B_term(x, y, z):   # Y[a,b,c] = sum_e v^{e x}_{a b} t^{y z}_{e c}
-        return np.einsum("eab,ec->abc", Vvovv[:, x], T2[:, :, y, z], optimize=False)
+        return np.tensordot(Vvovv[:, x], T2[:, :, y, z], axes=([0], [0]))
 
     E, n = 0.0, 0
     for i, j, k in itertools.combinations(range(nO), 3):

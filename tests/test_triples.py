@@ -257,3 +257,14 @@ def test_triples_batching_is_bitwise_invariant():
     E2, i2, _, _ = _gpu_case(7, 10, 2, 3, False, 4, 1000.0)
     assert i1["batches"] > 1 and i2["batches"] == 1
     assert E1 == E2
+
+
+@pytest.mark.gpu
+def test_triples_energy_gpu_parity_midsize():
+    """Several tiles per space with ragged tails (O=16 tiles 5,5,5,1; V=48 tiles 10 x4 + 8), several batches;
+    oracle = the by-triple form (pinned to the element loops above)."""
+    E, info, orc, _ = _gpu_case(16, 48, 5, 10, False, 7, 8.0)
+    Eo, n = TR.energy_by_triple(*orc)
+    assert info["batches"] > 1
+    assert abs(E - Eo) <= 1e-11 * abs(Eo), (E, Eo)
+    assert info["flops_alg"] == pytest.approx(18.0 * (16 + 48) * n, rel=1e-12)
