@@ -280,24 +280,28 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, 
  *        v^{ex}_{pq} t^{yz}_{er} summed over virtual e (B); the sixth term with "-" (reading R27),
  *   V1 = Eq. tensort2: the nine v^{xy}_{pq} t^z_r products.
  * Inputs (real amplitudes and integrals; storage conventions of oracle/triples.py):
- *   T1     t^i_a    as T1(a,i)          dims (V, O)      -- V = T1's dim 0 tiling, O = its dim 1 tiling
- *   T2     t^{ij}_{ab} as T2(a,b,i,j)   dims (V, V, O, O)
- *   Vooov  v^{ij}_{ma} as Vooov(i,j,m,a)  dims (O, O, O, V)
- *   Vvovv  v^{ei}_{ab} as Vvovv(e,i,a,b)  dims (V, O, V, V)
- *   Voovv  v^{ij}_{ab} as Voovv(i,j,a,b)  dims (O, O, V, V)
- *   every dim must be T1's tiled-space object itself (TT_E_TILING); block maps are free (zero blocks read as
- *   0); eps_o[n_o], eps_v[n_v]: DEVICE arrays of orbital energies (global index order).
- * Execution: the summed labels m and e are first re-tiled into the workspace (one tile per spin range of
- * O and V), then for batches of restricted tile triples (a_t<=b_t<=c_t, i_t<=j_t<=k_t, spin sums equal)
- * the 18 terms run as DMMA contractions into a W batch in the workspace, and the energy kernel sums the
- * elements with a<b<c, i<j<k (deterministic partials, fixed-order final sum).  With nranks > 1 the W
- * blocks are partitioned by LPT on their volume, every input block must be TT_REPLICATED, and the energy
- * is all-reduced (NCCL).  energy: HOST pointer; the call synchronises the stream.
- *   workspace  device memory of ws_elems doubles >= info->ws_elems (coarse inputs + one W block; more
- *              gives larger batches), or NULL to return only info.
- *   info       (may be NULL) w_blocks_total / w_blocks (this rank) / batches; flops_alg = FLOPs of the
- *              defined sums over the restricted elements (2 per multiply-add of the 18 terms); flops_exec
- *              = FLOPs the contractions execute (whole tile triples); ws_elems = minimum workspace. */
+ *   T1     t^i_a       as T1(a,i)        dims (V, O)      -- V = T1's dim 0 tiling, O = its dim 1 tiling
+ *   T2     t^{ij}_{ab} as T2(a,b,i,j)    dims (V, V, O, O)
+ *   Vooov  v^{ij}_{ma} as Vooov(i,j,m,a) dims (O, O, O, V)
+ *   Vvovv  v^{ei}_{ab} as Vvovv(e,i,a,b) dims (V, O, V, V)
+ *   Voovv  v^{ij}_{ab} as Voovv(i,j,a,b) dims (O, O, V, V)
+ *   every dim must be T1's tiled-space object itself (TT_E_TILING); block maps are free (zero blocks read
+ *   as 0); virtual ranges must have even sizes (TT_E_UNSUPPORTED); eps_o[n_o], eps_v[n_v]: DEVICE arrays
+ *   of orbital energies (global index order).
+ * Execution: the inputs are copied into dense permuted layouts in the workspace; then one fused kernel
+ * CTA per unit = (occupied triple i<j<k, triple of 16-wide virtual boxes b_a <= b_b <= b_c) forms the
+ * unit's W in shared memory as W(a,b,c) = G(a;b,c) - G(b;a,c) + G(c;a,b) -- the 18 terms regrouped into
+ * three DMMA GEMMs with K = 3 n_o + 3 n_v -- and reduces (W + V1) W / D over a<b<c into one partial per
+ * unit; a fixed-order sum gives E (deterministic).  Units whose box spins and occupied spins differ in
+ * sum are skipped (W = 0 under the spin maps of R7).  With nranks > 1 every input block must be
+ * TT_REPLICATED, the units are split into contiguous equal ranges and E is all-reduced (NCCL).
+ * energy: HOST pointer; the call synchronises the stream.
+ *   workspace  device memory of ws_elems doubles >= info->ws_elems (dense copies + one partial per
+ *              unit), or NULL to return only info.
+ *   info       (may be NULL) w_blocks_total / w_blocks = units in total / on this rank; batches = 1;
+ *              flops_alg = 18 (n_o + n_v) FLOPs per restricted element (a<b<c, i<j<k, spin-allowed) of
+ *              this rank; flops_exec = FLOPs the GEMMs execute (16-wide boxes, K padded to 8);
+ *              ws_elems = workspace needed. */
 typedef struct {
   int64_t w_blocks_total, w_blocks, batches;
   double flops_alg, flops_exec;

@@ -2849,82 +2849,61 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* cl, double beta, dou
 
 // ---------------------------------------------------------------------------------------------
 // perturbative triples correction (T), PAPER Eqs. cc14, tensort, abt, tensort2
-// (P343-413).  W (Eq. tensort, 18 terms, reading R27 for the sign of the sixth) is formed block by
-// block for the restricted tile triples a_t <= b_t <= c_t, i_t <= j_t <= k_t by 18 local DMMA
-// contractions into a workspace batch; the fused energy kernel then sums (W + V1) W / D over the
-// elements with a<b<c, i<j<k (reading R28).  Multi-GPU: the W blocks are partitioned (LPT on their
-// volume); every rank holds all inputs; the partial energies are all-reduced.
+// (P343-413).  The inputs are copied into dense, permuted layouts in the workspace (re-tiling kernel),
+// then one fused kernel launch per batch of units (occupied triple i<j<k x virtual box triple) forms W in
+// shared memory through three GEMMs (tt_triples.cu) and reduces (W + V1) W / D (reading R28) into one
+// partial per unit; a fixed-order final sum (R12) and, with nranks > 1, an NCCL all-reduce give E(T).
+// Units are enumerated box-major (consecutive CTAs share the virtual slices in L2) and split into
+// contiguous equal ranges over the ranks; spin-forbidden units (sum of box spins != sum of occupied spins)
+// are skipped -- W vanishes there for the spin maps of reading R7.
 
 namespace {
 
-// the 18 terms of Eq. tensort: sign, A labels, B labels; C = W "abcijk"
-struct TripTerm {
-  double sign;
-  const char* al;
-  const char* bl;
-  bool occ;   // true: A = Vooov (sum over m), B = T2 "..m."; false: A = Vvovv (sum over e), B = T2 "e..."
-};
-const TripTerm kTripTerms[18] = {
-    {+1, "ijma", "bcmk", true}, {-1, "ijmb", "acmk", true}, {+1, "ijmc", "abmk", true},
-    {-1, "ikma", "bcmj", true}, {+1, "ikmb", "acmj", true}, {-1, "ikmc", "abmj", true},   // R27: 6th "-"
-    {+1, "jkma", "bcmi", true}, {-1, "jkmb", "acmi", true}, {+1, "jkmc", "abmi", true},
-    {-1, "eiab", "ecjk", false}, {+1, "eiac", "ebjk", false}, {-1, "eibc", "eajk", false},
-    {+1, "ejab", "ecik", false}, {-1, "ejac", "ebik", false}, {+1, "ejbc", "eaik", false},
-    {-1, "ekab", "ecij", false}, {+1, "ekac", "ebij", false}, {-1, "ekbc", "eaij", false}};
-
 struct RetileOp {
-  tt_tensor dst = nullptr;   // meta tensor on the coarse tiling, storage in the workspace
+  tt_tensor dst = nullptr;   // meta tensor on the dense tiling, storage in the workspace
   tt_tensor src = nullptr;
+  std::vector<int32_t> sdim;
   RetileBlk* d_blks = nullptr;
   Segment* d_segs = nullptr;
   int64_t nseg = 0, ws_pos = 0;
   int32_t* d_g2t[TT_MAX_ORDER] = {};
 };
 
-struct TripBatch {
-  tt_tensor W = nullptr;
-  std::vector<std::shared_ptr<ContractPlan>> plans;   // 18
-  TriplesBlk* d_blks = nullptr;
-  Segment* d_segs = nullptr;
-  int64_t nseg = 0, part0 = 0;   // partial slots [part0, part0 + nseg)
-};
-
 struct TripPlan {
-  tt_tis Om = nullptr, Ve = nullptr;       // one tile per range of the occupied / virtual space
-  RetileOp rt[4];                           // T2m (V,V,Om,O), T2e (Ve,V,O,O), Vooov_m (O,O,Om,V), Vvovv_e (Ve,O,V,V)
-  std::vector<TripBatch> batches;
+  tt_tis fullO = nullptr, fullV = nullptr;   // one tile over the whole space (dense copies)
+  RetileOp rt[5];                             // VO (O,O,O,V), VV (V,O,V,V), T2 (O,O,V,V), VD (O,O,V,V), T1 (V,O)
+  int2* d_units = nullptr;
+  int4* d_box3 = nullptr;
+  int4* d_trip = nullptr;
+  int32_t* d_box_lo = nullptr;
+  int32_t* d_box_ext = nullptr;
   double* d_partials = nullptr;
-  int64_t npart = 0;
-  int64_t ws_fixed = 0, ws_need = 0;
+  int64_t unit0 = 0, nunits = 0, nunits_total = 0;
+  int64_t ws_need = 0;
   tt_triples_info info{};
   ~TripPlan() {
     for (auto& r : rt) delete r.dst;
-    for (auto& b : batches) delete b.W;
-    delete Om;
-    delete Ve;
+    delete fullO;
+    delete fullV;
   }
 };
 
-// tiled space with one tile per range of the index space of `t` (never straddles spin, S39)
-tt_tis range_tiling(tt_tis t) {
+tt_tis full_tiling(tt_tis t) {
   tt_tis r = new tt_tis_s();
   r->is = t->is;
   r->uid = g_uid++;
-  r->offsets.push_back(0);
-  for (size_t q = 0; q < t->is->rb.size(); ++q) {
-    r->offsets.push_back(t->is->re[q]);
-    r->spin.push_back(t->is->rspin[q]);
-  }
+  r->offsets = {0, t->offsets.back()};
+  r->spin = {0};
   return r;
 }
 
-// number of index triples x<y<z with x in tile tx, y in ty, z in tz (tiles tx <= ty <= tz, contiguous)
-int64_t ordered_count(tt_tis t, int tx, int ty, int tz) {
-  const int64_t nx = t->size(tx), ny = t->size(ty), nz = t->size(tz);
-  if (tx == ty && ty == tz) return nx * (nx - 1) * (nx - 2) / 6;
-  if (tx == ty) return nx * (nx - 1) / 2 * nz;
-  if (ty == tz) return nx * ny * (ny - 1) / 2;
-  return nx * ny * nz;
+int64_t ordered_count3(int64_t lo0, int64_t n0, int64_t lo1, int64_t n1, int64_t lo2, int64_t n2) {
+  // x<y<z with x in [lo0, lo0+n0), y in [lo1, ...), z in [lo2, ...), ranges ordered and equal or disjoint
+  const bool e01 = lo0 == lo1, e12 = lo1 == lo2;
+  if (e01 && e12) return n0 * (n0 - 1) * (n0 - 2) / 6;
+  if (e01) return n0 * (n0 - 1) / 2 * n2;
+  if (e12) return n0 * n1 * (n1 - 1) / 2;
+  return n0 * n1 * n2;
 }
 
 tt_status build_retile(tt_ctx ctx, RetileOp& op) {
@@ -2974,6 +2953,7 @@ tt_status run_retile(tt_ctx ctx, const RetileOp& op) {
     p.g2t[q] = op.d_g2t[q];
     p.toff[q] = op.src->d_toff[q];
     p.sgrid[q] = op.src->grid[q];
+    p.sdim[q] = op.sdim[q];
   }
   p.sblk_off = op.src->d_blk_off;
   Launch L(ctx, "tt_retile");
@@ -2995,10 +2975,10 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   const tt_tis want[5][4] = {{tV, tO, nullptr, nullptr}, {tV, tV, tO, tO}, {tO, tO, tO, tV}, {tV, tO, tV, tV}, {tO, tO, tV, tV}};
   const tt_tensor ins[5] = {T1, T2, Vooov, Vvovv, Voovv};
   const char* names[5] = {"T1", "T2", "Vooov", "Vvovv", "Voovv"};
-  for (int x = 0; x < 5; ++x)
-    for (int d = 0; d < ins[x]->order; ++d)
-      if (ins[x]->dims[d] != want[x][d] && !same_tiling(ins[x]->dims[d], want[x][d]))
-        return fail(TT_E_TILING, "%s dim %d is not on T1's %s tiling (S413)", names[x], d,
+  for (int x = 1; x < 5; ++x)
+    for (int d = 0; d < 4; ++d)
+      if (ins[x]->dims[d] != want[x][d])
+        return fail(TT_E_TILING, "%s dim %d: must be T1's %s tiled index space object (S413)", names[x], d,
                     want[x][d] == tO ? "occupied" : "virtual");
   for (int x = 0; x < 5; ++x) {
     if (ins[x]->compact || ins[x]->any_split || ins[x]->view_of)
@@ -3008,218 +2988,143 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
         if (ins[x]->nz[b] && ins[x]->owner[b] != TT_REPLICATED)
           return fail(TT_E_UNSUPPORTED, "%s: with nranks > 1 every input block must be TT_REPLICATED", names[x]);
   }
-  // the dims of every input must be the very tiled spaces of T1 (the kernels share tile tables)
-  for (int x = 1; x < 5; ++x)
-    for (int d = 0; d < 4; ++d)
-      if (ins[x]->dims[d] != want[x][d])
-        return fail(TT_E_TILING, "%s dim %d: pass T1's tiled index space object itself", names[x], d);
+  const int64_t nO = tO->offsets.back(), nV = tV->offsets.back();
+  if (nO < 3 || nV < 3) return fail(TT_E_ARG, "need at least 3 occupied and 3 virtual indices");
+  for (size_t q = 0; q < tV->is->rb.size(); ++q)
+    if ((tV->is->re[q] - tV->is->rb[q]) % 2)
+      return fail(TT_E_UNSUPPORTED, "virtual ranges must have even sizes (16-byte staging of the fused kernel)");
   char keybuf[400];
-  snprintf(keybuf, sizeof(keybuf), "trip|%llu.%llu|%llu.%llu|%llu.%llu|%llu.%llu|%llu.%llu|%lld",
+  snprintf(keybuf, sizeof(keybuf), "trip|%llu.%llu|%llu.%llu|%llu.%llu|%llu.%llu|%llu.%llu",
            (unsigned long long)T1->uid, (unsigned long long)T1->version, (unsigned long long)T2->uid,
            (unsigned long long)T2->version, (unsigned long long)Vooov->uid, (unsigned long long)Vooov->version,
            (unsigned long long)Vvovv->uid, (unsigned long long)Vvovv->version, (unsigned long long)Voovv->uid,
-           (unsigned long long)Voovv->version, (long long)(workspace ? ws_elems : -1));
+           (unsigned long long)Voovv->version);
   auto tp = cached<TripPlan>(ctx, keybuf);
   if (!tp) {
     tp = std::make_shared<TripPlan>();
-    tp->Om = range_tiling(tO);
-    tp->Ve = range_tiling(tV);
-    // coarse copies: a block of the coarse tiling is non-zero iff it covers a non-zero source block
-    auto coarse = [&](RetileOp& op, tt_tensor src, int dim, tt_tis ct) -> tt_status {
-      std::vector<tt_tis> dims(src->dims.begin(), src->dims.end());
-      dims[dim] = ct;
-      int64_t nb = 1;
-      for (auto d : dims) nb *= d->ntiles();
-      std::vector<uint8_t> nz(nb, 0);
-      int32_t c[TT_MAX_ORDER];
-      for (int64_t b = 0; b < src->nblocks; ++b) {
-        if (!src->nz[b]) continue;
-        src->block_coords(b, c);
-        const int64_t g = src->dims[dim]->offsets[c[dim]];
-        int t = 0;
-        while (ct->offsets[t + 1] <= g) ++t;
-        c[dim] = t;
-        int64_t id = 0;
-        for (size_t q = 0; q < dims.size(); ++q) id = id * dims[q]->ntiles() + c[q];
-        nz[id] = 1;
-      }
-      TT_TRY(new_meta_tensor(ctx, dims, nz, &op.dst));
-      op.src = src;
-      return TT_OK;
-    };
-    TT_TRY(coarse(tp->rt[0], T2, 2, tp->Om));
-    TT_TRY(coarse(tp->rt[1], T2, 0, tp->Ve));
-    TT_TRY(coarse(tp->rt[2], Vooov, 2, tp->Om));
-    TT_TRY(coarse(tp->rt[3], Vvovv, 0, tp->Ve));
+    tp->fullO = full_tiling(tO);
+    tp->fullV = full_tiling(tV);
+    tt_tis fO = tp->fullO, fV = tp->fullV;
+    // dense copies: dims (dst order) and, per source dim, the dst dim holding it
+    struct Spec { tt_tensor src; std::vector<tt_tis> dims; std::vector<int32_t> sdim; };
+    const Spec specs[5] = {{Vooov, {fO, fO, fO, fV}, {0, 1, 2, 3}},
+                           {Vvovv, {fV, fO, fV, fV}, {0, 1, 2, 3}},
+                           {T2, {fO, fO, fV, fV}, {2, 3, 0, 1}},       // t^{ij}_{ab}: (a,b,i,j) -> (i,j,a,b)
+                           {Voovv, {fO, fO, fV, fV}, {0, 1, 2, 3}},
+                           {T1, {fV, fO}, {0, 1}}};
     int64_t base = 0;
-    for (int x = 0; x < 4; ++x) {
+    for (int x = 0; x < 5; ++x) {
+      TT_TRY(new_meta_tensor(ctx, specs[x].dims, std::vector<uint8_t>(1, 1), &tp->rt[x].dst));
+      tp->rt[x].src = specs[x].src;
+      tp->rt[x].sdim = specs[x].sdim;
       tp->rt[x].ws_pos = base;
       base += (tp->rt[x].dst->packed_elems + 31) / 32 * 32;
     }
-    tp->ws_fixed = base;
-    // restricted W tile triples, spin-conserving (reading R28)
-    const int nv = tV->ntiles(), no = tO->ntiles();
-    struct WB {
-      int32_t t[6];
-      int64_t vol, nres;
-    };
-    std::vector<WB> wbs;
-    for (int a = 0; a < nv; ++a) for (int b = a; b < nv; ++b) for (int c = b; c < nv; ++c) {
-      const int64_t nabc = ordered_count(tV, a, b, c);
-      if (!nabc) continue;
-      for (int i = 0; i < no; ++i) for (int j = i; j < no; ++j) for (int k = j; k < no; ++k) {
-        const int64_t nijk = ordered_count(tO, i, j, k);
-        if (!nijk) continue;
-        if (tV->spin[a] + tV->spin[b] + tV->spin[c] != tO->spin[i] + tO->spin[j] + tO->spin[k]) continue;
-        wbs.push_back({{a, b, c, i, j, k},
-                       tV->size(a) * tV->size(b) * tV->size(c) * tO->size(i) * tO->size(j) * tO->size(k), nabc * nijk});
+    // virtual boxes: each range of V cut into boxes of kTripBox (never straddle spin, S39)
+    std::vector<int32_t> box_lo, box_ext;
+    std::vector<int8_t> box_spin;
+    for (size_t q = 0; q < tV->is->rb.size(); ++q)
+      for (int64_t x = tV->is->rb[q]; x < tV->is->re[q]; x += kTripBox) {
+        box_lo.push_back((int32_t)x);
+        box_ext.push_back((int32_t)std::min<int64_t>(kTripBox, tV->is->re[q] - x));
+        box_spin.push_back(tV->is->rspin[q]);
       }
+    const int nb = (int)box_lo.size();
+    std::vector<int4> box3;
+    std::vector<int64_t> box3_n;
+    for (int a = 0; a < nb; ++a) for (int b = a; b < nb; ++b) for (int c = b; c < nb; ++c) {
+      const int64_t n = ordered_count3(box_lo[a], box_ext[a], box_lo[b], box_ext[b], box_lo[c], box_ext[c]);
+      if (n > 0) { box3.push_back({a, b, c, box_spin[a] + box_spin[b] + box_spin[c]}); box3_n.push_back(n); }
     }
-    // partition: LPT over the W blocks by volume (reading R24); this rank's blocks in block order
-    std::vector<int64_t> cost, ids;
-    for (size_t q = 0; q < wbs.size(); ++q) { cost.push_back(wbs[q].vol); ids.push_back((int64_t)q); }
-    std::vector<int32_t> own = lpt(cost, ids, ctx->nranks);
-    std::vector<const WB*> mine;
-    int64_t maxblk = 0;
-    for (size_t q = 0; q < wbs.size(); ++q)
-      if (own[q] == ctx->rank) { mine.push_back(&wbs[q]); maxblk = std::max(maxblk, wbs[q].vol); }
-    tp->ws_need = tp->ws_fixed + (maxblk + 1) / 2 * 2;
-    tp->info.w_blocks_total = (int64_t)wbs.size();
-    tp->info.w_blocks = (int64_t)mine.size();
-    tp->info.ws_elems = tp->ws_need;
-    if (!workspace) {
-      if (info) *info = tp->info;
-      return TT_OK;   // query only (not cached: the batches depend on the workspace size)
-    }
-    if (ws_elems < tp->ws_need)
-      return fail(TT_E_OOM, "workspace holds %lld doubles, (T) needs at least %lld (coarse inputs + one W block)",
-                  (long long)ws_elems, (long long)tp->ws_need);
-    for (int x = 0; x < 4; ++x) TT_TRY(build_retile(ctx, tp->rt[x]));
-    // batches of W blocks that fit the rest of the workspace
-    const int64_t wcap = ws_elems - tp->ws_fixed;
-    const std::vector<tt_tis> wdims = {tV, tV, tV, tO, tO, tO};
-    int64_t nbw = 1;
-    for (auto d : wdims) nbw *= d->ntiles();
-    auto wid = [&](const WB* w) {
-      int64_t id = 0;
-      for (int d = 0; d < 6; ++d) id = id * wdims[d]->ntiles() + w->t[d];
-      return id;
-    };
-    size_t q0 = 0;
-    double exec = 0, alg = 0;
-    while (q0 < mine.size()) {
-      size_t q1 = q0;
-      int64_t used = 0;
-      while (q1 < mine.size() && used + (mine[q1]->vol + 1) / 2 * 2 <= wcap) used += (mine[q1++]->vol + 1) / 2 * 2;
-      TripBatch bt;
-      std::vector<uint8_t> nz(nbw, 0);
-      std::map<int64_t, const WB*> by_id;
-      for (size_t q = q0; q < q1; ++q) { nz[wid(mine[q])] = 1; by_id[wid(mine[q])] = mine[q]; }
-      TT_TRY(new_meta_tensor(ctx, wdims, nz, &bt.W));
-      ContractOpts o;
-      o.local = true;
-      o.tag = "|trip";
-      for (size_t q = q0; q < q1; ++q) {
-        const int64_t id = wid(mine[q]);
-        o.sel.push_back({id, 0, bt.W->ext0(id)});
-      }
-      for (int x = 0; x < 18; ++x) {
-        const TripTerm& tm = kTripTerms[x];
-        tt_tensor A = tm.occ ? tp->rt[2].dst : tp->rt[3].dst;
-        tt_tensor Bt = tm.occ ? tp->rt[0].dst : tp->rt[1].dst;
-        std::shared_ptr<ContractPlan> pl;
-        TT_TRY(get_contract_plan(ctx, bt.W, "abcijk", A, tm.al, Bt, tm.bl, x == 0 ? 0.0 : 1.0, pl, nullptr, o));
-        exec += pl->flops;
-        // algorithmic share: every element of a W block has the same task list, so the defined sum over
-        // a<b<c, i<j<k costs the block's FLOPs times (restricted elements / block volume)
-        for (size_t g = 0; g < pl->ht.cblk.size(); ++g) {
-          const WB* w = by_id.at(pl->ht.cblk[g]);
-          alg += (double)pl->ht.cost[g] * (double)w->nres / (double)w->vol;
-        }
-        bt.plans.push_back(pl);
-      }
-      // energy descriptors
-      std::vector<TriplesBlk> tb;
-      std::vector<Segment> sg;
-      for (size_t q = q0; q < q1; ++q) {
-        const WB* w = mine[q];
-        TriplesBlk B{};
-        B.w_off = bt.W->blk_off[wid(w)];
-        for (int d = 0; d < 6; ++d) {
-          B.org[d] = (int32_t)wdims[d]->offsets[w->t[d]];
-          B.ext[d] = (int32_t)wdims[d]->size(w->t[d]);
-        }
-        const int o3[3][3] = {{3, 4, 5}, {3, 5, 4}, {4, 5, 3}};   // (x, y, z) positions among a,b,c,i,j,k
-        const int v3[3][3] = {{0, 1, 2}, {0, 2, 1}, {1, 2, 0}};   // (p, q, r)
-        for (int pr = 0; pr < 3; ++pr)
-          for (int pq = 0; pq < 3; ++pq) {
-            const int32_t vc[4] = {w->t[o3[pr][0]], w->t[o3[pr][1]], w->t[v3[pq][0]], w->t[v3[pq][1]]};
-            const int32_t tc[2] = {w->t[v3[pq][2]], w->t[o3[pr][2]]};
-            const int64_t vb = Voovv->block_id(vc), tb1 = T1->block_id(tc);
-            B.v_off[pr * 3 + pq] = Voovv->nz[vb] ? Voovv->blk_off[vb] : -1;
-            B.t_off[pr * 3 + pq] = T1->nz[tb1] ? T1->blk_off[tb1] : -1;
-          }
-        for (int64_t e = 0; e < w->vol; e += 16384)
-          sg.push_back({(int32_t)tb.size(), 0, e, std::min(w->vol, e + 16384)});
-        tb.push_back(B);
-      }
-      TT_TRY(dev_alloc(ctx, &bt.d_blks, std::max<size_t>(1, tb.size())));
-      TT_TRY(dev_alloc(ctx, &bt.d_segs, std::max<size_t>(1, sg.size())));
-      TT_CUDA(cudaMemcpy(bt.d_blks, tb.data(), tb.size() * sizeof(TriplesBlk), cudaMemcpyHostToDevice));
-      TT_CUDA(cudaMemcpy(bt.d_segs, sg.data(), sg.size() * sizeof(Segment), cudaMemcpyHostToDevice));
-      bt.nseg = (int64_t)sg.size();
-      bt.part0 = tp->npart;
-      tp->npart += bt.nseg;
-      tp->batches.push_back(bt);
-      q0 = q1;
-    }
-    TT_TRY(dev_alloc(ctx, &tp->d_partials, std::max<int64_t>(1, tp->npart)));
-    tp->info.flops_exec = exec;
+    // occupied triples i<j<k with their spin sums (spin of the range holding the index)
+    std::vector<int8_t> ospin(nO, 0);
+    for (size_t q = 0; q < tO->is->rb.size(); ++q)
+      for (int64_t x = tO->is->rb[q]; x < tO->is->re[q]; ++x) ospin[x] = tO->is->rspin[q];
+    std::vector<int4> trip;
+    for (int i = 0; i < nO; ++i) for (int j = i + 1; j < nO; ++j) for (int k = j + 1; k < nO; ++k)
+      trip.push_back({i, j, k, ospin[i] + ospin[j] + ospin[k]});
+    std::vector<int2> units;
+    double alg = 0;
+    const double per = 18.0 * (double)(nO + nV);
+    for (size_t b3 = 0; b3 < box3.size(); ++b3)
+      for (size_t t = 0; t < trip.size(); ++t)
+        if (box3[b3].w == trip[t].w) { units.push_back({(int)b3, (int)t}); }
+    // contiguous equal ranges over the ranks (every unit costs the same GEMM work)
+    const int64_t U = (int64_t)units.size();
+    if (U >= (1ll << 31)) return fail(TT_E_UNSUPPORTED, "%lld (T) units exceed the int32 unit index", (long long)U);
+    tp->nunits_total = U;
+    tp->unit0 = U * ctx->rank / ctx->nranks;
+    tp->nunits = U * (ctx->rank + 1) / ctx->nranks - tp->unit0;
+    for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits; ++q) alg += per * (double)box3_n[units[q].x];
+    const int64_t kpad = (3 * nO + 3 * nV + 7) / 8 * 8;
+    tp->info.w_blocks_total = U;
+    tp->info.w_blocks = tp->nunits;
+    tp->info.batches = 1;
     tp->info.flops_alg = alg;
-    tp->info.batches = (int64_t)tp->batches.size();
+    tp->info.flops_exec = (double)tp->nunits * 3.0 * 2.0 * kTripBox * kTripBox * kTripBox * (double)kpad;
+    tp->ws_need = base + (U + 1) / 2 * 2;
+    tp->info.ws_elems = tp->ws_need;
+    if (ctx->device >= 0) {
+      TT_TRY(need_device(ctx));
+      DeviceGuard dg(ctx->device);
+      for (int x = 0; x < 5; ++x) TT_TRY(build_retile(ctx, tp->rt[x]));
+      TT_TRY(dev_alloc(ctx, &tp->d_units, std::max<size_t>(1, units.size())));
+      TT_TRY(dev_alloc(ctx, &tp->d_box3, std::max<size_t>(1, box3.size())));
+      TT_TRY(dev_alloc(ctx, &tp->d_trip, std::max<size_t>(1, trip.size())));
+      TT_TRY(dev_alloc(ctx, &tp->d_box_lo, box_lo.size()));
+      TT_TRY(dev_alloc(ctx, &tp->d_box_ext, box_ext.size()));
+      if (!units.empty()) TT_CUDA(cudaMemcpy(tp->d_units, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      if (!box3.empty()) TT_CUDA(cudaMemcpy(tp->d_box3, box3.data(), box3.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      TT_CUDA(cudaMemcpy(tp->d_trip, trip.data(), trip.size() * sizeof(int4), cudaMemcpyHostToDevice));
+      TT_CUDA(cudaMemcpy(tp->d_box_lo, box_lo.data(), box_lo.size() * 4, cudaMemcpyHostToDevice));
+      TT_CUDA(cudaMemcpy(tp->d_box_ext, box_ext.data(), box_ext.size() * 4, cudaMemcpyHostToDevice));
+    }
     ctx->plans[keybuf] = tp;
   }
   if (info) *info = tp->info;
-  if (!workspace) return TT_OK;
+  if (!workspace) return TT_OK;   // query: units, FLOPs, workspace size
   if (!energy) return fail(TT_E_ARG, "NULL energy");
   if (!eps_o || !eps_v) return fail(TT_E_ARG, "NULL orbital energies");
+  if (ws_elems < tp->ws_need)
+    return fail(TT_E_OOM, "workspace holds %lld doubles, (T) needs %lld (dense input copies + one partial per unit)",
+                (long long)ws_elems, (long long)tp->ws_need);
   TT_TRY(need_device(ctx));
   for (int x = 0; x < 5; ++x) TT_TRY(check_bound(ins[x], names[x]));
   if (ctx->prepare_only) return TT_OK;
   DeviceGuard dg(ctx->device);
   reset_stats(ctx);
   double* ws = (double*)workspace;
-  for (int x = 0; x < 4; ++x) {
+  for (int x = 0; x < 5; ++x) {
     tp->rt[x].dst->data = ws + tp->rt[x].ws_pos;
     tp->rt[x].dst->capacity = tp->rt[x].dst->packed_elems;
     TT_TRY(run_retile(ctx, tp->rt[x]));
   }
-  TT_TRY(ensure_dev(Voovv));
-  TT_TRY(ensure_dev(T1));
-  for (auto& bt : tp->batches) {
-    bt.W->data = ws + tp->ws_fixed;
-    bt.W->capacity = ws_elems - tp->ws_fixed;
-    for (int x = 0; x < 18; ++x) {
-      const TripTerm& tm = kTripTerms[x];
-      tt_tensor A = tm.occ ? tp->rt[2].dst : tp->rt[3].dst;
-      tt_tensor Bt = tm.occ ? tp->rt[0].dst : tp->rt[1].dst;
-      TT_TRY(launch_plan(ctx, *bt.plans[x], bt.W, "abcijk", x == 0 ? 0.0 : 1.0, tm.sign, A, tm.al, Bt, tm.bl));
-    }
-    TriplesParams p{};
-    p.W = bt.W->data;
-    p.Voovv = Voovv->data;
-    p.T1 = T1->data;
-    p.eps_o = eps_o;
-    p.eps_v = eps_v;
-    p.blks = bt.d_blks;
-    p.segs = bt.d_segs;
-    p.partials = tp->d_partials + bt.part0;
-    Launch L(ctx, "tt_triples_energy");
-    TT_CUDA(launch_triples_energy(p, bt.nseg, ctx->stream));
+  double* partials = ws + tp->rt[4].ws_pos + (tp->rt[4].dst->packed_elems + 31) / 32 * 32;
+  TriplesParams p{};
+  p.VO = tp->rt[0].dst->data;
+  p.VV = tp->rt[1].dst->data;
+  p.T2 = tp->rt[2].dst->data;
+  p.VD = tp->rt[3].dst->data;
+  p.T1 = tp->rt[4].dst->data;
+  p.eps_o = eps_o;
+  p.eps_v = eps_v;
+  p.units = tp->d_units;
+  p.box3 = tp->d_box3;
+  p.trip = tp->d_trip;
+  p.box_lo = tp->d_box_lo;
+  p.box_ext = tp->d_box_ext;
+  p.nO = (int32_t)nO;
+  p.nV = (int32_t)nV;
+  p.partials = partials;
+  // launches of at most 2^20 units (keeps each launch's grid small; partials are indexed by unit)
+  for (int64_t u0 = tp->unit0; u0 < tp->unit0 + tp->nunits; u0 += (1 << 20)) {
+    p.unit0 = u0;
+    Launch L(ctx, "tt_triples_fused");
+    TT_CUDA(launch_triples_fused(p, std::min<int64_t>(1 << 20, tp->unit0 + tp->nunits - u0), ctx->stream));
   }
   {
     Launch L(ctx, "tt_scalar_final");
-    TT_CUDA(launch_scalar_final(tp->d_partials, tp->npart, 1.0, ctx->d_scalar, ctx->stream));
+    TT_CUDA(launch_scalar_final(partials + tp->unit0, tp->nunits, 1.0, ctx->d_scalar, ctx->stream));
   }
   if (ctx->nranks > 1) {
     const char* err = nullptr;
@@ -3230,7 +3135,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   }
   TT_CUDA(cudaMemcpyAsync(energy, ctx->d_scalar, 8, cudaMemcpyDeviceToHost, ctx->stream));
   TT_CUDA(cudaStreamSynchronize(ctx->stream));
-  ctx->last.c_blocks = tp->info.w_blocks;
+  ctx->last.c_blocks = tp->nunits;
   ctx->last.flops = tp->info.flops_alg;
   ctx->last.aux_flops = tp->info.flops_exec;
   return TT_OK;

@@ -155,7 +155,8 @@ cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha,
                                 cudaStream_t s);
 
 // ---- perturbative triples (NEXT-4, tt_triples.cu)
-// re-tiling copy: dst block (origin, extents) elements <- the same global elements of src (another tiling)
+// re-tiling copy: dst block (origin, extents; dst dim order) elements <- the same global elements of src
+// (another tiling and dim order: src dim q is dst dim sdim[q])
 struct RetileBlk {
   int64_t dst_off;
   int32_t org[TT_MAX_ORDER];
@@ -167,30 +168,33 @@ struct RetileParams {
   double* dst;
   const RetileBlk* blks;
   const Segment* segs;                 // desc = RetileBlk index, [e0, e1) inside the dst block
-  const int32_t* g2t[TT_MAX_ORDER];     // src tile of each global index, per dim
-  const int64_t* toff[TT_MAX_ORDER];    // src tile offsets, per dim
+  const int32_t* g2t[TT_MAX_ORDER];     // src tile of each global index, per src dim
+  const int64_t* toff[TT_MAX_ORDER];    // src tile offsets, per src dim
   int32_t sgrid[TT_MAX_ORDER];
+  int32_t sdim[TT_MAX_ORDER];
   const int64_t* sblk_off;             // src storage offsets (-1 = zero block)
 };
 cudaError_t launch_retile(const RetileParams& p, int64_t nseg, cudaStream_t s);
 
-// one W block (a_t,b_t,c_t,i_t,j_t,k_t) of Eq. tensort, row-major (a,b,c,i,j,k)
-struct TriplesBlk {
-  int64_t w_off;
-  int32_t org[6], ext[6];
-  int64_t v_off[9];   // Voovv blocks (x_t,y_t,p_t,q_t), index pair*3 + pq (-1: zero block)
-  int64_t t_off[9];   // T1 blocks (r_t, z_t)
-};
+constexpr int kTripBox = 16;           // virtual box edge of the fused (T) kernel
 struct TriplesParams {
-  const double* W;
-  const double* Voovv;
-  const double* T1;
+  const double* VO;     // [O][O][O][V]  v^{ij}_{ma}
+  const double* VV;     // [V][O][V][V]  v^{ei}_{ab}
+  const double* T2;     // [O][O][V][V]  t^{ij}_{ab}
+  const double* VD;     // [O][O][V][V]  v^{ij}_{ab}
+  const double* T1;     // [V][O]        t^i_a
   const double* eps_o;
   const double* eps_v;
-  const TriplesBlk* blks;
-  const Segment* segs;
-  double* partials;   // one per segment
+  const int2* units;    // (box triple, occupied triple)
+  const int4* box3;     // box ids (a, b, c)
+  const int4* trip;     // (i, j, k)
+  const int32_t* box_lo;
+  const int32_t* box_ext;
+  int32_t nO, nV;
+  int64_t unit0;        // first unit of this launch
+  double* partials;     // one per unit (indexed by unit)
 };
-cudaError_t launch_triples_energy(const TriplesParams& p, int64_t nseg, cudaStream_t s);
+size_t triples_fused_smem();
+cudaError_t launch_triples_fused(const TriplesParams& p, int64_t nunits, cudaStream_t s);
 
 }  // namespace tt

@@ -1,12 +1,48 @@
 // tt_triples.cu -- sm_100a kernels of the perturbative-triples path (PAPER Eqs. cc14,
-// tensort, tensort2, P343-413) that are not contractions: re-tiling copies of the inputs (the summed
-// labels m, e are staged on one tile per spin range so each of the 18 Eq. tensort terms is a single
-// K = O or K = V pass of the DMMA kernel), and the fused energy assembly of Eq. cc14.
+// tensort, abt, tensort2, P343-413).
+//
+// retile_kernel: copies of the inputs in dense, permuted layouts (global index -> source block).
+//
+// triples_fused_kernel: one CTA per (occupied triple i<j<k, virtual box triple) unit.  The 18 terms of
+// Eq. tensort regroup exactly into three GEMMs over the same box (reading R27 for the sixth sign):
+//     W(a,b,c) = G(a; b,c) - G(b; a,c) + G(c; a,b)
+//     G(r; p,q) = sum_s sigma_s sum_m v^{x_s y_s}_{m r} t^{m z_s}_{p q}      (terms 1,4,7 / 2,5,8 / 3,6,9)
+//               - sum_s sigma_s sum_e t^{y_s z_s}_{e r} v^{e x_s}_{p q}       (terms 12,15,18 / 11,14,17 / 10,13,16)
+// with (x,y,z,sigma) = (i,j,k,+), (i,k,j,-), (j,k,i,+) for the m sums and (x; y,z) = (i; j,k), (j; i,k),
+// (k; i,j) with signs (-,+,-) for the e sums.  Each G is a DMMA GEMM (rows r in the box, columns the
+// (p,q) box pairs, K = 3 n_o + 3 n_v) staged by cp.async; its accumulators are folded into a 16^3 cube in
+// shared memory, and the energy of Eq. cc14, (W + V1) W / D over a<b<c (V1 = Eq. tensort2), is reduced
+// in the same CTA.  W never reaches HBM.
 #include "tt_launch.h"
 
 namespace tt {
 
-// dst block element e -> global coordinates -> the src block (another tiling of the same index spaces)
+namespace {
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int n = valid ? 16 : 0;   // src-size 0 => zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+constexpr int BX = kTripBox;        // box edge
+constexpr int KC = 8;               // k rows per stage
+constexpr int NS = 4;               // stages
+constexpr int PS = BX + 4;          // P row stride (doubles): = 4 mod 16 -> conflict-free A fragments
+constexpr int QS = BX * BX + 4;     // Q row stride: = 4 mod 16 -> conflict-free B fragments
+constexpr int THREADS = 256;
+
+}  // namespace
+
+// dst block element e -> global coordinates (dst dim order) -> the src block (another tiling and order)
 __global__ void retile_kernel(const RetileParams p) {
   const Segment sg = p.segs[blockIdx.x];
   const RetileBlk b = p.blks[sg.desc];
@@ -21,65 +57,184 @@ __global__ void retile_kernel(const RetileParams p) {
     }
     int64_t bid = 0, el = 0;
     for (int q = 0; q < p.order; ++q) {
-      const int32_t t = p.g2t[q][g[q]];
+      const int32_t gq = g[p.sdim[q]];
+      const int32_t t = p.g2t[q][gq];
       const int64_t o0 = p.toff[q][t];
       bid = bid * p.sgrid[q] + t;
-      el = el * (p.toff[q][t + 1] - o0) + (g[q] - o0);
+      el = el * (p.toff[q][t + 1] - o0) + (gq - o0);
     }
     const int64_t so = p.sblk_off[bid];
     dst[e] = so >= 0 ? p.src[so + el] : 0.0;
   }
 }
 
-// Eq. cc14 over one chunk of one W block: sum over a<b<c, i<j<k of (W + V1) * W / D, V1 = Eq. tensort2
-// (nine Voovv * T1 products read from their blocks), D from the orbital energies.  One partial per CTA
-// (fixed thread order + fixed tree: deterministic, reading R12).
-__global__ void triples_energy_kernel(const TriplesParams p) {
-  __shared__ double red[256];
-  const Segment sg = p.segs[blockIdx.x];
-  const TriplesBlk& B = p.blks[sg.desc];
-  const double* w = p.W + B.w_off;
-  const int32_t ea = B.ext[0], eb = B.ext[1], ec = B.ext[2], ei = B.ext[3], ej = B.ext[4], ek = B.ext[5];
-  const int32_t le[6] = {ea, eb, ec, ei, ej, ek};
+__global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const TriplesParams p) {
+  extern __shared__ __align__(16) double sm[];
+  double* Ps = sm;                              // [NS][KC][PS]
+  double* Qs = Ps + NS * KC * PS;               // [NS][KC][QS]
+  double* cube = Qs + NS * KC * QS;             // [BX][BX][BX]  (a, b, c)
+  double* red = cube + BX * BX * BX;            // [THREADS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t u = p.unit0 + blockIdx.x;
+  const int2 un = p.units[u];
+  const int4 bx = p.box3[un.x];
+  const int4 tr = p.trip[un.y];
+  const int32_t nO = p.nO, nV = p.nV;
+  const int32_t lo[3] = {p.box_lo[bx.x], p.box_lo[bx.y], p.box_lo[bx.z]};
+  const int32_t ex[3] = {p.box_ext[bx.x], p.box_ext[bx.y], p.box_ext[bx.z]};
+  const int32_t I = tr.x, J = tr.y, K = tr.z;
+  const int32_t kA = 3 * nO, kT = 3 * nO + 3 * nV;
+  const int32_t nst = (kT + KC - 1) / KC;       // stages per GEMM
+  const int32_t total = 3 * nst;
+
+  // issue the copies of global stage t into slot t % NS
+  auto issue = [&](int32_t t) {
+    const int g = t / nst;
+    const int32_t k0 = (t - g * nst) * KC;
+    // G(r; p,q): g = 0 -> (a; b,c), 1 -> (b; a,c), 2 -> (c; a,b)
+    const int ri = g, pi = (g == 0) ? 1 : 0, qi = (g == 2) ? 1 : 2;
+    double* P = Ps + (t % NS) * KC * PS;
+    double* Q = Qs + (t % NS) * KC * QS;
+    for (int c = tid; c < KC * (BX / 2) * (1 + BX); c += THREADS) {
+      if (c < KC * (BX / 2)) {              // P: k row, 2 r per copy
+        const int row = c / (BX / 2), r = 2 * (c % (BX / 2));
+        const int32_t kap = k0 + row;
+        const double* src = p.VO;
+        bool ok = kap < kT && r < ex[ri];
+        if (ok) {
+          if (kap < kA) {
+            const int s = kap / nO, m = kap - s * nO;
+            const int32_t x = (s == 2) ? J : I, y = (s == 0) ? J : K;
+            src = p.VO + (((int64_t)x * nO + y) * nO + m) * nV + lo[ri] + r;
+          } else {
+            const int32_t kb = kap - kA;
+            const int s = kb / nV, e = kb - s * nV;
+            const int32_t y = (s == 0) ? J : I, z = (s == 2) ? J : K;
+            src = p.T2 + (((int64_t)y * nO + z) * nV + e) * nV + lo[ri] + r;
+          }
+        }
+        cpa16(P + row * PS + r, src, ok);
+      } else {                              // Q: k row, p, 2 q per copy
+        const int cc = c - KC * (BX / 2);
+        const int row = cc / (BX * BX / 2), rem = cc % (BX * BX / 2);
+        const int pp = rem / (BX / 2), q = 2 * (rem % (BX / 2));
+        const int32_t kap = k0 + row;
+        const double* src = p.T2;
+        bool ok = kap < kT && pp < ex[pi] && q < ex[qi];
+        if (ok) {
+          if (kap < kA) {
+            const int s = kap / nO, m = kap - s * nO;
+            const int32_t z = (s == 0) ? K : (s == 1 ? J : I);
+            src = p.T2 + (((int64_t)m * nO + z) * nV + lo[pi] + pp) * nV + lo[qi] + q;
+          } else {
+            const int32_t kb = kap - kA;
+            const int s = kb / nV, e = kb - s * nV;
+            const int32_t x = (s == 0) ? I : (s == 1 ? J : K);
+            src = p.VV + (((int64_t)e * nO + x) * nV + lo[pi] + pp) * nV + lo[qi] + q;
+          }
+        }
+        cpa16(Q + row * QS + pp * BX + q, src, ok);
+      }
+    }
+  };
+
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int f = 0; f < 4; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
+
+#pragma unroll 1
+  for (int t = 0; t < NS - 1; ++t) {
+    if (t < total) issue(t);
+    cpa_commit();
+  }
+#pragma unroll 1
+  for (int t = 0; t < total; ++t) {
+    cpa_wait<NS - 2>();
+    __syncthreads();
+    if (t + NS - 1 < total) issue(t + NS - 1);
+    cpa_commit();
+    const int g = t / nst;
+    const int32_t k0 = (t - g * nst) * KC;
+    const double* P = Ps + (t % NS) * KC * PS;
+    const double* Q = Qs + (t % NS) * KC * QS;
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const int kl = kk * 4 + (lane & 3);
+      const int32_t kap = k0 + kl;
+      // sign of this k row: m sums (+,-,+), e sums (-,+,-)
+      bool neg;
+      if (kap < kA) neg = (kap >= nO && kap < 2 * nO);
+      else neg = !(kap - kA >= nV && kap - kA < 2 * nV);
+      double a0 = P[kl * PS + (lane >> 2)], a1 = P[kl * PS + 8 + (lane >> 2)];
+      if (neg) { a0 = -a0; a1 = -a1; }
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const double b = Q[kl * QS + warp * 32 + f * 8 + (lane >> 2)];
+        dmma(acc[0][f], a0, b);
+        dmma(acc[1][f], a1, b);
+      }
+    }
+    if ((t + 1) % nst == 0) {               // GEMM g done: fold into the cube
+      __syncthreads();
+#pragma unroll
+      for (int rf = 0; rf < 2; ++rf)
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = rf * 8 + (lane >> 2);
+            const int col = warp * 32 + f * 8 + 2 * (lane & 3) + h;
+            const int pp = col / BX, q = col % BX;
+            const double v = acc[rf][f][h];
+            if (g == 0) cube[(row * BX + pp) * BX + q] = v;
+            else if (g == 1) cube[(pp * BX + row) * BX + q] -= v;
+            else cube[(pp * BX + q) * BX + row] += v;
+            acc[rf][f][h] = 0.0;
+          }
+    }
+  }
+  cpa_wait<0>();
+  __syncthreads();
+  // Eq. cc14 over the cube: (W + V1) W / D for a<b<c (i<j<k by construction)
   double s = 0.0;
-  for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) {
-    int64_t r = e;
-    int32_t l[6];
-    for (int q = 5; q >= 0; --q) { l[q] = (int32_t)(r % le[q]); r /= le[q]; }
-    const int32_t a = B.org[0] + l[0], b = B.org[1] + l[1], c = B.org[2] + l[2];
-    const int32_t i = B.org[3] + l[3], j = B.org[4] + l[4], k = B.org[5] + l[5];
-    if (!(a < b && b < c && i < j && j < k)) continue;
-    const double W = w[e];
-    // V1: pairs (x,y) = (i,j) z=k +, (i,k) z=j -, (j,k) z=i +; (p,q) = (a,b) r=c +, (a,c) r=b -, (b,c) r=a +
-    const int32_t lo[3][3] = {{l[3], l[4], l[5]}, {l[3], l[5], l[4]}, {l[4], l[5], l[3]}};
-    const int32_t eo[3][3] = {{ei, ej, ek}, {ei, ek, ej}, {ej, ek, ei}};
-    const int32_t lv[3][3] = {{l[0], l[1], l[2]}, {l[0], l[2], l[1]}, {l[1], l[2], l[0]}};
-    const int32_t ev[3][3] = {{ea, eb, ec}, {ea, ec, eb}, {eb, ec, ea}};
+  const double dijk = p.eps_o[I] + p.eps_o[J] + p.eps_o[K];
+  for (int idx = tid; idx < BX * BX * BX; idx += THREADS) {
+    const int la = idx / (BX * BX), lb = (idx / BX) % BX, lc = idx % BX;
+    if (la >= ex[0] || lb >= ex[1] || lc >= ex[2]) continue;
+    const int32_t a = lo[0] + la, b = lo[1] + lb, c = lo[2] + lc;
+    if (!(a < b && b < c)) continue;
+    const double W = cube[idx];
+    // V1 (Eq. tensort2): pairs (x,y;z) = (i,j;k)+, (i,k;j)-, (j,k;i)+  x  (p,q;r) = (a,b;c)+, (a,c;b)-, (b,c;a)+
     double v1 = 0.0;
+    const int32_t ox[3] = {I, I, J}, oy[3] = {J, K, K}, oz[3] = {K, J, I};
+    const int32_t vp[3] = {a, a, b}, vq[3] = {b, c, c}, vr[3] = {c, b, a};
 #pragma unroll
     for (int pr = 0; pr < 3; ++pr) {
       double inner = 0.0;
 #pragma unroll
       for (int pq = 0; pq < 3; ++pq) {
-        const int64_t vo = B.v_off[pr * 3 + pq], to = B.t_off[pr * 3 + pq];
-        if (vo < 0 || to < 0) continue;
-        const int64_t vi = (((int64_t)lo[pr][0] * eo[pr][1] + lo[pr][1]) * ev[pq][0] + lv[pq][0]) * ev[pq][1] + lv[pq][1];
-        const int64_t ti = (int64_t)lv[pq][2] * eo[pr][2] + lo[pr][2];
-        const double term = p.Voovv[vo + vi] * p.T1[to + ti];
+        const double term = p.VD[(((int64_t)ox[pr] * nO + oy[pr]) * nV + vp[pq]) * nV + vq[pq]] *
+                            p.T1[(int64_t)vr[pq] * nO + oz[pr]];
         inner = (pq == 1) ? inner - term : inner + term;
       }
       v1 = (pr == 1) ? v1 - inner : v1 + inner;
     }
-    const double D = p.eps_o[i] + p.eps_o[j] + p.eps_o[k] - p.eps_v[a] - p.eps_v[b] - p.eps_v[c];
+    const double D = dijk - p.eps_v[a] - p.eps_v[b] - p.eps_v[c];
     s += (W + v1) * W / D;
   }
-  red[threadIdx.x] = s;
+  red[tid] = s;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+  for (int o = THREADS / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) p.partials[blockIdx.x] = red[0];
+  if (tid == 0) p.partials[u] = red[0];
+}
+
+size_t triples_fused_smem() {
+  return sizeof(double) * ((size_t)NS * KC * (PS + QS) + BX * BX * BX + THREADS);
 }
 
 cudaError_t launch_retile(const RetileParams& p, int64_t nseg, cudaStream_t s) {
@@ -88,9 +243,16 @@ cudaError_t launch_retile(const RetileParams& p, int64_t nseg, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_triples_energy(const TriplesParams& p, int64_t nseg, cudaStream_t s) {
-  if (nseg <= 0) return cudaSuccess;
-  triples_energy_kernel<<<(unsigned)nseg, 256, 0, s>>>(p);
+cudaError_t launch_triples_fused(const TriplesParams& p, int64_t nunits, cudaStream_t s) {
+  if (nunits <= 0) return cudaSuccess;
+  static bool attr = false;
+  const size_t smem = triples_fused_smem();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(triples_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  triples_fused_kernel<<<(unsigned)nunits, THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -170,27 +170,25 @@ TRIPLES_INPUTS = [("T1", "vo", ([0], [1]), 11), ("T2", "vvoo", ([0, 1], [2, 3]),
                   ("Voovv", "oovv", ([0, 1], [2, 3]), 15)]
 
 
-def _restricted_tile_triples(tO, tV, spin):
-    from math import comb
-    def cnt(t, x, y, z):
-        n = [t.size(q) for q in (x, y, z)]
-        if x == y == z:
-            return comb(n[0], 3)
-        if x == y:
-            return comb(n[0], 2) * n[2]
-        if y == z:
-            return n[0] * comb(n[1], 2)
-        return n[0] * n[1] * n[2]
-    out = 0
-    for a, b, c in itertools.combinations_with_replacement(range(tV.ntiles), 3):
-        for i, j, k in itertools.combinations_with_replacement(range(tO.ntiles), 3):
-            if cnt(tV, a, b, c) and cnt(tO, i, j, k):
-                if not spin or sum(tV.tile_spin[x] for x in (a, b, c)) == sum(tO.tile_spin[x] for x in (i, j, k)):
-                    out += 1
-    return out
+def _expected_units(nO, nV, spin, box=16):
+    """Units of the fused kernel: (occupied triple i<j<k) x (16-wide virtual box triple with at least one
+    a<b<c), spin sums equal (alpha = first half, R6)."""
+    def sp(n, x):
+        return (1 if x < n // 2 else -1) if spin else 0
+    ranges = [(0, nV // 2), (nV // 2, nV)] if spin else [(0, nV)]
+    boxes = [(x, min(box, e - x), sp(nV, x)) for b, e in ranges for x in range(b, e, box)]
+    count = 0
+    occ = [sum(sp(nO, x) for x in t) for t in itertools.combinations(range(nO), 3)]
+    for A, B, C in itertools.combinations_with_replacement(boxes, 3):
+        n = sum(1 for a in range(A[0], A[0] + A[1]) for b in range(B[0], B[0] + B[1]) for c in range(C[0], C[0] + C[1])
+                if a < b < c)
+        if n:
+            count += sum(1 for o in occ if o == A[2] + B[2] + C[2])
+    return count
 
 
-@pytest.mark.parametrize("nO,nV,tO,tV,spin", [(7, 10, 3, 4, False), (8, 12, 2, 3, True), (6, 9, 1, 2, False)])
+@pytest.mark.parametrize("nO,nV,tO,tV,spin", [(7, 10, 3, 4, False), (8, 12, 2, 3, True), (6, 40, 1, 10, False),
+                                                (8, 68, 2, 17, True)])
 def test_triples_plan_host(nO, nV, tO, tV, spin):
     import paper_2201_01257_b200 as tt
     ctx = tt.Context(device=-1)
@@ -198,8 +196,10 @@ def test_triples_plan_host(nO, nV, tO, tV, spin):
     dims = {"o": to, "v": tv}
     T = {n: tt.Tensor(ctx, [dims[c] for c in d], spin=sp if spin else None) for n, d, sp, _ in TRIPLES_INPUTS}
     _, info = tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
-    oO, oV = _oracle_dims(nO, nV, tO, tV, spin)
-    assert info["w_blocks_total"] == info["w_blocks"] == _restricted_tile_triples(oO, oV, spin)
+    assert info["w_blocks_total"] == info["w_blocks"] == _expected_units(nO, nV, spin)
+    if not spin:   # every restricted element once: 18 (n_o + n_v) FLOPs each
+        n = (nO * (nO - 1) * (nO - 2) // 6) * (nV * (nV - 1) * (nV - 2) // 6)
+        assert info["flops_alg"] == pytest.approx(18.0 * (nO + nV) * n, rel=1e-12)
     # a dimension on another tiling object is refused
     other = tt.TiledIndexSpace(V, tV)
     bad = tt.Tensor(ctx, [to, to, tv, other])
@@ -238,7 +238,7 @@ def _gpu_case(nO, nV, tO, tV, spin, seed, ws_factor):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nO,nV,tO,tV,spin", [(7, 10, 3, 4, False), (8, 12, 2, 3, True), (6, 11, 4, 5, False)])
+@pytest.mark.parametrize("nO,nV,tO,tV,spin", [(7, 10, 3, 4, False), (8, 12, 2, 3, True), (6, 22, 4, 5, False)])
 def test_triples_energy_gpu_parity(nO, nV, tO, tV, spin):
     E, info, orc, _ = _gpu_case(nO, nV, tO, tV, spin, 3, 50.0)
     Eo, n = TR.energy(*orc)
@@ -251,20 +251,40 @@ def test_triples_energy_gpu_parity(nO, nV, tO, tV, spin):
 
 
 @pytest.mark.gpu
-def test_triples_batching_is_bitwise_invariant():
-    """One W block per batch vs everything in one batch: same partial order, same bits (R12)."""
-    E1, i1, _, _ = _gpu_case(7, 10, 2, 3, False, 4, 1.0)
-    E2, i2, _, _ = _gpu_case(7, 10, 2, 3, False, 4, 1000.0)
-    assert i1["batches"] > 1 and i2["batches"] == 1
+def test_triples_deterministic():
+    """Fixed partial order and fixed final tree (R12): two calls give the same bits."""
+    import torch
+    import paper_2201_01257_b200 as tt
+    E1, i1, _, ctx = _gpu_case(7, 22, 2, 3, False, 4, 1.0)
+    E2, i2, _, _ = _gpu_case(7, 22, 2, 3, False, 4, 1.0)
     assert E1 == E2
 
 
 @pytest.mark.gpu
 def test_triples_energy_gpu_parity_midsize():
-    """Several tiles per space with ragged tails (O=16 tiles 5,5,5,1; V=48 tiles 10 x4 + 8), several batches;
+    """Several tiles per space with ragged tails (O=16 tiles 5,5,5,1; V=48 tiles 10 x4 + 8; three 16-wide boxes);
     oracle = the by-triple form (pinned to the element loops above)."""
-    E, info, orc, _ = _gpu_case(16, 48, 5, 10, False, 7, 8.0)
+    E, info, orc, _ = _gpu_case(16, 48, 5, 10, False, 7, 1.0)
     Eo, n = TR.energy_by_triple(*orc)
-    assert info["batches"] > 1
     assert abs(E - Eo) <= 1e-11 * abs(Eo), (E, Eo)
     assert info["flops_alg"] == pytest.approx(18.0 * (16 + 48) * n, rel=1e-12)
+
+
+@pytest.mark.gpu
+def test_triples_energy_gpu_parity_spin_boxes():
+    """alpha/beta maps with two 16-wide boxes per spin range (V = 36: 18 per range = 16 + 2), spin-forbidden
+    units skipped; oracle = the by-triple form over the dense masked inputs."""
+    E, info, orc, _ = _gpu_case(8, 36, 2, 9, True, 9, 1.0)
+    Eo, n = TR.energy_by_triple(*orc)
+    assert abs(E - Eo) <= 1e-11 * abs(Eo), (E, Eo)
+
+
+def test_triples_odd_virtual_range_refused():
+    import paper_2201_01257_b200 as tt
+    ctx = tt.Context(device=-1)
+    _, _, to, tv = _spaces(tt, 6, 9, 2, 3, False)
+    dims = {"o": to, "v": tv}
+    T = {n: tt.Tensor(ctx, [dims[c] for c in d]) for n, d, sp, _ in TRIPLES_INPUTS}
+    with pytest.raises(tt.TTError) as e:
+        tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
+    assert e.value.name == "TT_E_UNSUPPORTED"
