@@ -86,55 +86,107 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
   const int32_t kA = 3 * nO, kT = 3 * nO + 3 * nV;
   const int32_t nst = (kT + KC - 1) / KC;       // stages per GEMM
   const int32_t total = 3 * nst;
+  const int64_t sQ = (int64_t)nO * nV * nV;     // Q row step per k inside a segment (both parts)
 
-  // issue the copies of global stage t into slot t % NS
+  // Copy assignment (fixed per thread): Q = KC rows x BX p x BX/2 pairs = 4 copies per thread (rows
+  // qrow, +2, +4, +6), P = KC rows x BX/2 pairs for threads < 64.  Each copied k row keeps a cursor
+  // (pointer, step per k, end of its segment); the division-based address math runs only when a row
+  // crosses a segment (or GEMM) boundary.
+  const int qp = tid >> 4, qq = 2 * ((tid >> 1) & 7), qrow = tid & 1;
+  const int prow = tid >> 3, pr2 = 2 * (tid & 7);
+  const bool has_p = tid < KC * (BX / 2);
+  // per GEMM box roles: g = 0 -> (a; b,c), 1 -> (b; a,c), 2 -> (c; a,b)
+  int32_t lr = 0, lp = 0, lq = 0;
+  bool okr = false, okpq = false;
+  auto set_gemm = [&](int g) {
+    const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
+    const int32_t ex_r = g == 0 ? ex[0] : (g == 1 ? ex[1] : ex[2]);
+    const int32_t lo_p = g == 0 ? lo[1] : lo[0], ex_p = g == 0 ? ex[1] : ex[0];
+    const int32_t lo_q = g == 2 ? lo[1] : lo[2], ex_q = g == 2 ? ex[1] : ex[2];
+    lr = lo_r + pr2;
+    lp = lo_p + qp;
+    lq = lo_q + qq;
+    okr = pr2 < ex_r;
+    okpq = qp < ex_p && qq < ex_q;
+  };
+  // source of P row kap (this thread's pair pr2) and its step / segment end
+  auto p_src = [&](int32_t kap, const double*& ptr, int64_t& step, int32_t& end) {
+    if (kap < kA) {
+      const int s = kap / nO, m = kap - s * nO;
+      const int32_t x = (s == 2) ? J : I, y = (s == 0) ? J : K;
+      ptr = p.VO + (((int64_t)x * nO + y) * nO + m) * nV + lr;
+      step = nV;
+      end = (s + 1) * nO;
+    } else if (kap < kT) {
+      const int32_t kb = kap - kA;
+      const int s = kb / nV, e = kb - s * nV;
+      const int32_t y = (s == 0) ? J : I, z = (s == 2) ? J : K;
+      ptr = p.T2 + (((int64_t)y * nO + z) * nV + e) * nV + lr;
+      step = nV;
+      end = kA + (s + 1) * nV;
+    } else {
+      ptr = nullptr;
+      step = 0;
+      end = 0x7fffffff;
+    }
+  };
+  auto q_src = [&](int32_t kap, const double*& ptr, int32_t& end) {
+    if (kap < kA) {
+      const int s = kap / nO, m = kap - s * nO;
+      const int32_t z = (s == 0) ? K : (s == 1 ? J : I);
+      ptr = p.T2 + (((int64_t)m * nO + z) * nV + lp) * nV + lq;
+      end = (s + 1) * nO;
+    } else if (kap < kT) {
+      const int32_t kb = kap - kA;
+      const int s = kb / nV, e = kb - s * nV;
+      const int32_t x = (s == 0) ? I : (s == 1 ? J : K);
+      ptr = p.VV + (((int64_t)e * nO + x) * nV + lp) * nV + lq;
+      end = kA + (s + 1) * nV;
+    } else {
+      ptr = nullptr;
+      end = 0x7fffffff;
+    }
+  };
+  const double* pptr = nullptr;
+  int64_t pstep = 0;
+  int32_t pend = 0, pkap = 0;
+  const double* qptr[4];
+  int32_t qend[4], qkap[4];
+
+  // issue the copies of global stage t (stages are issued in order) into slot t % NS
   auto issue = [&](int32_t t) {
     const int g = t / nst;
     const int32_t k0 = (t - g * nst) * KC;
-    // G(r; p,q): g = 0 -> (a; b,c), 1 -> (b; a,c), 2 -> (c; a,b)
-    const int ri = g, pi = (g == 0) ? 1 : 0, qi = (g == 2) ? 1 : 2;
     double* P = Ps + (t % NS) * KC * PS;
     double* Q = Qs + (t % NS) * KC * QS;
-    for (int c = tid; c < KC * (BX / 2) * (1 + BX); c += THREADS) {
-      if (c < KC * (BX / 2)) {              // P: k row, 2 r per copy
-        const int row = c / (BX / 2), r = 2 * (c % (BX / 2));
-        const int32_t kap = k0 + row;
-        const double* src = p.VO;
-        bool ok = kap < kT && r < ex[ri];
-        if (ok) {
-          if (kap < kA) {
-            const int s = kap / nO, m = kap - s * nO;
-            const int32_t x = (s == 2) ? J : I, y = (s == 0) ? J : K;
-            src = p.VO + (((int64_t)x * nO + y) * nO + m) * nV + lo[ri] + r;
-          } else {
-            const int32_t kb = kap - kA;
-            const int s = kb / nV, e = kb - s * nV;
-            const int32_t y = (s == 0) ? J : I, z = (s == 2) ? J : K;
-            src = p.T2 + (((int64_t)y * nO + z) * nV + e) * nV + lo[ri] + r;
-          }
-        }
-        cpa16(P + row * PS + r, src, ok);
-      } else {                              // Q: k row, p, 2 q per copy
-        const int cc = c - KC * (BX / 2);
-        const int row = cc / (BX * BX / 2), rem = cc % (BX * BX / 2);
-        const int pp = rem / (BX / 2), q = 2 * (rem % (BX / 2));
-        const int32_t kap = k0 + row;
-        const double* src = p.T2;
-        bool ok = kap < kT && pp < ex[pi] && q < ex[qi];
-        if (ok) {
-          if (kap < kA) {
-            const int s = kap / nO, m = kap - s * nO;
-            const int32_t z = (s == 0) ? K : (s == 1 ? J : I);
-            src = p.T2 + (((int64_t)m * nO + z) * nV + lo[pi] + pp) * nV + lo[qi] + q;
-          } else {
-            const int32_t kb = kap - kA;
-            const int s = kb / nV, e = kb - s * nV;
-            const int32_t x = (s == 0) ? I : (s == 1 ? J : K);
-            src = p.VV + (((int64_t)e * nO + x) * nV + lo[pi] + pp) * nV + lo[qi] + q;
-          }
-        }
-        cpa16(Q + row * QS + pp * BX + q, src, ok);
+    if (k0 == 0) {   // new GEMM: roles and cursors from scratch
+      set_gemm(g);
+      pkap = prow;
+      p_src(pkap, pptr, pstep, pend);
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        qkap[n] = qrow + 2 * n;
+        q_src(qkap[n], qptr[n], qend[n]);
       }
+    } else {
+      pkap += KC;
+      if (pkap >= pend) p_src(pkap, pptr, pstep, pend);
+      else pptr += KC * pstep;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        qkap[n] += KC;
+        if (qkap[n] >= qend[n]) q_src(qkap[n], qptr[n], qend[n]);
+        else qptr[n] += KC * sQ;
+      }
+    }
+    if (has_p) {
+      const bool ok = okr && pptr != nullptr;
+      cpa16(P + prow * PS + pr2, ok ? (const void*)pptr : (const void*)p.VO, ok);
+    }
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const bool ok = okpq && qptr[n] != nullptr;
+      cpa16(Q + (qrow + 2 * n) * QS + qp * BX + qq, ok ? (const void*)qptr[n] : (const void*)p.T2, ok);
     }
   };
 
