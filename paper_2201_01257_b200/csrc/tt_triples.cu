@@ -40,6 +40,11 @@ constexpr int PS = BX + 4;          // P row stride (doubles): = 4 mod 16 -> con
 constexpr int QS = BX * BX + 4;     // Q row stride: = 4 mod 16 -> conflict-free B fragments
 constexpr int THREADS = 256;
 
+// W cube (a, b, c) in shared memory with the innermost index XOR-swizzled by f(a) ^ f(b): the fold of each
+// GEMM (lanes spread over {row} x {even or odd columns}) and the energy loop are then bank-conflict free
+__device__ __forceinline__ int swz(int x) { return (x & 1) | ((x & 2) << 2) | (x & 4); }
+__device__ __forceinline__ int cidx(int a, int b, int c) { return (a * BX + b) * BX + (c ^ swz(a) ^ swz(b)); }
+
 }  // namespace
 
 // dst block element e -> global coordinates (dst dim order) -> the src block (another tiling and order)
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
   // qrow, +2, +4, +6), P = KC rows x BX/2 pairs for threads < 64.  Each copied k row keeps a cursor
   // (pointer, step per k, end of its segment); the division-based address math runs only when a row
   // crosses a segment (or GEMM) boundary.
-  const int qp = tid >> 4, qq = 2 * ((tid >> 1) & 7), qrow = tid & 1;
+  const int qp = (tid & 127) >> 3, qq = 2 * (tid & 7), qrow = tid >> 7;   // a warp fills 512 contiguous bytes
   const int prow = tid >> 3, pr2 = 2 * (tid & 7);
   const bool has_p = tid < KC * (BX / 2);
   // per GEMM box roles: g = 0 -> (a; b,c), 1 -> (b; a,c), 2 -> (c; a,b)
@@ -219,8 +224,9 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
       bool neg;
       if (kap < kA) neg = (kap >= nO && kap < 2 * nO);
       else neg = !(kap - kA >= nV && kap - kA < 2 * nV);
-      double a0 = P[kl * PS + (lane >> 2)], a1 = P[kl * PS + 8 + (lane >> 2)];
-      if (neg) { a0 = -a0; a1 = -a1; }
+      const long long sg = neg ? (long long)0x8000000000000000ull : 0ll;   // sign bit flip (integer pipe)
+      const double a0 = __longlong_as_double(__double_as_longlong(P[kl * PS + (lane >> 2)]) ^ sg);
+      const double a1 = __longlong_as_double(__double_as_longlong(P[kl * PS + 8 + (lane >> 2)]) ^ sg);
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
         const double b = Q[kl * QS + warp * 32 + f * 8 + (lane >> 2)];
@@ -240,9 +246,9 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
             const int col = warp * 32 + f * 8 + 2 * (lane & 3) + h;
             const int pp = col / BX, q = col % BX;
             const double v = acc[rf][f][h];
-            if (g == 0) cube[(row * BX + pp) * BX + q] = v;
-            else if (g == 1) cube[(pp * BX + row) * BX + q] -= v;
-            else cube[(pp * BX + q) * BX + row] += v;
+            if (g == 0) cube[cidx(row, pp, q)] = v;
+            else if (g == 1) cube[cidx(pp, row, q)] -= v;
+            else cube[cidx(pp, q, row)] += v;
             acc[rf][f][h] = 0.0;
           }
     }
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
     if (la >= ex[0] || lb >= ex[1] || lc >= ex[2]) continue;
     const int32_t a = lo[0] + la, b = lo[1] + lb, c = lo[2] + lc;
     if (!(a < b && b < c)) continue;
-    const double W = cube[idx];
+    const double W = cube[cidx(la, lb, lc)];
     // V1 (Eq. tensort2): pairs (x,y;z) = (i,j;k)+, (i,k;j)-, (j,k;i)+  x  (p,q;r) = (a,b;c)+, (a,c;b)-, (b,c;a)+
     double v1 = 0.0;
     const int32_t ox[3] = {I, I, J}, oy[3] = {J, K, K}, oz[3] = {K, J, I};
