@@ -158,12 +158,13 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
   const double* qptr[4];
   int32_t qend[4], qkap[4];
 
-  // issue the copies of global stage t (stages are issued in order) into slot t % NS
-  auto issue = [&](int32_t t) {
-    const int g = t / nst;
-    const int32_t k0 = (t - g * nst) * KC;
-    double* P = Ps + (t % NS) * KC * PS;
-    double* Q = Qs + (t % NS) * KC * QS;
+  // issue the copies of the next stage (stages are issued in order; counters instead of divisions)
+  int ig = 0, ik0 = 0, islot = 0;
+  auto issue = [&]() {
+    const int g = ig;
+    const int32_t k0 = ik0;
+    double* P = Ps + islot * KC * PS;
+    double* Q = Qs + islot * KC * QS;
     if (k0 == 0) {   // new GEMM: roles and cursors from scratch
       set_gemm(g);
       pkap = prow;
@@ -193,6 +194,9 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
       const bool ok = okpq && qptr[n] != nullptr;
       cpa16(Q + (qrow + 2 * n) * QS + qp * BX + qq, ok ? (const void*)qptr[n] : (const void*)p.T2, ok);
     }
+    islot = (islot + 1 == NS) ? 0 : islot + 1;
+    ik0 += KC;
+    if (ik0 >= nst * KC) { ik0 = 0; ++ig; }
   };
 
   double acc[2][4][2];
@@ -203,19 +207,19 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
 
 #pragma unroll 1
   for (int t = 0; t < NS - 1; ++t) {
-    if (t < total) issue(t);
+    if (t < total) issue();
     cpa_commit();
   }
+  int g = 0, k0 = 0, slot = 0;
 #pragma unroll 1
   for (int t = 0; t < total; ++t) {
     cpa_wait<NS - 2>();
     __syncthreads();
-    if (t + NS - 1 < total) issue(t + NS - 1);
+    if (t + NS - 1 < total) issue();
     cpa_commit();
-    const int g = t / nst;
-    const int32_t k0 = (t - g * nst) * KC;
-    const double* P = Ps + (t % NS) * KC * PS;
-    const double* Q = Qs + (t % NS) * KC * QS;
+    const double* P = Ps + slot * KC * PS;
+    const double* Q = Qs + slot * KC * QS;
+    slot = (slot + 1 == NS) ? 0 : slot + 1;
 #pragma unroll
     for (int kk = 0; kk < KC / 4; ++kk) {
       const int kl = kk * 4 + (lane & 3);
@@ -234,7 +238,8 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
         dmma(acc[1][f], a1, b);
       }
     }
-    if ((t + 1) % nst == 0) {               // GEMM g done: fold into the cube
+    k0 += KC;
+    if (k0 >= nst * KC) {                    // GEMM g done: fold into the cube
       __syncthreads();
 #pragma unroll
       for (int rf = 0; rf < 2; ++rf)
@@ -251,6 +256,8 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
             else cube[cidx(pp, q, row)] += v;
             acc[rf][f][h] = 0.0;
           }
+      k0 = 0;
+      ++g;
     }
   }
   cpa_wait<0>();
