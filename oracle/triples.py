@@ -9,7 +9,7 @@ SURVEY §8(f) NEXT-4; PAPER §4.1.2, P343-413:
 * Eq. tensort: W = A + B (Eq. abt), A = the nine terms summed over occupied m, B = the nine terms
   summed over virtual e.  The sixth term is printed "+ v^{ik}_{mc} t^{mj}_{ab}"; the definition
   <Phi_ijk^abc|V_N T2|Phi> is antisymmetric under j<->k, which requires "-" (the third term with j,k
-  swapped).  Reading R27: "-" (pinned by a second-quantization evaluation of the definition,
+  swapped; P380).  Reading R27: "-" (pinned by a second-quantization evaluation of the definition,
   tests/test_triples.py).
 * Eq. tensort2: V1 = nine v^{..}_{..} t^k_c products, as printed.
 
