@@ -288,3 +288,21 @@ def test_triples_odd_virtual_range_refused():
     with pytest.raises(tt.TTError) as e:
         tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
     assert e.value.name == "TT_E_UNSUPPORTED"
+
+
+def test_triples_units_partition_over_ranks():
+    """Units split into contiguous equal ranges (every rank's count; the sum is the total)."""
+    import paper_2201_01257_b200 as tt
+    counts = []
+    for r in range(3):
+        ctx = tt.Context(device=-1, rank=r, nranks=3)
+        _, _, to, tv = _spaces(tt, 7, 20, 3, 5, False)
+        dims = {"o": to, "v": tv}
+        T = {n: tt.Tensor(ctx, [dims[c] for c in d]) for n, d, sp, _ in TRIPLES_INPUTS}
+        for X in T.values():
+            X.set_owner(np.full(X.nblocks, tt.TT_REPLICATED, np.int32))
+        _, info = tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
+        counts.append(info["w_blocks"])
+        total = info["w_blocks_total"]
+    assert sum(counts) == total == _expected_units(7, 20, False)
+    assert max(counts) - min(counts) <= 1
