@@ -39,6 +39,11 @@ constexpr int NS = 4;               // stages
 constexpr int PS = BX + 4;          // P row stride (doubles): = 4 mod 16 -> conflict-free A fragments
 constexpr int QS = BX * BX + 4;     // Q row stride: = 4 mod 16 -> conflict-free B fragments
 constexpr int THREADS = 256;
+constexpr int NWARP = THREADS / 32;
+constexpr int CW = BX * BX / NWARP;            // GEMM columns per warp
+constexpr int NFR = CW / 8;                    // 8-wide column fragments per warp
+constexpr int NQ = KC * 128 / THREADS;         // Q rows copied per thread per stage
+constexpr int QR = THREADS / 128;              // row step between them
 
 // W cube (a, b, c) in shared memory with the innermost index XOR-swizzled by f(a) ^ f(b): the fold of each
 // GEMM (lanes spread over {row} x {even or odd columns}) and the energy loop are then bank-conflict free
@@ -93,11 +98,12 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
   const int32_t total = 3 * nst;
   const int64_t sQ = (int64_t)nO * nV * nV;     // Q row step per k inside a segment (both parts)
 
-  // Copy assignment (fixed per thread): Q = KC rows x BX p x BX/2 pairs = 4 copies per thread (rows
-  // qrow, +2, +4, +6), P = KC rows x BX/2 pairs for threads < 64.  Each copied k row keeps a cursor
+  // Copy assignment (fixed per thread): Q = KC rows x BX p x BX/2 pairs = NQ copies per thread (rows
+  // qrow + QR n), P = KC rows x BX/2 pairs for threads < 64.  Each copied k row keeps a cursor
   // (pointer, step per k, end of its segment); the division-based address math runs only when a row
   // crosses a segment (or GEMM) boundary.
   const int qp = (tid & 127) >> 3, qq = 2 * (tid & 7), qrow = tid >> 7;   // a warp fills 512 contiguous bytes
+  static_assert(THREADS % 128 == 0 && KC * (BX / 2) <= THREADS, "copy mapping");
   const int prow = tid >> 3, pr2 = 2 * (tid & 7);
   const bool has_p = tid < KC * (BX / 2);
   // per GEMM box roles: g = 0 -> (a; b,c), 1 -> (b; a,c), 2 -> (c; a,b)
@@ -155,8 +161,8 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
   const double* pptr = nullptr;
   int64_t pstep = 0;
   int32_t pend = 0, pkap = 0;
-  const double* qptr[4];
-  int32_t qend[4], qkap[4];
+  const double* qptr[NQ];
+  int32_t qend[NQ], qkap[NQ];
 
   // issue the copies of the next stage (stages are issued in order; counters instead of divisions)
   int ig = 0, ik0 = 0, islot = 0;
@@ -170,8 +176,8 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
       pkap = prow;
       p_src(pkap, pptr, pstep, pend);
 #pragma unroll
-      for (int n = 0; n < 4; ++n) {
-        qkap[n] = qrow + 2 * n;
+      for (int n = 0; n < NQ; ++n) {
+        qkap[n] = qrow + QR * n;
         q_src(qkap[n], qptr[n], qend[n]);
       }
     } else {
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
       if (pkap >= pend) p_src(pkap, pptr, pstep, pend);
       else pptr += KC * pstep;
 #pragma unroll
-      for (int n = 0; n < 4; ++n) {
+      for (int n = 0; n < NQ; ++n) {
         qkap[n] += KC;
         if (qkap[n] >= qend[n]) q_src(qkap[n], qptr[n], qend[n]);
         else qptr[n] += KC * sQ;
@@ -190,20 +196,20 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
       cpa16(P + prow * PS + pr2, ok ? (const void*)pptr : (const void*)p.VO, ok);
     }
 #pragma unroll
-    for (int n = 0; n < 4; ++n) {
+    for (int n = 0; n < NQ; ++n) {
       const bool ok = okpq && qptr[n] != nullptr;
-      cpa16(Q + (qrow + 2 * n) * QS + qp * BX + qq, ok ? (const void*)qptr[n] : (const void*)p.T2, ok);
+      cpa16(Q + (qrow + QR * n) * QS + qp * BX + qq, ok ? (const void*)qptr[n] : (const void*)p.T2, ok);
     }
     islot = (islot + 1 == NS) ? 0 : islot + 1;
     ik0 += KC;
     if (ik0 >= nst * KC) { ik0 = 0; ++ig; }
   };
 
-  double acc[2][4][2];
+  double acc[2][NFR][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int f = 0; f < 4; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
+    for (int f = 0; f < NFR; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
 
 #pragma unroll 1
   for (int t = 0; t < NS - 1; ++t) {
@@ -232,8 +238,8 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
       const double a0 = __longlong_as_double(__double_as_longlong(P[kl * PS + (lane >> 2)]) ^ sg);
       const double a1 = __longlong_as_double(__double_as_longlong(P[kl * PS + 8 + (lane >> 2)]) ^ sg);
 #pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const double b = Q[kl * QS + warp * 32 + f * 8 + (lane >> 2)];
+      for (int f = 0; f < NFR; ++f) {
+        const double b = Q[kl * QS + warp * CW + f * 8 + (lane >> 2)];
         dmma(acc[0][f], a0, b);
         dmma(acc[1][f], a1, b);
       }
@@ -244,11 +250,11 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
 #pragma unroll
       for (int rf = 0; rf < 2; ++rf)
 #pragma unroll
-        for (int f = 0; f < 4; ++f)
+        for (int f = 0; f < NFR; ++f)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int row = rf * 8 + (lane >> 2);
-            const int col = warp * 32 + f * 8 + 2 * (lane & 3) + h;
+            const int col = warp * CW + f * 8 + 2 * (lane & 3) + h;
             const int pp = col / BX, q = col % BX;
             const double v = acc[rf][f][h];
             if (g == 0) cube[cidx(row, pp, q)] = v;
