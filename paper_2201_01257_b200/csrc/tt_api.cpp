@@ -1563,6 +1563,25 @@ tt_status encode_2d(CUtensorMap* m, const double* base, int64_t cols, int64_t ro
   return TT_OK;
 }
 
+// 4-D tensor map of a dense row-major array; dims innermost first (doubles), box likewise
+tt_status encode_4d(CUtensorMap* m, const double* base, const int64_t* dims4, const uint32_t* box4) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(TT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4], strides[3];
+  cuuint32_t box[4], es[4] = {1, 1, 1, 1};
+  cuuint64_t acc = 8;
+  for (int q = 0; q < 4; ++q) {
+    dims[q] = (cuuint64_t)dims4[q];
+    box[q] = box4[q];
+    if (q > 0) strides[q - 1] = acc;
+    acc *= (cuuint64_t)dims4[q];
+  }
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TT_E_CUDA, "cuTensorMapEncodeTiled (4-D) failed (%d)", (int)r);
+  return TT_OK;
+}
+
 // uniform extent of a fused label group over every non-zero block of T (-1 if it varies)
 int64_t uniform_group_extent(tt_tensor T, const std::vector<int>& tdims) {
   int64_t e = -1;
@@ -3094,6 +3113,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   DeviceGuard dg(ctx->device);
   reset_stats(ctx);
   double* ws = (double*)workspace;
+  if ((uintptr_t)ws % 16) return fail(TT_E_ARG, "workspace must be 16-byte aligned");
   for (int x = 0; x < 5; ++x) {
     tp->rt[x].dst->data = ws + tp->rt[x].ws_pos;
     tp->rt[x].dst->capacity = tp->rt[x].dst->packed_elems;
@@ -3116,11 +3136,26 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   p.nO = (int32_t)nO;
   p.nV = (int32_t)nV;
   p.partials = partials;
+  // TMA boxes (default) or cp.async staging (TT_TMA=0)
+  const char* ft = getenv("TT_TMA");
+  const bool use_tma = !ft || atoi(ft) != 0;
+  CUtensorMap maps[4];
+  if (use_tma) {
+    const uint32_t bP[4] = {(uint32_t)kTripBox + 4, 8, 1, 1}, bQ[4] = {(uint32_t)kTripBox + 2, (uint32_t)kTripBox + 2, 1, 8};
+    const int64_t dVO[4] = {nV, nO, nO, nO}, dT2[4] = {nV, nV, nO, nO}, dVV[4] = {nV, nV, nO, nV};
+    TT_TRY(encode_4d(&maps[0], p.VO, dVO, bP));
+    TT_TRY(encode_4d(&maps[1], p.T2, dT2, bP));
+    TT_TRY(encode_4d(&maps[2], p.T2, dT2, bQ));
+    TT_TRY(encode_4d(&maps[3], p.VV, dVV, bQ));
+  }
+  ctx->last.producer = use_tma ? 1 : 0;
   // launches of at most 2^20 units (keeps each launch's grid small; partials are indexed by unit)
   for (int64_t u0 = tp->unit0; u0 < tp->unit0 + tp->nunits; u0 += (1 << 20)) {
     p.unit0 = u0;
+    const int64_t n = std::min<int64_t>(1 << 20, tp->unit0 + tp->nunits - u0);
     Launch L(ctx, "tt_triples_fused");
-    TT_CUDA(launch_triples_fused(p, std::min<int64_t>(1 << 20, tp->unit0 + tp->nunits - u0), ctx->stream));
+    if (use_tma) TT_CUDA(launch_triples_tma(p, maps, n, ctx->stream));
+    else TT_CUDA(launch_triples_fused(p, n, ctx->stream));
   }
   {
     Launch L(ctx, "tt_scalar_final");

@@ -13,6 +13,8 @@
 // (p,q) box pairs, K = 3 n_o + 3 n_v) staged by cp.async; its accumulators are folded into a 16^3 cube in
 // shared memory, and the energy of Eq. cc14, (W + V1) W / D over a<b<c (V1 = Eq. tensort2), is reduced
 // in the same CTA.  W never reaches HBM.
+#include <cuda.h>
+
 #include "tt_launch.h"
 
 namespace tt {
@@ -302,6 +304,218 @@ __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const Triples
     __syncthreads();
   }
   if (tid == 0) p.partials[u] = red[0];
+}
+
+// -------------------------------------------------------------------------------------------------
+// TMA variant: one thread issues, per stage, two 4-D cp.async.bulk.tensor boxes (P: 20 r x 8 k; Q:
+// 18 q x 18 p x 8 k) that complete on the stage's mbarrier.  The boxes are 2 wider than the data so
+// that the shared-memory row strides (20 and 18 x 18 = 324 doubles, both = 4 mod 16) keep the DMMA
+// fragment loads conflict-free; their extra columns and the tail boxes' columns beyond the box extents
+// are computed and never read back; k rows beyond a segment (m >= n_o, e >= n_v) are TMA zero fill, so
+// every stage lies inside one segment (uniform sign) and no per-thread address arithmetic remains.
+namespace {
+constexpr int TPW = BX + 4;                 // P box width (r)
+constexpr int TQW = BX + 2;                 // Q box width (q) and height (p)
+constexpr int TQS = TQW * TQW;              // Q k-row stride (324 = 4 mod 16)
+constexpr int TNS = 3;                      // stages
+constexpr int TP_BYTES = KC * TPW * 8;      // 1280
+constexpr int TQ_BYTES = KC * TQS * 8;      // 20736
+constexpr int TSTAGE = TP_BYTES + TQ_BYTES;
+
+__device__ __forceinline__ void tbar_init(uint64_t* bar, unsigned count) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s), "r"(count));
+}
+__device__ __forceinline__ void tbar_expect(uint64_t* bar, unsigned bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TWAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TWAIT_%=;\n}\n" ::"r"(s),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma4(void* smem, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+      ::"r"(d), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(b)
+      : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(THREADS, 2)
+    triples_fused_tma_kernel(const TriplesParams p, const __grid_constant__ CUtensorMap mVO,
+                             const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
+                             const __grid_constant__ CUtensorMap mVV) {
+  extern __shared__ __align__(128) unsigned char tsm_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)tsm_raw + 127) & ~(uintptr_t)127);
+  double* cube = reinterpret_cast<double*>(base + TNS * TSTAGE);   // [BX][BX][BX]
+  double* red = cube + BX * BX * BX;                               // [THREADS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t u = p.unit0 + blockIdx.x;
+  const int2 un = p.units[u];
+  const int4 bx = p.box3[un.x];
+  const int4 tr = p.trip[un.y];
+  const int32_t nO = p.nO, nV = p.nV;
+  const int32_t lo[3] = {p.box_lo[bx.x], p.box_lo[bx.y], p.box_lo[bx.z]};
+  const int32_t ex[3] = {p.box_ext[bx.x], p.box_ext[bx.y], p.box_ext[bx.z]};
+  const int32_t I = tr.x, J = tr.y, K = tr.z;
+  const int32_t sA = (nO + KC - 1) / KC, sB = (nV + KC - 1) / KC;   // stages per A / B segment
+  const int32_t nst = 3 * sA + 3 * sB;                               // stages per GEMM
+  const int32_t total = 3 * nst;
+  if (tid == 0) {
+    for (int q = 0; q < TNS; ++q) tbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2Q) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
+  }
+  __syncthreads();
+  // stage t -> (GEMM g, segment, first k row); issued by thread 0 only, in order
+  auto issue = [&](int32_t t) {
+    const int g = t / nst;
+    int32_t r = t - g * nst;
+    const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
+    const int32_t lo_p = g == 0 ? lo[1] : lo[0];
+    const int32_t lo_q = g == 2 ? lo[1] : lo[2];
+    unsigned char* st = base + (t % TNS) * TSTAGE;
+    double* P = reinterpret_cast<double*>(st);
+    double* Q = reinterpret_cast<double*>(st + TP_BYTES);
+    tbar_expect(&full[t % TNS], (unsigned)TSTAGE);
+    if (r < 3 * sA) {
+      const int s = r / sA;
+      const int32_t m0 = (r - s * sA) * KC;
+      const int32_t x = (s == 2) ? J : I, y = (s == 0) ? J : K, z = (s == 0) ? K : (s == 1 ? J : I);
+      tma4(P, &mVO, lo_r, m0, y, x, &full[t % TNS]);          // VO[x][y][m][r]
+      tma4(Q, &mT2Q, lo_q, lo_p, z, m0, &full[t % TNS]);      // T2[m][z][p][q]
+    } else {
+      r -= 3 * sA;
+      const int s = r / sB;
+      const int32_t e0 = (r - s * sB) * KC;
+      const int32_t x = (s == 0) ? I : (s == 1 ? J : K), y = (s == 0) ? J : I, z = (s == 2) ? J : K;
+      tma4(P, &mT2P, lo_r, e0, z, y, &full[t % TNS]);         // T2[y][z][e][r]
+      tma4(Q, &mVV, lo_q, lo_p, x, e0, &full[t % TNS]);       // VV[e][x][p][q]
+    }
+  };
+  if (tid == 0)
+    for (int t = 0; t < TNS && t < total; ++t) issue(t);
+
+  double acc[2][NFR][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int f = 0; f < NFR; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
+  int g = 0, sg = 0, slot = 0;     // GEMM, stage inside the GEMM, ring slot
+  unsigned phase = 0;
+#pragma unroll 1
+  for (int t = 0; t < total; ++t) {
+    tbar_wait(&full[slot], phase);
+    const double* P = reinterpret_cast<const double*>(base + slot * TSTAGE);
+    const double* Q = reinterpret_cast<const double*>(base + slot * TSTAGE + TP_BYTES);
+    // segment of this stage: m sums (+,-,+), e sums (-,+,-)
+    bool neg;
+    if (sg < 3 * sA) neg = (sg >= sA && sg < 2 * sA);
+    else neg = !(sg - 3 * sA >= sB && sg - 3 * sA < 2 * sB);
+    const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const int kl = kk * 4 + (lane & 3);
+      const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
+      const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
+#pragma unroll
+      for (int f = 0; f < NFR; ++f) {
+        const int col = warp * CW + f * 8 + (lane >> 2);
+        const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
+        dmma(acc[0][f], a0, b);
+        dmma(acc[1][f], a1, b);
+      }
+    }
+    __syncthreads();                          // every warp is done with this slot
+    if (tid == 0 && t + TNS < total) issue(t + TNS);
+    slot = (slot + 1 == TNS) ? 0 : slot + 1;
+    if (slot == 0) phase ^= 1;
+    if (++sg == nst) {                        // GEMM g done: fold into the cube
+#pragma unroll
+      for (int rf = 0; rf < 2; ++rf)
+#pragma unroll
+        for (int f = 0; f < NFR; ++f)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = rf * 8 + (lane >> 2);
+            const int col = warp * CW + f * 8 + 2 * (lane & 3) + h;
+            const int pp = col / BX, q = col % BX;
+            const double v = acc[rf][f][h];
+            if (g == 0) cube[cidx(row, pp, q)] = v;
+            else if (g == 1) cube[cidx(pp, row, q)] -= v;
+            else cube[cidx(pp, q, row)] += v;
+            acc[rf][f][h] = 0.0;
+          }
+      __syncthreads();
+      sg = 0;
+      ++g;
+    }
+  }
+  // Eq. cc14 over the cube (as the cp.async kernel)
+  double s = 0.0;
+  const double dijk = p.eps_o[I] + p.eps_o[J] + p.eps_o[K];
+  for (int idx = tid; idx < BX * BX * BX; idx += THREADS) {
+    const int la = idx / (BX * BX), lb = (idx / BX) % BX, lc = idx % BX;
+    if (la >= ex[0] || lb >= ex[1] || lc >= ex[2]) continue;
+    const int32_t a = lo[0] + la, b = lo[1] + lb, c = lo[2] + lc;
+    if (!(a < b && b < c)) continue;
+    const double W = cube[cidx(la, lb, lc)];
+    double v1 = 0.0;
+    const int32_t ox[3] = {I, I, J}, oy[3] = {J, K, K}, oz[3] = {K, J, I};
+    const int32_t vp[3] = {a, a, b}, vq[3] = {b, c, c}, vr[3] = {c, b, a};
+#pragma unroll
+    for (int pr = 0; pr < 3; ++pr) {
+      double inner = 0.0;
+#pragma unroll
+      for (int pq = 0; pq < 3; ++pq) {
+        const double term = p.VD[(((int64_t)ox[pr] * nO + oy[pr]) * nV + vp[pq]) * nV + vq[pq]] *
+                            p.T1[(int64_t)vr[pq] * nO + oz[pr]];
+        inner = (pq == 1) ? inner - term : inner + term;
+      }
+      v1 = (pr == 1) ? v1 - inner : v1 + inner;
+    }
+    const double D = dijk - p.eps_v[a] - p.eps_v[b] - p.eps_v[c];
+    s += (W + v1) * W / D;
+  }
+  red[tid] = s;
+  __syncthreads();
+  for (int o = THREADS / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) p.partials[u] = red[0];
+}
+
+size_t triples_tma_smem() {
+  return 128 + (size_t)TNS * TSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 8 * TNS;
+}
+
+cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s) {
+  if (nunits <= 0) return cudaSuccess;
+  static bool attr = false;
+  const size_t smem = triples_tma_smem();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(triples_fused_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const CUtensorMap* m = static_cast<const CUtensorMap*>(maps);
+  triples_fused_tma_kernel<<<(unsigned)nunits, THREADS, smem, s>>>(p, m[0], m[1], m[2], m[3]);
+  return cudaGetLastError();
 }
 
 size_t triples_fused_smem() {

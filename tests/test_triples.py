@@ -306,3 +306,19 @@ def test_triples_units_partition_over_ranks():
         total = info["w_blocks_total"]
     assert sum(counts) == total == _expected_units(7, 20, False)
     assert max(counts) - min(counts) <= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tma", ["0", "1"])
+def test_triples_both_staging_paths(tma):
+    """TMA-box staging (default) and cp.async staging (TT_TMA=0) give the oracle's energy; O, V not
+    multiples of the 8-row stage (segment tails are TMA zero fill / cp.async zero fill)."""
+    import os
+    os.environ["TT_TMA"] = tma
+    try:
+        E, info, orc, ctx = _gpu_case(13, 38, 4, 7, False, 11, 1.0)
+        assert ctx.stats()["producer"] == int(tma)
+    finally:
+        os.environ.pop("TT_TMA", None)
+    Eo, _ = TR.energy_by_triple(*orc)
+    assert abs(E - Eo) <= 1e-11 * abs(Eo), (E, Eo)
