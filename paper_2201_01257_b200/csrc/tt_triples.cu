@@ -359,7 +359,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   unsigned char* base = (unsigned char*)(((uintptr_t)tsm_raw + 127) & ~(uintptr_t)127);
   double* cube = reinterpret_cast<double*>(base + TNS * TSTAGE);   // [BX][BX][BX]
   double* red = cube + BX * BX * BX;                               // [THREADS]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS] TMA bytes landed
+  uint64_t* empty = full + TNS;                                    // [TNS] every warp done with the slot
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t u = p.unit0 + blockIdx.x;
   const int2 un = p.units[u];
@@ -373,7 +374,10 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int32_t nst = 3 * sA + 3 * sB;                               // stages per GEMM
   const int32_t total = 3 * nst;
   if (tid == 0) {
-    for (int q = 0; q < TNS; ++q) tbar_init(&full[q], 1);
+    for (int q = 0; q < TNS; ++q) {
+      tbar_init(&full[q], 1);
+      tbar_init(&empty[q], NWARP);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
@@ -440,8 +444,15 @@ __global__ void __launch_bounds__(THREADS, 2)
         dmma(acc[1][f], a1, b);
       }
     }
-    __syncthreads();                          // every warp is done with this slot
-    if (tid == 0 && t + TNS < total) issue(t + TNS);
+    __syncwarp();
+    if (lane == 0) {                          // this warp is done with the slot
+      unsigned sa = (unsigned)__cvta_generic_to_shared(&empty[slot]);
+      asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(sa) : "memory");
+    }
+    if (tid == 0 && t + TNS < total) {        // refill it once every warp has released it
+      tbar_wait(&empty[slot], phase);
+      issue(t + TNS);
+    }
     slot = (slot + 1 == TNS) ? 0 : slot + 1;
     if (slot == 0) phase ^= 1;
     if (++sg == nst) {                        // GEMM g done: fold into the cube
@@ -501,7 +512,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 }
 
 size_t triples_tma_smem() {
-  return 128 + (size_t)TNS * TSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 8 * TNS;
+  return 128 + (size_t)TNS * TSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 16 * TNS;
 }
 
 cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s) {
