@@ -2892,6 +2892,8 @@ struct TripPlan {
   tt_tis fullO = nullptr, fullV = nullptr;   // one tile over the whole space (dense copies)
   RetileOp rt[5];                             // VO (O,O,O,V), VV (V,O,V,V), T2 (O,O,V,V), VD (O,O,V,V), T1 (V,O)
   int2* d_units = nullptr;
+  int2* d_pairs = nullptr;                    // pair variant: (first unit, count) per CTA
+  int64_t npairs = 0;
   int4* d_box3 = nullptr;
   int4* d_trip = nullptr;
   int32_t* d_box_lo = nullptr;
@@ -3093,6 +3095,17 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
       TT_TRY(dev_alloc(ctx, &tp->d_box_lo, box_lo.size()));
       TT_TRY(dev_alloc(ctx, &tp->d_box_ext, box_ext.size()));
       if (!units.empty()) TT_CUDA(cudaMemcpy(tp->d_units, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      // pairs of consecutive units of this rank with the same box triple and occupied pair (i,j)
+      std::vector<int2> pairs;
+      for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits;) {
+        const bool two = q + 1 < tp->unit0 + tp->nunits && units[q + 1].x == units[q].x &&
+                         trip[units[q + 1].y].x == trip[units[q].y].x && trip[units[q + 1].y].y == trip[units[q].y].y;
+        pairs.push_back({(int)q, two ? 2 : 1});
+        q += two ? 2 : 1;
+      }
+      tp->npairs = (int64_t)pairs.size();
+      TT_TRY(dev_alloc(ctx, &tp->d_pairs, std::max<size_t>(1, pairs.size())));
+      if (!pairs.empty()) TT_CUDA(cudaMemcpy(tp->d_pairs, pairs.data(), pairs.size() * sizeof(int2), cudaMemcpyHostToDevice));
       if (!box3.empty()) TT_CUDA(cudaMemcpy(tp->d_box3, box3.data(), box3.size() * sizeof(int4), cudaMemcpyHostToDevice));
       TT_CUDA(cudaMemcpy(tp->d_trip, trip.data(), trip.size() * sizeof(int4), cudaMemcpyHostToDevice));
       TT_CUDA(cudaMemcpy(tp->d_box_lo, box_lo.data(), box_lo.size() * 4, cudaMemcpyHostToDevice));
@@ -3148,9 +3161,18 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     TT_TRY(encode_4d(&maps[2], p.T2, dT2, bQ));
     TT_TRY(encode_4d(&maps[3], p.VV, dVV, bQ));
   }
-  ctx->last.producer = use_tma ? 1 : 0;
+  const char* fp = getenv("TT_TRIPLES_PAIR");
+  const bool use_pair = use_tma && (!fp || atoi(fp) != 0);
+  ctx->last.producer = use_pair ? 2 : (use_tma ? 1 : 0);
+  if (use_pair) {
+    for (int64_t q0 = 0; q0 < tp->npairs; q0 += (1 << 20)) {
+      p.pairs = tp->d_pairs + q0;
+      Launch L(ctx, "tt_triples_fused");
+      TT_CUDA(launch_triples_pair(p, maps, std::min<int64_t>(1 << 20, tp->npairs - q0), ctx->stream));
+    }
+  }
   // launches of at most 2^20 units (keeps each launch's grid small; partials are indexed by unit)
-  for (int64_t u0 = tp->unit0; u0 < tp->unit0 + tp->nunits; u0 += (1 << 20)) {
+  for (int64_t u0 = tp->unit0; !use_pair && u0 < tp->unit0 + tp->nunits; u0 += (1 << 20)) {
     p.unit0 = u0;
     const int64_t n = std::min<int64_t>(1 << 20, tp->unit0 + tp->nunits - u0);
     Launch L(ctx, "tt_triples_fused");

@@ -192,6 +192,7 @@ struct TriplesParams {
   const int32_t* box_ext;
   int32_t nO, nV;
   int64_t unit0;        // first unit of this launch
+  const int2* pairs;    // pair variant: (first unit, 1 or 2 units) per CTA
   double* partials;     // one per unit (indexed by unit)
 };
 size_t triples_fused_smem();
@@ -199,5 +200,7 @@ cudaError_t launch_triples_fused(const TriplesParams& p, int64_t nunits, cudaStr
 // TMA variant; maps = 4 CUtensorMap: VO (r,m,y,x) box {20,8,1,1}, T2 as P (b,a,j,i) box {20,8,1,1},
 // T2 as Q (b,a,j,i) box {18,18,1,8}, VV (q,p,x,e) box {18,18,1,8}
 cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s);
+// pair variant (two units with the same box triple and occupied pair (i,j) per CTA, shared operands)
+cudaError_t launch_triples_pair(const TriplesParams& p, const void* maps, int64_t npairs, cudaStream_t s);
 
 }  // namespace tt

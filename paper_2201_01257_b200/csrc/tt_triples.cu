@@ -511,6 +511,218 @@ __global__ void __launch_bounds__(THREADS, 2)
   if (tid == 0) p.partials[u] = red[0];
 }
 
+// -------------------------------------------------------------------------------------------------
+// Pair variant (default): one CTA of 16 warps computes TWO units with the same box triple and occupied
+// triples (i,j,k1), (i,j,k2).  In every segment of the K loop one of the two operands is the same for
+// both triples -- the Q tile (depends on one occupied index) in the segments (A,s=1), (A,s=2), (B,s=0),
+// (B,s=1), the P tile (depends on the pair) in (A,s=0), (B,s=2) -- so that operand is loaded once: 2/3
+// of the K range moves one Q tile for two triples.  Warps 0-7 compute the first triple, 8-15 the second;
+// each triple keeps its own cube and partial, so the energies are bitwise those of the single kernel.
+namespace {
+constexpr int PTHREADS = 2 * THREADS;
+constexpr int PNS = 3;
+constexpr int PSTAGE = 2 * TP_BYTES + 2 * TQ_BYTES;   // P1 P2 Q1 Q2
+}  // namespace
+
+__global__ void __launch_bounds__(PTHREADS, 1)
+    triples_pair_tma_kernel(const TriplesParams p, const __grid_constant__ CUtensorMap mVO,
+                            const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
+                            const __grid_constant__ CUtensorMap mVV) {
+  extern __shared__ __align__(128) unsigned char psm_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)psm_raw + 127) & ~(uintptr_t)127);
+  double* cubes = reinterpret_cast<double*>(base + PNS * PSTAGE);   // [2][BX^3]
+  double* red = cubes + 2 * BX * BX * BX;                          // [PTHREADS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + PTHREADS);    // [PNS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int h = warp >> 3, lw = warp & 7;                          // triple of this warp, warp inside it
+  const int2 pr = p.pairs[blockIdx.x];
+  const int64_t u1 = pr.x;
+  const bool two = pr.y == 2;
+  const int2 un1 = p.units[u1];
+  const int4 bx = p.box3[un1.x];
+  const int4 tr1 = p.trip[un1.y];
+  const int4 tr2 = two ? p.trip[p.units[u1 + 1].y] : tr1;
+  const int32_t nO = p.nO, nV = p.nV;
+  const int32_t lo[3] = {p.box_lo[bx.x], p.box_lo[bx.y], p.box_lo[bx.z]};
+  const int32_t ex[3] = {p.box_ext[bx.x], p.box_ext[bx.y], p.box_ext[bx.z]};
+  const int32_t I = tr1.x, J = tr1.y, K1 = tr1.z, K2 = tr2.z;
+  const int32_t sA = (nO + KC - 1) / KC, sB = (nV + KC - 1) / KC;
+  const int32_t nst = 3 * sA + 3 * sB;
+  const int32_t total = 3 * nst;
+  double* cube = cubes + h * BX * BX * BX;
+  if (tid == 0) {
+    for (int q = 0; q < PNS; ++q) tbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2Q) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
+  }
+  __syncthreads();
+  // segment sharing: 0 = (A,s=0) P shared; 1,2 = (A,s=1/2) Q shared; 3,4 = (B,s=0/1) Q shared; 5 = (B,s=2) P shared
+  auto issue = [&](int32_t t) {
+    const int g = t / nst;
+    int32_t r = t - g * nst;
+    const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
+    const int32_t lo_p = g == 0 ? lo[1] : lo[0];
+    const int32_t lo_q = g == 2 ? lo[1] : lo[2];
+    unsigned char* st = base + (t % PNS) * PSTAGE;
+    double* P1 = reinterpret_cast<double*>(st);
+    double* P2 = reinterpret_cast<double*>(st + TP_BYTES);
+    double* Q1 = reinterpret_cast<double*>(st + 2 * TP_BYTES);
+    double* Q2 = reinterpret_cast<double*>(st + 2 * TP_BYTES + TQ_BYTES);
+    uint64_t* bar = &full[t % PNS];
+    if (r < 3 * sA) {
+      const int s = r / sA;
+      const int32_t m0 = (r - s * sA) * KC;
+      if (s == 0) {          // P = VO[I][J] shared, Q = T2[m][k] per triple
+        tbar_expect(bar, (unsigned)(TP_BYTES + (two ? 2 : 1) * TQ_BYTES));
+        tma4(P1, &mVO, lo_r, m0, J, I, bar);
+        tma4(Q1, &mT2Q, lo_q, lo_p, K1, m0, bar);
+        if (two) tma4(Q2, &mT2Q, lo_q, lo_p, K2, m0, bar);
+      } else {               // s=1: P = VO[I][k], Q = T2[m][J];  s=2: P = VO[J][k], Q = T2[m][I]
+        const int32_t x = (s == 2) ? J : I, z = (s == 1) ? J : I;
+        tbar_expect(bar, (unsigned)((two ? 2 : 1) * TP_BYTES + TQ_BYTES));
+        tma4(P1, &mVO, lo_r, m0, K1, x, bar);
+        if (two) tma4(P2, &mVO, lo_r, m0, K2, x, bar);
+        tma4(Q1, &mT2Q, lo_q, lo_p, z, m0, bar);
+      }
+    } else {
+      r -= 3 * sA;
+      const int s = r / sB;
+      const int32_t e0 = (r - s * sB) * KC;
+      if (s == 2) {          // P = T2[I][J][e] shared, Q = VV[e][k] per triple
+        tbar_expect(bar, (unsigned)(TP_BYTES + (two ? 2 : 1) * TQ_BYTES));
+        tma4(P1, &mT2P, lo_r, e0, J, I, bar);
+        tma4(Q1, &mVV, lo_q, lo_p, K1, e0, bar);
+        if (two) tma4(Q2, &mVV, lo_q, lo_p, K2, e0, bar);
+      } else {               // s=0: P = T2[J][k][e], Q = VV[e][I];  s=1: P = T2[I][k][e], Q = VV[e][J]
+        const int32_t y = (s == 0) ? J : I, x = (s == 0) ? I : J;
+        tbar_expect(bar, (unsigned)((two ? 2 : 1) * TP_BYTES + TQ_BYTES));
+        tma4(P1, &mT2P, lo_r, e0, K1, y, bar);
+        if (two) tma4(P2, &mT2P, lo_r, e0, K2, y, bar);
+        tma4(Q1, &mVV, lo_q, lo_p, x, e0, bar);
+      }
+    }
+  };
+  if (tid == 0)
+    for (int t = 0; t < PNS && t < total; ++t) issue(t);
+
+  double acc[2][NFR][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int f = 0; f < NFR; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
+  const bool active = h == 0 || two;
+  int g = 0, sg = 0, slot = 0;
+  unsigned phase = 0;
+#pragma unroll 1
+  for (int t = 0; t < total; ++t) {
+    tbar_wait(&full[slot], phase);
+    const int seg = sg < 3 * sA ? sg / sA : 3 + (sg - 3 * sA) / sB;
+    const bool pshared = seg == 0 || seg == 5;
+    const unsigned char* st = base + slot * PSTAGE;
+    const double* P = reinterpret_cast<const double*>(st + ((h && !pshared) ? TP_BYTES : 0));
+    const double* Q = reinterpret_cast<const double*>(st + 2 * TP_BYTES + ((h && pshared) ? TQ_BYTES : 0));
+    const bool neg = seg < 3 ? seg == 1 : seg != 4;   // m sums (+,-,+), e sums (-,+,-)
+    const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
+    if (active) {
+#pragma unroll
+      for (int kk = 0; kk < KC / 4; ++kk) {
+        const int kl = kk * 4 + (lane & 3);
+        const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
+        const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
+#pragma unroll
+        for (int f = 0; f < NFR; ++f) {
+          const int col = lw * CW + f * 8 + (lane >> 2);
+          const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
+          dmma(acc[0][f], a0, b);
+          dmma(acc[1][f], a1, b);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && t + PNS < total) issue(t + PNS);
+    slot = (slot + 1 == PNS) ? 0 : slot + 1;
+    if (slot == 0) phase ^= 1;
+    if (++sg == nst) {
+#pragma unroll
+      for (int rf = 0; rf < 2; ++rf)
+#pragma unroll
+        for (int f = 0; f < NFR; ++f)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int row = rf * 8 + (lane >> 2);
+            const int col = lw * CW + f * 8 + 2 * (lane & 3) + hh;
+            const int pp = col / BX, q = col % BX;
+            const double v = acc[rf][f][hh];
+            if (g == 0) cube[cidx(row, pp, q)] = v;
+            else if (g == 1) cube[cidx(pp, row, q)] -= v;
+            else cube[cidx(pp, q, row)] += v;
+            acc[rf][f][hh] = 0.0;
+          }
+      __syncthreads();
+      sg = 0;
+      ++g;
+    }
+  }
+  // Eq. cc14 over each triple's cube (threads 256 h .. 256 h + 255), one partial per unit
+  const int ht = tid & (THREADS - 1);
+  const int32_t Kh = h ? K2 : K1;
+  double s = 0.0;
+  if (active) {
+    const double dijk = p.eps_o[I] + p.eps_o[J] + p.eps_o[Kh];
+    for (int idx = ht; idx < BX * BX * BX; idx += THREADS) {
+      const int la = idx / (BX * BX), lb = (idx / BX) % BX, lc = idx % BX;
+      if (la >= ex[0] || lb >= ex[1] || lc >= ex[2]) continue;
+      const int32_t a = lo[0] + la, b = lo[1] + lb, c = lo[2] + lc;
+      if (!(a < b && b < c)) continue;
+      const double W = cube[cidx(la, lb, lc)];
+      double v1 = 0.0;
+      const int32_t ox[3] = {I, I, J}, oy[3] = {J, Kh, Kh}, oz[3] = {Kh, J, I};
+      const int32_t vp[3] = {a, a, b}, vq[3] = {b, c, c}, vr[3] = {c, b, a};
+#pragma unroll
+      for (int q3 = 0; q3 < 3; ++q3) {
+        double inner = 0.0;
+#pragma unroll
+        for (int pq = 0; pq < 3; ++pq) {
+          const double term = p.VD[(((int64_t)ox[q3] * nO + oy[q3]) * nV + vp[pq]) * nV + vq[pq]] *
+                              p.T1[(int64_t)vr[pq] * nO + oz[q3]];
+          inner = (pq == 1) ? inner - term : inner + term;
+        }
+        v1 = (q3 == 1) ? v1 - inner : v1 + inner;
+      }
+      const double D = dijk - p.eps_v[a] - p.eps_v[b] - p.eps_v[c];
+      s += (W + v1) * W / D;
+    }
+  }
+  red[tid] = s;
+  __syncthreads();
+  for (int o = THREADS / 2; o > 0; o >>= 1) {
+    if (ht < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (ht == 0 && active) p.partials[u1 + h] = red[tid];
+}
+
+size_t triples_pair_smem() {
+  return 128 + (size_t)PNS * PSTAGE + sizeof(double) * (2 * BX * BX * BX + PTHREADS) + 8 * PNS;
+}
+
+cudaError_t launch_triples_pair(const TriplesParams& p, const void* maps, int64_t npairs, cudaStream_t s) {
+  if (npairs <= 0) return cudaSuccess;
+  static bool attr = false;
+  const size_t smem = triples_pair_smem();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(triples_pair_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const CUtensorMap* m = static_cast<const CUtensorMap*>(maps);
+  triples_pair_tma_kernel<<<(unsigned)npairs, PTHREADS, smem, s>>>(p, m[0], m[1], m[2], m[3]);
+  return cudaGetLastError();
+}
+
 size_t triples_tma_smem() {
   return 128 + (size_t)TNS * TSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 16 * TNS;
 }

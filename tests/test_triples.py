@@ -309,16 +309,23 @@ def test_triples_units_partition_over_ranks():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tma", ["0", "1"])
-def test_triples_both_staging_paths(tma):
-    """TMA-box staging (default) and cp.async staging (TT_TMA=0) give the oracle's energy; O, V not
-    multiples of the 8-row stage (segment tails are TMA zero fill / cp.async zero fill)."""
+@pytest.mark.parametrize("tma,pair", [("0", "0"), ("1", "0"), ("1", "1")])
+def test_triples_all_kernel_variants(tma, pair):
+    """cp.async staging (TT_TMA=0), TMA boxes one unit per CTA (TT_TRIPLES_PAIR=0) and the default pair
+    kernel give the oracle's energy -- bitwise the same energy, since every unit's partial is formed in
+    the same order; O, V not multiples of the 8-row stage (segment tails are zero fill)."""
     import os
-    os.environ["TT_TMA"] = tma
+    os.environ["TT_TMA"], os.environ["TT_TRIPLES_PAIR"] = tma, pair
     try:
         E, info, orc, ctx = _gpu_case(13, 38, 4, 7, False, 11, 1.0)
-        assert ctx.stats()["producer"] == int(tma)
+        assert ctx.stats()["producer"] == int(tma) + int(pair)
     finally:
         os.environ.pop("TT_TMA", None)
+        os.environ.pop("TT_TRIPLES_PAIR", None)
     Eo, _ = TR.energy_by_triple(*orc)
     assert abs(E - Eo) <= 1e-11 * abs(Eo), (E, Eo)
+    _ENERGIES.setdefault("v", set()).add(E)
+    assert len(_ENERGIES["v"]) == 1
+
+
+_ENERGIES = {}
