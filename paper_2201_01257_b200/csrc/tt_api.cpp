@@ -3162,7 +3162,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     TT_TRY(encode_4d(&maps[3], p.VV, dVV, bQ));
   }
   const char* fp = getenv("TT_TRIPLES_PAIR");
-  const bool use_pair = use_tma && (!fp || atoi(fp) != 0);
+  const bool use_pair = use_tma && fp && atoi(fp) != 0;   // measured slower (4.59 s vs 3.37 s): opt-in
   ctx->last.producer = use_pair ? 2 : (use_tma ? 1 : 0);
   if (use_pair) {
     for (int64_t q0 = 0; q0 < tp->npairs; q0 += (1 << 20)) {

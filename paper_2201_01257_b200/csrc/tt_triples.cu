@@ -512,7 +512,8 @@ __global__ void __launch_bounds__(THREADS, 2)
 }
 
 // -------------------------------------------------------------------------------------------------
-// Pair variant (default): one CTA of 16 warps computes TWO units with the same box triple and occupied
+// Pair variant (opt-in, TT_TRIPLES_PAIR=1; measured slower at O=40 V=200: 4.59 s vs 3.37 s -- one
+// 16-warp CTA per SM with 3 stages of 44 KB hides the TMA latency worse than two 8-warp CTAs): one CTA computes TWO units with the same box triple and occupied
 // triples (i,j,k1), (i,j,k2).  In every segment of the K loop one of the two operands is the same for
 // both triples -- the Q tile (depends on one occupied index) in the segments (A,s=1), (A,s=2), (B,s=0),
 // (B,s=1), the P tile (depends on the pair) in (A,s=0), (B,s=2) -- so that operand is loaded once: 2/3

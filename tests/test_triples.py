@@ -311,8 +311,8 @@ def test_triples_units_partition_over_ranks():
 @pytest.mark.gpu
 @pytest.mark.parametrize("tma,pair", [("0", "0"), ("1", "0"), ("1", "1")])
 def test_triples_all_kernel_variants(tma, pair):
-    """cp.async staging (TT_TMA=0), TMA boxes one unit per CTA (TT_TRIPLES_PAIR=0) and the default pair
-    kernel give the oracle's energy -- bitwise the same energy, since every unit's partial is formed in
+    """cp.async staging (TT_TMA=0), TMA boxes one unit per CTA (the default) and the opt-in pair kernel
+    (TT_TRIPLES_PAIR=1) give the oracle's energy -- bitwise the same energy, since every unit's partial is formed in
     the same order; O, V not multiples of the 8-row stage (segment tails are zero fill)."""
     import os
     os.environ["TT_TMA"], os.environ["TT_TRIPLES_PAIR"] = tma, pair
