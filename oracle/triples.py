@@ -89,11 +89,12 @@ def energy_elements(T1, T2, Vooov, Vvovv, Voovv, eps_o, eps_v, elems):
     return out
 
 
-def energy_by_triple(T1, T2, Vooov, Vvovv, Voovv, eps_o, eps_v):
+def energy_by_triple(T1, T2, Vooov, Vvovv, Voovv, eps_o, eps_v, max_triples=None):
     """The same Eq. cc14 sum, one occupied triple i<j<k at a time with the 18 terms of Eq. tensort formed
     for all (a,b,c) at once by matrix products (numpy.matmul as the step, P174's contraction of each
     term over m or e), then masked to a<b<c.  Pinned equal to energy() on small sizes; used where the
-    element loop is too slow.  Returns (E, number of terms)."""
+    element loop is too slow.  ``max_triples`` stops after that many occupied triples (a bounded sample
+    for CPU timing).  Returns (E, number of terms).""" 
     nO, nV = len(eps_o), len(eps_v)
     ev = np.asarray(eps_v, dtype=np.float64)
     mask = np.zeros((nV, nV, nV), dtype=bool)
@@ -108,7 +109,9 @@ def energy_by_triple(T1, T2, Vooov, Vvovv, Voovv, eps_o, eps_v):
         return np.tensordot(Vvovv[:, x], T2[:, :, y, z], axes=([0], [0]))
 
     E, n = 0.0, 0
-    for i, j, k in itertools.combinations(range(nO), 3):
+    for t, (i, j, k) in enumerate(itertools.combinations(range(nO), 3)):
+        if max_triples is not None and t >= max_triples:
+            break
         P = lambda X: X - X.transpose(1, 0, 2) + X.transpose(1, 2, 0)  # noqa: E731  X_abc - X_bac + X_cab
         # A: terms 1-3 = P[X_ij,k] over (a|bc): +X(a,b,c) - X(b,a,c) + X(c,a,b)
         A = P(A_term(i, j, k)) - P(A_term(i, k, j)) + P(A_term(j, k, i))

@@ -50,6 +50,23 @@ def build(ctx, nO, nV, tO, tV, spin, world, seed=1):
     return T, (O, V, to, tv), bufs, eo, ev
 
 
+def cpu_baseline(nO, nV, ntrip):
+    """The oracle as it stands (oracle/triples.py energy_by_triple, numpy/BLAS on the host cores) on a
+    bounded sample: the first ``ntrip`` occupied triples, every a<b<c; algorithmic FLOPs 18 (n_o + n_v)
+    per restricted element (values are random: only the time matters)."""
+    from oracle import triples as TR
+    rng = np.random.default_rng(0)
+    args = (rng.uniform(-1, 1, (nV, nO)), rng.uniform(-1, 1, (nV, nV, nO, nO)), rng.uniform(-1, 1, (nO, nO, nO, nV)),
+            rng.uniform(-1, 1, (nV, nO, nV, nV)), rng.uniform(-1, 1, (nO, nO, nV, nV)), rng.uniform(-2, -1, nO),
+            rng.uniform(1, 2, nV))
+    t0 = time.time()
+    _, n = TR.energy_by_triple(*args, max_triples=ntrip)
+    dt = time.time() - t0
+    flops = 18.0 * (nO + nV) * n
+    return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{ntrip} occupied triples x all a<b<c ({n} elements), oracle by-triple form", "seconds": dt}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--O", type=int, default=40)
@@ -60,6 +77,8 @@ def main():
     ap.add_argument("--ws-gb", type=float, default=40.0)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--cpu-triples", type=int, default=3,
+                    help="occupied triples of the CPU oracle sample (rank 0, N=1; 0 = skip)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -107,6 +126,9 @@ def main():
         ms = float(mx[0])
     else:
         ms = float(t[0])
+    cpu = None
+    if rank == 0 and world == 1 and a.cpu_triples > 0:
+        cpu = cpu_baseline(a.O, a.V, a.cpu_triples)
     if rank == 0:
         fexec, falg = float(t[1]), float(t[2])
         print(json.dumps({
@@ -116,7 +138,7 @@ def main():
             "pct_fp64_peak_executed": fexec / ms / 1e9 / 37.1 / world * 100,
             "w_blocks_total": info["w_blocks_total"], "w_blocks_rank0": info["w_blocks"],
             "batches_rank0": info["batches"], "kernels_rank0": kernels, "setup_s": round(setup_s, 1),
-            "workspace_gb": ws.numel() * 8e-9}), flush=True)
+            "workspace_gb": ws.numel() * 8e-9, "cpu_baseline": cpu}), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
