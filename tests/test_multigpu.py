@@ -3,7 +3,8 @@ with split and round-robin ownership, bitwise equal to 1 GPU and within 1e-11 of
 all-reduce; permuted add; implicit Cholesky ladder) and tests/mgpu_ccsd_check.py (the CCSD-shaped
 iteration with distributed placement and compact R2 vs the oracle transcription) and
 tests/mgpu_triples_check.py (the (T) energy with units split over the ranks vs the oracle and vs one
-rank), one process per GPU over NCCL.  Skipped on boxes with fewer than 2 GPUs."""
+rank) and tests/mgpu_next3_check.py (contract3 and sliced views with round-robin owners, gathered over
+NCCL), one process per GPU over NCCL.  Skipped on boxes with fewer than 2 GPUs."""
 import os
 import subprocess
 import sys
@@ -21,7 +22,8 @@ def _ngpus():
 
 @pytest.mark.parametrize("script,marker,port", [("mgpu_check.py", "MGPU_CHECK PASS", 29531),
                                                 ("mgpu_ccsd_check.py", "MGPU_CCSD_CHECK PASS", 29532),
-                                                ("mgpu_triples_check.py", "MGPU_TRIPLES_CHECK PASS", 29533)])
+                                                ("mgpu_triples_check.py", "MGPU_TRIPLES_CHECK PASS", 29533),
+                                                ("mgpu_next3_check.py", "MGPU_NEXT3_CHECK PASS", 29534)])
 def test_multigpu_script(script, marker, port):
     n = min(_ngpus(), 4)
     if n < 2:
