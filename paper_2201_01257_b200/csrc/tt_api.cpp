@@ -2900,6 +2900,7 @@ struct TripPlan {
   int32_t* d_box_ext = nullptr;
   double* d_partials = nullptr;
   int64_t unit0 = 0, nunits = 0, nunits_total = 0;
+  int32_t o_half = 0, v_half = 0;
   int64_t ws_need = 0;
   tt_triples_info info{};
   ~TripPlan() {
@@ -3077,12 +3078,47 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     tp->unit0 = U * ctx->rank / ctx->nranks;
     tp->nunits = U * (ctx->rank + 1) / ctx->nranks - tp->unit0;
     for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits; ++q) alg += per * (double)box3_n[units[q].x];
-    const int64_t kpad = (3 * nO + 3 * nV + 7) / 8 * 8;
+    // spin split points (R6: alpha = the first range) when each space is exactly (alpha, beta)
+    auto half = [](tt_tis t) -> int32_t {
+      const tt_is s = t->is;
+      return (s->rb.size() == 2 && s->rspin[0] == 1 && s->rspin[1] == -1) ? (int32_t)s->re[0] : 0;
+    };
+    tp->o_half = half(tO);
+    tp->v_half = half(tV);
+    // executed FLOPs of the default (TMA) kernel: per unit, per GEMM, per segment ceil(len / 8) stages of
+    // 8 k rows over the 16 x 256 output (the segment ranges follow the kernel's spin restriction)
+    {
+      const int32_t oh = tp->o_half, vh = tp->v_half;
+      auto so = [&](int32_t x) { return oh ? (x < oh ? 1 : -1) : 0; };
+      auto sv = [&](int32_t v) { return vh ? (v < vh ? 1 : -1) : 0; };
+      double stages = 0;
+      for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits; ++q) {
+        const int4 b3 = box3[units[q].x];
+        const int4 tr = trip[units[q].y];
+        const int32_t bl[3] = {box_lo[b3.x], box_lo[b3.y], box_lo[b3.z]};
+        for (int g = 0; g < 3; ++g) {
+          const int32_t sr = sv(bl[g]), sp = sv(g == 0 ? bl[1] : bl[0]), sq = sv(g == 2 ? bl[1] : bl[2]);
+          for (int sg = 0; sg < 6; ++sg) {
+            int64_t len;
+            if (sg < 3) {
+              const int32_t x = (sg == 2) ? tr.y : tr.x, y = (sg == 0) ? tr.y : tr.z;
+              const int32_t sm = so(x) + so(y) - sr;
+              len = !oh ? nO : (sm == 1 ? oh : (sm == -1 ? nO - oh : 0));
+            } else {
+              const int32_t x = (sg == 3) ? tr.x : (sg == 4 ? tr.y : tr.z);
+              const int32_t se = sp + sq - so(x);
+              len = !vh ? nV : (se == 1 ? vh : (se == -1 ? nV - vh : 0));
+            }
+            stages += (double)((len + 7) / 8);
+          }
+        }
+      }
+      tp->info.flops_exec = stages * 8.0 * 2.0 * kTripBox * kTripBox * kTripBox;
+    }
     tp->info.w_blocks_total = U;
     tp->info.w_blocks = tp->nunits;
     tp->info.batches = 1;
     tp->info.flops_alg = alg;
-    tp->info.flops_exec = (double)tp->nunits * 3.0 * 2.0 * kTripBox * kTripBox * kTripBox * (double)kpad;
     tp->ws_need = base + (U + 1) / 2 * 2;
     tp->info.ws_elems = tp->ws_need;
     if (ctx->device >= 0) {
@@ -3148,6 +3184,8 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   p.box_ext = tp->d_box_ext;
   p.nO = (int32_t)nO;
   p.nV = (int32_t)nV;
+  p.o_half = tp->o_half;
+  p.v_half = tp->v_half;
   p.partials = partials;
   // TMA boxes (default) or cp.async staging (TT_TMA=0)
   const char* ft = getenv("TT_TMA");

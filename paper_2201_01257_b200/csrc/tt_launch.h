@@ -191,6 +191,8 @@ struct TriplesParams {
   const int32_t* box_lo;
   const int32_t* box_ext;
   int32_t nO, nV;
+  int32_t o_half, v_half;   // spin split points (alpha = [0, half), R6); 0 = no spin (TMA kernel skips
+                            // the spin-forbidden half of every m / e sum)
   int64_t unit0;        // first unit of this launch
   const int2* pairs;    // pair variant: (first unit, 1 or 2 units) per CTA
   double* partials;     // one per unit (indexed by unit)

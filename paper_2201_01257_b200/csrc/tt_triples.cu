@@ -359,8 +359,9 @@ __global__ void __launch_bounds__(THREADS, 2)
   unsigned char* base = (unsigned char*)(((uintptr_t)tsm_raw + 127) & ~(uintptr_t)127);
   double* cube = reinterpret_cast<double*>(base + TNS * TSTAGE);   // [BX][BX][BX]
   double* red = cube + BX * BX * BX;                               // [THREADS]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS] TMA bytes landed
-  uint64_t* empty = full + TNS;                                    // [TNS] every warp done with the slot
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS]
+  int32_t* segb = reinterpret_cast<int32_t*>(full + TNS);          // [3][6] first summed index
+  int32_t* segn = segb + 18;                                       // [3][6] stages
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t u = p.unit0 + blockIdx.x;
   const int2 un = p.units[u];
@@ -370,111 +371,146 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int32_t lo[3] = {p.box_lo[bx.x], p.box_lo[bx.y], p.box_lo[bx.z]};
   const int32_t ex[3] = {p.box_ext[bx.x], p.box_ext[bx.y], p.box_ext[bx.z]};
   const int32_t I = tr.x, J = tr.y, K = tr.z;
-  const int32_t sA = (nO + KC - 1) / KC, sB = (nV + KC - 1) / KC;   // stages per A / B segment
-  const int32_t nst = 3 * sA + 3 * sB;                               // stages per GEMM
-  const int32_t total = 3 * nst;
   if (tid == 0) {
-    for (int q = 0; q < TNS; ++q) {
-      tbar_init(&full[q], 1);
-      tbar_init(&empty[q], NWARP);
-    }
+    for (int q = 0; q < TNS; ++q) tbar_init(&full[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2Q) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
   }
+  if (tid < 18) {
+    // summed range of segment sg of GEMM g.  With spin (R6: alpha = first half), the m of v^{xy}_{m r}
+    // must have spin s_x + s_y - s_r and the e of v^{e x}_{p q} spin s_p + s_q - s_x (R7 maps); the other
+    // half of the sum is identically zero and is skipped.
+    const int g = tid / 6, sg = tid % 6;
+    const int32_t oh = p.o_half, vh = p.v_half;
+    auto so = [&](int32_t x) { return oh ? (x < oh ? 1 : -1) : 0; };
+    auto sv = [&](int32_t v) { return vh ? (v < vh ? 1 : -1) : 0; };
+    const int32_t sr = sv(g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]));
+    const int32_t sp = sv(g == 0 ? lo[1] : lo[0]), sq = sv(g == 2 ? lo[1] : lo[2]);
+    int32_t b = 0, e = 0;
+    if (sg < 3) {
+      const int32_t x = (sg == 2) ? J : I, y = (sg == 0) ? J : K;
+      const int32_t sm = so(x) + so(y) - sr;
+      if (!oh) { b = 0; e = nO; }
+      else if (sm == 1) { b = 0; e = oh; }
+      else if (sm == -1) { b = oh; e = nO; }
+    } else {
+      const int32_t x = (sg == 3) ? I : (sg == 4 ? J : K);
+      const int32_t se = sp + sq - so(x);
+      if (!vh) { b = 0; e = nV; }
+      else if (se == 1) { b = 0; e = vh; }
+      else if (se == -1) { b = vh; e = nV; }
+    }
+    segb[tid] = b;
+    segn[tid] = (e - b + KC - 1) / KC;
+  }
   __syncthreads();
-  // stage t -> (GEMM g, segment, first k row); issued by thread 0 only, in order
-  auto issue = [&](int32_t t) {
-    const int g = t / nst;
-    int32_t r = t - g * nst;
+  int32_t total = 0;
+  for (int q = 0; q < 18; ++q) total += segn[q];
+  // stage cursor over (GEMM, segment, stage) skipping empty segments
+  struct Cur { int g, sg, j; };
+  auto advance = [&](Cur& c) {
+    if (++c.j < segn[c.g * 6 + c.sg]) return;
+    c.j = 0;
+    do {
+      if (++c.sg == 6) { c.sg = 0; ++c.g; }
+    } while (c.g < 3 && segn[c.g * 6 + c.sg] == 0);
+  };
+  auto first = [&]() {
+    Cur c{0, 0, 0};
+    while (c.g < 3 && segn[c.g * 6 + c.sg] == 0) {
+      if (++c.sg == 6) { c.sg = 0; ++c.g; }
+    }
+    return c;
+  };
+  int islot = 0;
+  Cur ic = first();
+  auto issue = [&]() {   // thread 0: the stage at cursor ic into slot islot
+    const int g = ic.g, sg = ic.sg;
+    const int32_t k0 = segb[g * 6 + sg] + ic.j * KC;
     const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
     const int32_t lo_p = g == 0 ? lo[1] : lo[0];
     const int32_t lo_q = g == 2 ? lo[1] : lo[2];
-    unsigned char* st = base + (t % TNS) * TSTAGE;
+    unsigned char* st = base + islot * TSTAGE;
     double* P = reinterpret_cast<double*>(st);
     double* Q = reinterpret_cast<double*>(st + TP_BYTES);
-    tbar_expect(&full[t % TNS], (unsigned)TSTAGE);
-    if (r < 3 * sA) {
-      const int s = r / sA;
-      const int32_t m0 = (r - s * sA) * KC;
+    tbar_expect(&full[islot], (unsigned)TSTAGE);
+    if (sg < 3) {
+      const int s = sg;
       const int32_t x = (s == 2) ? J : I, y = (s == 0) ? J : K, z = (s == 0) ? K : (s == 1 ? J : I);
-      tma4(P, &mVO, lo_r, m0, y, x, &full[t % TNS]);          // VO[x][y][m][r]
-      tma4(Q, &mT2Q, lo_q, lo_p, z, m0, &full[t % TNS]);      // T2[m][z][p][q]
+      tma4(P, &mVO, lo_r, k0, y, x, &full[islot]);          // VO[x][y][m][r]
+      tma4(Q, &mT2Q, lo_q, lo_p, z, k0, &full[islot]);      // T2[m][z][p][q]
     } else {
-      r -= 3 * sA;
-      const int s = r / sB;
-      const int32_t e0 = (r - s * sB) * KC;
+      const int s = sg - 3;
       const int32_t x = (s == 0) ? I : (s == 1 ? J : K), y = (s == 0) ? J : I, z = (s == 2) ? J : K;
-      tma4(P, &mT2P, lo_r, e0, z, y, &full[t % TNS]);         // T2[y][z][e][r]
-      tma4(Q, &mVV, lo_q, lo_p, x, e0, &full[t % TNS]);       // VV[e][x][p][q]
+      tma4(P, &mT2P, lo_r, k0, z, y, &full[islot]);         // T2[y][z][e][r]
+      tma4(Q, &mVV, lo_q, lo_p, x, k0, &full[islot]);       // VV[e][x][p][q]
     }
+    advance(ic);
+    islot = (islot + 1 == TNS) ? 0 : islot + 1;
   };
+  // rows past a segment's end read the next index range: zero (spin-forbidden half under R7 maps) or TMA
+  // out-of-bounds fill past n_o / n_v
   if (tid == 0)
-    for (int t = 0; t < TNS && t < total; ++t) issue(t);
+    for (int t = 0; t < TNS && t < total; ++t) issue();
 
   double acc[2][NFR][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int f = 0; f < NFR; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
-  int g = 0, sg = 0, slot = 0;     // GEMM, stage inside the GEMM, ring slot
+  int slot = 0, t = 0;
   unsigned phase = 0;
 #pragma unroll 1
-  for (int t = 0; t < total; ++t) {
-    tbar_wait(&full[slot], phase);
-    const double* P = reinterpret_cast<const double*>(base + slot * TSTAGE);
-    const double* Q = reinterpret_cast<const double*>(base + slot * TSTAGE + TP_BYTES);
-    // segment of this stage: m sums (+,-,+), e sums (-,+,-)
-    bool neg;
-    if (sg < 3 * sA) neg = (sg >= sA && sg < 2 * sA);
-    else neg = !(sg - 3 * sA >= sB && sg - 3 * sA < 2 * sB);
-    const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
+  for (int g = 0; g < 3; ++g) {
+#pragma unroll 1
+    for (int sg = 0; sg < 6; ++sg) {
+      const int32_t n = segn[g * 6 + sg];
+      const bool neg = sg < 3 ? sg == 1 : sg != 4;   // m sums (+,-,+), e sums (-,+,-)
+      const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
+#pragma unroll 1
+      for (int jj = 0; jj < n; ++jj, ++t) {
+        tbar_wait(&full[slot], phase);
+        const double* P = reinterpret_cast<const double*>(base + slot * TSTAGE);
+        const double* Q = reinterpret_cast<const double*>(base + slot * TSTAGE + TP_BYTES);
 #pragma unroll
-    for (int kk = 0; kk < KC / 4; ++kk) {
-      const int kl = kk * 4 + (lane & 3);
-      const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
-      const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
+        for (int kk = 0; kk < KC / 4; ++kk) {
+          const int kl = kk * 4 + (lane & 3);
+          const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
+          const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
 #pragma unroll
-      for (int f = 0; f < NFR; ++f) {
-        const int col = warp * CW + f * 8 + (lane >> 2);
-        const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
-        dmma(acc[0][f], a0, b);
-        dmma(acc[1][f], a1, b);
+          for (int f = 0; f < NFR; ++f) {
+            const int col = warp * CW + f * 8 + (lane >> 2);
+            const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
+            dmma(acc[0][f], a0, b);
+            dmma(acc[1][f], a1, b);
+          }
+        }
+        __syncthreads();                          // every warp is done with this slot
+        if (tid == 0 && t + TNS < total) issue();
+        slot = (slot + 1 == TNS) ? 0 : slot + 1;
+        if (slot == 0) phase ^= 1;
       }
     }
-    __syncwarp();
-    if (lane == 0) {                          // this warp is done with the slot
-      unsigned sa = (unsigned)__cvta_generic_to_shared(&empty[slot]);
-      asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(sa) : "memory");
-    }
-    if (tid == 0 && t + TNS < total) {        // refill it once every warp has released it
-      tbar_wait(&empty[slot], phase);
-      issue(t + TNS);
-    }
-    slot = (slot + 1 == TNS) ? 0 : slot + 1;
-    if (slot == 0) phase ^= 1;
-    if (++sg == nst) {                        // GEMM g done: fold into the cube
+    // GEMM g done: fold into the cube
 #pragma unroll
-      for (int rf = 0; rf < 2; ++rf)
+    for (int rf = 0; rf < 2; ++rf)
 #pragma unroll
-        for (int f = 0; f < NFR; ++f)
+      for (int f = 0; f < NFR; ++f)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int row = rf * 8 + (lane >> 2);
-            const int col = warp * CW + f * 8 + 2 * (lane & 3) + h;
-            const int pp = col / BX, q = col % BX;
-            const double v = acc[rf][f][h];
-            if (g == 0) cube[cidx(row, pp, q)] = v;
-            else if (g == 1) cube[cidx(pp, row, q)] -= v;
-            else cube[cidx(pp, q, row)] += v;
-            acc[rf][f][h] = 0.0;
-          }
-      __syncthreads();
-      sg = 0;
-      ++g;
-    }
+        for (int h = 0; h < 2; ++h) {
+          const int row = rf * 8 + (lane >> 2);
+          const int col = warp * CW + f * 8 + 2 * (lane & 3) + h;
+          const int pp = col / BX, q = col % BX;
+          const double v = acc[rf][f][h];
+          if (g == 0) cube[cidx(row, pp, q)] = v;
+          else if (g == 1) cube[cidx(pp, row, q)] -= v;
+          else cube[cidx(pp, q, row)] += v;
+          acc[rf][f][h] = 0.0;
+        }
+    __syncthreads();
   }
   // Eq. cc14 over the cube (as the cp.async kernel)
   double s = 0.0;
