@@ -299,8 +299,9 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, 
  *   workspace  device memory of ws_elems doubles >= info->ws_elems (dense copies + one partial per
  *              unit), or NULL to return only info.
  *   info       (may be NULL) w_blocks_total / w_blocks = units in total / on this rank; batches = 1;
- *              flops_alg = 18 (n_o + n_v) FLOPs per restricted element (a<b<c, i<j<k, spin-allowed) of
- *              this rank; flops_exec = FLOPs the default (TMA) kernel's GEMMs execute (16-wide boxes,
+ *              flops_alg = FLOPs of the defined sums over the restricted elements (a<b<c, i<j<k,
+ *              spin-allowed) of this rank: 2 per non-zero product of the 18 terms (18 (n_o + n_v) per
+ *              element without spin; only the spin-allowed half of each m / e sum with alpha/beta spaces); flops_exec = FLOPs the default (TMA) kernel's GEMMs execute (16-wide boxes,
  *              8-row stages per m / e segment; with alpha/beta spaces only the spin-allowed half of each
  *              m / e sum is run);
  *              ws_elems = workspace needed. */

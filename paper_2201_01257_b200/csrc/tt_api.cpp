@@ -3077,7 +3077,6 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     tp->nunits_total = U;
     tp->unit0 = U * ctx->rank / ctx->nranks;
     tp->nunits = U * (ctx->rank + 1) / ctx->nranks - tp->unit0;
-    for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits; ++q) alg += per * (double)box3_n[units[q].x];
     // spin split points (R6: alpha = the first range) when each space is exactly (alpha, beta)
     auto half = [](tt_tis t) -> int32_t {
       const tt_is s = t->is;
@@ -3092,7 +3091,9 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
       auto so = [&](int32_t x) { return oh ? (x < oh ? 1 : -1) : 0; };
       auto sv = [&](int32_t v) { return vh ? (v < vh ? 1 : -1) : 0; };
       double stages = 0;
+      (void)per;
       for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits; ++q) {
+        double unit_len = 0;   // summed indices with non-zero products over the 18 terms of one element
         const int4 b3 = box3[units[q].x];
         const int4 tr = trip[units[q].y];
         const int32_t bl[3] = {box_lo[b3.x], box_lo[b3.y], box_lo[b3.z]};
@@ -3110,8 +3111,10 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
               len = !vh ? nV : (se == 1 ? vh : (se == -1 ? nV - vh : 0));
             }
             stages += (double)((len + 7) / 8);
+            unit_len += (double)len;
           }
         }
+        alg += 2.0 * unit_len * (double)box3_n[units[q].x];
       }
       tp->info.flops_exec = stages * 8.0 * 2.0 * kTripBox * kTripBox * kTripBox;
     }

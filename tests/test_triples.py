@@ -329,3 +329,34 @@ def test_triples_all_kernel_variants(tma, pair):
 
 
 _ENERGIES = {}
+
+
+def test_triples_algorithmic_flops_spin_brute_force():
+    """flops_alg = 2 per non-zero product of the 18 terms over the restricted spin-allowed elements: counted
+    here element by element from the spin rule of R7 (v^{xy}_{m p} needs s_m = s_x + s_y - s_p, v^{e x}_{p q}
+    needs s_e = s_p + s_q - s_x)."""
+    import paper_2201_01257_b200 as tt
+    nO, nV = 8, 20
+    ctx = tt.Context(device=-1)
+    _, _, to, tv = _spaces(tt, nO, nV, 2, 5, True)
+    dims = {"o": to, "v": tv}
+    T = {n: tt.Tensor(ctx, [dims[c] for c in d], spin=sp) for n, d, sp, _ in TRIPLES_INPUTS}
+    _, info = tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
+    so = [1 if x < nO // 2 else -1 for x in range(nO)]
+    sv = [1 if x < nV // 2 else -1 for x in range(nV)]
+    nm = {1: sum(1 for x in so if x == 1), -1: sum(1 for x in so if x == -1)}
+    ne = {1: sum(1 for x in sv if x == 1), -1: sum(1 for x in sv if x == -1)}
+    total = 0
+    for i, j, k in itertools.combinations(range(nO), 3):
+        for a, b, c in itertools.combinations(range(nV), 3):
+            if so[i] + so[j] + so[k] != sv[a] + sv[b] + sv[c]:
+                continue
+            n = 0
+            for x, y in ((i, j), (i, k), (j, k)):          # A terms: v^{xy}_{m p}, p in (a, b, c)
+                for p in (a, b, c):
+                    n += nm.get(so[x] + so[y] - sv[p], 0)
+            for x in (i, j, k):                             # B terms: v^{e x}_{p q}, (p, q) in (ab, ac, bc)
+                for p, q in ((a, b), (a, c), (b, c)):
+                    n += ne.get(sv[p] + sv[q] - so[x], 0)
+            total += 2 * n
+    assert info["flops_alg"] == total
