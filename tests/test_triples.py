@@ -360,3 +360,21 @@ def test_triples_algorithmic_flops_spin_brute_force():
                     n += ne.get(sv[p] + sv[q] - so[x], 0)
             total += 2 * n
     assert info["flops_alg"] == total
+
+
+def test_triples_argument_errors():
+    """Too small a workspace -> TT_E_OOM; missing orbital energies -> TT_E_ARG (checked before any launch)."""
+    import paper_2201_01257_b200 as tt
+    ctx = tt.Context(device=-1)
+    _, _, to, tv = _spaces(tt, 6, 10, 2, 4, False)
+    dims = {"o": to, "v": tv}
+    T = {n: tt.Tensor(ctx, [dims[c] for c in d]) for n, d, sp, _ in TRIPLES_INPUTS}
+    args = (T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
+    _, info = tt.triples_energy(ctx, *args)
+    fake = 1 << 20   # never dereferenced: the calls fail during validation
+    with pytest.raises(tt.TTError) as e:
+        tt.triples_energy(ctx, *args, fake, fake, fake, ws_elems=info["ws_elems"] - 2)
+    assert e.value.name == "TT_E_OOM"
+    with pytest.raises(tt.TTError) as e:
+        tt.triples_energy(ctx, *args, None, fake, fake, ws_elems=info["ws_elems"])
+    assert e.value.name == "TT_E_ARG"
