@@ -285,6 +285,9 @@ def main():
     torch.cuda.synchronize()
 
     def step():
+        if world > 1:   # every term's input gather on the comm stream first: they overlap the kernels
+            for (c, cl, a, al, b, bl) in ops:
+                tt.contract_prefetch(ctx, T[c], cl, 1.0, T[a], al, T[b], bl)
         for (c, cl, a, al, b, bl) in ops:
             tt.contract(ctx, T[c], cl, 1.0, 1.0, T[a], al, T[b], bl)
 

@@ -240,6 +240,18 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double
                  const char* a_lbl);
 tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha,
                       tt_tensor A, const char* a_lbl, tt_tensor B, const char* b_lbl);
+/* Prefetch of the input gather of a later tt_contract with the same arguments (SURVEY §8(e) "gathers run on
+ * a comm stream ... overlapped with compute"): the NCCL send/recv of exactly the input ranges this rank's
+ * tasks read but does not hold is issued now on the context's communication stream, after everything
+ * already issued on the context stream (so earlier kernels that read those ranges are not overwritten);
+ * the next tt_contract of this plan (same tensors, labels, beta != 0 or == 0) waits for it instead of
+ * gathering, so its kernel starts as soon as the data is there and the transfer overlaps whatever runs on
+ * the context stream in between (e.g. the previous contraction's kernel).  Gathers that are not prefetched
+ * wait for pending prefetched ones (one communicator is never used by two streams at once).  SPMD: every
+ * rank issues the same prefetch / contract sequence.  No-op with nranks == 1.  TT_E_STATE if this
+ * contraction is already prefetched and not yet executed. */
+tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, tt_tensor A,
+                               const char* a_lbl, tt_tensor B, const char* b_lbl);
 tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* a_lbl, tt_tensor B,
                              const char* b_lbl, double* result);
 

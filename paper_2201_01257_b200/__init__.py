@@ -101,6 +101,7 @@ _SIGS = {
     "tt_contract": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p],
     "tt_contract_cholesky": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
                              _i64],
+    "tt_contract_prefetch": [_vp, _vp, ctypes.c_char_p, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p],
     "tt_contract3": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
                      ctypes.c_char_p, _vp, _i64, _vp],
     "tt_triples_energy": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _P(_dbl), _vp],
@@ -426,6 +427,13 @@ def contract_cholesky(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: f
         ws_elems = int(workspace.numel())
     _check(_lib.tt_contract_cholesky(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), X.h, _b(v_lbl), B.h,
                                      _b(b_lbl), _vp(_devptr(workspace)), int(ws_elems)))
+
+
+def contract_prefetch(ctx: Context, C: Tensor, c_lbl: str, beta: float, A: Tensor, a_lbl: str, B: Tensor,
+                      b_lbl: str):
+    """Issue the input gather of a later ``contract`` with the same arguments on the comm stream
+    (tt_contract_prefetch): it overlaps the kernels issued in between."""
+    _check(_lib.tt_contract_prefetch(ctx.h, C.h, _b(c_lbl), beta, A.h, _b(a_lbl), B.h, _b(b_lbl)))
 
 
 def contract3(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str, B: Tensor,

@@ -433,8 +433,14 @@ tt_status build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops
 // One group with thousands of point-to-point calls to several peers stalled NCCL at 4 ranks.
 constexpr size_t kGatherGroupOps = 128;
 
-tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops) {
+tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops,
+                     cudaStream_t stream = nullptr) {
   if (ctx->nranks <= 1 || (gp.recv.empty() && gp.send.empty())) return TT_OK;
+  if (!stream) {
+    stream = ctx->stream;
+    // never two streams on one communicator at once: wait for prefetched gathers still in flight
+    if (ctx->comm_pending) TT_CUDA(cudaStreamWaitEvent(stream, ctx->comm_done, 0));
+  }
   const char* err = nullptr;
   const NcclApi* api = nccl_api(&err);
   if (!api) return fail(TT_E_NCCL, "%s", err);
@@ -456,11 +462,11 @@ tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tens
       TT_TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
       for (size_t i = sb + g * kGatherGroupOps; i < std::min(se, sb + (g + 1) * kGatherGroupOps); ++i) {
         const Run& r = gp.send[i];
-        TT_TRY(nccl_check(api->Send(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclSend"));
+        TT_TRY(nccl_check(api->Send(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, stream), "ncclSend"));
       }
       for (size_t i = rb + g * kGatherGroupOps; i < std::min(re, rb + (g + 1) * kGatherGroupOps); ++i) {
         const Run& r = gp.recv[i];
-        TT_TRY(nccl_check(api->Recv(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, ctx->stream), "ncclRecv"));
+        TT_TRY(nccl_check(api->Recv(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, stream), "ncclRecv"));
       }
       TT_TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
     }
@@ -548,6 +554,8 @@ struct ContractPlan {
   int64_t* d_bblk = nullptr;
   int64_t* d_ptr = nullptr;
   bool device_built = false;
+  cudaEvent_t pf_event = nullptr;      // tt_contract_prefetch: this plan's gather issued on the comm stream
+  bool prefetched = false;
   double flops = 0, bytes = 0;
   int64_t tasks = 0;
 };
@@ -643,6 +651,12 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
   for (void* p : ctx->dev_allocs) cudaFree(p);
   for (auto& r : ctx->prof) { ctx->event_pool.push_back(r.e0); ctx->event_pool.push_back(r.e1); }
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->comm_stream) {
+    cudaStreamSynchronize(ctx->comm_stream);
+    cudaStreamDestroy(ctx->comm_stream);
+    cudaEventDestroy(ctx->comm_fork);
+    cudaEventDestroy(ctx->comm_done);
+  }
   if (ctx->comm) {
     const NcclApi* api = nccl_api(nullptr);
     if (api) api->CommDestroy(ctx->comm);
@@ -2022,7 +2036,12 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   TT_TRY(check_bound(B, "B"));
   DeviceGuard dg(ctx->device);
   reset_stats(ctx);
-  TT_TRY(run_gather(ctx, pl->gp, A == B ? std::vector<tt_tensor>{A} : std::vector<tt_tensor>{A, B}));
+  if (pl->prefetched) {   // the gather ran on the comm stream (tt_contract_prefetch)
+    TT_CUDA(cudaStreamWaitEvent(ctx->stream, pl->pf_event, 0));
+    pl->prefetched = false;
+  } else {
+    TT_TRY(run_gather(ctx, pl->gp, A == B ? std::vector<tt_tensor>{A} : std::vector<tt_tensor>{A, B}));
+  }
   TT_TRY(launch_plan(ctx, *pl, C, cl, beta, alpha, A, al, B, bl));
   ctx->last.c_blocks = (int64_t)pl->my.size();
   ctx->last.tasks = pl->tasks;
@@ -2033,6 +2052,35 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   ctx->last.plan_cached = was_cached ? 1 : 0;
   ctx->last.kernel_variant = pl->variant;
   ctx->last.producer = pl->tma ? 1 : 0;
+  return TT_OK;
+}
+
+tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* cl, double beta, tt_tensor A, const char* al,
+                               tt_tensor B, const char* bl) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  std::shared_ptr<ContractPlan> pl;
+  TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, pl, nullptr));
+  TT_TRY(need_device(ctx));
+  if (ctx->prepare_only || ctx->nranks <= 1) return TT_OK;
+  TT_TRY(check_bound(A, "A"));
+  TT_TRY(check_bound(B, "B"));
+  if (pl->prefetched) return fail(TT_E_STATE, "this contraction's gather is already prefetched");
+  DeviceGuard dg(ctx->device);
+  if (!ctx->comm_stream) {
+    TT_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    TT_CUDA(cudaEventCreateWithFlags(&ctx->comm_fork, cudaEventDisableTiming));
+    TT_CUDA(cudaEventCreateWithFlags(&ctx->comm_done, cudaEventDisableTiming));
+  }
+  if (!pl->pf_event) TT_CUDA(cudaEventCreateWithFlags(&pl->pf_event, cudaEventDisableTiming));
+  // the gather overwrites non-owned input ranges: it starts after everything issued on the context
+  // stream so far (no write-after-read hazard with earlier kernels), and the consuming tt_contract waits
+  TT_CUDA(cudaEventRecord(ctx->comm_fork, ctx->stream));
+  TT_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->comm_fork, 0));
+  TT_TRY(run_gather(ctx, pl->gp, A == B ? std::vector<tt_tensor>{A} : std::vector<tt_tensor>{A, B}, ctx->comm_stream));
+  TT_CUDA(cudaEventRecord(pl->pf_event, ctx->comm_stream));
+  TT_CUDA(cudaEventRecord(ctx->comm_done, ctx->comm_stream));
+  ctx->comm_pending = true;
+  pl->prefetched = true;
   return TT_OK;
 }
 

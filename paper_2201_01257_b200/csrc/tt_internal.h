@@ -183,4 +183,8 @@ struct tt_ctx_s {
   // results to a device slot instead of the host (inside a captured graph)
   bool prepare_only = false;
   double* scalar_dev_out = nullptr;
+  // prefetched input gathers (tt_contract_prefetch): NCCL on a side stream, overlapping earlier kernels
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t comm_fork = nullptr, comm_done = nullptr;
+  bool comm_pending = false;       // comm_done marks the last gather issued on comm_stream
 };

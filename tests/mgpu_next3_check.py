@@ -98,6 +98,23 @@ def main():
     ok &= err <= 1e-11
     if rank == 0:
         print(f"view contraction: err {err:.2e}", flush=True)
+    # --- tt_contract_prefetch: the gather on the comm stream gives bitwise the same result
+    res = []
+    for pf in (False, True):
+        cb = torch.from_numpy(O.pack(oC, DC)).cuda()
+        C.bind(cb)
+        keep.append(cb)
+        if pf:
+            tt.contract_prefetch(ctx, C, "ia", 1.0, A, "ix", B, "xa")
+            tt.contract_prefetch(ctx, C, "ia", 0.0, A, "ix", B, "xa")   # a second plan (beta = 0) queued too
+        tt.contract(ctx, C, "ia", 1.0, 0.5, A, "ix", B, "xa")
+        tt.contract(ctx, C, "ia", 0.0, 1.5, A, "ix", B, "xa")
+        res.append(C.download())
+        ctx.sync()
+    same = bool(np.array_equal(res[0], res[1]))
+    ok &= same
+    if rank == 0:
+        print(f"prefetched gathers bitwise equal: {same}", flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if rank == 0:
