@@ -330,6 +330,10 @@ def main():
                       "kernel_ms": t_avg, "tflops": st["flops"] / (t_avg * 1e-3) / 1e12 if t_avg > 0 else None,
                       "variant": st["kernel_variant"]})
     ctx.set_profiling(False)
+    if world > 1:   # per-rank term times (load balance evidence) on stderr
+        print(json.dumps({"rank": rank, "ms_per_step": ms / args.steps,
+                          "term_ms": [round(t["kernel_ms"], 2) for t in terms],
+                          "term_gflop": [round(t["flops"] / 1e9, 1) for t in terms]}), file=sys.stderr, flush=True)
     tot = torch.tensor([ms, flops_rank], dtype=torch.float64, device="cuda")
     if world > 1:
         mx = tot.clone()
