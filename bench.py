@@ -150,17 +150,11 @@ def build_problem(tt, ctx, c):
 
 def distribute(tt, ctx, T, ops, np):
     """Owner-computes placement for N > 1: R by (a,b) rows with the balanced row-splitting partition
-    (tt_partition_split_cost on the summed FLOPs of all terms, group dims a,b: a row straddling a rank
-    boundary is cut along a), V with the
+    (tt_partition_split, group dims a,b: a row straddling a rank boundary is cut along a), V with the
     R rows (or row parts) that read it; other inputs keep the default round-robin owners (P210)."""
     R = T["R"]
-    # one partition for all terms writing R: the water-filling split on the summed task-list FLOPs of
-    # every term per R block (the ring and hole-hole costs are not proportional to the ladder's)
-    cost = None
-    for (c, cl, a, al, b, bl) in ops:
-        tl = tt.task_list(ctx, R, cl, T[a], al, T[b], bl)["cost"]
-        cost = tl if cost is None else cost + tl
-    tt.partition_split_cost(ctx, R, cost, group_dims=(0, 1))
+    c, cl, a, al, b, bl = ops[0]
+    tt.partition_split(ctx, R, cl, T[a], al, T[b], bl, group_dims=(0, 1))
     if "V" in T:
         V = T["V"]
         whole, split = {}, {}
