@@ -285,7 +285,8 @@ def main():
     torch.cuda.synchronize()
 
     def step():
-        if world > 1:   # every term's input gather on the comm stream first: they overlap the kernels
+        if world > 1 and os.environ.get("TT_BENCH_PREFETCH", "1") != "0":
+            # every term's input gather on the comm stream first: they overlap the other terms' kernels
             for (c, cl, a, al, b, bl) in ops:
                 tt.contract_prefetch(ctx, T[c], cl, 1.0, T[a], al, T[b], bl)
         for (c, cl, a, al, b, bl) in ops:
