@@ -335,6 +335,7 @@ struct GatherPlan {
   std::vector<int64_t> recv_list, send_list;   // (op, block, peer, e0, e1) rows
   std::vector<Run> recv, send;
   int64_t recv_bytes = 0;
+  bool one_group = false;   // few pieces over ALL ranks (the same decision on every rank): one NCCL group
 };
 
 struct Need {
@@ -373,15 +374,19 @@ void pieces(tt_tensor T, int64_t b, int64_t e0, int64_t e1, F&& emit) {
   }
 }
 
+constexpr size_t kGatherGroupOps = 128;   // NCCL point-to-point calls per group and direction
+
 tt_status build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops, GatherPlan& gp) {
   const int me = ctx->rank, P = ctx->nranks;
   bool into_compact = false;
+  int64_t all_pieces = 0;
   for (int dst = 0; dst < P; ++dst) {
     normalize(need[dst]);
     for (const Need& n : need[dst]) {
       tt_tensor T = ops[n.op];
       pieces(T, n.blk, n.e0, n.e1, [&](int32_t src, int64_t a, int64_t z) {
         if (src == TT_REPLICATED || src == dst) return;
+        ++all_pieces;
         if (T->compact) into_compact = true;
         if (dst == me) gp.recv_list.insert(gp.recv_list.end(), {n.op, n.blk, src, a, z});
         if (src == me) gp.send_list.insert(gp.send_list.end(), {n.op, n.blk, dst, a, z});
@@ -424,14 +429,15 @@ tt_status build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops
   runs(gp.recv_list, gp.recv);
   runs(gp.send_list, gp.send);
   for (const Run& r : gp.recv) gp.recv_bytes += r.len * 8;
+  gp.one_group = all_pieces <= (int64_t)kGatherGroupOps * P;
   return TT_OK;
 }
 
-// Exchange schedule: P-1 rounds; in round k every rank sends to rank+k and receives from rank-k,
+// Exchange schedule: with at most kGatherGroupOps runs per direction, one group over all peers; else
+// P-1 rounds; in round k every rank sends to rank+k and receives from rank-k,
 // and each round is cut into NCCL groups of at most kGatherGroupOps runs per direction (the i-th
 // group of a round holds the i-th slices of both lists, which the partner slices identically).
 // One group with thousands of point-to-point calls to several peers stalled NCCL at 4 ranks.
-constexpr size_t kGatherGroupOps = 128;
 
 tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops,
                      cudaStream_t stream = nullptr) {
@@ -445,6 +451,16 @@ tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tens
   const NcclApi* api = nccl_api(&err);
   if (!api) return fail(TT_E_NCCL, "%s", err);
   const int P = ctx->nranks, me = ctx->rank;
+  // few pieces over all ranks: one NCCL group with every peer (all transfers in flight at once)
+  if (gp.one_group) {
+    TT_TRY(nccl_check(api->GroupStart(), "ncclGroupStart"));
+    for (const Run& r : gp.send)
+      TT_TRY(nccl_check(api->Send(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, stream), "ncclSend"));
+    for (const Run& r : gp.recv)
+      TT_TRY(nccl_check(api->Recv(ops[r.op]->data + r.off, (size_t)r.len, kNcclFloat64, r.peer, ctx->comm, stream), "ncclRecv"));
+    TT_TRY(nccl_check(api->GroupEnd(), "ncclGroupEnd"));
+    return TT_OK;
+  }
   auto peer_range = [](const std::vector<Run>& v, int peer, size_t& b, size_t& e) {   // runs sorted by peer
     b = 0;
     while (b < v.size() && v[b].peer < peer) ++b;
