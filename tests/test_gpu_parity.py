@@ -635,3 +635,21 @@ def test_tma_producer(env, variant, tv):
     os.environ.pop("TT_TMA", None)
     os.environ.pop("TT_FORCE_VARIANT", None)
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["spin_small_ladder", "ragged_dense_ring", "multi_tile_spin_ladder"])
+def test_variants_bitwise_equal(env, name):
+    """The warp-specialised tile variants (3, 4, 5; TMA or cp.async producers) accumulate every output
+    element over the same k sequence, so they give the same bits -- the measured autotuning between them
+    (tt_contract, TT_AUTOTUNE) therefore never changes a result (R12)."""
+    tt, torch = env
+    pb, k = PROBLEMS[name]
+    outs = []
+    for v in (3, 4, 5):
+        ctx = new_ctx(tt, torch, variant=v)
+        got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[k], seed=3)
+        assert normwise(got, ref) <= TOL
+        outs.append(got)
+    os.environ.pop("TT_FORCE_VARIANT", None)
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
