@@ -67,7 +67,7 @@ def main():
                     help="0: half of Bm + one W row + 1 GB, capped by the free memory (else two-pass)")
     ap.add_argument("--weak", action="store_true")
     ap.add_argument("--steps", type=int, default=1)
-    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=2)   # >= 2: tt_contract autotunes on the first two calls
     ap.add_argument("--samples-out", default="")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
