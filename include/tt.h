@@ -230,6 +230,10 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
  *              index permutation folded into the operand staging.  With nranks > 1
  *              the rank computes the C blocks it owns and first receives, over NCCL, exactly the A/B
  *              blocks its tasks read but does not own (P212 "access to the remote portions").
+ *              Kernel tile variant: a cost model, refined by measured autotuning for plans of
+ *              >= 5e10 FLOPs (the first two calls time the model's choice and its runner-up; later
+ *              calls use the faster; the variants give identical bits; TT_AUTOTUNE=0 disables it,
+ *              TT_FORCE_VARIANT=v forces one).
  * tt_contract_scalar  *result = alpha * sum_x A(x)*B(x) over all labels (order-0 result such as the
  *              CC energy, P534-536), summed over ranks with an NCCL all-reduce; *result is a HOST
  *              pointer and the call synchronises the stream.  With nranks > 1 each rank sums the A
