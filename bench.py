@@ -443,6 +443,44 @@ def main():
                 fin = torch.cuda.Event()
                 fin.record(copy_stream)
                 stream.wait_event(fin)
+        elif world > 1:
+            # N > 1: every rank moves only what it holds -- its own blocks / row parts (owner-computes;
+            # the gathers inside the step fetch the rest over NVLink) -- and reads back its own R parts
+            def held(Tn):
+                rs = []
+                parts = {}
+                for (blk, lo, hi, ow) in Tn.parts:
+                    parts.setdefault(blk, []).append((lo, hi, ow))
+                for blk in range(Tn.nblocks):
+                    if not Tn.nz[blk]:
+                        continue
+                    ext = [int(d.offsets[t + 1] - d.offsets[t]) for d, t in zip(Tn.dims, np.unravel_index(blk, Tn.grid))]
+                    vol, o = int(np.prod(ext)), int(Tn.blk_off[blk])
+                    if Tn.owner[blk] == rank or Tn.owner[blk] == tt.TT_REPLICATED:
+                        rs.append((o, o + vol))
+                    elif blk in parts:
+                        inner = vol // ext[0]
+                        rs += [(o + lo * inner, o + hi * inner) for (lo, hi, ow) in parts[blk] if ow == rank]
+                rs.sort()
+                merged = []
+                for a0, a1 in rs:   # merge runs that touch (or are separated by one alignment pad)
+                    if merged and a0 - merged[-1][1] <= 1:
+                        merged[-1] = (merged[-1][0], max(merged[-1][1], a1))
+                    else:
+                        merged.append((a0, a1))
+                return merged
+
+            own = {n: held(T[n]) for n in T}
+            h2d = 8 * sum(b - a for n in T for (a, b) in own[n])
+            d2h = 8 * sum(b - a for (a, b) in own["R"])
+
+            def e2e_step():
+                for n in T:
+                    for (a0, a1) in own[n]:
+                        bufs[n][a0:a1].copy_(hosts[n][a0:a1], non_blocking=True)
+                step()
+                for (a0, a1) in own["R"]:
+                    hosts["R"][a0:a1].copy_(bufs["R"][a0:a1], non_blocking=True)
         else:
             e2e_step = e2e_step_plain
 
@@ -471,12 +509,17 @@ def main():
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e_ms = float(ems[0]) / args.e2e_steps
-        e2e = {"value": flops_all / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d * world,
-               "d2h_bytes_per_step": d2h * world, "ms_per_step": e_ms, "steps": args.e2e_steps,
+        io = torch.tensor([h2d, d2h], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(io)
+        e2e = {"value": flops_all / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(io[0]),
+               "d2h_bytes_per_step": int(io[1]), "ms_per_step": e_ms, "steps": args.e2e_steps,
                "pipelined": bool(chunkable),
                "how": ("per dim-0 tile of R: H2D of the operand rows on a copy stream overlapping the previous "
                        "chunk's contraction through views, D2H of finished R rows overlapping the next")
-               if chunkable else "upload all, contract, download R"}
+               if chunkable else ("each rank: H2D of the blocks / row parts it holds, the step (gathers of "
+                                  "the rest over NVLink), D2H of its R parts" if world > 1 else
+                                  "upload all, contract, download R")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
