@@ -463,22 +463,13 @@ __global__ void __launch_bounds__(THREADS, 2)
     for (int f = 0; f < NFR; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
   int slot = 0, t = 0;
   unsigned phase = 0;
-  bool acc_neg = false;
 #pragma unroll 1
   for (int g = 0; g < 3; ++g) {
 #pragma unroll 1
     for (int sg = 0; sg < 6; ++sg) {
       const int32_t n = segn[g * 6 + sg];
       const bool neg = sg < 3 ? sg == 1 : sg != 4;   // m sums (+,-,+), e sums (-,+,-)
-      // the accumulators hold (neg ? -1 : +1) x the GEMM: flip them when the segment sign changes
-      // (exact), so the fragments go from shared memory to the DMMA unmodified
-      if (n > 0 && neg != acc_neg) {
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int f = 0; f < NFR; ++f) { acc[a][f][0] = -acc[a][f][0]; acc[a][f][1] = -acc[a][f][1]; }
-        acc_neg = neg;
-      }
+      const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
 #pragma unroll 1
       for (int jj = 0; jj < n; ++jj, ++t) {
         tbar_wait(&full[slot], phase);
@@ -487,8 +478,8 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
         for (int kk = 0; kk < KC / 4; ++kk) {
           const int kl = kk * 4 + (lane & 3);
-          const double a0 = P[kl * TPW + (lane >> 2)];
-          const double a1 = P[kl * TPW + 8 + (lane >> 2)];
+          const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
+          const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
 #pragma unroll
           for (int f = 0; f < NFR; ++f) {
             const int col = warp * CW + f * 8 + (lane >> 2);
@@ -513,13 +504,12 @@ __global__ void __launch_bounds__(THREADS, 2)
           const int row = rf * 8 + (lane >> 2);
           const int col = warp * CW + f * 8 + 2 * (lane & 3) + h;
           const int pp = col / BX, q = col % BX;
-          const double v = acc_neg ? -acc[rf][f][h] : acc[rf][f][h];
+          const double v = acc[rf][f][h];
           if (g == 0) cube[cidx(row, pp, q)] = v;
           else if (g == 1) cube[cidx(pp, row, q)] -= v;
           else cube[cidx(pp, q, row)] += v;
           acc[rf][f][h] = 0.0;
         }
-    acc_neg = false;
     __syncthreads();
   }
   // Eq. cc14 over the cube (as the cp.async kernel)
