@@ -17,8 +17,15 @@ time of the K timed steps (CUDA events on the context stream).  The operands (V 
 N > 1 (torchrun): strong scaling of the same problem.  Owner-computes: the R (a,b) rows are laid
 along a cost axis and cut into equal shares (tt_partition_split: a row straddling a rank boundary is
 split along a), the V blocks live with the R rows (or row parts) that read them, every other input is
-distributed round robin (P210 scheme 3) and gathered inside tt_contract with grouped NCCL send/recv
-every step.
+distributed round robin (P210 scheme 3) and gathered with grouped NCCL send/recv every step -- all
+terms' gathers are issued first on the communication stream (tt_contract_prefetch) so they overlap
+the other terms' kernels.  The kernel tile variant is autotuned by tt_contract on its first two calls
+(warm-up), with identical bits.
+
+e2e: the same step from pinned host memory through the C ABI.  N = 1: pipelined through sliced views
+(per dim-0 tile of R: H2D of the operand rows on a copy stream overlaps the previous chunk's
+contraction, finished R rows go back while the next computes; checked bit for bit against the plain
+step).  N > 1: every rank moves only the blocks / row parts it holds and reads back its R parts.
 
 --impl reference: the CPU oracle (oracle/) on the host cores, on a bounded sample of the same
 workload (rank 0 only), same metric and unit.
