@@ -1175,10 +1175,10 @@ struct ElemPlan {
   TileItem* d_tiles = nullptr;
   double* d_partials = nullptr;
   GatherPlan gp;
-  int mode = kElemGeneric;
   double bytes = 0;
   int64_t blocks = 0;
-  int64_t nwork() const { return mode == kElemTranspose ? (int64_t)tiles.size() : (int64_t)segs.size(); }
+  int64_t nseg() const { return (int64_t)segs.size(); }
+  int64_t ntiles() const { return (int64_t)tiles.size(); }
 };
 
 // Fuse adjacent x dims that are adjacent (same order) in y; fill the group extents / y strides of
@@ -1205,25 +1205,62 @@ int fuse_elem(ElemDesc& d, int order, const int32_t* ext, const int* ypos, const
     d.y_str[g] = (int32_t)ystr[last_y[g]];
     if (d.y_str[g] == 1) d.gy = g;
   }
-  if (n == 1 && d.y_str[0] == 1) return kElemContig;
-  if (d.y_str[n - 1] == 1 || d.gy < 0) return kElemGeneric;
-  return kElemTranspose;
+  if (n == 1 && d.y_str[0] == 1) d.mode = kElemContig;
+  else if (d.y_str[n - 1] == 1 || d.gy < 0) d.mode = kElemGeneric;
+  else d.mode = kElemTranspose;
+  return d.mode;
 }
 
-void add_tiles(ElemPlan& ep, int32_t desc) {
-  const ElemDesc& d = ep.descs[desc];
+// transpose-mode work of a whole block: 32x32 tiles over (gx = innermost X group, gy = the group with
+// Y stride 1), one per remaining-group index; bases precomputed (TileItem)
+void add_tiles(ElemPlan& ep, const ElemDesc& d) {
   const int gx = d.n - 1, gy = d.gy;
+  int64_t xs[TT_MAX_ORDER], acc = 1;
+  for (int g = d.n - 1; g >= 0; --g) { xs[g] = acc; acc *= d.div[g].d; }
   int64_t batch = 1;
   for (int g = 0; g < d.n; ++g)
     if (g != gx && g != gy) batch *= d.div[g].d;
-  const int ntx = (int)((d.div[gx].d + 31) / 32), nty = (int)((d.div[gy].d + 31) / 32);
-  for (int64_t b = 0; b < batch; ++b)
-    for (int ty = 0; ty < nty; ++ty)
-      for (int tx = 0; tx < ntx; ++tx) ep.tiles.push_back({desc, tx, ty, (int32_t)b});
+  const int ex = (int)d.div[gx].d, ey = (int)d.div[gy].d;
+  for (int64_t b = 0; b < batch; ++b) {
+    int64_t r = b, xb = 0, yb = 0;
+    for (int g = d.n - 1; g >= 0; --g) {
+      if (g == gx || g == gy) continue;
+      const int64_t c = r % d.div[g].d;
+      r /= d.div[g].d;
+      xb += c * xs[g];
+      yb += c * d.y_str[g];
+    }
+    for (int ty = 0; ty < ey; ty += 32)
+      for (int tx = 0; tx < ex; tx += 32) {
+        TileItem t;
+        t.x_base = d.x_off + xb + (int64_t)ty * xs[gy] + tx;
+        t.y_base = d.y_off < 0 ? -1 : d.y_off + yb + (int64_t)tx * d.y_str[gx] + ty;
+        t.nx = std::min(32, ex - tx);
+        t.ny = std::min(32, ey - ty);
+        t.x_ld = (int32_t)xs[gy];
+        t.y_ld = d.y_str[gx];
+        ep.tiles.push_back(t);
+      }
+  }
 }
 
 void add_segments(ElemPlan& ep, int32_t desc, int64_t e_begin, int64_t e_end) {
   for (int64_t e = e_begin; e < e_end; e += kSegElems) ep.segs.push_back({desc, 0, e, std::min(e_end, e + kSegElems)});
+}
+
+// Appends one block descriptor (mode set by fuse_elem) and its work: 32x32 tiles over the whole block
+// for a transpose descriptor (only when the block is processed whole), else segments over `ranges`.
+// Modes are per descriptor: blocks of one plan may differ (e.g. a remainder tile of extent 1 makes
+// a transposing block generic), and every block's work is kept.
+void emit_elem(ElemPlan& ep, ElemDesc& d, bool whole, const std::vector<std::pair<int64_t, int64_t>>& ranges) {
+  if (d.mode == kElemTranspose && !whole) d.mode = kElemGeneric;   // tiles need whole blocks
+  ep.descs.push_back(d);
+  const int32_t di = (int32_t)ep.descs.size() - 1;
+  if (d.mode == kElemTranspose) {
+    add_tiles(ep, d);
+    return;
+  }
+  for (auto& h : ranges) add_segments(ep, di, h.first, h.second);
 }
 
 // whether the dim-0 label of X is also the dim-0 label of Y: then a row range of an X part maps to
@@ -1251,7 +1288,10 @@ tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
     TT_TRY(dev_alloc(ctx, &ep.d_tiles, ep.tiles.size()));
     TT_CUDA(cudaMemcpy(ep.d_tiles, ep.tiles.data(), ep.tiles.size() * sizeof(TileItem), cudaMemcpyHostToDevice));
   }
-  if (partials) TT_TRY(dev_alloc(ctx, &ep.d_partials, std::max<size_t>(ep.segs.size(), ep.tiles.size())));
+  if (partials) {
+    const int64_t n = ep.nseg() + ep.ntiles();
+    TT_TRY(dev_alloc(ctx, &ep.d_partials, (size_t)(n + scalar_scratch_elems(n))));
+  }
   return TT_OK;
 }
 
@@ -1414,18 +1454,12 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
       for (int q = A->order - 1; q >= 0; --q) { sa[q] = acc; acc *= A->dims[q]->size(ac[q]); }
       int32_t ext[TT_MAX_ORDER];
       for (int q = 0; q < C->order; ++q) ext[q] = (int32_t)C->dims[q]->size(cc[q]);
-      ep->mode = fuse_elem(d, C->order, ext, perm.data(), sa);
-      if (ep->mode == kElemTranspose && C->any_split) ep->mode = kElemGeneric;   // tiles need whole blocks
-      ep->descs.push_back(d);
-      const int32_t di = (int32_t)ep->descs.size() - 1;
-      for (auto& h : mine) {
-        if (ep->mode == kElemTranspose) add_tiles(*ep, di);
-        else add_segments(*ep, di, h.first, h.second);
-        ep->bytes += 8.0 * (h.second - h.first) * ((beta != 0.0) + 1 + (A->nz[ab] ? 1 : 0));
-      }
+      fuse_elem(d, C->order, ext, perm.data(), sa);
+      const bool whole = mine.size() == 1 && mine[0].first == 0 && mine[0].second == C->block_volume(b);
+      emit_elem(*ep, d, whole, mine);
+      for (auto& h : mine) ep->bytes += 8.0 * (h.second - h.first) * ((beta != 0.0) + 1 + (A->nz[ab] ? 1 : 0));
       ep->blocks++;
     }
-    if (ep->mode != kElemTranspose) ep->tiles.clear();
     TT_TRY(build_gather(ctx, need, {A}, ep->gp));
     TT_TRY(upload_elem(ctx, *ep, false));
     ctx->plans[key] = ep;
@@ -1439,13 +1473,12 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
   p.descs = ep->d_descs;
   p.segs = ep->d_segs;
   p.tiles = ep->d_tiles;
-  p.mode = ep->mode;
   p.order = C->order;
   p.alpha = alpha;
   p.beta = beta;
   {
     Launch L(ctx, "tt_add");
-    TT_CUDA(launch_add(p, ep->nwork(), ctx->stream));
+    TT_CUDA(launch_add(p, ep->nseg(), ep->ntiles(), ctx->stream));
   }
   ctx->last.c_blocks = ep->blocks;
   ctx->last.bytes = ep->bytes;
@@ -1508,17 +1541,12 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
       for (int q = B->order - 1; q >= 0; --q) { sb[q] = acc; acc *= B->dims[q]->size(bc[q]); }
       int32_t ext[TT_MAX_ORDER];
       for (int q = 0; q < A->order; ++q) ext[q] = (int32_t)A->dims[q]->size(ac[q]);
-      ep->mode = fuse_elem(d, A->order, ext, perm.data(), sb);
-      if (ep->mode == kElemTranspose && A->any_split) ep->mode = kElemGeneric;
-      ep->descs.push_back(d);
-      for (auto& h : mine) {
-        if (ep->mode == kElemTranspose) add_tiles(*ep, (int32_t)ep->descs.size() - 1);
-        else add_segments(*ep, (int32_t)ep->descs.size() - 1, h.first, h.second);
-        ep->bytes += 16.0 * (h.second - h.first);
-      }
+      fuse_elem(d, A->order, ext, perm.data(), sb);
+      const bool whole = mine.size() == 1 && mine[0].first == 0 && mine[0].second == A->block_volume(blk);
+      emit_elem(*ep, d, whole, mine);
+      for (auto& h : mine) ep->bytes += 16.0 * (h.second - h.first);
       ep->blocks++;
     }
-    if (ep->mode != kElemTranspose) ep->tiles.clear();
     TT_TRY(build_gather(ctx, need, {A, B}, ep->gp));
     TT_TRY(upload_elem(ctx, *ep, true));
     ctx->plans[key] = ep;
@@ -1532,17 +1560,17 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
   p.descs = ep->d_descs;
   p.segs = ep->d_segs;
   p.order = A->order;
-  p.mode = ep->mode;
   p.tiles = ep->d_tiles;
   p.partials = ep->d_partials;
   double* dst = ctx->scalar_dev_out ? ctx->scalar_dev_out : ctx->d_scalar;
+  const int64_t npart = ep->nseg() + ep->ntiles();
   {
     Launch L(ctx, "tt_scalar_partials");
-    TT_CUDA(launch_scalar_partials(p, ep->nwork(), ctx->stream));
+    TT_CUDA(launch_scalar_partials(p, ep->nseg(), ep->ntiles(), ctx->stream));
   }
   {
     Launch L(ctx, "tt_scalar_final");
-    TT_CUDA(launch_scalar_final(ep->d_partials, scalar_num_partials(ep->mode, ep->nwork()), alpha, dst, ctx->stream));
+    TT_CUDA(launch_scalar_final(ep->d_partials, npart, alpha, dst, ep->d_partials + npart, ctx->stream));
   }
   if (ctx->nranks > 1) {
     const char* err = nullptr;
@@ -2451,14 +2479,11 @@ tt_status local_add_plan(tt_ctx ctx, tt_tensor Xt, tt_tensor Yt, const std::vect
     for (int q = Yt->order - 1; q >= 0; --q) { sa[q] = acc; acc *= Yt->dims[q]->size(ac[q]); }
     int32_t ext[TT_MAX_ORDER];
     for (int q = 0; q < Xt->order; ++q) ext[q] = (int32_t)Xt->dims[q]->size(cc[q]);
-    ep->mode = fuse_elem(d, Xt->order, ext, perm.data(), sa);
-    ep->descs.push_back(d);
-    if (ep->mode == kElemTranspose) add_tiles(*ep, (int32_t)ep->descs.size() - 1);
-    else add_segments(*ep, (int32_t)ep->descs.size() - 1, 0, Xt->block_volume(b));
+    fuse_elem(d, Xt->order, ext, perm.data(), sa);
+    emit_elem(*ep, d, true, {{0, Xt->block_volume(b)}});
     ep->bytes += 8.0 * Xt->block_volume(b) * ((beta != 0.0) + 2);
     ep->blocks++;
   }
-  if (ep->mode != kElemTranspose) ep->tiles.clear();
   TT_TRY(upload_elem(ctx, *ep, false));
   out = ep;
   return TT_OK;
@@ -2471,12 +2496,11 @@ tt_status run_local_add(tt_ctx ctx, const ElemPlan& ep, tt_tensor Xt, tt_tensor 
   p.descs = ep.d_descs;
   p.segs = ep.d_segs;
   p.tiles = ep.d_tiles;
-  p.mode = ep.mode;
   p.order = Xt->order;
   p.alpha = alpha;
   p.beta = beta;
   Launch L(ctx, "tt_add[cholesky Bh]");
-  TT_CUDA(launch_add(p, ep.nwork(), ctx->stream));
+  TT_CUDA(launch_add(p, ep.nseg(), ep.ntiles(), ctx->stream));
   return TT_OK;
 }
 
@@ -3339,7 +3363,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   }
   {
     Launch L(ctx, "tt_scalar_final");
-    TT_CUDA(launch_scalar_final(partials + tp->unit0, tp->nunits, 1.0, ctx->d_scalar, ctx->stream));
+    TT_CUDA(launch_scalar_final(partials + tp->unit0, tp->nunits, 1.0, ctx->d_scalar, nullptr, ctx->stream));
   }
   if (ctx->nranks > 1) {
     const char* err = nullptr;

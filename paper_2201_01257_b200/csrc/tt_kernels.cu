@@ -474,158 +474,138 @@ __global__ void set_kernel(const ElemParams p) {
   if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) x[sg.e1 - 1] = p.alpha;
 }
 
-template <int MODE>
-__global__ void add_kernel(const ElemParams p) {
+__device__ __forceinline__ double axpby(double alpha, double y, double beta, double x) {
+  return (beta == 0.0) ? alpha * y : beta * x + alpha * y;
+}
+
+// Deterministic warp-then-CTA sum of one value per thread (fixed shuffle tree, warps in order).
+__device__ __forceinline__ double cta_sum(double s, double* warp_sums) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x, nw = (blockDim.x * blockDim.y) / 32;
+  if ((tid & 31) == 0) warp_sums[tid >> 5] = s;
+  __syncthreads();
+  double t = 0.0;
+  if (tid == 0)
+    for (int w = 0; w < nw; ++w) t += warp_sums[w];
+  return t;
+}
+
+constexpr int kElemUnroll = 4;   // elements per thread in flight (generic decode path)
+
+// Segment work (descriptors in contiguous or generic mode; the mode is per descriptor, uniform per
+// CTA).  Every thread issues all its loads of a batch before any store (X and Y are distinct
+// buffers: __restrict__), so each thread keeps kElemUnroll loads of each operand in flight.
+__global__ void __launch_bounds__(kElemThreads) add_seg_kernel(const ElemParams p) {
   __shared__ ElemDesc d;
   const Segment sg = p.segs[blockIdx.x];
   load_desc(d, p.descs + sg.desc);
-  double* x = p.X + d.x_off;
-  const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
+  double* __restrict__ x = p.X + d.x_off;
+  const double* __restrict__ y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
   const double alpha = p.alpha, beta = p.beta;
-  if (MODE == kElemContig) {
+  if (d.mode == kElemContig) {
     const int64_t es = sg.e0 + (sg.e0 & 1);
     const int64_t n2 = (sg.e1 - es) / 2;
-    double2* x2 = reinterpret_cast<double2*>(x + es);
-    const double2* y2 = y ? reinterpret_cast<const double2*>(y + es) : nullptr;
-    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
-      double2 v = y2 ? y2[i] : make_double2(0.0, 0.0);
-      v.x *= alpha;
-      v.y *= alpha;
-      if (beta != 0.0) {
-        const double2 o = x2[i];
-        v.x += beta * o.x;
-        v.y += beta * o.y;
+    double2* __restrict__ x2 = reinterpret_cast<double2*>(x + es);
+    const double2* __restrict__ y2 = y ? reinterpret_cast<const double2*>(y + es) : nullptr;
+    for (int64_t i0 = threadIdx.x; i0 < n2; i0 += kElemThreads * 2) {
+      double2 v[2], o[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t i = i0 + u * kElemThreads;
+        v[u] = (y2 && i < n2) ? y2[i] : make_double2(0.0, 0.0);
+        o[u] = (beta != 0.0 && i < n2) ? x2[i] : make_double2(0.0, 0.0);
       }
-      x2[i] = v;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t i = i0 + u * kElemThreads;
+        if (i < n2) x2[i] = make_double2(axpby(alpha, v[u].x, beta, o[u].x), axpby(alpha, v[u].y, beta, o[u].y));
+      }
     }
     if (threadIdx.x == 0) {
       int64_t peel[2] = {es != sg.e0 ? sg.e0 : -1, es + 2 * n2 < sg.e1 ? sg.e1 - 1 : -1};
       for (int64_t e : peel) {
         if (e < 0) continue;
-        const double v = y ? alpha * y[e] : 0.0;
-        x[e] = (beta == 0.0) ? v : beta * x[e] + v;
+        x[e] = axpby(alpha, y ? y[e] : 0.0, beta, beta != 0.0 ? x[e] : 0.0);
       }
     }
   } else {
-    for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) {
-      const double v = y ? alpha * y[y_offset((uint32_t)e, d)] : 0.0;
-      x[e] = (beta == 0.0) ? v : beta * x[e] + v;
-    }
-  }
-}
-
-// Transpose mode: x innermost group gx = n-1 is strided in y, group gy has y stride 1.  Each CTA
-// moves one 32x32 tile: coalesced reads along gy, shared-memory transpose, coalesced x writes.
-__device__ __forceinline__ void tile_offsets(const ElemDesc& d, const TileItem& t, int64_t& xb, int64_t& yb,
-                                             int64_t& xs_gy) {
-  // x strides of the groups (row-major over group extents)
-  int64_t xs[TT_MAX_ORDER];
-  int64_t acc = 1;
-  for (int g = d.n - 1; g >= 0; --g) { xs[g] = acc; acc *= d.div[g].d; }
-  uint32_t b = (uint32_t)t.batch;
-  xb = 0;
-  yb = 0;
-  for (int g = d.n - 1; g >= 0; --g) {
-    if (g == d.n - 1 || g == d.gy) continue;
-    const uint32_t q = fdiv(b, d.div[g]);
-    const int64_t c = b - q * d.div[g].d;
-    b = q;
-    xb += c * xs[g];
-    yb += c * d.y_str[g];
-  }
-  xs_gy = xs[d.gy];
-}
-
-constexpr int kTilesPerCta = 8;
-
-__global__ void add_transpose_kernel(const ElemParams p, int64_t ntiles) {
-  __shared__ ElemDesc d;
-  __shared__ double tile[32][33];
-  int cur = -1;
-  for (int it = 0; it < kTilesPerCta; ++it) {
-    const int64_t ti = (int64_t)blockIdx.x * kTilesPerCta + it;
-    if (ti >= ntiles) break;
-    const TileItem t = p.tiles[ti];
-    if (t.desc != cur) {          // uniform across the CTA
-      __syncthreads();
-      load_desc(d, p.descs + t.desc);
-      cur = t.desc;
-    }
-    int64_t xb, yb, xs_gy;
-    tile_offsets(d, t, xb, yb, xs_gy);
-    const int gx = d.n - 1, gy = d.gy;
-    const int ex = d.div[gx].d, ey = d.div[gy].d;
-    const int x0 = t.tx * 32, y0 = t.ty * 32;
-    const double* y = (d.y_off >= 0) ? p.Y + d.y_off : nullptr;
-    // read: lanes along gy (y contiguous), rows along gx
+    for (int64_t e0 = sg.e0 + threadIdx.x; e0 < sg.e1; e0 += kElemThreads * kElemUnroll) {
+      double yv[kElemUnroll], xv[kElemUnroll];
 #pragma unroll
-    for (int r = threadIdx.y; r < 32; r += 8) {
-      const int ix = x0 + r, iy = y0 + threadIdx.x;
-      double v = 0.0;
-      if (y && ix < ex && iy < ey) v = y[yb + (int64_t)ix * d.y_str[gx] + iy];
-      tile[r][threadIdx.x] = v;
-    }
-    __syncthreads();
-    double* x = p.X + d.x_off;
-    // write: lanes along gx (x contiguous)
+      for (int u = 0; u < kElemUnroll; ++u) {
+        const int64_t e = e0 + u * kElemThreads;
+        yv[u] = (y && e < sg.e1) ? y[y_offset((uint32_t)e, d)] : 0.0;
+        xv[u] = (beta != 0.0 && e < sg.e1) ? x[e] : 0.0;
+      }
 #pragma unroll
-    for (int r = threadIdx.y; r < 32; r += 8) {
-      const int ix = x0 + threadIdx.x, iy = y0 + r;
-      if (ix < ex && iy < ey) {
-        double* o = x + xb + (int64_t)iy * xs_gy + ix;
-        const double v = p.alpha * tile[threadIdx.x][r];
-        *o = (p.beta == 0.0) ? v : p.beta * *o + v;
+      for (int u = 0; u < kElemUnroll; ++u) {
+        const int64_t e = e0 + u * kElemThreads;
+        if (e < sg.e1) x[e] = axpby(alpha, yv[u], beta, xv[u]);
       }
     }
-    __syncthreads();
   }
 }
 
-// Scalar in transpose mode: partial sum of one run of tiles (fixed order: tile by tile, then a
-// fixed tree over the CTA), transposing y through shared memory so both operands are read coalesced.
-__global__ void scalar_transpose_kernel(const ElemParams p, int64_t ntiles) {
-  __shared__ ElemDesc d;
+// Transpose work: one 32x32 tile per CTA (32 x 8 threads, 4 elements each).  Bases and strides come
+// precomputed in the TileItem (no descriptor decode).  All loads -- Y along its contiguous group into
+// registers, and (beta != 0) X along its contiguous group -- are issued before the barrier; Y goes
+// through a padded shared tile so both the reads and the writes are 256-B coalesced rows.
+__global__ void __launch_bounds__(256) add_tile_kernel(const ElemParams p) {
   __shared__ double tile[32][33];
-  __shared__ double red[256];
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  double s = 0.0;
-  int cur = -1;
-  for (int it = 0; it < kTilesPerCta; ++it) {
-    const int64_t ti = (int64_t)blockIdx.x * kTilesPerCta + it;
-    if (ti >= ntiles) break;
-    const TileItem t = p.tiles[ti];
-    if (t.desc != cur) {
-      __syncthreads();
-      load_desc(d, p.descs + t.desc);
-      cur = t.desc;
-    }
-    int64_t xb, yb, xs_gy;
-    tile_offsets(d, t, xb, yb, xs_gy);
-    const int gx = d.n - 1, gy = d.gy;
-    const int ex = d.div[gx].d, ey = d.div[gy].d;
-    const int x0 = t.tx * 32, y0 = t.ty * 32;
-    const double* y = p.Y + d.y_off;
+  const TileItem t = p.tiles[blockIdx.x];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const double* __restrict__ y = p.Y;
+  double* __restrict__ x = p.X;
+  const double alpha = p.alpha, beta = p.beta;
+  double yv[4], xv[4];
 #pragma unroll
-    for (int r = threadIdx.y; r < 32; r += 8) {
-      const int ix = x0 + r, iy = y0 + threadIdx.x;
-      tile[r][threadIdx.x] = (ix < ex && iy < ey) ? y[yb + (int64_t)ix * d.y_str[gx] + iy] : 0.0;
-    }
-    __syncthreads();
-    const double* x = p.X + d.x_off;
-#pragma unroll
-    for (int r = threadIdx.y; r < 32; r += 8) {
-      const int ix = x0 + threadIdx.x, iy = y0 + r;
-      if (ix < ex && iy < ey) s += x[xb + (int64_t)iy * xs_gy + ix] * tile[threadIdx.x][r];
-    }
-    __syncthreads();
+  for (int k = 0; k < 4; ++k) {   // read: lanes along the y-contiguous group (iy), rows along ix
+    const int ix = ly + 8 * k, iy = lx;
+    yv[k] = (t.y_base >= 0 && ix < t.nx && iy < t.ny) ? y[t.y_base + (int64_t)ix * t.y_ld + iy] : 0.0;
   }
-  red[tid] = s;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {   // write side: lanes along ix (x contiguous), rows along iy
+    const int ix = lx, iy = ly + 8 * k;
+    xv[k] = (beta != 0.0 && ix < t.nx && iy < t.ny) ? x[t.x_base + (int64_t)iy * t.x_ld + ix] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tile[ly + 8 * k][lx] = yv[k];
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int ix = lx, iy = ly + 8 * k;
+    if (ix < t.nx && iy < t.ny) x[t.x_base + (int64_t)iy * t.x_ld + ix] = axpby(alpha, tile[ix][iy], beta, xv[k]);
   }
-  if (tid == 0) p.partials[blockIdx.x] = red[0];
+}
+
+// Scalar partial of one 32x32 tile (one per CTA; fixed order: per thread, shuffle tree, warps in order).
+__global__ void __launch_bounds__(256) scalar_tile_kernel(const ElemParams p, double* __restrict__ partials) {
+  __shared__ double tile[32][33];
+  __shared__ double wsum[8];
+  const TileItem t = p.tiles[blockIdx.x];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const double* __restrict__ y = p.Y;
+  const double* __restrict__ x = p.X;
+  double yv[4], xv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int ix = ly + 8 * k, iy = lx;
+    yv[k] = (ix < t.nx && iy < t.ny) ? y[t.y_base + (int64_t)ix * t.y_ld + iy] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int ix = lx, iy = ly + 8 * k;
+    xv[k] = (ix < t.nx && iy < t.ny) ? x[t.x_base + (int64_t)iy * t.x_ld + ix] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tile[ly + 8 * k][lx] = yv[k];
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += xv[k] * tile[lx][ly + 8 * k];
+  s = cta_sum(s, wsum);
+  if (lx == 0 && ly == 0) partials[blockIdx.x] = s;
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -654,38 +634,64 @@ __global__ void fill_kernel(const ElemParams p) {
   }
 }
 
-// Deterministic: each CTA sums its segment in a fixed order (strided per thread, then a fixed tree).
-template <int MODE>
-__global__ void scalar_partials_kernel(const ElemParams p) {
-  __shared__ double red[kElemThreads];
+// Deterministic: each CTA sums its segment in a fixed order (per thread, shuffle tree, warps in order).
+__global__ void __launch_bounds__(kElemThreads) scalar_seg_kernel(const ElemParams p) {
+  __shared__ double wsum[kElemThreads / 32];
   __shared__ ElemDesc d;
   const Segment sg = p.segs[blockIdx.x];
   load_desc(d, p.descs + sg.desc);
-  const double* x = p.X + d.x_off;
-  const double* y = p.Y + d.y_off;
+  const double* __restrict__ x = p.X + d.x_off;
+  const double* __restrict__ y = p.Y + d.y_off;
   double s = 0.0;
-  if (MODE == kElemContig) {
+  if (d.mode == kElemContig) {
     const int64_t es = sg.e0 + (sg.e0 & 1);
     const int64_t n2 = (sg.e1 - es) / 2;
-    const double2* x2 = reinterpret_cast<const double2*>(x + es);
-    const double2* y2 = reinterpret_cast<const double2*>(y + es);
-    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
-      const double2 a = x2[i], b = y2[i];
-      s += a.x * b.x;
-      s += a.y * b.y;
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x + es);
+    const double2* __restrict__ y2 = reinterpret_cast<const double2*>(y + es);
+    for (int64_t i0 = threadIdx.x; i0 < n2; i0 += kElemThreads * 2) {
+      double2 a[2], b[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t i = i0 + u * kElemThreads;
+        a[u] = i < n2 ? x2[i] : make_double2(0.0, 0.0);
+        b[u] = i < n2 ? y2[i] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        s += a[u].x * b[u].x;
+        s += a[u].y * b[u].y;
+      }
     }
     if (threadIdx.x == 0 && es != sg.e0 && sg.e0 < sg.e1) s += x[sg.e0] * y[sg.e0];
     if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) s += x[sg.e1 - 1] * y[sg.e1 - 1];
   } else {
-    for (int64_t e = sg.e0 + threadIdx.x; e < sg.e1; e += blockDim.x) s += x[e] * y[y_offset((uint32_t)e, d)];
+    for (int64_t e0 = sg.e0 + threadIdx.x; e0 < sg.e1; e0 += kElemThreads * kElemUnroll) {
+      double yv[kElemUnroll], xv[kElemUnroll];
+#pragma unroll
+      for (int u = 0; u < kElemUnroll; ++u) {
+        const int64_t e = e0 + u * kElemThreads;
+        yv[u] = e < sg.e1 ? y[y_offset((uint32_t)e, d)] : 0.0;
+        xv[u] = e < sg.e1 ? x[e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kElemUnroll; ++u) s += xv[u] * yv[u];
+    }
   }
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = kElemThreads / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) p.partials[blockIdx.x] = red[0];
+  s = cta_sum(s, wsum);
+  if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
+}
+
+// First stage of the final sum when there are many partials: CTA c sums partials [c*4096, (c+1)*4096)
+// in a fixed order.
+constexpr int kFinalChunk = 4096;
+__global__ void __launch_bounds__(256) scalar_stage_kernel(const double* __restrict__ partials, int64_t n,
+                                                           double* __restrict__ out) {
+  __shared__ double wsum[8];
+  const int64_t b = (int64_t)blockIdx.x * kFinalChunk, e = min(n, b + kFinalChunk);
+  double s = 0.0;
+  for (int64_t i = b + threadIdx.x; i < e; i += 256) s += partials[i];
+  s = cta_sum(s, wsum);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
 __global__ void scalar_final_kernel(const double* partials, int64_t n, double alpha, double* out) {
@@ -706,11 +712,9 @@ cudaError_t launch_set(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   set_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
-cudaError_t launch_add(const ElemParams& p, int64_t nseg, cudaStream_t s) {
-  if (nseg <= 0) return cudaSuccess;
-  if (p.mode == kElemContig) add_kernel<kElemContig><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
-  else if (p.mode == kElemGeneric) add_kernel<kElemGeneric><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
-  else add_transpose_kernel<<<(unsigned)((nseg + kTilesPerCta - 1) / kTilesPerCta), dim3(32, 8), 0, s>>>(p, nseg);
+cudaError_t launch_add(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s) {
+  if (nseg > 0) add_seg_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  if (ntiles > 0) add_tile_kernel<<<(unsigned)ntiles, dim3(32, 8), 0, s>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
@@ -718,22 +722,24 @@ cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   fill_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
-cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, cudaStream_t s) {
-  if (nseg <= 0) return cudaSuccess;
-  if (p.mode == kElemContig) scalar_partials_kernel<kElemContig><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
-  else if (p.mode == kElemGeneric) scalar_partials_kernel<kElemGeneric><<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
-  else scalar_transpose_kernel<<<(unsigned)((nseg + kTilesPerCta - 1) / kTilesPerCta), dim3(32, 8), 0, s>>>(p, nseg);
+cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s) {
+  if (nseg > 0) scalar_seg_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
+  if (ntiles > 0) scalar_tile_kernel<<<(unsigned)ntiles, dim3(32, 8), 0, s>>>(p, p.partials + nseg);
   return cudaGetLastError();
 }
-int64_t scalar_num_partials(int mode, int64_t nseg) {
-  return mode == kElemTranspose ? (nseg + kTilesPerCta - 1) / kTilesPerCta : nseg;
-}
+int64_t scalar_scratch_elems(int64_t n) { return n > kFinalChunk ? (n + kFinalChunk - 1) / kFinalChunk : 0; }
 
-cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, cudaStream_t s) {
-  scalar_final_kernel<<<1, 1024, 0, s>>>(partials, n, alpha, out);
+cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, double* scratch,
+                               cudaStream_t s) {
+  const int64_t n1 = scratch ? scalar_scratch_elems(n) : 0;
+  if (n1 > 0) {
+    scalar_stage_kernel<<<(unsigned)n1, 256, 0, s>>>(partials, n, scratch);
+    scalar_final_kernel<<<1, 1024, 0, s>>>(scratch, n1, alpha, out);
+  } else {
+    scalar_final_kernel<<<1, 1024, 0, s>>>(partials, n, alpha, out);
+  }
   return cudaGetLastError();
 }
-
 
 // ------------------------------------------------------------------------------------------------
 // Split-K reduction (contractions with too few output tiles to fill the GPU): the chunks of a C part

@@ -116,6 +116,8 @@ struct ElemDesc {
   int64_t g_origin;                     // global linear index of the block origin (fill)
   int32_t n;                            // number of groups
   int32_t gy;                           // transpose mode: the group with y stride 1
+  int32_t mode;                         // kElemContig / kElemGeneric (segment work) or kElemTranspose
+  int32_t pad;
   FastDiv div[TT_MAX_ORDER];            // group extents
   int32_t y_str[TT_MAX_ORDER];          // strides of the other operand for each group
   int64_t g_str[TT_MAX_ORDER];          // global strides (fill; groups = dims)
@@ -125,10 +127,14 @@ struct ElemDesc {
 // transpose (innermost x group strided in y: 32x32 shared-memory tiles, coalesced both ways).
 enum { kElemContig = 0, kElemGeneric = 1, kElemTranspose = 2 };
 
-struct TileItem {        // transpose mode: one 32x32 tile of one block
-  int32_t desc;
-  int32_t tx, ty;        // tile index along the innermost x group / the y-contiguous group
-  int32_t batch;         // linear index over the remaining groups
+// Transpose-mode work: one 32x32 tile of one block, bases precomputed on the host.  Element (ix, iy)
+// of the tile (ix along X's contiguous group gx, iy along Y's contiguous group gy) is
+// X[x_base + iy*x_ld + ix] and Y[y_base + ix*y_ld + iy].
+struct TileItem {
+  int64_t x_base;        // X element offset of the tile origin
+  int64_t y_base;        // Y element offset of the tile origin (-1 = zero block: reads as 0)
+  int32_t nx, ny;        // valid extents (<= 32) along gx / gy
+  int32_t x_ld, y_ld;    // X stride of gy; Y stride of gx
 };
 
 struct ElemParams {
@@ -138,20 +144,23 @@ struct ElemParams {
   const Segment* segs;
   const TileItem* tiles;
   int32_t order;
-  int32_t mode;
   double alpha, beta;
   uint64_t key;           // fill: seed ^ tag*golden
   int32_t kind;           // fill kind
-  double* partials;       // scalar: one per segment / tile
+  double* partials;       // scalar: one per segment, then one per tile
 };
 
 cudaError_t launch_set(const ElemParams& p, int64_t nseg, cudaStream_t s);
-cudaError_t launch_add(const ElemParams& p, int64_t nseg, cudaStream_t s);
+// Descriptors carry their own mode: segment work (contiguous / generic descriptors) and tile work
+// (transpose descriptors) of one plan run as two launches on the same stream.
+cudaError_t launch_add(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s);
 cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s);
-// nseg = segments (contig / generic) or tiles (transpose); returns the number of partials written
-cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, cudaStream_t s);
-int64_t scalar_num_partials(int mode, int64_t nseg);
-cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out,
+// writes nseg + ntiles partials: p.partials[0, nseg) per segment, then one per tile
+cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s);
+// out = alpha * sum(partials[0, n)) in a fixed order; with scratch (scalar_scratch_elems(n) doubles)
+// large n is summed in two stages
+int64_t scalar_scratch_elems(int64_t n);
+cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, double* scratch,
                                 cudaStream_t s);
 
 // ---- perturbative triples (NEXT-4, tt_triples.cu)

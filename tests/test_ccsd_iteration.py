@@ -18,7 +18,7 @@ def _oracle_tensors(O_, V_, tO, tV, NL, tL):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("shape", [(8, 12, 2, 3, 10, 5), (12, 20, 3, 5, 14, 7)])
+@pytest.mark.parametrize("shape", [(8, 12, 2, 3, 10, 5), (12, 20, 3, 5, 14, 7), (14, 20, 3, 5, 14, 7)])
 def test_ccsd_iteration_vs_oracle(shape):
     import torch
     import paper_2201_01257_b200 as tt

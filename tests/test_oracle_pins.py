@@ -484,3 +484,62 @@ def test_freivalds_pins():
     Cbad[2, 1, 0, 2] *= 1 + 1e-9
     lhs2, _ = O.freivalds(Cbad, "abij", A, "acik", B, "cbkj", x, 0.7, 1.3, C0)
     assert np.abs(lhs2 - rhs).max() > 1e-11 * np.abs(C).max()
+
+
+# ------------------------------------------------------------------ add / scalar under k-cycle label maps
+
+def _brute_permuted(A, a_lbl, c_lbl):
+    """Pure-Python definition of P173 ``C(c_lbl) = A(a_lbl)``: C[x] = A[x re-indexed by label]."""
+    shape = tuple(A.shape[a_lbl.index(l)] for l in c_lbl)
+    C = np.empty(shape)
+    for x in product(*[range(n) for n in shape]):
+        lab = dict(zip(c_lbl, x))
+        C[x] = A[tuple(lab[l] for l in a_lbl)]
+    return C
+
+
+# (c_lbl, a_lbl): 2-cycles, 3-cycles and 4-cycles of the label map (VERDICT r1 item 1), with distinct
+# extents per label so that any inverted / transposed map changes shapes or values
+K_CYCLES = [("abij", "bija"), ("abij", "jabi"), ("abij", "ijab"), ("abij", "baji"), ("abc", "cab"),
+            ("abc", "bca"), ("ia", "ai"), ("abij", "ajbi"), ("abij", "aijb")]
+
+
+@pytest.mark.parametrize("c_lbl,a_lbl", K_CYCLES)
+def test_add_k_cycles_vs_einsum_and_brute_force(c_lbl, a_lbl):
+    """P173 AddOp 'with respect to the label permutation': ops.add equals numpy.einsum (independent
+    library routine) and the pure-Python element loop, for beta in {0, 1, -0.5}."""
+    ext = {"a": 3, "b": 4, "c": 2, "i": 5, "j": 2}
+    A = rnd(tuple(ext[l] for l in a_lbl), 41, 1)
+    C0 = rnd(tuple(ext[l] for l in c_lbl), 41, 3)
+    perm_ref = np.einsum(f"{a_lbl}->{c_lbl}", A)
+    assert np.array_equal(perm_ref, _brute_permuted(A, a_lbl, c_lbl))
+    for beta in (0.0, 1.0, -0.5):
+        got = O.add(C0, c_lbl, A, a_lbl, 0.75, beta)
+        ref = 0.75 * perm_ref if beta == 0.0 else beta * C0 + 0.75 * perm_ref
+        assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("c_lbl,a_lbl", K_CYCLES)
+def test_scalar_k_cycles_vs_brute_force(c_lbl, a_lbl):
+    """Order-0 contraction s = alpha * sum_x A[x_A] B[x_B]: ops.scalar equals a pure-Python loop over
+    the label values (exact on integer inputs), and numpy.einsum on uniform inputs."""
+    ext = {"a": 3, "b": 4, "c": 2, "i": 5, "j": 2}
+    for kind in (S.KIND_INTEGER, S.KIND_UNIFORM):
+        A = rnd(tuple(ext[l] for l in a_lbl), 43, 1, kind)
+        B = rnd(tuple(ext[l] for l in c_lbl), 43, 2, kind)
+        s = O.scalar(A, a_lbl, B, c_lbl, -0.5)
+        if kind == S.KIND_INTEGER:
+            tot = 0.0
+            for x in product(*[range(ext[l]) for l in c_lbl]):
+                lab = dict(zip(c_lbl, x))
+                tot += A[tuple(lab[l] for l in a_lbl)] * B[x]
+            assert s == -0.5 * tot
+        else:
+            ref = -0.5 * float(np.einsum(f"{a_lbl},{c_lbl}->", A, B))
+            assert abs(s - ref) <= 1e-14 * max(abs(ref), 1.0)
+
+
+def test_add_inverse_cycle_is_detected():
+    """A 3-cycle and its inverse differ: the pins above would fail an inverted permutation."""
+    X = rnd((3, 3, 3), 45, 1)
+    assert not np.array_equal(O.add(X, "abc", X, "cab", 1.0, 0.0), O.add(X, "abc", X, "bca", 1.0, 0.0))
