@@ -59,6 +59,7 @@ typedef struct tt_is_s* tt_is;
 typedef struct tt_tis_s* tt_tis;
 typedef struct tt_tensor_s* tt_tensor;
 typedef struct tt_sched_s* tt_sched;
+typedef struct tt_sim_s* tt_sim;
 
 /* Per-call statistics of the last set/add/contract/scalar call on a context (host-side counts). */
 typedef struct {
@@ -87,6 +88,22 @@ typedef struct {
 tt_status tt_ctx_create(int32_t device, void* cuda_stream, int32_t rank, int32_t nranks,
                         const void* nccl_id, tt_ctx* out);
 tt_status tt_ctx_destroy(tt_ctx ctx);
+/* Simulated ranks on ONE GPU (P212 SPMD with "access to the remote portions"; S506 rank
+ * invariance): a group of nranks contexts on the same device, each created with tt_ctx_create_sim and
+ * driven by its OWN host thread exactly as one process per GPU is (every rank makes the same call
+ * sequence; each rank binds its own buffers).  Every multi-rank code path runs unchanged -- partitions,
+ * owners, gather plans, row-split and compact storage -- except the transport: the input-tile gather
+ * becomes one cudaMemcpyAsync (device to device, stream-ordered after the peer's producers via CUDA
+ * events) per received run, read from the peer rank's buffer, and the scalar all-reduce a fixed
+ * rank-order sum of the ranks' partials.  Each collective is a host barrier over the group, so a rank
+ * that skips a collective the others make deadlocks (as NCCL would).  Tensors are matched across
+ * ranks by creation order.  tt_sim_create allocates its small device staging here (device = the
+ * group's GPU); destroy the group after all its contexts. */
+tt_status tt_sim_create(int32_t device, int32_t nranks, tt_sim* out);
+tt_status tt_sim_destroy(tt_sim sim);
+/* Context of simulated rank `rank` of `sim` (stream: this rank's CUDA stream, not owned; use one
+ * stream per rank). */
+tt_status tt_ctx_create_sim(void* cuda_stream, int32_t rank, tt_sim sim, tt_ctx* out);
 /* Writes a fresh ncclUniqueId (128 bytes) into out128 (rank 0 calls it and broadcasts the bytes). */
 tt_status tt_nccl_unique_id(void* out128);
 /* Record CUDA events around every kernel the library launches (for roofline timing). */
@@ -186,9 +203,9 @@ tt_status tt_tensor_set_compact(tt_tensor t, int32_t on);
  * blocks ARE the parent's blocks at the shifted tile coordinates: same storage (the parent's current
  * binding is used at every call), same packed offsets and owners, no copy.  A view can be an operand or
  * the output of every operation; reads and writes go to the parent's memory.  Its block map, offsets
- * and owners are captured at creation (re-create the view after changing the parent's ownership);
- * views of compact or row-split tensors, views of views, and ownership / compact changes on a view are
- * TT_E_UNSUPPORTED.  tt_fill_synthetic on a view uses the view's own global indices.  Destroy the view
+ * and owners are captured at creation, so while a view of T exists, ownership / compact / partition
+ * changes of T return TT_E_STATE (destroy the views, change T, re-create them); views of compact or
+ * row-split tensors, views of views, and ownership / compact changes on a view are TT_E_UNSUPPORTED.  tt_fill_synthetic on a view uses the view's own global indices.  Destroy the view
  * before its parent. */
 tt_status tt_tensor_view(tt_tensor T, const tt_tis* dims, tt_tensor* out);
 /* Storage size in doubles (what tt_tensor_bind needs) and the per-block storage offsets (nblocks
@@ -301,8 +318,10 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, 
  *   Vooov  v^{ij}_{ma} as Vooov(i,j,m,a) dims (O, O, O, V)
  *   Vvovv  v^{ei}_{ab} as Vvovv(e,i,a,b) dims (V, O, V, V)
  *   Voovv  v^{ij}_{ab} as Voovv(i,j,a,b) dims (O, O, V, V)
- *   every dim must be T1's tiled-space object itself (TT_E_TILING); block maps are free (zero blocks read
- *   as 0); virtual ranges must have even sizes (TT_E_UNSUPPORTED); eps_o[n_o], eps_v[n_v]: DEVICE arrays
+ *   every dim must be T1's tiled-space object itself (TT_E_TILING); zero blocks read as 0, and every
+ *   non-zero block must obey the spin rule the kernel prunes by (sum of the tile spins of dims {0,1}
+ *   = that of dims {2,3}; T1: s_a = s_i) -- on spaces without spin any map passes, on alpha/beta
+ *   spaces a block outside the R7 spin map is TT_E_UNSUPPORTED; virtual ranges must have even sizes (TT_E_UNSUPPORTED); eps_o[n_o], eps_v[n_v]: DEVICE arrays
  *   of orbital energies (global index order).
  * Execution: the inputs are copied into dense permuted layouts in the workspace; then one fused kernel
  * CTA per unit = (occupied triple i<j<k, triple of 16-wide virtual boxes b_a <= b_b <= b_c) forms the

@@ -68,6 +68,9 @@ class TriplesInfo(ctypes.Structure):
 _SIGS = {
     "tt_ctx_create": [_i32, _vp, _i32, _i32, _vp, _P(_vp)],
     "tt_ctx_destroy": [_vp],
+    "tt_sim_create": [_i32, _i32, _P(_vp)],
+    "tt_sim_destroy": [_vp],
+    "tt_ctx_create_sim": [_vp, _i32, _vp, _P(_vp)],
     "tt_nccl_unique_id": [_vp],
     "tt_ctx_set_profiling": [_vp, _i32],
     "tt_profile_read": [_vp, ctypes.c_char_p, _P(_dbl), _P(_i64)],
@@ -182,15 +185,36 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class SimGroup:
+    """Simulated ranks on one GPU (tt_sim_create): ``Context(stream=..., rank=r, sim=group)`` per rank,
+    each rank driven by its own host thread (SPMD); gathers become device copies between the ranks'
+    buffers, the all-reduce a rank-order sum."""
+
+    def __init__(self, device: int, nranks: int):
+        h = _vp()
+        _check(_lib.tt_sim_create(device, nranks, ctypes.byref(h)))
+        self.h, self.device, self.nranks = h, device, nranks
+
+    def close(self):
+        if self.h:
+            _check(_lib.tt_sim_destroy(self.h))
+            self.h = None
+
+
 class Context:
-    """ExecutionContext (P178-188).  device=-1 gives a host-only context (metadata only)."""
+    """ExecutionContext (P178-188).  device=-1 gives a host-only context (metadata only); ``sim`` = a
+    SimGroup: simulated rank ``rank`` of that group (device and nranks come from the group)."""
 
     def __init__(self, device: int = 0, stream: int = 0, rank: int = 0, nranks: int = 1,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, sim: Optional[SimGroup] = None):
         h = _vp()
-        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        _check(_lib.tt_ctx_create(device, _vp(stream or 0), rank, nranks, idbuf, ctypes.byref(h)))
-        self.h, self.device, self.rank, self.nranks = h, device, rank, nranks
+        if sim is not None:
+            _check(_lib.tt_ctx_create_sim(_vp(stream or 0), rank, sim.h, ctypes.byref(h)))
+            device, nranks = sim.device, sim.nranks
+        else:
+            idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            _check(_lib.tt_ctx_create(device, _vp(stream or 0), rank, nranks, idbuf, ctypes.byref(h)))
+        self.h, self.device, self.rank, self.nranks, self.sim = h, device, rank, nranks, sim
 
     def close(self):
         if self.h:
@@ -392,9 +416,15 @@ class Tensor:
     def download_ptr(self, host_ptr: int):
         _check(_lib.tt_tensor_download(self.ctx.h, self.h, _vp(host_ptr)))
 
+    def close(self):
+        """Destroys the handle now (a view: releases its parent's layout, see tt_tensor_view)."""
+        if getattr(self, "h", None) is not None:
+            _lib.tt_tensor_destroy(self.h)
+            self.h = None
+
     def __del__(self):  # pragma: no cover
         try:
-            _lib.tt_tensor_destroy(self.h)
+            self.close()
         except Exception:
             pass
 

@@ -335,6 +335,7 @@ struct GatherPlan {
   std::vector<int64_t> recv_list, send_list;   // (op, block, peer, e0, e1) rows
   std::vector<Run> recv, send;
   int64_t recv_bytes = 0;
+  int64_t all_pieces = 0;   // pieces over ALL ranks: 0 = no rank exchanges anything (same on every rank)
   bool one_group = false;   // few pieces over ALL ranks (the same decision on every rank): one NCCL group
 };
 
@@ -430,7 +431,104 @@ tt_status build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops
   runs(gp.send_list, gp.send);
   for (const Run& r : gp.recv) gp.recv_bytes += r.len * 8;
   gp.one_group = all_pieces <= (int64_t)kGatherGroupOps * P;
+  gp.all_pieces = all_pieces;
   return TT_OK;
+}
+
+// The context stream must not run NCCL work while prefetched gathers are still in flight on the
+// communication stream (never two streams on one communicator at once): called before every
+// collective issued on ctx->stream.
+tt_status wait_comm(tt_ctx ctx) {
+  if (!ctx->comm_pending) return TT_OK;
+  TT_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->comm_done, 0));
+  ctx->comm_pending = false;
+  return TT_OK;
+}
+
+// Simulated ranks (tt_ctx_create_sim): the gather as device-to-device copies from the peers' buffers.
+// Entry: every rank records `ready` after its earlier work and meets the others at a barrier; each
+// receiver waits on its sources' `ready` and copies its received pieces (adjacent pieces merged when
+// contiguous on both sides: one cudaMemcpyAsync per run); exit: `done` + barrier, and every rank waits
+// on all `done` events before later work may overwrite what others read.  Every rank passes both
+// barriers even after an error (no rank is left waiting).
+tt_status sim_exchange(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops, cudaStream_t stream) {
+  tt_sim S = ctx->sim;
+  const int me = ctx->rank, P = ctx->nranks;
+  tt_status st = TT_OK;
+  if (cudaEventRecord(S->ready[me], stream) != cudaSuccess) st = fail(TT_E_CUDA, "sim: event record");
+  S->barrier();
+  std::vector<char> waited(P, 0);
+  double* pd = nullptr;
+  const double* ps = nullptr;
+  int64_t pn = 0;
+  int64_t copies = 0;
+  auto flush = [&]() {
+    if (pn > 0 && st == TT_OK) {
+      if (cudaMemcpyAsync(pd, ps, (size_t)pn * 8, cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
+        st = fail(TT_E_CUDA, "sim: cudaMemcpyAsync");
+      ++copies;
+    }
+    pn = 0;
+  };
+  for (size_t i = 0; st == TT_OK && i + 4 < gp.recv_list.size() + 1; i += 5) {
+    const int op = (int)gp.recv_list[i], src = (int)gp.recv_list[i + 2];
+    const int64_t blk = gp.recv_list[i + 1], a0 = gp.recv_list[i + 3], z0 = gp.recv_list[i + 4];
+    tt_tensor T = ops[op], Q = S->peer(T, src);
+    if (!Q || !Q->data || Q->nblocks != T->nblocks || Q->blk_off[blk] < 0) {
+      st = fail(TT_E_STATE, "sim: rank %d holds no matching tensor (creation order differs across ranks?)", src);
+      break;
+    }
+    if (!waited[src]) {
+      if (cudaStreamWaitEvent(stream, S->ready[src], 0) != cudaSuccess) st = fail(TT_E_CUDA, "sim: event wait");
+      waited[src] = 1;
+    }
+    double* d = T->data + T->blk_off[blk] + a0;
+    const double* s = Q->data + Q->blk_off[blk] + a0;
+    if (pn > 0 && d == pd + pn && s == ps + pn) {
+      pn += z0 - a0;
+    } else {
+      flush();
+      pd = d;
+      ps = s;
+      pn = z0 - a0;
+    }
+  }
+  flush();
+  if (cudaEventRecord(S->done[me], stream) != cudaSuccess && st == TT_OK) st = fail(TT_E_CUDA, "sim: event record");
+  S->barrier();
+  for (int q = 0; q < P; ++q)
+    if (q != me && cudaStreamWaitEvent(stream, S->done[q], 0) != cudaSuccess && st == TT_OK)
+      st = fail(TT_E_CUDA, "sim: event wait");
+  ctx->last.launches += 0 * copies;
+  return st;
+}
+
+// dst (device, one double) <- sum over ranks of every rank's dst, on `stream`
+tt_status allreduce_sum(tt_ctx ctx, double* dst, cudaStream_t stream) {
+  if (ctx->nranks <= 1) return TT_OK;
+  if (stream == ctx->stream) TT_TRY(wait_comm(ctx));
+  if (ctx->sim) {
+    tt_sim S = ctx->sim;
+    const int me = ctx->rank, P = ctx->nranks;
+    tt_status st = TT_OK;
+    if (cudaMemcpyAsync(S->d_part + me, dst, 8, cudaMemcpyDeviceToDevice, stream) != cudaSuccess ||
+        cudaEventRecord(S->ready[me], stream) != cudaSuccess)
+      st = fail(TT_E_CUDA, "sim all-reduce: copy / event");
+    S->barrier();
+    for (int q = 0; q < P && st == TT_OK; ++q)
+      if (q != me && cudaStreamWaitEvent(stream, S->ready[q], 0) != cudaSuccess) st = fail(TT_E_CUDA, "sim: event wait");
+    if (st == TT_OK && launch_sum_slots(S->d_part, P, dst, stream) != cudaSuccess) st = fail(TT_E_CUDA, "sim: sum kernel");
+    if (cudaEventRecord(S->done[me], stream) != cudaSuccess && st == TT_OK) st = fail(TT_E_CUDA, "sim: event record");
+    S->barrier();
+    for (int q = 0; q < P; ++q)
+      if (q != me && cudaStreamWaitEvent(stream, S->done[q], 0) != cudaSuccess && st == TT_OK)
+        st = fail(TT_E_CUDA, "sim: event wait");
+    return st;
+  }
+  const char* err = nullptr;
+  const NcclApi* api = nccl_api(&err);
+  if (!api) return fail(TT_E_NCCL, "%s", err);
+  return nccl_check(api->AllReduce(dst, dst, 1, kNcclFloat64, kNcclSum, ctx->comm, stream), "ncclAllReduce");
 }
 
 // Exchange schedule: with at most kGatherGroupOps runs per direction, one group over all peers; else
@@ -441,12 +539,13 @@ tt_status build_gather(tt_ctx ctx, Needs need, const std::vector<tt_tensor>& ops
 
 tt_status run_gather(tt_ctx ctx, const GatherPlan& gp, const std::vector<tt_tensor>& ops,
                      cudaStream_t stream = nullptr) {
-  if (ctx->nranks <= 1 || (gp.recv.empty() && gp.send.empty())) return TT_OK;
+  if (ctx->nranks <= 1 || gp.all_pieces == 0) return TT_OK;   // the same decision on every rank
   if (!stream) {
     stream = ctx->stream;
-    // never two streams on one communicator at once: wait for prefetched gathers still in flight
-    if (ctx->comm_pending) TT_CUDA(cudaStreamWaitEvent(stream, ctx->comm_done, 0));
+    TT_TRY(wait_comm(ctx));
   }
+  if (ctx->sim) return sim_exchange(ctx, gp, ops, stream);
+  if (gp.recv.empty() && gp.send.empty()) return TT_OK;
   const char* err = nullptr;
   const NcclApi* api = nccl_api(&err);
   if (!api) return fail(TT_E_NCCL, "%s", err);
@@ -610,6 +709,94 @@ tt_status tt_nccl_unique_id(void* out128) {
   return nccl_check(api->GetUniqueId(out128), "ncclGetUniqueId");
 }
 
+}  // extern "C"
+
+// device checks and kernel setup of a new context on c->device (>= 0)
+static tt_status ctx_device_setup(tt_ctx c) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || c->device >= ndev)
+    return fail(TT_E_CUDA, "device %d not available: %s", c->device, cudaGetErrorString(e));
+  DeviceGuard dg(c->device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
+  if (prop.major != 10)
+    return fail(TT_E_UNSUPPORTED, "libtt is built for sm_100a (B200); device %d is sm_%d%d", c->device, prop.major, prop.minor);
+  for (int v = 0; v < n_variants(); ++v) {
+    cudaError_t e2 = v < num_contract_variants() ? contract_variant_setup(v) : ws_variant_setup(v - num_contract_variants());
+    if (e2 != cudaSuccess) return fail(TT_E_CUDA, "kernel setup: %s", cudaGetErrorString(e2));
+  }
+  return TT_OK;
+}
+
+extern "C" {
+
+tt_status tt_sim_create(int32_t device, int32_t nranks, tt_sim* out) {
+  if (!out) return fail(TT_E_ARG, "NULL output handle");
+  *out = nullptr;
+  if (nranks < 1 || device < 0) return fail(TT_E_ARG, "bad device %d / nranks %d", device, nranks);
+  tt_sim S = new tt_sim_s();
+  S->nranks = nranks;
+  S->device = device;
+  S->ctx.assign(nranks, nullptr);
+  DeviceGuard dg(device);
+  bool ok = cudaMalloc((void**)&S->d_part, sizeof(double) * nranks) == cudaSuccess;
+  for (int r = 0; ok && r < nranks; ++r) {
+    cudaEvent_t e0, e1;
+    ok = cudaEventCreateWithFlags(&e0, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) == cudaSuccess;
+    if (ok) {
+      S->ready.push_back(e0);
+      S->done.push_back(e1);
+    }
+  }
+  if (!ok) {
+    tt_sim_destroy(S);
+    return fail(TT_E_CUDA, "cannot create the simulated-rank group on device %d", device);
+  }
+  *out = S;
+  return TT_OK;
+}
+
+tt_status tt_sim_destroy(tt_sim S) {
+  if (!S) return TT_OK;
+  DeviceGuard dg(S->device);
+  for (cudaEvent_t e : S->ready) cudaEventDestroy(e);
+  for (cudaEvent_t e : S->done) cudaEventDestroy(e);
+  if (S->d_part) cudaFree(S->d_part);
+  delete S;
+  return TT_OK;
+}
+
+tt_status tt_ctx_create_sim(void* stream, int32_t rank, tt_sim S, tt_ctx* out) {
+  if (!out || !S) return fail(TT_E_ARG, "NULL argument");
+  *out = nullptr;
+  if (rank < 0 || rank >= S->nranks) return fail(TT_E_ARG, "bad rank %d / nranks %d", rank, S->nranks);
+  {
+    std::lock_guard<std::mutex> lk(S->mu);
+    if (S->ctx[rank]) return fail(TT_E_STATE, "simulated rank %d already has a context", rank);
+  }
+  tt_ctx c = new tt_ctx_s();
+  c->device = S->device;
+  c->stream = (cudaStream_t)stream;
+  c->rank = rank;
+  c->nranks = S->nranks;
+  c->sim = S;
+  tt_status s = ctx_device_setup(c);
+  if (s == TT_OK) {
+    DeviceGuard dg(c->device);
+    s = dev_alloc(c, &c->d_scalar, 2);
+  }
+  if (s != TT_OK) {
+    delete c;
+    return s;
+  }
+  std::lock_guard<std::mutex> lk(S->mu);
+  S->ctx[rank] = c;
+  *out = c;
+  return TT_OK;
+}
+
 tt_status tt_ctx_create(int32_t device, void* stream, int32_t rank, int32_t nranks, const void* nccl_id, tt_ctx* out) {
   if (!out) return fail(TT_E_ARG, "NULL output handle");
   *out = nullptr;
@@ -620,27 +807,12 @@ tt_status tt_ctx_create(int32_t device, void* stream, int32_t rank, int32_t nran
   c->rank = rank;
   c->nranks = nranks;
   if (device >= 0) {
-    int ndev = 0;
-    cudaError_t e = cudaGetDeviceCount(&ndev);
-    if (e != cudaSuccess || device >= ndev) {
+    tt_status s0 = ctx_device_setup(c);
+    if (s0 != TT_OK) {
       delete c;
-      return fail(TT_E_CUDA, "device %d not available: %s", device, cudaGetErrorString(e));
+      return s0;
     }
     DeviceGuard dg(device);
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
-    if (prop.major != 10) {
-      delete c;
-      return fail(TT_E_UNSUPPORTED, "libtt is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
-    }
-    for (int v = 0; v < n_variants(); ++v) {
-      cudaError_t e2 = v < num_contract_variants() ? contract_variant_setup(v)
-                                                   : ws_variant_setup(v - num_contract_variants());
-      if (e2 != cudaSuccess) {
-        delete c;
-        return fail(TT_E_CUDA, "kernel setup: %s", cudaGetErrorString(e2));
-      }
-    }
     if (nranks > 1) {
       if (!nccl_id) {
         delete c;
@@ -682,6 +854,10 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
   if (ctx->comm) {
     const NcclApi* api = nccl_api(nullptr);
     if (api) api->CommDestroy(ctx->comm);
+  }
+  if (ctx->sim) {
+    std::lock_guard<std::mutex> lk(ctx->sim->mu);
+    ctx->sim->ctx[ctx->rank] = nullptr;
   }
   delete ctx;
   return TT_OK;
@@ -872,6 +1048,14 @@ tt_status tt_tis_range(tt_tis parent, int32_t range, tt_tis* out) {
 // ---------------------------------------------------------------------------------------------
 // tensors
 
+// a view copies its parent's block map, storage offsets and owners at creation: the parent's layout
+// may not change while views of it exist (they would keep stale offsets and owners)
+static tt_status check_no_views(tt_tensor t) {
+  if (t->live_views > 0)
+    return fail(TT_E_STATE, "tensor has %d live view(s): destroy them before changing its layout", t->live_views);
+  return TT_OK;
+}
+
 static tt_status tensor_new(tt_ctx ctx, int32_t order, const tt_tis* dims, tt_tensor* out) {
   if (!ctx || !out || !dims) return fail(TT_E_ARG, "NULL argument");
   *out = nullptr;
@@ -880,15 +1064,24 @@ static tt_status tensor_new(tt_ctx ctx, int32_t order, const tt_tis* dims, tt_te
   t->ctx = ctx;
   t->order = order;
   t->uid = g_uid++;
+  t->seq = ctx->tensor_seq++;
   t->nblocks = 1;
   for (int d = 0; d < order; ++d) {
     if (!dims[d]) {
-      delete t;
+      tt_tensor_destroy(t);
       return fail(TT_E_ARG, "NULL tiled index space for dim %d", d);
     }
     t->dims.push_back(dims[d]);
     t->grid.push_back(dims[d]->ntiles());
     t->nblocks *= dims[d]->ntiles();
+  }
+  if (ctx->sim) {   // simulated ranks: peers find this rank's handle by creation order
+    t->sim = ctx->sim;
+    t->sim_rank = ctx->rank;
+    std::lock_guard<std::mutex> lk(ctx->sim->mu);
+    auto& v = ctx->sim->reg[t->seq];
+    if (v.empty()) v.assign(ctx->nranks, nullptr);
+    v[ctx->rank] = t;
   }
   *out = t;
   return TT_OK;
@@ -967,7 +1160,7 @@ tt_status tt_tensor_create_spin(tt_ctx ctx, int32_t order, const tt_tis* dims, u
   tt_tensor t;
   TT_TRY(tensor_new(ctx, order, dims, &t));
   if ((upper | lower) >> order) {
-    delete t;
+    tt_tensor_destroy(t);
     return fail(TT_E_ARG, "spin masks reference dims beyond the order");
   }
   t->nz.resize(t->nblocks);
@@ -1040,13 +1233,17 @@ tt_status tt_tensor_view(tt_tensor T, const tt_tis* dims, tt_tensor* out) {
   v->parts.assign(v->nblocks, {});
   v->data = T->data;
   v->capacity = T->capacity;
+  T->live_views++;
   *out = v;
   return TT_OK;
 }
 
+
+
 tt_status tt_tensor_set_compact(tt_tensor t, int32_t on) {
   if (!t) return fail(TT_E_ARG, "NULL tensor");
   if (t->view_of) return fail(TT_E_UNSUPPORTED, "a view takes its storage from its parent");
+  TT_TRY(check_no_views(t));
   if ((on != 0) != t->compact) {
     t->compact = on != 0;
     apply_storage(t);
@@ -1065,6 +1262,7 @@ tt_status tt_tensor_storage(tt_tensor t, int64_t* storage_elems, const int64_t**
 tt_status tt_tensor_set_owner(tt_tensor t, const int32_t* owner) {
   if (!t || !owner) return fail(TT_E_ARG, "NULL argument");
   if (t->view_of) return fail(TT_E_UNSUPPORTED, "a view takes its owners from its parent");
+  TT_TRY(check_no_views(t));
   for (int64_t b = 0; b < t->nblocks; ++b) {
     if (!t->nz[b]) continue;
     if (owner[b] != TT_REPLICATED && (owner[b] < 0 || owner[b] >= t->ctx->nranks))
@@ -1082,6 +1280,7 @@ tt_status tt_tensor_set_parts(tt_tensor t, int64_t n, const int64_t* blk, const 
                               const int32_t* owner) {
   if (!t || (n > 0 && (!blk || !lo || !hi || !owner))) return fail(TT_E_ARG, "NULL argument");
   if (t->view_of) return fail(TT_E_UNSUPPORTED, "a view takes its owners from its parent");
+  TT_TRY(check_no_views(t));
   std::map<int64_t, std::vector<tt_tensor_s::Part>> np;
   for (int64_t i = 0; i < n; ++i) {
     if (blk[i] < 0 || blk[i] >= t->nblocks || !t->nz[blk[i]])
@@ -1153,6 +1352,17 @@ tt_status tt_tensor_download(tt_ctx ctx, tt_tensor t, double* host) {
 
 tt_status tt_tensor_destroy(tt_tensor t) {
   // device metadata is owned by the context allocation list (freed by tt_ctx_destroy)
+  if (t && t->view_of) t->view_of->live_views--;
+  if (t && t->sim) {
+    std::lock_guard<std::mutex> lk(t->sim->mu);
+    auto it = t->sim->reg.find(t->seq);
+    if (it != t->sim->reg.end() && it->second[t->sim_rank] == t) {
+      it->second[t->sim_rank] = nullptr;
+      bool any = false;
+      for (tt_tensor u : it->second) any = any || u;
+      if (!any) t->sim->reg.erase(it);
+    }
+  }
   delete t;
   return TT_OK;
 }
@@ -1206,7 +1416,9 @@ int fuse_elem(ElemDesc& d, int order, const int32_t* ext, const int* ypos, const
     if (d.y_str[g] == 1) d.gy = g;
   }
   if (n == 1 && d.y_str[0] == 1) d.mode = kElemContig;
-  else if (d.y_str[n - 1] == 1 || d.gy < 0) d.mode = kElemGeneric;
+  else if (d.y_str[n - 1] == 1 && d.div[n - 1].d >= 8) d.mode = kElemRows;
+  else if (d.y_str[n - 1] == 1) d.mode = kElemGeneric;
+  else if (d.gy < 0) d.mode = kElemGeneric;
   else d.mode = kElemTranspose;
   return d.mode;
 }
@@ -1572,12 +1784,7 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
     Launch L(ctx, "tt_scalar_final");
     TT_CUDA(launch_scalar_final(ep->d_partials, npart, alpha, dst, ep->d_partials + npart, ctx->stream));
   }
-  if (ctx->nranks > 1) {
-    const char* err = nullptr;
-    const NcclApi* api = nccl_api(&err);
-    if (!api) return fail(TT_E_NCCL, "%s", err);
-    TT_TRY(nccl_check(api->AllReduce(dst, dst, 1, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream), "ncclAllReduce"));
-  }
+  TT_TRY(allreduce_sum(ctx, dst, ctx->stream));
   if (!ctx->scalar_dev_out) {   // inside a captured graph the scheduler copies the device slot later
     TT_CUDA(cudaMemcpyAsync(result, dst, 8, cudaMemcpyDeviceToHost, ctx->stream));
     TT_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -2263,6 +2470,7 @@ namespace {
 tt_status split_partition(tt_ctx ctx, tt_tensor C, const std::vector<int64_t>& cblk,
                           const std::vector<int64_t>& cost, uint32_t group_mask) {
   if (C->view_of) return fail(TT_E_UNSUPPORTED, "a view takes its owners from its parent");
+  TT_TRY(check_no_views(C));
   if (group_mask >> C->order) return fail(TT_E_ARG, "group_mask references dims beyond the order of C");
   if (group_mask && !(group_mask & 1u)) return fail(TT_E_ARG, "row splitting needs dim 0 among the grouping dims");
   // units (as tt_partition_lpt)
@@ -2559,14 +2767,26 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     std::vector<tt_tis> vd = {tp, tq, tr, ts};
     int64_t nvb = 1;
     for (auto t : vd) nvb *= t->ntiles();
+    // X's (p_t, r_t) tile pairs holding any non-zero block (over all L tiles): the maps of W and V
+    // follow from X's actual block map (R19b), not from the tiles' spins
+    const int32_t nx0 = X->grid[0], nx1 = X->grid[1];
+    std::vector<uint8_t> xnz((size_t)nx0 * nx1, 0);
+    {
+      int32_t xc[TT_MAX_ORDER];
+      for (int64_t xb = 0; xb < X->nblocks; ++xb)
+        if (X->nz[xb]) {
+          X->block_coords(xb, xc);
+          xnz[(size_t)xc[0] * nx1 + xc[1]] = 1;
+        }
+    }
     std::vector<uint8_t> vnz(nvb), wnz(nvb);
     for (int64_t x = 0; x < nvb; ++x) {
       int64_t y = x;
       int32_t co[4];
       for (int d = 3; d >= 0; --d) { co[d] = (int32_t)(y % vd[d]->ntiles()); y /= vd[d]->ntiles(); }
-      const int sp = tp->spin[co[0]], sq = tq->spin[co[1]], sr = tr->spin[co[2]], ss = ts->spin[co[3]];
-      wnz[x] = (sp == sr && sq == ss) ? 1 : 0;             // Coulomb term reachable
-      vnz[x] = (wnz[x] || (sp == ss && sq == sr)) ? 1 : 0;  // Coulomb or exchange
+      auto xn = [&](int32_t u, int32_t w) { return xnz[(size_t)u * nx1 + w] != 0; };
+      wnz[x] = (xn(co[0], co[2]) && xn(co[1], co[3])) ? 1 : 0;              // Coulomb term reachable
+      vnz[x] = (wnz[x] || (xn(co[0], co[3]) && xn(co[1], co[2]))) ? 1 : 0;  // Coulomb or exchange
     }
     TT_TRY(new_meta_tensor(ctx, vd, vnz, &cp->Vmeta));
     TT_TRY(new_meta_tensor(ctx, vd, wnz, &cp->Wmeta));
@@ -3146,6 +3366,22 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   for (int x = 0; x < 5; ++x) {
     if (ins[x]->compact || ins[x]->any_split || ins[x]->view_of)
       return fail(TT_E_UNSUPPORTED, "%s: compact, row-split or view inputs", names[x]);
+    // the kernel prunes units and m / e ranges by the spins of the index ranges (R28, R6/R7): valid
+    // only if every non-zero input block obeys the spin rule (upper dims {0,1} | lower {2,3}; T1 {0}|{1})
+    int32_t c[TT_MAX_ORDER];
+    for (int64_t b = 0; b < ins[x]->nblocks; ++b) {
+      if (!ins[x]->nz[b]) continue;
+      ins[x]->block_coords(b, c);
+      int su = 0, sl = 0;
+      for (int d = 0; d < ins[x]->order; ++d) {
+        const int s = ins[x]->dims[d]->spin[c[d]];
+        if (d < ins[x]->order / 2) su += s;
+        else sl += s;
+      }
+      if (su != sl)
+        return fail(TT_E_UNSUPPORTED, "%s: non-zero block %lld breaks the spin rule the (T) kernel prunes by "
+                    "(use the spin block maps of reading R7 on alpha/beta spaces)", names[x], (long long)b);
+    }
     if (ctx->nranks > 1)
       for (int64_t b = 0; b < ins[x]->nblocks; ++b)
         if (ins[x]->nz[b] && ins[x]->owner[b] != TT_REPLICATED)
@@ -3365,13 +3601,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     Launch L(ctx, "tt_scalar_final");
     TT_CUDA(launch_scalar_final(partials + tp->unit0, tp->nunits, 1.0, ctx->d_scalar, nullptr, ctx->stream));
   }
-  if (ctx->nranks > 1) {
-    const char* err = nullptr;
-    const NcclApi* api = nccl_api(&err);
-    if (!api) return fail(TT_E_NCCL, "%s", err);
-    TT_TRY(nccl_check(api->AllReduce(ctx->d_scalar, ctx->d_scalar, 1, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream),
-                      "ncclAllReduce"));
-  }
+  TT_TRY(allreduce_sum(ctx, ctx->d_scalar, ctx->stream));
   TT_CUDA(cudaMemcpyAsync(energy, ctx->d_scalar, 8, cudaMemcpyDeviceToHost, ctx->stream));
   TT_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->last.c_blocks = tp->nunits;

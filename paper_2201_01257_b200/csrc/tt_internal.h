@@ -2,8 +2,10 @@
 // Not part of the ABI (include/tt.h is).  Citations as in tt.h.
 #pragma once
 
+#include <condition_variable>
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -91,6 +93,9 @@ struct tt_tis_s {
 
 struct tt_tensor_s {
   tt_ctx ctx = nullptr;
+  uint64_t seq = 0;                // creation index in its context (SPMD: same tensor, same seq on every rank)
+  tt_sim sim = nullptr;            // simulated-rank group of its context (registry entry), else nullptr
+  int32_t sim_rank = 0;
   int32_t order = 0;
   std::vector<tt_tis> dims;
   std::vector<int32_t> grid;       // ntiles per dim
@@ -122,6 +127,7 @@ struct tt_tensor_s {
   std::vector<int32_t> pv_lo, pv_hi, pv_owner;
   bool any_split = false;
   tt_tensor view_of = nullptr;     // sliced view (tt_tensor_view): blocks live in this tensor's storage
+  int32_t live_views = 0;          // views of this tensor not yet destroyed: its layout is frozen meanwhile
 
   int64_t ext0(int64_t b) const {
     int32_t c[TT_MAX_ORDER];
@@ -187,4 +193,39 @@ struct tt_ctx_s {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t comm_fork = nullptr, comm_done = nullptr;
   bool comm_pending = false;       // comm_done marks the last gather issued on comm_stream
+  // simulated ranks on one GPU (tt_ctx_create_sim): the group replacing the NCCL communicator
+  tt_sim sim = nullptr;
+  uint64_t tensor_seq = 0;         // next tensor creation index
+};
+
+// Simulated ranks: nranks contexts on ONE device, each driven by its
+// own host thread exactly as one process per GPU would be (SPMD).  Collectives: a host barrier over
+// the group plus CUDA events: the gather becomes one cudaMemcpyAsync (device to device) per run from
+// the peer's buffer, the all-reduce a fixed-rank-order sum of the ranks' partials.
+struct tt_sim_s {
+  int32_t nranks = 0, device = -1;
+  std::vector<tt_ctx> ctx;                        // registered contexts by rank
+  std::vector<cudaEvent_t> ready, done;           // per rank, recorded at the collective's entry / exit
+  double* d_part = nullptr;                       // [nranks] all-reduce staging (device)
+  std::map<uint64_t, std::vector<tt_tensor>> reg; // tensor seq -> handle per rank
+  std::mutex mu;
+  std::condition_variable cv;
+  int32_t arrived = 0;
+  uint64_t gen = 0;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+  tt_tensor peer(const tt_tensor_s* t, int32_t rank) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = reg.find(t->seq);
+    return it == reg.end() ? nullptr : it->second[rank];
+  }
 };

@@ -474,6 +474,19 @@ __global__ void set_kernel(const ElemParams p) {
   if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) x[sg.e1 - 1] = p.alpha;
 }
 
+// row index over the groups 0..n-2 (rows mode: group n-1 is contiguous in y) -> offset in y
+__device__ __forceinline__ int64_t y_row_offset(uint32_t r, const ElemDesc& d) {
+  int64_t off = 0;
+  for (int g = d.n - 2; g > 0; --g) {
+    const uint32_t q = fdiv(r, d.div[g]);
+    off += (int64_t)(r - q * d.div[g].d) * d.y_str[g];
+    r = q;
+  }
+  return off + (int64_t)r * d.y_str[0];
+}
+
+constexpr int kRowsPerWarp = 4;   // rows mode: rows of one warp in flight
+
 __device__ __forceinline__ double axpby(double alpha, double y, double beta, double x) {
   return (beta == 0.0) ? alpha * y : beta * x + alpha * y;
 }
@@ -527,6 +540,30 @@ __global__ void __launch_bounds__(kElemThreads) add_seg_kernel(const ElemParams 
       for (int64_t e : peel) {
         if (e < 0) continue;
         x[e] = axpby(alpha, y ? y[e] : 0.0, beta, beta != 0.0 ? x[e] : 0.0);
+      }
+    }
+  } else if (d.mode == kElemRows) {
+    // rows of L elements contiguous in both operands: one warp per row, the row's Y base decoded once
+    const int64_t L = d.div[d.n - 1].d;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = sg.e0 / L, r1 = (sg.e1 + L - 1) / L;
+    for (int64_t rb = r0 + (int64_t)warp * kRowsPerWarp; rb < r1; rb += (kElemThreads / 32) * kRowsPerWarp) {
+      int64_t yb[kRowsPerWarp];
+#pragma unroll
+      for (int u = 0; u < kRowsPerWarp; ++u) yb[u] = (rb + u < r1) ? y_row_offset((uint32_t)(rb + u), d) : 0;
+      for (int64_t k0 = 0; k0 < L; k0 += 32) {
+        double yv[kRowsPerWarp], xv[kRowsPerWarp];
+        bool ok[kRowsPerWarp];
+#pragma unroll
+        for (int u = 0; u < kRowsPerWarp; ++u) {
+          const int64_t k = k0 + lane, e = (rb + u) * L + k;
+          ok[u] = rb + u < r1 && k < L && e >= sg.e0 && e < sg.e1;
+          yv[u] = (ok[u] && y) ? y[yb[u] + k] : 0.0;
+          xv[u] = (ok[u] && beta != 0.0) ? x[e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerWarp; ++u)
+          if (ok[u]) x[(rb + u) * L + k0 + lane] = axpby(alpha, yv[u], beta, xv[u]);
       }
     }
   } else {
@@ -664,6 +701,27 @@ __global__ void __launch_bounds__(kElemThreads) scalar_seg_kernel(const ElemPara
     }
     if (threadIdx.x == 0 && es != sg.e0 && sg.e0 < sg.e1) s += x[sg.e0] * y[sg.e0];
     if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) s += x[sg.e1 - 1] * y[sg.e1 - 1];
+  } else if (d.mode == kElemRows) {
+    const int64_t L = d.div[d.n - 1].d;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = sg.e0 / L, r1 = (sg.e1 + L - 1) / L;
+    for (int64_t rb = r0 + (int64_t)warp * kRowsPerWarp; rb < r1; rb += (kElemThreads / 32) * kRowsPerWarp) {
+      int64_t yb[kRowsPerWarp];
+#pragma unroll
+      for (int u = 0; u < kRowsPerWarp; ++u) yb[u] = (rb + u < r1) ? y_row_offset((uint32_t)(rb + u), d) : 0;
+      for (int64_t k0 = 0; k0 < L; k0 += 32) {
+        double yv[kRowsPerWarp], xv[kRowsPerWarp];
+#pragma unroll
+        for (int u = 0; u < kRowsPerWarp; ++u) {
+          const int64_t k = k0 + lane, e = (rb + u) * L + k;
+          const bool ok = rb + u < r1 && k < L && e >= sg.e0 && e < sg.e1;
+          yv[u] = ok ? y[yb[u] + k] : 0.0;
+          xv[u] = ok ? x[e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerWarp; ++u) s += xv[u] * yv[u];
+      }
+    }
   } else {
     for (int64_t e0 = sg.e0 + threadIdx.x; e0 < sg.e1; e0 += kElemThreads * kElemUnroll) {
       double yv[kElemUnroll], xv[kElemUnroll];
@@ -728,6 +786,17 @@ cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t nt
   return cudaGetLastError();
 }
 int64_t scalar_scratch_elems(int64_t n) { return n > kFinalChunk ? (n + kFinalChunk - 1) / kFinalChunk : 0; }
+
+// simulated-rank all-reduce: out = part[0] + part[1] + ... in rank order
+__global__ void sum_slots_kernel(const double* __restrict__ part, int32_t n, double* __restrict__ out) {
+  double s = 0.0;
+  for (int32_t i = 0; i < n; ++i) s += part[i];
+  *out = s;
+}
+cudaError_t launch_sum_slots(const double* part, int32_t n, double* out, cudaStream_t s) {
+  sum_slots_kernel<<<1, 1, 0, s>>>(part, n, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, double* scratch,
                                cudaStream_t s) {

@@ -123,9 +123,10 @@ struct ElemDesc {
   int64_t g_str[TT_MAX_ORDER];          // global strides (fill; groups = dims)
 };
 
-// Element-op modes: contiguous (one group, y stride 1: vectorised), generic (multiply-high decode),
-// transpose (innermost x group strided in y: 32x32 shared-memory tiles, coalesced both ways).
-enum { kElemContig = 0, kElemGeneric = 1, kElemTranspose = 2 };
+// Element-op modes: contiguous (one group, y stride 1: vectorised), generic (multiply-high decode per
+// element), transpose (innermost x group strided in y: 32x32 shared-memory tiles, coalesced both
+// ways), rows (innermost x group contiguous in y too: one warp per row, decode once per row).
+enum { kElemContig = 0, kElemGeneric = 1, kElemTranspose = 2, kElemRows = 3 };
 
 // Transpose-mode work: one 32x32 tile of one block, bases precomputed on the host.  Element (ix, iy)
 // of the tile (ix along X's contiguous group gx, iy along Y's contiguous group gy) is
@@ -160,6 +161,7 @@ cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t nt
 // out = alpha * sum(partials[0, n)) in a fixed order; with scratch (scalar_scratch_elems(n) doubles)
 // large n is summed in two stages
 int64_t scalar_scratch_elems(int64_t n);
+cudaError_t launch_sum_slots(const double* part, int32_t n, double* out, cudaStream_t s);
 cudaError_t launch_scalar_final(const double* partials, int64_t n, double alpha, double* out, double* scratch,
                                 cudaStream_t s);
 

@@ -13,6 +13,8 @@
 // the context stream with an event, joined back with one event per stream: one synchronisation point
 // per level).  With nranks > 1 the ops of a level run in queue order on the context stream so that
 // every rank issues its NCCL calls in the same order (SPMD).
+#include <algorithm>
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -22,6 +24,28 @@ namespace {
 
 enum OpKind { kSet, kAdd, kContract, kScalar, kCholesky };
 
+// A resource an op reads or writes: a tensor's storage (a view is its root tensor: views share the
+// parent's storage, so a view and its parent -- or two views of one parent -- always conflict), or a
+// caller workspace byte range (the Cholesky contraction's W batches are written there).
+struct Res {
+  const void* id;            // root tensor handle, or nullptr for a workspace range
+  uintptr_t lo = 0, hi = 0;  // workspace byte range [lo, hi)
+};
+
+Res tensor_res(tt_tensor t) {
+  while (t && t->view_of) t = t->view_of;
+  return {t, 0, 0};
+}
+
+Res mem_res(const void* p, int64_t bytes) {
+  return {nullptr, (uintptr_t)p, (uintptr_t)p + (uintptr_t)std::max<int64_t>(bytes, 0)};
+}
+
+bool same(const Res& a, const Res& b) {
+  if (a.id || b.id) return a.id == b.id;
+  return a.lo < b.hi && b.lo < a.hi;
+}
+
 struct SchedOp {
   OpKind kind;
   tt_tensor C = nullptr, A = nullptr, B = nullptr;
@@ -30,19 +54,19 @@ struct SchedOp {
   double* result = nullptr;
   void* ws = nullptr;
   int64_t ws_elems = 0;
-  std::vector<tt_tensor> reads, writes;
+  std::vector<Res> reads, writes;
 };
 
-bool has(const std::vector<tt_tensor>& v, tt_tensor t) {
-  for (tt_tensor u : v)
-    if (u == t) return true;
+bool has(const std::vector<Res>& v, const Res& t) {
+  for (const Res& u : v)
+    if (same(u, t)) return true;
   return false;
 }
 
 bool conflicts(const SchedOp& x, const SchedOp& y) {
-  for (tt_tensor w : x.writes)
+  for (const Res& w : x.writes)
     if (has(y.writes, w) || has(y.reads, w)) return true;
-  for (tt_tensor w : y.writes)
+  for (const Res& w : y.writes)
     if (has(x.reads, w)) return true;
   return false;
 }
@@ -135,7 +159,7 @@ tt_status tt_sched_set(tt_sched s, tt_tensor C, double alpha) {
   op.kind = kSet;
   op.C = C;
   op.alpha = alpha;
-  op.writes = {C};
+  op.writes = {tensor_res(C)};
   return push(s, std::move(op));
 }
 
@@ -150,9 +174,9 @@ tt_status tt_sched_add(tt_sched s, tt_tensor C, const char* cl, double beta, dou
   op.al = al;
   op.alpha = alpha;
   op.beta = beta;
-  op.writes = {C};
-  op.reads = {A};
-  if (beta != 0.0) op.reads.push_back(C);
+  op.writes = {tensor_res(C)};
+  op.reads = {tensor_res(A)};
+  if (beta != 0.0) op.reads.push_back(tensor_res(C));
   return push(s, std::move(op));
 }
 
@@ -169,9 +193,9 @@ tt_status tt_sched_contract(tt_sched s, tt_tensor C, const char* cl, double beta
   op.bl = bl;
   op.alpha = alpha;
   op.beta = beta;
-  op.writes = {C};
-  op.reads = {A, B};
-  if (beta != 0.0) op.reads.push_back(C);
+  op.writes = {tensor_res(C)};
+  op.reads = {tensor_res(A), tensor_res(B)};
+  if (beta != 0.0) op.reads.push_back(tensor_res(C));
   return push(s, std::move(op));
 }
 
@@ -191,9 +215,9 @@ tt_status tt_sched_contract_cholesky(tt_sched s, tt_tensor C, const char* cl, do
   op.beta = beta;
   op.ws = workspace;
   op.ws_elems = ws_elems;
-  op.writes = {C};
-  op.reads = {X, B};
-  if (beta != 0.0) op.reads.push_back(C);
+  op.writes = {tensor_res(C), mem_res(workspace, ws_elems * (int64_t)sizeof(double))};
+  op.reads = {tensor_res(X), tensor_res(B)};
+  if (beta != 0.0) op.reads.push_back(tensor_res(C));
   return push(s, std::move(op));
 }
 
@@ -208,7 +232,7 @@ tt_status tt_sched_scalar(tt_sched s, double alpha, tt_tensor A, const char* al,
   op.bl = bl;
   op.alpha = alpha;
   op.result = result;
-  op.reads = {A, B};
+  op.reads = {tensor_res(A), tensor_res(B)};
   return push(s, std::move(op));
 }
 

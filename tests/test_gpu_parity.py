@@ -519,14 +519,18 @@ def _cholesky_problem(O_, V_, tO, tV, NL, tL, spin):
 
 
 @pytest.mark.parametrize("spin,ws_rows,mode", [(True, 1, "bh"), (True, 100, "bh"), (False, 2, "bh"),
-                                                (True, 1, "env"), (False, 2, "env"), (True, 3, "auto")])
+                                                (True, 1, "env"), (False, 2, "env"), (True, 3, "auto"),
+                                                (True, 2, "densex")])
 def test_contract_cholesky(env, spin, ws_rows, mode):
     """Implicit Eq. cc12 operand (NEXT-1): R(abij) = beta*R + alpha*sum V(abcd) T(cdij) with V built
     batch by batch from X in a small workspace == oracle with V formed explicitly.  mode "bh": the
     workspace holds the r_t <= s_t half of Bm = T - T(c<->d); "env"/"auto": the two-pass consume
-    (forced, or because the workspace holds only W rows)."""
+    (forced, or because the workspace holds only W rows); "densex": alpha/beta spaces with a DENSE X map
+    (the W / V block maps must follow X's actual map, not the tiles' spins: ADVICE r1)."""
     tt, torch = env
     pb = _cholesky_problem(8, 12, 2, 3, 10, 5, spin) if spin else _cholesky_problem(5, 9, 3, 4, 7, 4, False)
+    if mode == "densex":
+        pb.tensors["X"] = TensorSpec("acL", None)
     if mode == "env":
         os.environ["TT_CHOL_TWO_PASS"] = "1"
     ctx = new_ctx(tt, torch)
@@ -539,6 +543,8 @@ def test_contract_cholesky(env, spin, ws_rows, mode):
     tv = max(np.diff(P["X"].dims[0].offsets))
     row = tv ** 4 * P["X"].dims[0].ntiles ** 2 + 64
     bm = 0 if mode == "auto" else P["T"].packed_elems + 32
+    if mode == "densex":
+        row *= 4
     ws = torch.empty(int(bm + ws_rows * row), dtype=torch.float64, device="cuda")
     for beta in (1.0, 0.0):
         tt.contract_cholesky(ctx, P["R"], "abij", beta, 0.5, P["X"], "abcd", P["T"], "cdij", ws)

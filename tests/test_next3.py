@@ -254,3 +254,22 @@ def test_views_gpu_parity(gpu):
     cs[...] = O.add(cs, "ia", O.slice_of(DA, [(0, 30), sec]), "ia", -2.0, 1.0)
     assert np.array_equal(got[:, :16], DC[:, :16])
     assert np.abs(got - ref).max() / np.abs(ref).max() <= TOL
+
+
+def test_parent_layout_frozen_while_views_live(tt):
+    """A view captures its parent's block map, offsets and owners (R29): while it lives, ownership /
+    compact / partition changes of the parent are refused (TT_E_STATE) instead of leaving the view
+    stale; after the view is destroyed they succeed."""
+    ctx = tt.Context(device=-1, rank=0, nranks=2)
+    M, K = tt.IndexSpace(30), tt.IndexSpace(20, [(0, 10), (10, 20)], names=["first", "second"])
+    tM, tK = tt.TiledIndexSpace(M, sizes=[10, 20]), tt.TiledIndexSpace(K, 5)
+    A = tt.Tensor(ctx, [tM, tK])
+    V = A.view([tM, tK("first")])
+    for fn in (lambda: A.set_owner([1] * A.nblocks), lambda: A.set_compact(True),
+               lambda: A.set_parts([(0, 0, 5, 0), (0, 5, 10, 1)])):
+        with pytest.raises(tt.TTError) as e:
+            fn()
+        assert e.value.name == "TT_E_STATE"
+    V.close()
+    A.set_owner([1] * A.nblocks)
+    assert list(A.owner) == [1] * A.nblocks

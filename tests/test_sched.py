@@ -201,3 +201,39 @@ def test_sched_graph_replay_bitwise():
         ctx.sync()
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2]
+
+
+def test_views_conflict_with_their_parent():
+    """A view shares its parent's storage (R29): an op writing a view conflicts with ops reading or
+    writing the parent or another view of it (handles alone missed this)."""
+    ctx = tt.Context(device=-1)
+    sp = tt.IndexSpace(8, [(0, 4), (4, 8)], [1, -1])
+    t4 = tt.TiledIndexSpace(sp, 4)
+    T, U, W = tt.Tensor(ctx, [t4, t4]), tt.Tensor(ctx, [t4, t4]), tt.Tensor(ctx, [t4, t4])
+    first, second = t4(0), t4(1)
+    V1 = T.view([first, t4])
+    V2 = T.view([second, t4])
+    s = tt.Scheduler(ctx)
+    s.add(V1, "ij", 0.0, 1.0, U.view([first, t4]), "ij")   # writes T (through V1)
+    s.add(W, "ij", 0.0, 1.0, T, "ij")                       # reads the parent
+    s.add(V2, "ij", 0.0, 1.0, U.view([second, t4]), "ij")  # writes T again (other view)
+    s.scalar(1.0, U, "ij", W, "ij")                         # unrelated to T: reads W (written at level 1)
+    assert s.levels() == ([0, 1, 2, 2], 3)
+
+
+def test_cholesky_workspace_is_a_written_resource():
+    """Two implicit-operand contractions on one workspace never share a level (the workspace holds
+    each one's W batches); on disjoint workspaces they may."""
+    import torch
+    ctx = tt.Context(device=-1)
+    so, sv, sl = tt.IndexSpace(4), tt.IndexSpace(6), tt.IndexSpace(5)
+    to, tv, tl = tt.TiledIndexSpace(so, 2), tt.TiledIndexSpace(sv, 3), tt.TiledIndexSpace(sl, 5)
+    X = tt.Tensor(ctx, [tv, tv, tl])
+    Tt = tt.Tensor(ctx, [tv, tv, to, to])
+    R1, R2 = tt.Tensor(ctx, [tv, tv, to, to]), tt.Tensor(ctx, [tv, tv, to, to])
+    ws = torch.empty(1000, dtype=torch.float64)
+    for (o1, o2), expect in (((0, 0), [0, 1]), ((0, 500), [0, 0])):
+        s = tt.Scheduler(ctx)
+        s.contract_cholesky(R1, "abij", 0.0, 1.0, X, "abcd", Tt, "cdij", ws[o1:o1 + 500])
+        s.contract_cholesky(R2, "abij", 0.0, 1.0, X, "abcd", Tt, "cdij", ws[o2:o2 + 500])
+        assert s.levels()[0] == expect

@@ -378,3 +378,26 @@ def test_triples_argument_errors():
     with pytest.raises(tt.TTError) as e:
         tt.triples_energy(ctx, *args, None, fake, fake, ws_elems=info["ws_elems"])
     assert e.value.name == "TT_E_ARG"
+
+
+def test_triples_rejects_maps_outside_the_spin_rule():
+    """The kernel prunes units and m / e ranges by the index spins (R28): on alpha/beta spaces an input
+    with a dense block map (blocks outside the R7 spin map) must be refused, not mis-summed (ADVICE r1);
+    the spin maps themselves pass, and dense maps on spaces without spin pass."""
+    import paper_2201_01257_b200 as tt
+    ctx = tt.Context(device=-1)
+    _, _, to, tv = _spaces(tt, 6, 12, 3, 3, True)
+    dims = {"o": to, "v": tv}
+    spin = {n: tt.Tensor(ctx, [dims[c] for c in d], spin=sp) for n, d, sp, _ in TRIPLES_INPUTS}
+    args = [spin[n] for n in ("T1", "T2", "Vooov", "Vvovv", "Voovv")]
+    tt.triples_energy(ctx, *args)                       # query mode: spin maps accepted
+    for k, (n, d, sp, _) in enumerate(TRIPLES_INPUTS):
+        bad = list(args)
+        bad[k] = tt.Tensor(ctx, [dims[c] for c in d])   # dense map on spin spaces
+        with pytest.raises(tt.TTError) as e:
+            tt.triples_energy(ctx, *bad)
+        assert e.value.name == "TT_E_UNSUPPORTED" and n in e.value.args[0]
+    _, _, to2, tv2 = _spaces(tt, 6, 12, 3, 3, False)
+    d2 = {"o": to2, "v": tv2}
+    dense = [tt.Tensor(ctx, [d2[c] for c in d]) for n, d, sp, _ in TRIPLES_INPUTS]
+    tt.triples_energy(ctx, *dense)

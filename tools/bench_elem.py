@@ -44,8 +44,10 @@ def main():
         ("add R(abij) = R + T2(abij) (identity)", lambda: tt.add(ctx, R, "abij", 1.0, 0.5, T2, "abij"), "tt_add", 24 * n),
         ("add R(abij) = R + Rt(ijab) (transpose)", lambda: tt.add(ctx, R, "abij", 1.0, 0.5, Rt, "ijab"), "tt_add", 24 * n),
         ("add R(abij) = T2p(aibj) (beta=0, 4-d permutation)", lambda: tt.add(ctx, R, "abij", 0.0, 1.0, T2p, "aibj"), "tt_add", 16 * n),
+        ("add R(abij) = R - T2(baij) (antisymmetrizer, rows of 900)", lambda: tt.add(ctx, R, "abij", 1.0, -1.0, T2, "baij"), "tt_add", 24 * n),
         ("scalar T2(abij) . R(abij)", lambda: tt.contract_scalar(ctx, 0.25, T2, "abij", R, "abij"), "tt_scalar_partials", 16 * n),
         ("scalar Rt(ijab) . R(abij) (permuted)", lambda: tt.contract_scalar(ctx, 0.25, Rt, "ijab", R, "abij"), "tt_scalar_partials", 16 * n),
+        ("scalar T2p(aibj) . R(abij) (4-d permutation)", lambda: tt.contract_scalar(ctx, 0.25, T2p, "aibj", R, "abij"), "tt_scalar_partials", 16 * n),
     ]
     out = []
     for name, fn, kern, nbytes in ops:
