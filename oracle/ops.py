@@ -11,8 +11,11 @@ definition:
 * scalar contraction (order-0 result, P534-536 energy as a sum of contributions):
       s = alpha * sum_x A[x_A] * B[x_B]
 
-The loops are in oracle.c (sequential FP64 sums, reading R12).  numpy is used only to move data
-(transpose/copy = memory order) and for masks; no numpy reduction touches a result.
+The loops of contract/add/set/scalar are in oracle.c (sequential FP64 sums, reading R12); there numpy
+only moves data (transpose/copy = memory order) and builds masks.  Library reductions appear only in
+the sampled checks for sizes the loops cannot reach, each named in its docstring as a library
+primitive and pinned in tests/test_oracle_pins.py: cholesky_v_row (BLAS matrix products over L),
+ladder_sample (numpy.sum), freivalds (numpy.einsum).
 """
 from __future__ import annotations
 
