@@ -12,10 +12,10 @@
  *   - Handles (tt_ctx, tt_is, tt_tis, tt_tensor) are opaque, created and destroyed by the library.
  *     They are immutable metadata with shallow-copy semantics (P212: "tensors in terms of handles ...
  *     any assignment done on tensor objects will be a shallow copy").
- *   - Tensor DATA is never allocated by the library: the caller binds device memory (e.g. a torch
- *     tensor) with tt_tensor_bind and keeps ownership; the library never frees it.  Small internal
- *     metadata (block maps, task lists, plans) is allocated by the library on the context's device
- *     and freed by tt_ctx_destroy.
+ *   - The library never allocates device memory on the execute path.  Tensor DATA is bound by the
+ *     caller (e.g. a torch tensor, tt_tensor_bind); internal metadata (block maps, task lists, plans)
+ *     and scratch (split-K and scalar partials) live in ONE caller-provided device workspace per
+ *     context (tt_workspace_bind).  The caller keeps ownership of both; the library never frees them.
  *   - Execution is SPMD (P212, "single program multiple data"): with nranks > 1 every rank makes
  *     the same sequence of calls with identical metadata.  Compute calls are asynchronous on the
  *     context's CUDA stream; argument/validation errors are returned synchronously; CUDA and NCCL
@@ -46,7 +46,9 @@ enum {
   TT_E_CUDA = -8,       /* CUDA runtime error (message in tt_last_error)                             */
   TT_E_NCCL = -9,       /* NCCL error                                                                */
   TT_E_STATE = -10,     /* call not valid in this state (e.g. device call on a host-only context)    */
-  TT_E_UNSUPPORTED = -11/* shape outside the supported envelope (e.g. order > TT_MAX_ORDER)          */
+  TT_E_UNSUPPORTED = -11,/* shape outside the supported envelope (e.g. order > TT_MAX_ORDER)         */
+  TT_E_WORKSPACE = -12  /* no device workspace bound, or it cannot hold this call's metadata even     */
+                        /* after evicting every unused cached plan (tt_workspace_bytes says how much) */
 };
 
 enum { TT_MAX_ORDER = 8 };          /* maximum tensor order                                        */
@@ -118,6 +120,29 @@ tt_status tt_last_stats(tt_ctx ctx, tt_stats* out);
 tt_status tt_launch_count(tt_ctx ctx, int64_t* out);
 /* Blocks until all work queued on the context stream has finished; surfaces deferred errors. */
 tt_status tt_sync(tt_ctx ctx);
+/* Device workspace (P182-186: the ExecutionContext carries the memory manager).
+ *   tt_workspace_bind(ctx, dev_ptr, bytes): binds caller-owned device memory (256-byte aligned,
+ *     on the context's device; not owned, never freed by the library) from which every piece of
+ *     library metadata and scratch of this context is carved.  Every device call needs a bound
+ *     workspace (TT_E_WORKSPACE otherwise).  Re-binding (e.g. a larger buffer) first synchronises the
+ *     device, drops every cached plan and every tensor's device metadata (rebuilt on next use); it
+ *     is refused (TT_E_STATE) while a scheduler holds a captured graph of this context.  The old
+ *     buffer may be freed by the caller once the call returns.  Cached plans that no running call
+ *     holds are evicted least-recently-used when the workspace is full (after a device
+ *     synchronisation: their regions may still be read by queued kernels).
+ *   tt_workspace_bytes(ctx, &bytes): the size this context's workload needs: the high-water mark of
+ *     live workspace bytes so far, raised to what a call that failed with TT_E_WORKSPACE needed
+ *     (at least 1 MiB).  A call returns TT_E_WORKSPACE before it modifies any tensor, except
+ *     tt_contract_cholesky, which builds its per-batch plans while it runs: give it room for all
+ *     of them (tt_sched_* prepares every plan before the first launch).
+ *   tt_workspace_info(ctx, &bound, &live, &high): bound size, bytes in use, high-water mark.
+ *   tt_ctx_set_plan_limit(ctx, n): cached plans kept at most (default 16384; n >= 1); tt_ctx_clear_plans
+ *     drops every cached plan that no running call or captured graph holds. */
+tt_status tt_workspace_bind(tt_ctx ctx, void* dev_ptr, int64_t bytes);
+tt_status tt_workspace_bytes(tt_ctx ctx, int64_t* bytes);
+tt_status tt_workspace_info(tt_ctx ctx, int64_t* bound, int64_t* live, int64_t* high);
+tt_status tt_ctx_set_plan_limit(tt_ctx ctx, int64_t max_plans);
+tt_status tt_ctx_clear_plans(tt_ctx ctx);
 
 /* ------------------------------------------------------------------------------------------------
  * IndexSpace (P116-122, Fig. 2: IndexSpace N{range(100)}).
@@ -407,6 +432,13 @@ tt_status tt_partition_split(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tens
  *   cost  [number of non-zero C blocks] non-negative cost of each non-zero C block, in block-id
  *         order (host pointer, read only).  TT_E_ARG on NULL or a negative cost. */
 tt_status tt_partition_split_cost(tt_ctx ctx, tt_tensor C, const int64_t* cost, uint32_t group_mask);
+/* R24b on the executed cost of the implicit-operand ladder C(..p..q..) += V(p,q,r,s) B(..r..s..)
+ * (tt_contract_cholesky, Eq. cc12; same arguments and checks): per non-zero C block, the GEMM FLOPs of
+ * its tasks over W's block map (W(pqrs) = sum_L X(prL) X(qsL), map from X's block map, R19b) plus the
+ * W formation of its (p_t, q_t) row, 2 N_L |p||q| sum over W's (r_t, s_t) blocks of |r||s|, shared
+ * evenly (integer division) by the row's non-zero C blocks; then as tt_partition_split_cost. */
+tt_status tt_partition_split_cholesky(tt_ctx ctx, tt_tensor C, const char* c_lbl, tt_tensor X, const char* v_lbl,
+                                      tt_tensor B, const char* b_lbl, uint32_t group_mask);
 
 /* Input-tile gather plan of this rank for tt_contract (host metadata; for tests and reports).
  * recv[5*i .. 5*i+4] = (operand 0=A/1=B, block id, source rank, e0, e1): element range [e0, e1) of

@@ -369,6 +369,43 @@ def partition_split(C: Tensor, cost: Sequence[int], cblocks: Sequence[int], grou
     return out
 
 
+def cholesky_ladder_cost(C: Tensor, c_lbl: str, X: Tensor, v_lbl: str, B: Tensor, b_lbl: str):
+    """Executed cost per non-zero C block of the implicit-operand ladder C += V(p,q,r,s) B (Eq. cc12,
+    P312-318): the FLOPs of the block's tasks against the Coulomb operand
+    W(p,q,r,s) = sum_L X(p,r,L) X(q,s,L), whose block (p_t,q_t,r_t,s_t) is non-zero iff X holds a
+    non-zero block at (p_t,r_t,.) and at (q_t,s_t,.) (reading R19b), plus the formation of W's
+    (p_t,q_t) row -- 2 N_L |p_t||q_t| sum over its non-zero (r_t,s_t) of |r_t||s_t| -- split evenly
+    (floor) over the row's non-zero C blocks.  Returns (cblocks, cost) in task_list order."""
+    p, q, r, s = v_lbl
+    dims = {x: d for T, lbl in ((C, c_lbl), (B, b_lbl)) for x, d in zip(lbl, T.dims)}
+    xpair = set()
+    for xb in range(X.nblocks()):
+        if X.nz[xb]:
+            co = X.block_coords(xb)
+            xpair.add((co[0], co[1]))
+    vd = [dims[p], dims[q], dims[r], dims[s]]
+    wnz = [1 if ((a, c) in xpair and (b, d) in xpair) else 0
+           for a in range(vd[0].ntiles) for b in range(vd[1].ntiles)
+           for c in range(vd[2].ntiles) for d in range(vd[3].ntiles)]
+    W = tensor_explicit(vd, wnz)
+    cblocks, _, _, _, cost = task_list(C, c_lbl, W, v_lbl, B, b_lbl)
+    NL = X.dims[2].space.extent
+    rows = {}
+    for cb in cblocks:
+        co = C.block_coords(cb)
+        key = (co[c_lbl.index(p)], co[c_lbl.index(q)])
+        rows[key] = rows.get(key, 0) + 1
+    out = []
+    for cb, c in zip(cblocks, cost):
+        co = C.block_coords(cb)
+        a, b = co[c_lbl.index(p)], co[c_lbl.index(q)]
+        w = sum(vd[2].size(c2) * vd[3].size(d2) for c2 in range(vd[2].ntiles) for d2 in range(vd[3].ntiles)
+                if (a, c2) in xpair and (b, d2) in xpair)
+        build = 2 * NL * vd[0].size(a) * vd[1].size(b) * w
+        out.append(c + build // rows[(a, b)])
+    return cblocks, out
+
+
 # ----------------------------------------------------------------------------- NEXT-3 factorization
 
 def contract3_plan(C: Tensor, c_lbl: str, A: Tensor, a_lbl: str, B: Tensor, b_lbl: str, D: Tensor, d_lbl: str):

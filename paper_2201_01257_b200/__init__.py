@@ -29,7 +29,11 @@ _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
 TT_OK = 0
 ERRORS = {-1: "TT_E_ARG", -2: "TT_E_COVERAGE", -3: "TT_E_LABEL", -4: "TT_E_TILING", -5: "TT_E_ZERO_BLOCK",
           -6: "TT_E_UNBOUND", -7: "TT_E_OOM", -8: "TT_E_CUDA", -9: "TT_E_NCCL", -10: "TT_E_STATE",
-          -11: "TT_E_UNSUPPORTED"}
+          -11: "TT_E_UNSUPPORTED", -12: "TT_E_WORKSPACE"}
+TT_E_WORKSPACE = -12
+# default device workspace per context (tt_workspace_bind): plan metadata and scratch; cached plans are
+# evicted least-recently-used when it is full.  Override with Context(workspace_bytes=...) or TT_WORKSPACE_MB.
+DEFAULT_WORKSPACE_BYTES = int(os.environ.get("TT_WORKSPACE_MB", "256")) << 20
 TT_REPLICATED = -2
 TT_SPLIT = -3
 KIND_UNIFORM, KIND_INTEGER = 0, 1
@@ -78,6 +82,11 @@ _SIGS = {
     "tt_last_stats": [_vp, _P(Stats)],
     "tt_launch_count": [_vp, _P(_i64)],
     "tt_sync": [_vp],
+    "tt_workspace_bind": [_vp, _vp, _i64],
+    "tt_workspace_bytes": [_vp, _P(_i64)],
+    "tt_workspace_info": [_vp, _P(_i64), _P(_i64), _P(_i64)],
+    "tt_ctx_set_plan_limit": [_vp, _i64],
+    "tt_ctx_clear_plans": [_vp],
     "tt_is_create": [_i64, _i32, _vp, _vp, _P(_vp)],
     "tt_is_destroy": [_vp],
     "tt_tis_fixed": [_vp, _i64, _P(_vp)],
@@ -114,6 +123,7 @@ _SIGS = {
     "tt_partition_lpt": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32, _vp],
     "tt_partition_split": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32],
     "tt_partition_split_cost": [_vp, _vp, _vp, _u32],
+    "tt_partition_split_cholesky": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _u32],
     "tt_tensor_set_compact": [_vp, _i32],
     "tt_tensor_storage": [_vp, _P(_i64), _P(_P(_i64))],
     "tt_gather_plan": [_vp, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _P(_i64), _vp,
@@ -203,10 +213,13 @@ class SimGroup:
 
 class Context:
     """ExecutionContext (P178-188).  device=-1 gives a host-only context (metadata only); ``sim`` = a
-    SimGroup: simulated rank ``rank`` of that group (device and nranks come from the group)."""
+    SimGroup: simulated rank ``rank`` of that group (device and nranks come from the group).  A device
+    context gets its workspace (tt_workspace_bind) from torch: ``workspace_bytes`` (default
+    DEFAULT_WORKSPACE_BYTES); ``bind_workspace`` re-binds a larger one."""
 
     def __init__(self, device: int = 0, stream: int = 0, rank: int = 0, nranks: int = 1,
-                 nccl_id: Optional[bytes] = None, sim: Optional[SimGroup] = None):
+                 nccl_id: Optional[bytes] = None, sim: Optional[SimGroup] = None,
+                 workspace_bytes: Optional[int] = None):
         h = _vp()
         if sim is not None:
             _check(_lib.tt_ctx_create_sim(_vp(stream or 0), rank, sim.h, ctypes.byref(h)))
@@ -215,11 +228,39 @@ class Context:
             idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
             _check(_lib.tt_ctx_create(device, _vp(stream or 0), rank, nranks, idbuf, ctypes.byref(h)))
         self.h, self.device, self.rank, self.nranks, self.sim = h, device, rank, nranks, sim
+        self._ws = None
+        if device >= 0:
+            self.bind_workspace(workspace_bytes or DEFAULT_WORKSPACE_BYTES)
+
+    def bind_workspace(self, nbytes: int):
+        """tt_workspace_bind with a fresh torch buffer of ``nbytes`` on the context's device (the old
+        buffer is released after the library has re-bound; it synchronises the device first)."""
+        import torch
+        buf = torch.empty(int(nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
+        _check(_lib.tt_workspace_bind(self.h, _vp(buf.data_ptr()), int(nbytes)))
+        self._ws = buf
+
+    def workspace_bytes(self) -> int:
+        n = _i64()
+        _check(_lib.tt_workspace_bytes(self.h, ctypes.byref(n)))
+        return n.value
+
+    def workspace_info(self) -> dict:
+        b, l, h = _i64(), _i64(), _i64()
+        _check(_lib.tt_workspace_info(self.h, ctypes.byref(b), ctypes.byref(l), ctypes.byref(h)))
+        return {"bound": b.value, "live": l.value, "high": h.value}
+
+    def set_plan_limit(self, n: int):
+        _check(_lib.tt_ctx_set_plan_limit(self.h, int(n)))
+
+    def clear_plans(self):
+        _check(_lib.tt_ctx_clear_plans(self.h))
 
     def close(self):
         if self.h:
             _check(_lib.tt_ctx_destroy(self.h))
             self.h = None
+            self._ws = None
 
     def __del__(self):  # pragma: no cover
         try:
@@ -539,6 +580,14 @@ def partition_split_cost(ctx: Context, C: Tensor, cost, group_dims: Sequence[int
         raise ValueError("cost needs one entry per non-zero block of C")
     mask = sum(1 << d for d in group_dims)
     _check(_lib.tt_partition_split_cost(ctx.h, C.h, _ptr(c), mask))
+    C._refresh()
+
+
+def partition_split_cholesky(ctx: Context, C: Tensor, c_lbl: str, X: Tensor, v_lbl: str, B: Tensor, b_lbl: str,
+                             group_dims: Sequence[int] = ()):
+    """tt_partition_split on the executed cost of the implicit-operand ladder (tt_contract_cholesky)."""
+    mask = sum(1 << d for d in group_dims)
+    _check(_lib.tt_partition_split_cholesky(ctx.h, C.h, _b(c_lbl), X.h, _b(v_lbl), B.h, _b(b_lbl), mask))
     C._refresh()
 
 

@@ -70,28 +70,6 @@ TERMS = [
 ]
 
 
-def cholesky_ladder_costs(tt, R, B, tv, NL: int) -> np.ndarray:
-    """Executed cost of R(abij) += V(abcd) B(cdij) per non-zero R block with the implicit V
-    (tt_contract_cholesky): the GEMMs over W's block map (W(pqrs) = sum_L X(prL) X(qsL) is non-zero
-    when spin p = spin r and spin q = spin s) against B, plus the W formation of the (a,b) row
-    (2 N_L |a||b| sum_{c,d in W's map} |c||d|), shared evenly by the row's blocks.  For
-    tt.partition_split_cost with group_dims (0, 1)."""
-    sp, n = tv.spin, tv.ntiles
-    sz = np.diff(tv.offsets)
-    wnz = (sp[:, None, None, None] == sp[None, None, :, None]) & (sp[None, :, None, None] == sp[None, None, None, :])
-    ctx0 = tt.Context(device=-1)
-    W = tt.Tensor(ctx0, [tv, tv, tv, tv], nz=wnz.astype(np.uint8).reshape(-1))
-    tl = tt.task_list(ctx0, R, "abij", W, "abcd", B, "cdij")
-    cost = tl["cost"].astype(np.int64)
-    coords = np.stack(np.unravel_index(tl["cblk"], R.grid), axis=1)
-    wsum = np.einsum("abcd,c,d->ab", wnz.astype(np.int64), sz, sz)
-    build = 2 * NL * sz[:, None] * sz[None, :] * wsum
-    ab = coords[:, 0] * n + coords[:, 1]
-    cnt = np.bincount(ab, minlength=n * n)
-    share = build.reshape(-1) // np.maximum(cnt, 1)
-    return cost + share[ab]
-
-
 class CCSDIteration:
     """Builds the tensors of the iteration on a libtt context and runs it through a Scheduler.
 
@@ -134,15 +112,12 @@ class CCSDIteration:
         for name in ("foo", "fvv", "T1", "T2", "Voovv", "tau", "Fo", "Fov", "R1", "X", "Voooo"):
             t = T[name]
             t.set_owner(np.where(t.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
-        tt.partition_split_cost(self.ctx, T["R2"], self.ladder_costs(), group_dims=(0, 1))
+        tt.partition_split_cholesky(self.ctx, T["R2"], "abij", T["X"], "abcd", T["tau"], "cdij", group_dims=(0, 1))
         T["R2"].set_compact(True)       # R2 is only written: each rank stores just its rows
         tt.partition_split(self.ctx, T["Wr"], "kbcj", T["T2"], "dblj", T["Voovv"], "cdkl")
         tt.partition_split(self.ctx, T["Z"], "abij", T["T2"], "acik", T["Wr"], "kbcj")
         tt.partition_split(self.ctx, T["Wo"], "klij", T["Voovv"], "cdkl", T["tau"], "cdij")
         tt.partition_split(self.ctx, T["Fv"], "ae", T["T2"], "afmn", T["Voovv"], "efmn")
-
-    def ladder_costs(self) -> np.ndarray:
-        return cholesky_ladder_costs(self.tt, self.T["R2"], self.T["tau"], self.tis["v"], self.spaces[2].extent)
 
     def reset_inputs(self):
         for name, (cls, spin, tag) in TENSORS.items():

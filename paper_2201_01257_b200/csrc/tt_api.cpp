@@ -73,15 +73,110 @@ tt_status need_device(tt_ctx ctx) {
   return TT_OK;
 }
 
-template <class T>
-tt_status dev_alloc(tt_ctx ctx, T** p, size_t n) {
-  *p = nullptr;
-  if (n == 0) n = 1;
-  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
-  if (e != cudaSuccess) return fail(TT_E_OOM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
-  ctx->dev_allocs.push_back(*p);
+// every device compute call: the context has a workspace (scratch lives there)
+tt_status need_ws(tt_ctx ctx) {
+  TT_TRY(need_device(ctx));
+  if (!ctx->ws.base || !ctx->d_scalar)
+    return fail(TT_E_WORKSPACE, "no device workspace bound (tt_workspace_bind; tt_workspace_bytes says how much)");
   return TT_OK;
 }
+
+template <class T>
+tt_status dev_alloc(tt_ctx ctx, DevMem& m, T** p, size_t n) {
+  void* v = nullptr;
+  *p = nullptr;
+  TT_TRY(ws_alloc(ctx, m, (int64_t)(std::max<size_t>(n, 1) * sizeof(T)), &v));
+  *p = (T*)v;
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// plan cache: LRU over entries that only the cache references (tt_internal.h "Device workspace")
+
+void plan_put(tt_ctx ctx, const std::string& key, std::shared_ptr<void> p) {
+  if (ctx->plan_sink) ctx->plan_sink->push_back(p);
+  auto& e = ctx->plans[key];
+  e.p = std::move(p);
+  e.tick = ++ctx->plan_tick;
+  if ((int64_t)ctx->plans.size() > ctx->plan_limit) {   // host-side bound on the cache
+    auto victim = ctx->plans.end();
+    for (auto it = ctx->plans.begin(); it != ctx->plans.end(); ++it)
+      if (it->second.p.use_count() == 1 && (victim == ctx->plans.end() || it->second.tick < victim->second.tick))
+        victim = it;
+    if (victim != ctx->plans.end()) ctx->plans.erase(victim);
+  }
+}
+
+// evicts the least-recently-used plan nobody else holds; false if there is none
+bool evict_one(tt_ctx ctx) {
+  auto victim = ctx->plans.end();
+  for (auto it = ctx->plans.begin(); it != ctx->plans.end(); ++it)
+    if (it->second.p.use_count() == 1 && (victim == ctx->plans.end() || it->second.tick < victim->second.tick))
+      victim = it;
+  if (victim == ctx->plans.end()) return false;
+  ctx->plans.erase(victim);   // its DevMem retires its regions
+  return true;
+}
+
+// retired regions become free once every queued kernel that may read them has finished
+tt_status drain_retired(tt_ctx ctx) {
+  if (ctx->ws.retired.empty()) return TT_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+    return fail(TT_E_WORKSPACE, "workspace full while a CUDA graph is being captured");
+  TT_CUDA(cudaDeviceSynchronize());
+  for (auto& r : ctx->ws.retired) ctx->ws.give(r.first, r.second);
+  ctx->ws.retired.clear();
+  return TT_OK;
+}
+
+}  // namespace
+
+void tt::DevMem::release() {
+  if (ctx && gen == ctx->ws.gen)
+    for (auto& r : regions) {
+      ctx->ws.retired.push_back(r);
+      ctx->ws.live -= r.second;
+    }
+  regions.clear();
+}
+
+tt_status tt::ws_alloc(tt_ctx ctx, DevMem& m, int64_t bytes, void** out) {
+  *out = nullptr;
+  Arena& A = ctx->ws;
+  const int64_t n = (bytes + kWsAlign - 1) / kWsAlign * kWsAlign;
+  if (!A.base) {
+    A.need = std::max(A.need, A.live + n);
+    return fail(TT_E_WORKSPACE, "no device workspace bound (tt_workspace_bind); this call needs >= %lld bytes",
+                (long long)A.need);
+  }
+  if (m.ctx != ctx || m.gen != A.gen) {
+    m.forget();
+    m.ctx = ctx;
+    m.gen = A.gen;
+  }
+  int64_t off = 0;
+  bool ok = A.take(n, &off);
+  while (!ok) {
+    if (!A.retired.empty()) {
+      TT_TRY(drain_retired(ctx));
+    } else if (!evict_one(ctx)) {
+      A.need = std::max(A.need, A.live + n);
+      return fail(TT_E_WORKSPACE, "device workspace of %lld bytes is full (%lld live, no evictable plan); bind >= %lld "
+                  "bytes (tt_workspace_bytes)", (long long)A.size, (long long)A.live, (long long)A.need);
+    }
+    ok = A.take(n, &off);
+  }
+  m.regions.push_back({off, n});
+  *out = A.base + off;
+  return TT_OK;
+}
+
+tt_tensor_s::~tt_tensor_s() {
+  if (ctx) ctx->tensors.erase(this);
+}
+
+namespace {
 
 // ---------------------------------------------------------------------------------------------
 // profiling scope: CUDA events around a launch on the ctx stream
@@ -597,12 +692,12 @@ tt_status ensure_dev(tt_tensor t) {
   tt_ctx ctx = t->ctx;
   TT_TRY(need_device(ctx));
   if (!t->dev_ready) {
-    TT_TRY(dev_alloc(ctx, &t->d_nz, t->nblocks));
-    TT_TRY(dev_alloc(ctx, &t->d_blk_off, t->nblocks));
+    TT_TRY(dev_alloc(ctx, t->mem, &t->d_nz, t->nblocks));
+    TT_TRY(dev_alloc(ctx, t->mem, &t->d_blk_off, t->nblocks));
     TT_CUDA(cudaMemcpy(t->d_nz, t->nz.data(), t->nblocks, cudaMemcpyHostToDevice));
     t->d_toff.assign(t->order, nullptr);
     for (int d = 0; d < t->order; ++d) {
-      TT_TRY(dev_alloc(ctx, &t->d_toff[d], t->dims[d]->offsets.size()));
+      TT_TRY(dev_alloc(ctx, t->mem, &t->d_toff[d], t->dims[d]->offsets.size()));
       TT_CUDA(cudaMemcpy(t->d_toff[d], t->dims[d]->offsets.data(), t->dims[d]->offsets.size() * 8, cudaMemcpyHostToDevice));
     }
   }
@@ -643,6 +738,7 @@ struct ContractOpts {
 };
 
 struct ContractPlan {
+  DevMem mem;                          // workspace regions of the device arrays below
   Analysis an;
   HostTasks ht;
   struct MyPart {
@@ -783,10 +879,6 @@ tt_status tt_ctx_create_sim(void* stream, int32_t rank, tt_sim S, tt_ctx* out) {
   c->nranks = S->nranks;
   c->sim = S;
   tt_status s = ctx_device_setup(c);
-  if (s == TT_OK) {
-    DeviceGuard dg(c->device);
-    s = dev_alloc(c, &c->d_scalar, 2);
-  }
   if (s != TT_OK) {
     delete c;
     return s;
@@ -830,8 +922,6 @@ tt_status tt_ctx_create(int32_t device, void* stream, int32_t rank, int32_t nran
         return fail(TT_E_NCCL, "ncclCommInitRank: %s", api->GetErrorString(r));
       }
     }
-    tt_status s = dev_alloc(c, &c->d_scalar, 2);
-    if (s != TT_OK) { delete c; return s; }
   }
   *out = c;
   return TT_OK;
@@ -842,7 +932,14 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
   DeviceGuard dg(ctx->device);
   if (ctx->device >= 0) cudaStreamSynchronize(ctx->stream);
   ctx->plans.clear();
-  for (void* p : ctx->dev_allocs) cudaFree(p);
+  ctx->scratch.forget();
+  for (tt_tensor_s* t : ctx->tensors) {   // tensors may outlive their context (their handles stay valid)
+    t->mem.forget();
+    t->mem.ctx = nullptr;
+    t->ctx = nullptr;
+    t->dev_ready = false;
+  }
+  ctx->tensors.clear();
   for (auto& r : ctx->prof) { ctx->event_pool.push_back(r.e0); ctx->event_pool.push_back(r.e1); }
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->comm_stream) {
@@ -860,6 +957,56 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
     ctx->sim->ctx[ctx->rank] = nullptr;
   }
   delete ctx;
+  return TT_OK;
+}
+
+tt_status tt_workspace_bind(tt_ctx ctx, void* ptr, int64_t bytes) {
+  TT_TRY(need_device(ctx));
+  if (!ptr || bytes < kWsAlign) return fail(TT_E_ARG, "workspace: NULL pointer or fewer than %lld bytes", (long long)kWsAlign);
+  if ((uintptr_t)ptr % kWsAlign) return fail(TT_E_ARG, "workspace must be %lld-byte aligned", (long long)kWsAlign);
+  if (ctx->graph_pins > 0) return fail(TT_E_STATE, "a scheduler holds a captured graph reading the workspace");
+  DeviceGuard dg(ctx->device);
+  if (ctx->ws.base) TT_CUDA(cudaDeviceSynchronize());   // queued kernels may read the old buffer
+  ctx->plans.clear();
+  for (tt_tensor_s* t : ctx->tensors) {   // device metadata is rebuilt on next use
+    t->mem.forget();
+    t->dev_ready = false;
+    t->d_nz = nullptr;
+    t->d_blk_off = nullptr;
+    t->d_toff.clear();
+  }
+  ctx->scratch.forget();
+  ctx->d_scalar = nullptr;
+  const int64_t need = ctx->ws.need;
+  ctx->ws.reset((char*)ptr, bytes / kWsAlign * kWsAlign);
+  ctx->ws.need = need > ctx->ws.size ? need : 0;
+  return dev_alloc(ctx, ctx->scratch, &ctx->d_scalar, 2);
+}
+
+tt_status tt_workspace_bytes(tt_ctx ctx, int64_t* bytes) {
+  if (!ctx || !bytes) return fail(TT_E_ARG, "NULL argument");
+  *bytes = std::max(kWsMin, std::max(ctx->ws.high, ctx->ws.need));
+  return TT_OK;
+}
+
+tt_status tt_workspace_info(tt_ctx ctx, int64_t* bound, int64_t* live, int64_t* high) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  if (bound) *bound = ctx->ws.size;
+  if (live) *live = ctx->ws.live;
+  if (high) *high = ctx->ws.high;
+  return TT_OK;
+}
+
+tt_status tt_ctx_set_plan_limit(tt_ctx ctx, int64_t max_plans) {
+  if (!ctx || max_plans < 1) return fail(TT_E_ARG, "NULL context or plan limit < 1");
+  ctx->plan_limit = max_plans;
+  while ((int64_t)ctx->plans.size() > ctx->plan_limit && evict_one(ctx)) {}
+  return TT_OK;
+}
+
+tt_status tt_ctx_clear_plans(tt_ctx ctx) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  while (evict_one(ctx)) {}
   return TT_OK;
 }
 
@@ -1062,6 +1209,7 @@ static tt_status tensor_new(tt_ctx ctx, int32_t order, const tt_tis* dims, tt_te
   if (order < 1 || order > TT_MAX_ORDER) return fail(TT_E_UNSUPPORTED, "order %d outside 1..%d", order, TT_MAX_ORDER);
   tt_tensor t = new tt_tensor_s();
   t->ctx = ctx;
+  ctx->tensors.insert(t);
   t->order = order;
   t->uid = g_uid++;
   t->seq = ctx->tensor_seq++;
@@ -1377,6 +1525,7 @@ namespace {
 constexpr int64_t kSegElems = 1 << 15;
 
 struct ElemPlan {
+  DevMem mem;                 // workspace regions of the device arrays below
   std::vector<ElemDesc> descs;
   std::vector<Segment> segs;
   std::vector<TileItem> tiles;
@@ -1492,17 +1641,17 @@ int64_t sub_range_inner(tt_tensor Y, int64_t yb, bool same_dim0, int64_t lo_row,
 }
 
 tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
-  TT_TRY(dev_alloc(ctx, &ep.d_descs, ep.descs.size()));
-  TT_TRY(dev_alloc(ctx, &ep.d_segs, ep.segs.size()));
+  TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_descs, ep.descs.size()));
+  TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_segs, ep.segs.size()));
   if (!ep.descs.empty()) TT_CUDA(cudaMemcpy(ep.d_descs, ep.descs.data(), ep.descs.size() * sizeof(ElemDesc), cudaMemcpyHostToDevice));
   if (!ep.segs.empty()) TT_CUDA(cudaMemcpy(ep.d_segs, ep.segs.data(), ep.segs.size() * sizeof(Segment), cudaMemcpyHostToDevice));
   if (!ep.tiles.empty()) {
-    TT_TRY(dev_alloc(ctx, &ep.d_tiles, ep.tiles.size()));
+    TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_tiles, ep.tiles.size()));
     TT_CUDA(cudaMemcpy(ep.d_tiles, ep.tiles.data(), ep.tiles.size() * sizeof(TileItem), cudaMemcpyHostToDevice));
   }
   if (partials) {
     const int64_t n = ep.nseg() + ep.ntiles();
-    TT_TRY(dev_alloc(ctx, &ep.d_partials, (size_t)(n + scalar_scratch_elems(n))));
+    TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_partials, (size_t)(n + scalar_scratch_elems(n))));
   }
   return TT_OK;
 }
@@ -1511,7 +1660,9 @@ template <class P>
 std::shared_ptr<P> cached(tt_ctx ctx, const std::string& key) {
   auto it = ctx->plans.find(key);
   if (it == ctx->plans.end()) return nullptr;
-  return std::static_pointer_cast<P>(it->second);
+  it->second.tick = ++ctx->plan_tick;
+  if (ctx->plan_sink) ctx->plan_sink->push_back(it->second.p);
+  return std::static_pointer_cast<P>(it->second.p);
 }
 
 void reset_stats(tt_ctx ctx) { ctx->last = tt_stats{}; }
@@ -1521,7 +1672,7 @@ void reset_stats(tt_ctx ctx) { ctx->last = tt_stats{}; }
 extern "C" {
 
 tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag, int32_t kind) {
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   if (!t) return fail(TT_E_ARG, "NULL tensor");
   if (kind != TT_KIND_UNIFORM && kind != TT_KIND_INTEGER) return fail(TT_E_ARG, "bad kind %d", kind);
   TT_TRY(check_bound(t, "fill"));
@@ -1554,7 +1705,7 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
       for (auto& r : hr) add_segments(*ep, (int32_t)ep->descs.size() - 1, r.first, r.second);
     }
     TT_TRY(upload_elem(ctx, *ep, false));
-    ctx->plans[keybuf] = ep;
+    plan_put(ctx, keybuf, ep);
   }
   if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
@@ -1573,7 +1724,7 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
 }
 
 tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha) {
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   if (!C) return fail(TT_E_ARG, "NULL tensor");
   TT_TRY(check_bound(C, "C"));
   DeviceGuard dg(ctx->device);
@@ -1597,7 +1748,7 @@ tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha) {
       ep->blocks++;
     }
     TT_TRY(upload_elem(ctx, *ep, false));
-    ctx->plans[keybuf] = ep;
+    plan_put(ctx, keybuf, ep);
   }
   if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
@@ -1629,7 +1780,7 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
     if (!same_tiling(C->dims[d], A->dims[p])) return fail(TT_E_TILING, "label '%c' on different tilings (S413)", c[d]);
     perm[d] = (int)p;
   }
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   TT_TRY(check_bound(C, "C"));
   TT_TRY(check_bound(A, "A"));
   DeviceGuard dg(ctx->device);
@@ -1674,7 +1825,7 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
     }
     TT_TRY(build_gather(ctx, need, {A}, ep->gp));
     TT_TRY(upload_elem(ctx, *ep, false));
-    ctx->plans[key] = ep;
+    plan_put(ctx, key, ep);
   }
   if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
@@ -1712,7 +1863,7 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
     if (!same_tiling(A->dims[d], B->dims[p])) return fail(TT_E_TILING, "label '%c' on different tilings (S413)", a[d]);
     perm[d] = (int)p;
   }
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   TT_TRY(check_bound(A, "A"));
   TT_TRY(check_bound(B, "B"));
   DeviceGuard dg(ctx->device);
@@ -1761,7 +1912,7 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
     }
     TT_TRY(build_gather(ctx, need, {A, B}, ep->gp));
     TT_TRY(upload_elem(ctx, *ep, true));
-    ctx->plans[key] = ep;
+    plan_put(ctx, key, ep);
   }
   if (ctx->prepare_only) return TT_OK;
   reset_stats(ctx);
@@ -1937,12 +2088,13 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
   TT_TRY(ensure_dev(B));
   const int64_t ncb = (int64_t)ht.cblk.size(), ntasks = (int64_t)ht.a_blk.size();
   int64_t *d_cblocks, *d_counts;
-  TT_TRY(dev_alloc(ctx, &d_cblocks, ncb));
-  TT_TRY(dev_alloc(ctx, &d_counts, ncb));
-  TT_TRY(dev_alloc(ctx, &pl.d_ptr, ncb + 1));
-  TT_TRY(dev_alloc(ctx, &pl.d_ablk, ntasks));
-  TT_TRY(dev_alloc(ctx, &pl.d_bblk, ntasks));
-  TT_TRY(dev_alloc(ctx, &pl.d_tasks, ntasks));
+  DevMem tmp;   // builder scratch, retired when the plan is built
+  TT_TRY(dev_alloc(ctx, tmp, &d_cblocks, ncb));
+  TT_TRY(dev_alloc(ctx, tmp, &d_counts, ncb));
+  TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_ptr, ncb + 1));
+  TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_ablk, ntasks));
+  TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_bblk, ntasks));
+  TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_tasks, ntasks));
   TT_CUDA(cudaMemcpy(d_cblocks, ht.cblk.data(), ncb * 8, cudaMemcpyHostToDevice));
   BuildParams bp{};
   bp.nc = an.nc;
@@ -2203,13 +2355,13 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     pl.persistent = !work.empty() && st_sum / (double)work.size() < 512.0;
     if (const char* fp = getenv("TT_PERSISTENT")) pl.persistent = atoi(fp) != 0;
   }
-  TT_TRY(dev_alloc(ctx, &pl.d_groups, groups.size()));
-  TT_TRY(dev_alloc(ctx, &pl.d_work, work.size()));
+  TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_groups, groups.size()));
+  TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_work, work.size()));
   if (!groups.empty()) TT_CUDA(cudaMemcpy(pl.d_groups, groups.data(), groups.size() * sizeof(CGroupDesc), cudaMemcpyHostToDevice));
   if (!work.empty()) TT_CUDA(cudaMemcpy(pl.d_work, work.data(), work.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
   if (!pl.splits.empty()) {
-    TT_TRY(dev_alloc(ctx, &pl.d_splits, pl.splits.size()));
-    TT_TRY(dev_alloc(ctx, &pl.d_partials, (size_t)pl.partial_elems));
+    TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_splits, pl.splits.size()));
+    TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_partials, (size_t)pl.partial_elems));
     TT_CUDA(cudaMemcpy(pl.d_splits, pl.splits.data(), pl.splits.size() * sizeof(SplitDesc), cudaMemcpyHostToDevice));
   }
   return TT_OK;
@@ -2229,7 +2381,7 @@ tt_status get_contract_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A
   pl->an = an;
   DeviceGuard dg(ctx->device);
   TT_TRY(build_contract_plan(ctx, C, A, B, beta, *pl, opts));
-  ctx->plans[key] = pl;
+  plan_put(ctx, key, pl);
   out = pl;
   return TT_OK;
 }
@@ -2293,7 +2445,7 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
   std::shared_ptr<ContractPlan> pl;
   bool was_cached = false;
   TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, pl, &was_cached));
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   if (ctx->prepare_only) return TT_OK;
   TT_TRY(check_bound(C, "C"));
   TT_TRY(check_bound(A, "A"));
@@ -2364,7 +2516,7 @@ tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* cl, double b
   if (!ctx) return fail(TT_E_ARG, "NULL context");
   std::shared_ptr<ContractPlan> pl;
   TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, pl, nullptr));
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   if (ctx->prepare_only || ctx->nranks <= 1) return TT_OK;
   TT_TRY(check_bound(A, "A"));
   TT_TRY(check_bound(B, "B"));
@@ -2408,7 +2560,7 @@ tt_status tt_task_list(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, con
     if (cost) std::copy(ht.cost.begin(), ht.cost.end(), cost);
     return TT_OK;
   }
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   std::shared_ptr<ContractPlan> pl;
   TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, 1.0, pl, nullptr));
   const HostTasks& ht = pl->ht;
@@ -2571,6 +2723,57 @@ tt_status tt_partition_split_cost(tt_ctx ctx, tt_tensor C, const int64_t* cost, 
   return split_partition(ctx, C, cblk, cst, group_mask);
 }
 
+}  // extern "C"
+
+namespace {   // defined with tt_contract_cholesky below
+void chol_maps(tt_tensor X, const std::vector<tt_tis>& vd, std::vector<uint8_t>& vnz, std::vector<uint8_t>& wnz);
+tt_status chol_check(tt_tensor C, const char* cl, tt_tensor X, const char* vl, tt_tensor B, const char* bl,
+                     std::vector<tt_tis>& vd);
+tt_status new_meta_tensor(tt_ctx ctx, const std::vector<tt_tis>& dims, const std::vector<uint8_t>& nz, tt_tensor* out);
+}  // namespace
+
+extern "C" {
+
+tt_status tt_partition_split_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor X, const char* vl,
+                                      tt_tensor B, const char* bl, uint32_t group_mask) {
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  std::vector<tt_tis> vd;
+  TT_TRY(chol_check(C, cl, X, vl, B, bl, vd));
+  std::vector<uint8_t> vnz, wnz;
+  chol_maps(X, vd, vnz, wnz);
+  tt_tensor W = nullptr;
+  TT_TRY(new_meta_tensor(ctx, vd, wnz, &W));
+  std::unique_ptr<tt_tensor_s> hold(W);
+  Analysis an;
+  TT_TRY(analyse(C, cl, W, vl, B, bl, an));
+  HostTasks ht;
+  enumerate_tasks(an, C, W, B, ht);
+  // W formation of one (p_t, q_t) row: 2 N_L |p||q| sum over W's (r_t, s_t) blocks of |r||s|, shared
+  // evenly (integer division) by the row's non-zero C blocks
+  const std::string c(cl);
+  const int pc = (int)c.find(vl[0]), qc = (int)c.find(vl[1]);
+  const int64_t NL = X->dims[2]->offsets.back();
+  const int32_t np = vd[0]->ntiles(), nq = vd[1]->ntiles(), nr = vd[2]->ntiles(), ns = vd[3]->ntiles();
+  std::vector<int64_t> build((size_t)np * nq, 0), cnt((size_t)np * nq, 0), row(ht.cblk.size());
+  for (int32_t a = 0; a < np; ++a)
+    for (int32_t bq = 0; bq < nq; ++bq) {
+      int64_t w = 0;
+      for (int32_t r = 0; r < nr; ++r)
+        for (int32_t s = 0; s < ns; ++s)
+          if (wnz[(((int64_t)a * nq + bq) * nr + r) * ns + s]) w += vd[2]->size(r) * vd[3]->size(s);
+      build[(size_t)a * nq + bq] = 2 * NL * vd[0]->size(a) * vd[1]->size(bq) * w;
+    }
+  int32_t cc[TT_MAX_ORDER];
+  for (size_t g = 0; g < ht.cblk.size(); ++g) {
+    C->block_coords(ht.cblk[g], cc);
+    row[g] = (int64_t)cc[pc] * nq + cc[qc];
+    cnt[row[g]]++;
+  }
+  std::vector<int64_t> cost(ht.cblk.size());
+  for (size_t g = 0; g < ht.cblk.size(); ++g) cost[g] = ht.cost[g] + build[row[g]] / std::max<int64_t>(cnt[row[g]], 1);
+  return split_partition(ctx, C, ht.cblk, cost, group_mask);
+}
+
 tt_status tt_gather_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,
                          const char* bl, int64_t* recv, int64_t* n_recv, int64_t* send, int64_t* n_send, int64_t cap) {
   if (!ctx || !n_recv || !n_send) return fail(TT_E_ARG, "NULL argument");
@@ -2697,6 +2900,59 @@ tt_status local_add_plan(tt_ctx ctx, tt_tensor Xt, tt_tensor Yt, const std::vect
   return TT_OK;
 }
 
+// Block maps of the implicit operand over its tiled spaces vd = (p, q, r, s) (reading R19b): from X's
+// (p_t, r_t) tile pairs holding any non-zero block (over all L tiles) -- X's actual block map, not the
+// tiles' spins.  W(pqrs) = sum_L X(prL) X(qsL) (the Coulomb term) is non-zero where both factors are;
+// V = W - W(r<->s) where the Coulomb or the exchange term is.
+void chol_maps(tt_tensor X, const std::vector<tt_tis>& vd, std::vector<uint8_t>& vnz, std::vector<uint8_t>& wnz) {
+  int64_t nvb = 1;
+  for (auto t : vd) nvb *= t->ntiles();
+  const int32_t nx0 = X->grid[0], nx1 = X->grid[1];
+  std::vector<uint8_t> xnz((size_t)nx0 * nx1, 0);
+  int32_t xc[TT_MAX_ORDER];
+  for (int64_t xb = 0; xb < X->nblocks; ++xb)
+    if (X->nz[xb]) {
+      X->block_coords(xb, xc);
+      xnz[(size_t)xc[0] * nx1 + xc[1]] = 1;
+    }
+  vnz.assign(nvb, 0);
+  wnz.assign(nvb, 0);
+  for (int64_t x = 0; x < nvb; ++x) {
+    int64_t y = x;
+    int32_t co[4];
+    for (int d = 3; d >= 0; --d) { co[d] = (int32_t)(y % vd[d]->ntiles()); y /= vd[d]->ntiles(); }
+    auto xn = [&](int32_t u, int32_t w) { return xnz[(size_t)u * nx1 + w] != 0; };
+    wnz[x] = (xn(co[0], co[2]) && xn(co[1], co[3])) ? 1 : 0;              // Coulomb term reachable
+    vnz[x] = (wnz[x] || (xn(co[0], co[3]) && xn(co[1], co[2]))) ? 1 : 0;  // Coulomb or exchange
+  }
+}
+
+// Shared validation of the implicit-operand ladder C(..p..q..) += V(p,q,r,s) B(..r..s..) (Eq. cc12):
+// labels, ladder form and tilings; returns the four tiled spaces and the labels.
+tt_status chol_check(tt_tensor C, const char* cl, tt_tensor X, const char* vl, tt_tensor B, const char* bl,
+                     std::vector<tt_tis>& vd) {
+  if (!C || !X || !B || !vl) return fail(TT_E_ARG, "NULL argument");
+  TT_TRY(check_labels(cl, C, "C"));
+  TT_TRY(check_labels(bl, B, "B"));
+  const std::string c(cl), v(vl), b(bl);
+  if (v.size() != 4) return fail(TT_E_LABEL, "the implicit operand V(p,q,r,s) needs 4 labels");
+  for (int i = 0; i < 4; ++i)
+    for (int j = i + 1; j < 4; ++j)
+      if (v[i] == v[j]) return fail(TT_E_LABEL, "repeated label in V");
+  if (X->order != 3) return fail(TT_E_ARG, "X must be order 3: X(p, r, L)");
+  const char p = v[0], q = v[1], r = v[2], s = v[3];
+  if (c.find(p) == std::string::npos || c.find(q) == std::string::npos)
+    return fail(TT_E_UNSUPPORTED, "V's first two labels must be free labels of C (ladder form)");
+  if (b.find(r) == std::string::npos || b.find(s) == std::string::npos || c.find(r) != std::string::npos ||
+      c.find(s) != std::string::npos)
+    return fail(TT_E_UNSUPPORTED, "V's last two labels must be contracted with B (ladder form)");
+  vd = {C->dims[c.find(p)], C->dims[c.find(q)], B->dims[b.find(r)], B->dims[b.find(s)]};
+  for (tt_tis t : vd)
+    if (!same_tiling(t, X->dims[0]) || !same_tiling(t, X->dims[1]))
+      return fail(TT_E_TILING, "V's labels and X's first two dims must share one tiled space (Eq. cc12)");
+  return TT_OK;
+}
+
 tt_status run_local_add(tt_ctx ctx, const ElemPlan& ep, tt_tensor Xt, tt_tensor Yt, double beta, double alpha) {
   ElemParams p{};
   p.X = Xt->data;
@@ -2718,25 +2974,12 @@ extern "C" {
 
 tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor X,
                                const char* vl, tt_tensor B, const char* bl, void* workspace, int64_t ws_elems) {
-  if (!ctx || !C || !X || !B || !vl) return fail(TT_E_ARG, "NULL argument");
-  TT_TRY(check_labels(cl, C, "C"));
-  TT_TRY(check_labels(bl, B, "B"));
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  std::vector<tt_tis> vdims;
+  TT_TRY(chol_check(C, cl, X, vl, B, bl, vdims));
   const std::string c(cl), v(vl), b(bl);
-  if (v.size() != 4) return fail(TT_E_LABEL, "the implicit operand V(p,q,r,s) needs 4 labels");
-  for (int i = 0; i < 4; ++i)
-    for (int j = i + 1; j < 4; ++j)
-      if (v[i] == v[j]) return fail(TT_E_LABEL, "repeated label in V");
-  if (X->order != 3) return fail(TT_E_ARG, "X must be order 3: X(p, r, L)");
   const char p = v[0], q = v[1], r = v[2], s = v[3];
-  if (c.find(p) == std::string::npos || c.find(q) == std::string::npos)
-    return fail(TT_E_UNSUPPORTED, "V's first two labels must be free labels of C (ladder form)");
-  if (b.find(r) == std::string::npos || b.find(s) == std::string::npos || c.find(r) != std::string::npos ||
-      c.find(s) != std::string::npos)
-    return fail(TT_E_UNSUPPORTED, "V's last two labels must be contracted with B (ladder form)");
-  tt_tis tp = C->dims[c.find(p)], tq = C->dims[c.find(q)], tr = B->dims[b.find(r)], ts = B->dims[b.find(s)];
-  for (tt_tis t : {tp, tq, tr, ts})
-    if (!same_tiling(t, X->dims[0]) || !same_tiling(t, X->dims[1]))
-      return fail(TT_E_TILING, "V's labels and X's first two dims must share one tiled space (Eq. cc12)");
+  tt_tis tp = vdims[0], tq = vdims[1], tr = vdims[2], ts = vdims[3];
   if (ctx->nranks > 1)
     for (int64_t x = 0; x < X->nblocks; ++x)
       if (X->nz[x] && X->owner[x] != TT_REPLICATED)
@@ -2747,7 +2990,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       lc = std::string(1, ch);
       break;
     }
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   TT_TRY(check_bound(C, "C"));
   TT_TRY(check_bound(X, "X"));
   TT_TRY(check_bound(B, "B"));
@@ -2765,29 +3008,8 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     cp = std::make_shared<CholPlan>();
     cp->lc = lc;
     std::vector<tt_tis> vd = {tp, tq, tr, ts};
-    int64_t nvb = 1;
-    for (auto t : vd) nvb *= t->ntiles();
-    // X's (p_t, r_t) tile pairs holding any non-zero block (over all L tiles): the maps of W and V
-    // follow from X's actual block map (R19b), not from the tiles' spins
-    const int32_t nx0 = X->grid[0], nx1 = X->grid[1];
-    std::vector<uint8_t> xnz((size_t)nx0 * nx1, 0);
-    {
-      int32_t xc[TT_MAX_ORDER];
-      for (int64_t xb = 0; xb < X->nblocks; ++xb)
-        if (X->nz[xb]) {
-          X->block_coords(xb, xc);
-          xnz[(size_t)xc[0] * nx1 + xc[1]] = 1;
-        }
-    }
-    std::vector<uint8_t> vnz(nvb), wnz(nvb);
-    for (int64_t x = 0; x < nvb; ++x) {
-      int64_t y = x;
-      int32_t co[4];
-      for (int d = 3; d >= 0; --d) { co[d] = (int32_t)(y % vd[d]->ntiles()); y /= vd[d]->ntiles(); }
-      auto xn = [&](int32_t u, int32_t w) { return xnz[(size_t)u * nx1 + w] != 0; };
-      wnz[x] = (xn(co[0], co[2]) && xn(co[1], co[3])) ? 1 : 0;              // Coulomb term reachable
-      vnz[x] = (wnz[x] || (xn(co[0], co[3]) && xn(co[1], co[2]))) ? 1 : 0;  // Coulomb or exchange
-    }
+    std::vector<uint8_t> vnz, wnz;
+    chol_maps(X, vd, vnz, wnz);
     TT_TRY(new_meta_tensor(ctx, vd, vnz, &cp->Vmeta));
     TT_TRY(new_meta_tensor(ctx, vd, wnz, &cp->Wmeta));
     // Bh: B's blocks with r_t <= s_t (the antisymmetric Bm's independent half), and its strict view
@@ -2922,7 +3144,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     auto flush = [&](std::vector<const Unit*>& cur) -> tt_status {
       if (cur.empty()) return TT_OK;
       CholBatch bt;
-      std::vector<uint8_t> bnz(nvb, 0);
+      std::vector<uint8_t> bnz(wnz.size(), 0);
       std::vector<int64_t> rb;
       for (const Unit* u : cur) {
         auto rows = u->wrows;
@@ -2971,7 +3193,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       cur_elems += uel;
     }
     TT_TRY(flush(cur));
-    ctx->plans[keybuf] = cp;
+    plan_put(ctx, keybuf, cp);
   }
   const std::string L = cp->lc;
   const std::string x1 = std::string(1, p) + r + L, x2 = std::string(1, q) + s + L;   // W = X(prL) X(qsL)
@@ -3200,7 +3422,7 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* cl, double beta, dou
     // remember the costs with the plan (returned on every call)
     cp->flops[0] = cand_flops[0]; cp->flops[1] = cand_flops[1]; cp->flops[2] = cand_flops[2];
     cp->naive = naive;
-    ctx->plans[keybuf] = cp;
+    plan_put(ctx, keybuf, cp);
   }
   const int64_t need = (cp->I->storage_elems + 1) / 2 * 2;
   if (info) {
@@ -3240,6 +3462,7 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* cl, double beta, dou
 namespace {
 
 struct RetileOp {
+  DevMem mem;                // workspace regions of the device arrays below
   tt_tensor dst = nullptr;   // meta tensor on the dense tiling, storage in the workspace
   tt_tensor src = nullptr;
   std::vector<int32_t> sdim;
@@ -3250,6 +3473,7 @@ struct RetileOp {
 };
 
 struct TripPlan {
+  DevMem mem;                                 // workspace regions of the device arrays below
   tt_tis fullO = nullptr, fullV = nullptr;   // one tile over the whole space (dense copies)
   RetileOp rt[5];                             // VO (O,O,O,V), VV (V,O,V,V), T2 (O,O,V,V), VD (O,O,V,V), T1 (V,O)
   int2* d_units = nullptr;
@@ -3309,8 +3533,8 @@ tt_status build_retile(tt_ctx ctx, RetileOp& op) {
       segs.push_back({(int32_t)blks.size(), 0, e, std::min(vol, e + 32768)});
     blks.push_back(rb);
   }
-  TT_TRY(dev_alloc(ctx, &op.d_blks, std::max<size_t>(1, blks.size())));
-  TT_TRY(dev_alloc(ctx, &op.d_segs, std::max<size_t>(1, segs.size())));
+  TT_TRY(dev_alloc(ctx, op.mem, &op.d_blks, std::max<size_t>(1, blks.size())));
+  TT_TRY(dev_alloc(ctx, op.mem, &op.d_segs, std::max<size_t>(1, segs.size())));
   if (!blks.empty()) TT_CUDA(cudaMemcpy(op.d_blks, blks.data(), blks.size() * sizeof(RetileBlk), cudaMemcpyHostToDevice));
   if (!segs.empty()) TT_CUDA(cudaMemcpy(op.d_segs, segs.data(), segs.size() * sizeof(Segment), cudaMemcpyHostToDevice));
   op.nseg = (int64_t)segs.size();
@@ -3319,7 +3543,7 @@ tt_status build_retile(tt_ctx ctx, RetileOp& op) {
     std::vector<int32_t> g2t(t->offsets.back());
     for (int x = 0; x < t->ntiles(); ++x)
       for (int64_t g = t->offsets[x]; g < t->offsets[x + 1]; ++g) g2t[g] = x;
-    TT_TRY(dev_alloc(ctx, &op.d_g2t[q], g2t.size()));
+    TT_TRY(dev_alloc(ctx, op.mem, &op.d_g2t[q], g2t.size()));
     TT_CUDA(cudaMemcpy(op.d_g2t[q], g2t.data(), g2t.size() * 4, cudaMemcpyHostToDevice));
   }
   return TT_OK;
@@ -3502,14 +3726,14 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     tp->ws_need = base + (U + 1) / 2 * 2;
     tp->info.ws_elems = tp->ws_need;
     if (ctx->device >= 0) {
-      TT_TRY(need_device(ctx));
+      TT_TRY(need_ws(ctx));
       DeviceGuard dg(ctx->device);
       for (int x = 0; x < 5; ++x) TT_TRY(build_retile(ctx, tp->rt[x]));
-      TT_TRY(dev_alloc(ctx, &tp->d_units, std::max<size_t>(1, units.size())));
-      TT_TRY(dev_alloc(ctx, &tp->d_box3, std::max<size_t>(1, box3.size())));
-      TT_TRY(dev_alloc(ctx, &tp->d_trip, std::max<size_t>(1, trip.size())));
-      TT_TRY(dev_alloc(ctx, &tp->d_box_lo, box_lo.size()));
-      TT_TRY(dev_alloc(ctx, &tp->d_box_ext, box_ext.size()));
+      TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_units, std::max<size_t>(1, units.size())));
+      TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_box3, std::max<size_t>(1, box3.size())));
+      TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_trip, std::max<size_t>(1, trip.size())));
+      TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_box_lo, box_lo.size()));
+      TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_box_ext, box_ext.size()));
       if (!units.empty()) TT_CUDA(cudaMemcpy(tp->d_units, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice));
       // pairs of consecutive units of this rank with the same box triple and occupied pair (i,j)
       std::vector<int2> pairs;
@@ -3520,14 +3744,14 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
         q += two ? 2 : 1;
       }
       tp->npairs = (int64_t)pairs.size();
-      TT_TRY(dev_alloc(ctx, &tp->d_pairs, std::max<size_t>(1, pairs.size())));
+      TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_pairs, std::max<size_t>(1, pairs.size())));
       if (!pairs.empty()) TT_CUDA(cudaMemcpy(tp->d_pairs, pairs.data(), pairs.size() * sizeof(int2), cudaMemcpyHostToDevice));
       if (!box3.empty()) TT_CUDA(cudaMemcpy(tp->d_box3, box3.data(), box3.size() * sizeof(int4), cudaMemcpyHostToDevice));
       TT_CUDA(cudaMemcpy(tp->d_trip, trip.data(), trip.size() * sizeof(int4), cudaMemcpyHostToDevice));
       TT_CUDA(cudaMemcpy(tp->d_box_lo, box_lo.data(), box_lo.size() * 4, cudaMemcpyHostToDevice));
       TT_CUDA(cudaMemcpy(tp->d_box_ext, box_ext.data(), box_ext.size() * 4, cudaMemcpyHostToDevice));
     }
-    ctx->plans[keybuf] = tp;
+    plan_put(ctx, keybuf, tp);
   }
   if (info) *info = tp->info;
   if (!workspace) return TT_OK;   // query: units, FLOPs, workspace size
@@ -3536,7 +3760,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   if (ws_elems < tp->ws_need)
     return fail(TT_E_OOM, "workspace holds %lld doubles, (T) needs %lld (dense input copies + one partial per unit)",
                 (long long)ws_elems, (long long)tp->ws_need);
-  TT_TRY(need_device(ctx));
+  TT_TRY(need_ws(ctx));
   for (int x = 0; x < 5; ++x) TT_TRY(check_bound(ins[x], names[x]));
   if (ctx->prepare_only) return TT_OK;
   DeviceGuard dg(ctx->device);

@@ -5,6 +5,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <map>
+#include <set>
 #include <mutex>
 #include <memory>
 #include <string>
@@ -69,6 +70,90 @@ struct ContractionShape {
   bool b_ncontig = true;                   // B's innermost label is an N label
 };
 
+// ------------------------------------------------------------------------------------------------
+// Device workspace (tt_workspace_bind; SURVEY §8(b), P182-186 "ExecutionContext ... memory manager"):
+// ONE caller-owned device buffer per context from which all library metadata (tensor block maps, task
+// descriptors, work lists, element-op segments) and scratch (split-K partials, scalar partials) are
+// carved.  There is no cudaMalloc on the execute path.  Host-side first-fit allocator over offsets with
+// coalescing; released regions are "retired" until the device has drained (they may still be read by
+// queued kernels) and become reusable after one device synchronisation.  When the buffer is full the
+// context evicts least-recently-used cached plans that nobody else references.
+constexpr int64_t kWsAlign = 256;
+constexpr int64_t kWsMin = 1 << 20;   // tt_workspace_bytes before any call
+
+struct Arena {
+  char* base = nullptr;
+  int64_t size = 0;
+  std::map<int64_t, int64_t> free_;                     // offset -> length, coalesced
+  std::vector<std::pair<int64_t, int64_t>> retired;     // released, reusable after a device drain
+  int64_t live = 0, high = 0, need = 0;                 // bytes in use, high-water, failed-call need
+  uint64_t gen = 0;                                     // bumped at every bind
+  void reset(char* b, int64_t n) {
+    base = b;
+    size = n;
+    free_.clear();
+    retired.clear();
+    if (n > 0) free_[0] = n;
+    live = high = need = 0;
+    ++gen;
+  }
+  bool take(int64_t n, int64_t* off) {                  // first fit
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second < n) continue;
+      *off = it->first;
+      const int64_t rest = it->second - n, at = it->first + n;
+      free_.erase(it);
+      if (rest > 0) free_[at] = rest;
+      live += n;
+      if (live > high) high = live;
+      return true;
+    }
+    return false;
+  }
+  void give(int64_t off, int64_t n) {                   // back to the free list, coalescing
+    auto it = free_.emplace(off, n).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+      }
+    }
+  }
+};
+
+// The regions one owner (a plan, a tensor's device metadata, the context scratch) holds in the
+// workspace; retired when the owner is destroyed.
+struct DevMem {
+  tt_ctx ctx = nullptr;
+  uint64_t gen = 0;
+  std::vector<std::pair<int64_t, int64_t>> regions;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  DevMem(DevMem&& o) noexcept : ctx(o.ctx), gen(o.gen), regions(std::move(o.regions)) { o.regions.clear(); }
+  DevMem& operator=(DevMem&& o) noexcept {
+    if (this != &o) {
+      release();
+      ctx = o.ctx;
+      gen = o.gen;
+      regions = std::move(o.regions);
+      o.regions.clear();
+    }
+    return *this;
+  }
+  ~DevMem() { release(); }
+  void release();              // retire every region (tt_api.cpp)
+  void forget() { regions.clear(); }   // the arena is being reset: nothing to give back
+};
+
+tt_status ws_alloc(tt_ctx ctx, DevMem& m, int64_t bytes, void** out);
+
 }  // namespace tt
 
 // ------------------------------------------------------------------------------------------------
@@ -115,6 +200,7 @@ struct tt_tensor_s {
   uint8_t* d_nz = nullptr;
   int64_t* d_blk_off = nullptr;
   std::vector<int64_t*> d_toff;   // per dim tile offsets on the device
+  tt::DevMem mem;                  // workspace regions of the device metadata above
   bool dev_ready = false;
   bool dev_off_stale = false;      // storage offsets changed since the last upload
   // row-range ownership (SURVEY §8(e) block splitting): a split block is owned by parts, each a
@@ -129,6 +215,7 @@ struct tt_tensor_s {
   tt_tensor view_of = nullptr;     // sliced view (tt_tensor_view): blocks live in this tensor's storage
   int32_t live_views = 0;          // views of this tensor not yet destroyed: its layout is frozen meanwhile
 
+  ~tt_tensor_s();                  // leaves the context's tensor registry (tt_api.cpp)
   int64_t ext0(int64_t b) const {
     int32_t c[TT_MAX_ORDER];
     block_coords(b, c);
@@ -180,8 +267,18 @@ struct tt_ctx_s {
   std::vector<cudaEvent_t> event_pool;
   int64_t launches = 0;
   tt_stats last{};
-  std::map<std::string, std::shared_ptr<void>> plans;   // plan cache (type-erased)
-  std::vector<void*> dev_allocs;                         // metadata allocations freed at destroy
+  struct PlanEntry {
+    std::shared_ptr<void> p;
+    uint64_t tick = 0;                                   // last use (LRU eviction)
+  };
+  std::map<std::string, PlanEntry> plans;                // plan cache (type-erased)
+  uint64_t plan_tick = 0;
+  int64_t plan_limit = 1 << 14;                          // cached plans kept at most (tt_ctx_set_plan_limit)
+  std::vector<std::shared_ptr<void>>* plan_sink = nullptr;   // scheduler capture: keeps every plan it uses alive
+  int32_t graph_pins = 0;                                // captured graphs reading workspace pointers
+  tt::Arena ws;                                          // the bound device workspace
+  tt::DevMem scratch;                                    // context scratch (d_scalar)
+  std::set<tt_tensor_s*> tensors;                        // live tensors (their metadata lives in ws)
   double* d_scalar = nullptr;                            // scratch for scalar results
   double* d_partials = nullptr;
   int32_t sm_count = 148;

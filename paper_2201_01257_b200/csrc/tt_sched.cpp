@@ -15,6 +15,7 @@
 // every rank issues its NCCL calls in the same order (SPMD).
 #include <algorithm>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -85,7 +86,10 @@ struct tt_sched_s {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int32_t graph_levels = 0;
-  double* d_results = nullptr;       // device slots of the scalar ops of the graph
+  double* d_results = nullptr;       // device slots of the scalar ops of the graph (in the workspace)
+  tt::DevMem mem;                    // ... their workspace region
+  std::vector<std::shared_ptr<void>> held;   // every plan the graph reads: never evicted while it lives
+  bool pinned = false;               // counted in ctx->graph_pins (the workspace cannot be re-bound)
   std::vector<double*> h_targets;    // their host destinations
   std::vector<double> h_results;
 };
@@ -147,9 +151,9 @@ tt_status tt_sched_destroy(tt_sched s) {
     if (s->cap) cudaStreamDestroy(s->cap);
     if (s->exec) cudaGraphExecDestroy(s->exec);
     if (s->graph) cudaGraphDestroy(s->graph);
-    if (s->d_results) cudaFree(s->d_results);
     if (prev >= 0) cudaSetDevice(prev);
   }
+  if (s->pinned) s->ctx->graph_pins--;
   delete s;
   return TT_OK;
 }
@@ -317,6 +321,11 @@ static void drop_graph(tt_sched s) {
   if (s->graph) cudaGraphDestroy(s->graph);
   s->exec = nullptr;
   s->graph = nullptr;
+  s->held.clear();
+  s->mem.release();
+  s->d_results = nullptr;
+  if (s->pinned) s->ctx->graph_pins--;
+  s->pinned = false;
 }
 
 tt_status tt_sched_execute(tt_sched s) {
@@ -352,20 +361,27 @@ tt_status tt_sched_capture(tt_sched s) {
   cudaGetDevice(&prev);
   cudaSetDevice(ctx->device);
   drop_graph(s);
-  // 1. build every plan (host work, uploads, device task builders) outside the capture
+  // 1. build every plan (host work, uploads, device task builders) outside the capture; the
+  //    scheduler keeps a reference to each so that none is evicted while the graph reads it
   ctx->prepare_only = true;
+  ctx->plan_sink = &s->held;
   for (const SchedOp& op : s->ops)
     if ((st = run_op(ctx, op)) != TT_OK) break;
   ctx->prepare_only = false;
-  // 2. device slots for the scalar results
+  // 2. device slots for the scalar results (workspace)
   s->h_targets.clear();
   for (const SchedOp& op : s->ops)
     if (op.kind == kScalar) s->h_targets.push_back(op.result);
   s->h_results.assign(s->h_targets.size(), 0.0);
-  if (st == TT_OK && s->d_results) { cudaFree(s->d_results); s->d_results = nullptr; }
-  if (st == TT_OK && !s->h_targets.empty() &&
-      cudaMalloc(&s->d_results, s->h_targets.size() * sizeof(double)) != cudaSuccess)
-    st = set_error(TT_E_OOM, "cannot allocate scalar result slots");
+  if (st == TT_OK && !s->h_targets.empty()) {
+    void* v = nullptr;
+    st = tt::ws_alloc(ctx, s->mem, (int64_t)(s->h_targets.size() * sizeof(double)), &v);
+    s->d_results = (double*)v;
+  }
+  if (st == TT_OK) {
+    s->pinned = true;
+    ctx->graph_pins++;
+  }
   // 3. record the levels into a CUDA graph (profiling events off while capturing)
   if (st == TT_OK) {
     const bool prof = ctx->profiling;
@@ -388,6 +404,7 @@ tt_status tt_sched_capture(tt_sched s) {
     ctx->profiling = prof;
     s->graph_levels = L;
   }
+  ctx->plan_sink = nullptr;
   if (st != TT_OK) drop_graph(s);
   if (prev >= 0) cudaSetDevice(prev);
   return st;

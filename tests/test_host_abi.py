@@ -397,3 +397,54 @@ def test_lpt_grouped_matches_oracle(nranks):
         key = orc[C].block_coords(x)[:2]
         rows.setdefault(key, set()).add(own[x])
     assert all(len(v) == 1 for v in rows.values())
+
+
+def _chol_problem(tt, c, O_, V_, tO, tV, NL, tL, spin):
+    so = tt.IndexSpace(O_, [(0, O_ // 2), (O_ // 2, O_)], [1, -1]) if spin else tt.IndexSpace(O_)
+    sv = tt.IndexSpace(V_, [(0, V_ // 2), (V_ // 2, V_)], [1, -1]) if spin else tt.IndexSpace(V_)
+    to, tv, tl = tt.TiledIndexSpace(so, tO), tt.TiledIndexSpace(sv, tV), tt.TiledIndexSpace(tt.IndexSpace(NL), tL)
+    sp = (lambda u, l: (u, l)) if spin else (lambda u, l: None)
+    R = tt.Tensor(c, [tv, tv, to, to], spin=sp([0, 1], [2, 3]))
+    T = tt.Tensor(c, [tv, tv, to, to], spin=sp([0, 1], [2, 3]))
+    X = tt.Tensor(c, [tv, tv, tl], spin=sp([0], [1]))
+    lo = L.IndexSpace(O_, [(0, O_ // 2, 1), (O_ // 2, O_, -1)] if spin else [])
+    lv = L.IndexSpace(V_, [(0, V_ // 2, 1), (V_ // 2, V_, -1)] if spin else [])
+    oo, ov, ol = L.tile_fixed(lo, tO), L.tile_fixed(lv, tV), L.tile_fixed(L.IndexSpace(NL), tL)
+    mk = (lambda d, u, l: L.tensor_spin(d, u, l)) if spin else (lambda d, u, l: L.tensor_dense_map(d))
+    oR, oT, oX = mk([ov, ov, oo, oo], [0, 1], [2, 3]), mk([ov, ov, oo, oo], [0, 1], [2, 3]), mk([ov, ov, ol], [0], [1])
+    return (R, T, X), (oR, oT, oX)
+
+
+@pytest.mark.parametrize("spin", [False, True])
+def test_oracle_cholesky_ladder_cost_closed_forms(spin):
+    """The oracle's executed-cost model of the implicit ladder (Eq. cc12) summed over blocks equals the
+    closed forms: GEMMs 2 nnz(R) n_W (n_W = v^2 dense, (v/2)^2 with alpha/beta maps: W's (c,d) must
+    match the spins of (a,b)), W formation 2 N_L v^2 n_W (every (a,b) row of R is non-zero)."""
+    O_, V_, NL = 8, 16, 12
+    _, (oR, oT, oX) = _chol_problem(tt, tt.Context(device=-1), O_, V_, 2, 4, NL, 6, spin)
+    cb, cost = L.cholesky_ladder_cost(oR, "abij", oX, "abcd", oT, "cdij")
+    nnzR = sum(oR.block_volume(b) for b in range(oR.nblocks()) if oR.nz[b])
+    nW = (V_ // 2) ** 2 if spin else V_ ** 2
+    assert nnzR == (6 * V_ * V_ * O_ * O_ // 16 if spin else V_ * V_ * O_ * O_)
+    assert sum(cost) == 2 * nnzR * nW + 2 * NL * V_ * V_ * nW
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("spin", [False, True])
+def test_partition_split_cholesky_matches_oracle(nranks, spin):
+    """tt_partition_split_cholesky == oracle partition_split on oracle.layout.cholesky_ladder_cost."""
+    c = tt.Context(device=-1, nranks=nranks)
+    (R, T, X), (oR, oT, oX) = _chol_problem(tt, c, 10, 14, 3, 4, 20, 7, spin)
+    cb, cost = L.cholesky_ladder_cost(oR, "abij", oX, "abcd", oT, "cdij")
+    exp = L.partition_split(oR, cost, cb, [0, 1], nranks)
+    tt.partition_split_cholesky(c, R, "abij", X, "abcd", T, "cdij", group_dims=(0, 1))
+    got = {}
+    for x in cb:
+        if R.owner[x] == tt.TT_SPLIT:
+            got[x] = [(lo, hi, o) for (bb, lo, hi, o) in R.parts if bb == x]
+        else:
+            got[x] = [(0, oR.block_extents(x)[0], int(R.owner[x]))]
+    assert got == exp
+    with pytest.raises(tt.TTError) as e:   # not the ladder form
+        tt.partition_split_cholesky(c, R, "abij", X, "cdab", T, "cdij")
+    assert e.value.name == "TT_E_UNSUPPORTED"

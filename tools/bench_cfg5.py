@@ -30,7 +30,6 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2201_01257_b200 as tt  # noqa: E402
-from paper_2201_01257_b200.ccsd import cholesky_ladder_costs  # noqa: E402
 
 WEAK_V = {1: 714, 2: 848, 4: 1010, 8: 1200}
 ALPHA = 0.5
@@ -102,7 +101,7 @@ def main():
     X = tt.Tensor(ctx, [tv, tv, tl], spin=([0], [1]))
     X.set_owner(np.where(X.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
     if world > 1:
-        tt.partition_split_cost(ctx, R, cholesky_ladder_costs(tt, R, T, tv, NL), group_dims=(0, 1))
+        tt.partition_split_cholesky(ctx, R, "abij", X, "abcd", T, "cdij", group_dims=(0, 1))
         R.set_compact(True)
         # T's (c,d) / (d,c) block pairs placed together, balanced by bytes (LPT over pair volumes)
         offs = [np.diff(d.offsets) for d in T.dims]
