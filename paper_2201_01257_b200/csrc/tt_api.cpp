@@ -130,6 +130,13 @@ tt_status drain_retired(tt_ctx ctx) {
   return TT_OK;
 }
 
+// A builder that failed part-way holds arrays that may split the free space: after it released them,
+// evict every plan nobody holds and drain, so that its retry allocates from one contiguous region.
+tt_status ws_make_room(tt_ctx ctx) {
+  while (evict_one(ctx)) {}
+  return drain_retired(ctx);
+}
+
 }  // namespace
 
 void tt::DevMem::release() {
@@ -156,7 +163,7 @@ tt_status tt::ws_alloc(tt_ctx ctx, DevMem& m, int64_t bytes, void** out) {
     m.gen = A.gen;
   }
   int64_t off = 0;
-  bool ok = A.take(n, &off);
+  bool ok = A.take(n, &off, m.top);
   while (!ok) {
     if (!A.retired.empty()) {
       TT_TRY(drain_retired(ctx));
@@ -165,7 +172,7 @@ tt_status tt::ws_alloc(tt_ctx ctx, DevMem& m, int64_t bytes, void** out) {
       return fail(TT_E_WORKSPACE, "device workspace of %lld bytes is full (%lld live, no evictable plan); bind >= %lld "
                   "bytes (tt_workspace_bytes)", (long long)A.size, (long long)A.live, (long long)A.need);
     }
-    ok = A.take(n, &off);
+    ok = A.take(n, &off, m.top);
   }
   m.regions.push_back({off, n});
   *out = A.base + off;
@@ -1640,7 +1647,7 @@ int64_t sub_range_inner(tt_tensor Y, int64_t yb, bool same_dim0, int64_t lo_row,
   return inner;
 }
 
-tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
+tt_status upload_elem_once(tt_ctx ctx, ElemPlan& ep, bool partials) {
   TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_descs, ep.descs.size()));
   TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_segs, ep.segs.size()));
   if (!ep.descs.empty()) TT_CUDA(cudaMemcpy(ep.d_descs, ep.descs.data(), ep.descs.size() * sizeof(ElemDesc), cudaMemcpyHostToDevice));
@@ -1654,6 +1661,16 @@ tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
     TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_partials, (size_t)(n + scalar_scratch_elems(n))));
   }
   return TT_OK;
+}
+
+tt_status upload_elem(tt_ctx ctx, ElemPlan& ep, bool partials) {
+  tt_status st = upload_elem_once(ctx, ep, partials);
+  if (st == TT_E_WORKSPACE && ctx->ws.base) {   // retry from an emptied cache (see ws_make_room)
+    ep.mem.release();
+    TT_TRY(ws_make_room(ctx));
+    st = upload_elem_once(ctx, ep, partials);
+  }
+  return st;
 }
 
 template <class P>
@@ -2380,7 +2397,15 @@ tt_status get_contract_plan(tt_ctx ctx, tt_tensor C, const char* cl, tt_tensor A
   auto pl = std::make_shared<ContractPlan>();
   pl->an = an;
   DeviceGuard dg(ctx->device);
-  TT_TRY(build_contract_plan(ctx, C, A, B, beta, *pl, opts));
+  tt_status st = build_contract_plan(ctx, C, A, B, beta, *pl, opts);
+  if (st == TT_E_WORKSPACE && ctx->ws.base) {   // the plan's own earlier arrays may split the free space
+    pl.reset();
+    TT_TRY(ws_make_room(ctx));
+    pl = std::make_shared<ContractPlan>();
+    pl->an = an;
+    st = build_contract_plan(ctx, C, A, B, beta, *pl, opts);
+  }
+  TT_TRY(st);
   plan_put(ctx, key, pl);
   out = pl;
   return TT_OK;

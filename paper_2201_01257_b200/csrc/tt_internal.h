@@ -97,17 +97,31 @@ struct Arena {
     live = high = need = 0;
     ++gen;
   }
-  bool take(int64_t n, int64_t* off) {                  // first fit
-    for (auto it = free_.begin(); it != free_.end(); ++it) {
-      if (it->second < n) continue;
-      *off = it->first;
-      const int64_t rest = it->second - n, at = it->first + n;
+  // first fit from the bottom (plans: short-lived, evictable), or last fit from the top (long-lived
+  // tensor metadata and scratch), so that the pinned regions do not fragment the plans' space
+  bool take(int64_t n, int64_t* off, bool top = false) {
+    auto fits = [&](std::map<int64_t, int64_t>::iterator it) {
+      const int64_t blo = it->first, blen = it->second;
+      *off = top ? blo + blen - n : blo;
       free_.erase(it);
-      if (rest > 0) free_[at] = rest;
+      if (top) {
+        if (blen > n) free_[blo] = blen - n;
+      } else if (blen > n) {
+        free_[blo + n] = blen - n;
+      }
       live += n;
       if (live > high) high = live;
       return true;
+    };
+    if (top) {
+      for (auto it = free_.end(); it != free_.begin();) {
+        --it;
+        if (it->second >= n) return fits(it);
+      }
+      return false;
     }
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+      if (it->second >= n) return fits(it);
     return false;
   }
   void give(int64_t off, int64_t n) {                   // back to the free list, coalescing
@@ -132,16 +146,19 @@ struct Arena {
 struct DevMem {
   tt_ctx ctx = nullptr;
   uint64_t gen = 0;
+  bool top = false;            // long-lived owner: allocated from the top of the workspace
   std::vector<std::pair<int64_t, int64_t>> regions;
   DevMem() = default;
   DevMem(const DevMem&) = delete;
   DevMem& operator=(const DevMem&) = delete;
-  DevMem(DevMem&& o) noexcept : ctx(o.ctx), gen(o.gen), regions(std::move(o.regions)) { o.regions.clear(); }
+  explicit DevMem(bool long_lived) : top(long_lived) {}
+  DevMem(DevMem&& o) noexcept : ctx(o.ctx), gen(o.gen), top(o.top), regions(std::move(o.regions)) { o.regions.clear(); }
   DevMem& operator=(DevMem&& o) noexcept {
     if (this != &o) {
       release();
       ctx = o.ctx;
       gen = o.gen;
+      top = o.top;
       regions = std::move(o.regions);
       o.regions.clear();
     }
@@ -200,7 +217,7 @@ struct tt_tensor_s {
   uint8_t* d_nz = nullptr;
   int64_t* d_blk_off = nullptr;
   std::vector<int64_t*> d_toff;   // per dim tile offsets on the device
-  tt::DevMem mem;                  // workspace regions of the device metadata above
+  tt::DevMem mem{true};            // workspace regions of the device metadata above (long-lived)
   bool dev_ready = false;
   bool dev_off_stale = false;      // storage offsets changed since the last upload
   // row-range ownership (SURVEY §8(e) block splitting): a split block is owned by parts, each a
@@ -277,7 +294,7 @@ struct tt_ctx_s {
   std::vector<std::shared_ptr<void>>* plan_sink = nullptr;   // scheduler capture: keeps every plan it uses alive
   int32_t graph_pins = 0;                                // captured graphs reading workspace pointers
   tt::Arena ws;                                          // the bound device workspace
-  tt::DevMem scratch;                                    // context scratch (d_scalar)
+  tt::DevMem scratch{true};                              // context scratch (d_scalar)
   std::set<tt_tensor_s*> tensors;                        // live tensors (their metadata lives in ws)
   double* d_scalar = nullptr;                            // scratch for scalar results
   double* d_partials = nullptr;

@@ -87,7 +87,7 @@ struct tt_sched_s {
   cudaGraphExec_t exec = nullptr;
   int32_t graph_levels = 0;
   double* d_results = nullptr;       // device slots of the scalar ops of the graph (in the workspace)
-  tt::DevMem mem;                    // ... their workspace region
+  tt::DevMem mem{true};              // ... their workspace region (long-lived)
   std::vector<std::shared_ptr<void>> held;   // every plan the graph reads: never evicted while it lives
   bool pinned = false;               // counted in ctx->graph_pins (the workspace cannot be re-bound)
   std::vector<double*> h_targets;    // their host destinations

@@ -659,3 +659,29 @@ def test_variants_bitwise_equal(env, name):
         outs.append(got)
     os.environ.pop("TT_FORCE_VARIANT", None)
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+def _vec_problem(spin):
+    spaces = {"O": SpaceSpec(6, tile=2, spin_split=spin), "V": SpaceSpec(10, tile=3, spin_split=spin),
+              "L": SpaceSpec(23, tile=7)}
+    ls = {"f": "V", "a": "V", "e": "V", "m": "O", "i": "O", "L": "L"}
+    sp = (lambda up, lo: ("spin", up, lo)) if spin else (lambda up, lo: None)
+    tensors = {"T1": TensorSpec("fm", sp([0], [1])), "Xov": TensorSpec("mfL", sp([0], [1])),
+               "g": TensorSpec("L"), "X": TensorSpec("aeL", sp([0], [1])), "F": TensorSpec("ae", sp([0], [1])),
+               "Xvo": TensorSpec("aiL", sp([0], [1])), "R1": TensorSpec("ai", sp([0], [1]))}
+    ops = [("g", "L", "T1", "fm", "Xov", "mfL"),       # A without free labels: M = 1
+           ("F", "ae", "X", "aeL", "g", "L"),          # B without free labels: N = 1
+           ("R1", "ai", "g", "L", "Xvo", "aiL")]       # A without free labels, K = 1 group
+    return Problem(spaces, ls, tensors, ops)
+
+
+@pytest.mark.parametrize("spin", [False, True])
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_vector_shaped_contractions(env, spin, k):
+    """Matrix-vector shapes of the Cholesky-factorized CCSD terms (g(L) = sum_mf t_m^f X(m,f,L),
+    F(a,e) += sum_L X(a,e,L) g(L)): an operand or the output without free labels on one GEMM side."""
+    tt, torch = env
+    pb = _vec_problem(spin)
+    ctx = new_ctx(tt, torch)
+    got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[k], alpha=0.5, beta=1.0)
+    assert normwise(got, ref) <= TOL, normwise(got, ref)

@@ -101,7 +101,7 @@ def test_small_workspace_evicts_and_matches():
     big.sync()
     need = big.workspace_info()["high"]
     big.close()
-    small = tt.Context(device=0, stream=st, workspace_bytes=max(64 << 10, need // 3))
+    small = tt.Context(device=0, stream=st, workspace_bytes=need * 6 // 10)   # holds the largest plan, not all
     _, Ps, ks, _ = _setup(tt, torch, small, pb)
     got = _run_all(tt, small, pb, Ps)
     small.sync()
