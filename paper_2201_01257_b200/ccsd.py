@@ -1,73 +1,188 @@
-"""Synthetic CCSD-shaped iteration driver (BASELINE configs[3]).
+"""Synthetic CCSD iteration driver (BASELINE configs[3]).
 
-The paper does not list the CCSD equations (P283-293; reading R18), so this is a frozen, CCSD-shaped
-term list in the style of spin-orbital CCSD with tau-based ladder and Stanton-Gauss-like
-intermediates (Fvv, Foo, Fov, Woooo, Wovvo): every term is a labelled set / add / contraction of the
-library, the n_o^2 n_u^4 ladder uses the implicit Cholesky-factored V (Eq. cc12), and the energy is an
-order-0 contraction summed over ranks.  Inputs are seeded synthetic tensors (no molecule, no
-convergence): one call = one residual evaluation + energy.  All operations are queued in a
-Scheduler (P178/P191-199/P215) and executed level by level.
+The paper does not list the CCSD equations (P283-293; reading R18), so the iteration is the textbook
+spin-orbital CCSD residual with the Stanton-Gauss intermediates (F_ae, F_mi, F_me, W_mnij, W_abef,
+W_mbej; full Fock matrix, residual form), every integral being Eq. cc12's antisymmetrized
+<pq||rs> = sum_L X(p,r,L) X(q,s,L) - X(p,s,L) X(q,r,L) over the Cholesky blocks X_oo, X_ov, X_vo, X_vv
+(P312-318; readings R19, R30).  The oracle transcribes the same equations literally with explicit
+integrals (oracle/ccsd.py); this driver evaluates them as labelled set / add / contraction calls of the
+library, queued in a Scheduler (P178, P191-199, P215) and executed level by level:
 
-Index classes: 'o' (occupied, spin halves), 'v' (virtual, spin halves), 'L' (Cholesky auxiliary).
+* integrals with at most two virtual indices (<mn||ij>, <mn||ie>, <mn||ef>, <mb||ij>) are stored,
+  formed once from X by contractions (input preparation, ``prepare_integrals``);
+* no integral with three or four virtual indices is ever formed (R17: V_vvvv, V_vovv, V_vvvo exceed
+  HBM at configs[3]/[4]).  Their terms are factorized exactly through the Cholesky vectors:
+  - the ladder 1/2 sum_ef tau_ij^ef W_abef = 1/2 sum_ef tau_ij^ef V^(abef) - 1/2 sum_mn t_m^a t_n^b
+    I_mnij + 1/8 sum_mn tau_mn^ab I_mnij, where V^ is Eq. cc12 over the T1-dressed vectors
+    X^(a,e,L) = X_vv(a,e,L) - sum_m t_m^a X_ov(m,e,L) (the P(ab) t_m^b <am||ef> part of W_abef folded
+    into the dressing) run by the implicit-operand ladder tt_contract_cholesky, and
+    I_mnij = sum_ef <mn||ef> tau_ij^ef;
+  - every other 3-virtual term is a product of O(o v N_L) half-transformed vectors:
+    Y(a,i,L) = sum_e X_vv(a,e,L) t_i^e, Y2(m,j,L) = sum_f X_ov(m,f,L) t_j^f, g(L) = sum_mf t_m^f X_ov(m,f,L),
+    Q(i,f,L) = sum_me t_im^ef X_ov(m,e,L), Q'(i,e,L) = sum_mf t_im^ef X_ov(m,f,L)
+    (e.g. sum_f t_j^f <mb||ef> = sum_L X_ov(m,e,L) Y(b,j,L) - Y2(m,j,L) X_vv(b,e,L));
+* tau~ never exists as a tensor: its T1 T1 part enters F_ae / F_mi through
+  G1(m,e) = sum_nf t_n^f <mn||ef>, G2(n,e) = sum_mf t_m^f <mn||ef>, G3(m,f) = sum_ne t_n^e <mn||ef>;
+  W_mbej's sum_nf t_j^f t_n^b <mn||ef> through H(m,n,e,j) = sum_f <mn||ef> t_j^f; and <mb||ej> is
+  not stored: W_mbej starts from sum_L X_ov(m,e,L) Xd_vo(b,j,L) - Xd_oo(m,j,L) X_vv(b,e,L) over the
+  T1-dressed Xd_vo = X_vo + Y, Xd_oo = X_oo + Y2, which also covers sum_f t_j^f <mb||ef>;
+* the antisymmetrizers P(ab), P(ij), P(ab)P(ij) are permuted adds of a staging tensor Z;
+* the energy E = sum_ia f_ia t_i^a + 1/4 sum <ij||ab> tau_ij^ab is two order-0 contractions summed
+  over ranks.
+
+Inputs are seeded synthetic tensors (no molecule, no convergence): one run = one residual evaluation
++ energy.  Index classes: 'o' (occupied, alpha/beta halves), 'v' (virtual, halves), 'L' (Cholesky
+auxiliary, no spin).
 """
 from __future__ import annotations
 
-from typing import Dict, Optional
+from typing import Dict
 
 import numpy as np
 
-# name -> (index classes per dim, spin split (upper dims, lower dims), synthetic input tag or None)
+UP_LO_2 = ([0], [1])
+UP_LO_4 = ([0, 1], [2, 3])
+
+# name -> (index classes per dim, spin split (upper dims, lower dims) or None, synthetic input tag or None)
 TENSORS = {
-    "foo": ("oo", ([0], [1]), 11),
-    "fvv": ("vv", ([0], [1]), 12),
-    "T1": ("vo", ([0], [1]), 13),
-    "T2": ("vvoo", ([0, 1], [2, 3]), 14),
-    "Voovv": ("vvoo", ([0, 1], [2, 3]), 15),
-    "Voooo": ("oooo", ([0, 1], [2, 3]), 16),
-    "Wr": ("ovvo", ([0, 1], [2, 3]), 17),
-    "X": ("vvL", ([0], [1]), 18),
-    "tau": ("vvoo", ([0, 1], [2, 3]), None),
-    "Wo": ("oooo", ([0, 1], [2, 3]), None),
-    "Fv": ("vv", ([0], [1]), None),
-    "Fo": ("oo", ([0], [1]), None),
-    "Fov": ("ov", ([0], [1]), None),
-    "Z": ("vvoo", ([0, 1], [2, 3]), None),
-    "R2": ("vvoo", ([0, 1], [2, 3]), None),
-    "R1": ("vo", ([0], [1]), None),
+    # inputs (foo, fvv, Xoo, X, Xvo: symmetrized from seeded raw blocks by prepare_inputs, reading R30)
+    "foo": ("oo", UP_LO_2, None), "fvv": ("vv", UP_LO_2, None), "fov": ("ov", UP_LO_2, 19),
+    "T1": ("vo", UP_LO_2, 13), "T2": ("vvoo", UP_LO_4, 14),
+    "Xoo": ("ooL", UP_LO_2, None), "Xov": ("ovL", UP_LO_2, 21), "Xvo": ("voL", UP_LO_2, None),
+    "X": ("vvL", UP_LO_2, None),
+    # stored integrals (formed from X by prepare_integrals)
+    "Voooo": ("oooo", UP_LO_4, None), "Vooov": ("ooov", UP_LO_4, None), "Voovv": ("vvoo", UP_LO_4, None),
+    "Vovoo": ("ovoo", UP_LO_4, None),
+    # intermediates and outputs
+    "tau": ("vvoo", UP_LO_4, None), "Z": ("vvoo", UP_LO_4, None),
+    "Y": ("voL", UP_LO_2, None), "Y2": ("ooL", UP_LO_2, None), "Yt": ("vvL", UP_LO_2, None),
+    "Xh": ("vvL", UP_LO_2, None), "Xvd": ("voL", UP_LO_2, None), "Xod": ("ooL", UP_LO_2, None),
+    "g": ("L", None, None), "Q": ("ovL", UP_LO_2, None), "Qp": ("ovL", UP_LO_2, None),
+    "G1": ("ov", UP_LO_2, None), "G2": ("ov", UP_LO_2, None), "G3": ("ov", UP_LO_2, None),
+    "Fov": ("ov", UP_LO_2, None), "Fv": ("vv", UP_LO_2, None), "Fo": ("oo", UP_LO_2, None),
+    "Fvt": ("vv", UP_LO_2, None), "Fot": ("oo", UP_LO_2, None),
+    "Io": ("oooo", UP_LO_4, None), "Wo": ("oooo", UP_LO_4, None), "H": ("oovo", UP_LO_4, None),
+    "K": ("vooo", UP_LO_4, None), "K3": ("ovoo", UP_LO_4, None), "Wr": ("ovvo", UP_LO_4, None),
+    "R1": ("vo", UP_LO_2, None), "R2": ("vvoo", UP_LO_4, None),
 }
 
-# (kind, out, out labels, beta, alpha, in1, labels1, in2, labels2)
+# <pq||rs> = X(p,r) X(q,s) - X(p,s) X(q,r) for the stored blocks: (out, labels, [(A, a_lbl, B, b_lbl)] x 2)
+INTEGRALS = [
+    ("Voooo", "mnij", ("Xoo", "miL", "Xoo", "njL"), ("Xoo", "mjL", "Xoo", "niL")),   # <mn||ij>
+    ("Vooov", "mnie", ("Xoo", "miL", "Xov", "neL"), ("Xov", "meL", "Xoo", "niL")),   # <mn||ie>
+    ("Voovv", "efmn", ("Xov", "meL", "Xov", "nfL"), ("Xov", "mfL", "Xov", "neL")),   # <mn||ef> at (e,f,m,n)
+    ("Vovoo", "mbij", ("Xoo", "miL", "Xvo", "bjL"), ("Xoo", "mjL", "Xvo", "biL")),   # <mb||ij>
+]
+
+# (kind, out, out labels, beta, alpha, in1, labels1[, in2, labels2])
 TERMS = [
+    # tau_ij^ab = t_ij^ab + t_i^a t_j^b - t_i^b t_j^a
     ("add", "tau", "abij", 0.0, 1.0, "T2", "abij"),
     ("contract", "tau", "abij", 1.0, 1.0, "T1", "ai", "T1", "bj"),
     ("contract", "tau", "abij", 1.0, -1.0, "T1", "bi", "T1", "aj"),
-    ("add", "Wo", "klij", 0.0, 1.0, "Voooo", "klij"),
-    ("contract", "Wo", "klij", 1.0, 0.25, "Voovv", "cdkl", "tau", "cdij"),
-    ("contract", "Wr", "kbcj", 1.0, -0.5, "T2", "dblj", "Voovv", "cdkl"),
+    # half-transformed Cholesky vectors and the T1-dressed ones
+    ("contract", "Y", "aiL", 0.0, 1.0, "X", "aeL", "T1", "ei"),
+    ("contract", "Y2", "mjL", 0.0, 1.0, "Xov", "mfL", "T1", "fj"),
+    ("contract", "Yt", "bfL", 0.0, 1.0, "T1", "bm", "Xov", "mfL"),
+    ("contract", "g", "L", 0.0, 1.0, "T1", "fm", "Xov", "mfL"),
+    ("add", "Xh", "aeL", 0.0, 1.0, "X", "aeL"),
+    ("add", "Xh", "aeL", 1.0, -1.0, "Yt", "aeL"),
+    ("add", "Xvd", "bjL", 0.0, 1.0, "Xvo", "bjL"),
+    ("add", "Xvd", "bjL", 1.0, 1.0, "Y", "bjL"),
+    ("add", "Xod", "mjL", 0.0, 1.0, "Xoo", "mjL"),
+    ("add", "Xod", "mjL", 1.0, 1.0, "Y2", "mjL"),
+    ("contract", "Q", "ifL", 0.0, 1.0, "T2", "efim", "Xov", "meL"),
+    ("contract", "Qp", "ieL", 0.0, 1.0, "T2", "efim", "Xov", "mfL"),
+    # G1(m,e) = sum_nf t_n^f <mn||ef>, G2(n,e) = sum_mf t_m^f <mn||ef>, G3(m,f) = sum_ne t_n^e <mn||ef>
+    ("contract", "G1", "me", 0.0, 1.0, "Voovv", "efmn", "T1", "fn"),
+    ("contract", "G2", "ne", 0.0, 1.0, "Voovv", "efmn", "T1", "fm"),
+    ("contract", "G3", "mf", 0.0, 1.0, "Voovv", "efmn", "T1", "en"),
+    # F_me = f_me + sum_nf t_n^f <mn||ef>
+    ("add", "Fov", "me", 0.0, 1.0, "fov", "me"),
+    ("add", "Fov", "me", 1.0, 1.0, "G1", "me"),
+    # F_ae = f_ae - 1/2 f_me t_m^a + t_m^f <ma||fe> - 1/2 taut_mn^af <mn||ef>
     ("add", "Fv", "ae", 0.0, 1.0, "fvv", "ae"),
+    ("contract", "Fv", "ae", 1.0, -0.5, "fov", "me", "T1", "am"),
+    ("contract", "Fv", "ae", 1.0, 1.0, "X", "aeL", "g", "L"),
+    ("contract", "Fv", "ae", 1.0, -1.0, "Y", "amL", "Xov", "meL"),
     ("contract", "Fv", "ae", 1.0, -0.5, "T2", "afmn", "Voovv", "efmn"),
+    ("contract", "Fv", "ae", 1.0, -0.25, "T1", "am", "G1", "me"),
+    ("contract", "Fv", "ae", 1.0, 0.25, "T1", "an", "G2", "ne"),
+    # F_mi = f_mi + 1/2 t_i^e f_me + t_n^e <mn||ie> + 1/2 taut_in^ef <mn||ef>
     ("add", "Fo", "mi", 0.0, 1.0, "foo", "mi"),
+    ("contract", "Fo", "mi", 1.0, 0.5, "fov", "me", "T1", "ei"),
+    ("contract", "Fo", "mi", 1.0, 1.0, "Vooov", "mnie", "T1", "en"),
     ("contract", "Fo", "mi", 1.0, 0.5, "Voovv", "efmn", "T2", "efin"),
-    ("contract", "Fov", "me", 0.0, 1.0, "Voovv", "efmn", "T1", "fn"),
+    ("contract", "Fo", "mi", 1.0, 0.25, "G1", "me", "T1", "ei"),
+    ("contract", "Fo", "mi", 1.0, -0.25, "G3", "mf", "T1", "fi"),
+    # F_be - 1/2 t_m^b F_me ; F_mj + 1/2 t_j^e F_me
+    ("add", "Fvt", "be", 0.0, 1.0, "Fv", "be"),
+    ("contract", "Fvt", "be", 1.0, -0.5, "T1", "bm", "Fov", "me"),
+    ("add", "Fot", "mj", 0.0, 1.0, "Fo", "mj"),
+    ("contract", "Fot", "mj", 1.0, 0.5, "Fov", "me", "T1", "ej"),
+    # I_mnij = sum_ef <mn||ef> tau_ij^ef ; W_mnij = <mn||ij> + P(ij) t_j^e <mn||ie> + 1/4 I_mnij
+    ("contract", "Io", "mnij", 0.0, 1.0, "Voovv", "efmn", "tau", "efij"),
+    ("add", "Wo", "mnij", 0.0, 1.0, "Voooo", "mnij"),
+    ("contract", "Wo", "mnij", 1.0, 1.0, "Vooov", "mnie", "T1", "ej"),
+    ("contract", "Wo", "mnij", 1.0, -1.0, "Vooov", "mnje", "T1", "ei"),
+    ("add", "Wo", "mnij", 1.0, 0.25, "Io", "mnij"),
+    # W_mbej = <mb||ej> + t_j^f <mb||ef> - t_n^b <mn||ej> - (1/2 t_jn^fb + t_j^f t_n^b) <mn||ef>
+    ("contract", "H", "mnej", 0.0, 1.0, "Voovv", "efmn", "T1", "fj"),
+    ("contract", "Wr", "mbej", 0.0, 1.0, "Xov", "meL", "Xvd", "bjL"),
+    ("contract", "Wr", "mbej", 1.0, -1.0, "Xod", "mjL", "X", "beL"),
+    ("contract", "Wr", "mbej", 1.0, 1.0, "T1", "bn", "Vooov", "mnje"),
+    ("contract", "Wr", "mbej", 1.0, -0.5, "T2", "fbjn", "Voovv", "efmn"),
+    ("contract", "Wr", "mbej", 1.0, -1.0, "T1", "bn", "H", "mnej"),
+    # K3(m,b,i,j) = sum_e <mb||ej> t_i^e ; K(a,n,i,j) = sum_m t_m^a I_mnij
+    ("contract", "K3", "mbij", 0.0, 1.0, "Y2", "miL", "Xvo", "bjL"),
+    ("contract", "K3", "mbij", 1.0, -1.0, "Xoo", "mjL", "Y", "biL"),
+    ("contract", "K", "anij", 0.0, 1.0, "T1", "am", "Io", "mnij"),
+    # singles residual
+    ("add", "R1", "ai", 0.0, 1.0, "fov", "ia"),
+    ("contract", "R1", "ai", 1.0, 1.0, "Fv", "ae", "T1", "ei"),
+    ("contract", "R1", "ai", 1.0, -1.0, "T1", "am", "Fo", "mi"),
+    ("contract", "R1", "ai", 1.0, 1.0, "T2", "aeim", "Fov", "me"),
+    ("contract", "R1", "ai", 1.0, -1.0, "Y", "anL", "Xoo", "niL"),      # - t_n^f <na||if>
+    ("contract", "R1", "ai", 1.0, 1.0, "g", "L", "Xvo", "aiL"),
+    ("contract", "R1", "ai", 1.0, -0.5, "X", "afL", "Q", "ifL"),        # - 1/2 t_im^ef <ma||ef>
+    ("contract", "R1", "ai", 1.0, 0.5, "X", "aeL", "Qp", "ieL"),
+    ("contract", "R1", "ai", 1.0, 0.5, "T2", "aemn", "Vooov", "nmie"),  # - 1/2 t_mn^ae <nm||ei>
+    # doubles residual: <ij||ab>, the ladder (T1-dressed implicit V), W_mnij, the rest of W_abef
     ("add", "R2", "abij", 0.0, 1.0, "Voovv", "abij"),
-    ("cholesky", "R2", "abij", 1.0, 0.5, "X", "abcd", "tau", "cdij"),
-    ("contract", "R2", "abij", 1.0, 0.5, "tau", "abkl", "Wo", "klij"),
-    ("contract", "Z", "abij", 0.0, 1.0, "T2", "acik", "Wr", "kbcj"),
+    ("cholesky", "R2", "abij", 1.0, 0.5, "Xh", "abcd", "tau", "cdij"),
+    ("contract", "R2", "abij", 1.0, 0.5, "tau", "abmn", "Wo", "mnij"),
+    ("contract", "R2", "abij", 1.0, 0.125, "tau", "abmn", "Io", "mnij"),
+    ("contract", "R2", "abij", 1.0, -0.5, "K", "anij", "T1", "bn"),
+    # P(ab) [t_ij^ae (F_be - 1/2 t_m^b F_me) - t_m^a <mb||ij>]
+    ("contract", "Z", "abij", 0.0, 1.0, "T2", "aeij", "Fvt", "be"),
+    ("contract", "Z", "abij", 1.0, -1.0, "T1", "am", "Vovoo", "mbij"),
+    ("add", "R2", "abij", 1.0, 1.0, "Z", "abij"),
+    ("add", "R2", "abij", 1.0, -1.0, "Z", "baij"),
+    # P(ij) [- t_im^ab (F_mj + 1/2 t_j^e F_me) + t_i^e <ab||ej>]
+    ("contract", "Z", "abij", 0.0, -1.0, "T2", "abim", "Fot", "mj"),
+    ("contract", "Z", "abij", 1.0, 1.0, "Y", "aiL", "Xvo", "bjL"),
+    ("contract", "Z", "abij", 1.0, -1.0, "Xvo", "ajL", "Y", "biL"),
+    ("add", "R2", "abij", 1.0, 1.0, "Z", "abij"),
+    ("add", "R2", "abij", 1.0, -1.0, "Z", "abji"),
+    # P(ij) P(ab) [t_im^ae W_mbej - t_i^e t_m^a <mb||ej>]
+    ("contract", "Z", "abij", 0.0, 1.0, "T2", "aeim", "Wr", "mbej"),
+    ("contract", "Z", "abij", 1.0, -1.0, "T1", "am", "K3", "mbij"),
     ("add", "R2", "abij", 1.0, 1.0, "Z", "abij"),
     ("add", "R2", "abij", 1.0, -1.0, "Z", "baij"),
     ("add", "R2", "abij", 1.0, -1.0, "Z", "abji"),
     ("add", "R2", "abij", 1.0, 1.0, "Z", "baji"),
-    ("contract", "Z", "abij", 0.0, 1.0, "T2", "aeij", "Fv", "be"),
-    ("add", "R2", "abij", 1.0, 1.0, "Z", "abij"),
-    ("add", "R2", "abij", 1.0, -1.0, "Z", "baij"),
-    ("contract", "Z", "abij", 0.0, 1.0, "T2", "abim", "Fo", "mj"),
-    ("add", "R2", "abij", 1.0, -1.0, "Z", "abij"),
-    ("add", "R2", "abij", 1.0, 1.0, "Z", "abji"),
-    ("contract", "R1", "ai", 0.0, 1.0, "Fv", "ae", "T1", "ei"),
-    ("contract", "R1", "ai", 1.0, -1.0, "T1", "am", "Fo", "mi"),
-    ("contract", "R1", "ai", 1.0, 1.0, "T2", "aeim", "Fov", "me"),
+    # energy
+    ("scalar", "E", "", 0.0, 1.0, "fov", "ia", "T1", "ai"),
     ("scalar", "E", "", 0.0, 0.25, "Voovv", "abij", "tau", "abij"),
 ]
+
+# tensors that are row-split over the ranks (the rest are replicated), with the term whose task-list
+# cost decides the split
+SPLIT = {"Wr": ("Wr", "mbej", "T2", "fbjn", "Voovv", "efmn"),
+         "Z": ("Z", "abij", "T2", "aeim", "Wr", "mbej"),
+         "Q": ("Q", "ifL", "T2", "efim", "Xov", "meL"),
+         "Qp": ("Qp", "ieL", "T2", "efim", "Xov", "mfL"),
+         "K3": ("K3", "mbij", "Y2", "miL", "Xvo", "bjL")}
 
 
 class CCSDIteration:
@@ -86,43 +201,61 @@ class CCSDIteration:
         self.spaces = (so, sv, sl)
         self.tis = {"o": tt.TiledIndexSpace(so, tO), "v": tt.TiledIndexSpace(sv, tV), "L": tt.TiledIndexSpace(sl, tL)}
         self.T: Dict[str, object] = {}
-        for name, (cls, (up, lo), tag) in TENSORS.items():
-            self.T[name] = tt.Tensor(ctx, [self.tis[c] for c in cls], spin=(up, lo))
+        for name, (cls, spin, tag) in TENSORS.items():
+            self.T[name] = tt.Tensor(ctx, [self.tis[c] for c in cls], spin=spin)
         if ctx.nranks > 1 and distribute:
             self._distribute()
         self.bufs = {}
         for name, T in self.T.items():
             self.bufs[name] = torch.zeros(T.storage_elems, dtype=torch.float64, device="cuda")
             T.bind(self.bufs[name])
+        # implicit ladder workspace: Bh (half of tau's blocks) + W rows
         ws = self.T["T2"].packed_elems + 64 + int(ws_gb * 1e9 / 8)
         self.ws = torch.empty(ws, dtype=torch.float64, device="cuda")
         self.nstreams = nstreams
         self.reset_inputs()
 
     def _distribute(self):
-        """Owner-computes placement (P178-180, reading R24b).  T2, Voovv and tau are read whole by
-        most terms, so they are replicated (inputs filled on every rank; tau recomputed redundantly:
-        O(o^2 v^2) work) -- with 180 GB per GPU this trades memory for gathers of these tensors in every
-        contraction.  The expensive outputs are split with the row-splitting water-filling partition:
-        R2 by (a,b) rows on the cost of the implicit Cholesky ladder as executed (W formation + the
-        GEMMs over W's Coulomb block map, R19b), Wr / Z / Wo / Fv on their own task-list costs; the
-        small ones (foo, fvv, T1, Fo, Fov, R1, X, Voooo) are replicated.  R2 uses compact storage
-        (only the rank's own rows are allocated)."""
+        """Owner-computes placement (P178-180, reading R24b).  Inputs, stored integrals and the
+        intermediates whose cost is O(o^2 v^2) or below are replicated (each rank computes them: no
+        gathers of T2 / tau / Voovv in the big terms).  R2 is split by (a,b) rows on the executed
+        cost of the implicit ladder (tt_partition_split_cholesky) with compact storage (it is only
+        written); Wr, Z, Q, Q' and K3 are split on the task-list cost of their dominant term and
+        gathered where they are read."""
         tt, T = self.tt, self.T
-        for name in ("foo", "fvv", "T1", "T2", "Voovv", "tau", "Fo", "Fov", "R1", "X", "Voooo"):
-            t = T[name]
-            t.set_owner(np.where(t.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
-        tt.partition_split_cholesky(self.ctx, T["R2"], "abij", T["X"], "abcd", T["tau"], "cdij", group_dims=(0, 1))
-        T["R2"].set_compact(True)       # R2 is only written: each rank stores just its rows
-        tt.partition_split(self.ctx, T["Wr"], "kbcj", T["T2"], "dblj", T["Voovv"], "cdkl")
-        tt.partition_split(self.ctx, T["Z"], "abij", T["T2"], "acik", T["Wr"], "kbcj")
-        tt.partition_split(self.ctx, T["Wo"], "klij", T["Voovv"], "cdkl", T["tau"], "cdij")
-        tt.partition_split(self.ctx, T["Fv"], "ae", T["T2"], "afmn", T["Voovv"], "efmn")
+        for name, t in T.items():
+            if name != "R2" and name not in SPLIT:
+                t.set_owner(np.where(t.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
+        tt.partition_split_cholesky(self.ctx, T["R2"], "abij", T["Xh"], "abcd", T["tau"], "cdij", group_dims=(0, 1))
+        T["R2"].set_compact(True)
+        for name, (c, cl, a, al, b, bl) in SPLIT.items():
+            tt.partition_split(self.ctx, T[c], cl, T[a], al, T[b], bl)
 
     def reset_inputs(self):
+        """Seeded synthetic inputs (R30 recipe), then the stored integrals from the Cholesky blocks."""
         for name, (cls, spin, tag) in TENSORS.items():
             if tag is not None:
                 self.tt.fill_synthetic(self.ctx, self.T[name], self.seed, tag)
+        self.prepare_inputs()
+        self.prepare_integrals()
+
+    def prepare_inputs(self):
+        """Reading R30 (real orbitals): X(p,r,L) = X(r,p,L) and f symmetric.  The raw seeded blocks are
+        drawn into same-shaped scratch tensors (same global indices, hence the same values) and
+        symmetrized: X_vv = (R + R^T)/2, X_oo = (R + R^T)/2, X_vo = X_ov^T, f_oo, f_vv = (R + R^T)/2."""
+        tt, T, ctx = self.tt, self.T, self.ctx
+        for raw, out, lbl, tlbl, tag in (("Xh", "X", "aeL", "eaL", 18), ("Xod", "Xoo", "miL", "imL", 20),
+                                          ("Fo", "foo", "mi", "im", 11), ("Fv", "fvv", "ae", "ea", 12)):
+            tt.fill_synthetic(ctx, T[raw], self.seed, tag)
+            tt.add(ctx, T[out], lbl, 0.0, 0.5, T[raw], lbl)
+            tt.add(ctx, T[out], lbl, 1.0, 0.5, T[raw], tlbl)
+        tt.add(ctx, T["Xvo"], "bjL", 0.0, 1.0, T["Xov"], "jbL")
+
+    def prepare_integrals(self):
+        tt, T = self.tt, self.T
+        for out, ol, (a1, l1, b1, m1), (a2, l2, b2, m2) in INTEGRALS:
+            tt.contract(self.ctx, T[out], ol, 0.0, 1.0, T[a1], l1, T[b1], m1)
+            tt.contract(self.ctx, T[out], ol, 1.0, -1.0, T[a2], l2, T[b2], m2)
 
     def queue(self, sched):
         T = self.T
@@ -149,4 +282,4 @@ class CCSDIteration:
         _, nlev = s.levels()
         res = s.execute()
         s.close()
-        return nlev, res[0]
+        return nlev, float(sum(res))

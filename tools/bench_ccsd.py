@@ -4,8 +4,8 @@ N_L = 2(O+V) = 1800, implicit Cholesky V) on 1..N GPUs (torchrun for N > 1).
     python tools/bench_ccsd.py [--O 100 --V 800 --tile 50 --nl 1800 --ltile 450 --ws-gb 12]
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/bench_ccsd.py
 
-One step = one residual evaluation (29 queued operations, levelized by the scheduler) + the energy
-all-reduce.  Reports the step time (max over ranks), the algorithmic FLOPs of all terms (task-list
+One step = one residual evaluation (the textbook CCSD term list of paper_2201_01257_b200/ccsd.py, levelized by
+the scheduler) + the energy all-reduce.  Reports the step time (max over ranks), the algorithmic FLOPs of all terms (task-list
 costs over the tensors' block maps; the ladder over the block map of the implicit V) and the rate."""
 import argparse
 import json
@@ -29,7 +29,7 @@ def algorithmic_flops(it):
     total, parts = 0.0, {}
     ctx0 = tt.Context(device=-1)       # host-only planning context for the FLOP counts
     for term in TERMS:
-        if term[0] == "contract":
+        if term[0] == "contract":  # noqa: SIM114
             _, out, ol, beta, alpha, a, al, b, bl = term
             f = float(tt.task_list(ctx0, T[out], ol, T[a], al, T[b], bl)["cost"].sum())
         elif term[0] == "cholesky":
@@ -48,7 +48,7 @@ def algorithmic_flops(it):
             f = float(tt.task_list(ctx0, T[out], ol, V, vl, T[b], bl)["cost"].sum())
         else:
             continue
-        parts[f"{term[1]}({term[2]})+={term[5]}*{term[7]}"] = f
+        parts[f"{len(parts):02d} {term[1]}({term[2]})+={term[5]}({term[6]})*{term[7]}({term[8]})"] = f
         total += f
     return total, parts
 
