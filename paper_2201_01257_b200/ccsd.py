@@ -55,7 +55,7 @@ TENSORS = {
     "Vovoo": ("ovoo", UP_LO_4, None),
     # intermediates and outputs
     "tau": ("vvoo", UP_LO_4, None), "Z": ("vvoo", UP_LO_4, None),
-    "Y": ("voL", UP_LO_2, None), "Y2": ("ooL", UP_LO_2, None), "Yt": ("vvL", UP_LO_2, None),
+    "Y": ("voL", UP_LO_2, None), "Y2": ("ooL", UP_LO_2, None),
     "Xh": ("vvL", UP_LO_2, None), "Xvd": ("voL", UP_LO_2, None), "Xod": ("ooL", UP_LO_2, None),
     "g": ("L", None, None), "Q": ("ovL", UP_LO_2, None), "Qp": ("ovL", UP_LO_2, None),
     "G1": ("ov", UP_LO_2, None), "G2": ("ov", UP_LO_2, None), "G3": ("ov", UP_LO_2, None),
@@ -83,10 +83,9 @@ TERMS = [
     # half-transformed Cholesky vectors and the T1-dressed ones
     ("contract", "Y", "aiL", 0.0, 1.0, "X", "aeL", "T1", "ei"),
     ("contract", "Y2", "mjL", 0.0, 1.0, "Xov", "mfL", "T1", "fj"),
-    ("contract", "Yt", "bfL", 0.0, 1.0, "T1", "bm", "Xov", "mfL"),
     ("contract", "g", "L", 0.0, 1.0, "T1", "fm", "Xov", "mfL"),
     ("add", "Xh", "aeL", 0.0, 1.0, "X", "aeL"),
-    ("add", "Xh", "aeL", 1.0, -1.0, "Yt", "aeL"),
+    ("contract", "Xh", "aeL", 1.0, -1.0, "T1", "am", "Xov", "meL"),
     ("add", "Xvd", "bjL", 0.0, 1.0, "Xvo", "bjL"),
     ("add", "Xvd", "bjL", 1.0, 1.0, "Y", "bjL"),
     ("add", "Xod", "mjL", 0.0, 1.0, "Xoo", "mjL"),
@@ -209,8 +208,8 @@ class CCSDIteration:
         for name, T in self.T.items():
             self.bufs[name] = torch.zeros(T.storage_elems, dtype=torch.float64, device="cuda")
             T.bind(self.bufs[name])
-        # implicit ladder workspace: Bh (half of tau's blocks) + W rows
-        ws = self.T["T2"].packed_elems + 64 + int(ws_gb * 1e9 / 8)
+        # implicit ladder workspace: Bh (tau's tile pairs c_t <= d_t: about half of tau) + W rows
+        ws = int(0.55 * self.T["T2"].packed_elems) + 64 + int(ws_gb * 1e9 / 8)
         self.ws = torch.empty(ws, dtype=torch.float64, device="cuda")
         self.nstreams = nstreams
         self.reset_inputs()

@@ -18,6 +18,7 @@
 #include "tt_launch.h"
 #include "tt_nccl.h"
 
+
 using namespace tt;
 
 namespace {
@@ -1488,6 +1489,7 @@ tt_status tt_tensor_bind(tt_tensor t, void* ptr, int64_t cap) {
 }
 
 tt_status tt_tensor_upload(tt_ctx ctx, tt_tensor t, const double* host) {
+  NvtxRange nvtx_("tt_tensor_upload");
   TT_TRY(need_device(ctx));
   if (!t || !host) return fail(TT_E_ARG, "NULL argument");
   TT_TRY(check_bound(t, "upload"));
@@ -1497,6 +1499,7 @@ tt_status tt_tensor_upload(tt_ctx ctx, tt_tensor t, const double* host) {
 }
 
 tt_status tt_tensor_download(tt_ctx ctx, tt_tensor t, double* host) {
+  NvtxRange nvtx_("tt_tensor_download");
   TT_TRY(need_device(ctx));
   if (!t || !host) return fail(TT_E_ARG, "NULL argument");
   TT_TRY(check_bound(t, "download"));
@@ -1689,6 +1692,7 @@ void reset_stats(tt_ctx ctx) { ctx->last = tt_stats{}; }
 extern "C" {
 
 tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag, int32_t kind) {
+  NvtxRange nvtx_("tt_fill_synthetic");
   TT_TRY(need_ws(ctx));
   if (!t) return fail(TT_E_ARG, "NULL tensor");
   if (kind != TT_KIND_UNIFORM && kind != TT_KIND_INTEGER) return fail(TT_E_ARG, "bad kind %d", kind);
@@ -1741,6 +1745,7 @@ tt_status tt_fill_synthetic(tt_ctx ctx, tt_tensor t, uint64_t seed, uint32_t tag
 }
 
 tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha) {
+  NvtxRange nvtx_("tt_set");
   TT_TRY(need_ws(ctx));
   if (!C) return fail(TT_E_ARG, "NULL tensor");
   TT_TRY(check_bound(C, "C"));
@@ -1784,6 +1789,7 @@ tt_status tt_set(tt_ctx ctx, tt_tensor C, double alpha) {
 }
 
 tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor A, const char* al) {
+  NvtxRange nvtx_("tt_add");
   if (!ctx || !C || !A) return fail(TT_E_ARG, "NULL argument");
   TT_TRY(check_labels(cl, C, "C"));
   TT_TRY(check_labels(al, A, "A"));
@@ -1868,6 +1874,7 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
 
 tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* al, tt_tensor B, const char* bl,
                              double* result) {
+  NvtxRange nvtx_("tt_contract_scalar");
   if (!ctx || !A || !B || !result) return fail(TT_E_ARG, "NULL argument");
   TT_TRY(check_labels(al, A, "A"));
   TT_TRY(check_labels(bl, B, "B"));
@@ -2466,6 +2473,7 @@ extern "C" {
 
 tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor A,
                       const char* al, tt_tensor B, const char* bl) {
+  NvtxRange nvtx_("tt_contract");
   if (!ctx) return fail(TT_E_ARG, "NULL context");
   std::shared_ptr<ContractPlan> pl;
   bool was_cached = false;
@@ -2538,6 +2546,7 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* cl, double beta, doub
 
 tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* cl, double beta, tt_tensor A, const char* al,
                                tt_tensor B, const char* bl) {
+  NvtxRange nvtx_("tt_contract_prefetch");
   if (!ctx) return fail(TT_E_ARG, "NULL context");
   std::shared_ptr<ContractPlan> pl;
   TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, pl, nullptr));
@@ -2999,6 +3008,7 @@ extern "C" {
 
 tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor X,
                                const char* vl, tt_tensor B, const char* bl, void* workspace, int64_t ws_elems) {
+  NvtxRange nvtx_("tt_contract_cholesky");
   if (!ctx) return fail(TT_E_ARG, "NULL context");
   std::vector<tt_tis> vdims;
   TT_TRY(chol_check(C, cl, X, vl, B, bl, vdims));
@@ -3398,6 +3408,7 @@ extern "C" {
 tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor A,
                        const char* al, tt_tensor B, const char* bl, tt_tensor D, const char* dl, void* workspace,
                        int64_t ws_elems, tt_contract3_info* info) {
+  NvtxRange nvtx_("tt_contract3");
   if (!ctx || !C || !A || !B || !D || !cl || !al || !bl || !dl) return fail(TT_E_ARG, "NULL argument");
   TT_TRY(check_labels(cl, C, "C"));
   TT_TRY(check_labels(al, A, "A"));
@@ -3600,6 +3611,7 @@ extern "C" {
 tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vooov, tt_tensor Vvovv,
                             tt_tensor Voovv, const double* eps_o, const double* eps_v, void* workspace,
                             int64_t ws_elems, double* energy, tt_triples_info* info) {
+  NvtxRange nvtx_("tt_triples_energy");
   if (!ctx || !T1 || !T2 || !Vooov || !Vvovv || !Voovv) return fail(TT_E_ARG, "NULL argument");
   if (T1->order != 2 || T2->order != 4 || Vooov->order != 4 || Vvovv->order != 4 || Voovv->order != 4)
     return fail(TT_E_ARG, "T1 (a,i) order 2; T2 (a,b,i,j), Vooov (i,j,m,a), Vvovv (e,i,a,b), Voovv (i,j,a,b) order 4");

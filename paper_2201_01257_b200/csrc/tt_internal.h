@@ -12,6 +12,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/tt.h"
 
@@ -267,6 +268,12 @@ struct tt_tensor_s {
     for (int d = 0; d < order; ++d) v *= dims[d]->size(c[d]);
     return v;
   }
+};
+
+// NVTX range per ABI call (visible in nsys / ncu --nvtx-include); header-only NVTX v3 (dlopen-based)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 struct ProfileRec {

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+
 #include "tt_internal.h"
 
 namespace {
@@ -329,6 +330,7 @@ static void drop_graph(tt_sched s) {
 }
 
 tt_status tt_sched_execute(tt_sched s) {
+  NvtxRange nvtx_("tt_sched_execute");
   if (!s) return set_error(TT_E_ARG, "NULL scheduler");
   tt_ctx ctx = s->ctx;
   if (ctx->device < 0) return set_error(TT_E_STATE, "host-only context cannot execute");
@@ -349,6 +351,7 @@ tt_status tt_sched_execute(tt_sched s) {
 }
 
 tt_status tt_sched_capture(tt_sched s) {
+  NvtxRange nvtx_("tt_sched_capture");
   if (!s) return set_error(TT_E_ARG, "NULL scheduler");
   tt_ctx ctx = s->ctx;
   if (ctx->device < 0) return set_error(TT_E_STATE, "host-only context cannot capture");
@@ -411,6 +414,7 @@ tt_status tt_sched_capture(tt_sched s) {
 }
 
 tt_status tt_sched_replay(tt_sched s) {
+  NvtxRange nvtx_("tt_sched_replay");
   if (!s) return set_error(TT_E_ARG, "NULL scheduler");
   if (!s->exec) return set_error(TT_E_STATE, "no captured graph (call tt_sched_capture)");
   tt_ctx ctx = s->ctx;

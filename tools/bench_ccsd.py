@@ -1,7 +1,7 @@
 """Synthetic CCSD-shaped iteration at BASELINE configs[3] scale (O=100 V=800 tile 50, alpha/beta maps,
 N_L = 2(O+V) = 1800, implicit Cholesky V) on 1..N GPUs (torchrun for N > 1).
 
-    python tools/bench_ccsd.py [--O 100 --V 800 --tile 50 --nl 1800 --ltile 450 --ws-gb 12]
+    python tools/bench_ccsd.py [--O 100 --V 800 --tile 50 --nl 1800 --ltile 450 --ws-gb 4]
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/bench_ccsd.py
 
 One step = one residual evaluation (the textbook CCSD term list of paper_2201_01257_b200/ccsd.py, levelized by
@@ -60,7 +60,7 @@ def main():
     ap.add_argument("--tile", type=int, default=50)
     ap.add_argument("--nl", type=int, default=1800)
     ap.add_argument("--ltile", type=int, default=450)
-    ap.add_argument("--ws-gb", type=float, default=12.0)
+    ap.add_argument("--ws-gb", type=float, default=4.0)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=2)   # >= 2: tt_contract autotunes on the first two calls
     a = ap.parse_args()
