@@ -298,6 +298,24 @@ tt_status tt_contract(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, d
  * contraction is already prefetched and not yet executed. */
 tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, tt_tensor A,
                                const char* a_lbl, tt_tensor B, const char* b_lbl);
+
+/* End-to-end contraction from HOST memory (P178-188 execution on host-resident data; the caller's
+ * pinned buffers give full overlap): hA, hB, hC are host copies of the packed STORAGE of A, B, C (the
+ * same layout as tt_tensor_upload; NULL = that operand is already resident on the device, no copy).
+ * c_flags: TT_HOST_C_IN uploads C first (needed when beta != 0 and C is not resident), TT_HOST_C_OUT
+ * downloads C after the contraction.  Device buffers of A, B, C must be bound (copy destinations).
+ * With nranks == 1 and A's dim 0 labelled like C's dim 0 (same tiled space; no views, A != B, C not
+ * compact) the call is PIPELINED: per dim-0 tile x of C, A's blocks with dim-0 coordinate x (one packed
+ * range) are copied host->device on the context's copy stream while tile x-1 contracts, and C's rows of
+ * tile x go back while tile x+1 contracts; each tile is computed by the same kernel and k order as the
+ * whole contraction, so the result is bitwise that of upload + tt_contract + download.  Otherwise every
+ * rank copies the ranges it holds (owned blocks / row parts, replicated blocks), runs tt_contract (the
+ * gathers fetch the rest over NVLink) and copies back its own C ranges.  Asynchronous on the context
+ * stream like tt_contract: the host buffers must stay valid until tt_sync.  Errors as tt_contract. */
+enum { TT_HOST_C_IN = 1, TT_HOST_C_OUT = 2 };
+tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha, tt_tensor A,
+                           const char* a_lbl, tt_tensor B, const char* b_lbl, const double* hA, const double* hB,
+                           double* hC, int32_t c_flags);
 tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* a_lbl, tt_tensor B,
                              const char* b_lbl, double* result);
 

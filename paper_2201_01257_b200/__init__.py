@@ -31,6 +31,7 @@ ERRORS = {-1: "TT_E_ARG", -2: "TT_E_COVERAGE", -3: "TT_E_LABEL", -4: "TT_E_TILIN
           -6: "TT_E_UNBOUND", -7: "TT_E_OOM", -8: "TT_E_CUDA", -9: "TT_E_NCCL", -10: "TT_E_STATE",
           -11: "TT_E_UNSUPPORTED", -12: "TT_E_WORKSPACE"}
 TT_E_WORKSPACE = -12
+HOST_C_IN, HOST_C_OUT = 1, 2
 # default device workspace per context (tt_workspace_bind): plan metadata and scratch; cached plans are
 # evicted least-recently-used when it is full.  Override with Context(workspace_bytes=...) or TT_WORKSPACE_MB.
 DEFAULT_WORKSPACE_BYTES = int(os.environ.get("TT_WORKSPACE_MB", "256")) << 20
@@ -114,6 +115,8 @@ _SIGS = {
     "tt_contract_cholesky": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
                              _i64],
     "tt_contract_prefetch": [_vp, _vp, ctypes.c_char_p, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p],
+    "tt_contract_host": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp, _vp,
+                         _vp, _i32],
     "tt_contract3": [_vp, _vp, ctypes.c_char_p, _dbl, _dbl, _vp, ctypes.c_char_p, _vp, ctypes.c_char_p, _vp,
                      ctypes.c_char_p, _vp, _i64, _vp],
     "tt_triples_energy": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _P(_dbl), _vp],
@@ -505,6 +508,17 @@ def contract_prefetch(ctx: Context, C: Tensor, c_lbl: str, beta: float, A: Tenso
     """Issue the input gather of a later ``contract`` with the same arguments on the comm stream
     (tt_contract_prefetch): it overlaps the kernels issued in between."""
     _check(_lib.tt_contract_prefetch(ctx.h, C.h, _b(c_lbl), beta, A.h, _b(a_lbl), B.h, _b(b_lbl)))
+
+
+def contract_host(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str, B: Tensor,
+                  b_lbl: str, hA=None, hB=None, hC=None, c_in: bool = False, c_out: bool = False):
+    """tt_contract_host: the contraction from host buffers (pinned torch tensors or addresses; None = the
+    operand is resident), pipelined inside the library (per dim-0 tile of C)."""
+    flags = (HOST_C_IN if c_in else 0) | (HOST_C_OUT if c_out else 0)
+    _check(_lib.tt_contract_host(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), A.h, _b(a_lbl), B.h, _b(b_lbl),
+                                 _vp(_devptr(hA)) if hA is not None else None,
+                                 _vp(_devptr(hB)) if hB is not None else None,
+                                 _vp(_devptr(hC)) if hC is not None else None, flags))
 
 
 def contract3(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str, B: Tensor,

@@ -950,6 +950,12 @@ tt_status tt_ctx_destroy(tt_ctx ctx) {
   ctx->tensors.clear();
   for (auto& r : ctx->prof) { ctx->event_pool.push_back(r.e0); ctx->event_pool.push_back(r.e1); }
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    cudaEventDestroy(ctx->copy_fork);
+  }
+  for (cudaEvent_t e : ctx->tile_events) cudaEventDestroy(e);
   if (ctx->comm_stream) {
     cudaStreamSynchronize(ctx->comm_stream);
     cudaStreamDestroy(ctx->comm_stream);
@@ -2571,6 +2577,163 @@ tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* cl, double b
   TT_CUDA(cudaEventRecord(ctx->comm_done, ctx->comm_stream));
   ctx->comm_pending = true;
   pl->prefetched = true;
+  return TT_OK;
+}
+
+// End to end from host memory (tt.h tt_contract_host).  Pipelined (nranks == 1, A's and C's dim 0 carry
+// the same label on the same tiling, no views): per dim-0 tile x of C, A's blocks with dim-0 coordinate x
+// -- one contiguous packed range (row-major block order) -- go host->device on the context's copy stream
+// while tile x-1 contracts; tile x is a local plan restricted to C's blocks with dim-0 coordinate x (the
+// same kernel and per-element k order as the whole contraction: bitwise the same result, R12); its C
+// rows go device->host while tile x+1 contracts.  Otherwise: H2D of every held range, tt_contract, D2H
+// of this rank's C ranges.
+namespace {
+struct HostPlan {
+  bool pipelined = false;
+  std::vector<std::pair<int64_t, int64_t>> a_rng, c_rng;   // per dim-0 tile of C: storage ranges of A, C
+  std::vector<std::shared_ptr<ContractPlan>> tiles;        // local plan of each tile (nullptr: no C block)
+};
+
+void held_storage(tt_tensor T, int32_t rank, std::vector<std::pair<int64_t, int64_t>>& out) {
+  out.clear();
+  std::vector<std::pair<int64_t, int64_t>> hr;
+  for (int64_t b = 0; b < T->nblocks; ++b) {
+    if (!T->nz[b] || T->blk_off[b] < 0) continue;
+    T->held_ranges(b, rank, hr);
+    for (auto& h : hr) {
+      const int64_t a0 = T->blk_off[b] + h.first, a1 = T->blk_off[b] + h.second;
+      if (!out.empty() && a0 - out.back().second <= 1) out.back().second = std::max(out.back().second, a1);
+      else out.push_back({a0, a1});
+    }
+  }
+}
+
+tt_status h2d(tt_tensor T, const double* h, const std::vector<std::pair<int64_t, int64_t>>& rng, cudaStream_t st) {
+  for (auto& r : rng)
+    if (r.second > r.first)
+      TT_CUDA(cudaMemcpyAsync(T->data + r.first, h + r.first, (r.second - r.first) * 8, cudaMemcpyHostToDevice, st));
+  return TT_OK;
+}
+tt_status d2h(tt_tensor T, double* h, const std::vector<std::pair<int64_t, int64_t>>& rng, cudaStream_t st) {
+  for (auto& r : rng)
+    if (r.second > r.first)
+      TT_CUDA(cudaMemcpyAsync(h + r.first, T->data + r.first, (r.second - r.first) * 8, cudaMemcpyDeviceToHost, st));
+  return TT_OK;
+}
+}  // namespace
+
+tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double alpha, tt_tensor A,
+                           const char* al, tt_tensor B, const char* bl, const double* hA, const double* hB, double* hC,
+                           int32_t c_flags) {
+  NvtxRange nvtx_("tt_contract_host");
+  if (!ctx) return fail(TT_E_ARG, "NULL context");
+  if ((c_flags & ~(TT_HOST_C_IN | TT_HOST_C_OUT)) != 0) return fail(TT_E_ARG, "unknown c_flags bits");
+  if ((c_flags & (TT_HOST_C_IN | TT_HOST_C_OUT)) && !hC) return fail(TT_E_ARG, "c_flags name C but hC is NULL");
+  std::shared_ptr<ContractPlan> whole;
+  TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, whole, nullptr));
+  TT_TRY(need_ws(ctx));
+  TT_TRY(check_bound(C, "C"));
+  TT_TRY(check_bound(A, "A"));
+  TT_TRY(check_bound(B, "B"));
+  DeviceGuard dg(ctx->device);
+  const std::string key = plan_key("host", C, cl, A, al, B, bl, beta);
+  auto hp = cached<HostPlan>(ctx, key);
+  if (!hp) {
+    hp = std::make_shared<HostPlan>();
+    const bool same0 = al[0] == cl[0] && same_tiling(A->dims[0], C->dims[0]);
+    hp->pipelined = ctx->nranks == 1 && same0 && !A->view_of && !C->view_of && A != B && !C->compact;
+    if (hp->pipelined) {
+      const int32_t nt = C->dims[0]->ntiles();
+      hp->a_rng.assign(nt, {0, 0});
+      hp->c_rng.assign(nt, {0, 0});
+      hp->tiles.assign(nt, nullptr);
+      int32_t co[TT_MAX_ORDER];
+      auto span = [&](tt_tensor T, std::vector<std::pair<int64_t, int64_t>>& rng) {
+        for (int64_t b = 0; b < T->nblocks; ++b) {
+          if (!T->nz[b] || T->blk_off[b] < 0) continue;
+          T->block_coords(b, co);
+          auto& r = rng[co[0]];
+          const int64_t a0 = T->blk_off[b], a1 = a0 + T->block_volume(b);
+          if (r.second == r.first) r = {a0, a1};
+          else r = {std::min(r.first, a0), std::max(r.second, a1)};
+        }
+      };
+      span(A, hp->a_rng);
+      span(C, hp->c_rng);
+      for (int32_t x = 0; x < nt; ++x) {
+        ContractOpts o;
+        o.local = true;
+        o.tag = "|host" + std::to_string(x);
+        for (int64_t b = 0; b < C->nblocks; ++b) {
+          if (!C->nz[b]) continue;
+          C->block_coords(b, co);
+          if (co[0] == x) o.sel.push_back({b, 0, C->ext0(b)});
+        }
+        if (o.sel.empty()) continue;
+        TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, hp->tiles[x], nullptr, o));
+      }
+    }
+    plan_put(ctx, key, hp);
+  }
+  std::vector<std::pair<int64_t, int64_t>> rB, rC, rA;
+  if (hB) held_storage(B, ctx->rank, rB);
+  if (hC) held_storage(C, ctx->rank, rC);
+  if (!hp->pipelined || !hA) {
+    if (hA) {
+      held_storage(A, ctx->rank, rA);
+      TT_TRY(h2d(A, hA, rA, ctx->stream));
+    }
+    if (hB) TT_TRY(h2d(B, hB, rB, ctx->stream));
+    if (c_flags & TT_HOST_C_IN) TT_TRY(h2d(C, hC, rC, ctx->stream));
+    TT_TRY(tt_contract(ctx, C, cl, beta, alpha, A, al, B, bl));
+    if (c_flags & TT_HOST_C_OUT) TT_TRY(d2h(C, hC, rC, ctx->stream));
+    return TT_OK;
+  }
+  if (!ctx->copy_stream) {
+    TT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    TT_CUDA(cudaEventCreateWithFlags(&ctx->copy_fork, cudaEventDisableTiming));
+  }
+  const int32_t nt = (int32_t)hp->tiles.size();
+  while ((int32_t)ctx->tile_events.size() < 2 * nt + 1) {
+    cudaEvent_t e;
+    TT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->tile_events.push_back(e);
+  }
+  cudaEvent_t* up = ctx->tile_events.data();          // A rows of tile x arrived
+  cudaEvent_t* done = up + nt;                        // tile x contracted
+  cudaEvent_t fin = ctx->tile_events[2 * nt];
+  // B and the incoming C on the context stream; A tile by tile on the copy stream, after everything
+  // already queued on the context stream (no overwrite of data earlier kernels still read)
+  if (hB) TT_TRY(h2d(B, hB, rB, ctx->stream));
+  if (c_flags & TT_HOST_C_IN) TT_TRY(h2d(C, hC, rC, ctx->stream));
+  TT_CUDA(cudaEventRecord(ctx->copy_fork, ctx->stream));
+  TT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_fork, 0));
+  for (int32_t x = 0; x < nt; ++x) {
+    TT_TRY(h2d(A, hA, {hp->a_rng[x]}, ctx->copy_stream));
+    TT_CUDA(cudaEventRecord(up[x], ctx->copy_stream));
+  }
+  reset_stats(ctx);
+  double flops = 0;
+  int64_t tasks = 0;
+  for (int32_t x = 0; x < nt; ++x) {
+    TT_CUDA(cudaStreamWaitEvent(ctx->stream, up[x], 0));
+    if (hp->tiles[x]) {
+      TT_TRY(launch_plan(ctx, *hp->tiles[x], C, cl, beta, alpha, A, al, B, bl));
+      flops += hp->tiles[x]->flops;
+      tasks += hp->tiles[x]->tasks;
+    }
+    TT_CUDA(cudaEventRecord(done[x], ctx->stream));
+  }
+  if (c_flags & TT_HOST_C_OUT)
+    for (int32_t x = 0; x < nt; ++x) {
+      TT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, done[x], 0));
+      TT_TRY(d2h(C, hC, {hp->c_rng[x]}, ctx->copy_stream));
+    }
+  TT_CUDA(cudaEventRecord(fin, ctx->copy_stream));
+  TT_CUDA(cudaStreamWaitEvent(ctx->stream, fin, 0));
+  ctx->last.flops = flops;
+  ctx->last.tasks = tasks;
+  ctx->last.bytes = whole->bytes;
   return TT_OK;
 }
 

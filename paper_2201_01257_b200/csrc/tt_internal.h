@@ -314,6 +314,10 @@ struct tt_ctx_s {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t comm_fork = nullptr, comm_done = nullptr;
   bool comm_pending = false;       // comm_done marks the last gather issued on comm_stream
+  // tt_contract_host: host<->device copies overlapping the contraction tiles
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_fork = nullptr;
+  std::vector<cudaEvent_t> tile_events;
   // simulated ranks on one GPU (tt_ctx_create_sim): the group replacing the NCCL communicator
   tt_sim sim = nullptr;
   uint64_t tensor_seq = 0;         // next tensor creation index
