@@ -22,10 +22,15 @@ terms' gathers are issued first on the communication stream (tt_contract_prefetc
 the other terms' kernels.  The kernel tile variant is autotuned by tt_contract on its first two calls
 (warm-up), with identical bits.
 
-e2e: the same step from pinned host memory through the C ABI.  N = 1: pipelined through sliced views
-(per dim-0 tile of R: H2D of the operand rows on a copy stream overlaps the previous chunk's
-contraction, finished R rows go back while the next computes; checked bit for bit against the plain
-step).  N > 1: every rank moves only the blocks / row parts it holds and reads back its R parts.
+e2e: the same step from pinned host memory through the library's own end-to-end call tt_contract_host
+(include/tt.h): N = 1 pipelines inside libtt (per dim-0 tile of R: H2D of the operand rows on the
+library's copy stream overlaps the previous tile's contraction, finished R rows go back while the next
+computes; checked bit for bit against upload + step + download); N > 1: every rank moves only the
+blocks / row parts it holds and reads back its R parts.
+
+sub_configs (N = 1, default run): configs[0] (launch-latency bound: us per contraction, HBM fraction
+of its compulsory bytes) and configs[2] (one step of its three terms, own roofline), measured after the
+configs[1] line's timed region.
 
 --impl reference: the CPU oracle (oracle/) on the host cores, on a bounded sample of the same
 workload (rank 0 only), same metric and unit.
@@ -50,6 +55,8 @@ FP64_PEAK_TFLOPS = 37.1
 FP64_PEAK_SOURCE = "measured DMMA probe profiles/r01_probe_fp64.jsonl (37.1 TF/s @1964 MHz; cuBLAS DGEMM 35.5)"
 
 CONFIGS = {
+    "cfg1": dict(O=4, V=8, tO=4, tV=4, spin=False, terms=("ring",),
+                 workload="cfg1 single contraction C(a,b,i,j) += A(a,c,i,k)*B(c,b,k,j), O=4 V=8 tile=4, dense, FP64"),
     "cfg2": dict(O=40, V=200, tO=40, tV=40, spin=False, terms=("ladder",),
                  workload="cfg2 CCSD ladder R(a,b,i,j) += V(a,b,c,d)*T(c,d,i,j), O=40 V=200 tile=40, dense, FP64"),
     "cfg3": dict(O=60, V=400, tO=30, tV=40, spin=True, terms=("ladder", "ring", "hh"),
@@ -215,6 +222,65 @@ def cpu_oracle_sample(c, a0: int = 0):
     return flops, dt, threads
 
 
+def sub_records(tt, ctx, stream, np, torch, peaks):
+    """configs[0] and configs[2] measured in the same run (N = 1), each with its own roofline: the
+    default line's value stays configs[1]'s.  configs[0] is launch-latency bound (reported in us per
+    contraction and as a fraction of the HBM roofline on its compulsory bytes), configs[2] is one step
+    of its three terms against the FP64 tensor-core peak."""
+    out = {}
+    for name, steps in (("cfg1", 200), ("cfg3", 3)):
+        c = CONFIGS[name]
+        keep, T, ops = build_problem(tt, ctx, c)
+        bufs = {}
+        tags = {"R": 3, "V": 4, "T": 5, "Ta": 1, "Wr": 2, "Tb": 6, "Wh": 7}
+        for n, Tn in T.items():
+            bufs[n] = torch.empty(Tn.packed_elems, dtype=torch.float64, device="cuda")
+            Tn.bind(bufs[n])
+            tt.fill_synthetic(ctx, Tn, 11, tags[n])
+        stats = []
+        for w in range(3):
+            stats = []
+            for (cc, cl, a, al, b, bl) in ops:
+                tt.contract(ctx, T[cc], cl, 1.0, 1.0, T[a], al, T[b], bl)
+                stats.append(ctx.stats())
+        torch.cuda.synchronize()
+        ctx.set_profiling(True)
+        ctx.profile_reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            for (cc, cl, a, al, b, bl) in ops:
+                tt.contract(ctx, T[cc], cl, 1.0, 1.0, T[a], al, T[b], bl)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        kms, kn = ctx.profile("tt_contract_dmma")
+        ctx.set_profiling(False)
+        flops = sum(st["flops"] for st in stats)
+        byts = sum(st["bytes"] for st in stats)
+        avg_k = kms / max(kn, 1)
+        rec = {"workload": c["workload"], "ms_per_step": ms, "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "flops_per_step": flops, "compulsory_bytes_per_step": byts, "steps": steps}
+        if name == "cfg1":
+            hbm = peaks.get("hbm_gbs") or 6533.5
+            rec["us_per_contraction"] = ms * 1e3
+            rec["kernel_us"] = avg_k * 1e3
+            rec["roofline"] = {"bound": "hbm", "achieved": byts / (avg_k * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                               "frac": byts / (avg_k * 1e-3) / 1e9 / hbm, "traffic": None,
+                               "note": "launch-latency bound: 32 KB per launch"}
+        else:
+            per_launch = flops / max(kn // steps, 1)
+            ach = per_launch / (avg_k * 1e-3) / 1e12
+            rec["roofline"] = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                               "frac": ach / FP64_PEAK_TFLOPS, "traffic": None, "kernel": "tt_contract_dmma",
+                               "kernel_share_of_step": kms / steps / ms}
+            rec["pct_fp64_peak"] = flops / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS * 100
+        out[name] = rec
+        del bufs, T
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -248,10 +314,11 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the configs[0] / configs[2] sub-records")
     ap.add_argument("--variant", type=int, default=None, help="force a contraction kernel variant (TT_FORCE_VARIANT)")
     args = ap.parse_args()
     if args.variant is not None:
@@ -360,12 +427,17 @@ def main():
     achieved = (flops_rank / launches_per_step) / (avg_kernel_ms * 1e-3) / 1e12
     variant = stats[0]["kernel_variant"]
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": load_traffic(args.config, variant),
+            "frac": achieved / FP64_PEAK_TFLOPS,
+            # dram bytes per launch from the committed ncu capture of this config and variant on ONE GPU;
+            # null at N > 1 (a rank's launch is a part of the problem the capture did not measure)
+            "traffic": load_traffic(args.config, variant) if world == 1 else None,
             "kernel": "tt_contract_dmma", "avg_kernel_ms": avg_kernel_ms,
             "kernel_share_of_step": kern_ms / args.steps / ms_per_step, "peak_source": FP64_PEAK_SOURCE,
             "algorithmic_bytes_per_step": sum(s["bytes"] for s in stats)}
 
-    # end to end through the C ABI with host buffers (pinned), N GPUs
+    # end to end through the C ABI with host buffers (pinned), N GPUs: tt_contract_host per term -- the
+    # library pipelines the host<->device copies with the contraction tiles (N = 1) or moves each rank's
+    # held ranges (N > 1); the pipelined step is checked bit for bit against upload + step + download
     e2e = None
     if not args.no_e2e:
         hosts = {}
@@ -373,8 +445,16 @@ def main():
             hosts[name] = torch.empty(Tn.packed_elems, dtype=torch.float64, pin_memory=True)
             Tn.download_ptr(hosts[name].data_ptr())
         torch.cuda.synchronize()
-        h2d = 8 * sum(Tn.packed_elems for Tn in T.values())
-        d2h = 8 * T["R"].packed_elems
+        last = len(ops) - 1
+
+        def e2e_step():
+            up = set()
+            for k, (c, cl, a, al, b, bl) in enumerate(ops):
+                hA = hosts[a] if a not in up else None
+                hB = hosts[b] if b not in up else None
+                tt.contract_host(ctx, T[c], cl, 1.0, 1.0, T[a], al, T[b], bl, hA, hB, hosts[c],
+                                 c_in=(k == 0), c_out=(k == last))
+                up |= {a, b}
 
         def e2e_step_plain():
             for name, Tn in T.items():
@@ -382,128 +462,37 @@ def main():
             step()
             T["R"].download_ptr(hosts["R"].data_ptr())
 
-        # N = 1: a pipelined step through sliced views (tt_tensor_view, P159).  The output's dim-0 tiles are
-        # processed in chunks; the operands whose dim 0 is the output's dim 0 (the big V of the ladder)
-        # are uploaded chunk by chunk on a copy stream, so chunk c's host->device copy overlaps chunk c-1's
-        # contraction, and each finished chunk of R goes back to the host while the next one computes.
-        # Every C block is still computed whole by one call: the bits equal the plain step's.
-        (_so, _sv, _to, tv) = keep
-        chunkable = world == 1 and all(al[0] == cl[0] and T[c].dims[0] is tv for (c, cl, a, al, b, bl) in ops)
-        if chunkable:
-            copy_stream = torch.cuda.Stream()
-            A_names = sorted({a for (c, cl, a, al, b, bl) in ops})
-            up_front = [n for n in T if n not in A_names]
-            nt = tv.ntiles
-            subs = [tv.sub(int(tv.offsets[x]), int(tv.offsets[x + 1])) for x in range(nt)]
+        def held_bytes(Tn):
+            own = 0
+            parts = {}
+            for (blk, lo, hi, ow) in Tn.parts:
+                parts.setdefault(blk, []).append((lo, hi, ow))
+            for blk in range(Tn.nblocks):
+                if not Tn.nz[blk]:
+                    continue
+                ext = [int(d.offsets[t + 1] - d.offsets[t]) for d, t in zip(Tn.dims, np.unravel_index(blk, Tn.grid))]
+                vol = int(np.prod(ext))
+                if Tn.owner[blk] == rank or Tn.owner[blk] == tt.TT_REPLICATED:
+                    own += vol
+                elif blk in parts:
+                    own += sum(hi - lo for (lo, hi, ow) in parts[blk] if ow == rank) * (vol // ext[0])
+            return 8 * own
 
-            def chunk_range(Tn, x):
-                lo, hi = None, None
-                for b in range(Tn.nblocks):
-                    if Tn.nz[b] and np.unravel_index(b, Tn.grid)[0] == x:
-                        o = int(Tn.blk_off[b])
-                        ext = [int(d.offsets[t + 1] - d.offsets[t]) for d, t in zip(Tn.dims, np.unravel_index(b, Tn.grid))]
-                        lo = o if lo is None else min(lo, o)
-                        hi = o + int(np.prod(ext)) if hi is None else max(hi, o + int(np.prod(ext)))
-                return (lo or 0), (hi or 0)
-
-            ranges = {n: [chunk_range(T[n], x) for x in range(nt)] for n in A_names + ["R"]}
-            views = []
-            for x in range(nt):
-                vv = {}
-                for (c, cl, a, al, b, bl) in ops:
-                    for n in (c, a):
-                        if n not in vv:
-                            vv[n] = T[n].view([subs[x]] + list(T[n].dims[1:]))
-                views.append(vv)
-
-            def e2e_step():
-                for n in up_front:
-                    T[n].upload_ptr(hosts[n].data_ptr())
-                up_done = torch.cuda.Event()
-                up_done.record(stream)
-                copy_stream.wait_event(up_done)
-                evs = []
-                with torch.cuda.stream(copy_stream):
-                    for x in range(nt):
-                        for n in A_names:
-                            lo, hi = ranges[n][x]
-                            if hi > lo:
-                                bufs[n][lo:hi].copy_(hosts[n][lo:hi], non_blocking=True)
-                        ev = torch.cuda.Event()
-                        ev.record(copy_stream)
-                        evs.append(ev)
-                done = []
-                for x in range(nt):
-                    stream.wait_event(evs[x])
-                    vv = views[x]
-                    for (c, cl, a, al, b, bl) in ops:
-                        tt.contract(ctx, vv[c], cl, 1.0, 1.0, vv[a], al, T[b], bl)
-                    ev = torch.cuda.Event()
-                    ev.record(stream)
-                    done.append(ev)
-                with torch.cuda.stream(copy_stream):
-                    for x in range(nt):
-                        copy_stream.wait_event(done[x])
-                        lo, hi = ranges["R"][x]
-                        if hi > lo:
-                            hosts["R"][lo:hi].copy_(bufs["R"][lo:hi], non_blocking=True)
-                fin = torch.cuda.Event()
-                fin.record(copy_stream)
-                stream.wait_event(fin)
-        elif world > 1:
-            # N > 1: every rank moves only what it holds -- its own blocks / row parts (owner-computes;
-            # the gathers inside the step fetch the rest over NVLink) -- and reads back its own R parts
-            def held(Tn):
-                rs = []
-                parts = {}
-                for (blk, lo, hi, ow) in Tn.parts:
-                    parts.setdefault(blk, []).append((lo, hi, ow))
-                for blk in range(Tn.nblocks):
-                    if not Tn.nz[blk]:
-                        continue
-                    ext = [int(d.offsets[t + 1] - d.offsets[t]) for d, t in zip(Tn.dims, np.unravel_index(blk, Tn.grid))]
-                    vol, o = int(np.prod(ext)), int(Tn.blk_off[blk])
-                    if Tn.owner[blk] == rank or Tn.owner[blk] == tt.TT_REPLICATED:
-                        rs.append((o, o + vol))
-                    elif blk in parts:
-                        inner = vol // ext[0]
-                        rs += [(o + lo * inner, o + hi * inner) for (lo, hi, ow) in parts[blk] if ow == rank]
-                rs.sort()
-                merged = []
-                for a0, a1 in rs:   # merge runs that touch (or are separated by one alignment pad)
-                    if merged and a0 - merged[-1][1] <= 1:
-                        merged[-1] = (merged[-1][0], max(merged[-1][1], a1))
-                    else:
-                        merged.append((a0, a1))
-                return merged
-
-            own = {n: held(T[n]) for n in T}
-            h2d = 8 * sum(b - a for n in T for (a, b) in own[n])
-            d2h = 8 * sum(b - a for (a, b) in own["R"])
-
-            def e2e_step():
-                for n in T:
-                    for (a0, a1) in own[n]:
-                        bufs[n][a0:a1].copy_(hosts[n][a0:a1], non_blocking=True)
-                step()
-                for (a0, a1) in own["R"]:
-                    hosts["R"][a0:a1].copy_(bufs["R"][a0:a1], non_blocking=True)
-        else:
-            e2e_step = e2e_step_plain
-
-        if chunkable:   # the pipelined step must reproduce the plain step bit for bit
+        h2d = sum(held_bytes(T[n]) for n in T)
+        d2h = held_bytes(T["R"])
+        if world == 1:   # the library's pipelined step must reproduce upload + step + download bit for bit
             r0 = hosts["R"].clone()
             e2e_step_plain()
             torch.cuda.synchronize()
             ref = hosts["R"].clone()
             hosts["R"].copy_(r0)
             e2e_step()
-            torch.cuda.synchronize()
+            ctx.sync()
             if not torch.equal(hosts["R"], ref):
-                raise RuntimeError("pipelined end-to-end step differs from the plain step")
+                raise RuntimeError("tt_contract_host step differs from upload + tt_contract + download")
             hosts["R"].copy_(r0)
         e2e_step()
-        torch.cuda.synchronize()
+        ctx.sync()
         if world > 1:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -521,12 +510,12 @@ def main():
             dist.all_reduce(io)
         e2e = {"value": flops_all / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(io[0]),
                "d2h_bytes_per_step": int(io[1]), "ms_per_step": e_ms, "steps": args.e2e_steps,
-               "pipelined": bool(chunkable),
-               "how": ("per dim-0 tile of R: H2D of the operand rows on a copy stream overlapping the previous "
-                       "chunk's contraction through views, D2H of finished R rows overlapping the next")
-               if chunkable else ("each rank: H2D of the blocks / row parts it holds, the step (gathers of "
-                                  "the rest over NVLink), D2H of its R parts" if world > 1 else
-                                  "upload all, contract, download R")}
+               "api": "tt_contract_host (include/tt.h)",
+               "how": ("pipelined inside libtt: per dim-0 tile of R, H2D of the operand rows on the library's copy "
+                       "stream overlapping the previous tile's contraction, D2H of finished R rows overlapping "
+                       "the next") if world == 1 else
+                      ("each rank: H2D of the blocks / row parts it holds, the contraction (gathers of the rest "
+                       "over NVLink), D2H of its R parts")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -543,8 +532,13 @@ def main():
         cpu = {"value": f / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": sample,
                "seconds": dt}
 
+    peaks = load_peaks()
+    subs = None
+    if world == 1 and not args.no_sub and args.config == "cfg2":
+        del bufs, T
+        torch.cuda.empty_cache()
+        subs = sub_records(tt, ctx, stream, np, torch, peaks)
     if rank == 0:
-        peaks = load_peaks()
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -557,6 +551,7 @@ def main():
             "pct_fp64_peak": value / world / (FP64_PEAK_TFLOPS * 1e3) * 100.0,
             "roofline": roof, "terms": terms, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"),
+            "sub_configs": subs,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

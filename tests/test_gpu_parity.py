@@ -685,3 +685,42 @@ def test_vector_shaped_contractions(env, spin, k):
     ctx = new_ctx(tt, torch)
     got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[k], alpha=0.5, beta=1.0)
     assert normwise(got, ref) <= TOL, normwise(got, ref)
+
+
+@pytest.mark.parametrize("terms", [("ladder",), ("ring",), ("ladder", "ring", "hh")])
+def test_contract_host_bitwise(env, terms):
+    """tt_contract_host (host buffers, pipelined per dim-0 tile inside the library) gives bitwise the
+    result of upload + tt_contract + download, and the oracle's within 1e-11."""
+    tt, torch = env
+    pb = ccsd_problem(12, 30, 3, 7, True, terms=terms)
+    orc = oracle_objects(pb)
+    ctx = new_ctx(tt, torch)
+    P = product_objects(tt, ctx, pb)
+    host, dense, dev = {}, {}, {}
+    for i, name in enumerate(sorted(orc)):
+        dense[name] = O.dense_masked(orc[name], S.dense(orc[name].shape, 4, 1 + i))
+        host[name] = torch.from_numpy(O.pack(orc[name], dense[name])).pin_memory()
+        dev[name] = torch.zeros(P[name].storage_elems, dtype=torch.float64, device="cuda")
+        P[name].bind(dev[name])
+    out = host["R"].clone().pin_memory()
+    ref_d = dense["R"]
+    for k, (c, cl, a, al, b, bl) in enumerate(pb.ops):
+        tt.contract_host(ctx, P[c], cl, 1.0, 0.5, P[a], al, P[b], bl, host[a], host[b], out,
+                         c_in=(k == 0), c_out=(k == len(pb.ops) - 1))
+        ref_d = O.contract(ref_d, cl, dense[a], al, dense[b], bl, 0.5, 1.0, cmask=O.nz_mask(orc[c]))
+    ctx.sync()
+    got = out.numpy().copy()
+    # plain path on a second context
+    ctx2 = new_ctx(tt, torch)
+    P2 = product_objects(tt, ctx2, pb)
+    keep = {}
+    for name in orc:
+        keep[name] = host[name].cuda()
+        P2[name].bind(keep[name])
+    for (c, cl, a, al, b, bl) in pb.ops:
+        tt.contract(ctx2, P2[c], cl, 1.0, 0.5, P2[a], al, P2[b], bl)
+    plain = P2["R"].download()
+    ctx2.sync()
+    assert np.array_equal(got, plain)
+    ref = O.pack(orc["R"], ref_d)
+    assert normwise(got, ref) <= TOL
