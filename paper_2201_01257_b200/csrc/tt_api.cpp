@@ -759,7 +759,8 @@ struct ContractPlan {
   bool a_vec = false, b_vec = false;   // 16-byte copies along the operand's contiguous direction
   bool persistent = false;             // short work items: persistent CTAs hide pipeline fill / epilogue
   bool tma = false;                    // TMA producer (uniform fused GEMM-shaped operands)
-  int64_t tma_k = 0, tma_n = 0;        // row lengths of the A [rows][K] and B [rows][N] views
+  int64_t tma_k = 0, tma_n = 0;        // row lengths of the A [rows][K] and B [rows][N|K] views
+  int tma_mode = 0;                    // bit 0: B is [N][K]; bit 1: multi-group C epilogue
   CUtensorMap maps[2];                 // A, B tensor maps (encoded for map_ptr)
   const void* map_ptr[2] = {nullptr, nullptr};
   int64_t nwork = 0;
@@ -2214,23 +2215,39 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     pl.a_vec = a_last == a_grp_last && even(a_last);
     pl.b_vec = b_last == b_grp_last && even(b_last);
   }
-  // TMA producer: warp-specialised variant, single fused groups, A = [M][K] and B = [K][N] with the
-  // same K extent in every A block, the same N extent in every B block, K a multiple of 16 (no K tail)
+  // TMA producer (warp-specialised family): every A block is one row-major [M][K] matrix -- A's labels
+  // are the M groups' labels (C order) followed by the K groups' labels -- with the same K extent in
+  // every block (a multiple of 16: no K tail), and every B block is [K][N] (K labels then N labels,
+  // same even N extent) or [N][K] (N labels then K labels: the implicit operand's X(q,s,L)).  Then the
+  // packed buffers are [rows][K] / [rows][N|K] matrices and the GEMM row / column index is the row of
+  // the block's matrix.  C's label order is free: several M or N groups use the multi-group epilogue.
   {
     const char* ft = getenv("TT_TMA");
     const bool allow = !ft || atoi(ft) != 0;
-    if (allow && !A->view_of && !B->view_of && an.mg.size() == 1 && an.ng.size() == 1 &&
-        an.kg.size() == 1 && an.a_kc && an.b_nc && !ht.K.empty()) {
+    std::vector<int> mlab, nlab, klab;
+    for (auto& gr : an.mg) mlab.insert(mlab.end(), gr.begin(), gr.end());
+    for (auto& gr : an.ng) nlab.insert(nlab.end(), gr.begin(), gr.end());
+    for (auto& gr : an.kg) klab.insert(klab.end(), gr.begin(), gr.end());
+    auto cat = [](const std::vector<int>& x, const std::vector<int>& y) {
+      std::vector<int> r(x);
+      r.insert(r.end(), y.begin(), y.end());
+      return r;
+    };
+    const bool a_mk = an.a_lab == cat(mlab, klab);
+    const bool b_kn = an.b_lab == cat(klab, nlab), b_nk = an.b_lab == cat(nlab, klab);
+    if (allow && !A->view_of && !B->view_of && a_mk && (b_kn || b_nk) && !ht.K.empty() && !klab.empty() &&
+        !mlab.empty() && !nlab.empty()) {
       std::vector<int> ak, bn;
-      for (int u : an.kg[0]) ak.push_back(an.a_pos[u]);
-      for (int u : an.ng[0]) bn.push_back(an.b_pos[u]);
+      for (int u : klab) ak.push_back(an.a_pos[u]);
+      for (int u : nlab) bn.push_back(an.b_pos[u]);
       const int64_t K = uniform_group_extent(A, ak), N = uniform_group_extent(B, bn);
-      bool ok = K > 0 && N > 0 && K % 16 == 0 && N % 2 == 0;
+      bool ok = K > 0 && N > 0 && K % 16 == 0 && (b_nk || N % 2 == 0);
       for (int32_t k : ht.K) ok = ok && k == K;
       if (ok) {
         pl.tma = true;
         pl.tma_k = K;
-        pl.tma_n = N;
+        pl.tma_n = b_nk ? K : N;
+        pl.tma_mode = (b_nk ? 1 : 0) | ((an.mg.size() > 1 || an.ng.size() > 1) ? 2 : 0);
       }
     }
   }
@@ -2453,11 +2470,14 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
       if (mp.map_ptr[0] != A->data || mp.map_ptr[1] != B->data) {
         const VariantInfo vi = variant_info(pl.variant);
         TT_TRY(encode_2d(&mp.maps[0], A->data, pl.tma_k, A->storage_elems / pl.tma_k, 16, (uint32_t)vi.bm, true));
-        TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->storage_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
+        if (pl.tma_mode & 1)   // [N][K] B: {16 k, BN rows} boxes, swizzled like A
+          TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->storage_elems / pl.tma_n, 16, (uint32_t)vi.bn, true));
+        else
+          TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->storage_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
         mp.map_ptr[0] = A->data;
         mp.map_ptr[1] = B->data;
       }
-      TT_CUDA(launch_contract_tma(pl.variant - num_contract_variants(), p, pl.maps, pl.nwork, ctx->stream));
+      TT_CUDA(launch_contract_tma(pl.variant - num_contract_variants(), pl.tma_mode, p, pl.maps, pl.nwork, ctx->stream));
     } else if (pl.variant < num_contract_variants())
       TT_CUDA(launch_contract(pl.variant, pl.an.a_kc, pl.an.b_nc, p, pl.nwork, ctx->stream));
     else

@@ -372,11 +372,13 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, 
       : "memory");
 }
 
-template <class K>
+// BKC: B is [N][K] in its blocks (k contiguous, e.g. the implicit operand's X(q,s,L)): its box is
+// {16 k, BN rows} with the 128-byte swizzle of A and its fragments are read like A's.
+template <class K, bool BKC = false>
 struct TmaSmem {
   static constexpr int A_BYTES = K::BM * 128;                 // BK = 16 doubles = 128 B rows, swizzled
-  static constexpr int B_LD = K::BN + 2;                      // doubles per B row (box width)
-  static constexpr int B_BYTES = K::BK * B_LD * 8;
+  static constexpr int B_LD = K::BN + 2;                      // doubles per B row (box width; [K][N] B)
+  static constexpr int B_BYTES = BKC ? K::BN * 128 : K::BK * B_LD * 8;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int BUDGET = (227 * 1024) / K::MINB - 2048;
   static constexpr int FIT = BUDGET / (STAGE + 16);
@@ -384,15 +386,17 @@ struct TmaSmem {
   static constexpr int BYTES = 1024 + STAGES * STAGE + 2 * STAGES * 8 + 64;
   static constexpr unsigned TX = (unsigned)(A_BYTES + B_BYTES);
   static_assert(K::BK == 16, "TMA variant assumes 128-byte A rows");
-  static_assert(A_BYTES % 1024 == 0, "swizzled A stages must stay 1024-byte aligned");
+  static_assert(A_BYTES % 1024 == 0 && (!BKC || B_BYTES % 1024 == 0), "swizzled stages must stay 1024-byte aligned");
   static_assert(STAGES >= 3, "pipeline too shallow");
 };
 
-template <class K>
+// MULTI: C's M / N index maps through several label groups (dot_decode, e.g. the implicit operand's
+// W(p,q,r,s) = X(p,r,L) X(q,s,L): rows (p,r), columns (q,s)); else one stride per side.
+template <class K, bool BKC, bool MULTI>
 __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
     tt_contract_tma_kernel(const ContractParams p, const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB) {
-  using SM = TmaSmem<K>;
+  using SM = TmaSmem<K, BKC>;
   constexpr int STAGES = SM::STAGES;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -430,7 +434,8 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
           mbar_wait_sleep(&empty[st], phase);
           mbar_expect_tx(&full[st], SM::TX);
           tma_load_2d(sA + st * SM::A_BYTES, &tmA, k0, arow, &full[st]);
-          tma_load_2d(sB + st * SM::B_BYTES, &tmB, n0, brow0 + k0, &full[st]);
+          if (BKC) tma_load_2d(sB + st * SM::B_BYTES, &tmB, k0, brow0 + n0, &full[st]);
+          else tma_load_2d(sB + st * SM::B_BYTES, &tmB, n0, brow0 + k0, &full[st]);
           if (++st == STAGES) { st = 0; phase ^= 1; }
         }
       }
@@ -457,7 +462,8 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
     for (int s = 0; s < nst; ++s) {
       mbar_wait(&full[st], phase);
       const unsigned char* a = sA + st * SM::A_BYTES;
-      const double* b = reinterpret_cast<const double*>(sB + st * SM::B_BYTES);
+      const unsigned char* bs = sB + st * SM::B_BYTES;
+      const double* b = reinterpret_cast<const double*>(bs);
 #pragma unroll
       for (int o = 0; o < K::BK / 8; ++o) {
         double af[K::MT][2], bf[K::NT][2];
@@ -471,9 +477,17 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
         }
 #pragma unroll
         for (int j = 0; j < K::NT; ++j) {
-          const int n = wn * K::WTN + j * 8 + r8;
-          bf[j][0] = b[(8 * o + 2 * q) * SM::B_LD + n];
-          bf[j][1] = b[(8 * o + 2 * q + 1) * SM::B_LD + n];
+          if (BKC) {   // swizzled [n][16 k] rows, fragment columns permuted like A's rows
+            const int n = wn * K::WTN + j * 8 + pr;
+            const double2 v =
+                *reinterpret_cast<const double2*>(bs + n * 128 + ((((4 * o + q) ^ (n & 7))) << 4));
+            bf[j][0] = v.x;
+            bf[j][1] = v.y;
+          } else {
+            const int n = wn * K::WTN + j * 8 + r8;
+            bf[j][0] = b[(8 * o + 2 * q) * SM::B_LD + n];
+            bf[j][1] = b[(8 * o + 2 * q + 1) * SM::B_LD + n];
+          }
         }
 #pragma unroll
         for (int t = 0; t < 2; ++t)
@@ -486,23 +500,34 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
       if (lane == 0) mbar_arrive(&empty[st]);
       if (++st == STAGES) { st = 0; phase ^= 1; }
     }
-    // epilogue (single M and N groups: C row m has stride cm_str[0], column n stride cn_str[0])
+    // epilogue: C row m, column n through one stride per side, or through the label groups (MULTI)
     const bool part = g->flags & kGroupPartial;
     double* Cb = (part ? p.P : p.C) + g->c_off;
     const double alpha = part ? 1.0 : alpha_, beta = part ? 0.0 : beta_;
     const int M = g->M, N = g->N;
     const int32_t cms = g->cm_str[0], cns = g->cn_str[0];
+    int32_t mext[kMaxGroup], next[kMaxGroup], cmv[kMaxGroup], cnv[kMaxGroup];
+    if (MULTI) {
+#pragma unroll
+      for (int i = 0; i < kMaxGroup; ++i) {
+        mext[i] = g->mext[i];
+        next[i] = g->next[i];
+        cmv[i] = g->cm_str[i];
+        cnv[i] = g->cn_str[i];
+      }
+    }
 #pragma unroll
     for (int i = 0; i < K::MT; ++i) {
       const int m = m0 + wm * K::WTM + i * 8 + pr;
       if (m >= M) continue;
+      const int64_t om = MULTI ? (int64_t)dot_decode(m, p.nM, mext, cmv) : (int64_t)m * cms;
 #pragma unroll
       for (int j = 0; j < K::NT; ++j) {
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-          const int n = n0 + wn * K::WTN + j * 8 + 2 * q + r;
+          const int n = n0 + wn * K::WTN + j * 8 + (BKC ? perm8(2 * q + r) : 2 * q + r);
           if (n >= N) continue;
-          double* c = Cb + (int64_t)m * cms + (int64_t)n * cns;
+          double* c = Cb + om + (MULTI ? (int64_t)dot_decode(n, p.nN, next, cnv) : (int64_t)n * cns);
           const double v = alpha * acc[i][j][r];
           *c = (beta == 0.0) ? v : beta * *c + v;
         }
@@ -511,20 +536,39 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
   }
 }
 
-template <class K>
-static cudaError_t setup_tma() {
-  return cudaFuncSetAttribute(tt_contract_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              TmaSmem<K>::BYTES);
+template <class K, bool BKC, bool MULTI>
+static cudaError_t setup_tma_one() {
+  return cudaFuncSetAttribute(tt_contract_tma_kernel<K, BKC, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              TmaSmem<K, BKC>::BYTES);
 }
 template <class K>
-static cudaError_t launch_tma(const ContractParams& p, const CUtensorMap& a, const CUtensorMap& b, int64_t nwork,
-                              cudaStream_t s) {
+static cudaError_t setup_tma() {
+  cudaError_t e;
+  if ((e = setup_tma_one<K, false, false>()) != cudaSuccess) return e;
+  if ((e = setup_tma_one<K, false, true>()) != cudaSuccess) return e;
+  if ((e = setup_tma_one<K, true, false>()) != cudaSuccess) return e;
+  return setup_tma_one<K, true, true>();
+}
+template <class K, bool BKC, bool MULTI>
+static cudaError_t launch_tma_one(const ContractParams& p, const CUtensorMap& a, const CUtensorMap& b, int64_t nwork,
+                                  cudaStream_t s) {
   const int64_t slots = (int64_t)p.sm_count * K::MINB;
   const unsigned grid = (unsigned)((p.persistent && nwork > slots) ? slots : nwork);
   ContractParams q = p;
   q.nwork = nwork;
-  tt_contract_tma_kernel<K><<<grid, K::NTHREADS, TmaSmem<K>::BYTES, s>>>(q, a, b);
+  tt_contract_tma_kernel<K, BKC, MULTI><<<grid, K::NTHREADS, TmaSmem<K, BKC>::BYTES, s>>>(q, a, b);
   return cudaGetLastError();
+}
+// mode bit 0: B is [N][K] (k contiguous); bit 1: multi-group C epilogue
+template <class K>
+static cudaError_t launch_tma(int mode, const ContractParams& p, const CUtensorMap& a, const CUtensorMap& b,
+                              int64_t nwork, cudaStream_t s) {
+  switch (mode & 3) {
+    case 0: return launch_tma_one<K, false, false>(p, a, b, nwork, s);
+    case 1: return launch_tma_one<K, true, false>(p, a, b, nwork, s);
+    case 2: return launch_tma_one<K, false, true>(p, a, b, nwork, s);
+    default: return launch_tma_one<K, true, true>(p, a, b, nwork, s);
+  }
 }
 
 template <class K, bool AKC, bool BNC, bool AV, bool BV>
@@ -592,9 +636,9 @@ static VariantInfo info_cfg(const char* name) {
     cudaError_t e = ws::setup_cfg<CFG>();                                                          \
     return e != cudaSuccess ? e : ws::setup_tma<CFG>();                                            \
   }                                                                                                \
-  cudaError_t ws_launch_tma_##NAME(const ContractParams& p, const CUtensorMap& a, const CUtensorMap& b, \
-                                   int64_t nwork, cudaStream_t s) {                                \
-    return ws::launch_tma<CFG>(p, a, b, nwork, s);                                                 \
+  cudaError_t ws_launch_tma_##NAME(int mode, const ContractParams& p, const CUtensorMap& a,       \
+                                   const CUtensorMap& b, int64_t nwork, cudaStream_t s) {          \
+    return ws::launch_tma<CFG>(mode, p, a, b, nwork, s);                                           \
   }                                                                                                \
   cudaError_t ws_launch_##NAME(bool akc, bool bnc, bool av, bool bv, const ContractParams& p,      \
                                int64_t nwork, cudaStream_t s) {                                    \

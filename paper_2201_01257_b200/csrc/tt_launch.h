@@ -57,7 +57,7 @@ struct ContractParams {
   int64_t nwork;          // work items (persistent kernels loop over them)
   int32_t sm_count;       // SMs of the device (persistent grid size)
   int32_t persistent;     // 1: grid = resident CTAs looping over items; 0: one CTA per item
-  int32_t tma_n;          // TMA variant: row length N of the B matrix view
+  int32_t tma_n;          // TMA variant: row length of the B matrix view (N for [K][N] B, K for [N][K] B)
 };
 
 // Split-K reduction: C part = beta*C + alpha * sum_{s < nslots} P[p_off + s*vol + .] in slot order
@@ -87,7 +87,9 @@ cudaError_t launch_contract_ws(int v, bool a_kcontig, bool b_ncontig, bool a_vec
                                const ContractParams& p, int64_t nwork, cudaStream_t s);
 // TMA producer variant of the warp-specialised family (uniform fused GEMM-shaped operands);
 // `maps` points to two CUtensorMap (A, B).
-cudaError_t launch_contract_tma(int v, const ContractParams& p, const void* maps, int64_t nwork, cudaStream_t s);
+// mode bit 0: B is [N][K] in its blocks (k contiguous); bit 1: multi-group C epilogue
+cudaError_t launch_contract_tma(int v, int mode, const ContractParams& p, const void* maps, int64_t nwork,
+                                cudaStream_t s);
 
 // Segment-based element kernels (set / add / scalar / synthetic fill).
 struct Segment {

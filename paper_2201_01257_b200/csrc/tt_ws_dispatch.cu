@@ -15,18 +15,19 @@ cudaError_t ws_launch_w0(bool, bool, bool, bool, const ContractParams&, int64_t,
 cudaError_t ws_launch_w1(bool, bool, bool, bool, const ContractParams&, int64_t, cudaStream_t);
 cudaError_t ws_launch_w2(bool, bool, bool, bool, const ContractParams&, int64_t, cudaStream_t);
 
-cudaError_t ws_launch_tma_w0(const ContractParams&, const CUtensorMap&, const CUtensorMap&, int64_t, cudaStream_t);
-cudaError_t ws_launch_tma_w1(const ContractParams&, const CUtensorMap&, const CUtensorMap&, int64_t, cudaStream_t);
-cudaError_t ws_launch_tma_w2(const ContractParams&, const CUtensorMap&, const CUtensorMap&, int64_t, cudaStream_t);
+cudaError_t ws_launch_tma_w0(int, const ContractParams&, const CUtensorMap&, const CUtensorMap&, int64_t, cudaStream_t);
+cudaError_t ws_launch_tma_w1(int, const ContractParams&, const CUtensorMap&, const CUtensorMap&, int64_t, cudaStream_t);
+cudaError_t ws_launch_tma_w2(int, const ContractParams&, const CUtensorMap&, const CUtensorMap&, int64_t, cudaStream_t);
 
 int num_ws_variants() { return 3; }
 
-cudaError_t launch_contract_tma(int v, const ContractParams& p, const void* maps, int64_t nwork, cudaStream_t s) {
+cudaError_t launch_contract_tma(int v, int mode, const ContractParams& p, const void* maps, int64_t nwork,
+                                cudaStream_t s) {
   if (nwork <= 0) return cudaSuccess;
   const CUtensorMap* m = static_cast<const CUtensorMap*>(maps);
-  return v == 0 ? ws_launch_tma_w0(p, m[0], m[1], nwork, s)
-       : v == 1 ? ws_launch_tma_w1(p, m[0], m[1], nwork, s)
-                : ws_launch_tma_w2(p, m[0], m[1], nwork, s);
+  return v == 0 ? ws_launch_tma_w0(mode, p, m[0], m[1], nwork, s)
+       : v == 1 ? ws_launch_tma_w1(mode, p, m[0], m[1], nwork, s)
+                : ws_launch_tma_w2(mode, p, m[0], m[1], nwork, s);
 }
 
 VariantInfo ws_variant_info(int v) {
