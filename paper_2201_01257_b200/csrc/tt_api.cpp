@@ -2016,6 +2016,19 @@ tt_status encode_2d(CUtensorMap* m, const double* base, int64_t cols, int64_t ro
   return TT_OK;
 }
 
+// 3-D tensor map of a dense row-major array; dims innermost first (doubles), box likewise, no swizzle
+tt_status encode_3d(CUtensorMap* m, const double* base, const int64_t* dims3, const uint32_t* box3) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(TT_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)dims3[0], (cuuint64_t)dims3[1], (cuuint64_t)dims3[2]};
+  cuuint64_t strides[2] = {(cuuint64_t)dims3[0] * 8, (cuuint64_t)(dims3[0] * dims3[1]) * 8};
+  cuuint32_t box[3] = {box3[0], box3[1], box3[2]}, es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TT_E_CUDA, "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
+  return TT_OK;
+}
+
 // 4-D tensor map of a dense row-major array; dims innermost first (doubles), box likewise
 tt_status encode_4d(CUtensorMap* m, const double* base, const int64_t* dims4, const uint32_t* box4) {
   EncodeTiledFn fn = encode_fn();
@@ -2241,8 +2254,15 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       for (int u : klab) ak.push_back(an.a_pos[u]);
       for (int u : nlab) bn.push_back(an.b_pos[u]);
       const int64_t K = uniform_group_extent(A, ak), N = uniform_group_extent(B, bn);
-      bool ok = K > 0 && N > 0 && K % 16 == 0 && (b_nk || N % 2 == 0);
+      // even rows (16-byte TMA strides); K tails are TMA out-of-bounds zero fill in both views
+      bool ok = K > 0 && N > 0 && K % 2 == 0 && N % 2 == 0;
       for (int32_t k : ht.K) ok = ok && k == K;
+      // every stored block starts on a row of its matrix view (no alignment pads between blocks)
+      for (int64_t b = 0; ok && b < A->nblocks; ++b)
+        if (A->nz[b] && A->blk_off[b] >= 0) ok = A->blk_off[b] % K == 0;
+      const int64_t bunit = b_nk ? K : K * N;
+      for (int64_t b = 0; ok && b < B->nblocks; ++b)
+        if (B->nz[b] && B->blk_off[b] >= 0) ok = B->blk_off[b] % bunit == 0;
       if (ok) {
         pl.tma = true;
         pl.tma_k = K;
@@ -2470,10 +2490,13 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
       if (mp.map_ptr[0] != A->data || mp.map_ptr[1] != B->data) {
         const VariantInfo vi = variant_info(pl.variant);
         TT_TRY(encode_2d(&mp.maps[0], A->data, pl.tma_k, A->storage_elems / pl.tma_k, 16, (uint32_t)vi.bm, true));
-        if (pl.tma_mode & 1)   // [N][K] B: {16 k, BN rows} boxes, swizzled like A
+        if (pl.tma_mode & 1) {   // [N][K] B: {16 k, BN rows} boxes, swizzled like A
           TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->storage_elems / pl.tma_n, 16, (uint32_t)vi.bn, true));
-        else
-          TT_TRY(encode_2d(&mp.maps[1], B->data, pl.tma_n, B->storage_elems / pl.tma_n, (uint32_t)vi.bn + 2, 16, false));
+        } else {                 // [K][N] B: [blocks][K][N], boxes {BN+2 n, 16 k, 1 block}
+          const int64_t d3[3] = {pl.tma_n, pl.tma_k, B->storage_elems / (pl.tma_n * pl.tma_k)};
+          const uint32_t b3[3] = {(uint32_t)vi.bn + 2, 16, 1};
+          TT_TRY(encode_3d(&mp.maps[1], B->data, d3, b3));
+        }
         mp.map_ptr[0] = A->data;
         mp.map_ptr[1] = B->data;
       }

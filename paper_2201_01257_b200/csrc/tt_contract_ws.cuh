@@ -374,6 +374,15 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, 
 
 // BKC: B is [N][K] in its blocks (k contiguous, e.g. the implicit operand's X(q,s,L)): its box is
 // {16 k, BN rows} with the 128-byte swizzle of A and its fragments are read like A's.
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(d),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(b)
+      : "memory");
+}
+
 template <class K, bool BKC = false>
 struct TmaSmem {
   static constexpr int A_BYTES = K::BM * 128;                 // BK = 16 doubles = 128 B rows, swizzled
@@ -385,7 +394,7 @@ struct TmaSmem {
   static constexpr int STAGES = FIT < K::MAXSTAGES ? FIT : K::MAXSTAGES;
   static constexpr int BYTES = 1024 + STAGES * STAGE + 2 * STAGES * 8 + 64;
   static constexpr unsigned TX = (unsigned)(A_BYTES + B_BYTES);
-  static_assert(K::BK == 16, "TMA variant assumes 128-byte A rows");
+  static_assert(K::BK == 16, "TMA variant assumes 128-byte A rows");   // K tails: TMA zero fill
   static_assert(A_BYTES % 1024 == 0 && (!BKC || B_BYTES % 1024 == 0), "swizzled stages must stay 1024-byte aligned");
   static_assert(STAGES >= 3, "pipeline too shallow");
 };
@@ -428,14 +437,16 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
       for (int t = g->task_begin; t < g->task_end; ++t) {
         const TaskDesc* td = p.tasks + t;
         const int Kt = td->K;
+        // A: [rows][K] view (k tail: out-of-bounds zero fill); B: [rows][K] view ([N][K] blocks) or the
+        // [blocks][K][N] view ([K][N] blocks: rows past the block's K are out of bounds, zero fill)
         const int arow = (int)(td->a_off / Kt) + m0;
-        const int brow0 = (int)(td->b_off / p.tma_n);
+        const int bsel = BKC ? (int)(td->b_off / Kt) + n0 : (int)(td->b_off / ((int64_t)Kt * p.tma_n));
         for (int k0 = 0; k0 < Kt; k0 += K::BK) {
           mbar_wait_sleep(&empty[st], phase);
           mbar_expect_tx(&full[st], SM::TX);
           tma_load_2d(sA + st * SM::A_BYTES, &tmA, k0, arow, &full[st]);
-          if (BKC) tma_load_2d(sB + st * SM::B_BYTES, &tmB, k0, brow0 + n0, &full[st]);
-          else tma_load_2d(sB + st * SM::B_BYTES, &tmB, n0, brow0 + k0, &full[st]);
+          if (BKC) tma_load_2d(sB + st * SM::B_BYTES, &tmB, k0, bsel, &full[st]);
+          else tma_load_3d(sB + st * SM::B_BYTES, &tmB, n0, k0, bsel, &full[st]);
           if (++st == STAGES) { st = 0; phase ^= 1; }
         }
       }

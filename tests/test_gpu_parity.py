@@ -724,3 +724,41 @@ def test_contract_host_bitwise(env, terms):
     assert np.array_equal(got, plain)
     ref = O.pack(orc["R"], ref_d)
     assert normwise(got, ref) <= TOL
+
+
+def _wbuild_problem(n, tv, NL, tl, spin):
+    spaces = {"V": SpaceSpec(n, tile=tv, spin_split=spin), "L": SpaceSpec(NL, tile=tl)}
+    sp = (lambda up, lo: ("spin", up, lo)) if spin else (lambda up, lo: None)
+    return Problem(spaces, {"p": "V", "q": "V", "r": "V", "s": "V", "L": "L"},
+                   {"W": TensorSpec("pqrs", sp([0, 1], [2, 3])), "X": TensorSpec("prL", sp([0], [1])),
+                    "Y": TensorSpec("qsL", sp([0], [1]))},
+                   [("W", "pqrs", "X", "prL", "Y", "qsL")])
+
+
+@pytest.mark.parametrize("variant", [3, 4, 5])
+@pytest.mark.parametrize("case", ["wbuild_ktail", "wbuild_k16", "ladder_ktail", "hh_ktail"])
+def test_tma_general_layouts(env, variant, case):
+    """TMA producer beyond the uniform ladder: [N][K] B operands with a permuted (multi-group) output --
+    the implicit operand's W(p,q,r,s) = X(p,r,L) X(q,s,L) -- and K extents that are not multiples of 16
+    (the k tail is TMA out-of-bounds zero fill: a [blocks][K][N] view for [K][N] operands).  Bitwise
+    equal to the cp.async producer and within 1e-11 of the oracle."""
+    tt, torch = env
+    if case == "wbuild_ktail":
+        pb, beta = _wbuild_problem(20, 5, 20, 10, True), 0.0        # K = L tile 10: a tail of 10
+    elif case == "wbuild_k16":
+        pb, beta = _wbuild_problem(24, 6, 64, 32, False), 0.0
+    elif case == "ladder_ktail":
+        pb, beta = ccsd_problem(12, 24, 6, 6, True, terms=("ladder",)), 1.0   # K = 36: tail of 4
+    else:
+        pb, beta = ccsd_problem(12, 12, 6, 6, False, terms=("hh",)), 1.0      # K = 36
+    outs = []
+    for tma in ("1", "0"):
+        os.environ["TT_TMA"] = tma
+        ctx = new_ctx(tt, torch, variant)
+        got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[0], alpha=0.5, beta=beta, seed=9)
+        assert ctx.stats()["producer"] == (1 if tma == "1" else 0), case
+        assert normwise(got, ref) <= TOL
+        outs.append(got)
+    os.environ.pop("TT_TMA", None)
+    os.environ.pop("TT_FORCE_VARIANT", None)
+    assert np.array_equal(outs[0], outs[1])
