@@ -2255,7 +2255,7 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
       for (int u : nlab) bn.push_back(an.b_pos[u]);
       const int64_t K = uniform_group_extent(A, ak), N = uniform_group_extent(B, bn);
       // even rows (16-byte TMA strides); K tails are TMA out-of-bounds zero fill in both views
-      bool ok = K > 0 && N > 0 && K % 2 == 0 && N % 2 == 0;
+      bool ok = K > 0 && N > 0 && K % 2 == 0 && (b_nk || N % 2 == 0);
       for (int32_t k : ht.K) ok = ok && k == K;
       // every stored block starts on a row of its matrix view (no alignment pads between blocks)
       for (int64_t b = 0; ok && b < A->nblocks; ++b)
