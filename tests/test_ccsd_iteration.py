@@ -216,3 +216,29 @@ def test_ccsd_iteration_vs_oracle(shape):
     got2 = {n: it.T[n].download() for n in ("R1", "R2")}
     ctx.sync()
     assert E2 == E and all(np.array_equal(got[n], got2[n]) for n in got)
+
+
+@pytest.mark.parametrize("shape", [(6, 8, 3, 2, 10, 5), (8, 12, 2, 3, 10, 5)])
+def test_sampled_elements_equal_literal_oracle(shape):
+    """oracle/ccsd_sample.py (element-wise evaluation from the seeded recipe, integrals by Eq. cc12 with
+    the L sum taken last -- the full-size checker) equals oracle.ccsd.iterate on every element."""
+    from oracle.ccsd_sample import Inputs, Sampler
+    O_, V_, tO, tV, NL, tL = shape
+    ot, ref = oracle_reference(shape, 3)
+    sm = Sampler(Inputs(O_, V_, NL, 3))
+    s1 = np.abs(ref["R1"]).max()
+    for a in range(V_):
+        for i in range(O_):
+            if sm.nonzero_r1(a, i):
+                assert abs(sm.r1(a, i) - ref["R1"][a, i]) <= 1e-12 * s1, (a, i)
+            else:
+                assert ref["R1"][a, i] == 0.0
+    s2 = np.abs(ref["R2"]).max()
+    rng = np.random.default_rng(1)
+    for _ in range(60):
+        a, b = rng.integers(0, V_, 2)
+        i, j = rng.integers(0, O_, 2)
+        if sm.nonzero_r2(a, b, i, j):
+            assert abs(sm.r2(a, b, i, j) - ref["R2"][a, b, i, j]) <= 1e-12 * s2, (a, b, i, j)
+        else:
+            assert ref["R2"][a, b, i, j] == 0.0

@@ -53,6 +53,42 @@ def algorithmic_flops(it):
     return total, parts
 
 
+def sample_positions(O, V, seed=5):
+    """R2 / R1 sample positions spread over the spin blocks (alpha = first half, R6): one (a,b) pair and
+    one (i,j) pair per spin combination; R2 elements where the spin rule allows them, R1 likewise."""
+    rng = np.random.default_rng(seed)
+    ha, ho = V // 2, O // 2
+    pick = lambda lo, hi: int(rng.integers(lo, hi))   # noqa: E731
+    ab = [(pick(0, ha), pick(0, ha)), (pick(0, ha), pick(ha, V)), (pick(ha, V), pick(0, ha)), (pick(ha, V), pick(ha, V))]
+    ij = [(pick(0, ho), pick(0, ho)), (pick(0, ho), pick(ho, O)), (pick(ho, O), pick(0, ho)), (pick(ho, O), pick(ho, O))]
+    sv = lambda x: 1 if x < ha else -1   # noqa: E731
+    so = lambda x: 1 if x < ho else -1   # noqa: E731
+    r2 = [(a, b, i, j) for (a, b) in ab for (i, j) in ij if sv(a) + sv(b) == so(i) + so(j)]
+    r1 = [(a, i) for (a, _) in ab for (i, _) in ij if sv(a) == so(i)]
+    return r2, r1
+
+
+def element(T, buf, rank, idx):
+    """Value of global element ``idx`` of tensor T on this rank if this rank owns it (replicated: rank
+    0), else 0.0 -- read from the device storage buffer (compact or packed layout)."""
+    offs = [np.asarray(d.offsets) for d in T.dims]
+    tc = [int(np.searchsorted(o, x, side="right") - 1) for o, x in zip(offs, idx)]
+    blk = int(np.ravel_multi_index(tc, T.grid))
+    if not T.nz[blk]:
+        return 0.0
+    ext = [int(o[t + 1] - o[t]) for o, t in zip(offs, tc)]
+    loc = [int(x - o[t]) for o, t, x in zip(offs, tc, idx)]
+    e = int(np.ravel_multi_index(loc, ext))
+    so = int(T.storage_off[blk])
+    own = T.owner[blk] == rank or (T.owner[blk] == tt.TT_REPLICATED and rank == 0)
+    for (bb, lo, hi, ow) in T.parts:
+        if bb == blk and lo <= loc[0] < hi:
+            own = ow == rank
+    if not own or so < 0:
+        return 0.0
+    return float(buf[so + e].item())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--O", type=int, default=100)
@@ -63,6 +99,8 @@ def main():
     ap.add_argument("--ws-gb", type=float, default=4.0)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=2)   # >= 2: tt_contract autotunes on the first two calls
+    ap.add_argument("--samples-out", default=None, help="write sampled R1/R2 elements (and the CPU recheck)")
+    ap.add_argument("--no-check", action="store_true", help="with --samples-out: skip the CPU recheck")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -118,6 +156,34 @@ def main():
                           "flops_by_term": parts, "setup_s": setup_s, "kernel_ms_rank0": kernels,
                           "max_rank_contract_kernel_ms": float(kt[0]),
                           "tensor_gb": round(sum(mem.values()), 1), "workspace_gb": a.ws_gb}), flush=True)
+    if a.samples_out:
+        r2s, r1s = sample_positions(a.O, a.V)
+        vals = [element(it.T["R2"], it.bufs["R2"], rank, p) for p in r2s] + \
+               [element(it.T["R1"], it.bufs["R1"], rank, p) for p in r1s]
+        v = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(v)
+        if rank == 0:
+            v = v.cpu().numpy()
+            rec = {"config": {"O": a.O, "V": a.V, "tile": a.tile, "N_L": a.nl, "L_tile": a.ltile, "seed": 1,
+                              "n_gpus": world}, "energy": E,
+                   "r2": [[*p, float(x)] for p, x in zip(r2s, v[:len(r2s)])],
+                   "r1": [[*p, float(x)] for p, x in zip(r1s, v[len(r2s):])]}
+            if not a.no_check:
+                from oracle.ccsd_sample import Inputs, Sampler
+                t0 = time.time()
+                sm = Sampler(Inputs(a.O, a.V, a.nl, 1))
+                ref2 = [sm.r2(*p) for p in r2s]
+                ref1 = [sm.r1(*p) for p in r1s]
+                n2, n1 = max(abs(x) for x in ref2), max(abs(x) for x in ref1)
+                rec["check"] = {"r2_ref": ref2, "r1_ref": ref1, "seconds": time.time() - t0,
+                                "r2_normwise": max(abs(x - y) for x, y in zip(v[:len(r2s)], ref2)) / n2,
+                                "r1_normwise": max(abs(x - y) for x, y in zip(v[len(r2s):], ref1)) / n1,
+                                "how": "oracle/ccsd_sample.py on the host cores (norm = max |ref| over the samples)"}
+            with open(a.samples_out, "w") as f:
+                json.dump(rec, f, indent=1)
+            print(json.dumps({"samples_out": a.samples_out, "check": rec.get("check", {}).get("r2_normwise")}),
+                  flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
