@@ -335,8 +335,8 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_ws_kernel(co
           const int n = n0 + wn * K::WTN + j * 8 + 2 * q + r;
           if (n >= N) continue;
           double* c = Cb + om + dot_decode(n, p.nN, next, cns);
-          const double v = alpha * acc[i][j][r];
-          *c = (beta == 0.0) ? v : beta * *c + v;
+          const double v = __dmul_rn(alpha, acc[i][j][r]);
+          *c = (beta == 0.0) ? v : __fma_rn(beta, *c, v);
         }
       }
     }
@@ -539,8 +539,8 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
           const int n = n0 + wn * K::WTN + j * 8 + (BKC ? perm8(2 * q + r) : 2 * q + r);
           if (n >= N) continue;
           double* c = Cb + om + (MULTI ? (int64_t)dot_decode(n, p.nN, next, cnv) : (int64_t)n * cns);
-          const double v = alpha * acc[i][j][r];
-          *c = (beta == 0.0) ? v : beta * *c + v;
+          const double v = __dmul_rn(alpha, acc[i][j][r]);
+          *c = (beta == 0.0) ? v : __fma_rn(beta, *c, v);
         }
       }
     }

@@ -189,11 +189,15 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_kernel(const
     const double* b = sB + (s % K::STAGES) * K::BK * K::LDB + wn * K::WTN + fr_r;
 #pragma unroll
     for (int kk = 0; kk < K::BK / 4; ++kk) {
+      // k of this lane in DMMA step kk: the two steps of every 8-wide k octet take k = 2*(lane%4) + t,
+      // the grouping of the warp-specialised family, so that every variant adds each output element's
+      // products in the same groups of four (identical bits across variants, R12)
+      const int kr = 8 * (kk >> 1) + 2 * fr_k + (kk & 1);
       double af[K::MT], bf[K::NT];
 #pragma unroll
-      for (int i = 0; i < K::MT; ++i) af[i] = a[(kk * 4 + fr_k) * K::LDA + i * 8];
+      for (int i = 0; i < K::MT; ++i) af[i] = a[kr * K::LDA + i * 8];
 #pragma unroll
-      for (int j = 0; j < K::NT; ++j) bf[j] = b[(kk * 4 + fr_k) * K::LDB + j * 8];
+      for (int j = 0; j < K::NT; ++j) bf[j] = b[kr * K::LDB + j * 8];
 #pragma unroll
       for (int i = 0; i < K::MT; ++i)
 #pragma unroll
@@ -218,8 +222,8 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB) tt_contract_kernel(const
         const int n = n0 + wn * K::WTN + j * 8 + 2 * fr_k + r;
         if (n >= N) continue;
         double* c = Cb + om + dot_decode(n, nN, g.next, g.cn_str);
-        const double v = alpha * acc[i][j][r];
-        *c = (beta == 0.0) ? v : beta * *c + v;
+        const double v = __dmul_rn(alpha, acc[i][j][r]);
+        *c = (beta == 0.0) ? v : __fma_rn(beta, *c, v);
       }
     }
   }
@@ -487,8 +491,12 @@ __device__ __forceinline__ int64_t y_row_offset(uint32_t r, const ElemDesc& d) {
 
 constexpr int kRowsPerWarp = 4;   // rows mode: rows of one warp in flight
 
+// beta*x + alpha*y with ONE rounding order in every kernel and block mode (explicit intrinsics: the
+// compiler never re-associates or contracts them differently per call site), so that a block gives the
+// same bits whether it runs as tiles, rows or segments (e.g. whole vs row-split blocks, R12)
 __device__ __forceinline__ double axpby(double alpha, double y, double beta, double x) {
-  return (beta == 0.0) ? alpha * y : beta * x + alpha * y;
+  const double t = __dmul_rn(alpha, y);
+  return (beta == 0.0) ? t : __fma_rn(beta, x, t);
 }
 
 // Deterministic warp-then-CTA sum of one value per thread (fixed shuffle tree, warps in order).
@@ -828,7 +836,8 @@ __global__ void split_reduce_kernel(const double* __restrict__ P, double* __rest
     double acc = 0.0;
     for (int32_t s = 0; s < sd.nslots; ++s) acc += ps[(int64_t)s * sd.vol];
     double* o = C + sd.c_off + off;
-    *o = (beta == 0.0) ? alpha * acc : beta * *o + alpha * acc;
+    const double v = __dmul_rn(alpha, acc);
+    *o = (beta == 0.0) ? v : __fma_rn(beta, *o, v);
   }
 }
 

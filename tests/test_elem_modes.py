@@ -106,3 +106,38 @@ def test_integer_add_bit_exact(env):
     ctx.sync()
     assert np.array_equal(got, O.pack(orc["C"], O.add(dense["C"], "abij", dense["A"], "jabi", -3.0, 2.0)))
     ctx.close()
+
+
+@pytest.mark.gpu
+def test_add_bits_independent_of_block_mode():
+    """A permuted add gives the same bits whether a block runs as 32x32 transpose tiles (whole block) or as
+    generic segments (row-split block): one rounding order, beta*x + alpha*y = fma(beta, x, alpha*y), in
+    every element kernel (R12: results independent of the partition)."""
+    import torch
+    import paper_2201_01257_b200 as tt
+    from tests.cases import ccsd_problem, oracle_objects, product_objects
+    import synthetic as S
+    from oracle import ops as O
+    pb = ccsd_problem(12, 24, 6, 8, True, terms=("ladder",))
+    orc = oracle_objects(pb)
+    outs = []
+    for split in (False, True):
+        ctx = tt.Context(device=0, stream=torch.cuda.current_stream().cuda_stream)
+        P = product_objects(tt, ctx, pb)
+        R, T = P["R"], P["T"]
+        if split:   # every non-zero R block owned by rank 0 in two row parts: segments instead of tiles
+            parts = []
+            for blk in range(R.nblocks):
+                if R.nz[blk]:
+                    e0 = int(np.diff(R.dims[0].offsets)[np.unravel_index(blk, R.grid)[0]])
+                    parts += [(blk, 0, e0 // 2, 0), (blk, e0 // 2, e0, 0)]
+            R.set_parts(parts)
+        bR = torch.from_numpy(O.pack(orc["R"], O.dense_masked(orc["R"], S.dense(orc["R"].shape, 4, 3)))).cuda()
+        bT = torch.from_numpy(O.pack(orc["T"], O.dense_masked(orc["T"], S.dense(orc["T"].shape, 4, 5)))).cuda()
+        R.bind(bR)
+        T.bind(bT)
+        tt.add(ctx, R, "abij", 0.7, -1.3, T, "abji")
+        outs.append(R.download())
+        ctx.sync()
+        ctx.close()
+    assert np.array_equal(outs[0], outs[1])

@@ -36,22 +36,25 @@ ALPHA = 0.5
 SEED = 1
 
 
-def sample_positions(O, V, nrows=3, ncols=12, seed=11):
-    """(a, b, i, j) global positions: rows of each spin type, columns with conserved spin."""
+def sample_positions(O, V, voffs, per_row=2, seed=11):
+    """(a, b, i, j) global positions: one (a,b) row per (a_t, b_t) tile pair -- every tile pair of R,
+    hence every R block row, is sampled -- at a seeded position inside the tiles,
+    with ``per_row`` (i,j) columns of conserved spin each."""
     rng = np.random.default_rng(seed)
     h, o = V // 2, O // 2
-    rows = [(int(rng.integers(0, h)), int(rng.integers(h, V))),       # alpha beta
-            (int(rng.integers(0, h)), int(rng.integers(0, h))),       # alpha alpha
-            (int(rng.integers(h, V)), int(rng.integers(h, V)))][:nrows]
     out = []
-    for a, b in rows:
-        sa, sb = a < h, b < h
-        k = 0
-        while k < ncols:
-            i, j = int(rng.integers(0, O)), int(rng.integers(0, O))
-            if (sa + sb) == ((i < o) + (j < o)):
-                out.append((a, b, i, j))
-                k += 1
+    nt = len(voffs) - 1
+    for ta in range(nt):
+        for tb in range(nt):
+            a = int(rng.integers(voffs[ta], voffs[ta + 1]))
+            b = int(rng.integers(voffs[tb], voffs[tb + 1]))
+            sa, sb = a < h, b < h
+            k = 0
+            while k < per_row:
+                i, j = int(rng.integers(0, O)), int(rng.integers(0, O))
+                if (sa + sb) == ((i < o) + (j < o)):
+                    out.append((a, b, i, j))
+                    k += 1
     return out
 
 
@@ -169,7 +172,7 @@ def main():
     samples = []
     if a.samples_out:
         offs = [tv.offsets, tv.offsets, to.offsets, to.offsets]
-        for pos in sample_positions(O, V):
+        for pos in sample_positions(O, V, [int(x) for x in tv.offsets]):
             t = [int(np.searchsorted(offs[d], pos[d], side="right") - 1) for d in range(4)]
             blk = int(np.ravel_multi_index(t, R.grid))
             loc = [pos[d] - int(offs[d][t[d]]) for d in range(4)]
