@@ -351,7 +351,41 @@ __device__ __forceinline__ void tma4(void* smem, const CUtensorMap* map, int c0,
 }
 }  // namespace
 
-__global__ void __launch_bounds__(THREADS, 2)
+// One more warp than the compute warps: warp 8 is the TMA producer (lane 0 issues the boxes of every
+// stage into a TNS-slot ring; per-slot "full" barriers complete on the transaction bytes, per-slot
+// "empty" barriers collect one arrival per compute warp), so no CTA-wide barrier sits in the k loop.
+constexpr int TTHREADS = THREADS + 32;
+
+// Whether the 8x8 output fragment (rows r0..r0+7 of the GEMM's row box, column pair (p, q0..q0+7)) of GEMM
+// g holds an element with a < b < c inside the boxes' extents (roles: g = 0 (a; b,c), 1 (b; a,c),
+// 2 (c; a,b)).  Greedy: the smallest a, then the smallest b > a, then the smallest c > b.
+__device__ __forceinline__ bool frag_needed(int g, int r0, int pp, int q0, const int32_t* lo, const int32_t* ex) {
+  int i0[3], i1[3];   // local [lo, hi) per virtual index a, b, c
+  const int rr = g == 0 ? 0 : (g == 1 ? 1 : 2), pr = g == 0 ? 1 : 0, qr = g == 2 ? 1 : 2;
+  i0[rr] = r0; i1[rr] = r0 + 8;
+  i0[pr] = pp; i1[pr] = pp + 1;
+  i0[qr] = q0; i1[qr] = q0 + 8;
+  int gl[3], gh[3];
+  for (int d = 0; d < 3; ++d) {
+    const int h = i1[d] < ex[d] ? i1[d] : ex[d];
+    if (i0[d] >= h) return false;
+    gl[d] = lo[d] + i0[d];
+    gh[d] = lo[d] + h - 1;
+  }
+  const int a = gl[0];
+  const int b = (a + 1 > gl[1]) ? a + 1 : gl[1];
+  if (b > gh[1]) return false;
+  const int c = (b + 1 > gl[2]) ? b + 1 : gl[2];
+  return c <= gh[2];
+}
+
+__device__ __forceinline__ void tbar_arrive(uint64_t* bar) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(s) : "memory");
+}
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(THREADS) : "memory"); }
+
+__global__ void __launch_bounds__(TTHREADS, 2)
     triples_fused_tma_kernel(const TriplesParams p, const __grid_constant__ CUtensorMap mVO,
                              const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
                              const __grid_constant__ CUtensorMap mVV) {
@@ -360,7 +394,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   double* cube = reinterpret_cast<double*>(base + TNS * TSTAGE);   // [BX][BX][BX]
   double* red = cube + BX * BX * BX;                               // [THREADS]
   uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS]
-  int32_t* segb = reinterpret_cast<int32_t*>(full + TNS);          // [3][6] first summed index
+  uint64_t* empty = full + TNS;                                    // [TNS]
+  int32_t* segb = reinterpret_cast<int32_t*>(empty + TNS);         // [3][6] first summed index
   int32_t* segn = segb + 18;                                       // [3][6] stages
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t u = p.unit0 + blockIdx.x;
@@ -372,12 +407,11 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int32_t ex[3] = {p.box_ext[bx.x], p.box_ext[bx.y], p.box_ext[bx.z]};
   const int32_t I = tr.x, J = tr.y, K = tr.z;
   if (tid == 0) {
-    for (int q = 0; q < TNS; ++q) tbar_init(&full[q], 1);
+    for (int q = 0; q < TNS; ++q) {
+      tbar_init(&full[q], 1);
+      tbar_init(&empty[q], NWARP);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2Q) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
   }
   if (tid < 18) {
     // summed range of segment sg of GEMM g.  With spin (R6: alpha = first half), the m of v^{xy}_{m r}
@@ -407,94 +441,98 @@ __global__ void __launch_bounds__(THREADS, 2)
     segn[tid] = (e - b + KC - 1) / KC;
   }
   __syncthreads();
-  int32_t total = 0;
-  for (int q = 0; q < 18; ++q) total += segn[q];
-  // stage cursor over (GEMM, segment, stage) skipping empty segments
-  struct Cur { int g, sg, j; };
-  auto advance = [&](Cur& c) {
-    if (++c.j < segn[c.g * 6 + c.sg]) return;
-    c.j = 0;
-    do {
-      if (++c.sg == 6) { c.sg = 0; ++c.g; }
-    } while (c.g < 3 && segn[c.g * 6 + c.sg] == 0);
-  };
-  auto first = [&]() {
-    Cur c{0, 0, 0};
-    while (c.g < 3 && segn[c.g * 6 + c.sg] == 0) {
-      if (++c.sg == 6) { c.sg = 0; ++c.g; }
-    }
-    return c;
-  };
-  int islot = 0;
-  Cur ic = first();
-  auto issue = [&]() {   // thread 0: the stage at cursor ic into slot islot
-    const int g = ic.g, sg = ic.sg;
-    const int32_t k0 = segb[g * 6 + sg] + ic.j * KC;
-    const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
-    const int32_t lo_p = g == 0 ? lo[1] : lo[0];
-    const int32_t lo_q = g == 2 ? lo[1] : lo[2];
-    unsigned char* st = base + islot * TSTAGE;
-    double* P = reinterpret_cast<double*>(st);
-    double* Q = reinterpret_cast<double*>(st + TP_BYTES);
-    tbar_expect(&full[islot], (unsigned)TSTAGE);
-    if (sg < 3) {
-      const int s = sg;
-      const int32_t x = (s == 2) ? J : I, y = (s == 0) ? J : K, z = (s == 0) ? K : (s == 1 ? J : I);
-      tma4(P, &mVO, lo_r, k0, y, x, &full[islot]);          // VO[x][y][m][r]
-      tma4(Q, &mT2Q, lo_q, lo_p, z, k0, &full[islot]);      // T2[m][z][p][q]
-    } else {
-      const int s = sg - 3;
-      const int32_t x = (s == 0) ? I : (s == 1 ? J : K), y = (s == 0) ? J : I, z = (s == 2) ? J : K;
-      tma4(P, &mT2P, lo_r, k0, z, y, &full[islot]);         // T2[y][z][e][r]
-      tma4(Q, &mVV, lo_q, lo_p, x, k0, &full[islot]);       // VV[e][x][p][q]
-    }
-    advance(ic);
-    islot = (islot + 1 == TNS) ? 0 : islot + 1;
-  };
-  // rows past a segment's end read the next index range: zero (spin-forbidden half under R7 maps) or TMA
-  // out-of-bounds fill past n_o / n_v
-  if (tid == 0)
-    for (int t = 0; t < TNS && t < total; ++t) issue();
 
+  if (warp == NWARP) {
+    // ---------------------------------------------------------------- TMA producer (one thread)
+    if (lane != 0) return;
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2Q) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
+    int slot = 0;
+    unsigned phase = 1;   // empty barriers: the first pass over the ring does not wait
+    for (int g = 0; g < 3; ++g) {
+      const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
+      const int32_t lo_p = g == 0 ? lo[1] : lo[0];
+      const int32_t lo_q = g == 2 ? lo[1] : lo[2];
+      for (int sg = 0; sg < 6; ++sg) {
+        const int32_t n = segn[g * 6 + sg];
+        for (int jj = 0; jj < n; ++jj) {
+          const int32_t k0 = segb[g * 6 + sg] + jj * KC;
+          tbar_wait(&empty[slot], phase);
+          unsigned char* st = base + slot * TSTAGE;
+          double* P = reinterpret_cast<double*>(st);
+          double* Q = reinterpret_cast<double*>(st + TP_BYTES);
+          tbar_expect(&full[slot], (unsigned)TSTAGE);
+          if (sg < 3) {
+            const int32_t x = (sg == 2) ? J : I, y = (sg == 0) ? J : K, z = (sg == 0) ? K : (sg == 1 ? J : I);
+            tma4(P, &mVO, lo_r, k0, y, x, &full[slot]);          // VO[x][y][m][r]
+            tma4(Q, &mT2Q, lo_q, lo_p, z, k0, &full[slot]);      // T2[m][z][p][q]
+          } else {
+            const int s3 = sg - 3;
+            const int32_t x = (s3 == 0) ? I : (s3 == 1 ? J : K), y = (s3 == 0) ? J : I, z = (s3 == 2) ? J : K;
+            tma4(P, &mT2P, lo_r, k0, z, y, &full[slot]);         // T2[y][z][e][r]
+            tma4(Q, &mVV, lo_q, lo_p, x, k0, &full[slot]);       // VV[e][x][p][q]
+          }
+          if (++slot == TNS) { slot = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ compute warps (8)
   double acc[2][NFR][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int f = 0; f < NFR; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
-  int slot = 0, t = 0;
+  int slot = 0;
   unsigned phase = 0;
 #pragma unroll 1
   for (int g = 0; g < 3; ++g) {
+    // output fragments of this warp that hold a needed W(a,b,c) (a<b<c inside the extents): the others
+    // (diagonal box triples, narrow tail boxes) are not computed
+    uint32_t need = 0;
+#pragma unroll
+    for (int rf = 0; rf < 2; ++rf)
+#pragma unroll
+      for (int f = 0; f < NFR; ++f) {
+        const int col = warp * CW + f * 8;
+        if (frag_needed(g, 8 * rf, col / BX, col % BX, lo, ex)) need |= 1u << (rf * NFR + f);
+      }
 #pragma unroll 1
     for (int sg = 0; sg < 6; ++sg) {
       const int32_t n = segn[g * 6 + sg];
       const bool neg = sg < 3 ? sg == 1 : sg != 4;   // m sums (+,-,+), e sums (-,+,-)
       const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
 #pragma unroll 1
-      for (int jj = 0; jj < n; ++jj, ++t) {
+      for (int jj = 0; jj < n; ++jj) {
         tbar_wait(&full[slot], phase);
-        const double* P = reinterpret_cast<const double*>(base + slot * TSTAGE);
-        const double* Q = reinterpret_cast<const double*>(base + slot * TSTAGE + TP_BYTES);
+        if (need) {
+          const double* P = reinterpret_cast<const double*>(base + slot * TSTAGE);
+          const double* Q = reinterpret_cast<const double*>(base + slot * TSTAGE + TP_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < KC / 4; ++kk) {
-          const int kl = kk * 4 + (lane & 3);
-          const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
-          const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
+          for (int kk = 0; kk < KC / 4; ++kk) {
+            const int kl = kk * 4 + (lane & 3);
+            const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
+            const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
 #pragma unroll
-          for (int f = 0; f < NFR; ++f) {
-            const int col = warp * CW + f * 8 + (lane >> 2);
-            const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
-            dmma(acc[0][f], a0, b);
-            dmma(acc[1][f], a1, b);
+            for (int f = 0; f < NFR; ++f) {
+              const int col = warp * CW + f * 8 + (lane >> 2);
+              const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
+              if (need & (1u << f)) dmma(acc[0][f], a0, b);
+              if (need & (1u << (NFR + f))) dmma(acc[1][f], a1, b);
+            }
           }
         }
-        __syncthreads();                          // every warp is done with this slot
-        if (tid == 0 && t + TNS < total) issue();
-        slot = (slot + 1 == TNS) ? 0 : slot + 1;
-        if (slot == 0) phase ^= 1;
+        __syncwarp();
+        if (lane == 0) tbar_arrive(&empty[slot]);
+        if (++slot == TNS) { slot = 0; phase ^= 1; }
       }
     }
-    // GEMM g done: fold into the cube
+    // GEMM g done: fold into the cube (each cube entry has one owner thread per GEMM; the barriers
+    // order the three folds)
 #pragma unroll
     for (int rf = 0; rf < 2; ++rf)
 #pragma unroll
@@ -510,7 +548,7 @@ __global__ void __launch_bounds__(THREADS, 2)
           else cube[cidx(pp, q, row)] += v;
           acc[rf][f][h] = 0.0;
         }
-    __syncthreads();
+    compute_sync();
   }
   // Eq. cc14 over the cube (as the cp.async kernel)
   double s = 0.0;
@@ -539,10 +577,10 @@ __global__ void __launch_bounds__(THREADS, 2)
     s += (W + v1) * W / D;
   }
   red[tid] = s;
-  __syncthreads();
+  compute_sync();
   for (int o = THREADS / 2; o > 0; o >>= 1) {
     if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
+    compute_sync();
   }
   if (tid == 0) p.partials[u] = red[0];
 }
@@ -761,7 +799,7 @@ cudaError_t launch_triples_pair(const TriplesParams& p, const void* maps, int64_
 }
 
 size_t triples_tma_smem() {
-  return 128 + (size_t)TNS * TSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 16 * TNS;
+  return 128 + (size_t)TNS * TSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 16 * TNS + 4 * 36;
 }
 
 cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s) {
@@ -774,7 +812,7 @@ cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t
     attr = true;
   }
   const CUtensorMap* m = static_cast<const CUtensorMap*>(maps);
-  triples_fused_tma_kernel<<<(unsigned)nunits, THREADS, smem, s>>>(p, m[0], m[1], m[2], m[3]);
+  triples_fused_tma_kernel<<<(unsigned)nunits, TTHREADS, smem, s>>>(p, m[0], m[1], m[2], m[3]);
   return cudaGetLastError();
 }
 

@@ -71,6 +71,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=2)   # >= 2: tt_contract autotunes on the first two calls
     ap.add_argument("--samples-out", default="")
+    ap.add_argument("--lib-ws-gb", type=float, default=2.0, help="libtt device workspace (tt_workspace_bind)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -94,7 +95,9 @@ def main():
     V = WEAK_V[world] if a.weak else a.V
     NL = a.nl or 2 * (O + V)
     stream = torch.cuda.current_stream()
-    ctx = tt.Context(device=local, stream=stream.cuda_stream, rank=rank, nranks=world, nccl_id=nid)
+    # library workspace (metadata of the 400k-task plans and of every batch of the implicit ladder)
+    ctx = tt.Context(device=local, stream=stream.cuda_stream, rank=rank, nranks=world, nccl_id=nid,
+                     workspace_bytes=int(a.lib_ws_gb * (1 << 30)))
     so = tt.IndexSpace(O, [(0, O // 2), (O // 2, O)], [1, -1])
     sv = tt.IndexSpace(V, [(0, V // 2), (V // 2, V)], [1, -1])
     to, tv = tt.TiledIndexSpace(so, a.tile), tt.TiledIndexSpace(sv, a.tile)
