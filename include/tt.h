@@ -74,7 +74,8 @@ typedef struct {
   int64_t launches;        /* kernels launched by the call                                         */
   int32_t plan_cached;     /* 1 if the task list / partition / gather plan came from the cache     */
   int32_t kernel_variant;  /* contraction kernel tile variant used                  */
-  int32_t producer;        /* operand staging of that kernel: 0 = cp.async, 1 = TMA                */
+  int32_t producer;        /* operand staging of that kernel: 0 = cp.async, 1 = TMA; (T): 2 = pair  */
+                           /* kernel, 3 = 2-CTA cluster with TMA multicast (tt_triples_energy)      */
   double aux_flops;        /* FLOPs spent building implicit operands (tt_contract_cholesky)         */
 } tt_stats;
 

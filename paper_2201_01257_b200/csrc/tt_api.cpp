@@ -3978,11 +3978,15 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
       TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_box_lo, box_lo.size()));
       TT_TRY(dev_alloc(ctx, tp->mem, &tp->d_box_ext, box_ext.size()));
       if (!units.empty()) TT_CUDA(cudaMemcpy(tp->d_units, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice));
-      // pairs of consecutive units of this rank with the same box triple and occupied pair (i,j)
+      // pairs of consecutive units of this rank with the same box triple, occupied pair (i,j) and spin of k
+      // (then both units run the same segment ranges: the cluster kernel shares one operand per segment)
       std::vector<int2> pairs;
+      const int32_t ohalf = tp->o_half;
+      auto kspin = [&](int32_t k) { return ohalf ? (k < ohalf ? 1 : -1) : 0; };
       for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits;) {
         const bool two = q + 1 < tp->unit0 + tp->nunits && units[q + 1].x == units[q].x &&
-                         trip[units[q + 1].y].x == trip[units[q].y].x && trip[units[q + 1].y].y == trip[units[q].y].y;
+                         trip[units[q + 1].y].x == trip[units[q].y].x && trip[units[q + 1].y].y == trip[units[q].y].y &&
+                         kspin(trip[units[q + 1].y].z) == kspin(trip[units[q].y].z);
         pairs.push_back({(int)q, two ? 2 : 1});
         q += two ? 2 : 1;
       }
@@ -4046,18 +4050,25 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     TT_TRY(encode_4d(&maps[2], p.T2, dT2, bQ));
     TT_TRY(encode_4d(&maps[3], p.VV, dVV, bQ));
   }
+  // opt-in: the 2-CTA cluster kernel with TMA multicast of the shared operand (TT_TRIPLES_CLUSTER=1;
+  // measured 5.79 s vs 3.08 s at O=40 V=200: the two CTAs release every slot together, so each waits on
+  // the other's slowest warp) or the 16-warp pair kernel (TT_TRIPLES_PAIR=1; 4.59 s)
   const char* fp = getenv("TT_TRIPLES_PAIR");
-  const bool use_pair = use_tma && fp && atoi(fp) != 0;   // measured slower (4.59 s vs 3.37 s): opt-in
-  ctx->last.producer = use_pair ? 2 : (use_tma ? 1 : 0);
-  if (use_pair) {
+  const char* fc = getenv("TT_TRIPLES_CLUSTER");
+  const bool use_pair = use_tma && fp && atoi(fp) != 0;
+  const bool use_cluster = use_tma && !use_pair && fc && atoi(fc) != 0;
+  ctx->last.producer = use_pair ? 2 : (use_cluster ? 3 : (use_tma ? 1 : 0));
+  if (use_pair || use_cluster) {
     for (int64_t q0 = 0; q0 < tp->npairs; q0 += (1 << 20)) {
       p.pairs = tp->d_pairs + q0;
       Launch L(ctx, "tt_triples_fused");
-      TT_CUDA(launch_triples_pair(p, maps, std::min<int64_t>(1 << 20, tp->npairs - q0), ctx->stream));
+      const int64_t np = std::min<int64_t>(1 << 20, tp->npairs - q0);
+      if (use_cluster) TT_CUDA(launch_triples_cluster(p, maps, np, ctx->stream));
+      else TT_CUDA(launch_triples_pair(p, maps, np, ctx->stream));
     }
   }
   // launches of at most 2^20 units (keeps each launch's grid small; partials are indexed by unit)
-  for (int64_t u0 = tp->unit0; !use_pair && u0 < tp->unit0 + tp->nunits; u0 += (1 << 20)) {
+  for (int64_t u0 = tp->unit0; !use_pair && !use_cluster && u0 < tp->unit0 + tp->nunits; u0 += (1 << 20)) {
     p.unit0 = u0;
     const int64_t n = std::min<int64_t>(1 << 20, tp->unit0 + tp->nunits - u0);
     Launch L(ctx, "tt_triples_fused");

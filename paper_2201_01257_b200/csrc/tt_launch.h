@@ -217,5 +217,7 @@ cudaError_t launch_triples_fused(const TriplesParams& p, int64_t nunits, cudaStr
 cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s);
 // pair variant (two units with the same box triple and occupied pair (i,j) per CTA, shared operands)
 cudaError_t launch_triples_pair(const TriplesParams& p, const void* maps, int64_t npairs, cudaStream_t s);
+// 2-CTA cluster variant over the same pairs: the shared operand of every segment by TMA multicast
+cudaError_t launch_triples_cluster(const TriplesParams& p, const void* maps, int64_t npairs, cudaStream_t s);
 
 }  // namespace tt

@@ -780,6 +780,274 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   if (ht == 0 && active) p.partials[u1 + h] = red[tid];
 }
 
+// -------------------------------------------------------------------------------------------------
+// Cluster variant (opt-in, TT_TRIPLES_CLUSTER=1; measured slower: 5.79 s vs 3.08 s at O=40 V=200 --
+// both CTAs must release a slot before either refills it, so each CTA runs at the pace of the other's
+// slowest warp through only 3 slots): a 2-CTA thread-block cluster computes the two units (i,j,k1), (i,j,k2) of
+// a pair (same box triple, same spin of k: identical segment ranges).  In every segment one operand is
+// the same for both triples (the pair analysis above); CTA 0 loads it ONCE with a TMA multicast into
+// both CTAs' shared memory, and each CTA loads its own per-triple operand.  L2->SM traffic per stage
+// drops from P + Q to about (P + Q/2) or (P/2 + Q): ~1/3 less, while each CTA keeps the single-unit
+// layout (8 compute warps + producer warp, 2 CTAs per SM).  Each slot's "empty" barrier collects the
+// releases of BOTH CTAs' compute warps (local arrive + remote arrive on the peer through its cluster
+// address), so neither producer refills a slot the other CTA still reads or the multicast still
+// targets.  A lone unit (odd run of k) gives both CTAs the same unit; CTA 1 then writes no partial.
+size_t triples_tma_smem();
+
+namespace {
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tbar_arrive_peer(uint64_t* bar, unsigned peer) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(bar), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(s), "r"(peer));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(r) : "memory");
+}
+__device__ __forceinline__ void tma4_mc(void* smem, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar,
+                                        unsigned short mask) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;\n"
+      ::"r"(d), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(b), "h"(mask)
+      : "memory");
+}
+}  // namespace
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TTHREADS, 2)
+    triples_cluster_tma_kernel(const TriplesParams p, const __grid_constant__ CUtensorMap mVO,
+                               const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
+                               const __grid_constant__ CUtensorMap mVV) {
+  extern __shared__ __align__(128) unsigned char csm_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)csm_raw + 127) & ~(uintptr_t)127);
+  double* cube = reinterpret_cast<double*>(base + TNS * TSTAGE);   // [BX][BX][BX]
+  double* red = cube + BX * BX * BX;                               // [THREADS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS]
+  uint64_t* empty = full + TNS;                                    // [TNS]
+  int32_t* segb = reinterpret_cast<int32_t*>(empty + TNS);         // [3][6]
+  int32_t* segn = segb + 18;                                       // [3][6]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned crank = cluster_rank(), peer = crank ^ 1u;
+  const int2 pr = p.pairs[blockIdx.x >> 1];
+  const bool two = pr.y == 2;
+  const int64_t u = (int64_t)pr.x + ((two && crank) ? 1 : 0);
+  const int2 un = p.units[u];
+  const int4 bx = p.box3[un.x];
+  const int4 tr = p.trip[un.y];
+  const int32_t nO = p.nO, nV = p.nV;
+  const int32_t lo[3] = {p.box_lo[bx.x], p.box_lo[bx.y], p.box_lo[bx.z]};
+  const int32_t ex[3] = {p.box_ext[bx.x], p.box_ext[bx.y], p.box_ext[bx.z]};
+  const int32_t I = tr.x, J = tr.y, K = tr.z;
+  if (tid == 0) {
+    for (int q = 0; q < TNS; ++q) {
+      tbar_init(&full[q], 1);
+      tbar_init(&empty[q], 2 * NWARP);   // this CTA's and the peer's compute warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (tid < 18) {   // segment ranges (identical in both CTAs: same i, j and spin of k)
+    const int g = tid / 6, sg = tid % 6;
+    const int32_t oh = p.o_half, vh = p.v_half;
+    auto so = [&](int32_t x) { return oh ? (x < oh ? 1 : -1) : 0; };
+    auto sv = [&](int32_t v) { return vh ? (v < vh ? 1 : -1) : 0; };
+    const int32_t sr = sv(g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]));
+    const int32_t sp = sv(g == 0 ? lo[1] : lo[0]), sq = sv(g == 2 ? lo[1] : lo[2]);
+    int32_t b = 0, e = 0;
+    if (sg < 3) {
+      const int32_t x = (sg == 2) ? J : I, y = (sg == 0) ? J : K;
+      const int32_t sm = so(x) + so(y) - sr;
+      if (!oh) { b = 0; e = nO; }
+      else if (sm == 1) { b = 0; e = oh; }
+      else if (sm == -1) { b = oh; e = nO; }
+    } else {
+      const int32_t x = (sg == 3) ? I : (sg == 4 ? J : K);
+      const int32_t se = sp + sq - so(x);
+      if (!vh) { b = 0; e = nV; }
+      else if (se == 1) { b = 0; e = vh; }
+      else if (se == -1) { b = vh; e = nV; }
+    }
+    segb[tid] = b;
+    segn[tid] = (e - b + KC - 1) / KC;
+  }
+  __syncthreads();
+  cluster_sync_all();   // the peer's barriers are initialised before any multicast or remote arrive
+
+  if (warp == NWARP) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2Q) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
+      int slot = 0;
+      unsigned phase = 1;
+      for (int g = 0; g < 3; ++g) {
+        const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
+        const int32_t lo_p = g == 0 ? lo[1] : lo[0];
+        const int32_t lo_q = g == 2 ? lo[1] : lo[2];
+        for (int sg = 0; sg < 6; ++sg) {
+          const int32_t n = segn[g * 6 + sg];
+          // shared operand of the segment: P in (m, s=0) and (e, s=2), else Q
+          const bool pshared = sg == 0 || sg == 5;
+          for (int jj = 0; jj < n; ++jj) {
+            const int32_t k0 = segb[g * 6 + sg] + jj * KC;
+            tbar_wait(&empty[slot], phase);
+            unsigned char* st = base + slot * TSTAGE;
+            double* P = reinterpret_cast<double*>(st);
+            double* Q = reinterpret_cast<double*>(st + TP_BYTES);
+            tbar_expect(&full[slot], (unsigned)TSTAGE);   // own operand + the multicast one
+            if (sg < 3) {
+              const int32_t x = (sg == 2) ? J : I, y = (sg == 0) ? J : K, z = (sg == 0) ? K : (sg == 1 ? J : I);
+              if (pshared) {
+                if (crank == 0) tma4_mc(P, &mVO, lo_r, k0, y, x, &full[slot], 3);
+                tma4(Q, &mT2Q, lo_q, lo_p, z, k0, &full[slot]);
+              } else {
+                tma4(P, &mVO, lo_r, k0, y, x, &full[slot]);
+                if (crank == 0) tma4_mc(Q, &mT2Q, lo_q, lo_p, z, k0, &full[slot], 3);
+              }
+            } else {
+              const int s3 = sg - 3;
+              const int32_t x = (s3 == 0) ? I : (s3 == 1 ? J : K), y = (s3 == 0) ? J : I, z = (s3 == 2) ? J : K;
+              if (pshared) {
+                if (crank == 0) tma4_mc(P, &mT2P, lo_r, k0, z, y, &full[slot], 3);
+                tma4(Q, &mVV, lo_q, lo_p, x, k0, &full[slot]);
+              } else {
+                tma4(P, &mT2P, lo_r, k0, z, y, &full[slot]);
+                if (crank == 0) tma4_mc(Q, &mVV, lo_q, lo_p, x, k0, &full[slot], 3);
+              }
+            }
+            if (++slot == TNS) { slot = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    cluster_sync_all();
+    return;
+  }
+
+  // ------------------------------------------------------------------ compute warps (8)
+  double acc[2][NFR][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int f = 0; f < NFR; ++f) acc[a][f][0] = acc[a][f][1] = 0.0;
+  int slot = 0;
+  unsigned phase = 0;
+#pragma unroll 1
+  for (int g = 0; g < 3; ++g) {
+    uint32_t need = 0;
+#pragma unroll
+    for (int rf = 0; rf < 2; ++rf)
+#pragma unroll
+      for (int f = 0; f < NFR; ++f) {
+        const int col = warp * CW + f * 8;
+        if (frag_needed(g, 8 * rf, col / BX, col % BX, lo, ex)) need |= 1u << (rf * NFR + f);
+      }
+#pragma unroll 1
+    for (int sg = 0; sg < 6; ++sg) {
+      const int32_t n = segn[g * 6 + sg];
+      const bool neg = sg < 3 ? sg == 1 : sg != 4;
+      const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
+#pragma unroll 1
+      for (int jj = 0; jj < n; ++jj) {
+        tbar_wait(&full[slot], phase);
+        if (need) {
+          const double* P = reinterpret_cast<const double*>(base + slot * TSTAGE);
+          const double* Q = reinterpret_cast<const double*>(base + slot * TSTAGE + TP_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < KC / 4; ++kk) {
+            const int kl = kk * 4 + (lane & 3);
+            const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
+            const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
+#pragma unroll
+            for (int f = 0; f < NFR; ++f) {
+              const int col = warp * CW + f * 8 + (lane >> 2);
+              const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
+              if (need & (1u << f)) dmma(acc[0][f], a0, b);
+              if (need & (1u << (NFR + f))) dmma(acc[1][f], a1, b);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          tbar_arrive(&empty[slot]);
+          tbar_arrive_peer(&empty[slot], peer);
+        }
+        if (++slot == TNS) { slot = 0; phase ^= 1; }
+      }
+    }
+#pragma unroll
+    for (int rf = 0; rf < 2; ++rf)
+#pragma unroll
+      for (int f = 0; f < NFR; ++f)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = rf * 8 + (lane >> 2);
+          const int col = warp * CW + f * 8 + 2 * (lane & 3) + h;
+          const int pp = col / BX, q = col % BX;
+          const double v = acc[rf][f][h];
+          if (g == 0) cube[cidx(row, pp, q)] = v;
+          else if (g == 1) cube[cidx(pp, row, q)] -= v;
+          else cube[cidx(pp, q, row)] += v;
+          acc[rf][f][h] = 0.0;
+        }
+    compute_sync();
+  }
+  double s = 0.0;
+  const double dijk = p.eps_o[I] + p.eps_o[J] + p.eps_o[K];
+  for (int idx = tid; idx < BX * BX * BX; idx += THREADS) {
+    const int la = idx / (BX * BX), lb = (idx / BX) % BX, lc = idx % BX;
+    if (la >= ex[0] || lb >= ex[1] || lc >= ex[2]) continue;
+    const int32_t a = lo[0] + la, b = lo[1] + lb, c = lo[2] + lc;
+    if (!(a < b && b < c)) continue;
+    const double W = cube[cidx(la, lb, lc)];
+    double v1 = 0.0;
+    const int32_t ox[3] = {I, I, J}, oy[3] = {J, K, K}, oz[3] = {K, J, I};
+    const int32_t vp[3] = {a, a, b}, vq[3] = {b, c, c}, vr[3] = {c, b, a};
+#pragma unroll
+    for (int q3 = 0; q3 < 3; ++q3) {
+      double inner = 0.0;
+#pragma unroll
+      for (int pq = 0; pq < 3; ++pq) {
+        const double term = p.VD[(((int64_t)ox[q3] * nO + oy[q3]) * nV + vp[pq]) * nV + vq[pq]] *
+                            p.T1[(int64_t)vr[pq] * nO + oz[q3]];
+        inner = (pq == 1) ? inner - term : inner + term;
+      }
+      v1 = (q3 == 1) ? v1 - inner : v1 + inner;
+    }
+    const double D = dijk - p.eps_v[a] - p.eps_v[b] - p.eps_v[c];
+    s += (W + v1) * W / D;
+  }
+  red[tid] = s;
+  compute_sync();
+  for (int o = THREADS / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    compute_sync();
+  }
+  if (tid == 0 && (two || crank == 0)) p.partials[u] = red[0];
+  cluster_sync_all();   // no CTA leaves while its peer may still arrive on its barriers
+}
+
+cudaError_t launch_triples_cluster(const TriplesParams& p, const void* maps, int64_t npairs, cudaStream_t s) {
+  if (npairs <= 0) return cudaSuccess;
+  static bool attr = false;
+  const size_t smem = triples_tma_smem();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(triples_cluster_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const CUtensorMap* m = static_cast<const CUtensorMap*>(maps);
+  triples_cluster_tma_kernel<<<(unsigned)(2 * npairs), TTHREADS, smem, s>>>(p, m[0], m[1], m[2], m[3]);
+  return cudaGetLastError();
+}
+
 size_t triples_pair_smem() {
   return 128 + (size_t)PNS * PSTAGE + sizeof(double) * (2 * BX * BX * BX + PTHREADS) + 8 * PNS;
 }

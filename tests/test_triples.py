@@ -309,19 +309,21 @@ def test_triples_units_partition_over_ranks():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tma,pair", [("0", "0"), ("1", "0"), ("1", "1")])
-def test_triples_all_kernel_variants(tma, pair):
-    """cp.async staging (TT_TMA=0), TMA boxes one unit per CTA (the default) and the opt-in pair kernel
-    (TT_TRIPLES_PAIR=1) give the oracle's energy -- bitwise the same energy, since every unit's partial is formed in
+@pytest.mark.parametrize("tma,pair,cluster,code", [("0", "0", "0", 0), ("1", "0", "0", 1), ("1", "1", "0", 2),
+                                                  ("1", "0", "1", 3)])
+def test_triples_all_kernel_variants(tma, pair, cluster, code):
+    """cp.async staging (TT_TMA=0), TMA boxes one unit per CTA, the opt-in 16-warp pair kernel
+    (TT_TRIPLES_PAIR=1) and the opt-in 2-CTA cluster kernel with TMA multicast of the shared operand
+    (TT_TRIPLES_CLUSTER=1) give the oracle's energy -- bitwise the same energy, since every unit's partial is formed in
     the same order; O, V not multiples of the 8-row stage (segment tails are zero fill)."""
     import os
-    os.environ["TT_TMA"], os.environ["TT_TRIPLES_PAIR"] = tma, pair
+    os.environ["TT_TMA"], os.environ["TT_TRIPLES_PAIR"], os.environ["TT_TRIPLES_CLUSTER"] = tma, pair, cluster
     try:
         E, info, orc, ctx = _gpu_case(13, 38, 4, 7, False, 11, 1.0)
-        assert ctx.stats()["producer"] == int(tma) + int(pair)
+        assert ctx.stats()["producer"] == code
     finally:
-        os.environ.pop("TT_TMA", None)
-        os.environ.pop("TT_TRIPLES_PAIR", None)
+        for k in ("TT_TMA", "TT_TRIPLES_PAIR", "TT_TRIPLES_CLUSTER"):
+            os.environ.pop(k, None)
     Eo, _ = TR.energy_by_triple(*orc)
     assert abs(E - Eo) <= 1e-11 * abs(Eo), (E, Eo)
     _ENERGIES.setdefault("v", set()).add(E)
