@@ -35,8 +35,10 @@ SPACES = {
                    "V": SpaceSpec(48, sizes=[20, 3, 1, 20, 3, 1], spin_split=True)},
     # ragged spin tiles wider than 32 (several transpose tiles per block and ragged tile edges)
     "spin_wide": {"O": SpaceSpec(18, tile=5, spin_split=True), "V": SpaceSpec(90, tile=37, spin_split=True)},
+    # rows of 8..12 along j (rows / row-tile modes: aibj, biaj keep j innermost in both operands)
+    "rows": {"O": SpaceSpec(40, tile=12, spin_split=True), "V": SpaceSpec(24, tile=7, spin_split=True)},
 }
-MAPS4 = ["bija", "jabi", "ijab", "baji", "abji", "ajbi", "jiba"]
+MAPS4 = ["bija", "jabi", "ijab", "baji", "abji", "ajbi", "jiba", "aibj", "biaj", "baij"]
 
 
 def _run_add_scalar(tt, torch, spaces, c_lbl, a_lbl, spin):
