@@ -360,23 +360,25 @@ constexpr int TTHREADS = THREADS + 32;
 // g holds an element with a < b < c inside the boxes' extents (roles: g = 0 (a; b,c), 1 (b; a,c),
 // 2 (c; a,b)).  Greedy: the smallest a, then the smallest b > a, then the smallest c > b.
 __device__ __forceinline__ bool frag_needed(int g, int r0, int pp, int q0, const int32_t* lo, const int32_t* ex) {
-  int i0[3], i1[3];   // local [lo, hi) per virtual index a, b, c
-  const int rr = g == 0 ? 0 : (g == 1 ? 1 : 2), pr = g == 0 ? 1 : 0, qr = g == 2 ? 1 : 2;
-  i0[rr] = r0; i1[rr] = r0 + 8;
-  i0[pr] = pp; i1[pr] = pp + 1;
-  i0[qr] = q0; i1[qr] = q0 + 8;
-  int gl[3], gh[3];
-  for (int d = 0; d < 3; ++d) {
-    const int h = i1[d] < ex[d] ? i1[d] : ex[d];
-    if (i0[d] >= h) return false;
-    gl[d] = lo[d] + i0[d];
-    gh[d] = lo[d] + h - 1;
-  }
-  const int a = gl[0];
-  const int b = (a + 1 > gl[1]) ? a + 1 : gl[1];
-  if (b > gh[1]) return false;
-  const int c = (b + 1 > gl[2]) ? b + 1 : gl[2];
-  return c <= gh[2];
+  // interval of virtual index d (0 = a, 1 = b, 2 = c): the row role (r0..r0+7) is d == g, the column-pair
+  // role (pp) is b for g = 0 and a otherwise, the inner column role (q0..q0+7) the remaining index;
+  // written without local arrays (no stack traffic)
+  auto iv = [&](int d, int& gl, int& gh) {
+    int s, e;
+    if (d == g) { s = r0; e = r0 + 8; }
+    else if (d == (g == 0 ? 1 : 0)) { s = pp; e = pp + 1; }
+    else { s = q0; e = q0 + 8; }
+    const int h = e < ex[d] ? e : ex[d];
+    gl = lo[d] + s;
+    gh = lo[d] + h - 1;
+    return s < h;
+  };
+  int l0, h0, l1, h1, l2, h2;
+  if (!iv(0, l0, h0) || !iv(1, l1, h1) || !iv(2, l2, h2)) return false;
+  const int b = (l0 + 1 > l1) ? l0 + 1 : l1;   // smallest a, then the smallest b > a, c > b
+  if (b > h1) return false;
+  const int c = (b + 1 > l2) ? b + 1 : l2;
+  return c <= h2;
 }
 
 __device__ __forceinline__ void tbar_arrive(uint64_t* bar) {
@@ -550,7 +552,37 @@ __global__ void __launch_bounds__(TTHREADS, 2)
         }
     compute_sync();
   }
-  // Eq. cc14 over the cube (as the cp.async kernel)
+  // Eq. cc14 over the cube.  The V1 inputs of the unit (Eq. tensort2: v^{xy}_{pq} over the 3 occupied
+  // pairs x 3 virtual box pairs, t^z_r over the 3 boxes x 3 occupied, eps_v of the boxes) are first
+  // staged in the (now free) stage buffers with coalesced loads, so the element loop reads shared
+  // memory only.
+  constexpr int VDP = BX + 1;                                       // padded tile row
+  double* vds = reinterpret_cast<double*>(base);                    // [3 pr][3 pq][BX][VDP]
+  double* t1s = vds + 9 * BX * VDP;                                 // [3 box][BX][3 z]
+  double* epv = t1s + 3 * BX * 3;                                   // [3 box][BX]
+  {
+    // selects instead of indexed local arrays (register resident)
+    auto box_lo = [&](int i) { return i == 0 ? lo[0] : (i == 1 ? lo[1] : lo[2]); };
+    auto box_ex = [&](int i) { return i == 0 ? ex[0] : (i == 1 ? ex[1] : ex[2]); };
+    for (int e = tid; e < 9 * BX * BX; e += THREADS) {
+      const int t = e / (BX * BX), rr = (e / BX) % BX, cc = e % BX;
+      const int pr = t / 3, pq = t % 3;
+      const int pbx = pq == 2 ? 1 : 0, qbx = pq == 0 ? 1 : 2;     // (a,b), (a,c), (b,c)
+      const int32_t ox = pr == 2 ? J : I, oy = pr == 0 ? J : K;    // (i,j), (i,k), (j,k)
+      vds[(t * BX + rr) * VDP + cc] = (rr < box_ex(pbx) && cc < box_ex(qbx))
+          ? p.VD[(((int64_t)ox * nO + oy) * nV + box_lo(pbx) + rr) * nV + box_lo(qbx) + cc] : 0.0;
+    }
+    for (int e = tid; e < 3 * BX * 3; e += THREADS) {
+      const int bxi = e / (BX * 3), rr = (e / 3) % BX, z = e % 3;
+      const int32_t oz = z == 0 ? K : (z == 1 ? J : I);
+      t1s[e] = rr < box_ex(bxi) ? p.T1[(int64_t)(box_lo(bxi) + rr) * nO + oz] : 0.0;
+    }
+    for (int e = tid; e < 3 * BX; e += THREADS) {
+      const int bxi = e / BX, rr = e % BX;
+      epv[e] = rr < box_ex(bxi) ? p.eps_v[box_lo(bxi) + rr] : 0.0;
+    }
+  }
+  compute_sync();
   double s = 0.0;
   const double dijk = p.eps_o[I] + p.eps_o[J] + p.eps_o[K];
   for (int idx = tid; idx < BX * BX * BX; idx += THREADS) {
@@ -559,21 +591,17 @@ __global__ void __launch_bounds__(TTHREADS, 2)
     const int32_t a = lo[0] + la, b = lo[1] + lb, c = lo[2] + lc;
     if (!(a < b && b < c)) continue;
     const double W = cube[cidx(la, lb, lc)];
+    // V1 (Eq. tensort2): pairs (x,y;z) = (i,j;k)+, (i,k;j)-, (j,k;i)+  x  (p,q;r) = (a,b;c)+, (a,c;b)-, (b,c;a)+
     double v1 = 0.0;
-    const int32_t ox[3] = {I, I, J}, oy[3] = {J, K, K}, oz[3] = {K, J, I};
-    const int32_t vp[3] = {a, a, b}, vq[3] = {b, c, c}, vr[3] = {c, b, a};
 #pragma unroll
     for (int pr = 0; pr < 3; ++pr) {
-      double inner = 0.0;
-#pragma unroll
-      for (int pq = 0; pq < 3; ++pq) {
-        const double term = p.VD[(((int64_t)ox[pr] * nO + oy[pr]) * nV + vp[pq]) * nV + vq[pq]] *
-                            p.T1[(int64_t)vr[pq] * nO + oz[pr]];
-        inner = (pq == 1) ? inner - term : inner + term;
-      }
+      const double* vt = vds + pr * 3 * BX * VDP;
+      const double inner = vt[(0 * BX + la) * VDP + lb] * t1s[(2 * BX + lc) * 3 + pr]
+                         - vt[(1 * BX + la) * VDP + lc] * t1s[(1 * BX + lb) * 3 + pr]
+                         + vt[(2 * BX + lb) * VDP + lc] * t1s[(0 * BX + la) * 3 + pr];
       v1 = (pr == 1) ? v1 - inner : v1 + inner;
     }
-    const double D = dijk - p.eps_v[a] - p.eps_v[b] - p.eps_v[c];
+    const double D = dijk - epv[la] - epv[BX + lb] - epv[2 * BX + lc];
     s += (W + v1) * W / D;
   }
   red[tid] = s;
