@@ -1549,15 +1549,12 @@ struct ElemPlan {
   ElemDesc* d_descs = nullptr;
   Segment* d_segs = nullptr;
   TileItem* d_tiles = nullptr;
-  std::vector<RowTile> rtiles;
-  RowTile* d_rtiles = nullptr;
   double* d_partials = nullptr;
   GatherPlan gp;
   double bytes = 0;
   int64_t blocks = 0;
   int64_t nseg() const { return (int64_t)segs.size(); }
   int64_t ntiles() const { return (int64_t)tiles.size(); }
-  int64_t nrtiles() const { return (int64_t)rtiles.size(); }
 };
 
 // Fuse adjacent x dims that are adjacent (same order) in y; fill the group extents / y strides of
@@ -1633,56 +1630,8 @@ void add_segments(ElemPlan& ep, int32_t desc, int64_t e_begin, int64_t e_end) {
 // for a transpose descriptor (only when the block is processed whole), else segments over `ranges`.
 // Modes are per descriptor: blocks of one plan may differ (e.g. a remainder tile of extent 1 makes
 // a transposing block generic), and every block's work is kept.
-// row-tile work of a whole block in rows mode (short rows): tiles of kRowTileRows x kRowTileRows rows over
-// (ga = X's innermost row group, gb = a row group whose Y stride is L), one per index of the other groups
-bool add_rowtiles(ElemPlan& ep, const ElemDesc& d) {
-  const int n = d.n;
-  if (n < 3) return false;
-  const int64_t L = d.div[n - 1].d;
-  if (L > 64) return false;
-  const int ga = n - 2;
-  int gb = -1;
-  for (int g = 0; g < n - 2; ++g)
-    if (d.y_str[g] == L) gb = g;
-  if (gb < 0 || d.y_str[ga] == L) return false;
-  int64_t xs[TT_MAX_ORDER], acc = 1;
-  for (int g = n - 1; g >= 0; --g) { xs[g] = acc; acc *= d.div[g].d; }
-  int64_t batch = 1;
-  for (int g = 0; g < n - 1; ++g)
-    if (g != ga && g != gb) batch *= d.div[g].d;
-  const int ea = (int)d.div[ga].d, eb = (int)d.div[gb].d;
-  for (int64_t bt = 0; bt < batch; ++bt) {
-    int64_t r = bt, xb = 0, yb = 0;
-    for (int g = n - 2; g >= 0; --g) {
-      if (g == ga || g == gb) continue;
-      const int64_t c = r % d.div[g].d;
-      r /= d.div[g].d;
-      xb += c * xs[g];
-      yb += c * d.y_str[g];
-    }
-    for (int ta = 0; ta < ea; ta += kRowTileRows)
-      for (int tb = 0; tb < eb; tb += kRowTileRows) {
-        RowTile t{};
-        t.x_base = d.x_off + xb + (int64_t)tb * xs[gb] + (int64_t)ta * L;
-        t.y_base = d.y_off < 0 ? -1 : d.y_off + yb + (int64_t)ta * d.y_str[ga] + (int64_t)tb * L;
-        t.na = std::min(kRowTileRows, ea - ta);
-        t.nb = std::min(kRowTileRows, eb - tb);
-        t.L = (int32_t)L;
-        t.x_ld = (int32_t)xs[gb];
-        t.y_ld = d.y_str[ga];
-        ep.rtiles.push_back(t);
-      }
-  }
-  return true;
-}
-
 void emit_elem(ElemPlan& ep, ElemDesc& d, bool whole, const std::vector<std::pair<int64_t, int64_t>>& ranges) {
   if (d.mode == kElemTranspose && !whole) d.mode = kElemGeneric;   // tiles need whole blocks
-  if (d.mode == kElemRows && whole && add_rowtiles(ep, d)) {       // short rows far apart in Y
-    d.mode = kElemRowTile;
-    ep.descs.push_back(d);
-    return;
-  }
   ep.descs.push_back(d);
   const int32_t di = (int32_t)ep.descs.size() - 1;
   if (d.mode == kElemTranspose) {
@@ -1717,12 +1666,8 @@ tt_status upload_elem_once(tt_ctx ctx, ElemPlan& ep, bool partials) {
     TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_tiles, ep.tiles.size()));
     TT_CUDA(cudaMemcpy(ep.d_tiles, ep.tiles.data(), ep.tiles.size() * sizeof(TileItem), cudaMemcpyHostToDevice));
   }
-  if (!ep.rtiles.empty()) {
-    TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_rtiles, ep.rtiles.size()));
-    TT_CUDA(cudaMemcpy(ep.d_rtiles, ep.rtiles.data(), ep.rtiles.size() * sizeof(RowTile), cudaMemcpyHostToDevice));
-  }
   if (partials) {
-    const int64_t n = ep.nseg() + ep.ntiles() + ep.nrtiles();
+    const int64_t n = ep.nseg() + ep.ntiles();
     TT_TRY(dev_alloc(ctx, ep.mem, &ep.d_partials, (size_t)(n + scalar_scratch_elems(n))));
   }
   return TT_OK;
@@ -1921,13 +1866,12 @@ tt_status tt_add(tt_ctx ctx, tt_tensor C, const char* cl, double beta, double al
   p.descs = ep->d_descs;
   p.segs = ep->d_segs;
   p.tiles = ep->d_tiles;
-  p.rtiles = ep->d_rtiles;
   p.order = C->order;
   p.alpha = alpha;
   p.beta = beta;
   {
     Launch L(ctx, "tt_add");
-    TT_CUDA(launch_add(p, ep->nseg(), ep->ntiles(), ctx->stream, ep->nrtiles()));
+    TT_CUDA(launch_add(p, ep->nseg(), ep->ntiles(), ctx->stream));
   }
   ctx->last.c_blocks = ep->blocks;
   ctx->last.bytes = ep->bytes;
@@ -2011,13 +1955,12 @@ tt_status tt_contract_scalar(tt_ctx ctx, double alpha, tt_tensor A, const char* 
   p.segs = ep->d_segs;
   p.order = A->order;
   p.tiles = ep->d_tiles;
-  p.rtiles = ep->d_rtiles;
   p.partials = ep->d_partials;
   double* dst = ctx->scalar_dev_out ? ctx->scalar_dev_out : ctx->d_scalar;
-  const int64_t npart = ep->nseg() + ep->ntiles() + ep->nrtiles();
+  const int64_t npart = ep->nseg() + ep->ntiles();
   {
     Launch L(ctx, "tt_scalar_partials");
-    TT_CUDA(launch_scalar_partials(p, ep->nseg(), ep->ntiles(), ctx->stream, ep->nrtiles()));
+    TT_CUDA(launch_scalar_partials(p, ep->nseg(), ep->ntiles(), ctx->stream));
   }
   {
     Launch L(ctx, "tt_scalar_final");
@@ -3257,12 +3200,11 @@ tt_status run_local_add(tt_ctx ctx, const ElemPlan& ep, tt_tensor Xt, tt_tensor 
   p.descs = ep.d_descs;
   p.segs = ep.d_segs;
   p.tiles = ep.d_tiles;
-  p.rtiles = ep.d_rtiles;
   p.order = Xt->order;
   p.alpha = alpha;
   p.beta = beta;
   Launch L(ctx, "tt_add[cholesky Bh]");
-  TT_CUDA(launch_add(p, ep.nseg(), ep.ntiles(), ctx->stream, ep.nrtiles()));
+  TT_CUDA(launch_add(p, ep.nseg(), ep.ntiles(), ctx->stream));
   return TT_OK;
 }
 

@@ -653,49 +653,6 @@ __global__ void __launch_bounds__(256) scalar_tile_kernel(const ElemParams p, do
   if (lx == 0 && ly == 0) partials[blockIdx.x] = s;
 }
 
-// Row tiles (kElemRowTile): Y's nb rows of each ia are one contiguous run (coalesced reads into shared
-// memory), X's na rows of each ib another (coalesced writes); no index decode beyond one division by L.
-constexpr int kRowTileMax = kRowTileRows * kRowTileRows * 64;   // L <= 64 (host rule)
-__global__ void __launch_bounds__(256) add_rowtile_kernel(const ElemParams p) {
-  __shared__ double s[kRowTileMax];
-  const RowTile t = p.rtiles[blockIdx.x];
-  const int nbl = t.nb * t.L, nal = t.na * t.L;
-  const double alpha = p.alpha, beta = p.beta;
-  for (int ia = 0; ia < t.na; ++ia)
-    for (int q = threadIdx.x; q < nbl; q += 256)
-      s[ia * nbl + q] = t.y_base >= 0 ? p.Y[t.y_base + (int64_t)ia * t.y_ld + q] : 0.0;
-  __syncthreads();
-  for (int ib = 0; ib < t.nb; ++ib) {
-    double* __restrict__ x = p.X + t.x_base + (int64_t)ib * t.x_ld;
-    for (int r = threadIdx.x; r < nal; r += 256) {
-      const int ia = r / t.L, l = r - ia * t.L;
-      x[r] = axpby(alpha, s[ia * nbl + ib * t.L + l], beta, beta != 0.0 ? x[r] : 0.0);
-    }
-  }
-}
-
-// Scalar partial of one row tile (fixed order: per thread, shuffle tree, warps in order).
-__global__ void __launch_bounds__(256) scalar_rowtile_kernel(const ElemParams p, double* __restrict__ partials) {
-  __shared__ double s[kRowTileMax];
-  __shared__ double wsum[8];
-  const RowTile t = p.rtiles[blockIdx.x];
-  const int nbl = t.nb * t.L, nal = t.na * t.L;
-  for (int ia = 0; ia < t.na; ++ia)
-    for (int q = threadIdx.x; q < nbl; q += 256)
-      s[ia * nbl + q] = t.y_base >= 0 ? p.Y[t.y_base + (int64_t)ia * t.y_ld + q] : 0.0;
-  __syncthreads();
-  double acc = 0.0;
-  for (int ib = 0; ib < t.nb; ++ib) {
-    const double* __restrict__ x = p.X + t.x_base + (int64_t)ib * t.x_ld;
-    for (int r = threadIdx.x; r < nal; r += 256) {
-      const int ia = r / t.L, l = r - ia * t.L;
-      acc += x[r] * s[ia * nbl + ib * t.L + l];
-    }
-  }
-  acc = cta_sum(acc, wsum);
-  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
-}
-
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -821,10 +778,9 @@ cudaError_t launch_set(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   set_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
-cudaError_t launch_add(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s, int64_t nrtiles) {
+cudaError_t launch_add(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s) {
   if (nseg > 0) add_seg_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   if (ntiles > 0) add_tile_kernel<<<(unsigned)ntiles, dim3(32, 8), 0, s>>>(p);
-  if (nrtiles > 0) add_rowtile_kernel<<<(unsigned)nrtiles, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
@@ -832,11 +788,9 @@ cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s) {
   fill_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
-cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s,
-                                   int64_t nrtiles) {
+cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s) {
   if (nseg > 0) scalar_seg_kernel<<<(unsigned)nseg, kElemThreads, 0, s>>>(p);
   if (ntiles > 0) scalar_tile_kernel<<<(unsigned)ntiles, dim3(32, 8), 0, s>>>(p, p.partials + nseg);
-  if (nrtiles > 0) scalar_rowtile_kernel<<<(unsigned)nrtiles, 256, 0, s>>>(p, p.partials + nseg + ntiles);
   return cudaGetLastError();
 }
 int64_t scalar_scratch_elems(int64_t n) { return n > kFinalChunk ? (n + kFinalChunk - 1) / kFinalChunk : 0; }

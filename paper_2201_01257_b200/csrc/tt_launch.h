@@ -128,7 +128,7 @@ struct ElemDesc {
 // Element-op modes: contiguous (one group, y stride 1: vectorised), generic (multiply-high decode per
 // element), transpose (innermost x group strided in y: 32x32 shared-memory tiles, coalesced both
 // ways), rows (innermost x group contiguous in y too: one warp per row, decode once per row).
-enum { kElemContig = 0, kElemGeneric = 1, kElemTranspose = 2, kElemRows = 3, kElemRowTile = 4 };
+enum { kElemContig = 0, kElemGeneric = 1, kElemTranspose = 2, kElemRows = 3 };
 
 // Transpose-mode work: one 32x32 tile of one block, bases precomputed on the host.  Element (ix, iy)
 // of the tile (ix along X's contiguous group gx, iy along Y's contiguous group gy) is
@@ -140,26 +140,12 @@ struct TileItem {
   int32_t x_ld, y_ld;    // X stride of gy; Y stride of gx
 };
 
-// Row-tile work (kElemRowTile): short rows of L elements contiguous in both operands, where X's
-// innermost row group ga and a row group gb that is row-contiguous in Y differ (e.g. abij <- aibj: rows
-// of j, ga = i, gb = b).  One na x nb tile of rows per CTA: Y rows (ia, ib..ib+nb) are one contiguous
-// run of nb*L, X rows (ib, ia..ia+na) another; element (ia, ib, l) is
-// X[x_base + ib*x_ld + ia*L + l] and Y[y_base + ia*y_ld + ib*L + l].
-struct RowTile {
-  int64_t x_base, y_base;   // y_base -1: zero block (reads as 0)
-  int32_t na, nb, L;
-  int32_t x_ld, y_ld;       // X stride of gb; Y stride of ga
-  int32_t pad;
-};
-constexpr int kRowTileRows = 8;    // rows of each group per tile
-
 struct ElemParams {
   double* X;
   const double* Y;
   const ElemDesc* descs;
   const Segment* segs;
   const TileItem* tiles;
-  const RowTile* rtiles;
   int32_t order;
   double alpha, beta;
   uint64_t key;           // fill: seed ^ tag*golden
@@ -170,11 +156,10 @@ struct ElemParams {
 cudaError_t launch_set(const ElemParams& p, int64_t nseg, cudaStream_t s);
 // Descriptors carry their own mode: segment work (contiguous / generic descriptors) and tile work
 // (transpose descriptors) of one plan run as two launches on the same stream.
-cudaError_t launch_add(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s, int64_t nrtiles = 0);
+cudaError_t launch_add(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s);
 cudaError_t launch_fill(const ElemParams& p, int64_t nseg, cudaStream_t s);
 // writes nseg + ntiles partials: p.partials[0, nseg) per segment, then one per tile
-cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s,
-                                   int64_t nrtiles = 0);
+cudaError_t launch_scalar_partials(const ElemParams& p, int64_t nseg, int64_t ntiles, cudaStream_t s);
 // out = alpha * sum(partials[0, n)) in a fixed order; with scratch (scalar_scratch_elems(n) doubles)
 // large n is summed in two stages
 int64_t scalar_scratch_elems(int64_t n);
