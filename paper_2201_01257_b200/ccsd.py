@@ -274,6 +274,41 @@ class CCSDIteration:
                 sched.scalar(alpha, T[a], al, T[b], bl)
         return sched
 
+    def run_timed(self, stream):
+        """One residual evaluation as immediate calls in queue order (no concurrency), each bracketed by
+        CUDA events on ``stream``: the per-term device time breakdown (the scheduled run overlaps terms of
+        a level on several streams, so per-kernel sums there exceed the wall time).  Returns
+        [(index, kind, description, ms)] and the energy."""
+        import torch
+        tt, T, ctx = self.tt, self.T, self.ctx
+        evs, out, energy = [], [], 0.0
+        for n, term in enumerate(TERMS):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            kind = term[0]
+            if kind == "add":
+                _, o, ol, beta, alpha, a, al = term
+                tt.add(ctx, T[o], ol, beta, alpha, T[a], al)
+                desc = f"{o}({ol}) += {a}({al})"
+            elif kind == "contract":
+                _, o, ol, beta, alpha, a, al, b, bl = term
+                tt.contract(ctx, T[o], ol, beta, alpha, T[a], al, T[b], bl)
+                desc = f"{o}({ol}) += {a}({al}) {b}({bl})"
+            elif kind == "cholesky":
+                _, o, ol, beta, alpha, x, vl, b, bl = term
+                tt.contract_cholesky(ctx, T[o], ol, beta, alpha, T[x], vl, T[b], bl, self.ws)
+                desc = f"{o}({ol}) += V[{x}]({vl}) {b}({bl})"
+            else:
+                _, o, ol, beta, alpha, a, al, b, bl = term
+                energy += tt.contract_scalar(ctx, alpha, T[a], al, T[b], bl)
+                desc = f"E += {a}({al}) {b}({bl})"
+            e1.record(stream)
+            evs.append((n, kind, desc, e0, e1))
+        torch.cuda.synchronize()
+        for n, kind, desc, e0, e1 in evs:
+            out.append((n, kind, desc, e0.elapsed_time(e1)))
+        return out, energy
+
     def run(self):
         """One residual evaluation; returns (levels, energy)."""
         s = self.tt.Scheduler(self.ctx, nstreams=self.nstreams)

@@ -99,6 +99,7 @@ def main():
     ap.add_argument("--ws-gb", type=float, default=4.0)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=2)   # >= 2: tt_contract autotunes on the first two calls
+    ap.add_argument("--terms-out", default=None, help="write the per-term device times of one serial run")
     ap.add_argument("--samples-out", default=None,
                     help="write sampled R1/R2 elements (rechecked on the host by tests/full_samples_check.py)")
     a = ap.parse_args()
@@ -156,6 +157,18 @@ def main():
                           "flops_by_term": parts, "setup_s": setup_s, "kernel_ms_rank0": kernels,
                           "max_rank_contract_kernel_ms": float(kt[0]),
                           "tensor_gb": round(sum(mem.values()), 1), "workspace_gb": a.ws_gb}), flush=True)
+    if a.terms_out:   # per-term breakdown (serial immediate calls), max over ranks per term
+        rows, _ = it.run_timed(stream)
+        tms = torch.tensor([r[3] for r in rows], dtype=torch.float64, device="cuda")
+        tmax = tms.clone()
+        if world > 1:
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            rec = {"n_gpus": world, "serial_ms_rank0": float(tms.sum()), "scheduled_ms": ms,
+                   "terms": [{"i": r[0], "kind": r[1], "term": r[2], "ms_rank0": round(r[3], 3),
+                              "ms_max_rank": round(float(tmax[k]), 3)} for k, r in enumerate(rows)]}
+            with open(a.terms_out, "w") as f:
+                json.dump(rec, f, indent=1)
     if a.samples_out:
         r2s, r1s = sample_positions(a.O, a.V)
         vals = [element(it.T["R2"], it.bufs["R2"], rank, p) for p in r2s] + \

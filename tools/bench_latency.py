@@ -15,6 +15,13 @@ import paper_2201_01257_b200 as tt  # noqa: E402
 
 
 def main():
+    if "--variants" in sys.argv:   # per kernel variant (TT_FORCE_VARIANT), each in a fresh process
+        import subprocess
+        for v in range(6):
+            env = dict(os.environ, TT_FORCE_VARIANT=str(v))
+            out = subprocess.run([sys.executable, __file__], env=env, capture_output=True, text=True).stdout
+            print(json.dumps({"variant": v, **json.loads(out.strip().splitlines()[-1])}), flush=True)
+        return
     stream = torch.cuda.current_stream()
     ctx = tt.Context(device=0, stream=stream.cuda_stream)
     so, sv = tt.IndexSpace(4), tt.IndexSpace(8)
@@ -48,8 +55,15 @@ def main():
         s.replay()
     torch.cuda.synchronize()
     gr = (time.perf_counter() - t0) / (reps * k) * 1e6
+    ctx.set_profiling(True)
+    ctx.profile_reset()
+    for _ in range(n):
+        tt.contract(ctx, C, "abij", 1.0, 1e-3, A, "acik", B, "cbkj")
+    kms, kn = ctx.profile("tt_contract_dmma")
+    ctx.set_profiling(False)
     print(json.dumps({"workload": "configs[0] ring O=4 V=8 tile 4 (65536 FLOPs)", "immediate_us_per_contraction": imm,
-                      "graph_us_per_contraction": gr, "contractions_per_graph": k}))
+                      "graph_us_per_contraction": gr, "contractions_per_graph": k,
+                      "kernel_us_events": kms / max(kn, 1) * 1e3, "variant": ctx.stats()["kernel_variant"]}))
 
 
 if __name__ == "__main__":
