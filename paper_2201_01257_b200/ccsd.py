@@ -181,7 +181,8 @@ SPLIT = {"Wr": ("Wr", "mbej", "T2", "fbjn", "Voovv", "efmn"),
          "Z": ("Z", "abij", "T2", "aeim", "Wr", "mbej"),
          "Q": ("Q", "ifL", "T2", "efim", "Xov", "meL"),
          "Qp": ("Qp", "ieL", "T2", "efim", "Xov", "mfL"),
-         "K3": ("K3", "mbij", "Y2", "miL", "Xvo", "bjL")}
+         "K3": ("K3", "mbij", "Y2", "miL", "Xvo", "bjL"),
+         "Io": ("Io", "mnij", "Voovv", "efmn", "tau", "efij")}
 
 
 class CCSDIteration:
@@ -219,8 +220,9 @@ class CCSDIteration:
         intermediates whose cost is O(o^2 v^2) or below are replicated (each rank computes them: no
         gathers of T2 / tau / Voovv in the big terms).  R2 is split by (a,b) rows on the executed
         cost of the implicit ladder (tt_partition_split_cholesky) with compact storage (it is only
-        written); Wr, Z, Q, Q' and K3 are split on the task-list cost of their dominant term and
-        gathered where they are read."""
+        written); Wr, Z, Q, Q', K3 and I_mnij (o^4 v^2 work: 4 % of the iteration at 4 GPUs when
+        replicated) are split on the task-list cost of their dominant term and gathered where they are
+        read."""
         tt, T = self.tt, self.T
         for name, t in T.items():
             if name != "R2" and name not in SPLIT:
