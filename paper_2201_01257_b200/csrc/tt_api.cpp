@@ -3729,6 +3729,8 @@ struct TripPlan {
   int64_t unit0 = 0, nunits = 0, nunits_total = 0;
   int32_t o_half = 0, v_half = 0;
   int64_t ws_need = 0;
+  int64_t blk_pos[4] = {0, 0, 0, 0}, blk_n[4] = {0, 0, 0, 0};   // blocked copies (QT2, QVV, PVO, PT2)
+  int32_t nbox = 0;
   tt_triples_info info{};
   ~TripPlan() {
     for (auto& r : rt) delete r.dst;
@@ -3896,6 +3898,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
         box_spin.push_back(tV->is->rspin[q]);
       }
     const int nb = (int)box_lo.size();
+    tp->nbox = nb;
     std::vector<int4> box3;
     std::vector<int64_t> box3_n;
     for (int a = 0; a < nb; ++a) for (int b = a; b < nb; ++b) for (int c = b; c < nb; ++c) {
@@ -3966,6 +3969,19 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     tp->info.w_blocks = tp->nunits;
     tp->info.batches = 1;
     tp->info.flops_alg = alg;
+    // blocked copies of the default kernel (TriplesParams): after the partials
+    {
+      const int64_t nbx = (int64_t)tp->nbox, o = nO, v = nV;
+      const int64_t ns[4] = {o * nbx * nbx * (o + 8) * kTripBox * kTripBox, o * nbx * nbx * (v + 8) * kTripBox * kTripBox,
+                             o * o * nbx * (o + 8) * kTripBox, o * o * nbx * (v + 8) * kTripBox};
+      int64_t pos = base + (U + 1) / 2 * 2;
+      for (int q = 0; q < 4; ++q) {
+        tp->blk_pos[q] = pos;
+        tp->blk_n[q] = ns[q];
+        pos += (ns[q] + 31) / 32 * 32;
+      }
+      base = pos - (U + 1) / 2 * 2;
+    }
     tp->ws_need = base + (U + 1) / 2 * 2;
     tp->info.ws_elems = tp->ws_need;
     if (ctx->device >= 0) {
@@ -4038,7 +4054,21 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   p.o_half = tp->o_half;
   p.v_half = tp->v_half;
   p.partials = partials;
-  // TMA boxes (default) or cp.async staging (TT_TMA=0)
+  p.nb = tp->nbox;
+  {   // blocked copies of the default kernel
+    double* bq[4];
+    for (int q = 0; q < 4; ++q) bq[q] = ws + tp->blk_pos[q];
+    p.QT2 = bq[0];
+    p.QVV = bq[1];
+    p.PVO = bq[2];
+    p.PT2 = bq[3];
+    for (int q = 0; q < 4; ++q) {
+      Launch L(ctx, "tt_triples_blockify");
+      TT_CUDA(launch_blockify(q, p, bq[q], tp->blk_n[q], ctx->stream));
+    }
+  }
+  // bulk copies of the blocked operands (default), TMA boxes (opt-in pair / cluster kernels) or cp.async
+  // staging (TT_TMA=0)
   const char* ft = getenv("TT_TMA");
   const bool use_tma = !ft || atoi(ft) != 0;
   CUtensorMap maps[4];

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(K::NTHREADS, K::MINB)
   using SM = TmaSmem<K, BKC>;
   constexpr int STAGES = SM::STAGES;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* base = smem_raw + ((1024 - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023)) & 1023);   // stays in the shared window (LDS, not generic LD)
   unsigned char* sA = base;                                   // STAGES * A_BYTES
   unsigned char* sB = base + STAGES * SM::A_BYTES;            // STAGES * B_BYTES
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * SM::B_BYTES);

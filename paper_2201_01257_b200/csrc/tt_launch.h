@@ -209,7 +209,18 @@ struct TriplesParams {
   int64_t unit0;        // first unit of this launch
   const int2* pairs;    // pair variant: (first unit, 1 or 2 units) per CTA
   double* partials;     // one per unit (indexed by unit)
+  // blocked copies of the default kernel: every 8-row stage of an operand tile is ONE contiguous run
+  // (a 1-D bulk copy), boxes of kTripBox indexed by box id, k rows padded by 8 zero rows, and the
+  // column index XOR-swizzled by 4 (k mod 4): a half-warp's 64-bit fragment load (4 k rows x 4
+  // columns) then touches 16 distinct double banks -- conflict-free without padding
+  const double* QT2;    // [z][bp][bq][m (nO+8)][16][16]   t^{m z}_{p q}
+  const double* QVV;    // [x][bp][bq][e (nV+8)][16][16]   v^{e x}_{p q}
+  const double* PVO;    // [x][y][br][m (nO+8)][16]        v^{x y}_{m r}
+  const double* PT2;    // [y][z][br][e (nV+8)][16]        t^{y z}_{e r}
+  int32_t nb;           // virtual boxes
 };
+// dense copy -> blocked copy (mode 0..3 = QT2, QVV, PVO, PT2)
+cudaError_t launch_blockify(int mode, const TriplesParams& p, double* dst, int64_t n, cudaStream_t s);
 size_t triples_fused_smem();
 cudaError_t launch_triples_fused(const TriplesParams& p, int64_t nunits, cudaStream_t s);
 // TMA variant; maps = 4 CUtensorMap: VO (r,m,y,x) box {20,8,1,1}, T2 as P (b,a,j,i) box {20,8,1,1},

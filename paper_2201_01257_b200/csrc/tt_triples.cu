@@ -15,6 +15,8 @@
 // in the same CTA.  W never reaches HBM.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "tt_launch.h"
 
 namespace tt {
@@ -78,6 +80,50 @@ __global__ void retile_kernel(const RetileParams p) {
     const int64_t so = p.sblk_off[bid];
     dst[e] = so >= 0 ? p.src[so + el] : 0.0;
   }
+}
+
+// dense copies (rt) -> blocked, pre-swizzled copies of the default kernel (see TriplesParams)
+__global__ void blockify_kernel(int mode, const TriplesParams p, double* __restrict__ dst, int64_t n) {
+  const int32_t nO = p.nO, nV = p.nV, nb = p.nb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (mode <= 1) {   // [o][bp][bq][k][16][16]
+      const int32_t kp = (mode == 0 ? nO : nV) + 8;
+      int64_t r = e;
+      const int qs = (int)(r % BX); r /= BX;
+      const int pl = (int)(r % BX); r /= BX;
+      const int32_t k = (int32_t)(r % kp); r /= kp;
+      const int32_t bq = (int32_t)(r % nb); r /= nb;
+      const int32_t bp = (int32_t)(r % nb); r /= nb;
+      const int32_t o = (int32_t)r;
+      const int ql = qs ^ ((k & 3) << 2);   // stored at column q ^ 4(k mod 4)
+      const int32_t pv = p.box_lo[bp] + pl, qv = p.box_lo[bq] + ql;
+      if (pl < p.box_ext[bp] && ql < p.box_ext[bq] && k < (mode == 0 ? nO : nV))
+        v = mode == 0 ? p.T2[(((int64_t)k * nO + o) * nV + pv) * nV + qv]      // T2[m][z][p][q]
+                      : p.VV[(((int64_t)k * nO + o) * nV + pv) * nV + qv];     // VV[e][x][p][q]
+    } else {           // [o1][o2][br][k][16]
+      const int32_t kp = (mode == 2 ? nO : nV) + 8;
+      int64_t r = e;
+      const int rs = (int)(r % BX); r /= BX;
+      const int32_t k = (int32_t)(r % kp); r /= kp;
+      const int32_t br = (int32_t)(r % nb); r /= nb;
+      const int32_t o2 = (int32_t)(r % nO); r /= nO;
+      const int32_t o1 = (int32_t)r;
+      const int rl = rs ^ ((k & 3) << 2);
+      const int32_t rv = p.box_lo[br] + rl;
+      if (rl < p.box_ext[br] && k < (mode == 2 ? nO : nV))
+        v = mode == 2 ? p.VO[(((int64_t)o1 * nO + o2) * nO + k) * nV + rv]     // VO[x][y][m][r]
+                      : p.T2[(((int64_t)o1 * nO + o2) * nV + k) * nV + rv];    // T2[y][z][e][r]
+    }
+    dst[e] = v;
+  }
+}
+
+cudaError_t launch_blockify(int mode, const TriplesParams& p, double* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 64);
+  blockify_kernel<<<(unsigned)blocks, 256, 0, s>>>(mode, p, dst, n);
+  return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(THREADS, 2) triples_fused_kernel(const TriplesParams p) {
@@ -322,6 +368,12 @@ constexpr int TP_BYTES = KC * TPW * 8;      // 1280
 constexpr int TQ_BYTES = KC * TQS * 8;      // 20736
 constexpr int TSTAGE = TP_BYTES + TQ_BYTES;
 
+// default kernel: 1-D bulk copies of the blocked copies, Q (8 x 16 x 16) then P (8 x 16) per stage
+constexpr int BQ_BYTES = KC * BX * BX * 8;   // 16384
+constexpr int BP_BYTES = KC * BX * 8;        // 1024
+constexpr int BSTAGE = BQ_BYTES + BP_BYTES;
+constexpr int BNS = 4;                       // stages
+
 __device__ __forceinline__ void tbar_init(uint64_t* bar, unsigned count) {
   unsigned s = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(s), "r"(count));
@@ -340,6 +392,13 @@ __device__ __forceinline__ void tbar_wait(uint64_t* bar, unsigned parity) {
       " @!p bra TWAIT_%=;\n}\n" ::"r"(s),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(d), "l"(gmem), "r"(bytes), "r"(b)
+               : "memory");
 }
 __device__ __forceinline__ void tma4(void* smem, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
   unsigned d = (unsigned)__cvta_generic_to_shared(smem);
@@ -392,12 +451,12 @@ __global__ void __launch_bounds__(TTHREADS, 2)
                              const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
                              const __grid_constant__ CUtensorMap mVV) {
   extern __shared__ __align__(128) unsigned char tsm_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)tsm_raw + 127) & ~(uintptr_t)127);
-  double* cube = reinterpret_cast<double*>(base + TNS * TSTAGE);   // [BX][BX][BX]
+  unsigned char* base = tsm_raw + ((128 - ((unsigned)__cvta_generic_to_shared(tsm_raw) & 127)) & 127);   // stays in the shared window (LDS, not generic LD)
+  double* cube = reinterpret_cast<double*>(base + BNS * BSTAGE);   // [BX][BX][BX]
   double* red = cube + BX * BX * BX;                               // [THREADS]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS]
-  uint64_t* empty = full + TNS;                                    // [TNS]
-  int32_t* segb = reinterpret_cast<int32_t*>(empty + TNS);         // [3][6] first summed index
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [BNS]
+  uint64_t* empty = full + BNS;                                    // [BNS]
+  int32_t* segb = reinterpret_cast<int32_t*>(empty + BNS);         // [3][6] first summed index
   int32_t* segn = segb + 18;                                       // [3][6] stages
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t u = p.unit0 + blockIdx.x;
@@ -409,7 +468,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
   const int32_t ex[3] = {p.box_ext[bx.x], p.box_ext[bx.y], p.box_ext[bx.z]};
   const int32_t I = tr.x, J = tr.y, K = tr.z;
   if (tid == 0) {
-    for (int q = 0; q < TNS; ++q) {
+    for (int q = 0; q < BNS; ++q) {
       tbar_init(&full[q], 1);
       tbar_init(&empty[q], NWARP);
     }
@@ -453,30 +512,32 @@ __global__ void __launch_bounds__(TTHREADS, 2)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
     int slot = 0;
     unsigned phase = 1;   // empty barriers: the first pass over the ring does not wait
+    const int32_t nb = p.nb, kpo = nO + 8, kpv = nV + 8;
     for (int g = 0; g < 3; ++g) {
-      const int32_t lo_r = g == 0 ? lo[0] : (g == 1 ? lo[1] : lo[2]);
-      const int32_t lo_p = g == 0 ? lo[1] : lo[0];
-      const int32_t lo_q = g == 2 ? lo[1] : lo[2];
+      const int32_t br = g == 0 ? bx.x : (g == 1 ? bx.y : bx.z);   // box ids of the roles (r; p, q)
+      const int32_t bp = g == 0 ? bx.y : bx.x;
+      const int32_t bq = g == 2 ? bx.y : bx.z;
       for (int sg = 0; sg < 6; ++sg) {
         const int32_t n = segn[g * 6 + sg];
         for (int jj = 0; jj < n; ++jj) {
           const int32_t k0 = segb[g * 6 + sg] + jj * KC;
           tbar_wait(&empty[slot], phase);
-          unsigned char* st = base + slot * TSTAGE;
-          double* P = reinterpret_cast<double*>(st);
-          double* Q = reinterpret_cast<double*>(st + TP_BYTES);
-          tbar_expect(&full[slot], (unsigned)TSTAGE);
+          unsigned char* st = base + slot * BSTAGE;
+          tbar_expect(&full[slot], (unsigned)BSTAGE);
+          const double *qsrc, *psrc;
           if (sg < 3) {
             const int32_t x = (sg == 2) ? J : I, y = (sg == 0) ? J : K, z = (sg == 0) ? K : (sg == 1 ? J : I);
-            tma4(P, &mVO, lo_r, k0, y, x, &full[slot]);          // VO[x][y][m][r]
-            tma4(Q, &mT2Q, lo_q, lo_p, z, k0, &full[slot]);      // T2[m][z][p][q]
+            qsrc = p.QT2 + ((((int64_t)z * nb + bp) * nb + bq) * kpo + k0) * (BX * BX);   // T2[m][z][p][q]
+            psrc = p.PVO + ((((int64_t)x * nO + y) * nb + br) * kpo + k0) * BX;          // VO[x][y][m][r]
           } else {
             const int s3 = sg - 3;
             const int32_t x = (s3 == 0) ? I : (s3 == 1 ? J : K), y = (s3 == 0) ? J : I, z = (s3 == 2) ? J : K;
-            tma4(P, &mT2P, lo_r, k0, z, y, &full[slot]);         // T2[y][z][e][r]
-            tma4(Q, &mVV, lo_q, lo_p, x, k0, &full[slot]);       // VV[e][x][p][q]
+            qsrc = p.QVV + ((((int64_t)x * nb + bp) * nb + bq) * kpv + k0) * (BX * BX);   // VV[e][x][p][q]
+            psrc = p.PT2 + ((((int64_t)y * nO + z) * nb + br) * kpv + k0) * BX;          // T2[y][z][e][r]
           }
-          if (++slot == TNS) { slot = 0; phase ^= 1; }
+          bulk_copy(st, qsrc, BQ_BYTES, &full[slot]);
+          bulk_copy(st + BQ_BYTES, psrc, BP_BYTES, &full[slot]);
+          if (++slot == BNS) { slot = 0; phase ^= 1; }
         }
       }
     }
@@ -512,17 +573,19 @@ __global__ void __launch_bounds__(TTHREADS, 2)
       for (int jj = 0; jj < n; ++jj) {
         tbar_wait(&full[slot], phase);
         if (need) {
-          const double* P = reinterpret_cast<const double*>(base + slot * TSTAGE);
-          const double* Q = reinterpret_cast<const double*>(base + slot * TSTAGE + TP_BYTES);
+          const double* Q = reinterpret_cast<const double*>(base + slot * BSTAGE);
+          const double* P = reinterpret_cast<const double*>(base + slot * BSTAGE + BQ_BYTES);
+          const int kb = (segb[g * 6 + sg] + jj * KC) & 3;   // stage's first k row mod 4
 #pragma unroll
           for (int kk = 0; kk < KC / 4; ++kk) {
             const int kl = kk * 4 + (lane & 3);
-            const double a0 = __longlong_as_double(__double_as_longlong(P[kl * TPW + (lane >> 2)]) ^ sgm);
-            const double a1 = __longlong_as_double(__double_as_longlong(P[kl * TPW + 8 + (lane >> 2)]) ^ sgm);
+            const int sw = ((kl + kb) & 3) << 2;                // global k row mod 4: columns XOR 4(k mod 4)
+            const double a0 = __longlong_as_double(__double_as_longlong(P[kl * BX + ((lane >> 2) ^ sw)]) ^ sgm);
+            const double a1 = __longlong_as_double(__double_as_longlong(P[kl * BX + ((8 + (lane >> 2)) ^ sw)]) ^ sgm);
 #pragma unroll
             for (int f = 0; f < NFR; ++f) {
               const int col = warp * CW + f * 8 + (lane >> 2);
-              const double b = Q[kl * TQS + (col / BX) * TQW + (col % BX)];
+              const double b = Q[kl * (BX * BX) + (col / BX) * BX + ((col % BX) ^ sw)];
               if (need & (1u << f)) dmma(acc[0][f], a0, b);
               if (need & (1u << (NFR + f))) dmma(acc[1][f], a1, b);
             }
@@ -530,7 +593,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
         }
         __syncwarp();
         if (lane == 0) tbar_arrive(&empty[slot]);
-        if (++slot == TNS) { slot = 0; phase ^= 1; }
+        if (++slot == BNS) { slot = 0; phase ^= 1; }
       }
     }
     // GEMM g done: fold into the cube (each cube entry has one owner thread per GEMM; the barriers
@@ -632,7 +695,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
                             const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
                             const __grid_constant__ CUtensorMap mVV) {
   extern __shared__ __align__(128) unsigned char psm_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)psm_raw + 127) & ~(uintptr_t)127);
+  unsigned char* base = psm_raw + ((128 - ((unsigned)__cvta_generic_to_shared(psm_raw) & 127)) & 127);   // stays in the shared window (LDS, not generic LD)
   double* cubes = reinterpret_cast<double*>(base + PNS * PSTAGE);   // [2][BX^3]
   double* red = cubes + 2 * BX * BX * BX;                          // [PTHREADS]
   uint64_t* full = reinterpret_cast<uint64_t*>(red + PTHREADS);    // [PNS]
@@ -820,7 +883,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
 // releases of BOTH CTAs' compute warps (local arrive + remote arrive on the peer through its cluster
 // address), so neither producer refills a slot the other CTA still reads or the multicast still
 // targets.  A lone unit (odd run of k) gives both CTAs the same unit; CTA 1 then writes no partial.
-size_t triples_tma_smem();
+size_t triples_cluster_smem();
 
 namespace {
 __device__ __forceinline__ unsigned cluster_rank() {
@@ -853,7 +916,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TTHREADS, 2)
                                const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
                                const __grid_constant__ CUtensorMap mVV) {
   extern __shared__ __align__(128) unsigned char csm_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)csm_raw + 127) & ~(uintptr_t)127);
+  unsigned char* base = csm_raw + ((128 - ((unsigned)__cvta_generic_to_shared(csm_raw) & 127)) & 127);   // stays in the shared window (LDS, not generic LD)
   double* cube = reinterpret_cast<double*>(base + TNS * TSTAGE);   // [BX][BX][BX]
   double* red = cube + BX * BX * BX;                               // [THREADS]
   uint64_t* full = reinterpret_cast<uint64_t*>(red + THREADS);     // [TNS]
@@ -1065,7 +1128,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TTHREADS, 2)
 cudaError_t launch_triples_cluster(const TriplesParams& p, const void* maps, int64_t npairs, cudaStream_t s) {
   if (npairs <= 0) return cudaSuccess;
   static bool attr = false;
-  const size_t smem = triples_tma_smem();
+  const size_t smem = triples_cluster_smem();
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(triples_cluster_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1094,8 +1157,11 @@ cudaError_t launch_triples_pair(const TriplesParams& p, const void* maps, int64_
   return cudaGetLastError();
 }
 
-size_t triples_tma_smem() {
+size_t triples_cluster_smem() {   // padded-layout TMA stages (cluster variant)
   return 128 + (size_t)TNS * TSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 16 * TNS + 4 * 36;
+}
+size_t triples_tma_smem() {   // the default kernel (bulk-copy stages)
+  return 128 + (size_t)BNS * BSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 16 * BNS + 4 * 36;
 }
 
 cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s) {

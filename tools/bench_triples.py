@@ -114,7 +114,7 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
     kernels = {}
-    for name in ["tt_triples_fused", "tt_retile", "tt_scalar_final"]:
+    for name in ["tt_triples_fused", "tt_triples_blockify", "tt_retile", "tt_scalar_final"]:
         kms, kn = ctx.profile(name)
         kernels[name] = {"ms": round(kms / a.steps, 3), "launches": kn // a.steps}
     ctx.set_profiling(False)
