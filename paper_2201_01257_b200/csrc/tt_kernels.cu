@@ -489,7 +489,13 @@ __device__ __forceinline__ int64_t y_row_offset(uint32_t r, const ElemDesc& d) {
   return off + (int64_t)r * d.y_str[0];
 }
 
-constexpr int kRowsPerWarp = 4;   // rows mode: rows of one warp in flight
+// rows mode walks 16-B pairs: needs an even row length, even Y strides and even block offsets (else the
+// generic per-element decode runs)
+__device__ __forceinline__ bool rows_pairs(const ElemDesc& d) {
+  bool ok = (d.div[d.n - 1].d % 2 == 0) && (d.x_off % 2 == 0) && (d.y_off < 0 || d.y_off % 2 == 0);
+  for (int g = 0; g < d.n - 1; ++g) ok = ok && (d.y_str[g] % 2 == 0);
+  return ok;
+}
 
 // beta*x + alpha*y with ONE rounding order in every kernel and block mode (explicit intrinsics: the
 // compiler never re-associates or contracts them differently per call site), so that a block gives the
@@ -550,28 +556,36 @@ __global__ void __launch_bounds__(kElemThreads) add_seg_kernel(const ElemParams 
         x[e] = axpby(alpha, y ? y[e] : 0.0, beta, beta != 0.0 ? x[e] : 0.0);
       }
     }
-  } else if (d.mode == kElemRows) {
-    // rows of L elements contiguous in both operands: one warp per row, the row's Y base decoded once
-    const int64_t L = d.div[d.n - 1].d;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t r0 = sg.e0 / L, r1 = (sg.e1 + L - 1) / L;
-    for (int64_t rb = r0 + (int64_t)warp * kRowsPerWarp; rb < r1; rb += (kElemThreads / 32) * kRowsPerWarp) {
-      int64_t yb[kRowsPerWarp];
+  } else if (d.mode == kElemRows && rows_pairs(d)) {
+    // rows of L elements contiguous in both operands, walked flat: consecutive threads take consecutive
+    // 16-B pairs of X (fully coalesced), each decoding its row's Y base (Y read in runs of L)
+    const uint32_t L = d.div[d.n - 1].d;
+    const int64_t es = sg.e0 + (sg.e0 & 1);
+    const int64_t n2 = (sg.e1 - es) / 2;
+    double2* __restrict__ x2 = reinterpret_cast<double2*>(x + es);
+    for (int64_t i0 = threadIdx.x; i0 < n2; i0 += kElemThreads * kElemUnroll) {
+      double2 v[kElemUnroll], o[kElemUnroll];
 #pragma unroll
-      for (int u = 0; u < kRowsPerWarp; ++u) yb[u] = (rb + u < r1) ? y_row_offset((uint32_t)(rb + u), d) : 0;
-      for (int64_t k0 = 0; k0 < L; k0 += 32) {
-        double yv[kRowsPerWarp], xv[kRowsPerWarp];
-        bool ok[kRowsPerWarp];
-#pragma unroll
-        for (int u = 0; u < kRowsPerWarp; ++u) {
-          const int64_t k = k0 + lane, e = (rb + u) * L + k;
-          ok[u] = rb + u < r1 && k < L && e >= sg.e0 && e < sg.e1;
-          yv[u] = (ok[u] && y) ? y[yb[u] + k] : 0.0;
-          xv[u] = (ok[u] && beta != 0.0) ? x[e] : 0.0;
+      for (int u = 0; u < kElemUnroll; ++u) {
+        const int64_t i = i0 + u * kElemThreads;
+        v[u] = o[u] = make_double2(0.0, 0.0);
+        if (i < n2) {
+          const uint32_t e = (uint32_t)(es + 2 * i), r = fdiv(e, d.div[d.n - 1]);
+          if (y) v[u] = *reinterpret_cast<const double2*>(y + y_row_offset(r, d) + (e - r * L));
+          if (beta != 0.0) o[u] = x2[i];
         }
+      }
 #pragma unroll
-        for (int u = 0; u < kRowsPerWarp; ++u)
-          if (ok[u]) x[(rb + u) * L + k0 + lane] = axpby(alpha, yv[u], beta, xv[u]);
+      for (int u = 0; u < kElemUnroll; ++u) {
+        const int64_t i = i0 + u * kElemThreads;
+        if (i < n2) x2[i] = make_double2(axpby(alpha, v[u].x, beta, o[u].x), axpby(alpha, v[u].y, beta, o[u].y));
+      }
+    }
+    if (threadIdx.x == 0) {
+      int64_t peel[2] = {es != sg.e0 ? sg.e0 : -1, es + 2 * n2 < sg.e1 ? sg.e1 - 1 : -1};
+      for (int64_t e : peel) {
+        if (e < 0) continue;
+        x[e] = axpby(alpha, y ? y[y_offset((uint32_t)e, d)] : 0.0, beta, beta != 0.0 ? x[e] : 0.0);
       }
     }
   } else {
@@ -709,27 +723,32 @@ __global__ void __launch_bounds__(kElemThreads) scalar_seg_kernel(const ElemPara
     }
     if (threadIdx.x == 0 && es != sg.e0 && sg.e0 < sg.e1) s += x[sg.e0] * y[sg.e0];
     if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) s += x[sg.e1 - 1] * y[sg.e1 - 1];
-  } else if (d.mode == kElemRows) {
-    const int64_t L = d.div[d.n - 1].d;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t r0 = sg.e0 / L, r1 = (sg.e1 + L - 1) / L;
-    for (int64_t rb = r0 + (int64_t)warp * kRowsPerWarp; rb < r1; rb += (kElemThreads / 32) * kRowsPerWarp) {
-      int64_t yb[kRowsPerWarp];
+  } else if (d.mode == kElemRows && rows_pairs(d)) {
+    // as in add_seg_kernel: flat 16-B pairs of X, the row's Y base decoded per pair
+    const uint32_t L = d.div[d.n - 1].d;
+    const int64_t es = sg.e0 + (sg.e0 & 1);
+    const int64_t n2 = (sg.e1 - es) / 2;
+    const double2* __restrict__ x2 = reinterpret_cast<const double2*>(x + es);
+    for (int64_t i0 = threadIdx.x; i0 < n2; i0 += kElemThreads * kElemUnroll) {
+      double2 a[kElemUnroll], b[kElemUnroll];
 #pragma unroll
-      for (int u = 0; u < kRowsPerWarp; ++u) yb[u] = (rb + u < r1) ? y_row_offset((uint32_t)(rb + u), d) : 0;
-      for (int64_t k0 = 0; k0 < L; k0 += 32) {
-        double yv[kRowsPerWarp], xv[kRowsPerWarp];
-#pragma unroll
-        for (int u = 0; u < kRowsPerWarp; ++u) {
-          const int64_t k = k0 + lane, e = (rb + u) * L + k;
-          const bool ok = rb + u < r1 && k < L && e >= sg.e0 && e < sg.e1;
-          yv[u] = ok ? y[yb[u] + k] : 0.0;
-          xv[u] = ok ? x[e] : 0.0;
+      for (int u = 0; u < kElemUnroll; ++u) {
+        const int64_t i = i0 + u * kElemThreads;
+        a[u] = b[u] = make_double2(0.0, 0.0);
+        if (i < n2) {
+          const uint32_t e = (uint32_t)(es + 2 * i), r = fdiv(e, d.div[d.n - 1]);
+          a[u] = x2[i];
+          b[u] = *reinterpret_cast<const double2*>(y + y_row_offset(r, d) + (e - r * L));
         }
+      }
 #pragma unroll
-        for (int u = 0; u < kRowsPerWarp; ++u) s += xv[u] * yv[u];
+      for (int u = 0; u < kElemUnroll; ++u) {
+        s += a[u].x * b[u].x;
+        s += a[u].y * b[u].y;
       }
     }
+    if (threadIdx.x == 0 && es != sg.e0 && sg.e0 < sg.e1) s += x[sg.e0] * y[y_offset((uint32_t)sg.e0, d)];
+    if (threadIdx.x == 0 && es + 2 * n2 < sg.e1) s += x[sg.e1 - 1] * y[y_offset((uint32_t)(sg.e1 - 1), d)];
   } else {
     for (int64_t e0 = sg.e0 + threadIdx.x; e0 < sg.e1; e0 += kElemThreads * kElemUnroll) {
       double yv[kElemUnroll], xv[kElemUnroll];

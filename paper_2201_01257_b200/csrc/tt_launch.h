@@ -127,7 +127,7 @@ struct ElemDesc {
 
 // Element-op modes: contiguous (one group, y stride 1: vectorised), generic (multiply-high decode per
 // element), transpose (innermost x group strided in y: 32x32 shared-memory tiles, coalesced both
-// ways), rows (innermost x group contiguous in y too: one warp per row, decode once per row).
+// ways), rows (innermost x group contiguous in y too: flat 16-B pairs of x, the y row base decoded per pair).
 enum { kElemContig = 0, kElemGeneric = 1, kElemTranspose = 2, kElemRows = 3 };
 
 // Transpose-mode work: one 32x32 tile of one block, bases precomputed on the host.  Element (ix, iy)
