@@ -554,38 +554,53 @@ __global__ void __launch_bounds__(TTHREADS, 2)
   unsigned phase = 0;
 #pragma unroll 1
   for (int g = 0; g < 3; ++g) {
-    // output fragments of this warp that hold a needed W(a,b,c) (a<b<c inside the extents): the others
-    // (diagonal box triples, narrow tail boxes) are not computed
-    uint32_t need = 0;
-#pragma unroll
-    for (int rf = 0; rf < 2; ++rf)
+    // the 8-column output fragments that hold a needed W(a,b,c) (a<b<c inside the extents) in either
+    // row half, dealt round-robin to the warps: no warp holds more than ceil(n/8) of them, so the
+    // diagonal box triples and narrow tail boxes shorten every warp's stage, not just some warps'
+    uint32_t need = 0, colp = 0xffffffffu;   // slot f: column fragment (colp >> 8f) & 0xff, 0xff = none
+    {
+      const int col = lane * 8;                 // lane c tests column fragment c
+      const uint32_t m0 = __ballot_sync(0xffffffffu, frag_needed(g, 0, col / BX, col % BX, lo, ex));
+      const uint32_t m1 = __ballot_sync(0xffffffffu, frag_needed(g, 8, col / BX, col % BX, lo, ex));
+      const uint32_t any = m0 | m1;
+      const int n = __popc(any);
 #pragma unroll
       for (int f = 0; f < NFR; ++f) {
-        const int col = warp * CW + f * 8;
-        if (frag_needed(g, 8 * rf, col / BX, col % BX, lo, ex)) need |= 1u << (rf * NFR + f);
+        const int k = f * NWARP + warp;         // this slot takes the k-th needed fragment
+        if (k < n) {
+          const uint32_t c = __fns(any, 0, k + 1);
+          colp = (colp & ~(0xffu << (8 * f))) | (c << (8 * f));
+          need |= (((m0 >> c) & 1u) << f) | (((m1 >> c) & 1u) << (NFR + f));
+        }
       }
+    }
 #pragma unroll 1
     for (int sg = 0; sg < 6; ++sg) {
       const int32_t n = segn[g * 6 + sg];
       const bool neg = sg < 3 ? sg == 1 : sg != 4;   // m sums (+,-,+), e sums (-,+,-)
       const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
+      // every stage of a segment starts at a k row = segb mod 4 (stages are 8 rows): one swizzle
+      const int sw = (((lane & 3) + segb[g * 6 + sg]) & 3) << 2;   // columns XOR 4(k mod 4)
+      int qa[NFR];                                                  // Q offsets of this lane's columns
+#pragma unroll
+      for (int f = 0; f < NFR; ++f) {
+        const int col = (int)((colp >> (8 * f)) & 31u) * 8 + (lane >> 2);
+        qa[f] = (lane & 3) * (BX * BX) + (col / BX) * BX + ((col % BX) ^ sw);
+      }
 #pragma unroll 1
       for (int jj = 0; jj < n; ++jj) {
         tbar_wait(&full[slot], phase);
         if (need) {
           const double* Q = reinterpret_cast<const double*>(base + slot * BSTAGE);
           const double* P = reinterpret_cast<const double*>(base + slot * BSTAGE + BQ_BYTES);
-          const int kb = (segb[g * 6 + sg] + jj * KC) & 3;   // stage's first k row mod 4
 #pragma unroll
           for (int kk = 0; kk < KC / 4; ++kk) {
             const int kl = kk * 4 + (lane & 3);
-            const int sw = ((kl + kb) & 3) << 2;                // global k row mod 4: columns XOR 4(k mod 4)
             const double a0 = __longlong_as_double(__double_as_longlong(P[kl * BX + ((lane >> 2) ^ sw)]) ^ sgm);
             const double a1 = __longlong_as_double(__double_as_longlong(P[kl * BX + ((8 + (lane >> 2)) ^ sw)]) ^ sgm);
 #pragma unroll
             for (int f = 0; f < NFR; ++f) {
-              const int col = warp * CW + f * 8 + (lane >> 2);
-              const double b = Q[kl * (BX * BX) + (col / BX) * BX + ((col % BX) ^ sw)];
+              const double b = Q[kk * 4 * (BX * BX) + qa[f]];
               if (need & (1u << f)) dmma(acc[0][f], a0, b);
               if (need & (1u << (NFR + f))) dmma(acc[1][f], a1, b);
             }
@@ -598,14 +613,16 @@ __global__ void __launch_bounds__(TTHREADS, 2)
     }
     // GEMM g done: fold into the cube (each cube entry has one owner thread per GEMM; the barriers
     // order the three folds)
+    // (cube entries outside every needed fragment are never written and never read)
 #pragma unroll
-    for (int rf = 0; rf < 2; ++rf)
+    for (int f = 0; f < NFR; ++f) {
+      if (((colp >> (8 * f)) & 0xffu) == 0xffu) continue;
 #pragma unroll
-      for (int f = 0; f < NFR; ++f)
+      for (int rf = 0; rf < 2; ++rf)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int row = rf * 8 + (lane >> 2);
-          const int col = warp * CW + f * 8 + 2 * (lane & 3) + h;
+          const int col = (int)((colp >> (8 * f)) & 31u) * 8 + 2 * (lane & 3) + h;
           const int pp = col / BX, q = col % BX;
           const double v = acc[rf][f][h];
           if (g == 0) cube[cidx(row, pp, q)] = v;
@@ -613,6 +630,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
           else cube[cidx(pp, q, row)] += v;
           acc[rf][f][h] = 0.0;
         }
+    }
     compute_sync();
   }
   // Eq. cc14 over the cube.  The V1 inputs of the unit (Eq. tensort2: v^{xy}_{pq} over the 3 occupied
