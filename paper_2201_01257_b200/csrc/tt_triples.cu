@@ -446,6 +446,41 @@ __device__ __forceinline__ void tbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(THREADS) : "memory"); }
 
+// One segment of a GEMM in the default kernel: n stages of 8 k rows.  The warp's column slots are NB
+// fragments needing both row halves, then N0 needing the first, then N1 needing the second (all
+// compile-time), so fewer needed fragments issue fewer DMMAs instead of predicated-off ones.
+template <int NB, int N0, int N1>
+__device__ __forceinline__ void seg_mma(double (&acc)[2][NFR][2], int n, int& slot, unsigned& phase,
+                                        unsigned char* base, uint64_t* full, uint64_t* empty,
+                                        const int (&qa)[NFR], int sw, long long sgm, int lane) {
+  constexpr int NS = NB + N0 + N1;
+#pragma unroll 1
+  for (int jj = 0; jj < n; ++jj) {
+    tbar_wait(&full[slot], phase);
+    if (NS > 0) {
+      const double* Q = reinterpret_cast<const double*>(base + slot * BSTAGE);
+      const double* P = reinterpret_cast<const double*>(base + slot * BSTAGE + BQ_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < KC / 4; ++kk) {
+        const int kl = kk * 4 + (lane & 3);
+        const double a0 = NB + N0 == 0 ? 0.0
+            : __longlong_as_double(__double_as_longlong(P[kl * BX + ((lane >> 2) ^ sw)]) ^ sgm);
+        const double a1 = NB + N1 == 0 ? 0.0
+            : __longlong_as_double(__double_as_longlong(P[kl * BX + ((8 + (lane >> 2)) ^ sw)]) ^ sgm);
+#pragma unroll
+        for (int f = 0; f < NS; ++f) {
+          const double b = Q[kk * 4 * (BX * BX) + qa[f]];
+          if (f < NB + N0) dmma(acc[0][f], a0, b);
+          if (f < NB || f >= NB + N0) dmma(acc[1][f], a1, b);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tbar_arrive(&empty[slot]);
+    if (++slot == BNS) { slot = 0; phase ^= 1; }
+  }
+}
+
 __global__ void __launch_bounds__(TTHREADS, 2)
     triples_fused_tma_kernel(const TriplesParams p, const __grid_constant__ CUtensorMap mVO,
                              const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
@@ -554,23 +589,26 @@ __global__ void __launch_bounds__(TTHREADS, 2)
   unsigned phase = 0;
 #pragma unroll 1
   for (int g = 0; g < 3; ++g) {
-    // the 8-column output fragments that hold a needed W(a,b,c) (a<b<c inside the extents) in either
-    // row half, dealt round-robin to the warps: no warp holds more than ceil(n/8) of them, so the
-    // diagonal box triples and narrow tail boxes shorten every warp's stage, not just some warps'
-    uint32_t need = 0, colp = 0xffffffffu;   // slot f: column fragment (colp >> 8f) & 0xff, 0xff = none
+    // the 8-column output fragments that hold a needed W(a,b,c) (a<b<c inside the extents), in three
+    // classes -- both row halves, the first only, the second only -- listed in that order and dealt
+    // round-robin to the warps: no warp holds more than ceil(n/8) of them, each warp's slots run
+    // both -> first -> second, and the slot counts per class (nb_, n0_, n1_) select a compile-time loop
+    // (diagonal box triples and narrow tail boxes issue fewer DMMAs, not predicated-off ones)
+    uint32_t colp = 0xffffffffu;   // slot f: column fragment (colp >> 8f) & 0xff, 0xff = none
+    int nb_ = 0, n0_ = 0, n1_ = 0;
     {
       const int col = lane * 8;                 // lane c tests column fragment c
       const uint32_t m0 = __ballot_sync(0xffffffffu, frag_needed(g, 0, col / BX, col % BX, lo, ex));
       const uint32_t m1 = __ballot_sync(0xffffffffu, frag_needed(g, 8, col / BX, col % BX, lo, ex));
-      const uint32_t any = m0 | m1;
-      const int n = __popc(any);
+      const uint32_t cb = m0 & m1, c0 = m0 & ~m1, c1 = m1 & ~m0;
+      const int kb = __popc(cb), k0 = kb + __popc(c0), kn = k0 + __popc(c1);
 #pragma unroll
       for (int f = 0; f < NFR; ++f) {
         const int k = f * NWARP + warp;         // this slot takes the k-th needed fragment
-        if (k < n) {
-          const uint32_t c = __fns(any, 0, k + 1);
+        if (k < kn) {
+          const uint32_t c = k < kb ? __fns(cb, 0, k + 1) : (k < k0 ? __fns(c0, 0, k - kb + 1) : __fns(c1, 0, k - k0 + 1));
           colp = (colp & ~(0xffu << (8 * f))) | (c << (8 * f));
-          need |= (((m0 >> c) & 1u) << f) | (((m1 >> c) & 1u) << (NFR + f));
+          if (k < kb) ++nb_; else if (k < k0) ++n0_; else ++n1_;
         }
       }
     }
@@ -587,28 +625,18 @@ __global__ void __launch_bounds__(TTHREADS, 2)
         const int col = (int)((colp >> (8 * f)) & 31u) * 8 + (lane >> 2);
         qa[f] = (lane & 3) * (BX * BX) + (col / BX) * BX + ((col % BX) ^ sw);
       }
-#pragma unroll 1
-      for (int jj = 0; jj < n; ++jj) {
-        tbar_wait(&full[slot], phase);
-        if (need) {
-          const double* Q = reinterpret_cast<const double*>(base + slot * BSTAGE);
-          const double* P = reinterpret_cast<const double*>(base + slot * BSTAGE + BQ_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < KC / 4; ++kk) {
-            const int kl = kk * 4 + (lane & 3);
-            const double a0 = __longlong_as_double(__double_as_longlong(P[kl * BX + ((lane >> 2) ^ sw)]) ^ sgm);
-            const double a1 = __longlong_as_double(__double_as_longlong(P[kl * BX + ((8 + (lane >> 2)) ^ sw)]) ^ sgm);
-#pragma unroll
-            for (int f = 0; f < NFR; ++f) {
-              const double b = Q[kk * 4 * (BX * BX) + qa[f]];
-              if (need & (1u << f)) dmma(acc[0][f], a0, b);
-              if (need & (1u << (NFR + f))) dmma(acc[1][f], a1, b);
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) tbar_arrive(&empty[slot]);
-        if (++slot == BNS) { slot = 0; phase ^= 1; }
+      switch (nb_ * 25 + n0_ * 5 + n1_) {
+#define TT_SEG(B_, F_, S_) \
+  case B_ * 25 + F_ * 5 + S_: seg_mma<B_, F_, S_>(acc, n, slot, phase, base, full, empty, qa, sw, sgm, lane); break;
+        TT_SEG(0, 0, 1) TT_SEG(0, 0, 2) TT_SEG(0, 0, 3) TT_SEG(0, 0, 4) TT_SEG(0, 1, 0)
+        TT_SEG(0, 1, 1) TT_SEG(0, 1, 2) TT_SEG(0, 1, 3) TT_SEG(0, 2, 0) TT_SEG(0, 2, 1)
+        TT_SEG(0, 2, 2) TT_SEG(0, 3, 0) TT_SEG(0, 3, 1) TT_SEG(0, 4, 0) TT_SEG(1, 0, 0)
+        TT_SEG(1, 0, 1) TT_SEG(1, 0, 2) TT_SEG(1, 0, 3) TT_SEG(1, 1, 0) TT_SEG(1, 1, 1)
+        TT_SEG(1, 1, 2) TT_SEG(1, 2, 0) TT_SEG(1, 2, 1) TT_SEG(1, 3, 0) TT_SEG(2, 0, 0)
+        TT_SEG(2, 0, 1) TT_SEG(2, 0, 2) TT_SEG(2, 1, 0) TT_SEG(2, 1, 1) TT_SEG(2, 2, 0)
+        TT_SEG(3, 0, 0) TT_SEG(3, 0, 1) TT_SEG(3, 1, 0) TT_SEG(4, 0, 0)
+#undef TT_SEG
+        default: seg_mma<0, 0, 0>(acc, n, slot, phase, base, full, empty, qa, sw, sgm, lane); break;
       }
     }
     // GEMM g done: fold into the cube (each cube entry has one owner thread per GEMM; the barriers
