@@ -373,21 +373,27 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, 
  * three DMMA GEMMs with K = 3 n_o + 3 n_v -- and reduces (W + V1) W / D over a<b<c into one partial per
  * unit; a fixed-order sum gives E (deterministic).  Units whose box spins and occupied spins differ in
  * sum are skipped (W = 0 under the spin maps of R7).  With nranks > 1 every input block must be
- * TT_REPLICATED, the units are split into contiguous equal ranges and E is all-reduced (NCCL).
+ * TT_REPLICATED, the units are split into contiguous ranges of equal modelled cost (cost_* below) and E
+ * is all-reduced (NCCL).
  * energy: HOST pointer; the call synchronises the stream.
  *   workspace  device memory of ws_elems doubles >= info->ws_elems (dense copies + one partial per
  *              unit), or NULL to return only info.
  *   info       (may be NULL) w_blocks_total / w_blocks = units in total / on this rank; batches = 1;
  *              flops_alg = FLOPs of the defined sums over the restricted elements (a<b<c, i<j<k,
  *              spin-allowed) of this rank: 2 per non-zero product of the 18 terms (18 (n_o + n_v) per
- *              element without spin; only the spin-allowed half of each m / e sum with alpha/beta spaces); flops_exec = FLOPs the default (TMA) kernel's GEMMs execute (16-wide boxes,
- *              8-row stages per m / e segment; with alpha/beta spaces only the spin-allowed half of each
- *              m / e sum is run);
- *              ws_elems = workspace needed. */
+ *              element without spin; only the spin-allowed half of each m / e sum with alpha/beta
+ *              spaces); flops_exec = FLOPs of the DMMAs the default kernel issues on this rank (only the
+ *              8x8 output fragments holding a needed element, 8-row stages per m / e segment; with
+ *              alpha/beta spaces only the spin-allowed half of each m / e sum is run);
+ *              ws_elems = workspace needed;
+ *              cost_rank / cost_total / cost_max_unit = modelled cost (needed fragments x stages over the
+ *              three GEMMs + a fixed 448 per unit) of this rank's units / all units / the costliest unit:
+ *              the split gives every rank cost_total / nranks within one unit's cost. */
 typedef struct {
   int64_t w_blocks_total, w_blocks, batches;
   double flops_alg, flops_exec;
   int64_t ws_elems;
+  double cost_rank, cost_total, cost_max_unit;
 } tt_triples_info;
 tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vooov, tt_tensor Vvovv,
                             tt_tensor Voovv, const double* eps_o, const double* eps_v, void* workspace,

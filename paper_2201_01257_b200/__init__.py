@@ -64,7 +64,8 @@ class Contract3Info(ctypes.Structure):
 
 class TriplesInfo(ctypes.Structure):
     _fields_ = [("w_blocks_total", _i64), ("w_blocks", _i64), ("batches", _i64), ("flops_alg", _dbl),
-                ("flops_exec", _dbl), ("ws_elems", _i64)]
+                ("flops_exec", _dbl), ("ws_elems", _i64), ("cost_rank", _dbl), ("cost_total", _dbl),
+                ("cost_max_unit", _dbl)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

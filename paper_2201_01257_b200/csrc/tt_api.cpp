@@ -1,6 +1,7 @@
 // tt_api.cpp -- host side of libtt: handles, validation, layout, task lists, partition, plans and
 // the C ABI entry points declared in include/tt.h.  Citations as in tt.h.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <atomic>
@@ -3918,12 +3919,9 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     for (size_t b3 = 0; b3 < box3.size(); ++b3)
       for (size_t t = 0; t < trip.size(); ++t)
         if (box3[b3].w == trip[t].w) { units.push_back({(int)b3, (int)t}); }
-    // contiguous equal ranges over the ranks (every unit costs the same GEMM work)
     const int64_t U = (int64_t)units.size();
     if (U >= (1ll << 31)) return fail(TT_E_UNSUPPORTED, "%lld (T) units exceed the int32 unit index", (long long)U);
     tp->nunits_total = U;
-    tp->unit0 = U * ctx->rank / ctx->nranks;
-    tp->nunits = U * (ctx->rank + 1) / ctx->nranks - tp->unit0;
     // spin split points (R6: alpha = the first range) when each space is exactly (alpha, beta)
     auto half = [](tt_tis t) -> int32_t {
       const tt_is s = t->is;
@@ -3931,39 +3929,116 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     };
     tp->o_half = half(tO);
     tp->v_half = half(tV);
-    // executed FLOPs of the default (TMA) kernel: per unit, per GEMM, per segment ceil(len / 8) stages of
-    // 8 k rows over the 16 x 256 output (the segment ranges follow the kernel's spin restriction)
-    {
-      const int32_t oh = tp->o_half, vh = tp->v_half;
-      auto so = [&](int32_t x) { return oh ? (x < oh ? 1 : -1) : 0; };
-      auto sv = [&](int32_t v) { return vh ? (v < vh ? 1 : -1) : 0; };
-      double stages = 0;
-      (void)per;
-      for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits; ++q) {
-        double unit_len = 0;   // summed indices with non-zero products over the 18 terms of one element
-        const int4 b3 = box3[units[q].x];
-        const int4 tr = trip[units[q].y];
-        const int32_t bl[3] = {box_lo[b3.x], box_lo[b3.y], box_lo[b3.z]};
-        for (int g = 0; g < 3; ++g) {
-          const int32_t sr = sv(bl[g]), sp = sv(g == 0 ? bl[1] : bl[0]), sq = sv(g == 2 ? bl[1] : bl[2]);
-          for (int sg = 0; sg < 6; ++sg) {
-            int64_t len;
-            if (sg < 3) {
-              const int32_t x = (sg == 2) ? tr.y : tr.x, y = (sg == 0) ? tr.y : tr.z;
-              const int32_t sm = so(x) + so(y) - sr;
-              len = !oh ? nO : (sm == 1 ? oh : (sm == -1 ? nO - oh : 0));
-            } else {
-              const int32_t x = (sg == 3) ? tr.x : (sg == 4 ? tr.y : tr.z);
-              const int32_t se = sp + sq - so(x);
-              len = !vh ? nV : (se == 1 ? vh : (se == -1 ? nV - vh : 0));
+    // Needed 8x8 output fragments per box triple and GEMM (the kernel's frag_needed: an 8-row half of
+    // the row box x one p x 8 q holding some a<b<c inside the extents); the default kernel issues DMMAs
+    // for these only.
+    std::vector<std::array<int, 3>> nfrag(box3.size());
+    for (size_t q = 0; q < box3.size(); ++q) {
+      const int4 b3 = box3[q];
+      const int32_t lo3[3] = {box_lo[b3.x], box_lo[b3.y], box_lo[b3.z]};
+      const int32_t ex3[3] = {box_ext[b3.x], box_ext[b3.y], box_ext[b3.z]};
+      for (int g = 0; g < 3; ++g) {
+        int cnt = 0;
+        for (int r0 = 0; r0 < kTripBox; r0 += 8)
+          for (int col = 0; col < kTripBox * kTripBox; col += 8) {
+            const int pp = col / kTripBox, q0 = col % kTripBox;
+            int l[3], h[3];
+            bool ok = true;
+            for (int d = 0; d < 3 && ok; ++d) {
+              int s0, e0;
+              if (d == g) { s0 = r0; e0 = r0 + 8; }
+              else if (d == (g == 0 ? 1 : 0)) { s0 = pp; e0 = pp + 1; }
+              else { s0 = q0; e0 = q0 + 8; }
+              const int hh = std::min(e0, (int)ex3[d]);
+              ok = s0 < hh;
+              l[d] = lo3[d] + s0;
+              h[d] = lo3[d] + hh - 1;
             }
-            stages += (double)((len + 7) / 8);
-            unit_len += (double)len;
+            if (!ok) continue;
+            const int bb = std::max(l[0] + 1, l[1]);
+            if (bb > h[1]) continue;
+            if (std::max(bb + 1, l[2]) <= h[2]) ++cnt;
           }
-        }
-        alg += 2.0 * unit_len * (double)box3_n[units[q].x];
+        nfrag[q][g] = cnt;
       }
-      tp->info.flops_exec = stages * 8.0 * 2.0 * kTripBox * kTripBox * kTripBox;
+    }
+    // per unit: stages of each GEMM (ceil(len / 8) per m / e segment; the segment ranges follow the
+    // kernel's spin restriction) and the summed lengths of the non-zero products
+    const int32_t oh = tp->o_half, vh = tp->v_half;
+    auto so = [&](int32_t x) { return oh ? (x < oh ? 1 : -1) : 0; };
+    auto sv = [&](int32_t v) { return vh ? (v < vh ? 1 : -1) : 0; };
+    auto unit_stages = [&](int64_t q, int64_t st[3], int64_t& unit_len) {
+      const int4 b3 = box3[units[q].x];
+      const int4 tr = trip[units[q].y];
+      const int32_t bl[3] = {box_lo[b3.x], box_lo[b3.y], box_lo[b3.z]};
+      unit_len = 0;
+      for (int g = 0; g < 3; ++g) {
+        const int32_t sr = sv(bl[g]), sp = sv(g == 0 ? bl[1] : bl[0]), sq = sv(g == 2 ? bl[1] : bl[2]);
+        st[g] = 0;
+        for (int sg = 0; sg < 6; ++sg) {
+          int64_t len;
+          if (sg < 3) {
+            const int32_t x = (sg == 2) ? tr.y : tr.x, y = (sg == 0) ? tr.y : tr.z;
+            const int32_t sm = so(x) + so(y) - sr;
+            len = !oh ? nO : (sm == 1 ? oh : (sm == -1 ? nO - oh : 0));
+          } else {
+            const int32_t x = (sg == 3) ? tr.x : (sg == 4 ? tr.y : tr.z);
+            const int32_t se = sp + sq - so(x);
+            len = !vh ? nV : (se == 1 ? vh : (se == -1 ? nV - vh : 0));
+          }
+          st[g] += (len + 7) / 8;
+          unit_len += len;
+        }
+      }
+    };
+    // Cost-balanced contiguous ranges over the ranks: a unit costs its issued DMMA fragment-stages
+    // (sum over the GEMMs of needed fragments x stages) plus a fixed per-unit share (prologue, three
+    // folds, energy epilogue) of 3 x 64 + 256 -- diagonal box triples and spin-halved sums are cheaper.
+    constexpr double kUnitFixed = 3.0 * 64.0 + 256.0;
+    std::vector<double> cost((size_t)U);
+    double cost_total = 0, cost_max = 0;
+    for (int64_t q = 0; q < U; ++q) {
+      int64_t st[3], ul;
+      unit_stages(q, st, ul);
+      const auto& nf = nfrag[units[q].x];
+      cost[q] = (double)(nf[0] * st[0] + nf[1] * st[1] + nf[2] * st[2]) + kUnitFixed;
+      cost_total += cost[q];
+      cost_max = std::max(cost_max, cost[q]);
+    }
+    {
+      // rank r takes the units whose cost midpoint falls in [C r / N, C (r + 1) / N)
+      int64_t first = -1, last = -1;
+      double acc = 0;
+      const double lo_c = cost_total * (double)ctx->rank / (double)ctx->nranks;
+      const double hi_c = cost_total * (double)(ctx->rank + 1) / (double)ctx->nranks;
+      for (int64_t q = 0; q < U; ++q) {
+        const double mid = acc + 0.5 * cost[q];
+        acc += cost[q];
+        if (mid >= lo_c && (mid < hi_c || ctx->rank == ctx->nranks - 1)) {
+          if (first < 0) first = q;
+          last = q;
+        }
+      }
+      tp->unit0 = first < 0 ? 0 : first;
+      tp->nunits = first < 0 ? 0 : last - first + 1;
+    }
+    // executed FLOPs of the default kernel: per unit and GEMM, the needed 8x8 fragments x stages of 8 k
+    // rows (2 x 8 x 8 x 8 per fragment-stage)
+    {
+      double frag_stages = 0, rank_cost = 0;
+      for (int64_t q = tp->unit0; q < tp->unit0 + tp->nunits; ++q) {
+        int64_t st[3], ul;
+        unit_stages(q, st, ul);
+        const auto& nf = nfrag[units[q].x];
+        frag_stages += (double)(nf[0] * st[0] + nf[1] * st[1] + nf[2] * st[2]);
+        rank_cost += cost[q];
+        alg += 2.0 * (double)ul * (double)box3_n[units[q].x];
+      }
+      (void)per;
+      tp->info.flops_exec = frag_stages * 2.0 * 8.0 * 8.0 * 8.0;
+      tp->info.cost_rank = rank_cost;
+      tp->info.cost_total = cost_total;
+      tp->info.cost_max_unit = cost_max;
     }
     tp->info.w_blocks_total = U;
     tp->info.w_blocks = tp->nunits;

@@ -290,22 +290,73 @@ def test_triples_odd_virtual_range_refused():
     assert e.value.name == "TT_E_UNSUPPORTED"
 
 
-def test_triples_units_partition_over_ranks():
-    """Units split into contiguous equal ranges (every rank's count; the sum is the total)."""
+@pytest.mark.parametrize("nO,nV,tO,tV,spin,nranks", [(7, 20, 3, 5, False, 3), (8, 40, 2, 10, True, 4),
+                                                       (9, 36, 3, 9, False, 2)])
+def test_triples_units_partition_over_ranks(nO, nV, tO, tV, spin, nranks):
+    """Units split into contiguous ranges of equal modelled cost: the counts sum to the total, the rank
+    costs sum to the total cost, and each rank is within one unit's cost of total / nranks."""
     import paper_2201_01257_b200 as tt
-    counts = []
-    for r in range(3):
-        ctx = tt.Context(device=-1, rank=r, nranks=3)
-        _, _, to, tv = _spaces(tt, 7, 20, 3, 5, False)
+    counts, costs, flops = [], [], []
+    for r in range(nranks):
+        ctx = tt.Context(device=-1, rank=r, nranks=nranks)
+        _, _, to, tv = _spaces(tt, nO, nV, tO, tV, spin)
         dims = {"o": to, "v": tv}
-        T = {n: tt.Tensor(ctx, [dims[c] for c in d]) for n, d, sp, _ in TRIPLES_INPUTS}
+        T = {n: tt.Tensor(ctx, [dims[c] for c in d], spin=sp if spin else None) for n, d, sp, _ in TRIPLES_INPUTS}
         for X in T.values():
             X.set_owner(np.full(X.nblocks, tt.TT_REPLICATED, np.int32))
         _, info = tt.triples_energy(ctx, T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
         counts.append(info["w_blocks"])
-        total = info["w_blocks_total"]
-    assert sum(counts) == total == _expected_units(7, 20, False)
-    assert max(counts) - min(counts) <= 1
+        costs.append(info["cost_rank"])
+        flops.append(info["flops_exec"])
+        total, ctotal, cmax = info["w_blocks_total"], info["cost_total"], info["cost_max_unit"]
+    assert sum(counts) == total == _expected_units(nO, nV, spin)
+    assert sum(costs) == pytest.approx(ctotal, rel=1e-12)
+    assert max(abs(c - ctotal / nranks) for c in costs) <= cmax
+    assert sum(flops) == _expected_exec_flops(nO, nV, spin)
+
+
+def _expected_exec_flops(nO, nV, spin, box=16):
+    """DMMA FLOPs the default kernel issues, counted by brute force: per unit and GEMM g (row role = index
+    g of (a,b,c); columns = (p, q) with p the first remaining index and q the other), every 8-row x
+    (one p, 8 q) output fragment holding an element a<b<c inside the boxes, times the 8-row stages of its
+    m and e segments (spin: only the allowed half of each sum), x 2 x 8 x 8 x 8 per fragment-stage."""
+    def sp(n, x):
+        return (1 if x < n // 2 else -1) if spin else 0
+    ranges = [(0, nV // 2), (nV // 2, nV)] if spin else [(0, nV)]
+    boxes = [(x, min(box, e - x), sp(nV, x)) for b, e in ranges for x in range(b, e, box)]
+    half_o, half_v = (nO // 2, nV // 2) if spin else (0, 0)
+
+    def seg(n, half, s):           # stages of a sum over n indices restricted to spin s (0 = no spin)
+        ln = n if not half else (half if s == 1 else (n - half if s == -1 else 0))
+        return -(-ln // 8)
+    total = 0
+    for bx in itertools.combinations_with_replacement(boxes, 3):
+        if not any(a < b < c for a in range(bx[0][0], bx[0][0] + bx[0][1]) for b in range(bx[1][0], bx[1][0] + bx[1][1])
+                   for c in range(bx[2][0], bx[2][0] + bx[2][1])):
+            continue
+        for i, j, k in itertools.combinations(range(nO), 3):
+            if spin and sp(nO, i) + sp(nO, j) + sp(nO, k) != bx[0][2] + bx[1][2] + bx[2][2]:
+                continue
+            for g in range(3):
+                roles = [g] + [d for d in range(3) if d != g]      # row, p, q
+                nf = 0
+                for r0 in (0, 8):
+                    for p in range(box):
+                        for q0 in (0, 8):
+                            cell = {roles[0]: range(r0, min(r0 + 8, bx[roles[0]][1])),
+                                    roles[1]: range(p, min(p + 1, bx[roles[1]][1])),
+                                    roles[2]: range(q0, min(q0 + 8, bx[roles[2]][1]))}
+                            if any(bx[0][0] + x < bx[1][0] + y < bx[2][0] + z
+                                   for x in cell[0] for y in cell[1] for z in cell[2]):
+                                nf += 1
+                # segments: m sums over v^{xy}_{m r} (s_m = s_x + s_y - s_r), e sums over v^{ex}_{pq}
+                # (s_e = s_p + s_q - s_x), occupied pairs / singles of the three terms of G
+                so = [sp(nO, i), sp(nO, j), sp(nO, k)]
+                sr, spp, sq = bx[roles[0]][2], bx[roles[1]][2], bx[roles[2]][2]
+                st = sum(seg(nO, half_o, so[x] + so[y] - sr) for x, y in ((0, 1), (0, 2), (1, 2)))
+                st += sum(seg(nV, half_v, spp + sq - so[x]) for x in range(3))
+                total += nf * st * 2 * 8 * 8 * 8
+    return total
 
 
 @pytest.mark.gpu
