@@ -3732,6 +3732,7 @@ struct TripPlan {
   int64_t ws_need = 0;
   int64_t blk_pos[4] = {0, 0, 0, 0}, blk_n[4] = {0, 0, 0, 0};   // blocked copies (QT2, QVV, PVO, PT2)
   int32_t nbox = 0;
+  int32_t kpo = 0, kpv = 0, ko2 = 0, kv2 = 0;   // padded summed rows of the blocked copies
   tt_triples_info info{};
   ~TripPlan() {
     for (auto& r : rt) delete r.dst;
@@ -4046,9 +4047,15 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     tp->info.flops_alg = alg;
     // blocked copies of the default kernel (TriplesParams): after the partials
     {
-      const int64_t nbx = (int64_t)tp->nbox, o = nO, v = nV;
-      const int64_t ns[4] = {o * nbx * nbx * (o + 8) * kTripBox * kTripBox, o * nbx * nbx * (v + 8) * kTripBox * kTripBox,
-                             o * o * nbx * (o + 8) * kTripBox, o * o * nbx * (v + 8) * kTripBox};
+      // padded summed rows: each spin range rounded up to a multiple of 8 (TriplesParams)
+      auto pad8 = [](int64_t x) { return (x + 7) / 8 * 8; };
+      tp->ko2 = (int32_t)pad8(tp->o_half);
+      tp->kv2 = (int32_t)pad8(tp->v_half);
+      tp->kpo = (int32_t)(tp->ko2 + pad8(nO - tp->o_half));
+      tp->kpv = (int32_t)(tp->kv2 + pad8(nV - tp->v_half));
+      const int64_t nbx = (int64_t)tp->nbox, o = nO, kpo = tp->kpo, kpv = tp->kpv;
+      const int64_t ns[4] = {o * nbx * nbx * kpo * kTripBox * kTripBox, o * nbx * nbx * kpv * kTripBox * kTripBox,
+                             o * o * nbx * kpo * kTripBox, o * o * nbx * kpv * kTripBox};
       int64_t pos = base + (U + 1) / 2 * 2;
       for (int q = 0; q < 4; ++q) {
         tp->blk_pos[q] = pos;
@@ -4130,6 +4137,10 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   p.v_half = tp->v_half;
   p.partials = partials;
   p.nb = tp->nbox;
+  p.kpo = tp->kpo;
+  p.kpv = tp->kpv;
+  p.ko2 = tp->ko2;
+  p.kv2 = tp->kv2;
   {   // blocked copies of the default kernel
     double* bq[4];
     for (int q = 0; q < 4; ++q) bq[q] = ws + tp->blk_pos[q];

@@ -210,14 +210,20 @@ struct TriplesParams {
   const int2* pairs;    // pair variant: (first unit, 1 or 2 units) per CTA
   double* partials;     // one per unit (indexed by unit)
   // blocked copies of the default kernel: every 8-row stage of an operand tile is ONE contiguous run
-  // (a 1-D bulk copy), boxes of kTripBox indexed by box id, k rows padded by 8 zero rows, and the
-  // column index XOR-swizzled by 4 (k mod 4): a half-warp's 64-bit fragment load (4 k rows x 4
-  // columns) then touches 16 distinct double banks -- conflict-free without padding
-  const double* QT2;    // [z][bp][bq][m (nO+8)][16][16]   t^{m z}_{p q}
-  const double* QVV;    // [x][bp][bq][e (nV+8)][16][16]   v^{e x}_{p q}
-  const double* PVO;    // [x][y][br][m (nO+8)][16]        v^{x y}_{m r}
-  const double* PT2;    // [y][z][br][e (nV+8)][16]        t^{y z}_{e r}
+  // (1-D bulk copies), boxes of kTripBox indexed by box id, and the column index XOR-swizzled by
+  // 4 (k mod 4): a half-warp's 64-bit fragment load (4 k rows x 4 columns) then touches 16 distinct
+  // double banks -- conflict-free without padding
+  // The summed index k runs over kp rows: each spin range [0, half) and [half, n) padded with zero rows
+  // to a multiple of 8 (no spin: [0, n) padded), so every 8-row stage of a segment is one aligned run.
+  // Q tiles store a stage p-major ([k/8][p][k%8][q]): a box narrower than 16 in the p role is loaded as
+  // ext_p contiguous KB.
+  const double* QT2;    // [z][bp][bq][m'/8][p][m'%8][q]  t^{m z}_{p q}
+  const double* QVV;    // [x][bp][bq][e'/8][p][e'%8][q]  v^{e x}_{p q}
+  const double* PVO;    // [x][y][br][m'][16]             v^{x y}_{m r}
+  const double* PT2;    // [y][z][br][e'][16]             t^{y z}_{e r}
   int32_t nb;           // virtual boxes
+  int32_t kpo, kpv;     // padded row counts m', e'
+  int32_t ko2, kv2;     // first padded row of the second spin range (0 without spin)
 };
 // dense copy -> blocked copy (mode 0..3 = QT2, QVV, PVO, PT2)
 cudaError_t launch_blockify(int mode, const TriplesParams& p, double* dst, int64_t n, cudaStream_t s);

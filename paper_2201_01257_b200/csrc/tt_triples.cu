@@ -83,35 +83,45 @@ __global__ void retile_kernel(const RetileParams p) {
 }
 
 // dense copies (rt) -> blocked, pre-swizzled copies of the default kernel (see TriplesParams)
+__device__ __forceinline__ int32_t unpad_row(int32_t kq, int32_t half, int32_t k2, int32_t n) {
+  // padded row -> summed index, -1 for a padding row
+  const int32_t k = kq < k2 ? kq : half + (kq - k2);
+  return (kq < k2 ? k < half : k < n) ? k : -1;
+}
+
 __global__ void blockify_kernel(int mode, const TriplesParams p, double* __restrict__ dst, int64_t n) {
   const int32_t nO = p.nO, nV = p.nV, nb = p.nb;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
-    if (mode <= 1) {   // [o][bp][bq][k][16][16]
-      const int32_t kp = (mode == 0 ? nO : nV) + 8;
+    if (mode <= 1) {   // [o][bp][bq][k'/8][p][k'%8][q]
+      const int32_t kp = mode == 0 ? p.kpo : p.kpv;
       int64_t r = e;
       const int qs = (int)(r % BX); r /= BX;
+      const int k8 = (int)(r % KC); r /= KC;
       const int pl = (int)(r % BX); r /= BX;
-      const int32_t k = (int32_t)(r % kp); r /= kp;
+      const int32_t kst = (int32_t)(r % (kp / KC)); r /= kp / KC;
       const int32_t bq = (int32_t)(r % nb); r /= nb;
       const int32_t bp = (int32_t)(r % nb); r /= nb;
       const int32_t o = (int32_t)r;
-      const int ql = qs ^ ((k & 3) << 2);   // stored at column q ^ 4(k mod 4)
+      const int32_t kq = kst * KC + k8;
+      const int32_t k = mode == 0 ? unpad_row(kq, p.o_half, p.ko2, nO) : unpad_row(kq, p.v_half, p.kv2, nV);
+      const int ql = qs ^ ((kq & 3) << 2);   // stored at column q ^ 4(k' mod 4)
       const int32_t pv = p.box_lo[bp] + pl, qv = p.box_lo[bq] + ql;
-      if (pl < p.box_ext[bp] && ql < p.box_ext[bq] && k < (mode == 0 ? nO : nV))
+      if (pl < p.box_ext[bp] && ql < p.box_ext[bq] && k >= 0)
         v = mode == 0 ? p.T2[(((int64_t)k * nO + o) * nV + pv) * nV + qv]      // T2[m][z][p][q]
                       : p.VV[(((int64_t)k * nO + o) * nV + pv) * nV + qv];     // VV[e][x][p][q]
-    } else {           // [o1][o2][br][k][16]
-      const int32_t kp = (mode == 2 ? nO : nV) + 8;
+    } else {           // [o1][o2][br][k'][16]
+      const int32_t kp = mode == 2 ? p.kpo : p.kpv;
       int64_t r = e;
       const int rs = (int)(r % BX); r /= BX;
-      const int32_t k = (int32_t)(r % kp); r /= kp;
+      const int32_t kq = (int32_t)(r % kp); r /= kp;
       const int32_t br = (int32_t)(r % nb); r /= nb;
       const int32_t o2 = (int32_t)(r % nO); r /= nO;
       const int32_t o1 = (int32_t)r;
-      const int rl = rs ^ ((k & 3) << 2);
+      const int32_t k = mode == 2 ? unpad_row(kq, p.o_half, p.ko2, nO) : unpad_row(kq, p.v_half, p.kv2, nV);
+      const int rl = rs ^ ((kq & 3) << 2);
       const int32_t rv = p.box_lo[br] + rl;
-      if (rl < p.box_ext[br] && k < (mode == 2 ? nO : nV))
+      if (rl < p.box_ext[br] && k >= 0)
         v = mode == 2 ? p.VO[(((int64_t)o1 * nO + o2) * nO + k) * nV + rv]     // VO[x][y][m][r]
                       : p.T2[(((int64_t)o1 * nO + o2) * nV + k) * nV + rv];    // T2[y][z][e][r]
     }
@@ -469,7 +479,7 @@ __device__ __forceinline__ void seg_mma(double (&acc)[2][NFR][2], int n, int& sl
             : __longlong_as_double(__double_as_longlong(P[kl * BX + ((8 + (lane >> 2)) ^ sw)]) ^ sgm);
 #pragma unroll
         for (int f = 0; f < NS; ++f) {
-          const double b = Q[kk * 4 * (BX * BX) + qa[f]];
+          const double b = Q[kk * 4 * BX + qa[f]];
           if (f < NB + N0) dmma(acc[0][f], a0, b);
           if (f < NB || f >= NB + N0) dmma(acc[1][f], a1, b);
         }
@@ -547,7 +557,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
     int slot = 0;
     unsigned phase = 1;   // empty barriers: the first pass over the ring does not wait
-    const int32_t nb = p.nb, kpo = nO + 8, kpv = nV + 8;
+    const int32_t nb = p.nb, kpo = p.kpo, kpv = p.kpv;
     for (int g = 0; g < 3; ++g) {
       const int32_t br = g == 0 ? bx.x : (g == 1 ? bx.y : bx.z);   // box ids of the roles (r; p, q)
       const int32_t bp = g == 0 ? bx.y : bx.x;
@@ -555,10 +565,12 @@ __global__ void __launch_bounds__(TTHREADS, 2)
       for (int sg = 0; sg < 6; ++sg) {
         const int32_t n = segn[g * 6 + sg];
         for (int jj = 0; jj < n; ++jj) {
-          const int32_t k0 = segb[g * 6 + sg] + jj * KC;
+          // padded first row: segments start at 0 or at the second spin range
+          const int32_t k0 = (segb[g * 6 + sg] == 0 ? 0 : (sg < 3 ? p.ko2 : p.kv2)) + jj * KC;
+          const unsigned qbytes = (unsigned)p.box_ext[bp] * (KC * BX * 8);   // ext_p rows of p
           tbar_wait(&empty[slot], phase);
           unsigned char* st = base + slot * BSTAGE;
-          tbar_expect(&full[slot], (unsigned)BSTAGE);
+          tbar_expect(&full[slot], qbytes + (unsigned)BP_BYTES);
           const double *qsrc, *psrc;
           if (sg < 3) {
             const int32_t x = (sg == 2) ? J : I, y = (sg == 0) ? J : K, z = (sg == 0) ? K : (sg == 1 ? J : I);
@@ -570,7 +582,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
             qsrc = p.QVV + ((((int64_t)x * nb + bp) * nb + bq) * kpv + k0) * (BX * BX);   // VV[e][x][p][q]
             psrc = p.PT2 + ((((int64_t)y * nO + z) * nb + br) * kpv + k0) * BX;          // T2[y][z][e][r]
           }
-          bulk_copy(st, qsrc, BQ_BYTES, &full[slot]);
+          bulk_copy(st, qsrc, qbytes, &full[slot]);
           bulk_copy(st + BQ_BYTES, psrc, BP_BYTES, &full[slot]);
           if (++slot == BNS) { slot = 0; phase ^= 1; }
         }
@@ -617,13 +629,13 @@ __global__ void __launch_bounds__(TTHREADS, 2)
       const int32_t n = segn[g * 6 + sg];
       const bool neg = sg < 3 ? sg == 1 : sg != 4;   // m sums (+,-,+), e sums (-,+,-)
       const long long sgm = neg ? (long long)0x8000000000000000ull : 0ll;
-      // every stage of a segment starts at a k row = segb mod 4 (stages are 8 rows): one swizzle
-      const int sw = (((lane & 3) + segb[g * 6 + sg]) & 3) << 2;   // columns XOR 4(k mod 4)
-      int qa[NFR];                                                  // Q offsets of this lane's columns
+      // every stage starts at a padded row = 0 mod 8: the swizzle is (k' mod 4) = the lane's k row
+      const int sw = (lane & 3) << 2;                               // columns XOR 4(k' mod 4)
+      int qa[NFR];                                                  // Q offsets ([p][k'%8][q]) of this lane
 #pragma unroll
       for (int f = 0; f < NFR; ++f) {
         const int col = (int)((colp >> (8 * f)) & 31u) * 8 + (lane >> 2);
-        qa[f] = (lane & 3) * (BX * BX) + (col / BX) * BX + ((col % BX) ^ sw);
+        qa[f] = (col / BX) * (KC * BX) + (lane & 3) * BX + ((col % BX) ^ sw);
       }
       switch (nb_ * 25 + n0_ * 5 + n1_) {
 #define TT_SEG(B_, F_, S_) \
