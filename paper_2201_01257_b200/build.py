@@ -9,6 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtt.so")
 SOURCES = ["tt_kernels.cu", "tt_ws_w0.cu", "tt_ws_w1.cu", "tt_ws_w2.cu", "tt_ws_dispatch.cu", "tt_triples.cu", "tt_api.cpp",
+           "tt_elem.cpp", "tt_contract.cpp", "tt_cholesky.cpp", "tt_contract3.cpp", "tt_triples_host.cpp",
            "tt_nccl.cpp", "tt_sched.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
