@@ -306,10 +306,12 @@ tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* c_lbl, doubl
  * c_flags: TT_HOST_C_IN uploads C first (needed when beta != 0 and C is not resident), TT_HOST_C_OUT
  * downloads C after the contraction.  Device buffers of A, B, C must be bound (copy destinations).
  * With nranks == 1 and A's dim 0 labelled like C's dim 0 (same tiled space; no views, A != B, C not
- * compact) the call is PIPELINED: per dim-0 tile x of C, A's blocks with dim-0 coordinate x (one packed
- * range) are copied host->device on the context's copy stream while tile x-1 contracts, and C's rows of
- * tile x go back while tile x+1 contracts; each tile is computed by the same kernel and k order as the
- * whole contraction, so the result is bitwise that of upload + tt_contract + download.  Otherwise every
+ * compact) the call is PIPELINED: per chunk x of C (its blocks sharing the dim-0 tile, or the (dim-0,
+ * dim-1) tile pair when dim 0 has fewer than 16 tiles and A's dim 1 carries C's dim-1 label), A's blocks
+ * with the same leading coordinates (one packed range) are copied host->device on the context's copy
+ * stream while chunk x-1 contracts, and C's rows of chunk x go back while chunk x+1 contracts; each chunk
+ * is computed with the same per-element k order as the whole contraction, so the result is bitwise that
+ * of upload + tt_contract + download.  Otherwise every
  * rank copies the ranges it holds (owned blocks / row parts, replicated blocks), runs tt_contract (the
  * gathers fetch the rest over NVLink) and copies back its own C ranges.  Asynchronous on the context
  * stream like tt_contract: the host buffers must stay valid until tt_sync.  Errors as tt_contract. */

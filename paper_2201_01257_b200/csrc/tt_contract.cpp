@@ -664,18 +664,26 @@ tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* cl, double b
 }
 
 // End to end from host memory (tt.h tt_contract_host).  Pipelined (nranks == 1, A's and C's dim 0 carry
-// the same label on the same tiling, no views): per dim-0 tile x of C, A's blocks with dim-0 coordinate x
-// -- one contiguous packed range (row-major block order) -- go host->device on the context's copy stream
-// while tile x-1 contracts; tile x is a local plan restricted to C's blocks with dim-0 coordinate x (the
-// same kernel and per-element k order as the whole contraction: bitwise the same result, R12); its C
-// rows go device->host while tile x+1 contracts.  Otherwise: H2D of every held range, tt_contract, D2H
-// of this rank's C ranges.
+// the same label on the same tiling, no views): per chunk x of C -- the blocks sharing C's dim-0 tile,
+// or its (dim-0, dim-1) tile pair when dim 0 has fewer than kHostMinChunks tiles and A's dim 1 carries
+// C's dim-1 label -- A's blocks with the same leading coordinates (one contiguous packed range,
+// row-major block order) go host->device on the context's copy stream while chunk x-1 contracts; chunk
+// x is a local plan restricted to its C blocks (the same per-element k order as the whole contraction:
+// bitwise the same result, R12); its C rows go device->host while chunk x+1 contracts.  Otherwise: H2D
+// of every held range, tt_contract, D2H of this rank's C ranges.
 namespace {
 struct HostPlan {
   bool pipelined = false;
-  std::vector<std::pair<int64_t, int64_t>> a_rng, c_rng;   // per dim-0 tile of C: storage ranges of A, C
-  std::vector<std::shared_ptr<ContractPlan>> tiles;        // local plan of each tile (nullptr: no C block)
+  int32_t lead = 1;   // leading dims of C (shared with A) that define a pipeline chunk: 1 or 2
+  int32_t nt1 = 1;    // tiles of C's dim 1 when lead == 2
+  std::vector<std::pair<int64_t, int64_t>> a_rng, c_rng;   // per chunk: storage ranges of A, C
+  std::vector<std::shared_ptr<ContractPlan>> tiles;        // local plan of each chunk (nullptr: no C block)
+  int32_t chunk(const int32_t* co) const { return lead == 2 ? co[0] * nt1 + co[1] : co[0]; }
 };
+
+// chunks of the host pipeline: finer chunks shorten the exposed first upload and last contraction;
+// dims 0 and 1 are used together when dim 0 alone gives fewer than this many
+constexpr int32_t kHostMinChunks = 16;
 
 void held_storage(tt_tensor T, int32_t rank, std::vector<std::pair<int64_t, int64_t>>& out) {
   out.clear();
@@ -726,7 +734,13 @@ tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* cl, double beta,
     const bool same0 = al[0] == cl[0] && same_tiling(A->dims[0], C->dims[0]);
     hp->pipelined = ctx->nranks == 1 && same0 && !A->view_of && !C->view_of && A != B && !C->compact;
     if (hp->pipelined) {
-      const int32_t nt = C->dims[0]->ntiles();
+      // blocks sharing C's (and A's) leading block coordinates are contiguous in packed order, so each
+      // chunk's A rows and C rows are one storage range each
+      const bool two = C->order >= 2 && A->order >= 2 && C->dims[0]->ntiles() < kHostMinChunks && al[1] == cl[1] &&
+                       same_tiling(A->dims[1], C->dims[1]);
+      hp->lead = two ? 2 : 1;
+      hp->nt1 = two ? C->dims[1]->ntiles() : 1;
+      const int32_t nt = C->dims[0]->ntiles() * hp->nt1;
       hp->a_rng.assign(nt, {0, 0});
       hp->c_rng.assign(nt, {0, 0});
       hp->tiles.assign(nt, nullptr);
@@ -735,7 +749,7 @@ tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* cl, double beta,
         for (int64_t b = 0; b < T->nblocks; ++b) {
           if (!T->nz[b] || T->blk_off[b] < 0) continue;
           T->block_coords(b, co);
-          auto& r = rng[co[0]];
+          auto& r = rng[hp->chunk(co)];
           const int64_t a0 = T->blk_off[b], a1 = a0 + T->block_volume(b);
           if (r.second == r.first) r = {a0, a1};
           else r = {std::min(r.first, a0), std::max(r.second, a1)};
@@ -750,7 +764,7 @@ tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* cl, double beta,
         for (int64_t b = 0; b < C->nblocks; ++b) {
           if (!C->nz[b]) continue;
           C->block_coords(b, co);
-          if (co[0] == x) o.sel.push_back({b, 0, C->ext0(b)});
+          if (hp->chunk(co) == x) o.sel.push_back({b, 0, C->ext0(b)});
         }
         if (o.sel.empty()) continue;
         TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, hp->tiles[x], nullptr, o));
