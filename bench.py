@@ -25,8 +25,8 @@ the other terms' kernels.  The kernel tile variant is autotuned by tt_contract o
 e2e: the same step from pinned host memory through the library's own end-to-end call tt_contract_host
 (include/tt.h): N = 1 pipelines inside libtt (per (a, b) tile pair of R: H2D of the operand rows on the
 library's copy stream overlaps the previous chunk's contraction, finished R rows go back while the next
-computes; checked bit for bit against upload + step + download); N > 1: every rank moves only the
-blocks / row parts it holds and reads back its R parts.
+computes; checked bit for bit against upload + step + download); N > 1: the same per rank over the
+blocks / row parts it holds (T's remote blocks gathered over NVLink first), also checked bit for bit.
 
 sub_configs (N = 1, default run): configs[0] (launch-latency bound: us per contraction, HBM fraction
 of its compulsory bytes) and configs[2] (one step of its three terms, own roofline), measured after the
@@ -480,7 +480,7 @@ def main():
 
         h2d = sum(held_bytes(T[n]) for n in T)
         d2h = held_bytes(T["R"])
-        if world == 1:   # the library's pipelined step must reproduce upload + step + download bit for bit
+        if True:   # the library's pipelined step must reproduce upload + step + download bit for bit
             r0 = hosts["R"].clone()
             e2e_step_plain()
             torch.cuda.synchronize()
@@ -514,8 +514,9 @@ def main():
                "how": ("pipelined inside libtt: per (a, b) tile pair of R, H2D of the operand rows on the "
                        "library's copy stream overlapping the previous chunk's contraction, D2H of finished R rows "
                        "overlapping the next; PCIe floor 13.8 GB / 55.6 GB/s = 249 ms") if world == 1 else
-                      ("each rank: H2D of the blocks / row parts it holds, the contraction (gathers of the rest "
-                       "over NVLink), D2H of its R parts")}
+                      ("each rank, pipelined inside libtt: H2D of T's held blocks and NVLink gather of the rest, "
+                       "then per (a, b) tile pair the V rows it holds on the copy stream overlapping the previous "
+                       "chunk's contraction, D2H of its finished R rows")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

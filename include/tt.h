@@ -305,8 +305,9 @@ tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* c_lbl, doubl
  * same layout as tt_tensor_upload; NULL = that operand is already resident on the device, no copy).
  * c_flags: TT_HOST_C_IN uploads C first (needed when beta != 0 and C is not resident), TT_HOST_C_OUT
  * downloads C after the contraction.  Device buffers of A, B, C must be bound (copy destinations).
- * With nranks == 1 and A's dim 0 labelled like C's dim 0 (same tiled space; no views, A != B, C not
- * compact) the call is PIPELINED: per chunk x of C (its blocks sharing the dim-0 tile, or the (dim-0,
+ * With A's dim 0 labelled like C's dim 0 (same tiled space; no views, A != B, C not compact) and, with
+ * several ranks, A's rows local to this rank's C rows (no gather of A; B's remote blocks are gathered
+ * first), the call is PIPELINED over the blocks / row parts this rank holds: per chunk x of C (its blocks sharing the dim-0 tile, or the (dim-0,
  * dim-1) tile pair when dim 0 has fewer than 16 tiles and A's dim 1 carries C's dim-1 label), A's blocks
  * with the same leading coordinates (one packed range) are copied host->device on the context's copy
  * stream while chunk x-1 contracts, and C's rows of chunk x go back while chunk x+1 contracts; each chunk

@@ -663,8 +663,9 @@ tt_status tt_contract_prefetch(tt_ctx ctx, tt_tensor C, const char* cl, double b
   return TT_OK;
 }
 
-// End to end from host memory (tt.h tt_contract_host).  Pipelined (nranks == 1, A's and C's dim 0 carry
-// the same label on the same tiling, no views): per chunk x of C -- the blocks sharing C's dim-0 tile,
+// End to end from host memory (tt.h tt_contract_host).  Pipelined (A's and C's dim 0 carry the same label
+// on the same tiling, no views; with several ranks A's rows local to the rank's C rows, B's remote
+// blocks gathered once up front): per chunk x of C -- the blocks sharing C's dim-0 tile,
 // or its (dim-0, dim-1) tile pair when dim 0 has fewer than kHostMinChunks tiles and A's dim 1 carries
 // C's dim-1 label -- A's blocks with the same leading coordinates (one contiguous packed range,
 // row-major block order) go host->device on the context's copy stream while chunk x-1 contracts; chunk
@@ -676,7 +677,7 @@ struct HostPlan {
   bool pipelined = false;
   int32_t lead = 1;   // leading dims of C (shared with A) that define a pipeline chunk: 1 or 2
   int32_t nt1 = 1;    // tiles of C's dim 1 when lead == 2
-  std::vector<std::pair<int64_t, int64_t>> a_rng, c_rng;   // per chunk: storage ranges of A, C
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> a_rng, c_rng;   // per chunk: held storage of A, C
   std::vector<std::shared_ptr<ContractPlan>> tiles;        // local plan of each chunk (nullptr: no C block)
   int32_t chunk(const int32_t* co) const { return lead == 2 ? co[0] * nt1 + co[1] : co[0]; }
 };
@@ -732,41 +733,54 @@ tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* cl, double beta,
   if (!hp) {
     hp = std::make_shared<HostPlan>();
     const bool same0 = al[0] == cl[0] && same_tiling(A->dims[0], C->dims[0]);
-    hp->pipelined = ctx->nranks == 1 && same0 && !A->view_of && !C->view_of && A != B && !C->compact;
+    // with several ranks, A's rows must be local to this rank's C rows (no gather entry of A): B's gather
+    // runs once up front, A arrives chunk by chunk
+    bool a_local = true;
+    if (A != B)
+      for (const auto* lst : {&whole->gp.send_list, &whole->gp.recv_list})
+        for (size_t i = 0; i + 4 < lst->size(); i += 5) a_local = a_local && (*lst)[i] != 0;
+    hp->pipelined = same0 && a_local && !A->view_of && !C->view_of && A != B && !C->compact;
     if (hp->pipelined) {
-      // blocks sharing C's (and A's) leading block coordinates are contiguous in packed order, so each
-      // chunk's A rows and C rows are one storage range each
+      // blocks sharing C's (and A's) leading block coordinates are contiguous in packed order; each
+      // chunk moves this rank's held ranges of those blocks
       const bool two = C->order >= 2 && A->order >= 2 && C->dims[0]->ntiles() < kHostMinChunks && al[1] == cl[1] &&
                        same_tiling(A->dims[1], C->dims[1]);
       hp->lead = two ? 2 : 1;
       hp->nt1 = two ? C->dims[1]->ntiles() : 1;
       const int32_t nt = C->dims[0]->ntiles() * hp->nt1;
-      hp->a_rng.assign(nt, {0, 0});
-      hp->c_rng.assign(nt, {0, 0});
+      hp->a_rng.assign(nt, {});
+      hp->c_rng.assign(nt, {});
       hp->tiles.assign(nt, nullptr);
       int32_t co[TT_MAX_ORDER];
-      auto span = [&](tt_tensor T, std::vector<std::pair<int64_t, int64_t>>& rng) {
+      std::vector<std::pair<int64_t, int64_t>> hr;
+      auto held = [&](tt_tensor T, std::vector<std::vector<std::pair<int64_t, int64_t>>>& rng) {
         for (int64_t b = 0; b < T->nblocks; ++b) {
           if (!T->nz[b] || T->blk_off[b] < 0) continue;
           T->block_coords(b, co);
-          auto& r = rng[hp->chunk(co)];
-          const int64_t a0 = T->blk_off[b], a1 = a0 + T->block_volume(b);
-          if (r.second == r.first) r = {a0, a1};
-          else r = {std::min(r.first, a0), std::max(r.second, a1)};
+          auto& v = rng[hp->chunk(co)];
+          T->held_ranges(b, ctx->rank, hr);
+          for (auto& h : hr) {
+            const int64_t a0 = T->blk_off[b] + h.first, a1 = T->blk_off[b] + h.second;
+            if (!v.empty() && a0 - v.back().second <= 1) v.back().second = std::max(v.back().second, a1);
+            else v.push_back({a0, a1});
+          }
         }
       };
-      span(A, hp->a_rng);
-      span(C, hp->c_rng);
+      held(A, hp->a_rng);
+      held(C, hp->c_rng);
+      // each chunk's plan: this rank's parts of the chunk's C blocks (the whole plan's owner-computes rows)
+      std::vector<std::vector<PartSel>> sel(nt);
+      for (const auto& mp : whole->my) {
+        const int64_t cb = whole->ht.cblk[mp.g];
+        C->block_coords(cb, co);
+        sel[hp->chunk(co)].push_back({cb, mp.lo, mp.hi});
+      }
       for (int32_t x = 0; x < nt; ++x) {
+        if (sel[x].empty()) continue;
         ContractOpts o;
         o.local = true;
         o.tag = "|host" + std::to_string(x);
-        for (int64_t b = 0; b < C->nblocks; ++b) {
-          if (!C->nz[b]) continue;
-          C->block_coords(b, co);
-          if (hp->chunk(co) == x) o.sel.push_back({b, 0, C->ext0(b)});
-        }
-        if (o.sel.empty()) continue;
+        o.sel = std::move(sel[x]);
         TT_TRY(get_contract_plan(ctx, C, cl, A, al, B, bl, beta, hp->tiles[x], nullptr, o));
       }
     }
@@ -806,9 +820,11 @@ tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* cl, double beta,
   TT_CUDA(cudaEventRecord(ctx->copy_fork, ctx->stream));
   TT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_fork, 0));
   for (int32_t x = 0; x < nt; ++x) {
-    TT_TRY(h2d(A, hA, {hp->a_rng[x]}, ctx->copy_stream));
+    TT_TRY(h2d(A, hA, hp->a_rng[x], ctx->copy_stream));
     TT_CUDA(cudaEventRecord(up[x], ctx->copy_stream));
   }
+  // B's remote parts (several ranks) while A streams in; the chunk plans are local
+  TT_TRY(run_gather(ctx, whole->gp, {A, B}));
   reset_stats(ctx);
   double flops = 0;
   int64_t tasks = 0;
@@ -824,7 +840,7 @@ tt_status tt_contract_host(tt_ctx ctx, tt_tensor C, const char* cl, double beta,
   if (c_flags & TT_HOST_C_OUT)
     for (int32_t x = 0; x < nt; ++x) {
       TT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, done[x], 0));
-      TT_TRY(d2h(C, hC, {hp->c_rng[x]}, ctx->copy_stream));
+      TT_TRY(d2h(C, hC, hp->c_rng[x], ctx->copy_stream));
     }
   TT_CUDA(cudaEventRecord(fin, ctx->copy_stream));
   TT_CUDA(cudaStreamWaitEvent(ctx->stream, fin, 0));
