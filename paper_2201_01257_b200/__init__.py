@@ -514,7 +514,7 @@ def contract_prefetch(ctx: Context, C: Tensor, c_lbl: str, beta: float, A: Tenso
 def contract_host(ctx: Context, C: Tensor, c_lbl: str, beta: float, alpha: float, A: Tensor, a_lbl: str, B: Tensor,
                   b_lbl: str, hA=None, hB=None, hC=None, c_in: bool = False, c_out: bool = False):
     """tt_contract_host: the contraction from host buffers (pinned torch tensors or addresses; None = the
-    operand is resident), pipelined inside the library (per dim-0 tile of C)."""
+    operand is resident), pipelined inside the library (per chunk of C, see include/tt.h)."""
     flags = (HOST_C_IN if c_in else 0) | (HOST_C_OUT if c_out else 0)
     _check(_lib.tt_contract_host(ctx.h, C.h, _b(c_lbl), float(beta), float(alpha), A.h, _b(a_lbl), B.h, _b(b_lbl),
                                  _vp(_devptr(hA)) if hA is not None else None,

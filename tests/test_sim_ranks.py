@@ -150,3 +150,71 @@ def test_simulated_gather_moves_exactly_the_plan(env):
     res = run_ranks(tt, torch, 3, body)
     for (recv, send), got in res:
         assert len(recv) > 0 and got == int(sum(8 * (e - b) for (_, _, _, b, e) in recv))
+
+
+def _mirror_rows(tt, C, A):
+    """A's (a,b) rows follow C's owner-computes rows (whole blocks or row parts), as bench.py places V."""
+    whole, split = {}, {}
+    for blk in range(C.nblocks):
+        if C.nz[blk] and C.owner[blk] >= 0:
+            whole[tuple(int(x) for x in np.unravel_index(blk, C.grid)[:2])] = int(C.owner[blk])
+    for (blk, lo, hi, ow) in C.parts:
+        split.setdefault(tuple(int(x) for x in np.unravel_index(blk, C.grid)[:2]), set()).add((lo, hi, ow))
+    own = np.full(A.nblocks, -1, np.int32)
+    parts = []
+    for blk in range(A.nblocks):
+        if not A.nz[blk]:
+            continue
+        key = tuple(int(x) for x in np.unravel_index(blk, A.grid)[:2])
+        if key in split:
+            parts += [(blk, lo, hi, ow) for (lo, hi, ow) in sorted(split[key])]
+            own[blk] = 0
+        else:
+            own[blk] = whole.get(key, 0)
+    A.set_owner(own)
+    if parts:
+        A.set_parts(parts)
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_simulated_contract_host_pipelined(env, p):
+    """tt_contract_host with several ranks: R row-split on (a,b) rows, V's rows mirrored (local to each
+    rank's R rows), T round robin (gathered up front): each rank pipelines its held V rows chunk by chunk
+    (several kernel launches), and the R ranges the ranks own, assembled from their host buffers, equal
+    bit for bit the 1-rank result, which is within 1e-11 of the oracle."""
+    tt, torch = env
+    pb = _problem()
+    c, cl, a, al, b, bl = pb.ops[0]   # the ladder R(abij) += Vv(abcd) T(cdij)
+    orc = oracle_objects(pb)
+    tags = dict(TAGS)
+    dense = {n: O.dense_masked(orc[n], S.dense(orc[n].shape, 3, tags[n])) for n in (a, b, c)}
+    packed = {n: O.pack(orc[n], dense[n]) for n in (a, b, c)}
+
+    def body(rank, ctx):
+        P = product_objects(tt, ctx, pb)
+        if ctx.nranks > 1:
+            tt.partition_split(ctx, P[c], cl, P[a], al, P[b], bl, group_dims=(0, 1))
+            _mirror_rows(tt, P[c], P[a])
+        bufs = {}
+        for n in (a, b, c):   # device buffers start as NaN: only the uploads and the gather fill them
+            bufs[n] = torch.full((P[n].storage_elems,), float("nan"), dtype=torch.float64, device="cuda")
+            P[n].bind(bufs[n])
+        host = {n: torch.from_numpy(packed[n].copy()).pin_memory() for n in (a, b, c)}
+        ctx.set_profiling(True)
+        tt.contract_host(ctx, P[c], cl, 1.0, 0.5, P[a], al, P[b], bl, host[a], host[b], host[c],
+                         c_in=True, c_out=True)
+        ctx.sync()
+        launches = ctx.profile("tt_contract_dmma")[1]
+        ctx.set_profiling(False)
+        return P[c], host[c].numpy().copy(), launches
+
+    one = run_ranks(tt, torch, 1, body)
+    R1, seen1 = assemble([one[0][0]], [one[0][1]], one[0][0].packed_elems)
+    res = run_ranks(tt, torch, p, body)
+    Rp, seenp = assemble([r[0] for r in res], [r[1] for r in res], res[0][0].packed_elems)
+    assert np.array_equal(seenp, seen1) and not np.isnan(Rp[seenp]).any()
+    assert np.array_equal(Rp[seenp], R1[seen1]), "pipelined host contraction depends on the rank count"
+    assert all(r[2] > 1 for r in res), [r[2] for r in res]   # chunked: one launch per chunk
+    ref = O.pack(orc[c], O.contract(dense[c], cl, dense[a], al, dense[b], bl, 0.5, 1.0, cmask=O.nz_mask(orc[c])))
+    err = np.abs(R1[seen1] - ref[seen1]).max() / np.abs(ref[seen1]).max()
+    assert err <= 1e-11, err
