@@ -40,6 +40,8 @@ using namespace tt;
 // bytes; B itself may then use compact storage); otherwise B is all-gathered and every rank forms
 // all of Bh.  The rank's C parts are processed in batches of (p,q) tile rows: W of the batch is
 // built into the workspace and immediately consumed restricted to the batch.  X must be replicated.
+// When the workspace also holds BsT(s,r,..) = Bs(r,s,..) (TT_CHOL_BST != 0) pass 2 reads
+//   - sum W(p,q,s,r) BsT(s,r)   (both operands in K order (s,r): TMA-eligible, unlike W(p,q,s,r) Bs(r,s)).
 // When the workspace cannot hold Bh plus one W row (or TT_CHOL_TWO_PASS=1) the consume reads B
 // directly in two passes, C += alpha W.B and C -= alpha W.B(r<->s): no Bh, twice the consume FLOPs.
 
@@ -70,6 +72,9 @@ struct CholPlan {
   tt_tensor Vmeta = nullptr, Wmeta = nullptr;   // block maps of V (algorithmic count) and W
   tt_tensor Bh = nullptr;                       // (B - B(r<->s)) on tile pairs r_t <= s_t, in the workspace
   tt_tensor Bs = nullptr;                       // view of Bh's strictly-upper blocks (r_t < s_t)
+  tt_tensor BsT = nullptr;                      // Bs with r and s swapped (K order of W read as (p,q,s,r))
+  std::shared_ptr<ElemPlan> t_plan;             // BsT formation from Bh
+  bool use_t = false;                           // exchange consume on BsT (TMA-eligible) instead of Bs
   std::shared_ptr<ContractPlan> vplan, wplan;   // SPMD plans: this rank's C parts, FLOP counts
   std::shared_ptr<ElemPlan> copy_plan, swap_plan;   // Bh formation (this rank's Bh blocks)
   GatherPlan bgather;                           // all-gather of B (not co-located) ...
@@ -83,6 +88,7 @@ struct CholPlan {
     delete Wmeta;
     delete Bh;
     delete Bs;
+    delete BsT;
     for (auto& b : batches) delete b.Wb;
   }
 };
@@ -260,6 +266,16 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       if (snz[x]) cp->Bs->owner[x] = TT_REPLICATED;
     }
     cp->Bs->packed_elems = cp->Bs->storage_elems = cp->Bh->packed_elems;
+    // BsT(s,r,..) = Bs(r,s,..): the exchange consume -W(p,q,s,r) Bs(r,s,..) then reads both operands
+    // in the same K order (s,r), which the TMA producer can stage (Bs's order against W's cannot)
+    {
+      std::vector<uint8_t> tnz(B->nblocks, 0);
+      for (int64_t x = 0; x < B->nblocks; ++x)
+        if (snz[x]) tnz[swap_of[x]] = 1;
+      TT_TRY(new_meta_tensor(ctx, B->dims, tnz, &cp->BsT));
+      for (int64_t x = 0; x < B->nblocks; ++x)
+        if (tnz[x]) cp->BsT->owner[x] = TT_REPLICATED;
+    }
     // formation owner of each Bh block: the rank holding both B(x) and B(swap x) whole (replicated
     // blocks are held everywhere); B pairs split across ranks -> all-gather B instead
     cp->colocated = true;
@@ -358,7 +374,17 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     if (ws_elems < max_uel)
       return fail(TT_E_OOM, "workspace holds %lld doubles; one (p,q) row of W needs %lld", (long long)ws_elems,
                   (long long)max_uel);
-    const int64_t w_off = cp->two_pass ? 0 : bh_elems;
+    // BsT after Bh when the workspace still holds a W row after both (TT_CHOL_BST=0: off)
+    const int64_t bst_elems = (cp->BsT->packed_elems + 31) / 32 * 32;
+    const char* fb = getenv("TT_CHOL_BST");
+    cp->use_t = !cp->two_pass && (!fb || atoi(fb) != 0) && cp->BsT->packed_elems > 0 &&
+                ws_elems >= bh_elems + bst_elems + max_uel;
+    if (cp->use_t) {
+      cp->BsT->data = (double*)workspace + bh_elems;
+      cp->BsT->capacity = bst_elems;
+      TT_TRY(local_add_plan(ctx, cp->BsT, cp->Bs, sw, 0.0, cp->t_plan));
+    }
+    const int64_t w_off = cp->two_pass ? 0 : bh_elems + (cp->use_t ? bst_elems : 0);
     double* wbase = (double*)workspace + w_off;
     const int64_t w_elems = ws_elems - w_off;
     if (!cp->two_pass) {
@@ -424,6 +450,8 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   std::string bsw(bl);                                                              // B with r <-> s
   std::swap(bsw[b.find(r)], bsw[b.find(s)]);
   const std::string vsw = std::string(1, p) + q + s + r;                              // W read as (p,q,s,r)
+  tt_tensor xB = cp->use_t ? cp->BsT : cp->Bs;                                        // exchange operand
+  const char* xl = cp->use_t ? bsw.c_str() : bl;                                      // ... and its labels
   if (ctx->prepare_only) {   // build every batch plan now (they are cached), launch nothing
     for (auto& bt : cp->batches) {
       std::shared_ptr<ContractPlan> pw, pu, px;
@@ -434,7 +462,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
         TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, B, bsw.c_str(), 1.0, px, &dummy, bt.copt));
       } else {
         TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bh, bl, beta, pu, &dummy, bt.copt));
-        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vsw.c_str(), cp->Bs, bl, 1.0, px, &dummy, bt.copt));
+        TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vsw.c_str(), xB, xl, 1.0, px, &dummy, bt.copt));
       }
     }
     return TT_OK;
@@ -449,6 +477,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     trace("Bh formed");
     TT_TRY(run_gather(ctx, cp->hgather, {cp->Bh}));
     trace("Bh gathered, runs", (long long)(cp->hgather.recv.size() + cp->hgather.send.size()));
+    if (cp->use_t) TT_TRY(run_local_add(ctx, *cp->t_plan, cp->BsT, cp->Bs, 0.0, 1.0));
   }
   double exec = 0, build = 0;
   int64_t tasks = 0;
@@ -467,9 +496,9 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
       tasks += pu->tasks + px->tasks;
     } else {
       TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vl, cp->Bh, bl, beta, pu, &dummy, bt.copt));
-      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vsw.c_str(), cp->Bs, bl, 1.0, px, &dummy, bt.copt));
+      TT_TRY(get_contract_plan(ctx, C, cl, bt.Wb, vsw.c_str(), xB, xl, 1.0, px, &dummy, bt.copt));
       TT_TRY(launch_plan(ctx, *pu, C, cl, beta, alpha, bt.Wb, vl, cp->Bh, bl));
-      TT_TRY(launch_plan(ctx, *px, C, cl, 1.0, -alpha, bt.Wb, vsw.c_str(), cp->Bs, bl));
+      TT_TRY(launch_plan(ctx, *px, C, cl, 1.0, -alpha, bt.Wb, vsw.c_str(), xB, xl));
       exec += pu->flops + px->flops;
       tasks += pu->tasks + px->tasks;
     }
