@@ -350,14 +350,23 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
         }
     };
     // workspace: Bh then the W batches; without room for Bh plus the largest W row, two passes
-    std::vector<int64_t> rb;
+    std::vector<int64_t> rb, uels;
     int64_t max_uel = 0;
     for (auto& kv : units) {
       row_blocks(kv.second, rb);
       int64_t uel = 0;
       for (int64_t vb : rb) uel += (cp->Wmeta->block_volume(vb) + 1) / 2 * 2;
       max_uel = std::max(max_uel, uel);
+      uels.push_back(uel);
     }
+    auto n_batches = [&](int64_t cap) {   // the greedy packing of flush() below
+      int64_t n = 0, cur = 0;
+      for (int64_t u : uels) {
+        if (cur > 0 && cur + u > cap) { ++n; cur = 0; }
+        cur += u;
+      }
+      return n + (cur > 0 ? 1 : 0);
+    };
     if (const char* f2 = getenv("TT_CHOL_TWO_PASS")) cp->two_pass = atoi(f2) != 0;
     const int64_t bh_elems = (cp->Bh->packed_elems + 31) / 32 * 32;
     if (ws_elems < bh_elems + max_uel) cp->two_pass = true;
@@ -374,11 +383,16 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
     if (ws_elems < max_uel)
       return fail(TT_E_OOM, "workspace holds %lld doubles; one (p,q) row of W needs %lld", (long long)ws_elems,
                   (long long)max_uel);
-    // BsT after Bh when the workspace still holds a W row after both (TT_CHOL_BST=0: off)
+    // BsT after Bh when the workspace still holds a W row after both and the smaller W space adds at
+    // most half again as many batches (smaller batches lose more to tails than the TMA consume gains:
+    // configs[3]-scale ladder in 40 GB 29 -> 43 batches, 2 % faster; the CCSD iteration's ladder in
+    // 12 GB 86 -> 256 batches, 3 % slower).  TT_CHOL_BST=0: off, =1: whenever it fits.
     const int64_t bst_elems = (cp->BsT->packed_elems + 31) / 32 * 32;
     const char* fb = getenv("TT_CHOL_BST");
-    cp->use_t = !cp->two_pass && (!fb || atoi(fb) != 0) && cp->BsT->packed_elems > 0 &&
-                ws_elems >= bh_elems + bst_elems + max_uel;
+    const int bst_mode = fb ? atoi(fb) : 2;
+    cp->use_t = !cp->two_pass && bst_mode != 0 && cp->BsT->packed_elems > 0 &&
+                ws_elems >= bh_elems + bst_elems + max_uel &&
+                (bst_mode == 1 || 2 * n_batches(ws_elems - bh_elems - bst_elems) <= 3 * n_batches(ws_elems - bh_elems));
     if (cp->use_t) {
       cp->BsT->data = (double*)workspace + bh_elems;
       cp->BsT->capacity = bst_elems;
@@ -469,6 +483,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   }
   reset_stats(ctx);
   trace("cholesky: plans ready, batches", (long long)cp->batches.size());
+  trace("cholesky: exchange consume on BsT", cp->use_t ? 1 : 0);
   TT_TRY(run_gather(ctx, cp->bgather, {B}));
   trace("B gathered, runs", (long long)(cp->bgather.recv.size() + cp->bgather.send.size()));
   if (!cp->two_pass) {

@@ -520,23 +520,23 @@ def _cholesky_problem(O_, V_, tO, tV, NL, tL, spin):
 
 @pytest.mark.parametrize("spin,ws_rows,mode", [(True, 1, "bh"), (True, 100, "bh"), (False, 2, "bh"),
                                                 (True, 1, "env"), (False, 2, "env"), (True, 3, "auto"),
-                                                (True, 2, "densex"), (True, 100, "nobst")])
+                                                (True, 2, "densex"), (True, 100, "nobst"), (True, 100, "bst")])
 def test_contract_cholesky(env, spin, ws_rows, mode):
     """Implicit Eq. cc12 operand (NEXT-1): R(abij) = beta*R + alpha*sum V(abcd) T(cdij) with V built
     batch by batch from X in a small workspace == oracle with V formed explicitly.  mode "bh": the
     workspace holds the r_t <= s_t half of Bm = T - T(c<->d); "env"/"auto": the two-pass consume
     (forced, or because the workspace holds only W rows); "densex": alpha/beta spaces with a DENSE X map
     (the W / V block maps must follow X's actual map, not the tiles' spins: ADVICE r1).  A roomy
-    workspace also holds BsT (the exchange consume on TMA); "nobst": the same with TT_CHOL_BST=0 (the
-    cp.async exchange consume)."""
+    workspace may also hold BsT (the exchange consume on TMA); "bst" / "nobst": forced on / off
+    (TT_CHOL_BST=1 / 0; off = the cp.async exchange consume)."""
     tt, torch = env
     pb = _cholesky_problem(8, 12, 2, 3, 10, 5, spin) if spin else _cholesky_problem(5, 9, 3, 4, 7, 4, False)
     if mode == "densex":
         pb.tensors["X"] = TensorSpec("acL", None)
     if mode == "env":
         os.environ["TT_CHOL_TWO_PASS"] = "1"
-    if mode == "nobst":
-        os.environ["TT_CHOL_BST"] = "0"
+    if mode in ("nobst", "bst"):
+        os.environ["TT_CHOL_BST"] = "0" if mode == "nobst" else "1"
     ctx = new_ctx(tt, torch)
     orc = oracle_objects(pb)
     P = product_objects(tt, ctx, pb)
