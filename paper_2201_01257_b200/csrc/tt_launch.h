@@ -231,7 +231,7 @@ size_t triples_fused_smem();
 cudaError_t launch_triples_fused(const TriplesParams& p, int64_t nunits, cudaStream_t s);
 // TMA variant; maps = 4 CUtensorMap: VO (r,m,y,x) box {20,8,1,1}, T2 as P (b,a,j,i) box {20,8,1,1},
 // T2 as Q (b,a,j,i) box {18,18,1,8}, VV (q,p,x,e) box {18,18,1,8}
-cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s);
+cudaError_t launch_triples_tma(const TriplesParams& p, int64_t nunits, cudaStream_t s);   // default kernel
 // pair variant (two units with the same box triple and occupied pair (i,j) per CTA, shared operands)
 cudaError_t launch_triples_pair(const TriplesParams& p, const void* maps, int64_t npairs, cudaStream_t s);
 // 2-CTA cluster variant over the same pairs: the shared operand of every segment by TMA multicast

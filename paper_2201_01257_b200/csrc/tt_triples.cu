@@ -492,9 +492,7 @@ __device__ __forceinline__ void seg_mma(double (&acc)[2][NFR][2], int n, int& sl
 }
 
 __global__ void __launch_bounds__(TTHREADS, 2)
-    triples_fused_tma_kernel(const TriplesParams p, const __grid_constant__ CUtensorMap mVO,
-                             const __grid_constant__ CUtensorMap mT2P, const __grid_constant__ CUtensorMap mT2Q,
-                             const __grid_constant__ CUtensorMap mVV) {
+    triples_fused_tma_kernel(const TriplesParams p) {
   extern __shared__ __align__(128) unsigned char tsm_raw[];
   unsigned char* base = tsm_raw + ((128 - ((unsigned)__cvta_generic_to_shared(tsm_raw) & 127)) & 127);   // stays in the shared window (LDS, not generic LD)
   double* cube = reinterpret_cast<double*>(base + BNS * BSTAGE);   // [BX][BX][BX]
@@ -551,10 +549,6 @@ __global__ void __launch_bounds__(TTHREADS, 2)
   if (warp == NWARP) {
     // ---------------------------------------------------------------- TMA producer (one thread)
     if (lane != 0) return;
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVO) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2P) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mT2Q) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mVV) : "memory");
     int slot = 0;
     unsigned phase = 1;   // empty barriers: the first pass over the ring does not wait
     const int32_t nb = p.nb, kpo = p.kpo, kpv = p.kpv;
@@ -1222,7 +1216,7 @@ size_t triples_tma_smem() {   // the default kernel (bulk-copy stages)
   return 128 + (size_t)BNS * BSTAGE + sizeof(double) * (BX * BX * BX + THREADS) + 16 * BNS + 4 * 36;
 }
 
-cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t nunits, cudaStream_t s) {
+cudaError_t launch_triples_tma(const TriplesParams& p, int64_t nunits, cudaStream_t s) {
   if (nunits <= 0) return cudaSuccess;
   static bool attr = false;
   const size_t smem = triples_tma_smem();
@@ -1231,8 +1225,7 @@ cudaError_t launch_triples_tma(const TriplesParams& p, const void* maps, int64_t
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const CUtensorMap* m = static_cast<const CUtensorMap*>(maps);
-  triples_fused_tma_kernel<<<(unsigned)nunits, TTHREADS, smem, s>>>(p, m[0], m[1], m[2], m[3]);
+  triples_fused_tma_kernel<<<(unsigned)nunits, TTHREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 

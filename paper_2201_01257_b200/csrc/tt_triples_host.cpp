@@ -472,7 +472,18 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   p.kpv = tp->kpv;
   p.ko2 = tp->ko2;
   p.kv2 = tp->kv2;
-  {   // blocked copies of the default kernel
+  // bulk copies of the blocked operands (default), TMA boxes (opt-in pair / cluster kernels) or cp.async
+  // staging (TT_TMA=0).  Opt-in: the 2-CTA cluster kernel with TMA multicast of the shared operand
+  // (TT_TRIPLES_CLUSTER=1; measured 5.79 s vs 3.08 s at O=40 V=200: the two CTAs release every slot
+  // together, so each waits on the other's slowest warp) or the 16-warp pair kernel (TT_TRIPLES_PAIR=1;
+  // 4.59 s)
+  const char* ft = getenv("TT_TMA");
+  const bool use_tma = !ft || atoi(ft) != 0;
+  const char* fp = getenv("TT_TRIPLES_PAIR");
+  const char* fc = getenv("TT_TRIPLES_CLUSTER");
+  const bool use_pair = use_tma && fp && atoi(fp) != 0;
+  const bool use_cluster = use_tma && !use_pair && fc && atoi(fc) != 0;
+  if (use_tma && !use_pair && !use_cluster) {   // blocked copies of the default kernel
     double* bq[4];
     for (int q = 0; q < 4; ++q) bq[q] = ws + tp->blk_pos[q];
     p.QT2 = bq[0];
@@ -484,12 +495,8 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
       TT_CUDA(launch_blockify(q, p, bq[q], tp->blk_n[q], ctx->stream));
     }
   }
-  // bulk copies of the blocked operands (default), TMA boxes (opt-in pair / cluster kernels) or cp.async
-  // staging (TT_TMA=0)
-  const char* ft = getenv("TT_TMA");
-  const bool use_tma = !ft || atoi(ft) != 0;
   CUtensorMap maps[4];
-  if (use_tma) {
+  if (use_pair || use_cluster) {   // 4-D TMA boxes over the dense copies
     const uint32_t bP[4] = {(uint32_t)kTripBox + 4, 8, 1, 1}, bQ[4] = {(uint32_t)kTripBox + 2, (uint32_t)kTripBox + 2, 1, 8};
     const int64_t dVO[4] = {nV, nO, nO, nO}, dT2[4] = {nV, nV, nO, nO}, dVV[4] = {nV, nV, nO, nV};
     TT_TRY(encode_4d(&maps[0], p.VO, dVO, bP));
@@ -497,13 +504,6 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     TT_TRY(encode_4d(&maps[2], p.T2, dT2, bQ));
     TT_TRY(encode_4d(&maps[3], p.VV, dVV, bQ));
   }
-  // opt-in: the 2-CTA cluster kernel with TMA multicast of the shared operand (TT_TRIPLES_CLUSTER=1;
-  // measured 5.79 s vs 3.08 s at O=40 V=200: the two CTAs release every slot together, so each waits on
-  // the other's slowest warp) or the 16-warp pair kernel (TT_TRIPLES_PAIR=1; 4.59 s)
-  const char* fp = getenv("TT_TRIPLES_PAIR");
-  const char* fc = getenv("TT_TRIPLES_CLUSTER");
-  const bool use_pair = use_tma && fp && atoi(fp) != 0;
-  const bool use_cluster = use_tma && !use_pair && fc && atoi(fc) != 0;
   ctx->last.producer = use_pair ? 2 : (use_cluster ? 3 : (use_tma ? 1 : 0));
   if (use_pair || use_cluster) {
     for (int64_t q0 = 0; q0 < tp->npairs; q0 += (1 << 20)) {
@@ -519,7 +519,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     p.unit0 = u0;
     const int64_t n = std::min<int64_t>(1 << 20, tp->unit0 + tp->nunits - u0);
     Launch L(ctx, "tt_triples_fused");
-    if (use_tma) TT_CUDA(launch_triples_tma(p, maps, n, ctx->stream));
+    if (use_tma) TT_CUDA(launch_triples_tma(p, n, ctx->stream));
     else TT_CUDA(launch_triples_fused(p, n, ctx->stream));
   }
   {
