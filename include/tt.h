@@ -375,8 +375,10 @@ tt_status tt_contract3(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, 
  * unit's W in shared memory as W(a,b,c) = G(a;b,c) - G(b;a,c) + G(c;a,b) -- the 18 terms regrouped into
  * three DMMA GEMMs with K = 3 n_o + 3 n_v -- and reduces (W + V1) W / D over a<b<c into one partial per
  * unit; a fixed-order sum gives E (deterministic).  Units whose box spins and occupied spins differ in
- * sum are skipped (W = 0 under the spin maps of R7).  With nranks > 1 every input block must be
- * TT_REPLICATED, the units are split into contiguous ranges of equal modelled cost (cost_* below) and E
+ * sum are skipped (W = 0 under the spin maps of R7).  With nranks > 1 the inputs may have any whole-block
+ * owners (not compact): every rank first gathers the blocks it does not hold into the inputs' own
+ * storage (the kernel reads all of them), the units are split into contiguous ranges of equal modelled
+ * cost (cost_* below) and E
  * is all-reduced (NCCL).
  * energy: HOST pointer; the call synchronises the stream.
  *   workspace  device memory of ws_elems doubles >= info->ws_elems (dense copies + one partial per

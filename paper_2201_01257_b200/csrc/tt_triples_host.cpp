@@ -64,6 +64,7 @@ struct TripPlan {
   int64_t blk_pos[4] = {0, 0, 0, 0}, blk_n[4] = {0, 0, 0, 0};   // blocked copies (QT2, QVV, PVO, PT2)
   int32_t nbox = 0;
   int32_t kpo = 0, kpv = 0, ko2 = 0, kv2 = 0;   // padded summed rows of the blocked copies
+  GatherPlan gp;                              // nranks > 1: every input block this rank does not hold
   tt_triples_info info{};
   ~TripPlan() {
     for (auto& r : rt) delete r.dst;
@@ -184,10 +185,9 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
         return fail(TT_E_UNSUPPORTED, "%s: non-zero block %lld breaks the spin rule the (T) kernel prunes by "
                     "(use the spin block maps of reading R7 on alpha/beta spaces)", names[x], (long long)b);
     }
-    if (ctx->nranks > 1)
-      for (int64_t b = 0; b < ins[x]->nblocks; ++b)
-        if (ins[x]->nz[b] && ins[x]->owner[b] != TT_REPLICATED)
-          return fail(TT_E_UNSUPPORTED, "%s: with nranks > 1 every input block must be TT_REPLICATED", names[x]);
+    if (ctx->nranks > 1 && ins[x]->compact)
+      return fail(TT_E_UNSUPPORTED, "%s: with nranks > 1 the inputs need their full packed storage (not compact): "
+                  "every rank reads all of them", names[x]);
   }
   const int64_t nO = tO->offsets.back(), nV = tV->offsets.back();
   if (nO < 3 || nV < 3) return fail(TT_E_ARG, "need at least 3 occupied and 3 virtual indices");
@@ -397,6 +397,14 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
     }
     tp->ws_need = base + (U + 1) / 2 * 2;
     tp->info.ws_elems = tp->ws_need;
+    if (ctx->nranks > 1) {   // owner-distributed inputs: every rank receives all blocks it does not hold
+      Needs need(ctx->nranks);
+      for (int r = 0; r < ctx->nranks; ++r)
+        for (int x = 0; x < 5; ++x)
+          for (int64_t b = 0; b < ins[x]->nblocks; ++b)
+            if (ins[x]->nz[b]) need[r].push_back({x, b, 0, ins[x]->block_volume(b)});
+      TT_TRY(build_gather(ctx, need, {ins[0], ins[1], ins[2], ins[3], ins[4]}, tp->gp));
+    }
     if (ctx->device >= 0) {
       TT_TRY(need_ws(ctx));
       DeviceGuard dg(ctx->device);
@@ -443,6 +451,7 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
   reset_stats(ctx);
   double* ws = (double*)workspace;
   if ((uintptr_t)ws % 16) return fail(TT_E_ARG, "workspace must be 16-byte aligned");
+  TT_TRY(run_gather(ctx, tp->gp, {ins[0], ins[1], ins[2], ins[3], ins[4]}));
   for (int x = 0; x < 5; ++x) {
     tp->rt[x].dst->data = ws + tp->rt[x].ws_pos;
     tp->rt[x].dst->capacity = tp->rt[x].dst->packed_elems;

@@ -1,4 +1,5 @@
-"""Multi-GPU check of the (T) energy (run under torchrun, NCCL): inputs replicated on every rank, units
+"""Multi-GPU check of the (T) energy (run under torchrun, NCCL): inputs replicated on every rank (or
+owner-distributed: round-robin owners, blocks held elsewhere NaN, gathered by each rank), units
 split over the ranks, the partial energies all-reduced; compared with the oracle (by-triple form) and
 with a 1-rank context on the same GPU (the same units summed in one place).
 
@@ -41,7 +42,14 @@ def run(ctx, nO, nV, tO, tV, spin, replicated, seed=5):
             T[n].set_owner(np.full(T[n].nblocks, tt.TT_REPLICATED, np.int32))
         ot = L.tensor_spin([odims[c] for c in d], *sp) if spin else L.tensor_dense_map([odims[c] for c in d])
         dense[n] = O.dense_masked(ot, S.dense(ot.shape, seed, tag))
-        buf = torch.from_numpy(O.pack(ot, dense[n])).cuda()
+        host = O.pack(ot, dense[n])
+        if not replicated and ctx.nranks > 1:   # owner-distributed: blocks held elsewhere start as NaN
+            for blk in range(T[n].nblocks):
+                if T[n].nz[blk] and T[n].owner[blk] not in (ctx.rank, tt.TT_REPLICATED):
+                    o = int(T[n].blk_off[blk])
+                    ext = [int(dd.offsets[t + 1] - dd.offsets[t]) for dd, t in zip(T[n].dims, np.unravel_index(blk, T[n].grid))]
+                    host[o:o + int(np.prod(ext))] = np.nan
+        buf = torch.from_numpy(host).cuda()
         T[n].bind(buf)
         keep.append(buf)
     rng = np.random.default_rng(seed)
@@ -64,8 +72,9 @@ def main():
     ctx = tt.Context(device=local, stream=stream, rank=rank, nranks=world, nccl_id=obj[0])
     ctx1 = tt.Context(device=local, stream=stream)
     ok = True
-    for case in ((10, 40, 3, 10, False), (8, 36, 2, 9, True)):
-        E, info, orc = run(ctx, *case, replicated=True)
+    for case, repl in (((10, 40, 3, 10, False), True), ((8, 36, 2, 9, True), True), ((8, 36, 2, 9, True), False)):
+        # replicated inputs, then owner-distributed ones (round-robin owners, gathered by each rank)
+        E, info, orc = run(ctx, *case, replicated=repl)
         E1, info1, _ = run(ctx1, *case, replicated=False)
         units = torch.tensor([info["w_blocks"]], dtype=torch.int64, device="cuda")
         dist.all_reduce(units)
@@ -75,7 +84,7 @@ def main():
         good = err <= 1e-11 and rel1 <= 1e-13 and int(units[0]) == info1["w_blocks_total"]
         ok &= good
         if rank == 0:
-            print(f"case {case}: E={E!r} 1-rank={E1!r} oracle={Eo!r} err={err:.2e} vs1={rel1:.2e} "
+            print(f"case {case} {'replicated' if repl else 'distributed'}: E={E!r} 1-rank={E1!r} oracle={Eo!r} err={err:.2e} vs1={rel1:.2e} "
                   f"units {int(units[0])}/{info1['w_blocks_total']} {'ok' if good else 'FAIL'}", flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)

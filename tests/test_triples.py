@@ -454,3 +454,61 @@ def test_triples_rejects_maps_outside_the_spin_rule():
     d2 = {"o": to2, "v": tv2}
     dense = [tt.Tensor(ctx, [d2[c] for c in d]) for n, d, sp, _ in TRIPLES_INPUTS]
     tt.triples_energy(ctx, *dense)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [2, 3])
+def test_triples_owner_distributed_inputs_simulated_ranks(p):
+    """With several ranks the inputs may be owner-distributed (round robin here, non-held blocks NaN):
+    each rank gathers what it does not hold before re-tiling, the units split by cost, and every rank
+    returns the same energy as one rank, within 1e-11 of the oracle (simulated ranks on one GPU)."""
+    import torch
+    import paper_2201_01257_b200 as tt
+    import synthetic as S
+    from oracle import layout as L
+    from oracle import ops as O_
+    from tests.simranks import run_ranks
+    nO, nV, tO, tV, spin, seed = 8, 20, 2, 5, True, 4
+    oO, oV = _oracle_dims(nO, nV, tO, tV, spin)
+    odims = {"o": oO, "v": oV}
+    dense, packed = {}, {}
+    for n, d, sp, tag in TRIPLES_INPUTS:
+        ot = L.tensor_spin([odims[c] for c in d], *sp)
+        dense[n] = O_.dense_masked(ot, S.dense(ot.shape, seed, tag))
+        packed[n] = O_.pack(ot, dense[n])
+    rng = np.random.default_rng(seed)
+    eo, ev = rng.uniform(-2, -1, nO), rng.uniform(1, 2, nV)
+
+    def body(rank, ctx):
+        _, _, to, tv = _spaces(tt, nO, nV, tO, tV, spin)
+        dims = {"o": to, "v": tv}
+        T, keep = {}, []
+        for n, d, sp, _ in TRIPLES_INPUTS:
+            X = tt.Tensor(ctx, [dims[c] for c in d], spin=sp)
+            X.set_owner(np.where(X.nz > 0, np.arange(X.nblocks) % ctx.nranks, -1).astype(np.int32))
+            host = packed[n].copy()
+            for blk in range(X.nblocks):   # only the owned blocks hold data
+                if X.nz[blk] and X.owner[blk] != rank:
+                    o = int(X.blk_off[blk])
+                    ext = [int(dd.offsets[t + 1] - dd.offsets[t]) for dd, t in zip(X.dims, np.unravel_index(blk, X.grid))]
+                    host[o:o + int(np.prod(ext))] = np.nan
+            buf = torch.from_numpy(host).cuda()
+            X.bind(buf)
+            T[n] = X
+            keep.append(buf)
+        args = (T["T1"], T["T2"], T["Vooov"], T["Vvovv"], T["Voovv"])
+        _, info = tt.triples_energy(ctx, *args)
+        ws = torch.empty(int(info["ws_elems"] * 1.5), dtype=torch.float64, device="cuda")
+        E, _ = tt.triples_energy(ctx, *args, torch.from_numpy(eo).cuda(), torch.from_numpy(ev).cuda(), ws)
+        ctx.sync()
+        return E
+
+    E1 = run_ranks(tt, torch, 1, body)[0]
+    Ep = run_ranks(tt, torch, p, body)
+    assert all(np.isfinite(e) for e in Ep) and len(set(Ep)) == 1, Ep
+    assert abs(Ep[0] - E1) <= 1e-13 * abs(E1)
+    orc = (dense["T1"], dense["T2"], dense["Vooov"], dense["Vvovv"], dense["Voovv"], eo, ev)
+    Eo, _ = TR.energy(*orc)
+    scale = sum(abs(c[0]) for c in TR.energy_elements(*orc, [(i, j, k, a, b, c)
+                for i, j, k in itertools.combinations(range(nO), 3) for a, b, c in itertools.combinations(range(nV), 3)]))
+    assert abs(E1 - Eo) <= 1e-11 * scale, (E1, Eo, scale)
