@@ -415,7 +415,8 @@ tt_status tt_triples_energy(tt_ctx ctx, tt_tensor T1, tt_tensor T2, tt_tensor Vo
  * by the contraction restricted to the batch.  workspace: caller-owned device memory of ws_elems
  * doubles >= B's packed size (rounded up to 32) + one (p,q) row of W.  Ladder form only: p, q free
  * labels of C, r, s contracted with B; X(p,r,L) order 3 with dims 0 and 1 on the tiled space of p,q,r,s.
- * B is all-gathered once per call; with nranks > 1 every X block must be TT_REPLICATED.
+ * B is all-gathered once per call; with nranks > 1 X may have any owners (not compact): the blocks a rank
+ * does not hold are gathered once per call (every rank builds W from all of X).
  * tt_stats.flops = algorithmic FLOPs of the defined contraction over V's block map (non-zero iff the
  * Coulomb or the exchange term conserves spin pairwise); aux_flops = FLOPs executed (W build + consume). */
 tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* c_lbl, double beta, double alpha,

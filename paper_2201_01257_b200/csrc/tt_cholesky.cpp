@@ -79,6 +79,7 @@ struct CholPlan {
   std::shared_ptr<ElemPlan> copy_plan, swap_plan;   // Bh formation (this rank's Bh blocks)
   GatherPlan bgather;                           // all-gather of B (not co-located) ...
   GatherPlan hgather;                           // ... or of Bh (co-located B pairs)
+  GatherPlan xgather;                           // nranks > 1: the blocks of X this rank does not hold
   std::vector<CholBatch> batches;
   std::string lc;                               // the auxiliary label used for L
   bool two_pass = false;                        // no room for Bh: consume W.B and W.B(r<->s)
@@ -210,10 +211,9 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   const std::string c(cl), v(vl), b(bl);
   const char p = v[0], q = v[1], r = v[2], s = v[3];
   tt_tis tp = vdims[0], tq = vdims[1], tr = vdims[2], ts = vdims[3];
-  if (ctx->nranks > 1)
-    for (int64_t x = 0; x < X->nblocks; ++x)
-      if (X->nz[x] && X->owner[x] != TT_REPLICATED)
-        return fail(TT_E_UNSUPPORTED, "with nranks > 1 the Cholesky vectors X must be replicated");
+  if (ctx->nranks > 1 && X->compact)
+    return fail(TT_E_UNSUPPORTED, "with nranks > 1 the Cholesky vectors X need their full packed storage "
+                "(not compact): every rank builds W from all of X");
   std::string lc;
   for (char ch : std::string("LMNOPQRSTUVWXYZ0123456789"))
     if (c.find(ch) == std::string::npos && v.find(ch) == std::string::npos && b.find(ch) == std::string::npos) {
@@ -308,6 +308,13 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
         for (int64_t x = 0; x < B->nblocks; ++x)
           if (B->nz[x]) need[rr].push_back({0, x, 0, B->block_volume(x)});
       TT_TRY(build_gather(ctx, need, {B}, cp->bgather));
+    }
+    if (ctx->nranks > 1) {   // owner-distributed X: every rank builds W from all of X
+      Needs nx(ctx->nranks);
+      for (int rr = 0; rr < ctx->nranks; ++rr)
+        for (int64_t x = 0; x < X->nblocks; ++x)
+          if (X->nz[x]) nx[rr].push_back({0, x, 0, X->block_volume(x)});
+      TT_TRY(build_gather(ctx, nx, {X}, cp->xgather));
     }
     // Bh = B - B(r<->s) on this rank's Bh blocks
     TT_TRY(local_add_plan(ctx, cp->Bh, B, id, 0.0, cp->copy_plan, &mine));
@@ -484,6 +491,7 @@ tt_status tt_contract_cholesky(tt_ctx ctx, tt_tensor C, const char* cl, double b
   reset_stats(ctx);
   trace("cholesky: plans ready, batches", (long long)cp->batches.size());
   trace("cholesky: exchange consume on BsT", cp->use_t ? 1 : 0);
+  TT_TRY(run_gather(ctx, cp->xgather, {X}));
   TT_TRY(run_gather(ctx, cp->bgather, {B}));
   trace("B gathered, runs", (long long)(cp->bgather.recv.size() + cp->bgather.send.size()));
   if (!cp->two_pass) {

@@ -218,3 +218,56 @@ def test_simulated_contract_host_pipelined(env, p):
     ref = O.pack(orc[c], O.contract(dense[c], cl, dense[a], al, dense[b], bl, 0.5, 1.0, cmask=O.nz_mask(orc[c])))
     err = np.abs(R1[seen1] - ref[seen1]).max() / np.abs(ref[seen1]).max()
     assert err <= 1e-11, err
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_simulated_cholesky_owner_distributed_x(env, p):
+    """The implicit Cholesky ladder with X owner-distributed (round robin; blocks held elsewhere NaN):
+    each rank gathers X before building W; the assembled R2 equals bit for bit the run with X
+    replicated and the 1-rank run."""
+    tt, torch = env
+    pb = _problem()
+
+    def body_for(distributed):
+        def body(rank, ctx):
+            P = product_objects(tt, ctx, pb)
+            so, sv = P["_keep"][1]["O"], P["_keep"][1]["V"]
+            tL = tt.TiledIndexSpace(tt.IndexSpace(10), 5)
+            X = tt.Tensor(ctx, [sv, sv, tL], spin=([0], [1]))
+            if distributed:
+                X.set_owner(np.where(X.nz > 0, np.arange(X.nblocks) % ctx.nranks, -1).astype(np.int32))
+            else:
+                X.set_owner(np.where(X.nz > 0, tt.TT_REPLICATED, -1).astype(np.int32))
+            R2 = tt.Tensor(ctx, [sv, sv, so, so], spin=([0, 1], [2, 3]))
+            tt.partition_split(ctx, R2, "abij", P["Vv"], "abcd", P["T"], "cdij", group_dims=(0, 1))
+            xb = torch.empty(X.storage_elems, dtype=torch.float64, device="cuda")
+            tb = torch.empty(P["T"].storage_elems, dtype=torch.float64, device="cuda")
+            r2b = torch.full((R2.storage_elems,), float("nan"), dtype=torch.float64, device="cuda")
+            X.bind(xb)
+            P["T"].bind(tb)
+            R2.bind(r2b)
+            tt.fill_synthetic(ctx, X, 3, 9)
+            tt.fill_synthetic(ctx, P["T"], 3, 5)
+            tt.fill_synthetic(ctx, R2, 3, 10)
+            if distributed:   # poison what this rank does not hold
+                for blk in range(X.nblocks):
+                    if X.nz[blk] and X.owner[blk] != rank:
+                        o = int(X.storage_off[blk])
+                        n = int(np.prod([int(d.offsets[t + 1] - d.offsets[t])
+                                         for d, t in zip(X.dims, np.unravel_index(blk, X.grid))]))
+                        xb[o:o + n] = float("nan")
+            ws = torch.empty(P["T"].packed_elems + 32 + 12 ** 4 * 16, dtype=torch.float64, device="cuda")
+            tt.contract_cholesky(ctx, R2, "abij", 1.0, 0.5, X, "abcd", P["T"], "cdij", ws)
+            out = (R2, R2.download())
+            ctx.sync()
+            return out
+        return body
+
+    def assembled(res):
+        return assemble([r[0] for r in res], [r[1] for r in res], res[0][0].packed_elems)
+
+    R1, seen1 = assembled(run_ranks(tt, torch, 1, body_for(False)))
+    Rr, seenr = assembled(run_ranks(tt, torch, p, body_for(False)))
+    Rd, seend = assembled(run_ranks(tt, torch, p, body_for(True)))
+    assert np.array_equal(seend, seen1) and not np.isnan(Rd[seend]).any()
+    assert np.array_equal(Rd[seend], Rr[seenr]) and np.array_equal(Rd[seend], R1[seen1])
