@@ -453,6 +453,53 @@ tt_status build_contract_plan(tt_ctx ctx, tt_tensor C, tt_tensor A, tt_tensor B,
     }
     if (nch > 1) pl.partial_elems += nch * pl.splits.back().vol;
   }
+  // Wave tail (TT_TAIL_SPLIT=0: off).  With W work items on S = SMs x CTAs/SM resident slots the last
+  // W mod S items run while the other slots idle; when they fit one per SM after re-tiling with the
+  // smallest warp-specialised tile, they form a second launch of that variant over narrowed copies of
+  // their groups (same tasks, same per-element k order: bitwise the same C, R12), which takes a fraction
+  // of a full wave instead of a whole one.
+  {
+    const char* ft = getenv("TT_TAIL_SPLIT");
+    int tv = -1;
+    if ((!ft || atoi(ft) != 0) && pl.splits.empty() && pl.variant >= num_contract_variants()) {
+      auto area = [](const VariantInfo& x) { return (int64_t)x.bm * x.bn; };
+      for (int v = num_contract_variants(); v < n_variants(); ++v)
+        if (area(variant_info(v)) < area(vi) && (tv < 0 || area(variant_info(v)) < area(variant_info(tv)))) tv = v;
+    }
+    if (tv >= 0) {
+      const VariantInfo tvi = variant_info(tv);
+      int64_t slots = (int64_t)ctx->sm_count * std::max(vi.ctas_per_sm, 1);
+      if (const char* fs = getenv("TT_TAIL_SLOTS")) slots = std::max<int64_t>(1, atoll(fs));   // tests
+      const int64_t W = (int64_t)work.size(), r = W % slots;
+      const int64_t per = ((int64_t)vi.bm / tvi.bm + (vi.bm % tvi.bm != 0)) * ((int64_t)vi.bn / tvi.bn + (vi.bn % tvi.bn != 0));
+      if (getenv("TT_DEBUG") && atoi(getenv("TT_DEBUG")) != 0)
+        fprintf(stderr, "[tt rank %d] wave tail: %lld items, %lld slots, remainder %lld x %lld tail tiles, variant %d -> %d\n",
+                ctx->rank, (long long)W, (long long)slots, (long long)r, (long long)per, pl.variant, tv);
+      if (W > slots && r > 0 && r * per <= std::max<int64_t>(ctx->sm_count, 1)) {
+        std::vector<CGroupDesc> tg;
+        std::vector<WorkItem> tw;
+        for (int64_t i = W - r; i < W; ++i) {
+          const WorkItem& w = work[i];
+          CGroupDesc g = groups[w.group];
+          g.m_begin = groups[w.group].m_begin + w.mt * vi.bm;
+          g.M = std::min<int32_t>(groups[w.group].M, g.m_begin + vi.bm);
+          g.n_begin = groups[w.group].n_begin + w.nt * vi.bn;
+          g.N = std::min<int32_t>(groups[w.group].N, g.n_begin + vi.bn);
+          const int32_t gi = (int32_t)tg.size();
+          tg.push_back(g);
+          for (int32_t mt = 0; mt < (g.M - g.m_begin + tvi.bm - 1) / tvi.bm; ++mt)
+            for (int32_t nt = 0; nt < (g.N - g.n_begin + tvi.bn - 1) / tvi.bn; ++nt) tw.push_back({gi, mt, nt});
+        }
+        work.resize(W - r);
+        TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_tail_groups, tg.size()));
+        TT_TRY(dev_alloc(ctx, pl.mem, &pl.d_tail_work, tw.size()));
+        TT_CUDA(cudaMemcpy(pl.d_tail_groups, tg.data(), tg.size() * sizeof(CGroupDesc), cudaMemcpyHostToDevice));
+        TT_CUDA(cudaMemcpy(pl.d_tail_work, tw.data(), tw.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
+        pl.tail_variant = tv;
+        pl.tail_nwork = (int64_t)tw.size();
+      }
+    }
+  }
   pl.nwork = (int64_t)work.size();
   {
     // persistent CTAs pay off when items are short (pipeline fill and epilogue are a visible share);
@@ -546,6 +593,34 @@ tt_status launch_plan(tt_ctx ctx, const ContractPlan& pl, tt_tensor C, const cha
     else
       TT_CUDA(launch_contract_ws(pl.variant - num_contract_variants(), pl.an.a_kc, pl.an.b_nc, pl.a_vec, pl.b_vec, p,
                                  pl.nwork, ctx->stream));
+  }
+  if (pl.tail_nwork > 0) {   // the wave tail on the smallest tile (see build_contract_plan)
+    Launch L(ctx, nm.c_str());
+    ContractParams q = p;
+    q.groups = pl.d_tail_groups;
+    q.work = pl.d_tail_work;
+    q.nwork = pl.tail_nwork;
+    q.persistent = 0;
+    const int tv = pl.tail_variant - num_contract_variants();
+    if (pl.tma) {
+      ContractPlan& mp = const_cast<ContractPlan&>(pl);
+      if (mp.tail_map_ptr[0] != A->data || mp.tail_map_ptr[1] != B->data) {
+        const VariantInfo vt = variant_info(pl.tail_variant);
+        TT_TRY(encode_2d(&mp.tail_maps[0], A->data, pl.tma_k, A->storage_elems / pl.tma_k, 16, (uint32_t)vt.bm, true));
+        if (pl.tma_mode & 1) {
+          TT_TRY(encode_2d(&mp.tail_maps[1], B->data, pl.tma_n, B->storage_elems / pl.tma_n, 16, (uint32_t)vt.bn, true));
+        } else {
+          const int64_t d3[3] = {pl.tma_n, pl.tma_k, B->storage_elems / (pl.tma_n * pl.tma_k)};
+          const uint32_t b3[3] = {(uint32_t)vt.bn + 2, 16, 1};
+          TT_TRY(encode_3d(&mp.tail_maps[1], B->data, d3, b3));
+        }
+        mp.tail_map_ptr[0] = A->data;
+        mp.tail_map_ptr[1] = B->data;
+      }
+      TT_CUDA(launch_contract_tma(tv, pl.tma_mode, q, pl.tail_maps, pl.tail_nwork, ctx->stream));
+    } else {
+      TT_CUDA(launch_contract_ws(tv, pl.an.a_kc, pl.an.b_nc, pl.a_vec, pl.b_vec, q, pl.tail_nwork, ctx->stream));
+    }
   }
   if (!pl.splits.empty()) {
     const std::string rn = std::string("tt_contract_reduce[") + cl + "=" + al + "*" + bl + "]";

@@ -204,6 +204,14 @@ struct ContractPlan {
   bool prefetched = false;
   double flops = 0, bytes = 0;
   int64_t tasks = 0;
+  // wave tail: the last work items (less than one wave of resident CTAs) re-tiled with the smallest
+  // warp-specialised tile and launched right after the main kernel, one small CTA per idle SM
+  int tail_variant = -1;
+  int64_t tail_nwork = 0;
+  CGroupDesc* d_tail_groups = nullptr;
+  WorkItem* d_tail_work = nullptr;
+  CUtensorMap tail_maps[2];
+  const void* tail_map_ptr[2] = {nullptr, nullptr};
 };
 
 std::string plan_key(const char* kind, tt_tensor C, const char* cl, tt_tensor A, const char* al, tt_tensor B,

@@ -768,3 +768,32 @@ def test_tma_general_layouts(env, variant, case):
     os.environ.pop("TT_TMA", None)
     os.environ.pop("TT_FORCE_VARIANT", None)
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("name", ["multi_tile_spin_ring", "ragged_dense_ring", "ragged_dense_ladder"])
+@pytest.mark.parametrize("variant", [3, 4])
+def test_wave_tail_split_bitwise(env, name, variant):
+    """The wave tail (the last work items re-tiled with the smallest warp-specialised tile and launched
+    after the main kernel; TT_TAIL_SLOTS forces it on small plans) gives bitwise the C of the unsplit
+    plan, on the TMA and the cp.async producer, and the oracle's within 1e-11."""
+    tt, torch = env
+    pb, k = PROBLEMS[name]
+    out, launches = {}, {}
+    try:
+        for mode in ("off", "on"):
+            os.environ["TT_TAIL_SPLIT"] = "0" if mode == "off" else "1"
+            if mode == "on":   # a slot count that leaves a partial last wave
+                w = out["work_items"]
+                os.environ["TT_TAIL_SLOTS"] = str(next(x for x in (7, 5, 11, 13, 3, 2) if w > x and w % x))
+            ctx = new_ctx(tt, torch, variant=variant)
+            ctx.set_profiling(True)
+            got, ref, _, _ = run_contract(tt, torch, ctx, pb, pb.ops[k], alpha=0.5, beta=1.0)
+            launches[mode] = ctx.profile("tt_contract_dmma")[1]
+            out["work_items"] = ctx.stats()["work_items"]
+            out[mode] = got
+            assert normwise(got, ref) <= TOL
+    finally:
+        for e in ("TT_TAIL_SPLIT", "TT_TAIL_SLOTS", "TT_FORCE_VARIANT"):
+            os.environ.pop(e, None)
+    assert launches["off"] == 1 and launches["on"] == 2, launches
+    assert np.array_equal(out["on"], out["off"])
