@@ -285,6 +285,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if "RANK" in os.environ:   # torchrun pins OMP_NUM_THREADS=1; rank 0 runs alone, so give it the host cores
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     from oracle import _lib
     _lib.build()
     c = CONFIGS[args.config]
