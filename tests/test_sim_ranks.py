@@ -271,3 +271,23 @@ def test_simulated_cholesky_owner_distributed_x(env, p):
     Rd, seend = assembled(run_ranks(tt, torch, p, body_for(True)))
     assert np.array_equal(seend, seen1) and not np.isnan(Rd[seend]).any()
     assert np.array_equal(Rd[seend], Rr[seenr]) and np.array_equal(Rd[seend], R1[seen1])
+
+
+def test_simulated_ranks_with_wave_tail(env):
+    """Row-split R on 3 simulated ranks with the wave tail forced on every contraction plan
+    (TT_TAIL_SLOTS=2, warp-specialised variant forced): the owned R ranges equal bit for bit the 1-rank
+    result without the tail."""
+    import os
+    tt, torch = env
+    R1, seen1, _, _, _ = _run(tt, torch, 1, True)
+    pb = _problem()
+    os.environ["TT_TAIL_SLOTS"] = "2"
+    os.environ["TT_FORCE_VARIANT"] = "3"
+    try:
+        res = run_ranks(tt, torch, 3, _body(tt, torch, pb, True))
+    finally:
+        os.environ.pop("TT_TAIL_SLOTS", None)
+        os.environ.pop("TT_FORCE_VARIANT", None)
+    Rp, seenp = assemble([r["R"][0] for r in res], [r["R"][1] for r in res], res[0]["R"][0].packed_elems)
+    assert np.array_equal(seenp, seen1) and not np.isnan(Rp[seenp]).any()
+    assert np.array_equal(Rp[seenp], R1[seen1])
